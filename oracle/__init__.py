@@ -1,0 +1,229 @@
+"""CPU oracle for the ProtoX 2D Poisson point-Jacobi relaxation.
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py`` (its ``cpu_baseline`` leg and ``--impl reference``) may import
+this package.  The product library (``paper_2307_07931_b200``) never imports
+it, and the two share no code: this wrapper marshals numpy arrays into the
+single-threaded C++ oracle ``protox_oracle.cpp`` (see its header for the
+paper passages each function follows).
+
+Array convention: a *global ghosted array* of a problem with domain n0 x n1 and
+ghost width g is a numpy float64 array of shape (n1 + 2g, n0 + 2g); element
+[y + g, x + g] is cell (x, y) (x = dimension 0, fastest in memory, as fixed by
+the index arithmetic of Fig. ProtoX).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "protox_oracle.cpp")
+_LIB = os.path.join(_HERE, "liborc.so")
+
+BC_PERIODIC, BC_DIRICHLET_CC, BC_FIXED = 0, 1, 2
+ST_LAPLACE5, ST_MEHRSTELLEN9 = 0, 1
+
+_CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c++17", "-fPIC", "-shared"]
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with g++ (plain -O2, -ffp-contract=off)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["g++", *_CFLAGS, _SRC, "-o", tmp])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+class _Problem(ctypes.Structure):
+    _fields_ = [
+        ("n0", ctypes.c_int64), ("n1", ctypes.c_int64),
+        ("b0", ctypes.c_int64), ("b1", ctypes.c_int64),
+        ("ghost", ctypes.c_int32), ("bc", ctypes.c_int32),
+        ("stencil", ctypes.c_int32), ("rhs_correction", ctypes.c_int32),
+        ("h", ctypes.c_double), ("lam", ctypes.c_double),
+        ("nsweeps", ctypes.c_int64), ("norm_every", ctypes.c_int64),
+    ]
+
+
+_lib = None
+
+
+def _L():
+    global _lib
+    if _lib is None:
+        # PROTOX_ORACLE_LIB: a mutated build for scripts/oracle_mutation_check.py
+        _lib = ctypes.CDLL(os.environ.get("PROTOX_ORACLE_LIB") or build())
+        d = ctypes.POINTER(ctypes.c_double)
+        i64 = ctypes.c_int64
+        P = ctypes.POINTER(_Problem)
+        _lib.orc_last_error.restype = ctypes.c_char_p
+        _lib.orc_solve.argtypes = [P, d, d, d, d, i64, ctypes.POINTER(i64)]
+        _lib.orc_apply_laplacian.argtypes = [P, d, d]
+        _lib.orc_residual.argtypes = [P, d, d, d]
+        _lib.orc_rhs.argtypes = [P, d, d]
+        _lib.orc_exchange.argtypes = [P, d]
+        _lib.orc_exchange_box.argtypes = [P, d, i64, d]
+        _lib.orc_apply_taps.argtypes = [i64, ctypes.POINTER(i64), d, ctypes.c_double, d,
+                                        i64, i64, i64, i64, i64, i64, i64, i64, d]
+        _lib.orc_stencil_taps.argtypes = [ctypes.c_int32, ctypes.c_double,
+                                          ctypes.POINTER(i64), d, d]
+        _lib.orc_stencil_taps.restype = i64
+        _lib.orc_box_ordinal.argtypes = [i64] * 6
+        _lib.orc_box_ordinal.restype = i64
+        _lib.orc_neumaier_sum.argtypes = [d, i64]
+        _lib.orc_neumaier_sum.restype = ctypes.c_double
+    return _lib
+
+
+def _dp(a: np.ndarray):
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+class OracleError(RuntimeError):
+    pass
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise OracleError(_L().orc_last_error().decode())
+
+
+@dataclass
+class Problem:
+    """A relaxation problem (domain n0 x n1 split into b0 x b1 boxes)."""
+    n0: int
+    n1: int
+    h: float
+    lam: float
+    b0: int | None = None
+    b1: int | None = None
+    ghost: int = 1
+    bc: int = BC_PERIODIC
+    stencil: int = ST_LAPLACE5
+    rhs_correction: bool = False
+    nsweeps: int = 0
+    norm_every: int = 0
+
+    def c(self) -> _Problem:
+        return _Problem(self.n0, self.n1, self.b0 or self.n0, self.b1 or self.n1,
+                        self.ghost, self.bc, self.stencil, int(self.rhs_correction),
+                        self.h, self.lam, self.nsweeps, self.norm_every)
+
+    @property
+    def gshape(self):
+        return (self.n1 + 2 * self.ghost, self.n0 + 2 * self.ghost)
+
+    def n_norms(self) -> int:
+        if self.norm_every < 0:
+            return 0
+        k = 0
+        if self.norm_every > 0:
+            k = (self.nsweeps + self.norm_every - 1) // self.norm_every
+        return k + 1
+
+
+def ghosted(p: Problem, interior: np.ndarray, ghost_values: float | np.ndarray = 0.0) -> np.ndarray:
+    """Embed an (n1, n0) interior array into a global ghosted array."""
+    g = p.ghost
+    out = np.empty(p.gshape, dtype=np.float64)
+    out[...] = ghost_values
+    out[g:g + p.n1, g:g + p.n0] = interior
+    return out
+
+
+def solve(p: Problem, phi0_g: np.ndarray, rho_g: np.ndarray):
+    """Run p.nsweeps iterations of figure `Proto`.  Returns (phi_g, norms)
+    where norms[j] = (max|r|, sum r^2) of phi^(j*E) for j*E < N, then of phi^N."""
+    phi0_g = np.ascontiguousarray(phi0_g, dtype=np.float64)
+    rho_g = np.ascontiguousarray(rho_g, dtype=np.float64)
+    assert phi0_g.shape == p.gshape and rho_g.shape == p.gshape
+    out = np.zeros(p.gshape, dtype=np.float64)
+    cap = max(p.n_norms(), 1)
+    norms = np.zeros((cap, 2), dtype=np.float64)
+    nw = ctypes.c_int64(0)
+    pc = p.c()
+    _check(_L().orc_solve(ctypes.byref(pc), _dp(phi0_g), _dp(rho_g), _dp(out), _dp(norms), cap,
+                          ctypes.byref(nw)))
+    return out, norms[: nw.value]
+
+
+def apply_laplacian(p: Problem, phi_g: np.ndarray) -> np.ndarray:
+    """Δ_h φ on the interior (after the boundary exchange)."""
+    phi_g = np.ascontiguousarray(phi_g, dtype=np.float64)
+    out = np.zeros((p.n1, p.n0), dtype=np.float64)
+    pc = p.c()
+    _check(_L().orc_apply_laplacian(ctypes.byref(pc), _dp(phi_g), _dp(out)))
+    return out
+
+
+def residual(p: Problem, phi_g: np.ndarray, rho_g: np.ndarray) -> tuple[float, float]:
+    phi_g = np.ascontiguousarray(phi_g, dtype=np.float64)
+    rho_g = np.ascontiguousarray(rho_g, dtype=np.float64)
+    out = np.zeros(2, dtype=np.float64)
+    pc = p.c()
+    _check(_L().orc_residual(ctypes.byref(pc), _dp(phi_g), _dp(rho_g), _dp(out)))
+    return float(out[0]), float(out[1])
+
+
+def rhs(p: Problem, rho_g: np.ndarray) -> np.ndarray:
+    rho_g = np.ascontiguousarray(rho_g, dtype=np.float64)
+    out = np.zeros((p.n1, p.n0), dtype=np.float64)
+    pc = p.c()
+    _check(_L().orc_rhs(ctypes.byref(pc), _dp(rho_g), _dp(out)))
+    return out
+
+
+def exchange(p: Problem, glob: np.ndarray) -> np.ndarray:
+    g = np.array(glob, dtype=np.float64, order="C", copy=True)
+    pc = p.c()
+    _check(_L().orc_exchange(ctypes.byref(pc), _dp(g)))
+    return g
+
+
+def exchange_box(p: Problem, glob: np.ndarray, ib: int) -> np.ndarray:
+    glob = np.ascontiguousarray(glob, dtype=np.float64)
+    b0, b1, g = p.b0 or p.n0, p.b1 or p.n1, p.ghost
+    out = np.zeros((b1 + 2 * g, b0 + 2 * g), dtype=np.float64)
+    pc = p.c()
+    _check(_L().orc_exchange_box(ctypes.byref(pc), _dp(glob), ib, _dp(out)))
+    return out
+
+
+def apply_taps(offs, alpha, scale, src: np.ndarray, src_lo, dest_lo, dest_hi) -> np.ndarray:
+    """Eq.1 on one box: src has shape (ny, nx) over box [src_lo, src_lo+(nx-1,ny-1)]."""
+    src = np.ascontiguousarray(src, dtype=np.float64)
+    offs_a = np.ascontiguousarray(np.asarray(offs, dtype=np.int64).reshape(-1))
+    alpha_a = np.ascontiguousarray(np.asarray(alpha, dtype=np.float64))
+    ny, nx = src.shape
+    dny, dnx = dest_hi[1] - dest_lo[1] + 1, dest_hi[0] - dest_lo[0] + 1
+    out = np.zeros((dny, dnx), dtype=np.float64)
+    _check(_L().orc_apply_taps(len(alpha_a), offs_a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                               _dp(alpha_a), scale, _dp(src), src_lo[0], src_lo[1],
+                               src_lo[0] + nx - 1, src_lo[1] + ny - 1, dest_lo[0], dest_lo[1],
+                               dest_hi[0], dest_hi[1], _dp(out)))
+    return out
+
+
+def stencil_taps(kind: int, h: float):
+    offs = np.zeros(32, dtype=np.int64)
+    alpha = np.zeros(16, dtype=np.float64)
+    scale = ctypes.c_double(0)
+    n = _L().orc_stencil_taps(kind, h, offs.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                              _dp(alpha), ctypes.byref(scale))
+    return offs[: 2 * n].reshape(n, 2).copy(), alpha[:n].copy(), scale.value
+
+
+def box_ordinal(lo, hi, p) -> int:
+    return int(_L().orc_box_ordinal(lo[0], lo[1], hi[0], hi[1], p[0], p[1]))
+
+
+def neumaier_sum(x: np.ndarray) -> float:
+    x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1)
+    return float(_L().orc_neumaier_sum(_dp(x), x.size))
