@@ -1,0 +1,358 @@
+#!/usr/bin/env python
+"""bench.py -- fp64 Gcell-updates/s of the fused relax sweep (BASELINE.json metric).
+
+Default workload (N=1): BASELINE config 3, a 16384x16384 fp64 periodic 2D
+Poisson problem, 5-point Laplacian, slab layout of 256x256 boxes, ρ = the
+seeded counter-hash field (synthetic, generated on the device), φ0 = 0,
+h = 2^-14, λ = h²/8.  One STEP = one px_solve of 100 Jacobi sweeps (the
+paper's fixed 100 iterations) with the residual max/L2 norm recorded
+every sweep, replayed from a CUDA graph; the multi-GPU run splits the same
+16384² domain into slabs over N ranks (strong scaling) with a per-sweep
+NCCL ghost exchange and the residual all-reduce.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3|C2|C1|C5]
+    python bench.py --impl reference ...   # the CPU oracle on a bounded sample
+
+Prints ONE JSON line on rank 0.  Inputs (3 x 2.15 GB) exceed the 126 MB L2,
+so no L2 flush is needed between steps (config.l2 says so).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fp64 Gcell-updates/s of fused relax sweep at 1/2/4/8 B200; % HBM roofline"
+UNIT = "Gcell-updates/s"
+BYTES_PER_CELL_UPDATE = 24  # read φ 8 + read ρ 8 + write φ' 8
+
+CONFIGS = {
+    "C3": dict(n=16384, box=256, bc=0, stencil=0, sweeps=100, norm_every=1, rho="hash",
+               desc="BASELINE config 3: 2D Poisson 16384x16384 fp64, periodic, 5-point, "
+                    "slab-decomposed, per-sweep ghost exchange and residual all-reduce"),
+    "C2": dict(n=1024, box=1024, bc=0, stencil=0, sweeps=1000, norm_every=10, rho="hash",
+               desc="BASELINE config 2: 2D Poisson 1024x1024 single box, 1000 sweeps, "
+                    "max-norm every 10 (L2-resident)"),
+    "C1": dict(n=64, box=64, bc=1, stencil=0, sweeps=100, norm_every=1, rho="sine",
+               desc="BASELINE config 1: 64x64 box + 1 ghost layer, Dirichlet, 100 sweeps"),
+    "C5": dict(n=8192, box=256, bc=1, stencil=1, sweeps=100, norm_every=1, rho="sine",
+               desc="BASELINE config 5: 8192x8192 Mehrstellen 9-point, Dirichlet-CC"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        return float(m["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic(config):
+    """Per-launch DRAM bytes of the relax kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "relax_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        e = d.get(config)
+        return None if e is None else float(e["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------- oracle arm
+def oracle_sample(cfg, n_sample: int, sweeps: int):
+    """Run the CPU oracle (test infrastructure, allowed here for cpu_baseline /
+    --impl reference only) on a bounded sample of the workload."""
+    import numpy as np
+
+    import oracle
+    from paper_2307_07931_b200 import inputs
+    n = n_sample
+    h = 1.0 / n
+    bc = {0: oracle.BC_PERIODIC, 1: oracle.BC_DIRICHLET_CC}[cfg["bc"]]
+    lam = h * h / 8
+    box = min(cfg["box"], n)
+    p = oracle.Problem(n, n, h, lam, b0=box, b1=box, bc=bc, stencil=cfg["stencil"],
+                       nsweeps=sweeps, norm_every=cfg["norm_every"])
+    rho = inputs.hash_field(n, n) if cfg["rho"] == "hash" else inputs.sine_field(n, n)
+    rho_g = oracle.ghosted(p, rho)
+    phi_g = np.zeros_like(rho_g)
+    t0 = time.perf_counter()
+    oracle.solve(p, phi_g, rho_g)
+    dt = time.perf_counter() - t0
+    return n * n * sweeps / dt / 1e9, dt
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg = CONFIGS[args.config]
+    n_s = min(cfg["n"], 2048)
+    sweeps = 10 if cfg["n"] > 2048 else cfg["sweeps"]
+    for _ in range(args.warmup):
+        oracle_sample(cfg, n_s, sweeps)
+    rates, times = [], []
+    for _ in range(args.steps):
+        r, dt = oracle_sample(cfg, n_s, sweeps)
+        rates.append(r)
+        times.append(dt)
+    total = n_s * n_s * sweeps * args.steps / sum(times) / 1e9
+    sample = f"oracle (single-threaded C++, unfused Proto order) on {n_s}x{n_s} of the same recipe, {sweeps} sweeps per step"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": total, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": cfg["desc"], "sample": sample},
+        "cpu_baseline": {"value": total, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": total, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ----------------------------------------------------------------- native arm
+def run_native(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2307_07931_b200 import inputs
+    from paper_2307_07931_b200 import protox as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = CONFIGS[args.config]
+    n, S, E = cfg["n"], cfg["sweeps"], cfg["norm_every"]
+    h = 1.0 / n
+    lam = h * h / 8
+    box = cfg["box"]
+    lay = P.Layout(P.box(0, 0, n - 1, n - 1), (box, box), 1, cfg["bc"], world)
+    li = lay.local(rank)
+    phi, scr, rho = lay.alloc(rank, dev), lay.alloc(rank, dev), lay.alloc(rank, dev)
+    comm = None
+    if world > 1:
+        obj = [P.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = P.Comm(obj[0], world, rank, local)
+    stream = torch.cuda.Stream(device=dev)
+    prm = P.relax_params(h, lam, cfg["stencil"])
+    with torch.cuda.stream(stream):
+        kind = P.PX_FIELD_HASH if cfg["rho"] == "hash" else P.PX_FIELD_SINE
+        P.init_field(lay, rank, lay.patch(rank, rho), kind, inputs.DEFAULT_SEED, 1, 1, stream=stream)
+        rhs = rho
+        if cfg["stencil"] == 1:
+            P.exchange_ghosts(lay, comm, rank, lay.patch(rank, rho), stream=stream)
+            rhs = lay.alloc(rank, dev)
+            P.mehrstellen_rhs(lay.patch(rank, rho), lay.patch(rank, rhs), li.owned, stream=stream)
+    stream.synchronize()
+    pa, pb, pr = lay.patch(rank, phi), lay.patch(rank, scr), lay.patch(rank, rhs)
+
+    def step():
+        return P.solve(lay, comm, rank, prm, S, E, pa, pb, pr, use_graph=True, stream=stream)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 3)):
+        res = step()
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = P.kernel_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        res = step()
+    ev1.record(stream)
+    barrier()
+    launches = P.kernel_launch_count() - launches0
+    clk = clocks.stop()
+    t_ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_ms = float(t.item())
+    cells = n * n * S * args.steps
+    value = cells / (t_ms * 1e-3) / 1e9
+
+    # ---- roofline of the dominant kernel (fused relax sweep, the same
+    # k_stream<RELAX> launch geometry over this rank's slab), timed live with
+    # CUDA events on the launching stream.
+    nb = P.norm_buffer(li.owned, dev)
+    reps = 20
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    P.exchange_ghosts(lay, comm, rank, pa, stream=stream)
+    for i in range(reps):
+        evs[i][0].record(stream)
+        P.relax_step(prm, pa if i % 2 == 0 else pb, pb if i % 2 == 0 else pa, pr, li.owned, nb, stream=stream)
+        evs[i][1].record(stream)
+    stream.synchronize()
+    k_ms = statistics.mean(a.elapsed_time(b) for a, b in evs[2:])
+    local_cells = (li.owned.hi.c[0] - li.owned.lo.c[0] + 1) * (li.owned.hi.c[1] - li.owned.lo.c[1] + 1)
+    achieved = BYTES_PER_CELL_UPDATE * local_cells / (k_ms * 1e-3) / 1e9
+    peak, peak_src = load_peaks()
+    traffic = load_traffic(args.config) if world == 1 else None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "kernel": "k_stream<RELAX,5pt>" if cfg["stencil"] == 0 else "k_stream<RELAX,9pt>",
+                "kernel_ms": k_ms, "algorithmic_bytes_per_launch": BYTES_PER_CELL_UPDATE * local_cells,
+                "peak_source": peak_src, "whole_step_GBps": BYTES_PER_CELL_UPDATE * value}
+
+    # ---- end to end through the public host API (pinned host buffers, H2D of
+    # φ0 and ρ, the solve, D2H of φ^N and the norms inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        ny = li.owned.hi.c[1] - li.owned.lo.c[1] + 1
+        h_phi0 = torch.zeros((ny, n), dtype=torch.float64).pin_memory()
+        h_rho = lay.view(rank, rho if cfg["stencil"] == 0 else rhs).cpu().pin_memory()
+        h_out = torch.empty((ny, n), dtype=torch.float64).pin_memory()
+        ke = min(args.steps, 5)
+        if world == 1:
+            def e2e_step():
+                P.solve_host(lay, prm, S, E, h_phi0.numpy(), h_rho.numpy(), h_out.numpy(),
+                             use_graph=True, stream=stream)
+        else:
+            d_phi, d_scr, d_rhs = lay.alloc(rank, dev), lay.alloc(rank, dev), lay.alloc(rank, dev)
+            qa, qb, qr = lay.patch(rank, d_phi), lay.patch(rank, d_scr), lay.patch(rank, d_rhs)
+
+            def e2e_step():
+                with torch.cuda.stream(stream):
+                    lay.view(rank, d_phi).copy_(h_phi0, non_blocking=True)
+                    lay.view(rank, d_rhs).copy_(h_rho, non_blocking=True)
+                r = P.solve(lay, comm, rank, prm, S, E, qa, qb, qr, use_graph=True, stream=stream)
+                with torch.cuda.stream(stream):
+                    h_out.copy_(lay.view(rank, d_scr if r.in_scratch else d_phi), non_blocking=True)
+                stream.synchronize()
+        e2e_step()
+        barrier()
+        w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w0.record(stream)
+        for _ in range(ke):
+            e2e_step()
+        w1.record(stream)
+        barrier()
+        te = torch.tensor([w0.elapsed_time(w1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        n_norm = (S + E - 1) // E + 1 if E > 0 else 1
+        e2e = {"value": n * n * S * ke / (te.item() * 1e-3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": 2 * n * n * 8, "d2h_bytes_per_step": n * n * 8 + 16 * n_norm,
+               "steps": ke, "api": "px_solve_host" if world == 1 else "torch pinned copies + px_solve"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        n_s, sw = (min(n, 4096), 40) if n > 1024 else (n, S)
+        r, dt = oracle_sample(cfg, n_s, sw)
+        cpu = {"value": r, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"single-threaded C++ oracle, {n_s}x{n_s} of the same recipe, {sw} sweeps, {dt:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["desc"], "n": n, "sweeps_per_step": S, "norm_every": E,
+                       "box": box, "partition": f"slabs x{world}", "rho": cfg["rho"], "h": h, "lambda": lam,
+                       "l2": "inputs (3 x %.2f GB) exceed L2; no flush" % (lay.local(0).alloc_elems * 8 / 1e9)
+                       if n >= 4096 else "L2-resident working set (no flush: that is the config)"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk, "final_residual_max": float(res.norms[-1, 0]) if len(res.norms) else None,
+        }
+        print(json.dumps(line))
+    if comm is not None:
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_native(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

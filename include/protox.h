@@ -1,0 +1,296 @@
+/*
+ * protox.h -- C ABI of libprotox, the B200-native fused 2D Poisson point-Jacobi
+ * relaxation of ProtoX (arXiv 2307.07931; /root/reference/PAPER.md = "P").
+ *
+ * The method (figure `Proto` P:154-180): on a domain Ω split into
+ * boxes with ghost cells, iterate
+ *     φ ← φ + λ (Δ_h φ − ρ)                  (Eq.3)
+ * where Δ_h φ = scale · S(φ), S the 5-point stencil [0,1,0;1,-4,1;0,1,0]
+ * (Eq.1) with scale = 1/h², and report the residual
+ * r = Δ_h φ − ρ by its max norm (Eq.7) and Σr².
+ * ProtoX fuses stencil, update and norm into one loop; libprotox
+ * fuses them into one memory-bound CUDA pass per sweep on sm_100a.
+ *
+ * Conventions (all calls):
+ *  - Every call returns px_status; nothing throws or aborts across the ABI.
+ *    On failure px_last_error() holds a thread-local message.
+ *  - Arguments are validated before anything is enqueued; a failed call
+ *    enqueues no work.
+ *  - x = dimension 0 = fastest in memory; cell (x, y) of a patch is
+ *    data[(x - box.lo.c[0]) + (y - box.lo.c[1]) * ld]  (layout fixed by the
+ *    index arithmetic of Fig. ProtoX).
+ *  - Field memory (φ, φ', ρ, norm buffers) is ALLOCATED BY THE CALLER
+ *    (e.g. torch tensors) with sizes from px_layout_local / px_norm_buffer_len.
+ *    The library never frees or retains caller memory beyond a call, except
+ *    that px_solve's cached CUDA-graph plans capture the pointers (see there).
+ *  - `px_stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *    stream).  Device-side calls are asynchronous on that stream unless stated.
+ *  - Handles (px_layout, px_comm) are not thread-safe.
+ *  - fp64 throughout.  All kernels evaluate each cell with the same
+ *    expression tree as the oracle, each * and + rounded separately
+ *    (DESIGN.md §3 R10), so results are bit-identical to oracle/ for any h, λ.
+ */
+#ifndef PROTOX_H
+#define PROTOX_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PX_API_VERSION 1
+
+typedef enum {
+  PX_OK = 0,
+  PX_ERR_ARG = 1,         /* null pointer, bad enum, non-positive size          */
+  PX_ERR_SHAPE = 2,       /* layout/patch shape mismatch     */
+  PX_ERR_DOMAIN = 3,      /* point outside box, stencil reads outside src patch */
+  PX_ERR_ALIGN = 4,       /* ld odd, or phi/rhs/out 16-byte phases differ       */
+  PX_ERR_UNSUPPORTED = 5, /* valid request this build does not implement       */
+  PX_ERR_CUDA = 6,        /* CUDA runtime error (message has the CUDA string)   */
+  PX_ERR_NCCL = 7,        /* NCCL error                                          */
+  PX_ERR_STATE = 8        /* handle in the wrong state                           */
+} px_status;
+
+const char* px_status_str(px_status s);
+/* Thread-local detail of the last failing call on this thread, e.g.
+ * "stencil domain violation at i=(63,0) tap=(1,0)".  Empty if none. */
+const char* px_last_error(void);
+int32_t px_api_version(void);
+
+/* ------------------------------------------------------------------ geometry
+ * Point in Z² and Box B = [lo, hi] with INCLUSIVE corners.
+ * A box is empty iff lo.c[d] > hi.c[d] for some d.  Host-only, pure. */
+typedef struct { int32_t c[2]; } px_point;
+typedef struct { px_point lo, hi; } px_box;
+
+int64_t px_box_size(px_box b);                    /* 0 if empty                      */
+int32_t px_box_is_empty(px_box b);
+px_box px_box_grow(px_box b, int32_t r);          /* lo-r, hi+r; may become empty    */
+px_box px_box_intersect(px_box a, px_box b);      /* componentwise max lo / min hi   */
+/* Ordinal of p in b, dimension 0 fastest: (p0-lo0) + (p1-lo1)*(hi0-lo0+1).
+ * PX_ERR_DOMAIN if p is not in b (e.g. box [(-1,-1),(64,64)]: (0,0) -> 67,
+ * (1,0) -> 68, (0,1) -> 133, the offsets of Fig. ProtoX). */
+px_status px_box_ordinal(px_box b, px_point p, int64_t* out);
+
+/* ---------------------------------------------------------- layout (Proto's
+ * box decomposition of Ω) ------------------------------
+ * The domain is split into boxes of box_size (must divide the domain).
+ * Boxes are assigned to ranks as SLABS of whole box-rows along y (dimension 1,
+ * the slow one), contiguous by rank.  Each rank stores its slab as ONE ghosted
+ * patch; boxes are logical tiles inside it.
+ *
+ * Boundary conditions (DESIGN.md §3 R5):
+ *   PERIODIC      Proto's model problems: ghosts wrap around Ω.
+ *   DIRICHLET_CC  cell-centred homogeneous Dirichlet: the ghost at depth t
+ *                 outside a face holds minus the interior cell at depth t
+ *                 (x=-t <- -φ(t-1)); corners take the product of the signs.
+ *   FIXED_GHOSTS  ghost cells outside Ω belong to the caller and are never
+ *                 written (inter-rank ghosts are still exchanged). */
+typedef enum { PX_BC_PERIODIC = 0, PX_BC_DIRICHLET_CC = 1, PX_BC_FIXED_GHOSTS = 2 } px_bc;
+typedef enum { PX_PART_SLABS = 0 } px_partition;
+typedef struct px_layout px_layout; /* opaque, library-owned */
+
+/* domain: interior cells of Ω (must be non-empty; lo may be any point).
+ * ghost: ghost width g, 1 <= g <= 16 and g <= box size; temporal blocking
+ * with k sweeps per exchange needs g >= k.  nranks >= 1 and
+ * nranks <= number of box-rows.  PX_ERR_SHAPE if box_size does not divide the
+ * domain.  *out must be released with px_layout_destroy. */
+px_status px_layout_create(px_box domain, px_point box_size, int32_t ghost, px_bc bc,
+                           int32_t nranks, px_partition part, px_layout** out);
+void px_layout_destroy(px_layout* l);
+px_status px_layout_num_boxes(const px_layout* l, int32_t* n);
+/* Box ibox (ordered dim-0 fastest over the box grid) and its owning rank. */
+px_status px_layout_box(const px_layout* l, int32_t ibox, px_box* box, int32_t* owner);
+
+/* Storage of one rank's slab (caller allocates alloc_elems doubles, 16-byte
+ * aligned, e.g. a torch.float64 CUDA tensor):
+ *   owned          interior cells of the slab
+ *   alloc          owned grown by g (the ghosted box the patch covers)
+ *   ld             row pitch in elements: roundup(n0 + 32, 16) (16 padding
+ *                  columns on each side hold the g ghost columns)
+ *   patch_offset   element offset of alloc.lo from the allocation start
+ *                  (= 16 - g, so that interior column 0 sits at element 16 of
+ *                  every row: 128-byte aligned rows for TMA / v2.f64 access)
+ *   alloc_elems    ld * (rows of alloc)
+ *   nbr_lo/nbr_hi  rank owning the cells just below/above the slab in y,
+ *                  -1 at a non-periodic domain face. */
+typedef struct {
+  px_box owned, alloc;
+  int64_t ld, patch_offset, alloc_elems;
+  int32_t nbr_lo, nbr_hi;
+} px_local_info;
+px_status px_layout_local(const px_layout* l, int32_t rank, px_local_info* out);
+
+/* ------------------------------------------------------------------ patches
+ * A device view of caller-owned memory: data points at cell box.lo, rows
+ * are ld elements apart.  (px_layout_patch builds the view of a rank's slab
+ * from the allocation start.) */
+typedef struct {
+  double* data;
+  px_box box;
+  int64_t ld;
+} px_patch;
+px_status px_layout_patch(const px_layout* l, int32_t rank, double* alloc_base, px_patch* out);
+
+/* Halo plan of one rank (host-only, pure): the y-ghost-row transfers of one
+ * exchange, in the order the library posts them inside one NCCL group --
+ * send up (to nbr_hi), send down (to nbr_lo), recv from down, recv from up.
+ * Between two ranks NCCL matches sends and receives in posting order, so
+ * the k-th send to a peer fills that peer's k-th receive from this rank.
+ * Each span starts at x = -g of its first row and holds `count` =
+ * (g-1)*ld + (n0+2g) elements (whole ghosted rows; the row padding rides
+ * along), `offset` elements from patch.data of the rank's px_layout_patch.
+ * Ranks at a non-periodic face have fewer ops; a one-rank layout has none
+ * (its periodic wrap is local).  ops must hold 4 entries. */
+typedef struct {
+  int32_t peer;    /* rank sent to / received from               */
+  int32_t is_recv; /* 0 = send, 1 = receive                      */
+  int32_t row;     /* first global row y of the span              */
+  int32_t nrows;   /* g                                           */
+  int64_t offset;  /* element offset from patch.data (x = -g, y = row) */
+  int64_t count;   /* elements in the span                        */
+} px_halo_op;
+px_status px_layout_halo_plan(const px_layout* l, int32_t rank, px_halo_op ops[4], int32_t* nops);
+
+/* ----------------------------------------------------------------- kernels */
+typedef enum { PX_LAPLACE_5PT = 0, PX_MEHRSTELLEN_9PT = 1 } px_stencil;
+/* stencil: taps in the fixed order W,E,S,N(1),C(-4) for 5-point; W,E,S,N(4),
+ * SW,SE,NW,NE(1),C(-20) for Mehrstellen (not in the paper, BASELINE config 5).
+ * scale = 1/(h*h) (5-point) or 1/(6*h*h) (9-point), computed in double on the
+ * host.  lambda is the Jacobi factor λ of Eq.3 (paper: h²/4D; an
+ * explicit parameter here, R1). */
+typedef struct {
+  int32_t stencil;
+  int32_t reserved;
+  double h;
+  double lambda;
+} px_relax_params;
+
+/* Norm buffers.  A device buffer of px_norm_buffer_len(region) doubles,
+ * ZERO-INITIALISED ONCE by the caller (the kernels restore its scratch to
+ * zero).  After a norm-producing call completes, buf[0] = max|r| (NaN if any
+ * r is NaN) and buf[1] = Σ r² over the region's cells (deterministic
+ * fixed-order reduction).  The grid L2 norm is sqrt(h² · buf[1]).
+ * Calls sharing one buffer must be ordered on one stream. */
+int64_t px_norm_buffer_len(px_box region);
+
+/* dst(i) = scale · S(src)(i) for i in dest_box (Eq.1; Proto's
+ * laplace(phiPatch, wgt)).  PX_ERR_DOMAIN (naming the first point and
+ * tap) if grow(dest_box, 1) is not inside src->box or dest_box not inside
+ * dst->box. */
+px_status px_stencil_apply(int32_t stencil, double scale, const px_patch* src, px_patch* dst,
+                           px_box dest_box, void* stream);
+
+/* One fused sweep on one patch over `region` (Fig. ProtoX semantics,
+ * P:218-238): for every cell, r = scale·S(φ_in) − rhs, φ_out = φ_in + λ·r.
+ * Ghosts of φ_in must be valid; φ_out outside region is not written.
+ * If d_norms != NULL it receives the norms of r, i.e. the residual of φ_in
+ * (the PRE-update iterate, as the fused code reports it).
+ * φ_in and φ_out must not overlap.  PX_ERR_ALIGN unless all ld are even and
+ * φ_in, φ_out, rhs have the same 16-byte phase at region.lo. */
+px_status px_relax_step(const px_relax_params* p, const px_patch* phi_in, px_patch* phi_out,
+                        const px_patch* rhs, px_box region, double* d_norms, void* stream);
+
+/* Residual norms of φ as given (computeMaxResidualAcrossProcs, single
+ * patch): r = scale·S(φ) − rhs over region, into d_norms (required). */
+px_status px_residual_norm(const px_relax_params* p, const px_patch* phi, const px_patch* rhs,
+                           px_box region, double* d_norms, void* stream);
+
+/* Mehrstellen right-hand side f = ρ + (1/12)·S5(ρ) over region (DESIGN.md
+ * R18): fourth-order correction; ρ's ghosts must be filled. */
+px_status px_mehrstellen_rhs(const px_patch* rho, px_patch* f, px_box region, void* stream);
+
+/* Device synthetic fields over a rank's patch (its owned cells; ghosts are
+ * then filled with px_fill_ghosts).  kind:
+ *   PX_FIELD_ZERO  0
+ *   PX_FIELD_HASH  ((splitmix64(seed ^ (i + j*n0)) >> 11) * 2^-53) * 2 - 1 over
+ *                  global cell (i, j) relative to domain.lo, n0 = domain width
+ *                  (bit-identical to paper_2307_07931_b200/inputs.py)
+ *   PX_FIELD_SINE  sin(kπx) sin(lπy), x = (i+½)/n0, y = (j+½)/n1 */
+typedef enum { PX_FIELD_ZERO = 0, PX_FIELD_HASH = 1, PX_FIELD_SINE = 2 } px_field;
+px_status px_init_field(const px_layout* l, int32_t rank, px_patch* dst, int32_t kind,
+                        uint64_t seed, int32_t k, int32_t l_wave, void* stream);
+
+/* Fill the ghost cells a rank can fill locally: the x-ghosts of every row
+ * (a slab always spans the domain in x: periodic wrap / Dirichlet
+ * reflection), then full-width y-ghost rows at domain faces (reflection) or,
+ * when the rank owns the whole domain, by periodic wrap.  Two phases (x then
+ * y over full rows) so corners are right. */
+px_status px_fill_ghosts(const px_layout* l, int32_t rank, px_patch* phi, void* stream);
+
+/* ------------------------------------------------------------ communicator
+ * One process per GPU.  The 128-byte NCCL unique id is created on rank 0
+ * (px_comm_unique_id) and broadcast by the caller (torch.distributed). */
+typedef struct px_comm px_comm;
+px_status px_comm_unique_id(uint8_t id[128]);
+px_status px_comm_create(const uint8_t id[128], int32_t nranks, int32_t rank, int32_t device,
+                         px_comm** out);
+void px_comm_destroy(px_comm* c);
+/* Global all-reduce of n residual norms in device memory: d_max[i] by max,
+ * d_sum[i] by sum (computeMaxResidualAcrossProcs). */
+px_status px_comm_allreduce_norms(px_comm* c, double* d_max, double* d_sum, int32_t n,
+                                  void* stream);
+
+/* Full ghost exchange of rank `rank`'s patch: px_fill_ghosts, then the
+ * y-ghost rows from the neighbour ranks over NCCL (full padded rows, so
+ * corners are right).  c may be NULL only if the layout has one rank. */
+px_status px_exchange_ghosts(const px_layout* l, px_comm* c, int32_t rank, px_patch* phi,
+                             void* stream);
+
+/* Exchange among ALL slabs of a multi-rank layout held on ONE device
+ * (local transport: device-to-device copies).  parts[r] is rank r's patch. */
+px_status px_exchange_ghosts_local(const px_layout* l, const px_patch* parts, void* stream);
+
+/* ------------------------------------------------------------------- solve
+ * N-sweep solve (figure `Proto`, fused).  nsweeps >= 0.
+ * norm_every = E: record the global residual norms of φ^(jE) for every
+ * jE < N (computed inside the sweep that consumes φ^(jE)), plus a final
+ * entry for φ^N; E = 0: final entry only; E < 0: no norms.
+ * temporal_k: sweeps per ghost exchange (1, or k <= ghost width: temporal
+ * blocking).  use_graph: capture the sweep sequence in a CUDA
+ * graph cached per (layout, comm, params, opts, pointers, stream); the
+ * captured pointers must stay valid while the layout lives.
+ *
+ * Parts: with c == NULL the layout must have exactly one rank, or be solved
+ * entirely on this device: then phi/phi_scratch/rhs are arrays of
+ * nranks patches (local transport).  With an NCCL communicator they are
+ * this rank's single patch.
+ *
+ * Host-synchronous.  On return h_norms[2j], h_norms[2j+1] hold (max|r|, Σr²)
+ * of entry j (global over all ranks), *n_written the number of entries
+ * (capped at cap), and φ^N is in phi (*in_scratch = 0) or in phi_scratch
+ * (*in_scratch = 1, odd N).  If in_scratch is NULL, φ^N is copied into phi.
+ * Inputs: phi holds φ^0 (ghosts need not be filled), rhs holds the
+ * right-hand side (ρ, or f from px_mehrstellen_rhs) on owned cells plus, for
+ * temporal_k > 1, its ghosts to depth k filled (px_exchange_ghosts). */
+typedef struct {
+  int32_t nsweeps;
+  int32_t norm_every;
+  int32_t temporal_k;
+  int32_t use_graph;
+} px_solve_opts;
+px_status px_solve(const px_layout* l, px_comm* c, int32_t rank, const px_relax_params* p,
+                   const px_solve_opts* o, px_patch* phi, px_patch* phi_scratch,
+                   const px_patch* rhs, double* h_norms, int32_t cap, int32_t* n_written,
+                   int32_t* in_scratch, void* stream);
+
+/* End-to-end solve on HOST arrays (single rank): copies φ^0 and ρ
+ * (n1 x n0 interior, dim-0 fastest, pinned or pageable host memory) to the
+ * device, solves, copies φ^N back to h_phi_out.  Device buffers are
+ * library-owned and cached by shape between calls (freed by
+ * px_release_cached).  h_norms as in px_solve. */
+px_status px_solve_host(const px_layout* l, const px_relax_params* p, const px_solve_opts* o,
+                        const double* h_phi0, const double* h_rho, double* h_phi_out,
+                        double* h_norms, int32_t cap, int32_t* n_written, void* stream);
+void px_release_cached(void);
+
+/* Diagnostics: number of kernel launches libprotox enqueued so far in this
+ * process (graph replays count their kernel nodes). */
+int64_t px_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PROTOX_H */

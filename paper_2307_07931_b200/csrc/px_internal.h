@@ -1,0 +1,127 @@
+// px_internal.h -- internal declarations shared by the libprotox sources.
+// Nothing here is part of the ABI (include/protox.h is).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "protox.h"
+
+namespace px {
+
+// ---- errors --------------------------------------------------------------
+px_status fail(px_status s, const char* fmt, ...);
+void clear_error();
+
+#define PX_TRY(expr)                   \
+  do {                                 \
+    px_status _s = (expr);             \
+    if (_s != PX_OK) return _s;        \
+  } while (0)
+
+// ---- geometry helpers ------------------------------------------------------
+inline int32_t ext(const px_box& b, int d) {
+  return b.lo.c[d] > b.hi.c[d] ? 0 : b.hi.c[d] - b.lo.c[d] + 1;
+}
+inline bool empty(const px_box& b) { return b.lo.c[0] > b.hi.c[0] || b.lo.c[1] > b.hi.c[1]; }
+inline bool contains(const px_box& outer, const px_box& inner) {
+  if (empty(inner)) return true;
+  return inner.lo.c[0] >= outer.lo.c[0] && inner.lo.c[1] >= outer.lo.c[1] &&
+         inner.hi.c[0] <= outer.hi.c[0] && inner.hi.c[1] <= outer.hi.c[1];
+}
+inline px_box mkbox(int32_t x0, int32_t y0, int32_t x1, int32_t y1) {
+  px_box b;
+  b.lo.c[0] = x0;
+  b.lo.c[1] = y0;
+  b.hi.c[0] = x1;
+  b.hi.c[1] = y1;
+  return b;
+}
+inline px_box grow(const px_box& b, int32_t r) {
+  return mkbox(b.lo.c[0] - r, b.lo.c[1] - r, b.hi.c[0] + r, b.hi.c[1] + r);
+}
+// pointer to cell (x, y) of a patch
+inline double* at(const px_patch& p, int32_t x, int32_t y) {
+  return p.data + (int64_t)(x - p.box.lo.c[0]) + (int64_t)(y - p.box.lo.c[1]) * p.ld;
+}
+
+}  // namespace px
+
+// the opaque layout (defined here so the solve driver can read it)
+struct px_layout {
+  px_box domain;
+  px_point box_size;
+  int32_t ghost;
+  px_bc bc;
+  int32_t nranks;
+  int32_t nbx, nby;                 // box grid
+  std::vector<int32_t> row_lo;      // rank r owns box-rows [row_lo[r], row_lo[r+1])
+  int64_t ld;                       // common row pitch of every rank's patch
+  uint64_t gen;                     // unique id (plan-cache key)
+};
+
+namespace px {
+
+// ---- kernel-side descriptors ----------------------------------------------
+enum : int { MODE_RELAX = 0, MODE_RESID = 1, MODE_APPLY = 2, MODE_MRHS = 3 };
+enum : int { GH_NONE = 0, GH_WRAP = 1, GH_REFLECT = 2 };
+
+// Which ghost images a relax sweep writes along with each owned cell
+// (fused exchange).  For dimension d, side 0 = lo, 1 = hi:
+// a cell within `g` of that face also writes its image there.
+struct GhostSpec {
+  int32_t mode[2][2];   // [dim][side]
+  int32_t n[2];         // extent of the owned box (the image shift for WRAP)
+  int32_t o[2];         // region.lo - owned.lo
+  int32_t g;            // depth written (0: no images)
+};
+
+// Norm reduction slot: `expected` blocks over one or more launches write
+// partials[offset + block]; the last one to finish reduces them in fixed
+// order into out[0] (max|r|) and out[1] (Σr²) and re-zeroes *counter.
+struct NormSlot {
+  double* out_max;      // null: no norms
+  double* out_sum;
+  double* partials;
+  unsigned int* counter;
+  int32_t offset;
+  int32_t expected;
+};
+
+struct StreamLaunch {
+  const double* src;  // φ_in at region.lo
+  const double* rhs;  // rhs at region.lo (may be null in APPLY mode)
+  double* dst;        // output at region.lo
+  int64_t ld_src, ld_rhs, ld_dst;
+  int32_t nx, ny;     // region extent
+  int32_t phase;      // 1 if region.lo is not 16-byte aligned (pairs start at column -1)
+  int32_t src_x0, src_x1;  // readable column range of src relative to region.lo
+  double scale, lambda;
+  GhostSpec gs;
+  NormSlot norms;     // norms.out_max == null: none
+};
+
+// number of thread blocks the stream kernel uses for a region
+int32_t stream_blocks(int32_t nx, int32_t ny, int32_t phase);
+// launchers (px_kernels.cu); return PX_ERR_CUDA on launch failure
+px_status launch_stream(int mode, int stencil, const StreamLaunch& a, cudaStream_t s);
+px_status launch_fill_ghosts(const px_layout* l, int32_t rank, const px_patch& p, cudaStream_t s);
+px_status launch_init_field(const px_layout* l, int32_t rank, const px_patch& p, int kind,
+                            uint64_t seed, int k, int lw, cudaStream_t s);
+px_status cuda_check(cudaError_t e, const char* what);
+void count_launches(int64_t n);
+
+// validation helpers (px_host.cpp)
+px_status check_patch(const px_patch* p, const char* name);
+px_status local_info(const px_layout* l, int32_t rank, px_local_info* out);
+px_status make_stream_launch(int mode, int stencil, double scale, double lambda,
+                             const px_patch* src, const px_patch* rhs, px_patch* dst,
+                             px_box region, StreamLaunch* a);
+double stencil_scale(int stencil, double h);
+uint64_t layout_generation(const px_layout* l);
+
+}  // namespace px

@@ -1,0 +1,475 @@
+// px_kernels.cu -- the hot path of libprotox: one fused, register-streaming
+// pass per sweep of
+//     L   = S(φ)                 5-point (Eq.1, taps P:198) or 9-point
+//     r   = scale·L − rhs        residual (Eq.7)
+//     φ'  = φ + λ·r              point-Jacobi update (Eq.3)
+//     max|r|, Σr²                norms, warp-shuffle + fixed-order
+//                                block/grid reduction
+// plus the fused ghost images of the new iterate (exchange).
+//
+// Design: the sweep is HBM-bound (24 B/cell-update: read φ,
+// read rhs, write φ'), so the kernel streams each array through the SM once.
+// A warp owns a 64-column strip (lane = 2 adjacent cells, 16-byte ld/st.v2.f64)
+// and walks down SW_ROWS rows keeping the rows S, C, N in registers; W/E
+// neighbours come from the adjacent lane by __shfl (lanes 0/31 load the one
+// halo cell).  Loads are issued SW_PF rows ahead of use so each thread keeps
+// several 16-byte requests in flight.  Every cell is evaluated with the
+// oracle's expression tree, each * and + rounded separately (__dmul_rn /
+// __dadd_rn), so results are bit-identical to oracle/ for any h and λ.
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdint>
+
+#include "px_internal.h"
+
+namespace px {
+
+constexpr int SW_WARPS = 8;
+constexpr int SW_THREADS = SW_WARPS * 32;
+constexpr int SW_COLS = SW_WARPS * 64;
+constexpr int SW_ROWS = 32;
+constexpr int SW_PF = 2;                  // prefetch distance in rows
+constexpr int SW_RING = SW_PF + 3;        // raw φ rows kept in flight
+constexpr unsigned FULL = 0xffffffffu;
+
+int32_t stream_blocks(int32_t nx, int32_t ny, int32_t phase) {
+  if (nx <= 0 || ny <= 0) return 0;
+  int32_t gx = (nx + phase + SW_COLS - 1) / SW_COLS;
+  int32_t gy = (ny + SW_ROWS - 1) / SW_ROWS;
+  return gx * gy;
+}
+
+// --------------------------------------------------------------- helpers
+struct Raw {            // a row as loaded: the lane's pair plus its halo cell
+  double a, b, h;       // h: column c-1 on lane 0, c+2 on lane 31
+};
+struct Fin {            // a row after the neighbour exchange
+  double w, a, b, e;    // columns c-1, c, c+1, c+2
+};
+
+__device__ __forceinline__ Raw load_raw(const double* __restrict__ row, int c, int lane, int x0,
+                                        int x1) {
+  Raw v;
+  if (c >= x0 && c + 1 <= x1) {
+    double2 p = __ldg(reinterpret_cast<const double2*>(row + c));
+    v.a = p.x;
+    v.b = p.y;
+  } else {
+    v.a = (c >= x0 && c <= x1) ? __ldg(row + c) : 0.0;
+    v.b = (c + 1 >= x0 && c + 1 <= x1) ? __ldg(row + c + 1) : 0.0;
+  }
+  v.h = 0.0;
+  if (lane == 0) {
+    if (c - 1 >= x0 && c - 1 <= x1) v.h = __ldg(row + c - 1);
+  } else if (lane == 31) {
+    if (c + 2 >= x0 && c + 2 <= x1) v.h = __ldg(row + c + 2);
+  }
+  return v;
+}
+
+__device__ __forceinline__ Fin finish(const Raw& v, int lane) {
+  Fin f;
+  f.a = v.a;
+  f.b = v.b;
+  double w = __shfl_up_sync(FULL, v.b, 1);
+  double e = __shfl_down_sync(FULL, v.a, 1);
+  f.w = (lane == 0) ? v.h : w;
+  f.e = (lane == 31) ? v.h : e;
+  return f;
+}
+
+// Undivided stencil sums for the two cells of a lane, tap order fixed
+// (R10):  5-point  W, E, S, N, C(-4);
+//                   9-point  W, E, S, N (4), SW, SE, NW, NE (1), C(-20).
+template <int ST>
+__device__ __forceinline__ void taps(const Fin& S, const Fin& C, const Fin& N, double& L0,
+                                     double& L1) {
+  if (ST == 0) {
+    L0 = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(C.w, C.b), S.a), N.a), __dmul_rn(-4.0, C.a));
+    L1 = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(C.a, C.e), S.b), N.b), __dmul_rn(-4.0, C.b));
+  } else {
+    double t;
+    t = __dmul_rn(4.0, C.w);
+    t = __dadd_rn(t, __dmul_rn(4.0, C.b));
+    t = __dadd_rn(t, __dmul_rn(4.0, S.a));
+    t = __dadd_rn(t, __dmul_rn(4.0, N.a));
+    t = __dadd_rn(t, S.w);
+    t = __dadd_rn(t, S.b);
+    t = __dadd_rn(t, N.w);
+    t = __dadd_rn(t, N.b);
+    L0 = __dadd_rn(t, __dmul_rn(-20.0, C.a));
+    t = __dmul_rn(4.0, C.a);
+    t = __dadd_rn(t, __dmul_rn(4.0, C.e));
+    t = __dadd_rn(t, __dmul_rn(4.0, S.b));
+    t = __dadd_rn(t, __dmul_rn(4.0, N.b));
+    t = __dadd_rn(t, S.a);
+    t = __dadd_rn(t, S.e);
+    t = __dadd_rn(t, N.a);
+    t = __dadd_rn(t, N.e);
+    L1 = __dadd_rn(t, __dmul_rn(-20.0, C.b));
+  }
+}
+
+__device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) {
+  return a > b ? a : b;
+}
+
+// Ghost images of one owned cell (fused exchange).  Rarely executed: only
+// cells within g of a face.
+__device__ __noinline__ void write_images(const StreamLaunch& a, int x, int y, double v) {
+  const GhostSpec& g = a.gs;
+  const int X = x + g.o[0], Y = y + g.o[1];
+  int ix[3], iy[3];
+  double sx[3], sy[3];
+  int nxi = 1, nyi = 1;
+  ix[0] = X;
+  iy[0] = Y;
+  sx[0] = sy[0] = 1.0;
+  for (int d = 0; d < 2; ++d) {
+    const int P = d ? Y : X, n = g.n[d];
+    int* im = d ? iy : ix;
+    double* sg = d ? sy : sx;
+    int& cnt = d ? nyi : nxi;
+    if (P < g.g && g.mode[d][0] != GH_NONE) {
+      im[cnt] = g.mode[d][0] == GH_WRAP ? P + n : -P - 1;
+      sg[cnt] = g.mode[d][0] == GH_REFLECT ? -1.0 : 1.0;
+      ++cnt;
+    }
+    if (P >= n - g.g && g.mode[d][1] != GH_NONE) {
+      im[cnt] = g.mode[d][1] == GH_WRAP ? P - n : 2 * n - 1 - P;
+      sg[cnt] = g.mode[d][1] == GH_REFLECT ? -1.0 : 1.0;
+      ++cnt;
+    }
+  }
+  for (int j = 0; j < nyi; ++j)
+    for (int i = 0; i < nxi; ++i) {
+      if (i == 0 && j == 0) continue;
+      a.dst[(int64_t)(ix[i] - g.o[0]) + (int64_t)(iy[j] - g.o[1]) * a.ld_dst] = v * sx[i] * sy[j];
+    }
+}
+
+// Fixed-order block reduction of (max-bits, sum), then the last block of the
+// slot reduces all partials.  Deterministic for a given launch geometry.
+__device__ void reduce_norms(const NormSlot& ns, unsigned long long mx, double ss) {
+  __shared__ unsigned long long s_mx[SW_THREADS / 32];
+  __shared__ double s_ss[SW_THREADS / 32];
+  __shared__ int s_last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nthreads = blockDim.x;
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = umax64(mx, __shfl_xor_sync(FULL, mx, o));
+    ss = ss + __shfl_xor_sync(FULL, ss, o);
+  }
+  if (lane == 0) {
+    s_mx[warp] = mx;
+    s_ss[warp] = ss;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long m = s_mx[0];
+    double s = s_ss[0];
+    for (int w = 1; w < nthreads / 32; ++w) {
+      m = umax64(m, s_mx[w]);
+      s = s + s_ss[w];
+    }
+    const int bid = ns.offset + blockIdx.x + blockIdx.y * gridDim.x;
+    ns.partials[2 * bid] = __longlong_as_double((long long)m);
+    ns.partials[2 * bid + 1] = s;
+    __threadfence();
+    unsigned t = atomicAdd(ns.counter, 1u);
+    s_last = (t == (unsigned)ns.expected - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  unsigned long long m = 0;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < ns.expected; i += nthreads) {
+    m = umax64(m, (unsigned long long)__double_as_longlong(__ldcg(ns.partials + 2 * i)));
+    s = s + __ldcg(ns.partials + 2 * i + 1);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    m = umax64(m, __shfl_xor_sync(FULL, m, o));
+    s = s + __shfl_xor_sync(FULL, s, o);
+  }
+  __syncthreads();
+  if (lane == 0) {
+    s_mx[warp] = m;
+    s_ss[warp] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    m = s_mx[0];
+    s = s_ss[0];
+    for (int w = 1; w < nthreads / 32; ++w) {
+      m = umax64(m, s_mx[w]);
+      s = s + s_ss[w];
+    }
+    *ns.out_max = __longlong_as_double((long long)m);
+    *ns.out_sum = s;
+    *ns.counter = 0u;
+    __threadfence();
+  }
+}
+
+// ------------------------------------------------------- the stream kernel
+template <int MODE, int ST>
+__global__ void __launch_bounds__(SW_THREADS, 2) k_stream(const StreamLaunch a) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = -a.phase + (blockIdx.x * SW_WARPS + warp) * 64 + 2 * lane;
+  const int r0 = blockIdx.y * SW_ROWS;
+  const int rend = min(a.ny, r0 + SW_ROWS);   // rows computed: [r0, rend)
+  const int rlast = rend;                      // last φ row needed (N of rend-1)
+  const bool need_rhs = (MODE == MODE_RELAX || MODE == MODE_RESID);
+  const bool warp_live = (-a.phase + (int)(blockIdx.x * SW_WARPS + warp) * 64) < a.nx;
+
+  unsigned long long mx = 0ull;
+  double ss = 0.0;
+
+  if (warp_live) {
+    Raw raw[SW_RING];
+    double2 rr[SW_PF + 1];
+    // prologue: φ rows r0-1 .. r0+SW_PF, rhs rows r0 .. r0+SW_PF-1
+#pragma unroll
+    for (int k = 0; k < SW_PF + 2; ++k) {
+      const int r = r0 - 1 + k;
+      if (r <= rlast) raw[k] = load_raw(a.src + (int64_t)r * a.ld_src, c, lane, a.src_x0, a.src_x1);
+    }
+    if (need_rhs) {
+#pragma unroll
+      for (int k = 0; k < SW_PF; ++k) {
+        const int r = r0 + k;
+        if (r < rend) {
+          const double* rp = a.rhs + (int64_t)r * a.ld_rhs;
+          if (c >= 0 && c + 1 < a.nx)
+            rr[k] = __ldcs(reinterpret_cast<const double2*>(rp + c));
+          else
+            rr[k] = make_double2((c >= 0 && c < a.nx) ? __ldcs(rp + c) : 0.0,
+                                 (c + 1 >= 0 && c + 1 < a.nx) ? __ldcs(rp + c + 1) : 0.0);
+        }
+      }
+    }
+    Fin fS = finish(raw[0], lane);
+    Fin fC = finish(raw[1], lane);
+
+#pragma unroll
+    for (int i = 0; i < SW_ROWS; ++i) {
+      const int r = r0 + i;
+      if (r >= rend) break;
+      // issue the loads SW_PF rows ahead
+      {
+        const int rp = r + 1 + SW_PF;
+        if (rp <= rlast)
+          raw[(i + SW_PF + 2) % SW_RING] =
+              load_raw(a.src + (int64_t)rp * a.ld_src, c, lane, a.src_x0, a.src_x1);
+        if (need_rhs) {
+          const int rq = r + SW_PF;
+          if (rq < rend) {
+            const double* q = a.rhs + (int64_t)rq * a.ld_rhs;
+            double2 v;
+            if (c >= 0 && c + 1 < a.nx)
+              v = __ldcs(reinterpret_cast<const double2*>(q + c));
+            else
+              v = make_double2((c >= 0 && c < a.nx) ? __ldcs(q + c) : 0.0,
+                               (c + 1 >= 0 && c + 1 < a.nx) ? __ldcs(q + c + 1) : 0.0);
+            rr[(i + SW_PF) % (SW_PF + 1)] = v;
+          }
+        }
+      }
+      const Fin fN = finish(raw[(i + 2) % SW_RING], lane);
+      double L0, L1;
+      taps<ST>(fS, fC, fN, L0, L1);
+      const bool va = (c >= 0 && c < a.nx), vb = (c + 1 >= 0 && c + 1 < a.nx);
+      double o0 = 0.0, o1 = 0.0;
+      if (MODE == MODE_RELAX || MODE == MODE_RESID) {
+        const double2 f = rr[i % (SW_PF + 1)];
+        const double d0 = __dmul_rn(a.scale, L0), d1 = __dmul_rn(a.scale, L1);
+        const double e0 = __dsub_rn(d0, f.x), e1 = __dsub_rn(d1, f.y);
+        if (va) {
+          mx = umax64(mx, (unsigned long long)__double_as_longlong(fabs(e0)));
+          ss = fma(e0, e0, ss);
+        }
+        if (vb) {
+          mx = umax64(mx, (unsigned long long)__double_as_longlong(fabs(e1)));
+          ss = fma(e1, e1, ss);
+        }
+        if (MODE == MODE_RELAX) {
+          o0 = __dadd_rn(fC.a, __dmul_rn(a.lambda, e0));
+          o1 = __dadd_rn(fC.b, __dmul_rn(a.lambda, e1));
+        }
+      } else if (MODE == MODE_APPLY) {
+        o0 = __dmul_rn(a.scale, L0);
+        o1 = __dmul_rn(a.scale, L1);
+      } else {  // MODE_MRHS: f = ρ + c12·S5(ρ)
+        o0 = __dadd_rn(fC.a, __dmul_rn(a.scale, L0));
+        o1 = __dadd_rn(fC.b, __dmul_rn(a.scale, L1));
+      }
+      if (MODE != MODE_RESID) {
+        double* dp = a.dst + (int64_t)r * a.ld_dst;
+        if (va && vb) {
+          *reinterpret_cast<double2*>(dp + c) = make_double2(o0, o1);
+        } else {
+          if (va) dp[c] = o0;
+          if (vb) dp[c + 1] = o1;
+        }
+        if (MODE == MODE_RELAX && a.gs.g > 0) {
+          const int Y = r + a.gs.o[1];
+          const bool yface = (Y < a.gs.g) || (Y >= a.gs.n[1] - a.gs.g);
+          const int X0 = c + a.gs.o[0];
+          const bool xface0 = (X0 < a.gs.g) || (X0 >= a.gs.n[0] - a.gs.g);
+          const bool xface1 = (X0 + 1 < a.gs.g) || (X0 + 1 >= a.gs.n[0] - a.gs.g);
+          if (va && (yface || xface0)) write_images(a, c, r, o0);
+          if (vb && (yface || xface1)) write_images(a, c + 1, r, o1);
+        }
+      }
+      fS = fC;
+      fC = fN;
+    }
+  }
+  if (MODE == MODE_RELAX || MODE == MODE_RESID) {
+    if (a.norms.out_max) reduce_norms(a.norms, mx, ss);
+  }
+}
+
+static int64_t g_launches = 0;
+void count_launches(int64_t n) { g_launches += n; }
+
+px_status cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return PX_OK;
+  return fail(PX_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+template <int MODE, int ST>
+static void launch_t(const StreamLaunch& a, dim3 grid, cudaStream_t s) {
+  k_stream<MODE, ST><<<grid, SW_THREADS, 0, s>>>(a);
+}
+
+px_status launch_stream(int mode, int stencil, const StreamLaunch& a, cudaStream_t s) {
+  if (a.nx <= 0 || a.ny <= 0) return PX_OK;
+  dim3 grid((a.nx + a.phase + SW_COLS - 1) / SW_COLS, (a.ny + SW_ROWS - 1) / SW_ROWS);
+  if (grid.y > 65535) return fail(PX_ERR_UNSUPPORTED, "region too tall (%d rows)", a.ny);
+  switch (mode * 2 + stencil) {
+    case MODE_RELAX * 2 + 0: launch_t<MODE_RELAX, 0>(a, grid, s); break;
+    case MODE_RELAX * 2 + 1: launch_t<MODE_RELAX, 1>(a, grid, s); break;
+    case MODE_RESID * 2 + 0: launch_t<MODE_RESID, 0>(a, grid, s); break;
+    case MODE_RESID * 2 + 1: launch_t<MODE_RESID, 1>(a, grid, s); break;
+    case MODE_APPLY * 2 + 0: launch_t<MODE_APPLY, 0>(a, grid, s); break;
+    case MODE_APPLY * 2 + 1: launch_t<MODE_APPLY, 1>(a, grid, s); break;
+    case MODE_MRHS * 2 + 0: launch_t<MODE_MRHS, 0>(a, grid, s); break;
+    default: return fail(PX_ERR_ARG, "bad stream mode %d / stencil %d", mode, stencil);
+  }
+  count_launches(1);
+  return cuda_check(cudaPeekAtLastError(), "stream kernel launch");
+}
+
+// ------------------------------------------------------------ ghost fill
+// Phase x: for rows [0, ny) fill columns [-g, 0) and [nx, nx+g).
+__global__ void k_ghost_x(double* o, int64_t ld, int nx, int ny, int g, int mlo, int mhi) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t total = (int64_t)ny * g * 2;
+  if (idx >= total) return;
+  const int side = (int)(idx & 1);
+  const int t = (int)((idx >> 1) % g) + 1;
+  const int y = (int)((idx >> 1) / g);
+  double* row = o + (int64_t)y * ld;
+  if (side == 0) {
+    if (mlo == GH_WRAP) row[-t] = row[nx - t];
+    else if (mlo == GH_REFLECT) row[-t] = -row[t - 1];
+  } else {
+    if (mhi == GH_WRAP) row[nx - 1 + t] = row[t - 1];
+    else if (mhi == GH_REFLECT) row[nx - 1 + t] = -row[nx - t];
+  }
+}
+// Phase y: full rows x in [-g, nx+g) of ghost rows [-g, 0) and [ny, ny+g).
+__global__ void k_ghost_y(double* o, int64_t ld, int nx, int ny, int g, int mlo, int mhi) {
+  const int64_t W = nx + 2 * g;
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= W * g * 2) return;
+  const int x = (int)(idx % W) - g;
+  const int t = (int)((idx / W) % g) + 1;
+  const int side = (int)(idx / (W * g));
+  if (side == 0) {
+    if (mlo == GH_WRAP) o[x - (int64_t)t * ld] = o[x + (int64_t)(ny - t) * ld];
+    else if (mlo == GH_REFLECT) o[x - (int64_t)t * ld] = -o[x + (int64_t)(t - 1) * ld];
+  } else {
+    if (mhi == GH_WRAP) o[x + (int64_t)(ny - 1 + t) * ld] = o[x + (int64_t)(t - 1) * ld];
+    else if (mhi == GH_REFLECT) o[x + (int64_t)(ny - 1 + t) * ld] = -o[x + (int64_t)(ny - t) * ld];
+  }
+}
+
+px_status launch_fill_ghosts(const px_layout* l, int32_t rank, const px_patch& p, cudaStream_t s) {
+  px_local_info li;
+  PX_TRY(local_info(l, rank, &li));
+  const int nx = ext(li.owned, 0), ny = ext(li.owned, 1), g = l->ghost;
+  double* o = at(p, li.owned.lo.c[0], li.owned.lo.c[1]);
+  int mx = GH_NONE, my_lo = GH_NONE, my_hi = GH_NONE;
+  if (l->bc == PX_BC_PERIODIC) mx = GH_WRAP;
+  else if (l->bc == PX_BC_DIRICHLET_CC) mx = GH_REFLECT;
+  if (li.nbr_lo < 0 && l->bc == PX_BC_DIRICHLET_CC) my_lo = GH_REFLECT;
+  if (li.nbr_hi < 0 && l->bc == PX_BC_DIRICHLET_CC) my_hi = GH_REFLECT;
+  if (l->bc == PX_BC_PERIODIC && l->nranks == 1) my_lo = my_hi = GH_WRAP;
+  if (mx != GH_NONE) {
+    int64_t n = (int64_t)ny * g * 2;
+    k_ghost_x<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(o, p.ld, nx, ny, g, mx, mx);
+    count_launches(1);
+    PX_TRY(cuda_check(cudaPeekAtLastError(), "ghost x launch"));
+  }
+  if (my_lo != GH_NONE || my_hi != GH_NONE) {
+    int64_t n = (int64_t)(nx + 2 * g) * g * 2;
+    k_ghost_y<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(o, p.ld, nx, ny, g, my_lo, my_hi);
+    count_launches(1);
+    PX_TRY(cuda_check(cudaPeekAtLastError(), "ghost y launch"));
+  }
+  return PX_OK;
+}
+
+// ------------------------------------------------------ synthetic fields
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void k_init(double* o, int64_t ld, int nx, int ny, int gx0, int gy0, int n0, int n1,
+                       int kind, uint64_t seed, int kw, int lw) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y;
+  if (x >= nx) return;
+  const int64_t i = gx0 + x, j = gy0 + y;
+  double v = 0.0;
+  if (kind == PX_FIELD_HASH) {
+    const uint64_t u = splitmix64(seed ^ (uint64_t)(i + j * (int64_t)n0));
+    v = ((double)(u >> 11) * 0x1p-53) * 2.0 - 1.0;
+  } else if (kind == PX_FIELD_SINE) {
+    v = sin(kw * M_PI * ((i + 0.5) / n0)) * sin(lw * M_PI * ((j + 0.5) / n1));
+  }
+  o[x + (int64_t)y * ld] = v;
+}
+
+px_status launch_init_field(const px_layout* l, int32_t rank, const px_patch& p, int kind,
+                            uint64_t seed, int k, int lw, cudaStream_t s) {
+  px_local_info li;
+  PX_TRY(local_info(l, rank, &li));
+  const int nx = ext(li.owned, 0), ny = ext(li.owned, 1);
+  double* o = at(p, li.owned.lo.c[0], li.owned.lo.c[1]);
+  dim3 grid((nx + 255) / 256, ny);
+  if (ny > 65535 * 32) return fail(PX_ERR_UNSUPPORTED, "too many rows");
+  // grid.y is limited to 65535: split tall slabs
+  for (int y0 = 0; y0 < ny; y0 += 65535) {
+    int h = ny - y0 < 65535 ? ny - y0 : 65535;
+    dim3 g2((nx + 255) / 256, h);
+    k_init<<<g2, 256, 0, s>>>(o + (int64_t)y0 * p.ld, p.ld, nx, h,
+                              li.owned.lo.c[0] - l->domain.lo.c[0],
+                              li.owned.lo.c[1] - l->domain.lo.c[1] + y0, ext(l->domain, 0),
+                              ext(l->domain, 1), kind, seed, k, lw);
+    count_launches(1);
+    PX_TRY(cuda_check(cudaPeekAtLastError(), "init launch"));
+  }
+  return PX_OK;
+}
+
+}  // namespace px
+
+extern "C" int64_t px_kernel_launch_count(void) { return px::g_launches; }

@@ -1,0 +1,605 @@
+// px_solve.cu -- communicator (NCCL over NVLink/NVSwitch), ghost exchange
+// and the N-sweep solve driver of libprotox (figure `Proto`, P:156-175,
+// with stencil + update + norm fused into one kernel per sweep).
+//
+// Per sweep, for a slab decomposition over P ranks:
+//   compute stream:  boundary rows [0,g) and [ny-g,ny) of φ'   (fused ghost
+//                    images along x, and at Dirichlet faces along y)
+//   comm stream:     NCCL grouped send/recv of those rows into the
+//                    neighbours' ghost rows (full padded rows -> corners right)
+//   compute stream:  interior rows [g, ny-g) of φ' -- overlaps the exchange
+//   next sweep:      waits on the exchange event.
+// Residual norms of every recorded iterate land in a device ring (max, Σr²);
+// one ncclAllReduce (max) + one (sum) over the ring at the end
+// (computeMaxResidualAcrossProcs, batched -- the solve runs a fixed
+// sweep count, R23).  Single-rank layouts skip NCCL: the fused
+// kernel writes its own periodic/Dirichlet images in both dimensions.
+// The whole sweep sequence can be captured once into a CUDA graph.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "px_internal.h"
+
+struct px_comm {
+  ncclComm_t nccl = nullptr;
+  int32_t nranks = 1, rank = 0, device = 0;
+  cudaStream_t stream = nullptr;
+};
+
+namespace px {
+
+static px_status nccl_check(ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return PX_OK;
+  return fail(PX_ERR_NCCL, "%s: %s", what, ncclGetErrorString(r));
+}
+
+static px_status check_rank_patch(const px_layout* l, int32_t rank, const px_patch* p,
+                                  const char* name, px_local_info* li) {
+  PX_TRY(check_patch(p, name));
+  PX_TRY(local_info(l, rank, li));
+  if (p->box.lo.c[0] != li->alloc.lo.c[0] || p->box.lo.c[1] != li->alloc.lo.c[1] ||
+      p->box.hi.c[0] != li->alloc.hi.c[0] || p->box.hi.c[1] != li->alloc.hi.c[1])
+    return fail(PX_ERR_SHAPE, "%s: patch box is not rank %d's ghosted slab", name, rank);
+  if (p->ld != li->ld) return fail(PX_ERR_SHAPE, "%s: ld %lld != layout ld %lld", name,
+                                   (long long)p->ld, (long long)li->ld);
+  return PX_OK;
+}
+
+// NCCL row exchange of one rank (y-ghost rows from the neighbours), posted
+// in the order of px_layout_halo_plan inside one group.
+static px_status nccl_rows(const px_layout* l, px_comm* c, int32_t rank, const px_patch& p,
+                           cudaStream_t s) {
+  px_halo_op ops[4];
+  int32_t n = 0;
+  PX_TRY(px_layout_halo_plan(l, rank, ops, &n));
+  PX_TRY(nccl_check(ncclGroupStart(), "ncclGroupStart"));
+  for (int32_t i = 0; i < n; ++i) {
+    double* buf = p.data + ops[i].offset;
+    ncclResult_t r = ops[i].is_recv
+                         ? ncclRecv(buf, (size_t)ops[i].count, ncclDouble, ops[i].peer, c->nccl, s)
+                         : ncclSend(buf, (size_t)ops[i].count, ncclDouble, ops[i].peer, c->nccl, s);
+    if (r != ncclSuccess) {
+      ncclGroupEnd();
+      return nccl_check(r, ops[i].is_recv ? "ncclRecv" : "ncclSend");
+    }
+  }
+  return nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+}
+
+// The same plan executed among all slabs held on ONE device: each receive
+// is served by the matching send of the peer (k-th send to this rank fills
+// its k-th receive from that peer) with a device-to-device copy.
+static px_status local_rows(const px_layout* l, const px_patch* parts, cudaStream_t s) {
+  for (int32_t r = 0; r < l->nranks; ++r) {
+    px_halo_op ops[4];
+    int32_t n = 0;
+    PX_TRY(px_layout_halo_plan(l, r, ops, &n));
+    for (int32_t i = 0; i < n; ++i) {
+      if (!ops[i].is_recv) continue;
+      int32_t k = 0;  // ordinal of this receive among receives from the peer
+      for (int32_t j = 0; j < i; ++j) k += (ops[j].is_recv && ops[j].peer == ops[i].peer);
+      px_halo_op pops[4];
+      int32_t pn = 0;
+      PX_TRY(px_layout_halo_plan(l, ops[i].peer, pops, &pn));
+      int32_t seen = 0, match = -1;
+      for (int32_t j = 0; j < pn; ++j)
+        if (!pops[j].is_recv && pops[j].peer == r && seen++ == k) match = j;
+      if (match < 0) return fail(PX_ERR_STATE, "halo plan mismatch between ranks %d and %d", r, ops[i].peer);
+      PX_TRY(cuda_check(cudaMemcpyAsync(parts[r].data + ops[i].offset,
+                                        parts[ops[i].peer].data + pops[match].offset,
+                                        (size_t)ops[i].count * sizeof(double),
+                                        cudaMemcpyDeviceToDevice, s),
+                        "local exchange copy"));
+    }
+  }
+  return PX_OK;
+}
+
+// ------------------------------------------------------------ solve plans
+struct PlanKey {
+  uint64_t layout_gen;
+  const px_comm* comm;
+  int32_t rank, stencil, nsweeps, norm_every, k, nparts;
+  double h, lambda;
+  std::vector<const double*> ptrs;
+  cudaStream_t stream;
+  bool operator==(const PlanKey& o) const {
+    return layout_gen == o.layout_gen && comm == o.comm && rank == o.rank && stencil == o.stencil &&
+           nsweeps == o.nsweeps && norm_every == o.norm_every && k == o.k && nparts == o.nparts &&
+           h == o.h && lambda == o.lambda && ptrs == o.ptrs && stream == o.stream;
+  }
+};
+
+struct Plan {
+  PlanKey key;
+  int32_t n_entries = 0;
+  double* d_max = nullptr;      // ring of recorded norms
+  double* d_sum = nullptr;
+  double* d_ws = nullptr;       // counter (2 doubles) + partials
+  int64_t ws_len = 0;
+  cudaGraphExec_t exec = nullptr;
+  int64_t launches_per_run = 0;
+  cudaEvent_t ev_bnd = nullptr, ev_comm = nullptr;
+  ~Plan() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (d_max) cudaFree(d_max);
+    if (d_sum) cudaFree(d_sum);
+    if (d_ws) cudaFree(d_ws);
+    if (ev_bnd) cudaEventDestroy(ev_bnd);
+    if (ev_comm) cudaEventDestroy(ev_comm);
+  }
+};
+
+static std::vector<std::unique_ptr<Plan>>& plans() {
+  static std::vector<std::unique_ptr<Plan>> v;
+  return v;
+}
+
+struct SolveCtx {
+  const px_layout* l;
+  px_comm* c;
+  int32_t rank;
+  const px_relax_params* p;
+  const px_solve_opts* o;
+  int32_t nparts;
+  const px_patch* phi;
+  const px_patch* scr;
+  const px_patch* rhs;
+  Plan* plan;
+  cudaStream_t s;
+};
+
+// fused ghost images of a part's sweep
+static GhostSpec ghost_spec(const px_layout* l, const px_local_info& li, const px_box& region,
+                            bool single_rank) {
+  GhostSpec gs;
+  std::memset(&gs, 0, sizeof gs);
+  gs.g = l->ghost;
+  gs.n[0] = ext(li.owned, 0);
+  gs.n[1] = ext(li.owned, 1);
+  gs.o[0] = region.lo.c[0] - li.owned.lo.c[0];
+  gs.o[1] = region.lo.c[1] - li.owned.lo.c[1];
+  int mx = l->bc == PX_BC_PERIODIC ? GH_WRAP : (l->bc == PX_BC_DIRICHLET_CC ? GH_REFLECT : GH_NONE);
+  gs.mode[0][0] = gs.mode[0][1] = mx;
+  if (l->bc == PX_BC_PERIODIC && single_rank) {
+    gs.mode[1][0] = gs.mode[1][1] = GH_WRAP;
+  } else if (l->bc == PX_BC_DIRICHLET_CC) {
+    gs.mode[1][0] = li.nbr_lo < 0 ? GH_REFLECT : GH_NONE;
+    gs.mode[1][1] = li.nbr_hi < 0 ? GH_REFLECT : GH_NONE;
+  }
+  return gs;
+}
+
+// The launches of one sweep (or of the final residual when resid=true).
+struct SweepLaunch {
+  StreamLaunch a;
+  int32_t blocks;
+};
+
+static px_status build_part_launches(const SolveCtx& x, int32_t part, const px_patch& in,
+                                     const px_patch& out, bool resid, bool split,
+                                     std::vector<SweepLaunch>& v) {
+  const int32_t rank = x.c ? x.rank : (x.nparts > 1 ? part : 0);
+  px_local_info li;
+  PX_TRY(local_info(x.l, rank, &li));
+  const int32_t g = x.l->ghost, ny = ext(li.owned, 1);
+  std::vector<px_box> regions;
+  const px_box& ow = li.owned;
+  if (split && ny > 2 * g) {
+    regions.push_back(mkbox(ow.lo.c[0], ow.lo.c[1], ow.hi.c[0], ow.lo.c[1] + g - 1));
+    regions.push_back(mkbox(ow.lo.c[0], ow.hi.c[1] - g + 1, ow.hi.c[0], ow.hi.c[1]));
+    regions.push_back(mkbox(ow.lo.c[0], ow.lo.c[1] + g, ow.hi.c[0], ow.hi.c[1] - g));
+  } else {
+    regions.push_back(ow);
+  }
+  const double scale = stencil_scale(x.p->stencil, x.p->h);
+  for (const px_box& rg : regions) {
+    SweepLaunch sl;
+    px_patch outp = out;
+    PX_TRY(make_stream_launch(resid ? MODE_RESID : MODE_RELAX, x.p->stencil, scale, x.p->lambda,
+                              &in, &x.rhs[part], resid ? nullptr : &outp, rg, &sl.a));
+    if (!resid) sl.a.gs = ghost_spec(x.l, li, rg, x.l->nranks == 1);
+    sl.blocks = stream_blocks(sl.a.nx, sl.a.ny, sl.a.phase);
+    v.push_back(sl);
+  }
+  return PX_OK;
+}
+
+static void set_slot(std::vector<SweepLaunch>& v, size_t first, Plan* plan, int32_t entry) {
+  int32_t total = 0;
+  for (size_t i = first; i < v.size(); ++i) total += v[i].blocks;
+  int32_t off = 0;
+  for (size_t i = first; i < v.size(); ++i) {
+    NormSlot& ns = v[i].a.norms;
+    if (entry < 0) {
+      std::memset(&ns, 0, sizeof ns);
+      continue;
+    }
+    ns.out_max = plan->d_max + entry;
+    ns.out_sum = plan->d_sum + entry;
+    ns.counter = reinterpret_cast<unsigned int*>(plan->d_ws);
+    ns.partials = plan->d_ws + 2;
+    ns.offset = off;
+    ns.expected = total;
+    off += v[i].blocks;
+  }
+}
+
+static px_status exchange_all(const SolveCtx& x, const px_patch* parts) {
+  if (x.c) {
+    PX_TRY(launch_fill_ghosts(x.l, x.rank, parts[0], x.s));
+    if (x.l->nranks > 1) {
+      PX_TRY(cuda_check(cudaEventRecord(x.plan->ev_bnd, x.s), "event record"));
+      PX_TRY(cuda_check(cudaStreamWaitEvent(x.c->stream, x.plan->ev_bnd, 0), "stream wait"));
+      PX_TRY(nccl_rows(x.l, x.c, x.rank, parts[0], x.c->stream));
+      PX_TRY(cuda_check(cudaEventRecord(x.plan->ev_comm, x.c->stream), "event record"));
+      PX_TRY(cuda_check(cudaStreamWaitEvent(x.s, x.plan->ev_comm, 0), "stream wait"));
+    }
+    return PX_OK;
+  }
+  for (int32_t r = 0; r < x.nparts; ++r) PX_TRY(launch_fill_ghosts(x.l, x.nparts > 1 ? r : 0, parts[r], x.s));
+  if (x.nparts > 1) PX_TRY(local_rows(x.l, parts, x.s));
+  return PX_OK;
+}
+
+// Copy the ghost cells at the domain faces of a rank's slab (x-ghost columns
+// of every row; full ghost rows at y faces) from `a` to `b`.
+static px_status copy_face_ghosts(const px_layout* l, int32_t rank, const px_patch& a,
+                                  const px_patch& b, cudaStream_t s) {
+  px_local_info li;
+  PX_TRY(local_info(l, rank, &li));
+  const int32_t g = l->ghost, nx = ext(li.owned, 0), ny = ext(li.owned, 1);
+  const size_t pitch = li.ld * sizeof(double);
+  const int32_t x0 = li.owned.lo.c[0], y0 = li.owned.lo.c[1];
+  for (int side = 0; side < 2; ++side) {
+    const int32_t xs = side ? x0 + nx : x0 - g;
+    PX_TRY(cuda_check(cudaMemcpy2DAsync(at(b, xs, y0), pitch, at(a, xs, y0), pitch, g * sizeof(double),
+                                        ny, cudaMemcpyDeviceToDevice, s), "copy ghost columns"));
+  }
+  const size_t row = ext(li.alloc, 0) * sizeof(double);
+  if (li.nbr_lo < 0)
+    PX_TRY(cuda_check(cudaMemcpy2DAsync(at(b, x0 - g, y0 - g), pitch, at(a, x0 - g, y0 - g), pitch, row, g,
+                                        cudaMemcpyDeviceToDevice, s), "copy ghost rows"));
+  if (li.nbr_hi < 0)
+    PX_TRY(cuda_check(cudaMemcpy2DAsync(at(b, x0 - g, y0 + ny), pitch, at(a, x0 - g, y0 + ny), pitch, row, g,
+                                        cudaMemcpyDeviceToDevice, s), "copy ghost rows"));
+  return PX_OK;
+}
+
+// Enqueue the whole solve on x.s (directly, or under graph capture).
+static px_status enqueue_solve(const SolveCtx& x) {
+  const int32_t N = x.o->nsweeps, E = x.o->norm_every;
+  Plan* plan = x.plan;
+  const bool nccl_multi = x.c && x.l->nranks > 1;
+  // exchange ghosts of φ^0
+  PX_TRY(exchange_all(x, x.phi));
+  // FIXED_GHOSTS: the caller's ghost cells at domain faces belong to every
+  // iterate (oracle R5); copy them into the scratch buffer once.
+  if (x.l->bc == PX_BC_FIXED_GHOSTS) {
+    for (int32_t part = 0; part < x.nparts; ++part)
+      PX_TRY(copy_face_ghosts(x.l, x.c ? x.rank : part, x.phi[part], x.scr[part], x.s));
+  }
+  const px_patch* cur = x.phi;
+  const px_patch* nxt = x.scr;
+  int32_t entry = 0;
+  for (int32_t it = 0; it < N; ++it) {
+    const int32_t slot = (E > 0 && it % E == 0) ? entry++ : -1;
+    std::vector<SweepLaunch> v;
+    for (int32_t part = 0; part < x.nparts; ++part)
+      PX_TRY(build_part_launches(x, part, cur[part], nxt[part], false, nccl_multi, v));
+    set_slot(v, 0, plan, slot);
+    if (nccl_multi) {
+      // boundary rows, exchange on the comm stream, interior concurrently
+      const bool split = v.size() == 3;
+      PX_TRY(launch_stream(MODE_RELAX, x.p->stencil, v[0].a, x.s));
+      if (split) PX_TRY(launch_stream(MODE_RELAX, x.p->stencil, v[1].a, x.s));
+      PX_TRY(cuda_check(cudaEventRecord(plan->ev_bnd, x.s), "event record"));
+      PX_TRY(cuda_check(cudaStreamWaitEvent(x.c->stream, plan->ev_bnd, 0), "stream wait"));
+      PX_TRY(nccl_rows(x.l, x.c, x.rank, nxt[0], x.c->stream));
+      PX_TRY(cuda_check(cudaEventRecord(plan->ev_comm, x.c->stream), "event record"));
+      if (split) PX_TRY(launch_stream(MODE_RELAX, x.p->stencil, v[2].a, x.s));
+      PX_TRY(cuda_check(cudaStreamWaitEvent(x.s, plan->ev_comm, 0), "stream wait"));
+    } else {
+      for (auto& sl : v) PX_TRY(launch_stream(MODE_RELAX, x.p->stencil, sl.a, x.s));
+      if (x.nparts > 1) PX_TRY(local_rows(x.l, nxt, x.s));
+    }
+    std::swap(cur, nxt);
+  }
+  if (E >= 0) {
+    std::vector<SweepLaunch> v;
+    for (int32_t part = 0; part < x.nparts; ++part)
+      PX_TRY(build_part_launches(x, part, cur[part], cur[part], true, false, v));
+    set_slot(v, 0, plan, entry++);
+    for (auto& sl : v) PX_TRY(launch_stream(MODE_RESID, x.p->stencil, sl.a, x.s));
+  }
+  if (nccl_multi && plan->n_entries > 0) {
+    PX_TRY(nccl_check(ncclAllReduce(plan->d_max, plan->d_max, plan->n_entries, ncclDouble,
+                                    ncclMax, x.c->nccl, x.s), "ncclAllReduce(max)"));
+    PX_TRY(nccl_check(ncclAllReduce(plan->d_sum, plan->d_sum, plan->n_entries, ncclDouble,
+                                    ncclSum, x.c->nccl, x.s), "ncclAllReduce(sum)"));
+  }
+  return PX_OK;
+}
+
+static int32_t count_entries(int32_t N, int32_t E) {
+  if (E < 0) return 0;
+  return (E > 0 ? (N + E - 1) / E : 0) + 1;
+}
+
+}  // namespace px
+
+using namespace px;
+
+extern "C" {
+
+px_status px_comm_unique_id(uint8_t id[128]) {
+  if (!id) return fail(PX_ERR_ARG, "null id");
+  static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id size");
+  ncclUniqueId u;
+  PX_TRY(nccl_check(ncclGetUniqueId(&u), "ncclGetUniqueId"));
+  std::memcpy(id, &u, 128);
+  return PX_OK;
+}
+
+px_status px_comm_create(const uint8_t id[128], int32_t nranks, int32_t rank, int32_t device,
+                         px_comm** out) {
+  if (!id || !out) return fail(PX_ERR_ARG, "null argument");
+  *out = nullptr;
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(PX_ERR_ARG, "bad rank/nranks");
+  PX_TRY(cuda_check(cudaSetDevice(device), "cudaSetDevice"));
+  std::unique_ptr<px_comm> c(new px_comm());
+  c->nranks = nranks;
+  c->rank = rank;
+  c->device = device;
+  ncclUniqueId u;
+  std::memcpy(&u, id, 128);
+  PX_TRY(nccl_check(ncclCommInitRank(&c->nccl, nranks, u, rank), "ncclCommInitRank"));
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  PX_TRY(cuda_check(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, hi),
+                    "comm stream"));
+  *out = c.release();
+  return PX_OK;
+}
+
+void px_comm_destroy(px_comm* c) {
+  if (!c) return;
+  // drop plans that reference this communicator
+  auto& v = plans();
+  v.erase(std::remove_if(v.begin(), v.end(), [c](const std::unique_ptr<Plan>& p) { return p->key.comm == c; }),
+          v.end());
+  if (c->nccl) ncclCommDestroy(c->nccl);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+px_status px_comm_allreduce_norms(px_comm* c, double* d_max, double* d_sum, int32_t n,
+                                  void* stream) {
+  if (!c || !d_max || !d_sum || n < 0) return fail(PX_ERR_ARG, "bad argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  PX_TRY(nccl_check(ncclGroupStart(), "ncclGroupStart"));
+  PX_TRY(nccl_check(ncclAllReduce(d_max, d_max, n, ncclDouble, ncclMax, c->nccl, s), "ncclAllReduce"));
+  PX_TRY(nccl_check(ncclAllReduce(d_sum, d_sum, n, ncclDouble, ncclSum, c->nccl, s), "ncclAllReduce"));
+  return nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+}
+
+px_status px_exchange_ghosts(const px_layout* l, px_comm* c, int32_t rank, px_patch* phi,
+                             void* stream) {
+  px_local_info li;
+  PX_TRY(check_rank_patch(l, rank, phi, "phi", &li));
+  if (!c && l->nranks != 1) return fail(PX_ERR_ARG, "multi-rank layout needs a communicator");
+  if (c && (c->nranks != l->nranks || c->rank != rank))
+    return fail(PX_ERR_STATE, "communicator (rank %d of %d) does not match layout/rank", c->rank,
+                c->nranks);
+  cudaStream_t s = (cudaStream_t)stream;
+  PX_TRY(launch_fill_ghosts(l, rank, *phi, s));
+  if (c && l->nranks > 1) PX_TRY(nccl_rows(l, c, rank, *phi, s));
+  return PX_OK;
+}
+
+px_status px_exchange_ghosts_local(const px_layout* l, const px_patch* parts, void* stream) {
+  if (!l || !parts) return fail(PX_ERR_ARG, "null argument");
+  px_local_info li;
+  for (int32_t r = 0; r < l->nranks; ++r) PX_TRY(check_rank_patch(l, r, &parts[r], "part", &li));
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int32_t r = 0; r < l->nranks; ++r) PX_TRY(launch_fill_ghosts(l, r, parts[r], s));
+  return local_rows(l, parts, s);
+}
+
+px_status px_solve(const px_layout* l, px_comm* c, int32_t rank, const px_relax_params* p,
+                   const px_solve_opts* o, px_patch* phi, px_patch* phi_scratch,
+                   const px_patch* rhs, double* h_norms, int32_t cap, int32_t* n_written,
+                   int32_t* in_scratch, void* stream) {
+  if (!l || !p || !o || !phi || !phi_scratch || !rhs) return fail(PX_ERR_ARG, "null argument");
+  if (o->nsweeps < 0) return fail(PX_ERR_ARG, "nsweeps must be >= 0");
+  if (!(p->h > 0.0)) return fail(PX_ERR_ARG, "h must be positive");
+  if (p->stencil != PX_LAPLACE_5PT && p->stencil != PX_MEHRSTELLEN_9PT)
+    return fail(PX_ERR_ARG, "bad stencil %d", p->stencil);
+  if (o->temporal_k != 1 && o->temporal_k != 0)
+    return fail(PX_ERR_UNSUPPORTED, "temporal_k=%d: temporal blocking not in this build", o->temporal_k);
+  if (cap < 0 || (cap > 0 && !h_norms)) return fail(PX_ERR_ARG, "bad norm output");
+  int32_t nparts = 1;
+  if (c) {
+    if (c->nranks != l->nranks || c->rank != rank)
+      return fail(PX_ERR_STATE, "communicator (rank %d of %d) does not match layout/rank",
+                  c->rank, c->nranks);
+  } else {
+    nparts = l->nranks;
+    rank = 0;
+  }
+  px_local_info li;
+  for (int32_t i = 0; i < nparts; ++i) {
+    const int32_t r = c ? rank : i;
+    PX_TRY(check_rank_patch(l, r, &phi[i], "phi", &li));
+    PX_TRY(check_rank_patch(l, r, &phi_scratch[i], "phi_scratch", &li));
+    PX_TRY(check_patch(&rhs[i], "rhs"));
+    if (!contains(rhs[i].box, li.owned)) return fail(PX_ERR_SHAPE, "rhs does not cover the slab");
+    if (((uintptr_t)phi[i].data / 8 + 0) % 2 != ((uintptr_t)phi_scratch[i].data / 8) % 2)
+      return fail(PX_ERR_ALIGN, "phi and phi_scratch have different 16-byte phases");
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  PlanKey key;
+  key.layout_gen = layout_generation(l);
+  key.comm = c;
+  key.rank = rank;
+  key.stencil = p->stencil;
+  key.nsweeps = o->nsweeps;
+  key.norm_every = o->norm_every;
+  key.k = 1;
+  key.nparts = nparts;
+  key.h = p->h;
+  key.lambda = p->lambda;
+  for (int32_t i = 0; i < nparts; ++i) {
+    key.ptrs.push_back(phi[i].data);
+    key.ptrs.push_back(phi_scratch[i].data);
+    key.ptrs.push_back(rhs[i].data);
+  }
+  key.stream = s;
+  Plan* plan = nullptr;
+  for (auto& pl : plans())
+    if (pl->key == key) plan = pl.get();
+  if (!plan) {
+    std::unique_ptr<Plan> np(new Plan());
+    np->key = key;
+    np->n_entries = count_entries(o->nsweeps, o->norm_every);
+    const int32_t ne = std::max(np->n_entries, 1);
+    int64_t maxblocks = 0;
+    for (int32_t i = 0; i < nparts; ++i) {
+      px_local_info lj;
+      PX_TRY(local_info(l, c ? rank : i, &lj));
+      // split launches add at most 2 extra partial rows of blocks
+      maxblocks += stream_blocks(ext(lj.owned, 0), ext(lj.owned, 1), 1) + 2 * stream_blocks(ext(lj.owned, 0), 1, 1);
+    }
+    np->ws_len = 2 + 2 * maxblocks;
+    PX_TRY(cuda_check(cudaMalloc(&np->d_max, ne * sizeof(double)), "cudaMalloc ring"));
+    PX_TRY(cuda_check(cudaMalloc(&np->d_sum, ne * sizeof(double)), "cudaMalloc ring"));
+    PX_TRY(cuda_check(cudaMalloc(&np->d_ws, np->ws_len * sizeof(double)), "cudaMalloc ws"));
+    PX_TRY(cuda_check(cudaMemset(np->d_ws, 0, np->ws_len * sizeof(double)), "memset ws"));
+    PX_TRY(cuda_check(cudaEventCreateWithFlags(&np->ev_bnd, cudaEventDisableTiming), "event"));
+    PX_TRY(cuda_check(cudaEventCreateWithFlags(&np->ev_comm, cudaEventDisableTiming), "event"));
+    plan = np.get();
+    plans().push_back(std::move(np));
+  }
+  SolveCtx x{l, c, rank, p, o, nparts, phi, phi_scratch, rhs, plan, s};
+  if (o->use_graph && !s) return fail(PX_ERR_ARG, "use_graph needs a non-default stream");
+  if (o->use_graph) {
+    if (!plan->exec) {
+      const int64_t before = px_kernel_launch_count();
+      PX_TRY(cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture"));
+      px_status st = enqueue_solve(x);
+      cudaGraph_t graph = nullptr;
+      cudaError_t ce = cudaStreamEndCapture(s, &graph);
+      if (st != PX_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return st;
+      }
+      PX_TRY(cuda_check(ce, "end capture"));
+      plan->launches_per_run = px_kernel_launch_count() - before;
+      count_launches(-plan->launches_per_run);
+      ce = cudaGraphInstantiate(&plan->exec, graph, 0);
+      cudaGraphDestroy(graph);
+      PX_TRY(cuda_check(ce, "graph instantiate"));
+    }
+    PX_TRY(cuda_check(cudaGraphLaunch(plan->exec, s), "graph launch"));
+    count_launches(plan->launches_per_run);
+  } else {
+    PX_TRY(enqueue_solve(x));
+  }
+  const int32_t ne = plan->n_entries;
+  std::vector<double> hm(ne), hs(ne);
+  if (ne > 0) {
+    PX_TRY(cuda_check(cudaMemcpyAsync(hm.data(), plan->d_max, ne * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H norms"));
+    PX_TRY(cuda_check(cudaMemcpyAsync(hs.data(), plan->d_sum, ne * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H norms"));
+  }
+  const bool odd = (o->nsweeps % 2) == 1;
+  if (odd && !in_scratch) {
+    for (int32_t i = 0; i < nparts; ++i) {
+      const px_patch& a = phi_scratch[i];
+      const px_patch& b = phi[i];
+      PX_TRY(cuda_check(cudaMemcpy2DAsync(b.data, b.ld * sizeof(double), a.data, a.ld * sizeof(double),
+                                          ext(a.box, 0) * sizeof(double), ext(a.box, 1),
+                                          cudaMemcpyDeviceToDevice, s), "copy result"));
+    }
+  }
+  PX_TRY(cuda_check(cudaStreamSynchronize(s), "solve"));
+  if (c && c->nccl) {
+    ncclResult_t ar;
+    ncclCommGetAsyncError(c->nccl, &ar);
+    PX_TRY(nccl_check(ar, "NCCL async error"));
+  }
+  const int32_t nw = std::min(ne, cap);
+  for (int32_t j = 0; j < nw; ++j) {
+    h_norms[2 * j] = hm[j];
+    h_norms[2 * j + 1] = hs[j];
+  }
+  if (n_written) *n_written = nw;
+  if (in_scratch) *in_scratch = odd ? 1 : 0;
+  return PX_OK;
+}
+
+// ----------------------------------------------------------- host e2e path
+struct HostBufs {
+  uint64_t gen = 0;
+  double *phi = nullptr, *scr = nullptr, *rhs = nullptr;
+  int64_t elems = 0;
+  cudaStream_t s = nullptr;
+  void release() {
+    if (phi) cudaFree(phi);
+    if (scr) cudaFree(scr);
+    if (rhs) cudaFree(rhs);
+    phi = scr = rhs = nullptr;
+    elems = 0;
+    gen = 0;
+  }
+};
+static HostBufs g_host;
+
+px_status px_solve_host(const px_layout* l, const px_relax_params* p, const px_solve_opts* o,
+                        const double* h_phi0, const double* h_rho, double* h_phi_out,
+                        double* h_norms, int32_t cap, int32_t* n_written, void* stream) {
+  if (!l || !p || !o || !h_phi0 || !h_rho || !h_phi_out) return fail(PX_ERR_ARG, "null argument");
+  if (l->nranks != 1) return fail(PX_ERR_UNSUPPORTED, "px_solve_host needs a single-rank layout");
+  px_local_info li;
+  PX_TRY(local_info(l, 0, &li));
+  if (g_host.elems != li.alloc_elems || g_host.gen != layout_generation(l)) {
+    g_host.release();
+    size_t b = li.alloc_elems * sizeof(double);
+    PX_TRY(cuda_check(cudaMalloc(&g_host.phi, b), "cudaMalloc"));
+    PX_TRY(cuda_check(cudaMalloc(&g_host.scr, b), "cudaMalloc"));
+    PX_TRY(cuda_check(cudaMalloc(&g_host.rhs, b), "cudaMalloc"));
+    PX_TRY(cuda_check(cudaMemset(g_host.phi, 0, b), "memset"));
+    PX_TRY(cuda_check(cudaMemset(g_host.scr, 0, b), "memset"));
+    PX_TRY(cuda_check(cudaMemset(g_host.rhs, 0, b), "memset"));
+    g_host.elems = li.alloc_elems;
+    g_host.gen = layout_generation(l);
+  }
+  px_patch ph, sc, rh;
+  PX_TRY(px_layout_patch(l, 0, g_host.phi, &ph));
+  PX_TRY(px_layout_patch(l, 0, g_host.scr, &sc));
+  PX_TRY(px_layout_patch(l, 0, g_host.rhs, &rh));
+  cudaStream_t s = (cudaStream_t)stream;
+  const int32_t n0 = ext(li.owned, 0), n1 = ext(li.owned, 1);
+  const size_t w = n0 * sizeof(double), dp = li.ld * sizeof(double);
+  PX_TRY(cuda_check(cudaMemcpy2DAsync(at(ph, li.owned.lo.c[0], li.owned.lo.c[1]), dp, h_phi0, w, w,
+                                      n1, cudaMemcpyHostToDevice, s), "H2D phi"));
+  PX_TRY(cuda_check(cudaMemcpy2DAsync(at(rh, li.owned.lo.c[0], li.owned.lo.c[1]), dp, h_rho, w, w,
+                                      n1, cudaMemcpyHostToDevice, s), "H2D rho"));
+  int32_t in_scr = 0;
+  PX_TRY(px_solve(l, nullptr, 0, p, o, &ph, &sc, &rh, h_norms, cap, n_written, &in_scr, stream));
+  const px_patch& res = in_scr ? sc : ph;
+  PX_TRY(cuda_check(cudaMemcpy2DAsync(h_phi_out, w, at(res, li.owned.lo.c[0], li.owned.lo.c[1]), dp, w,
+                                      n1, cudaMemcpyDeviceToHost, s), "D2H phi"));
+  return cuda_check(cudaStreamSynchronize(s), "solve_host");
+}
+
+void px_release_cached(void) {
+  plans().clear();
+  g_host.release();
+}
+
+}  // extern "C"

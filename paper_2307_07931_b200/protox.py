@@ -1,0 +1,424 @@
+"""Thin ctypes binding of libprotox (include/protox.h), same names as the C ABI.
+
+Argument marshalling only: every step of the method runs in libprotox's CUDA
+kernels.  PyTorch supplies device memory (float64 tensors), streams
+(``torch.cuda.Stream``) and process groups (only to broadcast the NCCL id).
+There is no fallback: if ``libprotox.so`` is missing or fails to load, every
+call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libprotox.so")
+
+# ---------------------------------------------------------------- constants
+PX_OK, PX_ERR_ARG, PX_ERR_SHAPE, PX_ERR_DOMAIN, PX_ERR_ALIGN = 0, 1, 2, 3, 4
+PX_ERR_UNSUPPORTED, PX_ERR_CUDA, PX_ERR_NCCL, PX_ERR_STATE = 5, 6, 7, 8
+PX_BC_PERIODIC, PX_BC_DIRICHLET_CC, PX_BC_FIXED_GHOSTS = 0, 1, 2
+PX_PART_SLABS = 0
+PX_LAPLACE_5PT, PX_MEHRSTELLEN_9PT = 0, 1
+PX_FIELD_ZERO, PX_FIELD_HASH, PX_FIELD_SINE = 0, 1, 2
+
+
+class px_point(ctypes.Structure):
+    _fields_ = [("c", ctypes.c_int32 * 2)]
+
+
+class px_box(ctypes.Structure):
+    _fields_ = [("lo", px_point), ("hi", px_point)]
+
+    def __repr__(self):
+        return f"px_box(({self.lo.c[0]},{self.lo.c[1]}),({self.hi.c[0]},{self.hi.c[1]}))"
+
+    def tuple(self):
+        return (self.lo.c[0], self.lo.c[1], self.hi.c[0], self.hi.c[1])
+
+
+class px_local_info(ctypes.Structure):
+    _fields_ = [("owned", px_box), ("alloc", px_box), ("ld", ctypes.c_int64),
+                ("patch_offset", ctypes.c_int64), ("alloc_elems", ctypes.c_int64),
+                ("nbr_lo", ctypes.c_int32), ("nbr_hi", ctypes.c_int32)]
+
+
+class px_halo_op(ctypes.Structure):
+    _fields_ = [("peer", ctypes.c_int32), ("is_recv", ctypes.c_int32), ("row", ctypes.c_int32),
+                ("nrows", ctypes.c_int32), ("offset", ctypes.c_int64), ("count", ctypes.c_int64)]
+
+
+class px_patch(ctypes.Structure):
+    _fields_ = [("data", ctypes.c_void_p), ("box", px_box), ("ld", ctypes.c_int64)]
+
+
+class px_relax_params(ctypes.Structure):
+    _fields_ = [("stencil", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("h", ctypes.c_double), ("lam", ctypes.c_double)]
+
+
+class px_solve_opts(ctypes.Structure):
+    _fields_ = [("nsweeps", ctypes.c_int32), ("norm_every", ctypes.c_int32),
+                ("temporal_k", ctypes.c_int32), ("use_graph", ctypes.c_int32)]
+
+
+def point(x, y) -> px_point:
+    p = px_point()
+    p.c[0], p.c[1] = int(x), int(y)
+    return p
+
+
+def box(x0, y0, x1, y1) -> px_box:
+    return px_box(point(x0, y0), point(x1, y1))
+
+
+# ---------------------------------------------------------------- loading
+_lib = None
+
+EXPORTS = [
+    "px_status_str", "px_last_error", "px_api_version",
+    "px_box_size", "px_box_is_empty", "px_box_grow", "px_box_intersect", "px_box_ordinal",
+    "px_layout_create", "px_layout_destroy", "px_layout_num_boxes", "px_layout_box",
+    "px_layout_local", "px_layout_patch", "px_layout_halo_plan", "px_norm_buffer_len",
+    "px_stencil_apply", "px_relax_step", "px_residual_norm", "px_mehrstellen_rhs",
+    "px_init_field", "px_fill_ghosts",
+    "px_comm_unique_id", "px_comm_create", "px_comm_destroy", "px_comm_allreduce_norms",
+    "px_exchange_ghosts", "px_exchange_ghosts_local",
+    "px_solve", "px_solve_host", "px_release_cached", "px_kernel_launch_count",
+]
+
+
+def lib():
+    """Load libprotox.so (raises if it is missing: there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"libprotox.so not built ({LIB_PATH}); run __graft_entry__.build()")
+    L = ctypes.CDLL(LIB_PATH)
+    st, i32, i64, vp = ctypes.c_int, ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p
+    P = ctypes.POINTER
+    L.px_status_str.restype = ctypes.c_char_p
+    L.px_status_str.argtypes = [st]
+    L.px_last_error.restype = ctypes.c_char_p
+    L.px_api_version.restype = i32
+    L.px_box_size.restype = i64
+    L.px_box_size.argtypes = [px_box]
+    L.px_box_is_empty.restype = i32
+    L.px_box_is_empty.argtypes = [px_box]
+    L.px_box_grow.restype = px_box
+    L.px_box_grow.argtypes = [px_box, i32]
+    L.px_box_intersect.restype = px_box
+    L.px_box_intersect.argtypes = [px_box, px_box]
+    L.px_box_ordinal.restype = st
+    L.px_box_ordinal.argtypes = [px_box, px_point, P(i64)]
+    L.px_layout_create.restype = st
+    L.px_layout_create.argtypes = [px_box, px_point, i32, st, i32, st, P(vp)]
+    L.px_layout_destroy.restype = None
+    L.px_layout_destroy.argtypes = [vp]
+    L.px_layout_num_boxes.restype = st
+    L.px_layout_num_boxes.argtypes = [vp, P(i32)]
+    L.px_layout_box.restype = st
+    L.px_layout_box.argtypes = [vp, i32, P(px_box), P(i32)]
+    L.px_layout_local.restype = st
+    L.px_layout_local.argtypes = [vp, i32, P(px_local_info)]
+    L.px_layout_patch.restype = st
+    L.px_layout_patch.argtypes = [vp, i32, vp, P(px_patch)]
+    L.px_layout_halo_plan.restype = st
+    L.px_layout_halo_plan.argtypes = [vp, i32, P(px_halo_op), P(i32)]
+    L.px_norm_buffer_len.restype = i64
+    L.px_norm_buffer_len.argtypes = [px_box]
+    L.px_stencil_apply.restype = st
+    L.px_stencil_apply.argtypes = [i32, ctypes.c_double, P(px_patch), P(px_patch), px_box, vp]
+    L.px_relax_step.restype = st
+    L.px_relax_step.argtypes = [P(px_relax_params), P(px_patch), P(px_patch), P(px_patch), px_box, vp, vp]
+    L.px_residual_norm.restype = st
+    L.px_residual_norm.argtypes = [P(px_relax_params), P(px_patch), P(px_patch), px_box, vp, vp]
+    L.px_mehrstellen_rhs.restype = st
+    L.px_mehrstellen_rhs.argtypes = [P(px_patch), P(px_patch), px_box, vp]
+    L.px_init_field.restype = st
+    L.px_init_field.argtypes = [vp, i32, P(px_patch), i32, ctypes.c_uint64, i32, i32, vp]
+    L.px_fill_ghosts.restype = st
+    L.px_fill_ghosts.argtypes = [vp, i32, P(px_patch), vp]
+    L.px_comm_unique_id.restype = st
+    L.px_comm_unique_id.argtypes = [ctypes.c_char_p]
+    L.px_comm_create.restype = st
+    L.px_comm_create.argtypes = [ctypes.c_char_p, i32, i32, i32, P(vp)]
+    L.px_comm_destroy.restype = None
+    L.px_comm_destroy.argtypes = [vp]
+    L.px_comm_allreduce_norms.restype = st
+    L.px_comm_allreduce_norms.argtypes = [vp, vp, vp, i32, vp]
+    L.px_exchange_ghosts.restype = st
+    L.px_exchange_ghosts.argtypes = [vp, vp, i32, P(px_patch), vp]
+    L.px_exchange_ghosts_local.restype = st
+    L.px_exchange_ghosts_local.argtypes = [vp, P(px_patch), vp]
+    L.px_solve.restype = st
+    L.px_solve.argtypes = [vp, vp, i32, P(px_relax_params), P(px_solve_opts), P(px_patch),
+                           P(px_patch), P(px_patch), P(ctypes.c_double), i32, P(i32), P(i32), vp]
+    L.px_solve_host.restype = st
+    L.px_solve_host.argtypes = [vp, P(px_relax_params), P(px_solve_opts), vp, vp, vp,
+                                P(ctypes.c_double), i32, P(i32), vp]
+    L.px_release_cached.restype = None
+    L.px_kernel_launch_count.restype = i64
+    _lib = L
+    return L
+
+
+class PxError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{lib().px_status_str(status).decode()}: {msg}")
+        self.status = status
+
+
+def _check(status: int):
+    if status != PX_OK:
+        raise PxError(status, lib().px_last_error().decode())
+
+
+def _stream(stream) -> int | None:
+    """Accept a torch.cuda.Stream, an int handle or None (torch's current stream)."""
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream or None
+    if isinstance(stream, int):
+        return stream or None
+    return stream.cuda_stream or None
+
+
+# ---------------------------------------------------------------- geometry
+def box_size(b: px_box) -> int:
+    return lib().px_box_size(b)
+
+
+def box_is_empty(b: px_box) -> bool:
+    return bool(lib().px_box_is_empty(b))
+
+
+def box_grow(b: px_box, r: int) -> px_box:
+    return lib().px_box_grow(b, r)
+
+
+def box_intersect(a: px_box, b: px_box) -> px_box:
+    return lib().px_box_intersect(a, b)
+
+
+def box_ordinal(b: px_box, p: px_point) -> int:
+    out = ctypes.c_int64()
+    _check(lib().px_box_ordinal(b, p, ctypes.byref(out)))
+    return out.value
+
+
+# ---------------------------------------------------------------- layout
+class Layout:
+    """px_layout handle: Proto's box decomposition into slabs."""
+
+    def __init__(self, domain: px_box, box_size, ghost: int = 1, bc: int = PX_BC_PERIODIC,
+                 nranks: int = 1, part: int = PX_PART_SLABS):
+        h = ctypes.c_void_p()
+        _check(lib().px_layout_create(domain, point(*box_size), ghost, bc, nranks, part,
+                                      ctypes.byref(h)))
+        self.h = h
+        self.domain = domain
+        self.ghost = ghost
+        self.bc = bc
+        self.nranks = nranks
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.px_layout_destroy(self.h)
+            self.h = None
+
+    @property
+    def _as_parameter_(self):
+        return self.h
+
+    def num_boxes(self) -> int:
+        n = ctypes.c_int32()
+        _check(lib().px_layout_num_boxes(self.h, ctypes.byref(n)))
+        return n.value
+
+    def box(self, i: int):
+        b, o = px_box(), ctypes.c_int32()
+        _check(lib().px_layout_box(self.h, i, ctypes.byref(b), ctypes.byref(o)))
+        return b, o.value
+
+    def local(self, rank: int = 0) -> px_local_info:
+        li = px_local_info()
+        _check(lib().px_layout_local(self.h, rank, ctypes.byref(li)))
+        return li
+
+    def halo_plan(self, rank: int) -> list:
+        """px_layout_halo_plan: the rank's y-ghost transfers in posting order."""
+        ops = (px_halo_op * 4)()
+        n = ctypes.c_int32()
+        _check(lib().px_layout_halo_plan(self.h, rank, ops, ctypes.byref(n)))
+        return [ops[i] for i in range(n.value)]
+
+    def alloc(self, rank: int = 0, device=None):
+        """Zero-filled float64 CUDA tensor sized for rank's ghosted slab."""
+        import torch
+        li = self.local(rank)
+        return torch.zeros(li.alloc_elems, dtype=torch.float64, device=device or "cuda")
+
+    def patch(self, rank: int, tensor) -> px_patch:
+        p = px_patch()
+        _check(lib().px_layout_patch(self.h, rank, ctypes.c_void_p(tensor.data_ptr()),
+                                     ctypes.byref(p)))
+        return p
+
+    def view(self, rank: int, tensor, ghosts: bool = False):
+        """(rows, cols) strided view of rank's owned cells (ghosts=True: ghosted box)."""
+        li = self.local(rank)
+        b = li.alloc if ghosts else li.owned
+        off = li.patch_offset + (b.lo.c[0] - li.alloc.lo.c[0]) + (b.lo.c[1] - li.alloc.lo.c[1]) * li.ld
+        return tensor.as_strided((b.hi.c[1] - b.lo.c[1] + 1, b.hi.c[0] - b.lo.c[0] + 1), (li.ld, 1), off)
+
+
+def norm_buffer_len(region: px_box) -> int:
+    return lib().px_norm_buffer_len(region)
+
+
+def norm_buffer(region: px_box, device=None):
+    import torch
+    return torch.zeros(norm_buffer_len(region), dtype=torch.float64, device=device or "cuda")
+
+
+def relax_params(h: float, lam: float, stencil: int = PX_LAPLACE_5PT) -> px_relax_params:
+    return px_relax_params(stencil, 0, h, lam)
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+# ---------------------------------------------------------------- kernels
+def stencil_apply(stencil: int, scale: float, src: px_patch, dst: px_patch, dest_box: px_box,
+                  stream=None):
+    _check(lib().px_stencil_apply(stencil, scale, ctypes.byref(src), ctypes.byref(dst), dest_box,
+                                  _stream(stream)))
+
+
+def relax_step(p: px_relax_params, phi_in: px_patch, phi_out: px_patch, rhs: px_patch,
+               region: px_box, norms=None, stream=None):
+    _check(lib().px_relax_step(ctypes.byref(p), ctypes.byref(phi_in), ctypes.byref(phi_out),
+                               ctypes.byref(rhs), region, _ptr(norms), _stream(stream)))
+
+
+def residual_norm(p: px_relax_params, phi: px_patch, rhs: px_patch, region: px_box, norms,
+                  stream=None):
+    _check(lib().px_residual_norm(ctypes.byref(p), ctypes.byref(phi), ctypes.byref(rhs), region,
+                                  _ptr(norms), _stream(stream)))
+
+
+def mehrstellen_rhs(rho: px_patch, f: px_patch, region: px_box, stream=None):
+    _check(lib().px_mehrstellen_rhs(ctypes.byref(rho), ctypes.byref(f), region, _stream(stream)))
+
+
+def init_field(layout: Layout, rank: int, dst: px_patch, kind: int, seed: int = 0, k: int = 1,
+               l: int = 1, stream=None):
+    _check(lib().px_init_field(layout.h, rank, ctypes.byref(dst), kind, seed, k, l, _stream(stream)))
+
+
+def fill_ghosts(layout: Layout, rank: int, phi: px_patch, stream=None):
+    _check(lib().px_fill_ghosts(layout.h, rank, ctypes.byref(phi), _stream(stream)))
+
+
+# ---------------------------------------------------------------- comm
+class Comm:
+    """NCCL communicator (one process per GPU)."""
+
+    def __init__(self, uid: bytes, nranks: int, rank: int, device: int):
+        h = ctypes.c_void_p()
+        _check(lib().px_comm_create(uid, nranks, rank, device, ctypes.byref(h)))
+        self.h = h
+        self.nranks, self.rank = nranks, rank
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().px_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        if _lib is not None:
+            self.close()
+
+
+def comm_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().px_comm_unique_id(buf))
+    return buf.raw
+
+
+def comm_allreduce_norms(comm: Comm, d_max, d_sum, n: int, stream=None):
+    _check(lib().px_comm_allreduce_norms(comm.h, _ptr(d_max), _ptr(d_sum), n, _stream(stream)))
+
+
+def exchange_ghosts(layout: Layout, comm: Comm | None, rank: int, phi: px_patch, stream=None):
+    _check(lib().px_exchange_ghosts(layout.h, comm.h if comm else None, rank, ctypes.byref(phi),
+                                    _stream(stream)))
+
+
+def exchange_ghosts_local(layout: Layout, parts: list, stream=None):
+    arr = (px_patch * len(parts))(*parts)
+    _check(lib().px_exchange_ghosts_local(layout.h, arr, _stream(stream)))
+
+
+# ---------------------------------------------------------------- solve
+@dataclass
+class SolveResult:
+    norms: np.ndarray      # (n, 2): max|r|, sum r^2 per recorded iterate
+    in_scratch: bool
+
+
+def solve(layout: Layout, comm: Comm | None, rank: int, p: px_relax_params, nsweeps: int,
+          norm_every: int, phi, phi_scratch, rhs, temporal_k: int = 1, use_graph: bool = False,
+          cap: int | None = None, stream=None, keep_in_scratch: bool = True) -> SolveResult:
+    """px_solve.  phi / phi_scratch / rhs: a px_patch, or a list of patches
+    (one per rank of the layout) when comm is None and nranks > 1."""
+    as_list = lambda v: v if isinstance(v, (list, tuple)) else [v]
+    ph, sc, rh = as_list(phi), as_list(phi_scratch), as_list(rhs)
+    n = len(ph)
+    A = px_patch * n
+    opts = px_solve_opts(nsweeps, norm_every, temporal_k, int(use_graph))
+    if cap is None:
+        cap = 0 if norm_every < 0 else ((nsweeps + norm_every - 1) // norm_every if norm_every > 0 else 0) + 1
+    norms = np.zeros((max(cap, 1), 2), dtype=np.float64)
+    nw, ins = ctypes.c_int32(0), ctypes.c_int32(0)
+    _check(lib().px_solve(layout.h, comm.h if comm else None, rank, ctypes.byref(p),
+                          ctypes.byref(opts), A(*ph), A(*sc), A(*rh),
+                          norms.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), cap,
+                          ctypes.byref(nw), ctypes.byref(ins) if keep_in_scratch else None,
+                          _stream(stream)))
+    return SolveResult(norms[: nw.value].copy(), bool(ins.value))
+
+
+def solve_host(layout: Layout, p: px_relax_params, nsweeps: int, norm_every: int,
+               phi0: np.ndarray, rho: np.ndarray, out: np.ndarray | None = None,
+               use_graph: bool = False, stream=None):
+    """px_solve_host: numpy (n1, n0) float64 host arrays (pinned torch CPU
+    tensors also accepted via .numpy()).  Returns (phi_N, norms)."""
+    phi0 = np.ascontiguousarray(phi0, dtype=np.float64)
+    rho = np.ascontiguousarray(rho, dtype=np.float64)
+    if out is None:
+        out = np.empty_like(phi0)
+    cap = 0 if norm_every < 0 else ((nsweeps + norm_every - 1) // norm_every if norm_every > 0 else 0) + 1
+    norms = np.zeros((max(cap, 1), 2), dtype=np.float64)
+    nw = ctypes.c_int32(0)
+    opts = px_solve_opts(nsweeps, norm_every, 1, int(use_graph))
+    _check(lib().px_solve_host(layout.h, ctypes.byref(p), ctypes.byref(opts),
+                               phi0.ctypes.data_as(ctypes.c_void_p), rho.ctypes.data_as(ctypes.c_void_p),
+                               out.ctypes.data_as(ctypes.c_void_p),
+                               norms.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), cap,
+                               ctypes.byref(nw), _stream(stream)))
+    return out, norms[: nw.value].copy()
+
+
+def release_cached():
+    lib().px_release_cached()
+
+
+def kernel_launch_count() -> int:
+    return lib().px_kernel_launch_count()

@@ -1,0 +1,368 @@
+"""GPU parity: libprotox (through its C ABI) against the CPU oracle on the
+same seeded inputs.  Bar: φ bit-identical to the oracle
+(canonical expression tree, every * and + rounded separately), max-norms
+bit-identical (max is order-independent), Σr² within 1e-12 relative
+(different summation order; BASELINE north star tolerance 1e-12)."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2307_07931_b200 import inputs
+from paper_2307_07931_b200 import protox as P
+
+from helpers import BC_MAP, bits_equal, owned_to_host, rel_max, to_device_ghosted, ulp_diff
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+SUM_RTOL = 1e-12
+
+
+def _orc_problem(n0, n1, h, lam, bc, st, nsweeps, E, b0=None, b1=None, g=1, corr=False):
+    return oracle.Problem(n0, n1, h, lam, b0=b0 or n0, b1=b1 or n1, ghost=g, bc=BC_MAP[bc],
+                          stencil=st, rhs_correction=corr, nsweeps=nsweeps, norm_every=E)
+
+
+def _fields(n0, n1, g, seed, bc, kind="random"):
+    rng = np.random.default_rng(seed)
+    if kind == "random":
+        phi0 = rng.uniform(-1, 1, (n1 + 2 * g, n0 + 2 * g))
+        rho = rng.uniform(-1, 1, (n1 + 2 * g, n0 + 2 * g))
+    else:
+        phi0 = np.zeros((n1 + 2 * g, n0 + 2 * g))
+        rho = np.zeros_like(phi0)
+        rho[g:g + n1, g:g + n0] = inputs.sine_field(n0, n1)
+    return phi0, rho
+
+
+def _check_norms(gpu, orc):
+    assert gpu.shape == orc.shape, (gpu.shape, orc.shape)
+    assert bits_equal(gpu[:, 0], orc[:, 0]), np.max(np.abs(gpu[:, 0] - orc[:, 0]))
+    np.testing.assert_allclose(gpu[:, 1], orc[:, 1], rtol=SUM_RTOL, atol=0)
+
+
+def run_gpu_solve(n0, n1, h, lam, bc, st, N, E, phi0_g, rho_g, g=1, box=None, nranks=1,
+                  graph=True, corr=False):
+    """Solve on the GPU; nranks > 1 runs all slabs on this device (local transport)."""
+    dom = P.box(0, 0, n0 - 1, n1 - 1)
+    lay = P.Layout(dom, box or (n0, n1 // nranks), g, bc, nranks)
+    phis, scrs, rhss, fs = [], [], [], []
+    for r in range(nranks):
+        phis.append(to_device_ghosted(lay, r, phi0_g, g))
+        scrs.append(lay.alloc(r))
+        rhss.append(to_device_ghosted(lay, r, rho_g, g))
+    if corr:
+        # Mehrstellen right-hand side f = ρ + S5(ρ)/12 (ρ ghosts by the BC rule)
+        parts = [lay.patch(r, rhss[r]) for r in range(nranks)]
+        P.exchange_ghosts_local(lay, parts)
+        for r in range(nranks):
+            f = lay.alloc(r)
+            P.mehrstellen_rhs(lay.patch(r, rhss[r]), lay.patch(r, f), lay.local(r).owned)
+            fs.append(f)
+        rhss = fs
+    stream = torch.cuda.Stream()
+    res = P.solve(lay, None, 0, P.relax_params(h, lam, st), N, E,
+                  [lay.patch(r, t) for r, t in enumerate(phis)],
+                  [lay.patch(r, t) for r, t in enumerate(scrs)],
+                  [lay.patch(r, t) for r, t in enumerate(rhss)], use_graph=graph, stream=stream)
+    out_t = scrs if res.in_scratch else phis
+    out = np.concatenate([owned_to_host(lay, r, out_t[r]) for r in range(nranks)], axis=0)
+    return out, res.norms, lay
+
+
+# --------------------------------------------------------- single sweep
+@pytest.mark.parametrize("bc", [P.PX_BC_PERIODIC, P.PX_BC_DIRICHLET_CC, P.PX_BC_FIXED_GHOSTS])
+@pytest.mark.parametrize("st", [P.PX_LAPLACE_5PT, P.PX_MEHRSTELLEN_9PT])
+@pytest.mark.parametrize("shape", [(64, 64), (1000, 77), (3, 5), (513, 70)])
+def test_relax_step_bitwise(bc, st, shape):
+    n0, n1 = shape
+    h = 1.0 / max(n0, n1)
+    lam = h * h / 8 if st == P.PX_LAPLACE_5PT else 3 * h * h / 16
+    phi0, rho = _fields(n0, n1, 1, 7 + n0, bc)
+    p = _orc_problem(n0, n1, h, lam, bc, st, 1, 1)
+    ref, rnorm = oracle.solve(p, phi0, rho)
+    lay = P.Layout(P.box(0, 0, n0 - 1, n1 - 1), (n0, n1), 1, bc, 1)
+    a = to_device_ghosted(lay, 0, phi0, 1)
+    b = lay.alloc(0)
+    r = to_device_ghosted(lay, 0, rho, 1)
+    P.fill_ghosts(lay, 0, lay.patch(0, a))
+    nb = P.norm_buffer(lay.local(0).owned)
+    P.relax_step(P.relax_params(h, lam, st), lay.patch(0, a), lay.patch(0, b), lay.patch(0, r),
+                 lay.local(0).owned, nb)
+    torch.cuda.synchronize()
+    out = owned_to_host(lay, 0, b)
+    assert bits_equal(out, ref[1:-1, 1:-1]), ulp_diff(out, ref[1:-1, 1:-1])
+    nrm = nb[:2].cpu().numpy()
+    assert nrm[0] == rnorm[0, 0]
+    assert abs(nrm[1] - rnorm[0, 1]) <= SUM_RTOL * rnorm[0, 1]
+    # the scratch of the norm buffer is left zeroed for the next call
+    assert torch.count_nonzero(nb[2:4]).item() == 0
+
+
+def test_relax_step_unaligned_region_and_phase():
+    """A region starting at an odd column (pairs start at column -1) and
+    a sub-region of the patch."""
+    n0, n1 = 130, 40
+    h = 1.0 / 128
+    lam = h * h / 8
+    phi0, rho = _fields(n0, n1, 1, 3, P.PX_BC_PERIODIC)
+    lay = P.Layout(P.box(0, 0, n0 - 1, n1 - 1), (n0, n1), 1, P.PX_BC_PERIODIC, 1)
+    a = to_device_ghosted(lay, 0, phi0, 1)
+    b = lay.alloc(0)
+    r = to_device_ghosted(lay, 0, rho, 1)
+    P.fill_ghosts(lay, 0, lay.patch(0, a))
+    region = P.box(7, 3, 100, 30)
+    nb = P.norm_buffer(region)
+    P.relax_step(P.relax_params(h, lam), lay.patch(0, a), lay.patch(0, b), lay.patch(0, r), region, nb)
+    torch.cuda.synchronize()
+    p = _orc_problem(n0, n1, h, lam, P.PX_BC_PERIODIC, 0, 1, 1)
+    ref, _ = oracle.solve(p, phi0, rho)
+    out = owned_to_host(lay, 0, b)
+    assert bits_equal(out[3:31, 7:101], ref[1:-1, 1:-1][3:31, 7:101])
+    # cells outside the region are untouched (zero)
+    assert np.all(out[:3] == 0) and np.all(out[:, :7] == 0) and np.all(out[:, 101:] == 0)
+    # residual of φ^0 restricted to the region
+    lapl = oracle.apply_laplacian(p, phi0)
+    rr = (lapl - rho[1:-1, 1:-1])[3:31, 7:101]
+    assert nb[0].item() == np.max(np.abs(rr))
+
+
+# ------------------------------------------------------------ full solves
+def test_config1_full_bitwise_and_closed_form():
+    """BASELINE config 1: 64x64 box, 1 ghost layer, Dirichlet-CC, 100 sweeps,
+    ρ = sin πx sin πy, λ = 2^-15, norms every sweep."""
+    n, N = 64, 100
+    h, lam = 1.0 / 64, 2.0**-15
+    phi0, rho = _fields(n, n, 1, 0, P.PX_BC_DIRICHLET_CC, kind="sine")
+    out, norms, _ = run_gpu_solve(n, n, h, lam, P.PX_BC_DIRICHLET_CC, 0, N, 1, phi0, rho)
+    ref, rn = oracle.solve(_orc_problem(n, n, h, lam, P.PX_BC_DIRICHLET_CC, 0, N, 1), phi0, rho)
+    assert bits_equal(out, ref[1:-1, 1:-1])
+    _check_norms(norms, rn)
+    g = math.cos(math.pi / 128) ** 2
+    np.testing.assert_allclose(norms[:, 0], g ** (np.arange(101) + 1), rtol=2e-13)
+
+
+@pytest.mark.parametrize("kind", ["sine", "hash"])
+def test_config2_full_bitwise(kind):
+    """BASELINE config 2: 1024² single box, periodic, 1000 sweeps, max-norm every 10."""
+    n, N, E = 1024, 1000, 10
+    h, lam = 1.0 / n, 2.0**-23
+    phi0 = np.zeros((n + 2, n + 2))
+    rho = np.zeros_like(phi0)
+    rho[1:-1, 1:-1] = inputs.sine_field(n, n, 2, 2) if kind == "sine" else inputs.hash_field(n, n)
+    out, norms, _ = run_gpu_solve(n, n, h, lam, P.PX_BC_PERIODIC, 0, N, E, phi0, rho)
+    ref, rn = oracle.solve(_orc_problem(n, n, h, lam, P.PX_BC_PERIODIC, 0, N, E), phi0, rho)
+    assert norms.shape == (101, 2)
+    assert bits_equal(out, ref[1:-1, 1:-1]), ulp_diff(out, ref[1:-1, 1:-1])
+    _check_norms(norms, rn)
+    if kind == "sine":
+        g = math.cos(math.pi / n) ** 2
+        m = np.arange(0, 1001, 10)
+        np.testing.assert_allclose(norms[:, 0], g**m * np.max(np.abs(rho)), rtol=1e-12)
+
+
+@pytest.mark.parametrize("bc", [P.PX_BC_PERIODIC, P.PX_BC_DIRICHLET_CC, P.PX_BC_FIXED_GHOSTS])
+@pytest.mark.parametrize("st", [P.PX_LAPLACE_5PT, P.PX_MEHRSTELLEN_9PT])
+@pytest.mark.parametrize("graph", [True, False])
+def test_solve_ragged_multibox(bc, st, graph):
+    """Non-power-of-two, ragged shapes (last warp strip and row chunk partial),
+    several boxes, odd sweep count (result in scratch), norms every 3."""
+    n0, n1, N, E = 600, 90, 17, 3
+    h = 1.0 / 600
+    lam = h * h / 8 if st == 0 else 3 * h * h / 16
+    phi0, rho = _fields(n0, n1, 1, 11, bc)
+    out, norms, _ = run_gpu_solve(n0, n1, h, lam, bc, st, N, E, phi0, rho, box=(200, 30), graph=graph)
+    ref, rn = oracle.solve(_orc_problem(n0, n1, h, lam, bc, st, N, E, b0=200, b1=30), phi0, rho)
+    assert bits_equal(out, ref[1:-1, 1:-1]), ulp_diff(out, ref[1:-1, 1:-1])
+    _check_norms(norms, rn)
+
+
+@pytest.mark.parametrize("nranks", [2, 3, 5])
+@pytest.mark.parametrize("bc", [P.PX_BC_PERIODIC, P.PX_BC_DIRICHLET_CC, P.PX_BC_FIXED_GHOSTS])
+@pytest.mark.parametrize("st", [P.PX_LAPLACE_5PT, P.PX_MEHRSTELLEN_9PT])
+def test_slab_decomposition_local_transport(nranks, bc, st):
+    """Slabs of box-rows on one device exchanging by D2D copies: identical
+    to the undecomposed oracle (decomposition invariance, P12)."""
+    n0, n1, N, E = 256, 150, 12, 4
+    h = 1.0 / 256
+    lam = h * h / 8 if st == 0 else 3 * h * h / 16
+    phi0, rho = _fields(n0, n1, 1, 5 + nranks, bc)
+    out, norms, _ = run_gpu_solve(n0, n1, h, lam, bc, st, N, E, phi0, rho, box=(64, 10), nranks=nranks)
+    ref, rn = oracle.solve(_orc_problem(n0, n1, h, lam, bc, st, N, E), phi0, rho)
+    assert bits_equal(out, ref[1:-1, 1:-1]), ulp_diff(out, ref[1:-1, 1:-1])
+    _check_norms(norms, rn)
+
+
+@pytest.mark.parametrize("g", [2, 4])
+def test_wider_ghosts_k1(g):
+    n0, n1, N = 128, 96, 9
+    h = 1.0 / 128
+    lam = h * h / 8
+    for bc in (P.PX_BC_PERIODIC, P.PX_BC_DIRICHLET_CC):
+        phi0, rho = _fields(n0, n1, g, 2 + g, bc)
+        out, norms, _ = run_gpu_solve(n0, n1, h, lam, bc, 0, N, 2, phi0, rho, g=g, box=(32, 32), nranks=3)
+        ref, rn = oracle.solve(_orc_problem(n0, n1, h, lam, bc, 0, N, 2, g=g), phi0, rho)
+        assert bits_equal(out, ref[g:-g, g:-g])
+        _check_norms(norms, rn)
+
+
+def test_mehrstellen_corrected_rhs_solve():
+    """BASELINE config 5 shape at reduced size: Dirichlet-CC, Mehrstellen with
+    f = ρ + S5(ρ)/12 computed on the device (px_mehrstellen_rhs)."""
+    n, N = 256, 50
+    h = 1.0 / n
+    lam = 2.0**-19  # h²/8
+    phi0, rho = _fields(n, n, 1, 0, P.PX_BC_DIRICHLET_CC, kind="sine")
+    out, norms, _ = run_gpu_solve(n, n, h, lam, P.PX_BC_DIRICHLET_CC, 1, N, 5, phi0, rho,
+                                  box=(64, 64), nranks=2, corr=True)
+    p = _orc_problem(n, n, h, lam, P.PX_BC_DIRICHLET_CC, 1, N, 5, corr=True)
+    ref, rn = oracle.solve(p, phi0, rho)
+    assert bits_equal(out, ref[1:-1, 1:-1])
+    _check_norms(norms, rn)
+
+
+def test_norm_every_variants_and_zero_sweeps():
+    n0, n1 = 96, 64
+    h = 1.0 / 96
+    lam = h * h / 8
+    phi0, rho = _fields(n0, n1, 1, 1, P.PX_BC_PERIODIC)
+    for N, E in [(0, 1), (0, 0), (5, 0), (5, -1), (6, 7), (8, 1)]:
+        out, norms, _ = run_gpu_solve(n0, n1, h, lam, P.PX_BC_PERIODIC, 0, N, E, phi0, rho)
+        ref, rn = oracle.solve(_orc_problem(n0, n1, h, lam, P.PX_BC_PERIODIC, 0, N, E), phi0, rho)
+        assert bits_equal(out, ref[1:-1, 1:-1])
+        if E < 0:
+            assert norms.shape[0] == 0
+        else:
+            _check_norms(norms, rn)
+
+
+def test_solve_host_e2e_matches_oracle():
+    n0, n1, N = 256, 128, 20
+    h = 1.0 / 256
+    lam = h * h / 8
+    phi0, rho = _fields(n0, n1, 1, 21, P.PX_BC_PERIODIC)
+    lay = P.Layout(P.box(0, 0, n0 - 1, n1 - 1), (n0, n1), 1, P.PX_BC_PERIODIC, 1)
+    out, norms = P.solve_host(lay, P.relax_params(h, lam), N, 5, phi0[1:-1, 1:-1], rho[1:-1, 1:-1],
+                              stream=torch.cuda.Stream())
+    ref, rn = oracle.solve(_orc_problem(n0, n1, h, lam, P.PX_BC_PERIODIC, 0, N, 5), phi0, rho)
+    assert bits_equal(out, ref[1:-1, 1:-1])
+    _check_norms(norms, rn)
+
+
+# ------------------------------------------------------------ other ops
+@pytest.mark.parametrize("st", [P.PX_LAPLACE_5PT, P.PX_MEHRSTELLEN_9PT])
+def test_stencil_apply_vs_oracle(st):
+    n0, n1 = 200, 50
+    rng = np.random.default_rng(8)
+    src = rng.uniform(-1, 1, (n1 + 2, n0 + 2))
+    lay = P.Layout(P.box(0, 0, n0 - 1, n1 - 1), (n0, n1), 1, P.PX_BC_FIXED_GHOSTS, 1)
+    a = to_device_ghosted(lay, 0, src, 1)
+    b = lay.alloc(0)
+    scale = 3.0
+    P.stencil_apply(st, scale, lay.patch(0, a), lay.patch(0, b), lay.local(0).owned)
+    torch.cuda.synchronize()
+    offs, alpha, _ = oracle.stencil_taps(st, 1.0)
+    ref = oracle.apply_taps(offs, alpha, scale, src, (-1, -1), (0, 0), (n0 - 1, n1 - 1))
+    assert bits_equal(owned_to_host(lay, 0, b), ref)
+
+
+def test_stencil_apply_domain_violation():
+    lay = P.Layout(P.box(0, 0, 63, 63), (64, 64), 1, P.PX_BC_PERIODIC, 1)
+    a, b = lay.alloc(0), lay.alloc(0)
+    with pytest.raises(P.PxError, match=r"i=\(-1,0\) tap=\(-1,0\)"):
+        P.stencil_apply(0, 1.0, lay.patch(0, a), lay.patch(0, b), P.box(-1, 0, 10, 10))
+
+
+def test_mehrstellen_rhs_vs_oracle():
+    n = 128
+    rng = np.random.default_rng(4)
+    rho = rng.uniform(-1, 1, (n + 2, n + 2))
+    lay = P.Layout(P.box(0, 0, n - 1, n - 1), (n, n), 1, P.PX_BC_DIRICHLET_CC, 1)
+    r = to_device_ghosted(lay, 0, rho, 1)
+    P.fill_ghosts(lay, 0, lay.patch(0, r))
+    f = lay.alloc(0)
+    P.mehrstellen_rhs(lay.patch(0, r), lay.patch(0, f), lay.local(0).owned)
+    torch.cuda.synchronize()
+    p = _orc_problem(n, n, 1.0 / n, 0.0, P.PX_BC_DIRICHLET_CC, 1, 0, 0, corr=True)
+    assert bits_equal(owned_to_host(lay, 0, f), oracle.rhs(p, rho))
+
+
+def test_residual_norm_vs_oracle():
+    n0, n1 = 300, 200
+    h = 1.0 / 300
+    phi0, rho = _fields(n0, n1, 1, 9, P.PX_BC_DIRICHLET_CC)
+    lay = P.Layout(P.box(0, 0, n0 - 1, n1 - 1), (n0, n1), 1, P.PX_BC_DIRICHLET_CC, 1)
+    a = to_device_ghosted(lay, 0, phi0, 1)
+    r = to_device_ghosted(lay, 0, rho, 1)
+    P.fill_ghosts(lay, 0, lay.patch(0, a))
+    nb = P.norm_buffer(lay.local(0).owned)
+    for _ in range(3):  # repeated use of one buffer (scratch restored)
+        P.residual_norm(P.relax_params(h, 0.0), lay.patch(0, a), lay.patch(0, r), lay.local(0).owned, nb)
+    torch.cuda.synchronize()
+    ref = oracle.residual(_orc_problem(n0, n1, h, 0.0, P.PX_BC_DIRICHLET_CC, 0, 0, 0), phi0, rho)
+    assert nb[0].item() == ref[0]
+    assert abs(nb[1].item() - ref[1]) <= SUM_RTOL * ref[1]
+
+
+def test_nan_propagates_to_max_norm():
+    n = 64
+    phi0, rho = _fields(n, n, 1, 1, P.PX_BC_PERIODIC)
+    phi0[20, 30] = np.nan
+    lay = P.Layout(P.box(0, 0, n - 1, n - 1), (n, n), 1, P.PX_BC_PERIODIC, 1)
+    a = to_device_ghosted(lay, 0, phi0, 1)
+    r = to_device_ghosted(lay, 0, rho, 1)
+    nb = P.norm_buffer(lay.local(0).owned)
+    P.residual_norm(P.relax_params(1.0 / n, 0.0), lay.patch(0, a), lay.patch(0, r), lay.local(0).owned, nb)
+    assert math.isnan(nb[0].item())
+
+
+def test_init_field_hash_bitwise():
+    n0, n1 = 1000, 300
+    lay = P.Layout(P.box(5, -7, 5 + n0 - 1, -7 + n1 - 1), (n0, 100), 1, P.PX_BC_PERIODIC, 3)
+    parts = []
+    for r in range(3):
+        t = lay.alloc(r)
+        P.init_field(lay, r, lay.patch(r, t), P.PX_FIELD_HASH, inputs.DEFAULT_SEED)
+        parts.append(owned_to_host(lay, r, t))
+    assert bits_equal(np.concatenate(parts, 0), inputs.hash_field(n0, n1))
+
+
+def test_fill_ghosts_matches_oracle_exchange():
+    n0, n1, g = 40, 24, 3
+    for bc in (P.PX_BC_PERIODIC, P.PX_BC_DIRICHLET_CC):
+        rng = np.random.default_rng(bc)
+        glob = rng.uniform(-1, 1, (n1 + 2 * g, n0 + 2 * g))
+        lay = P.Layout(P.box(0, 0, n0 - 1, n1 - 1), (8, 8), g, bc, 1)
+        t = to_device_ghosted(lay, 0, glob, g)
+        P.fill_ghosts(lay, 0, lay.patch(0, t))
+        ex = oracle.exchange(_orc_problem(n0, n1, 1.0, 0.0, bc, 0, 0, 0, b0=8, b1=8, g=g), glob)
+        assert bits_equal(lay.view(0, t, ghosts=True).cpu().numpy(), ex)
+
+
+def test_error_paths_on_device():
+    lay = P.Layout(P.box(0, 0, 63, 63), (64, 64), 1, P.PX_BC_PERIODIC, 1)
+    a, b, r = lay.alloc(0), lay.alloc(0), lay.alloc(0)
+    pa, pb, pr = lay.patch(0, a), lay.patch(0, b), lay.patch(0, r)
+    prm = P.relax_params(1.0 / 64, 1e-5)
+    # overlapping input/output
+    with pytest.raises(P.PxError, match="overlap"):
+        P.relax_step(prm, pa, pa, pr, lay.local(0).owned)
+    # different 16-byte phases
+    pr2 = P.px_patch(pr.data + 8, pr.box, pr.ld)
+    with pytest.raises(P.PxError, match="PX_ERR_ALIGN"):
+        P.relax_step(prm, pa, pb, pr2, lay.local(0).owned)
+    # wrong layout patch for solve
+    bad = P.px_patch(pa.data, P.box(0, 0, 63, 63), pa.ld)
+    with pytest.raises(P.PxError, match="PX_ERR_SHAPE"):
+        P.solve(lay, None, 0, prm, 2, 1, bad, pb, pr)
+    with pytest.raises(P.PxError, match="non-default stream"):
+        P.solve(lay, None, 0, prm, 2, 1, pa, pb, pr, use_graph=True, stream=0)
+
+
+def test_kernels_are_counted():
+    before = P.kernel_launch_count()
+    test_relax_step_bitwise(P.PX_BC_PERIODIC, 0, (64, 64))
+    assert P.kernel_launch_count() > before
