@@ -289,6 +289,19 @@ void px_release_cached(void);
 /* Diagnostics: number of kernel launches libprotox enqueued so far in this
  * process (graph replays count their kernel nodes). */
 int64_t px_kernel_launch_count(void);
+/* Diagnostics: which relax kernel a px_relax_step over `region` would run:
+ * 1 = TMA bulk-copy pipeline (16-byte aligned region start, even width,
+ * >= 4M cells), 0 = register-streaming LDG.128 kernel, <0 = invalid args.
+ * Setting PROTOX_KERNEL=ldg in the environment (read once) forces 0. */
+int32_t px_relax_variant(const px_patch* phi_in, const px_patch* phi_out, const px_patch* rhs,
+                         px_box region);
+
+/* Measurement helper (not part of the method): the streaming ceiling of the
+ * GPU for the sweep's access pattern.  variant 0: c[i] = a[i] + b[i] (2 reads,
+ * 1 write, like the fused sweep); variant 1: c[i] = a[i] (copy).  n even,
+ * pointers 16-byte aligned, device memory.  Asynchronous on stream. */
+px_status px_stream_ceiling(const double* a, const double* b, double* c, int64_t n,
+                            int32_t variant, void* stream);
 
 #ifdef __cplusplus
 }

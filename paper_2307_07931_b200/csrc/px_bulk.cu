@@ -1,0 +1,388 @@
+// px_bulk.cu -- the TMA-staged fused relax sweep (kernel K1b).
+//
+// Same arithmetic as k_stream (px_kernels.cu) -- per cell the oracle's
+// expression tree, every * and + rounded separately -- but the HBM streams
+// are moved by the Tensor Memory Accelerator: a producer warp issues
+// cp.async.bulk (TMA bulk copies, SASS UBLKCP) of whole row segments of φ and
+// of the right-hand side into a ring of shared-memory stages, each guarded by
+// an mbarrier with a transaction count; eight consumer warps read a stage,
+// keep the rows S, C, N of their column pair in registers, write φ' with
+// 16-byte stores and release the stage.  The bytes in flight per SM are set
+// by the ring depth (up to NST-1 stages of 32 KB), not by registers, so one
+// 288-thread CTA per SM saturates HBM.  Persistent grid: one CTA per SM walks
+// (strip of 512 columns) x (chunk of rows) work items.
+//
+// Halo: the W neighbour of a strip's first column and the E neighbour of its
+// last column come from the adjacent strips; the two edge threads load them
+// with plain 8-byte loads one stage ahead (into registers).  The row above
+// a chunk is re-read once per chunk (2 rows per CHUNK_ROWS).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdlib>
+
+#include "px_internal.h"
+#include "px_device.cuh"
+
+namespace px {
+
+namespace bulk {
+
+constexpr int W = 512;                   // strip width (columns)
+constexpr int PAIRS = W / 2;             // consumer threads
+constexpr int NCW = PAIRS / 32;          // consumer warps (8)
+constexpr int THREADS = PAIRS + 32;      // + producer warp
+constexpr int R = 4;                     // rows per stage
+constexpr int STAGE_DOUBLES = R * 2 * W; // φ rows + rhs rows (32 KB)
+constexpr int NST_DEFAULT = 7;           // stages in the ring (224 KB)
+constexpr int CHUNK_ROWS = 256;          // nominal rows per work item
+template <int NST>
+constexpr size_t smem_bytes() {
+  return (size_t)NST * STAGE_DOUBLES * sizeof(double) + 2 * NST * sizeof(uint64_t);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* b, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(tx)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+// TMA bulk copy global -> shared, completion counted on an mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+struct Item {
+  int c;       // first column of the strip (relative to region.lo)
+  int w;       // strip width (even)
+  int y0, y1;  // rows computed: [y0, y1)
+};
+
+__device__ __forceinline__ Item item_of(const StreamLaunch& a, int it, int nstrips, int crows) {
+  Item t;
+  const int s = it % nstrips, k = it / nstrips;
+  t.c = s * W;
+  t.w = min(W, a.nx - t.c);
+  t.y0 = k * crows;
+  t.y1 = min(a.ny, t.y0 + crows);
+  return t;
+}
+// φ rows streamed for an item: y0-1 .. y1 (inclusive) -> y1-y0+2 rows
+__device__ __forceinline__ int item_stages(const Item& t) { return (t.y1 - t.y0 + 2 + R - 1) / R; }
+
+}  // namespace bulk
+
+using namespace bulk;
+
+
+template <int MODE, int ST, int NST>
+__global__ void __launch_bounds__(THREADS, 1) k_bulk(const StreamLaunch a, int nstrips, int nitems,
+                                                     int crows) {
+  extern __shared__ __align__(128) double smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NST * STAGE_DOUBLES);
+  uint64_t* empty = full + NST;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  unsigned long long mx = 0ull;
+  double ss = 0.0;
+
+  if (warp == NCW) {
+    // ================= producer (one elected lane) =================
+    if (lane == 0) {
+      const uint64_t pol = evict_first_policy();
+      int slot = 0;
+      uint32_t phase = 0;
+      for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+        const Item t = item_of(a, it, nstrips, crows);
+        const int nst = item_stages(t);
+        const uint32_t rowbytes = (uint32_t)t.w * 8u;
+        for (int st = 0; st < nst; ++st) {
+          mbar_wait(&empty[slot], phase ^ 1u);
+          double* sp = smem + (size_t)slot * STAGE_DOUBLES;
+          uint32_t bytes = 0;
+          int nphi = 0, nrhs = 0;
+          for (int i = 0; i < R; ++i) {
+            const int yf = t.y0 - 1 + st * R + i;  // φ row of entry i
+            if (yf <= t.y1) ++nphi;
+            const int yr = yf - 1;                 // rhs row of entry i
+            if (yr >= t.y0 && yr < t.y1) ++nrhs;
+          }
+          bytes = rowbytes * (uint32_t)(nphi + ((MODE == MODE_RELAX || MODE == MODE_RESID) ? nrhs : 0));
+          mbar_arrive_expect_tx(&full[slot], bytes);
+          for (int i = 0; i < R; ++i) {
+            const int yf = t.y0 - 1 + st * R + i;
+            if (yf <= t.y1)
+              bulk_g2s(sp + i * W, a.src + (int64_t)yf * a.ld_src + t.c, rowbytes, &full[slot], pol);
+            const int yr = yf - 1;
+            if ((MODE == MODE_RELAX || MODE == MODE_RESID) && yr >= t.y0 && yr < t.y1)
+              bulk_g2s(sp + (R + i) * W, a.rhs + (int64_t)yr * a.ld_rhs + t.c, rowbytes, &full[slot], pol);
+          }
+          if (++slot == NST) {
+            slot = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+  } else {
+    // ================= consumers =================
+    const int j = tid;                     // pair index within the strip
+    const int c0 = 2 * j;                  // strip-relative first column of the pair
+    int slot = 0;
+    uint32_t phase = 0;
+    // W / E halo of the strip for the rows of the NEXT stage (loaded one
+    // stage ahead by the two edge threads; 0 elsewhere)
+    double hw_next[R], he_next[R];
+    auto load_halo = [&](const Item& t, int st) {
+      const bool L = (j == 0), Rt = (c0 + 2 == t.w);
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const int yf = t.y0 - 1 + st * R + i;
+        hw_next[i] = 0.0;
+        he_next[i] = 0.0;
+        if (yf <= t.y1) {
+          const double* row = a.src + (int64_t)yf * a.ld_src;
+          if (L && t.c - 1 >= a.src_x0) hw_next[i] = row[t.c - 1];
+          if (Rt && t.c + t.w <= a.src_x1) he_next[i] = row[t.c + t.w];
+        }
+      }
+    };
+    int it = blockIdx.x;
+    Item t;
+    if (it < nitems) {
+      t = item_of(a, it, nstrips, crows);
+      load_halo(t, 0);
+    }
+    for (; it < nitems; it += gridDim.x) {
+      const int nst = item_stages(t);
+      const bool live = c0 < t.w;
+      const bool left = (j == 0);
+      const bool edge_r = (c0 + 2 == t.w);        // this pair ends the strip
+      double w_s = 0, a_s = 0, b_s = 0, e_s = 0;  // row S
+      double w_c = 0, a_c = 0, b_c = 0, e_c = 0;  // row C
+      for (int st = 0; st < nst; ++st) {
+        double hw[R], he[R];
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          hw[i] = hw_next[i];
+          he[i] = he_next[i];
+        }
+        // prefetch the halos of the next stage (this item's or the next item's)
+        if (st + 1 < nst) {
+          load_halo(t, st + 1);
+        } else if (it + (int)gridDim.x < nitems) {
+          load_halo(item_of(a, it + gridDim.x, nstrips, crows), 0);
+        }
+        mbar_wait(&full[slot], phase);
+        const double* sp = smem + (size_t)slot * STAGE_DOUBLES;
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          const int yf = t.y0 - 1 + st * R + i;
+          if (yf > t.y1) break;
+          // row N = φ row yf, from shared memory
+          double w_n = 0, a_n = 0, b_n = 0, e_n = 0;
+          if (live) {
+            const double2 pr = *reinterpret_cast<const double2*>(sp + i * W + c0);
+            a_n = pr.x;
+            b_n = pr.y;
+            w_n = left ? hw[i] : sp[i * W + c0 - 1];
+            e_n = edge_r ? he[i] : sp[i * W + c0 + 2];
+          }
+          const int r = yf - 1;  // the row computed now
+          if (r >= t.y0 && live) {
+            double L0, L1;
+            if (ST == 0) {
+              L0 = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(w_c, b_c), a_s), a_n), __dmul_rn(-4.0, a_c));
+              L1 = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(a_c, e_c), b_s), b_n), __dmul_rn(-4.0, b_c));
+            } else {
+              double q;
+              q = __dmul_rn(4.0, w_c);
+              q = __dadd_rn(q, __dmul_rn(4.0, b_c));
+              q = __dadd_rn(q, __dmul_rn(4.0, a_s));
+              q = __dadd_rn(q, __dmul_rn(4.0, a_n));
+              q = __dadd_rn(q, w_s);
+              q = __dadd_rn(q, b_s);
+              q = __dadd_rn(q, w_n);
+              q = __dadd_rn(q, b_n);
+              L0 = __dadd_rn(q, __dmul_rn(-20.0, a_c));
+              q = __dmul_rn(4.0, a_c);
+              q = __dadd_rn(q, __dmul_rn(4.0, e_c));
+              q = __dadd_rn(q, __dmul_rn(4.0, b_s));
+              q = __dadd_rn(q, __dmul_rn(4.0, b_n));
+              q = __dadd_rn(q, a_s);
+              q = __dadd_rn(q, e_s);
+              q = __dadd_rn(q, a_n);
+              q = __dadd_rn(q, e_n);
+              L1 = __dadd_rn(q, __dmul_rn(-20.0, b_c));
+            }
+            const double2 f = *reinterpret_cast<const double2*>(sp + (R + i) * W + c0);
+            const double d0 = __dmul_rn(a.scale, L0), d1 = __dmul_rn(a.scale, L1);
+            const double e0 = __dsub_rn(d0, f.x), e1 = __dsub_rn(d1, f.y);
+            mx = umax64(mx, (unsigned long long)__double_as_longlong(fabs(e0)));
+            mx = umax64(mx, (unsigned long long)__double_as_longlong(fabs(e1)));
+            ss = fma(e0, e0, ss);
+            ss = fma(e1, e1, ss);
+            if (MODE == MODE_RELAX) {
+              const double o0 = __dadd_rn(a_c, __dmul_rn(a.lambda, e0));
+              const double o1 = __dadd_rn(b_c, __dmul_rn(a.lambda, e1));
+              const int x = t.c + c0;
+              double* dp = a.dst + (int64_t)r * a.ld_dst + x;
+              *reinterpret_cast<double2*>(dp) = make_double2(o0, o1);
+              if (a.gs.g > 0) {
+                images(a, x, r, o0);
+                images(a, x + 1, r, o1);
+              }
+            }
+          }
+          w_s = w_c; a_s = a_c; b_s = b_c; e_s = e_c;
+          w_c = w_n; a_c = a_n; b_c = b_n; e_c = e_n;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        if (++slot == NST) {
+          slot = 0;
+          phase ^= 1u;
+        }
+      }
+      if (it + (int)gridDim.x < nitems) t = item_of(a, it + gridDim.x, nstrips, crows);
+    }
+  }
+  if (a.norms.out_max) reduce_norms(a.norms, mx, ss);
+}
+
+static int g_nsm = 0;
+static int num_sms() {
+  if (!g_nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (g_nsm <= 0) g_nsm = 148;
+  }
+  return g_nsm;
+}
+
+static int bulk_nst() {
+  static int nst = 0;
+  if (!nst) {
+    const char* e = getenv("PROTOX_BULK_NST");  // A/B knob: 5 or 7 stages
+    nst = (e && atoi(e) == 5) ? 5 : NST_DEFAULT;
+  }
+  return nst;
+}
+
+bool bulk_eligible(int mode, const StreamLaunch& a) {
+  static int disabled = -1;
+  if (disabled < 0) {
+    const char* e = getenv("PROTOX_KERNEL");
+    disabled = (e && e[0] == 'l') ? 1 : 0;  // PROTOX_KERNEL=ldg forces the LDG kernel (A/B)
+  }
+  if (disabled) return false;
+  if (mode != MODE_RELAX && mode != MODE_RESID) return false;
+  if (a.phase != 0 || (a.nx & 1) || a.nx <= 0 || a.ny <= 0) return false;
+  // small (L2-resident, launch-bound) problems cannot fill a persistent grid
+  if ((int64_t)a.nx * a.ny < (int64_t)4 * 1024 * 1024) return false;
+  if ((a.ld_src & 1) || (mode == MODE_RELAX && (a.ld_dst & 1)) || (a.ld_rhs & 1)) return false;
+  // bulk copies need 16-byte aligned row starts
+  if (((uintptr_t)a.src & 15) || ((uintptr_t)a.rhs & 15)) return false;
+  return true;
+}
+
+// Work decomposition: strips of W columns x chunks of rows.  The chunk
+// count is chosen (from the nominal CHUNK_ROWS up to twice as many chunks)
+// so that the item count divides evenly over the persistent grid.
+struct BulkGeom {
+  int nstrips, nchunks, crows, nitems, grid;
+};
+static BulkGeom bulk_geom(const StreamLaunch& a) {
+  BulkGeom g;
+  g.nstrips = (a.nx + W - 1) / W;
+  int gmax = num_sms() < BULK_MAX_GRID ? num_sms() : BULK_MAX_GRID;
+  const int c0 = (a.ny + CHUNK_ROWS - 1) / CHUNK_ROWS;
+  double best = 1e30;
+  g.nchunks = c0;
+  for (int c = c0; c <= 2 * c0 && c <= a.ny; ++c) {
+    const int rows = (a.ny + c - 1) / c;
+    const int cc = (a.ny + rows - 1) / rows;       // chunks actually produced
+    const int items = g.nstrips * cc;
+    const int waves = (items + gmax - 1) / gmax;
+    // time ~ waves * (rows + 2): balance and per-chunk halo overhead
+    const double cost = (double)waves * (rows + 2);
+    if (cost < best - 1e-9) {
+      best = cost;
+      g.nchunks = cc;
+    }
+  }
+  g.crows = (a.ny + g.nchunks - 1) / g.nchunks;
+  g.nchunks = (a.ny + g.crows - 1) / g.crows;
+  g.nitems = g.nstrips * g.nchunks;
+  g.grid = g.nitems < gmax ? g.nitems : gmax;
+  return g;
+}
+
+int32_t bulk_blocks(const StreamLaunch& a) { return bulk_geom(a).grid; }
+
+template <int MODE, int ST, int NST>
+static cudaError_t launch_b(const StreamLaunch& a, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_bulk<MODE, ST, NST>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<NST>());
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const BulkGeom g = bulk_geom(a);
+  k_bulk<MODE, ST, NST><<<g.grid, THREADS, smem_bytes<NST>(), s>>>(a, g.nstrips, g.nitems, g.crows);
+  return cudaPeekAtLastError();
+}
+
+px_status launch_bulk(int mode, int stencil, const StreamLaunch& a, cudaStream_t s) {
+  cudaError_t e;
+  const bool deep = bulk_nst() == 7;
+  switch (mode * 2 + stencil) {
+    case MODE_RELAX * 2 + 0: e = deep ? launch_b<MODE_RELAX, 0, 7>(a, s) : launch_b<MODE_RELAX, 0, 5>(a, s); break;
+    case MODE_RELAX * 2 + 1: e = deep ? launch_b<MODE_RELAX, 1, 7>(a, s) : launch_b<MODE_RELAX, 1, 5>(a, s); break;
+    case MODE_RESID * 2 + 0: e = deep ? launch_b<MODE_RESID, 0, 7>(a, s) : launch_b<MODE_RESID, 0, 5>(a, s); break;
+    case MODE_RESID * 2 + 1: e = deep ? launch_b<MODE_RESID, 1, 7>(a, s) : launch_b<MODE_RESID, 1, 5>(a, s); break;
+    default: return fail(PX_ERR_ARG, "bulk kernel: bad mode");
+  }
+  count_launches(1);
+  return cuda_check(e, "bulk relax kernel launch");
+}
+
+}  // namespace px

@@ -297,14 +297,14 @@ double stencil_scale(int stencil, double h) {
   return stencil == PX_MEHRSTELLEN_9PT ? 1.0 / (6.0 * h * h) : 1.0 / (h * h);
 }
 
-static px_status attach_norms(StreamLaunch* a, double* d_norms) {
+static px_status attach_norms(int mode, StreamLaunch* a, double* d_norms) {
   if (!d_norms) return PX_OK;
   a->norms.out_max = d_norms;
   a->norms.out_sum = d_norms + 1;
   a->norms.counter = reinterpret_cast<unsigned int*>(d_norms + 2);
   a->norms.partials = d_norms + 4;
   a->norms.offset = 0;
-  a->norms.expected = stream_blocks(a->nx, a->ny, a->phase);
+  a->norms.expected = launch_blocks(mode, *a);
   return PX_OK;
 }
 
@@ -334,8 +334,18 @@ px_status px_relax_step(const px_relax_params* p, const px_patch* phi_in, px_pat
                         "memset norms");
     return PX_OK;
   }
-  attach_norms(&a, d_norms);
+  attach_norms(MODE_RELAX, &a, d_norms);
   return launch_stream(MODE_RELAX, p->stencil, a, (cudaStream_t)stream);
+}
+
+int32_t px_relax_variant(const px_patch* phi_in, const px_patch* phi_out, const px_patch* rhs,
+                         px_box region) {
+  StreamLaunch a;
+  px_patch out = phi_out ? *phi_out : px_patch{};
+  if (make_stream_launch(MODE_RELAX, PX_LAPLACE_5PT, 1.0, 0.0, phi_in, rhs, phi_out ? &out : nullptr,
+                         region, &a) != PX_OK)
+    return -1;
+  return bulk_eligible(MODE_RELAX, a) ? 1 : 0;
 }
 
 px_status px_residual_norm(const px_relax_params* p, const px_patch* phi, const px_patch* rhs,
@@ -348,7 +358,7 @@ px_status px_residual_norm(const px_relax_params* p, const px_patch* phi, const 
   if (empty(region))
     return cuda_check(cudaMemsetAsync(d_norms, 0, 2 * sizeof(double), (cudaStream_t)stream),
                       "memset norms");
-  attach_norms(&a, d_norms);
+  attach_norms(MODE_RESID, &a, d_norms);
   return launch_stream(MODE_RESID, p->stencil, a, (cudaStream_t)stream);
 }
 

@@ -105,8 +105,15 @@ struct StreamLaunch {
   NormSlot norms;     // norms.out_max == null: none
 };
 
-// number of thread blocks the stream kernel uses for a region
+// upper bound of the thread blocks a relax/residual launch over a region uses
+constexpr int32_t BULK_MAX_GRID = 512;
 int32_t stream_blocks(int32_t nx, int32_t ny, int32_t phase);
+// blocks the launch of `a` will actually use (norm slot accounting)
+int32_t launch_blocks(int mode, const StreamLaunch& a);
+// the TMA bulk-copy kernel (px_bulk.cu)
+bool bulk_eligible(int mode, const StreamLaunch& a);
+int32_t bulk_blocks(const StreamLaunch& a);
+px_status launch_bulk(int mode, int stencil, const StreamLaunch& a, cudaStream_t s);
 // launchers (px_kernels.cu); return PX_ERR_CUDA on launch failure
 px_status launch_stream(int mode, int stencil, const StreamLaunch& a, cudaStream_t s);
 px_status launch_fill_ghosts(const px_layout* l, int32_t rank, const px_patch& p, cudaStream_t s);

@@ -22,6 +22,7 @@
 #include <cstdint>
 
 #include "px_internal.h"
+#include "px_device.cuh"
 
 namespace px {
 
@@ -33,11 +34,23 @@ constexpr int SW_PF = 2;                  // prefetch distance in rows
 constexpr int SW_RING = SW_PF + 3;        // raw φ rows kept in flight
 constexpr unsigned FULL = 0xffffffffu;
 
-int32_t stream_blocks(int32_t nx, int32_t ny, int32_t phase) {
+static int32_t ldg_blocks(int32_t nx, int32_t ny, int32_t phase) {
   if (nx <= 0 || ny <= 0) return 0;
   int32_t gx = (nx + phase + SW_COLS - 1) / SW_COLS;
   int32_t gy = (ny + SW_ROWS - 1) / SW_ROWS;
   return gx * gy;
+}
+
+// upper bound of the blocks any relax/residual launch over the region uses
+// (sizes norm buffers; host-only)
+int32_t stream_blocks(int32_t nx, int32_t ny, int32_t phase) {
+  const int32_t b = ldg_blocks(nx, ny, phase);
+  return b > BULK_MAX_GRID ? b : BULK_MAX_GRID;
+}
+
+int32_t launch_blocks(int mode, const StreamLaunch& a) {
+  if (bulk_eligible(mode, a)) return bulk_blocks(a);
+  return ldg_blocks(a.nx, a.ny, a.phase);
 }
 
 // --------------------------------------------------------------- helpers
@@ -108,108 +121,6 @@ __device__ __forceinline__ void taps(const Fin& S, const Fin& C, const Fin& N, d
     t = __dadd_rn(t, N.a);
     t = __dadd_rn(t, N.e);
     L1 = __dadd_rn(t, __dmul_rn(-20.0, C.b));
-  }
-}
-
-__device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) {
-  return a > b ? a : b;
-}
-
-// Ghost images of one owned cell (fused exchange).  Rarely executed: only
-// cells within g of a face.
-__device__ __noinline__ void write_images(const StreamLaunch& a, int x, int y, double v) {
-  const GhostSpec& g = a.gs;
-  const int X = x + g.o[0], Y = y + g.o[1];
-  int ix[3], iy[3];
-  double sx[3], sy[3];
-  int nxi = 1, nyi = 1;
-  ix[0] = X;
-  iy[0] = Y;
-  sx[0] = sy[0] = 1.0;
-  for (int d = 0; d < 2; ++d) {
-    const int P = d ? Y : X, n = g.n[d];
-    int* im = d ? iy : ix;
-    double* sg = d ? sy : sx;
-    int& cnt = d ? nyi : nxi;
-    if (P < g.g && g.mode[d][0] != GH_NONE) {
-      im[cnt] = g.mode[d][0] == GH_WRAP ? P + n : -P - 1;
-      sg[cnt] = g.mode[d][0] == GH_REFLECT ? -1.0 : 1.0;
-      ++cnt;
-    }
-    if (P >= n - g.g && g.mode[d][1] != GH_NONE) {
-      im[cnt] = g.mode[d][1] == GH_WRAP ? P - n : 2 * n - 1 - P;
-      sg[cnt] = g.mode[d][1] == GH_REFLECT ? -1.0 : 1.0;
-      ++cnt;
-    }
-  }
-  for (int j = 0; j < nyi; ++j)
-    for (int i = 0; i < nxi; ++i) {
-      if (i == 0 && j == 0) continue;
-      a.dst[(int64_t)(ix[i] - g.o[0]) + (int64_t)(iy[j] - g.o[1]) * a.ld_dst] = v * sx[i] * sy[j];
-    }
-}
-
-// Fixed-order block reduction of (max-bits, sum), then the last block of the
-// slot reduces all partials.  Deterministic for a given launch geometry.
-__device__ void reduce_norms(const NormSlot& ns, unsigned long long mx, double ss) {
-  __shared__ unsigned long long s_mx[SW_THREADS / 32];
-  __shared__ double s_ss[SW_THREADS / 32];
-  __shared__ int s_last;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nthreads = blockDim.x;
-  for (int o = 16; o > 0; o >>= 1) {
-    mx = umax64(mx, __shfl_xor_sync(FULL, mx, o));
-    ss = ss + __shfl_xor_sync(FULL, ss, o);
-  }
-  if (lane == 0) {
-    s_mx[warp] = mx;
-    s_ss[warp] = ss;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long m = s_mx[0];
-    double s = s_ss[0];
-    for (int w = 1; w < nthreads / 32; ++w) {
-      m = umax64(m, s_mx[w]);
-      s = s + s_ss[w];
-    }
-    const int bid = ns.offset + blockIdx.x + blockIdx.y * gridDim.x;
-    ns.partials[2 * bid] = __longlong_as_double((long long)m);
-    ns.partials[2 * bid + 1] = s;
-    __threadfence();
-    unsigned t = atomicAdd(ns.counter, 1u);
-    s_last = (t == (unsigned)ns.expected - 1);
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  unsigned long long m = 0;
-  double s = 0.0;
-  for (int i = threadIdx.x; i < ns.expected; i += nthreads) {
-    m = umax64(m, (unsigned long long)__double_as_longlong(__ldcg(ns.partials + 2 * i)));
-    s = s + __ldcg(ns.partials + 2 * i + 1);
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    m = umax64(m, __shfl_xor_sync(FULL, m, o));
-    s = s + __shfl_xor_sync(FULL, s, o);
-  }
-  __syncthreads();
-  if (lane == 0) {
-    s_mx[warp] = m;
-    s_ss[warp] = s;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    m = s_mx[0];
-    s = s_ss[0];
-    for (int w = 1; w < nthreads / 32; ++w) {
-      m = umax64(m, s_mx[w]);
-      s = s + s_ss[w];
-    }
-    *ns.out_max = __longlong_as_double((long long)m);
-    *ns.out_sum = s;
-    *ns.counter = 0u;
-    __threadfence();
   }
 }
 
@@ -314,13 +225,8 @@ __global__ void __launch_bounds__(SW_THREADS, 2) k_stream(const StreamLaunch a) 
           if (vb) dp[c + 1] = o1;
         }
         if (MODE == MODE_RELAX && a.gs.g > 0) {
-          const int Y = r + a.gs.o[1];
-          const bool yface = (Y < a.gs.g) || (Y >= a.gs.n[1] - a.gs.g);
-          const int X0 = c + a.gs.o[0];
-          const bool xface0 = (X0 < a.gs.g) || (X0 >= a.gs.n[0] - a.gs.g);
-          const bool xface1 = (X0 + 1 < a.gs.g) || (X0 + 1 >= a.gs.n[0] - a.gs.g);
-          if (va && (yface || xface0)) write_images(a, c, r, o0);
-          if (vb && (yface || xface1)) write_images(a, c + 1, r, o1);
+          if (va) images(a, c, r, o0);
+          if (vb) images(a, c + 1, r, o1);
         }
       }
       fS = fC;
@@ -347,6 +253,7 @@ static void launch_t(const StreamLaunch& a, dim3 grid, cudaStream_t s) {
 
 px_status launch_stream(int mode, int stencil, const StreamLaunch& a, cudaStream_t s) {
   if (a.nx <= 0 || a.ny <= 0) return PX_OK;
+  if (bulk_eligible(mode, a)) return launch_bulk(mode, stencil, a, s);
   dim3 grid((a.nx + a.phase + SW_COLS - 1) / SW_COLS, (a.ny + SW_ROWS - 1) / SW_ROWS);
   if (grid.y > 65535) return fail(PX_ERR_UNSUPPORTED, "region too tall (%d rows)", a.ny);
   switch (mode * 2 + stencil) {

@@ -204,7 +204,7 @@ static px_status build_part_launches(const SolveCtx& x, int32_t part, const px_p
     PX_TRY(make_stream_launch(resid ? MODE_RESID : MODE_RELAX, x.p->stencil, scale, x.p->lambda,
                               &in, &x.rhs[part], resid ? nullptr : &outp, rg, &sl.a));
     if (!resid) sl.a.gs = ghost_spec(x.l, li, rg, x.l->nranks == 1);
-    sl.blocks = stream_blocks(sl.a.nx, sl.a.ny, sl.a.phase);
+    sl.blocks = launch_blocks(resid ? MODE_RESID : MODE_RELAX, sl.a);
     v.push_back(sl);
   }
   return PX_OK;

@@ -88,6 +88,7 @@ EXPORTS = [
     "px_comm_unique_id", "px_comm_create", "px_comm_destroy", "px_comm_allreduce_norms",
     "px_exchange_ghosts", "px_exchange_ghosts_local",
     "px_solve", "px_solve_host", "px_release_cached", "px_kernel_launch_count",
+    "px_relax_variant", "px_stream_ceiling",
 ]
 
 
@@ -163,6 +164,10 @@ def lib():
                                 P(ctypes.c_double), i32, P(i32), vp]
     L.px_release_cached.restype = None
     L.px_kernel_launch_count.restype = i64
+    L.px_stream_ceiling.restype = st
+    L.px_stream_ceiling.argtypes = [vp, vp, vp, i64, i32, vp]
+    L.px_relax_variant.restype = i32
+    L.px_relax_variant.argtypes = [P(px_patch), P(px_patch), P(px_patch), px_box]
     _lib = L
     return L
 
@@ -418,6 +423,16 @@ def solve_host(layout: Layout, p: px_relax_params, nsweeps: int, norm_every: int
 
 def release_cached():
     lib().px_release_cached()
+
+
+def relax_variant(phi_in: px_patch, phi_out: px_patch, rhs: px_patch, region: px_box) -> int:
+    """1 = TMA bulk-copy kernel, 0 = LDG streaming kernel, -1 = invalid."""
+    return lib().px_relax_variant(ctypes.byref(phi_in), ctypes.byref(phi_out), ctypes.byref(rhs), region)
+
+
+def stream_ceiling(a, b, c, variant: int = 0, stream=None):
+    """K12 measurement helper: c = a + b (variant 0) or c = a (variant 1)."""
+    _check(lib().px_stream_ceiling(_ptr(a), _ptr(b), _ptr(c), c.numel(), variant, _stream(stream)))
 
 
 def kernel_launch_count() -> int:
