@@ -213,6 +213,7 @@ def run_native(args):
         dist.broadcast_object_list(obj, src=0)
         comm = P.Comm(obj[0], world, rank, local)
     stream = torch.cuda.Stream(device=dev)
+    stream.wait_stream(torch.cuda.current_stream(dev))  # the zero-fills ran on the current stream
     prm = P.relax_params(h, lam, cfg["stencil"])
     with torch.cuda.stream(stream):
         kind = P.PX_FIELD_HASH if cfg["rho"] == "hash" else P.PX_FIELD_SINE
@@ -221,6 +222,7 @@ def run_native(args):
         if cfg["stencil"] == 1:
             P.exchange_ghosts(lay, comm, rank, lay.patch(rank, rho), stream=stream)
             rhs = lay.alloc(rank, dev)
+            stream.wait_stream(torch.cuda.current_stream(dev))
             P.mehrstellen_rhs(lay.patch(rank, rho), lay.patch(rank, rhs), li.owned, stream=stream)
     stream.synchronize()
     pa, pb, pr = lay.patch(rank, phi), lay.patch(rank, scr), lay.patch(rank, rhs)
@@ -260,6 +262,7 @@ def run_native(args):
     # k_stream<RELAX> launch geometry over this rank's slab), timed live with
     # CUDA events on the launching stream.
     nb = P.norm_buffer(li.owned, dev)
+    stream.wait_stream(torch.cuda.current_stream(dev))
     reps = 20
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
     P.exchange_ghosts(lay, comm, rank, pa, stream=stream)
@@ -294,6 +297,7 @@ def run_native(args):
                              use_graph=True, stream=stream)
         else:
             d_phi, d_scr, d_rhs = lay.alloc(rank, dev), lay.alloc(rank, dev), lay.alloc(rank, dev)
+            stream.wait_stream(torch.cuda.current_stream(dev))
             qa, qb, qr = lay.patch(rank, d_phi), lay.patch(rank, d_scr), lay.patch(rank, d_rhs)
 
             def e2e_step():

@@ -103,9 +103,11 @@ __device__ __forceinline__ int item_stages(const Item& t) { return (t.y1 - t.y0 
 using namespace bulk;
 
 
-template <int MODE, int ST, int NST>
-__global__ void __launch_bounds__(THREADS, 1) k_bulk(const StreamLaunch a, int nstrips, int nitems,
-                                                     int crows) {
+// NST stages per CTA; NST <= 3 runs two CTAs per SM.  STP: 1 = streaming
+// (evict-first) stores of φ'.
+template <int MODE, int ST, int NST, int STP>
+__global__ void __launch_bounds__(THREADS, (NST <= 3 ? 2 : 1)) k_bulk(const StreamLaunch a, int nstrips,
+                                                                     int nitems, int crows) {
   extern __shared__ __align__(128) double smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NST * STAGE_DOUBLES);
   uint64_t* empty = full + NST;
@@ -263,7 +265,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_bulk(const StreamLaunch a, int n
               const double o1 = __dadd_rn(b_c, __dmul_rn(a.lambda, e1));
               const int x = t.c + c0;
               double* dp = a.dst + (int64_t)r * a.ld_dst + x;
-              *reinterpret_cast<double2*>(dp) = make_double2(o0, o1);
+              if (STP)
+                __stcs(reinterpret_cast<double2*>(dp), make_double2(o0, o1));
+              else
+                *reinterpret_cast<double2*>(dp) = make_double2(o0, o1);
               if (a.gs.g > 0) {
                 images(a, x, r, o0);
                 images(a, x + 1, r, o1);
@@ -297,13 +302,28 @@ static int num_sms() {
   return g_nsm;
 }
 
-static int bulk_nst() {
-  static int nst = 0;
-  if (!nst) {
-    const char* e = getenv("PROTOX_BULK_NST");  // A/B knob: 5 or 7 stages
-    nst = (e && atoi(e) == 5) ? 5 : NST_DEFAULT;
+// Tuning knobs (read once; defaults are the measured best):
+// PROTOX_BULK_NST = 3 (two CTAs per SM) | 5 | 7 stages, PROTOX_BULK_CHUNK =
+// nominal rows per work item, PROTOX_BULK_STORE = 1 for streaming stores.
+struct BulkCfg {
+  int nst = 5, chunk = CHUNK_ROWS, stp = 0;
+};
+static const BulkCfg& bulk_cfg() {
+  static BulkCfg c;
+  static bool init = false;
+  if (!init) {
+    if (const char* e = getenv("PROTOX_BULK_NST")) {
+      const int v = atoi(e);
+      c.nst = (v == 3 || v == 5 || v == 7) ? v : c.nst;
+    }
+    if (const char* e = getenv("PROTOX_BULK_CHUNK")) {
+      const int v = atoi(e);
+      if (v >= 8 && v <= 65536) c.chunk = v;
+    }
+    if (const char* e = getenv("PROTOX_BULK_STORE")) c.stp = atoi(e) ? 1 : 0;
+    init = true;
   }
-  return nst;
+  return c;
 }
 
 bool bulk_eligible(int mode, const StreamLaunch& a) {
@@ -332,8 +352,10 @@ struct BulkGeom {
 static BulkGeom bulk_geom(const StreamLaunch& a) {
   BulkGeom g;
   g.nstrips = (a.nx + W - 1) / W;
-  int gmax = num_sms() < BULK_MAX_GRID ? num_sms() : BULK_MAX_GRID;
-  const int c0 = (a.ny + CHUNK_ROWS - 1) / CHUNK_ROWS;
+  const BulkCfg& cfg = bulk_cfg();
+  const int per_sm = cfg.nst <= 3 ? 2 : 1;
+  int gmax = num_sms() * per_sm < BULK_MAX_GRID ? num_sms() * per_sm : BULK_MAX_GRID;
+  const int c0 = (a.ny + cfg.chunk - 1) / cfg.chunk;
   double best = 1e30;
   g.nchunks = c0;
   for (int c = c0; c <= 2 * c0 && c <= a.ny; ++c) {
@@ -357,28 +379,40 @@ static BulkGeom bulk_geom(const StreamLaunch& a) {
 
 int32_t bulk_blocks(const StreamLaunch& a) { return bulk_geom(a).grid; }
 
-template <int MODE, int ST, int NST>
+template <int MODE, int ST, int NST, int STP>
 static cudaError_t launch_b(const StreamLaunch& a, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_bulk<MODE, ST, NST>,
+    cudaError_t e = cudaFuncSetAttribute(k_bulk<MODE, ST, NST, STP>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<NST>());
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const BulkGeom g = bulk_geom(a);
-  k_bulk<MODE, ST, NST><<<g.grid, THREADS, smem_bytes<NST>(), s>>>(a, g.nstrips, g.nitems, g.crows);
+  k_bulk<MODE, ST, NST, STP><<<g.grid, THREADS, smem_bytes<NST>(), s>>>(a, g.nstrips, g.nitems, g.crows);
   return cudaPeekAtLastError();
+}
+
+template <int MODE, int ST>
+static cudaError_t launch_cfg(const StreamLaunch& a, cudaStream_t s) {
+  const BulkCfg& c = bulk_cfg();
+  if (c.stp) {
+    if (c.nst == 3) return launch_b<MODE, ST, 3, 1>(a, s);
+    if (c.nst == 7) return launch_b<MODE, ST, 7, 1>(a, s);
+    return launch_b<MODE, ST, 5, 1>(a, s);
+  }
+  if (c.nst == 3) return launch_b<MODE, ST, 3, 0>(a, s);
+  if (c.nst == 7) return launch_b<MODE, ST, 7, 0>(a, s);
+  return launch_b<MODE, ST, 5, 0>(a, s);
 }
 
 px_status launch_bulk(int mode, int stencil, const StreamLaunch& a, cudaStream_t s) {
   cudaError_t e;
-  const bool deep = bulk_nst() == 7;
   switch (mode * 2 + stencil) {
-    case MODE_RELAX * 2 + 0: e = deep ? launch_b<MODE_RELAX, 0, 7>(a, s) : launch_b<MODE_RELAX, 0, 5>(a, s); break;
-    case MODE_RELAX * 2 + 1: e = deep ? launch_b<MODE_RELAX, 1, 7>(a, s) : launch_b<MODE_RELAX, 1, 5>(a, s); break;
-    case MODE_RESID * 2 + 0: e = deep ? launch_b<MODE_RESID, 0, 7>(a, s) : launch_b<MODE_RESID, 0, 5>(a, s); break;
-    case MODE_RESID * 2 + 1: e = deep ? launch_b<MODE_RESID, 1, 7>(a, s) : launch_b<MODE_RESID, 1, 5>(a, s); break;
+    case MODE_RELAX * 2 + 0: e = launch_cfg<MODE_RELAX, 0>(a, s); break;
+    case MODE_RELAX * 2 + 1: e = launch_cfg<MODE_RELAX, 1>(a, s); break;
+    case MODE_RESID * 2 + 0: e = launch_cfg<MODE_RESID, 0>(a, s); break;
+    case MODE_RESID * 2 + 1: e = launch_cfg<MODE_RESID, 1>(a, s); break;
     default: return fail(PX_ERR_ARG, "bulk kernel: bad mode");
   }
   count_launches(1);

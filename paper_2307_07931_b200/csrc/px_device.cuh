@@ -14,37 +14,38 @@ static __device__ __forceinline__ unsigned long long umax64(unsigned long long a
   return a > b ? a : b;
 }
 
-// Ghost images of one owned cell (fused exchange).  Rarely executed: only
-// cells within g of a face.
-static __device__ __noinline__ void write_images(const StreamLaunch& a, int x, int y, double v) {
-  const GhostSpec& g = a.gs;
-  const int X = x + g.o[0], Y = y + g.o[1];
+// Ghost images of one owned cell (fused exchange), general case (cells in
+// the g rows next to a y face, corners).  Rare: called for 2g rows per sweep.
+// Scalar arguments only, so the kernel parameters never need a local copy.
+static __device__ __noinline__ void write_images(double* dst, int64_t ld, int X, int Y, int ox,
+                                                 int oy, int n0, int n1, int g, int mx0, int mx1,
+                                                 int my0, int my1, double v) {
   int ix[3], iy[3];
   double sx[3], sy[3];
   int nxi = 1, nyi = 1;
   ix[0] = X;
   iy[0] = Y;
   sx[0] = sy[0] = 1.0;
-  for (int d = 0; d < 2; ++d) {
-    const int P = d ? Y : X, n = g.n[d];
-    int* im = d ? iy : ix;
-    double* sg = d ? sy : sx;
-    int& cnt = d ? nyi : nxi;
-    if (P < g.g && g.mode[d][0] != GH_NONE) {
-      im[cnt] = g.mode[d][0] == GH_WRAP ? P + n : -P - 1;
-      sg[cnt] = g.mode[d][0] == GH_REFLECT ? -1.0 : 1.0;
-      ++cnt;
-    }
-    if (P >= n - g.g && g.mode[d][1] != GH_NONE) {
-      im[cnt] = g.mode[d][1] == GH_WRAP ? P - n : 2 * n - 1 - P;
-      sg[cnt] = g.mode[d][1] == GH_REFLECT ? -1.0 : 1.0;
-      ++cnt;
-    }
+  if (X < g && mx0 != GH_NONE) {
+    ix[nxi] = mx0 == GH_WRAP ? X + n0 : -X - 1;
+    sx[nxi++] = mx0 == GH_REFLECT ? -1.0 : 1.0;
+  }
+  if (X >= n0 - g && mx1 != GH_NONE) {
+    ix[nxi] = mx1 == GH_WRAP ? X - n0 : 2 * n0 - 1 - X;
+    sx[nxi++] = mx1 == GH_REFLECT ? -1.0 : 1.0;
+  }
+  if (Y < g && my0 != GH_NONE) {
+    iy[nyi] = my0 == GH_WRAP ? Y + n1 : -Y - 1;
+    sy[nyi++] = my0 == GH_REFLECT ? -1.0 : 1.0;
+  }
+  if (Y >= n1 - g && my1 != GH_NONE) {
+    iy[nyi] = my1 == GH_WRAP ? Y - n1 : 2 * n1 - 1 - Y;
+    sy[nyi++] = my1 == GH_REFLECT ? -1.0 : 1.0;
   }
   for (int j = 0; j < nyi; ++j)
     for (int i = 0; i < nxi; ++i) {
       if (i == 0 && j == 0) continue;
-      a.dst[(int64_t)(ix[i] - g.o[0]) + (int64_t)(iy[j] - g.o[1]) * a.ld_dst] = v * sx[i] * sy[j];
+      dst[(int64_t)(ix[i] - ox) + (int64_t)(iy[j] - oy) * ld] = v * sx[i] * sy[j];
     }
 }
 
@@ -65,7 +66,8 @@ static __device__ __forceinline__ void images(const StreamLaunch& a, int x, int 
     a.dst[(int64_t)(ix - g.o[0]) + (int64_t)y * a.ld_dst] = (m == GH_REFLECT) ? -v : v;
     return;
   }
-  write_images(a, x, y, v);
+  write_images(a.dst, a.ld_dst, X, Y, g.o[0], g.o[1], g.n[0], g.n[1], g.g, g.mode[0][0],
+               g.mode[0][1], g.mode[1][0], g.mode[1][1], v);
 }
 
 // Fixed-order block reduction of (max-bits, sum), then the last block of the

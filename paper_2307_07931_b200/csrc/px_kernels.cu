@@ -30,8 +30,7 @@ constexpr int SW_WARPS = 8;
 constexpr int SW_THREADS = SW_WARPS * 32;
 constexpr int SW_COLS = SW_WARPS * 64;
 constexpr int SW_ROWS = 32;
-constexpr int SW_PF = 2;                  // prefetch distance in rows
-constexpr int SW_RING = SW_PF + 3;        // raw φ rows kept in flight
+constexpr int SW_PF = 4;                  // prefetch distance in rows (= ring slots)
 constexpr unsigned FULL = 0xffffffffu;
 
 static int32_t ldg_blocks(int32_t nx, int32_t ny, int32_t phase) {
@@ -139,62 +138,58 @@ __global__ void __launch_bounds__(SW_THREADS, 2) k_stream(const StreamLaunch a) 
   double ss = 0.0;
 
   if (warp_live) {
-    Raw raw[SW_RING];
-    double2 rr[SW_PF + 1];
-    // prologue: φ rows r0-1 .. r0+SW_PF, rhs rows r0 .. r0+SW_PF-1
+    // Ring of SW_PF raw φ rows and SW_PF rhs rows in flight.  φ row
+    // r0-1+q lives in slot q % SW_PF; a slot is refilled right after the
+    // row in it has been consumed (finish-then-load), so SW_PF loads of each
+    // array are always outstanding.  The row loop is unrolled by SW_PF only
+    // (slot indices stay compile-time; code stays small for the I-cache).
+    Raw raw[SW_PF];
+    double2 rr[SW_PF];
+    auto load_rhs = [&](int r) {
+      const double* q = a.rhs + (int64_t)r * a.ld_rhs;
+      if (c >= 0 && c + 1 < a.nx) return __ldcs(reinterpret_cast<const double2*>(q + c));
+      return make_double2((c >= 0 && c < a.nx) ? __ldcs(q + c) : 0.0,
+                          (c + 1 >= 0 && c + 1 < a.nx) ? __ldcs(q + c + 1) : 0.0);
+    };
+    raw[0] = load_raw(a.src + (int64_t)(r0 - 1) * a.ld_src, c, lane, a.src_x0, a.src_x1);
+    raw[1] = load_raw(a.src + (int64_t)r0 * a.ld_src, c, lane, a.src_x0, a.src_x1);
+    Fin fS = finish(raw[0], lane);
+    Fin fC = finish(raw[1], lane);
 #pragma unroll
-    for (int k = 0; k < SW_PF + 2; ++k) {
-      const int r = r0 - 1 + k;
-      if (r <= rlast) raw[k] = load_raw(a.src + (int64_t)r * a.ld_src, c, lane, a.src_x0, a.src_x1);
+    for (int q = 2; q < SW_PF + 2; ++q) {
+      const int r = r0 - 1 + q;
+      if (r <= rlast) raw[q % SW_PF] = load_raw(a.src + (int64_t)r * a.ld_src, c, lane, a.src_x0, a.src_x1);
     }
     if (need_rhs) {
 #pragma unroll
-      for (int k = 0; k < SW_PF; ++k) {
-        const int r = r0 + k;
-        if (r < rend) {
-          const double* rp = a.rhs + (int64_t)r * a.ld_rhs;
-          if (c >= 0 && c + 1 < a.nx)
-            rr[k] = __ldcs(reinterpret_cast<const double2*>(rp + c));
-          else
-            rr[k] = make_double2((c >= 0 && c < a.nx) ? __ldcs(rp + c) : 0.0,
-                                 (c + 1 >= 0 && c + 1 < a.nx) ? __ldcs(rp + c + 1) : 0.0);
-        }
-      }
+      for (int k = 0; k < SW_PF; ++k)
+        if (r0 + k < rend) rr[k] = load_rhs(r0 + k);
     }
-    Fin fS = finish(raw[0], lane);
-    Fin fC = finish(raw[1], lane);
 
+#pragma unroll 1
+    for (int i0 = 0; i0 < SW_ROWS; i0 += SW_PF) {
 #pragma unroll
-    for (int i = 0; i < SW_ROWS; ++i) {
+    for (int jj = 0; jj < SW_PF; ++jj) {
+      const int i = i0 + jj;
       const int r = r0 + i;
       if (r >= rend) break;
-      // issue the loads SW_PF rows ahead
+      // row N = φ row r+1 (slot (i+2) % SW_PF), then refill that slot
+      const Fin fN = finish(raw[(jj + 2) % SW_PF], lane);
       {
         const int rp = r + 1 + SW_PF;
         if (rp <= rlast)
-          raw[(i + SW_PF + 2) % SW_RING] =
-              load_raw(a.src + (int64_t)rp * a.ld_src, c, lane, a.src_x0, a.src_x1);
-        if (need_rhs) {
-          const int rq = r + SW_PF;
-          if (rq < rend) {
-            const double* q = a.rhs + (int64_t)rq * a.ld_rhs;
-            double2 v;
-            if (c >= 0 && c + 1 < a.nx)
-              v = __ldcs(reinterpret_cast<const double2*>(q + c));
-            else
-              v = make_double2((c >= 0 && c < a.nx) ? __ldcs(q + c) : 0.0,
-                               (c + 1 >= 0 && c + 1 < a.nx) ? __ldcs(q + c + 1) : 0.0);
-            rr[(i + SW_PF) % (SW_PF + 1)] = v;
-          }
-        }
+          raw[(jj + 2) % SW_PF] = load_raw(a.src + (int64_t)rp * a.ld_src, c, lane, a.src_x0, a.src_x1);
       }
-      const Fin fN = finish(raw[(i + 2) % SW_RING], lane);
+      double2 f = make_double2(0.0, 0.0);
+      if (need_rhs) {
+        f = rr[jj];
+        if (r + SW_PF < rend) rr[jj] = load_rhs(r + SW_PF);
+      }
       double L0, L1;
       taps<ST>(fS, fC, fN, L0, L1);
       const bool va = (c >= 0 && c < a.nx), vb = (c + 1 >= 0 && c + 1 < a.nx);
       double o0 = 0.0, o1 = 0.0;
       if (MODE == MODE_RELAX || MODE == MODE_RESID) {
-        const double2 f = rr[i % (SW_PF + 1)];
         const double d0 = __dmul_rn(a.scale, L0), d1 = __dmul_rn(a.scale, L1);
         const double e0 = __dsub_rn(d0, f.x), e1 = __dsub_rn(d1, f.y);
         if (va) {
@@ -231,6 +226,7 @@ __global__ void __launch_bounds__(SW_THREADS, 2) k_stream(const StreamLaunch a) 
       }
       fS = fC;
       fC = fN;
+    }
     }
   }
   if (MODE == MODE_RELAX || MODE == MODE_RESID) {

@@ -27,10 +27,12 @@ lay = P.Layout(P.box(0, 0, n - 1, n - 1), (min(256, n), min(256, n)), 1, P.PX_BC
 li = lay.local(0)
 a, b, r = lay.alloc(0), lay.alloc(0), lay.alloc(0)
 s = torch.cuda.Stream()
+s.wait_stream(torch.cuda.current_stream())
 P.init_field(lay, 0, lay.patch(0, r), P.PX_FIELD_HASH, inputs.DEFAULT_SEED, stream=s)
 P.init_field(lay, 0, lay.patch(0, a), P.PX_FIELD_HASH, 7, stream=s)
 P.fill_ghosts(lay, 0, lay.patch(0, a), stream=s)
 nb = P.norm_buffer(li.owned)
+s.wait_stream(torch.cuda.current_stream())
 prm = P.relax_params(1.0 / n, (1.0 / n) ** 2 / 8, args.stencil)
 pa, pb, pr = lay.patch(0, a), lay.patch(0, b), lay.patch(0, r)
 evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.reps)]

@@ -45,6 +45,7 @@ def test_config3_fullsize_sampled_bitwise():
     lay = P.Layout(P.box(0, 0, n - 1, n - 1), (256, 256), 1, P.PX_BC_PERIODIC, 1)
     phi, scr, rho = lay.alloc(0), lay.alloc(0), lay.alloc(0)
     s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())  # zero-fills ran on the current stream
     P.init_field(lay, 0, lay.patch(0, rho), P.PX_FIELD_HASH, inputs.DEFAULT_SEED, stream=s)
     s.synchronize()
     pa, pb, pr = lay.patch(0, phi), lay.patch(0, scr), lay.patch(0, rho)
@@ -74,6 +75,7 @@ def test_config3_fullsize_sine_closed_form_norms():
     lay = P.Layout(P.box(0, 0, n - 1, n - 1), (256, 256), 1, P.PX_BC_PERIODIC, 1)
     phi, scr, rho = lay.alloc(0), lay.alloc(0), lay.alloc(0)
     s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())  # zero-fills ran on the current stream
     P.init_field(lay, 0, lay.patch(0, rho), P.PX_FIELD_SINE, 0, 2, 2, stream=s)
     res = P.solve(lay, None, 0, P.relax_params(h, lam), N, 1, lay.patch(0, phi), lay.patch(0, scr),
                   lay.patch(0, rho), use_graph=True, stream=s)
@@ -95,6 +97,7 @@ def test_config5_fullsize_mehrstellen_sampled_bitwise():
     rho_h = inputs.sine_field(n, n)
     lay.view(0, rho).copy_(torch.from_numpy(rho_h))
     s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())  # zero-fills ran on the current stream
     P.fill_ghosts(lay, 0, lay.patch(0, rho), stream=s)
     P.mehrstellen_rhs(lay.patch(0, rho), lay.patch(0, f), lay.local(0).owned, stream=s)
     res = P.solve(lay, None, 0, P.relax_params(h, lam, P.PX_MEHRSTELLEN_9PT), N, 1, lay.patch(0, phi),

@@ -64,6 +64,7 @@ def run_gpu_solve(n0, n1, h, lam, bc, st, N, E, phi0_g, rho_g, g=1, box=None, nr
             fs.append(f)
         rhss = fs
     stream = torch.cuda.Stream()
+    stream.wait_stream(torch.cuda.current_stream())  # allocations/copies ran on the current stream
     res = P.solve(lay, None, 0, P.relax_params(h, lam, st), N, E,
                   [lay.patch(r, t) for r, t in enumerate(phis)],
                   [lay.patch(r, t) for r, t in enumerate(scrs)],
@@ -245,6 +246,7 @@ def test_solve_host_e2e_matches_oracle():
     lam = h * h / 8
     phi0, rho = _fields(n0, n1, 1, 21, P.PX_BC_PERIODIC)
     lay = P.Layout(P.box(0, 0, n0 - 1, n1 - 1), (n0, n1), 1, P.PX_BC_PERIODIC, 1)
+    torch.cuda.synchronize()
     out, norms = P.solve_host(lay, P.relax_params(h, lam), N, 5, phi0[1:-1, 1:-1], rho[1:-1, 1:-1],
                               stream=torch.cuda.Stream())
     ref, rn = oracle.solve(_orc_problem(n0, n1, h, lam, P.PX_BC_PERIODIC, 0, N, 5), phi0, rho)
