@@ -39,6 +39,9 @@ CONFIGS = {
     "C3": dict(n=16384, box=256, bc=0, stencil=0, sweeps=100, norm_every=1, rho="hash",
                desc="BASELINE config 3: 2D Poisson 16384x16384 fp64, periodic, 5-point, "
                     "slab-decomposed, per-sweep ghost exchange and residual all-reduce"),
+    "C4": dict(n=32768, box=256, bc=0, stencil=0, sweeps=100, norm_every=4, rho="hash", ghost=4, tk=4,
+               desc="BASELINE config 4: 2D Poisson 32768x32768 fp64, periodic, 5-point, 256x256-box "
+                    "DisjointBoxLayout, temporal blocking k=4 sweeps per halo exchange (norm per exchange)"),
     "C2": dict(n=1024, box=1024, bc=0, stencil=0, sweeps=1000, norm_every=10, rho="hash",
                desc="BASELINE config 2: 2D Poisson 1024x1024 single box, 1000 sweeps, "
                     "max-norm every 10 (L2-resident)"),
@@ -204,7 +207,8 @@ def run_native(args):
     h = 1.0 / n
     lam = h * h / 8
     box = cfg["box"]
-    lay = P.Layout(P.box(0, 0, n - 1, n - 1), (box, box), 1, cfg["bc"], world)
+    ghost, tk = cfg.get("ghost", 1), cfg.get("tk", 1)
+    lay = P.Layout(P.box(0, 0, n - 1, n - 1), (box, box), ghost, cfg["bc"], world)
     li = lay.local(rank)
     phi, scr, rho = lay.alloc(rank, dev), lay.alloc(rank, dev), lay.alloc(rank, dev)
     comm = None
@@ -224,11 +228,20 @@ def run_native(args):
             rhs = lay.alloc(rank, dev)
             stream.wait_stream(torch.cuda.current_stream(dev))
             P.mehrstellen_rhs(lay.patch(rank, rho), lay.patch(rank, rhs), li.owned, stream=stream)
+        if tk > 1:  # temporal blocking advances the halo: ρ needs its ghosts
+            P.exchange_ghosts(lay, comm, rank, lay.patch(rank, rhs), stream=stream)
     stream.synchronize()
     pa, pb, pr = lay.patch(rank, phi), lay.patch(rank, scr), lay.patch(rank, rhs)
 
+    bufs = [pa, pb]
+
     def step():
-        return P.solve(lay, comm, rank, prm, S, E, pa, pb, pr, use_graph=True, stream=stream)
+        # each step continues the relaxation from the previous step's iterate
+        r = P.solve(lay, comm, rank, prm, S, E, bufs[0], bufs[1], pr, use_graph=True, stream=stream,
+                    temporal_k=tk)
+        if r.in_scratch:
+            bufs.reverse()
+        return r
 
     def barrier():
         torch.cuda.synchronize()
@@ -265,10 +278,15 @@ def run_native(args):
     stream.wait_stream(torch.cuda.current_stream(dev))
     reps = 20
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
-    P.exchange_ghosts(lay, comm, rank, pa, stream=stream)
+    qa, qb = bufs
     for i in range(reps):
+        src, dst = (qa, qb) if i % 2 == 0 else (qb, qa)
+        P.exchange_ghosts(lay, comm, rank, src, stream=stream)
         evs[i][0].record(stream)
-        P.relax_step(prm, pa if i % 2 == 0 else pb, pb if i % 2 == 0 else pa, pr, li.owned, nb, stream=stream)
+        if tk > 1:
+            P.relax_block(prm, tk, src, dst, pr, li.owned, nb, stream=stream)
+        else:
+            P.relax_step(prm, src, dst, pr, li.owned, nb, stream=stream)
         evs[i][1].record(stream)
     stream.synchronize()
     k_ms = statistics.mean(a.elapsed_time(b) for a, b in evs[2:])
@@ -278,7 +296,9 @@ def run_native(args):
     traffic = load_traffic(args.config) if world == 1 else None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
-                "kernel": "k_stream<RELAX,5pt>" if cfg["stencil"] == 0 else "k_stream<RELAX,9pt>",
+                "kernel": (f"k_tb<5pt,K={tk}> (temporal blocking: one launch = {tk} sweeps, "
+                           f"{BYTES_PER_CELL_UPDATE}/{tk} B per cell-update)") if tk > 1 else
+                          ("k_bulk<RELAX,5pt> (TMA bulk-copy pipeline)" if cfg["stencil"] == 0 else "k_bulk<RELAX,9pt>"),
                 "kernel_ms": k_ms, "algorithmic_bytes_per_launch": BYTES_PER_CELL_UPDATE * local_cells,
                 "peak_source": peak_src, "whole_step_GBps": BYTES_PER_CELL_UPDATE * value}
 
@@ -294,7 +314,7 @@ def run_native(args):
         if world == 1:
             def e2e_step():
                 P.solve_host(lay, prm, S, E, h_phi0.numpy(), h_rho.numpy(), h_out.numpy(),
-                             use_graph=True, stream=stream)
+                             use_graph=True, stream=stream, temporal_k=tk)
         else:
             d_phi, d_scr, d_rhs = lay.alloc(rank, dev), lay.alloc(rank, dev), lay.alloc(rank, dev)
             stream.wait_stream(torch.cuda.current_stream(dev))
@@ -304,7 +324,10 @@ def run_native(args):
                 with torch.cuda.stream(stream):
                     lay.view(rank, d_phi).copy_(h_phi0, non_blocking=True)
                     lay.view(rank, d_rhs).copy_(h_rho, non_blocking=True)
-                r = P.solve(lay, comm, rank, prm, S, E, qa, qb, qr, use_graph=True, stream=stream)
+                if tk > 1:
+                    P.exchange_ghosts(lay, comm, rank, qr, stream=stream)
+                r = P.solve(lay, comm, rank, prm, S, E, qa, qb, qr, use_graph=True, stream=stream,
+                            temporal_k=tk)
                 with torch.cuda.stream(stream):
                     h_out.copy_(lay.view(rank, d_scr if r.in_scratch else d_phi), non_blocking=True)
                 stream.synchronize()
@@ -337,6 +360,8 @@ def run_native(args):
             "warmup": max(args.warmup, 3), "ms_per_step": t_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["desc"], "n": n, "sweeps_per_step": S, "norm_every": E,
+                       "temporal_k": tk, "ghost": ghost,
+                       "steps_continue": "each step continues from the previous step's iterate",
                        "box": box, "partition": f"slabs x{world}", "rho": cfg["rho"], "h": h, "lambda": lam,
                        "l2": "inputs (3 x %.2f GB) exceed L2; no flush" % (lay.local(0).alloc_elems * 8 / 1e9)
                        if n >= 4096 else "L2-resident working set (no flush: that is the config)"},

@@ -193,6 +193,19 @@ px_status px_stencil_apply(int32_t stencil, double scale, const px_patch* src, p
 px_status px_relax_step(const px_relax_params* p, const px_patch* phi_in, px_patch* phi_out,
                         const px_patch* rhs, px_box region, double* d_norms, void* stream);
 
+/* k fused sweeps in ONE pass over memory (temporal blocking, DESIGN.md §6
+ * K7): φ_out = k Jacobi sweeps of φ_in over `region`, bit-identical to k
+ * px_relax_step calls.  k in {2, 4}.  φ_in must hold valid values on
+ * grow(region, k) and rhs on grow(region, k): cells outside the region are
+ * advanced along with it as ordinary cells (the semantics of periodic
+ * images and inter-rank ghost copies); their results are not written.
+ * d_norms (optional) receives the norms of the residual of φ_in, as in
+ * px_relax_step.  Needs a 16-byte aligned region start and an even width
+ * (PX_ERR_ALIGN otherwise). */
+px_status px_relax_block(const px_relax_params* p, int32_t k, const px_patch* phi_in,
+                         px_patch* phi_out, const px_patch* rhs, px_box region, double* d_norms,
+                         void* stream);
+
 /* Residual norms of φ as given (computeMaxResidualAcrossProcs, single
  * patch): r = scale·S(φ) − rhs over region, into d_norms (required). */
 px_status px_residual_norm(const px_relax_params* p, const px_patch* phi, const px_patch* rhs,
@@ -261,7 +274,9 @@ px_status px_exchange_ghosts_local(const px_layout* l, const px_patch* parts, vo
  * Host-synchronous.  On return h_norms[2j], h_norms[2j+1] hold (max|r|, Σr²)
  * of entry j (global over all ranks), *n_written the number of entries
  * (capped at cap), and φ^N is in phi (*in_scratch = 0) or in phi_scratch
- * (*in_scratch = 1, odd N).  If in_scratch is NULL, φ^N is copied into phi.
+ * (*in_scratch = 1: an odd number of buffer swaps -- one per sweep, or with
+ * temporal_k = K one per K-sweep pass plus one per remaining sweep).  If
+ * in_scratch is NULL, φ^N is copied into phi.
  * Inputs: phi holds φ^0 (ghosts need not be filled), rhs holds the
  * right-hand side (ρ, or f from px_mehrstellen_rhs) on owned cells plus, for
  * temporal_k > 1, its ghosts to depth k filled (px_exchange_ghosts). */

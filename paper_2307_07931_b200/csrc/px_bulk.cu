@@ -32,13 +32,11 @@ constexpr int W = 512;                   // strip width (columns)
 constexpr int PAIRS = W / 2;             // consumer threads
 constexpr int NCW = PAIRS / 32;          // consumer warps (8)
 constexpr int THREADS = PAIRS + 32;      // + producer warp
-constexpr int R = 4;                     // rows per stage
-constexpr int STAGE_DOUBLES = R * 2 * W; // φ rows + rhs rows (32 KB)
-constexpr int NST_DEFAULT = 7;           // stages in the ring (224 KB)
-constexpr int CHUNK_ROWS = 256;          // nominal rows per work item
-template <int NST>
+constexpr int CHUNK_ROWS = 1024;         // nominal rows per work item
+// ring of NST stages of R rows of φ and of the rhs (R * 8 KB per stage)
+template <int NST, int R>
 constexpr size_t smem_bytes() {
-  return (size_t)NST * STAGE_DOUBLES * sizeof(double) + 2 * NST * sizeof(uint64_t);
+  return (size_t)NST * (R * 2 * W) * sizeof(double) + 2 * NST * sizeof(uint64_t);
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -96,6 +94,7 @@ __device__ __forceinline__ Item item_of(const StreamLaunch& a, int it, int nstri
   return t;
 }
 // φ rows streamed for an item: y0-1 .. y1 (inclusive) -> y1-y0+2 rows
+template <int R>
 __device__ __forceinline__ int item_stages(const Item& t) { return (t.y1 - t.y0 + 2 + R - 1) / R; }
 
 }  // namespace bulk
@@ -103,11 +102,11 @@ __device__ __forceinline__ int item_stages(const Item& t) { return (t.y1 - t.y0 
 using namespace bulk;
 
 
-// NST stages per CTA; NST <= 3 runs two CTAs per SM.  STP: 1 = streaming
-// (evict-first) stores of φ'.
-template <int MODE, int ST, int NST, int STP>
-__global__ void __launch_bounds__(THREADS, (NST <= 3 ? 2 : 1)) k_bulk(const StreamLaunch a, int nstrips,
-                                                                     int nitems, int crows) {
+// NST stages of R rows per CTA, CPS CTAs per SM.
+template <int MODE, int ST, int NST, int R, int CPS>
+__global__ void __launch_bounds__(THREADS, CPS) k_bulk(const StreamLaunch a, int nstrips, int nitems,
+                                                       int crows) {
+  constexpr int STAGE_DOUBLES = R * 2 * W;
   extern __shared__ __align__(128) double smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NST * STAGE_DOUBLES);
   uint64_t* empty = full + NST;
@@ -132,7 +131,7 @@ __global__ void __launch_bounds__(THREADS, (NST <= 3 ? 2 : 1)) k_bulk(const Stre
       uint32_t phase = 0;
       for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
         const Item t = item_of(a, it, nstrips, crows);
-        const int nst = item_stages(t);
+        const int nst = item_stages<R>(t);
         const uint32_t rowbytes = (uint32_t)t.w * 8u;
         for (int st = 0; st < nst; ++st) {
           mbar_wait(&empty[slot], phase ^ 1u);
@@ -192,7 +191,7 @@ __global__ void __launch_bounds__(THREADS, (NST <= 3 ? 2 : 1)) k_bulk(const Stre
       load_halo(t, 0);
     }
     for (; it < nitems; it += gridDim.x) {
-      const int nst = item_stages(t);
+      const int nst = item_stages<R>(t);
       const bool live = c0 < t.w;
       const bool left = (j == 0);
       const bool edge_r = (c0 + 2 == t.w);        // this pair ends the strip
@@ -265,10 +264,7 @@ __global__ void __launch_bounds__(THREADS, (NST <= 3 ? 2 : 1)) k_bulk(const Stre
               const double o1 = __dadd_rn(b_c, __dmul_rn(a.lambda, e1));
               const int x = t.c + c0;
               double* dp = a.dst + (int64_t)r * a.ld_dst + x;
-              if (STP)
-                __stcs(reinterpret_cast<double2*>(dp), make_double2(o0, o1));
-              else
-                *reinterpret_cast<double2*>(dp) = make_double2(o0, o1);
+              *reinterpret_cast<double2*>(dp) = make_double2(o0, o1);
               if (a.gs.g > 0) {
                 images(a, x, r, o0);
                 images(a, x + 1, r, o1);
@@ -302,26 +298,35 @@ static int num_sms() {
   return g_nsm;
 }
 
-// Tuning knobs (read once; defaults are the measured best):
-// PROTOX_BULK_NST = 3 (two CTAs per SM) | 5 | 7 stages, PROTOX_BULK_CHUNK =
-// nominal rows per work item, PROTOX_BULK_STORE = 1 for streaming stores.
+// Ring configurations built (stages x rows per stage x CTAs per SM); the
+// default is the measured best at 16384² (profiles/).
+// PROTOX_BULK_CFG=<index> selects another for A/B, PROTOX_BULK_CHUNK the
+// nominal rows per work item.
 struct BulkCfg {
-  int nst = 5, chunk = CHUNK_ROWS, stp = 0;
+  int nst, r, cps;
 };
+// measured at 16384² (GB/s): {3,2,3} 6132, {4,2,3} 6038, {3,4,2} 5917, {6,2,2} 5727,
+// {5,4,1} 5433 (profiles/round1_bulk_configs.json)
+static const BulkCfg kCfgs[] = {{3, 2, 3}, {3, 4, 2}, {5, 4, 1}, {7, 4, 1}, {6, 2, 2}, {4, 2, 3}};
 static const BulkCfg& bulk_cfg() {
-  static BulkCfg c;
-  static bool init = false;
-  if (!init) {
-    if (const char* e = getenv("PROTOX_BULK_NST")) {
+  static int idx = -1;
+  if (idx < 0) {
+    idx = 0;
+    if (const char* e = getenv("PROTOX_BULK_CFG")) {
       const int v = atoi(e);
-      c.nst = (v == 3 || v == 5 || v == 7) ? v : c.nst;
+      if (v >= 0 && v < (int)(sizeof(kCfgs) / sizeof(kCfgs[0]))) idx = v;
     }
+  }
+  return kCfgs[idx];
+}
+static int bulk_chunk() {
+  static int c = 0;
+  if (!c) {
+    c = CHUNK_ROWS;
     if (const char* e = getenv("PROTOX_BULK_CHUNK")) {
       const int v = atoi(e);
-      if (v >= 8 && v <= 65536) c.chunk = v;
+      if (v >= 8 && v <= 65536) c = v;
     }
-    if (const char* e = getenv("PROTOX_BULK_STORE")) c.stp = atoi(e) ? 1 : 0;
-    init = true;
   }
   return c;
 }
@@ -353,9 +358,9 @@ static BulkGeom bulk_geom(const StreamLaunch& a) {
   BulkGeom g;
   g.nstrips = (a.nx + W - 1) / W;
   const BulkCfg& cfg = bulk_cfg();
-  const int per_sm = cfg.nst <= 3 ? 2 : 1;
+  const int per_sm = cfg.cps;
   int gmax = num_sms() * per_sm < BULK_MAX_GRID ? num_sms() * per_sm : BULK_MAX_GRID;
-  const int c0 = (a.ny + cfg.chunk - 1) / cfg.chunk;
+  const int c0 = (a.ny + bulk_chunk() - 1) / bulk_chunk();
   double best = 1e30;
   g.nchunks = c0;
   for (int c = c0; c <= 2 * c0 && c <= a.ny; ++c) {
@@ -379,31 +384,29 @@ static BulkGeom bulk_geom(const StreamLaunch& a) {
 
 int32_t bulk_blocks(const StreamLaunch& a) { return bulk_geom(a).grid; }
 
-template <int MODE, int ST, int NST, int STP>
+template <int MODE, int ST, int NST, int R, int CPS>
 static cudaError_t launch_b(const StreamLaunch& a, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_bulk<MODE, ST, NST, STP>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<NST>());
+    cudaError_t e = cudaFuncSetAttribute(k_bulk<MODE, ST, NST, R, CPS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<NST, R>());
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const BulkGeom g = bulk_geom(a);
-  k_bulk<MODE, ST, NST, STP><<<g.grid, THREADS, smem_bytes<NST>(), s>>>(a, g.nstrips, g.nitems, g.crows);
-  return cudaPeekAtLastError();
+  k_bulk<MODE, ST, NST, R, CPS><<<g.grid, THREADS, smem_bytes<NST, R>(), s>>>(a, g.nstrips, g.nitems, g.crows);
+  return cudaGetLastError();
 }
 
 template <int MODE, int ST>
 static cudaError_t launch_cfg(const StreamLaunch& a, cudaStream_t s) {
   const BulkCfg& c = bulk_cfg();
-  if (c.stp) {
-    if (c.nst == 3) return launch_b<MODE, ST, 3, 1>(a, s);
-    if (c.nst == 7) return launch_b<MODE, ST, 7, 1>(a, s);
-    return launch_b<MODE, ST, 5, 1>(a, s);
-  }
-  if (c.nst == 3) return launch_b<MODE, ST, 3, 0>(a, s);
-  if (c.nst == 7) return launch_b<MODE, ST, 7, 0>(a, s);
-  return launch_b<MODE, ST, 5, 0>(a, s);
+  if (c.nst == 3 && c.r == 2) return launch_b<MODE, ST, 3, 2, 3>(a, s);
+  if (c.nst == 3 && c.r == 4) return launch_b<MODE, ST, 3, 4, 2>(a, s);
+  if (c.nst == 5) return launch_b<MODE, ST, 5, 4, 1>(a, s);
+  if (c.nst == 7) return launch_b<MODE, ST, 7, 4, 1>(a, s);
+  if (c.nst == 6) return launch_b<MODE, ST, 6, 2, 2>(a, s);
+  return launch_b<MODE, ST, 4, 2, 3>(a, s);
 }
 
 px_status launch_bulk(int mode, int stencil, const StreamLaunch& a, cudaStream_t s) {

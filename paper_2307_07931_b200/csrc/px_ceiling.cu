@@ -63,5 +63,5 @@ extern "C" px_status px_stream_ceiling(const double* a, const double* b, double*
   else
     k_triad<false><<<grid, 256, 0, s>>>((const double2*)a, nullptr, (double2*)c, n / 2);
   count_launches(1);
-  return cuda_check(cudaPeekAtLastError(), "ceiling kernel launch");
+  return cuda_check(cudaGetLastError(), "ceiling kernel launch");
 }

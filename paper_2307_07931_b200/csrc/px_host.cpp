@@ -348,6 +348,36 @@ int32_t px_relax_variant(const px_patch* phi_in, const px_patch* phi_out, const 
   return bulk_eligible(MODE_RELAX, a) ? 1 : 0;
 }
 
+px_status px_relax_block(const px_relax_params* p, int32_t k, const px_patch* phi_in,
+                         px_patch* phi_out, const px_patch* rhs, px_box region, double* d_norms,
+                         void* stream) {
+  if (!p) return fail(PX_ERR_ARG, "null params");
+  if (!phi_out || !rhs) return fail(PX_ERR_ARG, "null phi_out or rhs");
+  if (!(p->h > 0.0)) return fail(PX_ERR_ARG, "h must be positive");
+  if (k != 2 && k != 4) return fail(PX_ERR_UNSUPPORTED, "k=%d not built (2 or 4)", k);
+  StreamLaunch a;
+  PX_TRY(make_stream_launch(MODE_RELAX, p->stencil, stencil_scale(p->stencil, p->h), p->lambda,
+                            phi_in, rhs, phi_out, region, &a));
+  if (empty(region)) return PX_OK;
+  if (!contains(phi_in->box, grow(region, k)))
+    return fail(PX_ERR_DOMAIN, "phi_in must cover the region grown by k=%d", k);
+  if (!contains(rhs->box, grow(region, k)))
+    return fail(PX_ERR_DOMAIN, "rhs must cover the region grown by k=%d", k);
+  if (a.phase != 0 || (a.nx & 1))
+    return fail(PX_ERR_ALIGN, "temporal blocking needs a 16-byte aligned region start and an even width");
+  TbLaunch x;
+  std::memset(&x, 0, sizeof x);
+  if (d_norms) {
+    x.lvl[0].out_max = d_norms;
+    x.lvl[0].out_sum = d_norms + 1;
+    x.lvl[0].counter = reinterpret_cast<unsigned int*>(d_norms + 2);
+    x.lvl[0].partials = d_norms + 4;
+    x.lvl[0].offset = 0;
+    x.lvl[0].expected = tb_blocks(k, a);
+  }
+  return launch_tb(p->stencil, k, a, x, (cudaStream_t)stream);
+}
+
 px_status px_residual_norm(const px_relax_params* p, const px_patch* phi, const px_patch* rhs,
                            px_box region, double* d_norms, void* stream) {
   if (!p || !d_norms || !rhs) return fail(PX_ERR_ARG, "null argument");

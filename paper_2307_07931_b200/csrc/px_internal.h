@@ -105,6 +105,14 @@ struct StreamLaunch {
   NormSlot norms;     // norms.out_max == null: none
 };
 
+// Extra launch state of a temporal-blocking pass (px_tb.cu).
+struct TbLaunch {
+  NormSlot lvl[4];   // norms of the residual computed at level t (iterate base+t-1)
+  int32_t fix[2][2]; // FIXED faces: ghost cells there keep their level-0 value
+};
+int32_t tb_blocks(int K, const StreamLaunch& a);
+px_status launch_tb(int stencil, int K, const StreamLaunch& a, const TbLaunch& x, cudaStream_t s);
+
 // upper bound of the thread blocks a relax/residual launch over a region uses
 constexpr int32_t BULK_MAX_GRID = 512;
 int32_t stream_blocks(int32_t nx, int32_t ny, int32_t phase);

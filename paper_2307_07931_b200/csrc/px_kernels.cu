@@ -263,7 +263,7 @@ px_status launch_stream(int mode, int stencil, const StreamLaunch& a, cudaStream
     default: return fail(PX_ERR_ARG, "bad stream mode %d / stencil %d", mode, stencil);
   }
   count_launches(1);
-  return cuda_check(cudaPeekAtLastError(), "stream kernel launch");
+  return cuda_check(cudaGetLastError(), "stream kernel launch");
 }
 
 // ------------------------------------------------------------ ghost fill
@@ -316,13 +316,13 @@ px_status launch_fill_ghosts(const px_layout* l, int32_t rank, const px_patch& p
     int64_t n = (int64_t)ny * g * 2;
     k_ghost_x<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(o, p.ld, nx, ny, g, mx, mx);
     count_launches(1);
-    PX_TRY(cuda_check(cudaPeekAtLastError(), "ghost x launch"));
+    PX_TRY(cuda_check(cudaGetLastError(), "ghost x launch"));
   }
   if (my_lo != GH_NONE || my_hi != GH_NONE) {
     int64_t n = (int64_t)(nx + 2 * g) * g * 2;
     k_ghost_y<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(o, p.ld, nx, ny, g, my_lo, my_hi);
     count_launches(1);
-    PX_TRY(cuda_check(cudaPeekAtLastError(), "ghost y launch"));
+    PX_TRY(cuda_check(cudaGetLastError(), "ghost y launch"));
   }
   return PX_OK;
 }
@@ -368,7 +368,7 @@ px_status launch_init_field(const px_layout* l, int32_t rank, const px_patch& p,
                               li.owned.lo.c[1] - l->domain.lo.c[1] + y0, ext(l->domain, 0),
                               ext(l->domain, 1), kind, seed, k, lw);
     count_launches(1);
-    PX_TRY(cuda_check(cudaPeekAtLastError(), "init launch"));
+    PX_TRY(cuda_check(cudaGetLastError(), "init launch"));
   }
   return PX_OK;
 }

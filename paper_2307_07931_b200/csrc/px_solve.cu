@@ -120,8 +120,8 @@ struct Plan {
   int32_t n_entries = 0;
   double* d_max = nullptr;      // ring of recorded norms
   double* d_sum = nullptr;
-  double* d_ws = nullptr;       // counter (2 doubles) + partials
-  int64_t ws_len = 0;
+  double* d_ws = nullptr;       // per region: counter (2 doubles) + partials
+  int64_t ws_len = 0, ws_stride = 0;
   cudaGraphExec_t exec = nullptr;
   int64_t launches_per_run = 0;
   cudaEvent_t ev_bnd = nullptr, ev_comm = nullptr;
@@ -210,6 +210,10 @@ static px_status build_part_launches(const SolveCtx& x, int32_t part, const px_p
   return PX_OK;
 }
 
+// Norm-slot workspace region j (one per level of a temporal-blocking pass):
+// a ticket counter (2 doubles) followed by 2 partials per block.
+static double* ws_region(Plan* plan, int32_t j) { return plan->d_ws + (int64_t)j * plan->ws_stride; }
+
 static void set_slot(std::vector<SweepLaunch>& v, size_t first, Plan* plan, int32_t entry) {
   int32_t total = 0;
   for (size_t i = first; i < v.size(); ++i) total += v[i].blocks;
@@ -222,8 +226,8 @@ static void set_slot(std::vector<SweepLaunch>& v, size_t first, Plan* plan, int3
     }
     ns.out_max = plan->d_max + entry;
     ns.out_sum = plan->d_sum + entry;
-    ns.counter = reinterpret_cast<unsigned int*>(plan->d_ws);
-    ns.partials = plan->d_ws + 2;
+    ns.counter = reinterpret_cast<unsigned int*>(ws_region(plan, 0));
+    ns.partials = ws_region(plan, 0) + 2;
     ns.offset = off;
     ns.expected = total;
     off += v[i].blocks;
@@ -286,9 +290,62 @@ static px_status enqueue_solve(const SolveCtx& x) {
   }
   const px_patch* cur = x.phi;
   const px_patch* nxt = x.scr;
-  int32_t entry = 0;
-  for (int32_t it = 0; it < N; ++it) {
-    const int32_t slot = (E > 0 && it % E == 0) ? entry++ : -1;
+  const int32_t K = x.o->temporal_k > 1 ? x.o->temporal_k : 1;
+  int32_t it = 0;
+  // temporal blocking: K sweeps per pass, ghost exchange every K sweeps
+  while (K > 1 && it + K <= N) {
+    std::vector<StreamLaunch> la(x.nparts);
+    std::vector<TbLaunch> tl(x.nparts);
+    std::vector<int32_t> blocks(x.nparts);
+    int32_t total = 0;
+    for (int32_t part = 0; part < x.nparts; ++part) {
+      const int32_t rank = x.c ? x.rank : (x.nparts > 1 ? part : 0);
+      px_local_info li;
+      PX_TRY(local_info(x.l, rank, &li));
+      px_patch outp = nxt[part];
+      PX_TRY(make_stream_launch(MODE_RELAX, x.p->stencil, stencil_scale(x.p->stencil, x.p->h),
+                                x.p->lambda, &cur[part], &x.rhs[part], &outp, li.owned, &la[part]));
+      la[part].gs = ghost_spec(x.l, li, li.owned, x.l->nranks == 1);
+      std::memset(&tl[part], 0, sizeof(TbLaunch));
+      const bool fixed = x.l->bc == PX_BC_FIXED_GHOSTS;
+      tl[part].fix[0][0] = tl[part].fix[0][1] = fixed;
+      tl[part].fix[1][0] = fixed && li.nbr_lo < 0;
+      tl[part].fix[1][1] = fixed && li.nbr_hi < 0;
+      blocks[part] = tb_blocks(K, la[part]);
+      total += blocks[part];
+    }
+    int32_t off = 0;
+    for (int32_t part = 0; part < x.nparts; ++part) {
+      for (int32_t t = 0; t < K; ++t) {
+        const int32_t m = it + t;
+        NormSlot& ns = tl[part].lvl[t];
+        if (E > 0 && m % E == 0) {
+          ns.out_max = plan->d_max + m / E;
+          ns.out_sum = plan->d_sum + m / E;
+          ns.counter = reinterpret_cast<unsigned int*>(ws_region(plan, t));
+          ns.partials = ws_region(plan, t) + 2;
+          ns.offset = off;
+          ns.expected = total;
+        }
+      }
+      off += blocks[part];
+    }
+    for (int32_t part = 0; part < x.nparts; ++part)
+      PX_TRY(launch_tb(x.p->stencil, K, la[part], tl[part], x.s));
+    if (nccl_multi) {
+      PX_TRY(cuda_check(cudaEventRecord(plan->ev_bnd, x.s), "event record"));
+      PX_TRY(cuda_check(cudaStreamWaitEvent(x.c->stream, plan->ev_bnd, 0), "stream wait"));
+      PX_TRY(nccl_rows(x.l, x.c, x.rank, nxt[0], x.c->stream));
+      PX_TRY(cuda_check(cudaEventRecord(plan->ev_comm, x.c->stream), "event record"));
+      PX_TRY(cuda_check(cudaStreamWaitEvent(x.s, plan->ev_comm, 0), "stream wait"));
+    } else if (x.nparts > 1) {
+      PX_TRY(local_rows(x.l, nxt, x.s));
+    }
+    std::swap(cur, nxt);
+    it += K;
+  }
+  for (; it < N; ++it) {
+    const int32_t slot = (E > 0 && it % E == 0) ? it / E : -1;
     std::vector<SweepLaunch> v;
     for (int32_t part = 0; part < x.nparts; ++part)
       PX_TRY(build_part_launches(x, part, cur[part], nxt[part], false, nccl_multi, v));
@@ -310,11 +367,12 @@ static px_status enqueue_solve(const SolveCtx& x) {
     }
     std::swap(cur, nxt);
   }
+  const int32_t entry = plan->n_entries - 1;
   if (E >= 0) {
     std::vector<SweepLaunch> v;
     for (int32_t part = 0; part < x.nparts; ++part)
       PX_TRY(build_part_launches(x, part, cur[part], cur[part], true, false, v));
-    set_slot(v, 0, plan, entry++);
+    set_slot(v, 0, plan, entry);
     for (auto& sl : v) PX_TRY(launch_stream(MODE_RESID, x.p->stencil, sl.a, x.s));
   }
   if (nccl_multi && plan->n_entries > 0) {
@@ -420,8 +478,17 @@ px_status px_solve(const px_layout* l, px_comm* c, int32_t rank, const px_relax_
   if (!(p->h > 0.0)) return fail(PX_ERR_ARG, "h must be positive");
   if (p->stencil != PX_LAPLACE_5PT && p->stencil != PX_MEHRSTELLEN_9PT)
     return fail(PX_ERR_ARG, "bad stencil %d", p->stencil);
-  if (o->temporal_k != 1 && o->temporal_k != 0)
-    return fail(PX_ERR_UNSUPPORTED, "temporal_k=%d: temporal blocking not in this build", o->temporal_k);
+  if (o->temporal_k < 0) return fail(PX_ERR_ARG, "temporal_k must be >= 0");
+  if (o->temporal_k > 1) {
+    if (o->temporal_k != 2 && o->temporal_k != 4)
+      return fail(PX_ERR_UNSUPPORTED, "temporal_k=%d not built (1, 2 or 4)", o->temporal_k);
+    if (o->temporal_k > l->ghost)
+      return fail(PX_ERR_UNSUPPORTED, "temporal_k=%d exceeds the ghost width %d", o->temporal_k, l->ghost);
+    if (l->bc == PX_BC_DIRICHLET_CC)
+      return fail(PX_ERR_UNSUPPORTED, "temporal blocking with DIRICHLET_CC (per-level reflection) not built");
+    if (ext(l->domain, 0) % 2)
+      return fail(PX_ERR_UNSUPPORTED, "temporal blocking needs an even domain width");
+  }
   if (cap < 0 || (cap > 0 && !h_norms)) return fail(PX_ERR_ARG, "bad norm output");
   int32_t nparts = 1;
   if (c) {
@@ -450,7 +517,7 @@ px_status px_solve(const px_layout* l, px_comm* c, int32_t rank, const px_relax_
   key.stencil = p->stencil;
   key.nsweeps = o->nsweeps;
   key.norm_every = o->norm_every;
-  key.k = 1;
+  key.k = o->temporal_k > 1 ? o->temporal_k : 1;
   key.nparts = nparts;
   key.h = p->h;
   key.lambda = p->lambda;
@@ -475,7 +542,8 @@ px_status px_solve(const px_layout* l, px_comm* c, int32_t rank, const px_relax_
       // split launches add at most 2 extra partial rows of blocks
       maxblocks += stream_blocks(ext(lj.owned, 0), ext(lj.owned, 1), 1) + 2 * stream_blocks(ext(lj.owned, 0), 1, 1);
     }
-    np->ws_len = 2 + 2 * maxblocks;
+    np->ws_stride = 2 + 2 * maxblocks;
+    np->ws_len = np->ws_stride * (o->temporal_k > 1 ? o->temporal_k : 1);
     PX_TRY(cuda_check(cudaMalloc(&np->d_max, ne * sizeof(double)), "cudaMalloc ring"));
     PX_TRY(cuda_check(cudaMalloc(&np->d_sum, ne * sizeof(double)), "cudaMalloc ring"));
     PX_TRY(cuda_check(cudaMalloc(&np->d_ws, np->ws_len * sizeof(double)), "cudaMalloc ws"));
@@ -516,7 +584,11 @@ px_status px_solve(const px_layout* l, px_comm* c, int32_t rank, const px_relax_
     PX_TRY(cuda_check(cudaMemcpyAsync(hm.data(), plan->d_max, ne * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H norms"));
     PX_TRY(cuda_check(cudaMemcpyAsync(hs.data(), plan->d_sum, ne * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H norms"));
   }
-  const bool odd = (o->nsweeps % 2) == 1;
+  // φ^N is in the buffer the last pass wrote: one buffer swap per sweep, or
+  // per temporal-blocking pass of K sweeps plus one per remaining sweep.
+  const int32_t K = o->temporal_k > 1 ? o->temporal_k : 1;
+  const int32_t nswaps = K > 1 ? o->nsweeps / K + o->nsweeps % K : o->nsweeps;
+  const bool odd = (nswaps % 2) == 1;
   if (odd && !in_scratch) {
     for (int32_t i = 0; i < nparts; ++i) {
       const px_patch& a = phi_scratch[i];
@@ -589,6 +661,7 @@ px_status px_solve_host(const px_layout* l, const px_relax_params* p, const px_s
                                       n1, cudaMemcpyHostToDevice, s), "H2D phi"));
   PX_TRY(cuda_check(cudaMemcpy2DAsync(at(rh, li.owned.lo.c[0], li.owned.lo.c[1]), dp, h_rho, w, w,
                                       n1, cudaMemcpyHostToDevice, s), "H2D rho"));
+  if (o->temporal_k > 1) PX_TRY(launch_fill_ghosts(l, 0, rh, s));  // ρ ghosts for the halo levels
   int32_t in_scr = 0;
   PX_TRY(px_solve(l, nullptr, 0, p, o, &ph, &sc, &rh, h_norms, cap, n_written, &in_scr, stream));
   const px_patch& res = in_scr ? sc : ph;

@@ -1,0 +1,460 @@
+// px_tb.cu -- temporal blocking: K Jacobi sweeps per pass over HBM
+// (BASELINE config 4; DESIGN.md §6 K7).
+//
+// Exactly K plain sweeps (bit-identical to them and to the oracle): the
+// level-0 iterate streams through shared memory by TMA bulk copies (as in
+// k_bulk); each warp advances its 64 loaded columns through K time levels in
+// registers, one row behind per level (a wavefront down the chunk):
+//     level-0 row q arrives  ->  level 1 row q-1, level 2 row q-2, ...,
+//     level K row q-K  ->  HBM
+// W/E neighbours at every level come from the adjacent lane (__shfl); a
+// warp's two outermost columns have no neighbour, so the valid region
+// shrinks by one column per level and each warp writes its inner 64-2K
+// columns (redundant halo compute, no inter-warp synchronisation).  Rows of a
+// chunk are extended by K above and below (redundant, re-read from L2/HBM).
+// Ghost cells inside the loaded halo are advanced like interior cells
+// (periodic images and inter-rank copies compute the same values), except
+// FIXED_GHOSTS domain faces, which keep their level-0 values.  ρ must carry
+// valid ghosts to depth K.  HBM traffic: 24/K bytes per cell-update
+// (+ 2K/chunk rows + 2K/(64-2K)... halo, measured in profiles/).
+//
+// Arithmetic per cell is the oracle's tree; when scale and λ are powers of
+// two (h = 2^-p, λ = h²·2^-j, every BASELINE config) the products
+// scale·L, λ·r and 4·C are exact, so the fused multiply-adds
+// fma(scale, L, -ρ), fma(λ, r, φ), fma(-4, C, t) round exactly like the
+// separate operations -- bit-identical, fewer FP64 instructions (P2=1).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+
+#include "px_device.cuh"
+#include "px_internal.h"
+
+namespace px {
+
+namespace tb {
+
+constexpr int R = 3;               // rows per stage = rows per unrolled body (the S/C/N cycle)
+constexpr int NST = 4;             // ring stages (consumers hold the current and previous one)
+constexpr int CHUNK_ROWS = 255;    // nominal rows per work item (multiple of R)
+
+// NW consumer warps + 1 producer warp per CTA; NW = 8 runs 2 CTAs per SM,
+// NW = 16 one CTA per SM (more registers per thread).
+template <int K, int NW>
+struct Geom {
+  static constexpr int THREADS = NW * 32 + 32;
+  static constexpr int CPS = NW == 8 ? 2 : 1;
+  static constexpr int WO = 64 - 2 * K;          // output columns per warp
+  static constexpr int CO = NW * WO;             // output columns per CTA strip
+  static constexpr int CL = CO + 2 * K;          // loaded columns per CTA strip
+  static constexpr int CLS = (CL + 15) / 16 * 16; // smem row stride (doubles)
+  static constexpr int STAGE = R * 2 * CLS;      // φ rows + ρ rows
+  static constexpr size_t SMEM = (size_t)NST * STAGE * sizeof(double) + 2 * NST * sizeof(uint64_t);
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mb_init(uint64_t* b, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(c) : "memory");
+}
+__device__ __forceinline__ void mb_expect(uint64_t* b, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mb_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t par) {
+  asm volatile(
+      "{\n.reg .pred P1;\nW_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra W_%=;\n}\n" ::"r"(su32(b)),
+      "r"(par)
+      : "memory");
+}
+__device__ __forceinline__ void g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar)), "l"(pol)
+      : "memory");
+}
+
+struct P2d {
+  double a, b;  // the lane's two cells of a row
+};
+
+__device__ __forceinline__ int m3(int v) { return ((v % 3) + 3) % 3; }
+
+}  // namespace tb
+
+using namespace tb;
+
+// One level-t update of a lane's two cells from level t-1 rows S, C, N.
+template <int ST, int P2>
+__device__ __forceinline__ void lvl_update(const P2d& S, const P2d& C, const P2d& N, double2 f,
+                                           double scale, double lambda, double& o0, double& o1,
+                                           double& r0, double& r1) {
+  const double w = __shfl_up_sync(FULL_MASK, C.b, 1);    // lane 0: invalid column anyway
+  const double e = __shfl_down_sync(FULL_MASK, C.a, 1);  // lane 31: invalid column anyway
+  double L0, L1;
+  if (ST == 0) {
+    if (P2) {
+      L0 = fma(-4.0, C.a, __dadd_rn(__dadd_rn(__dadd_rn(w, C.b), S.a), N.a));
+      L1 = fma(-4.0, C.b, __dadd_rn(__dadd_rn(__dadd_rn(C.a, e), S.b), N.b));
+    } else {
+      L0 = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(w, C.b), S.a), N.a), __dmul_rn(-4.0, C.a));
+      L1 = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(C.a, e), S.b), N.b), __dmul_rn(-4.0, C.b));
+    }
+  } else {
+    const double sw = __shfl_up_sync(FULL_MASK, S.b, 1), se = __shfl_down_sync(FULL_MASK, S.a, 1);
+    const double nw = __shfl_up_sync(FULL_MASK, N.b, 1), ne = __shfl_down_sync(FULL_MASK, N.a, 1);
+    double q;
+    q = __dmul_rn(4.0, w);
+    q = __dadd_rn(q, __dmul_rn(4.0, C.b));
+    q = __dadd_rn(q, __dmul_rn(4.0, S.a));
+    q = __dadd_rn(q, __dmul_rn(4.0, N.a));
+    q = __dadd_rn(q, sw);
+    q = __dadd_rn(q, S.b);
+    q = __dadd_rn(q, nw);
+    q = __dadd_rn(q, N.b);
+    L0 = __dadd_rn(q, __dmul_rn(-20.0, C.a));
+    q = __dmul_rn(4.0, C.a);
+    q = __dadd_rn(q, __dmul_rn(4.0, e));
+    q = __dadd_rn(q, __dmul_rn(4.0, S.b));
+    q = __dadd_rn(q, __dmul_rn(4.0, N.b));
+    q = __dadd_rn(q, S.a);
+    q = __dadd_rn(q, se);
+    q = __dadd_rn(q, N.a);
+    q = __dadd_rn(q, ne);
+    L1 = __dadd_rn(q, __dmul_rn(-20.0, C.b));
+  }
+  if (P2) {
+    r0 = fma(scale, L0, -f.x);
+    r1 = fma(scale, L1, -f.y);
+    o0 = fma(lambda, r0, C.a);
+    o1 = fma(lambda, r1, C.b);
+  } else {
+    r0 = __dsub_rn(__dmul_rn(scale, L0), f.x);
+    r1 = __dsub_rn(__dmul_rn(scale, L1), f.y);
+    o0 = __dadd_rn(C.a, __dmul_rn(lambda, r0));
+    o1 = __dadd_rn(C.b, __dmul_rn(lambda, r1));
+  }
+}
+
+// Per-item consumer state shared by the stage bodies.
+struct TbCtx {
+  int qbase;        // first level-0 row of the item (y0 - K)
+  int y0, y1;       // output rows
+  int nrows;        // level-0 rows streamed: y1 - y0 + 2K
+  int xg;           // column (rel. region) of the lane's pair
+  bool own0, own1;  // lane writes / counts these cells
+  bool fx0, fx1;    // FIXED ghost columns (keep level-0 values)
+  bool xface;       // a written cell is within g of an x face (ghost images)
+};
+
+// Process the R rows of one stage.  CHECK: warm-up / drain stage (row-range
+// conditions evaluated); otherwise every level is computable and every row
+// is an output row (steady state, no per-row conditions).
+template <int ST, int K, int NW, int P2, int FIX, bool CHECK>
+__device__ __forceinline__ void tb_stage(const StreamLaunch& a, const TbLaunch& x, const TbCtx& c,
+                                         int s, const double* sp, const double* pp, int cl,
+                                         P2d (&st)[K][3], unsigned long long (&mx)[K], double (&ss)[K],
+                                         const bool (&act)[K]) {
+  using G = Geom<K, NW>;
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    const int r = s * R + j;                  // level-0 row index within the item
+    if (CHECK && r >= c.nrows) break;
+    const double2 v = *reinterpret_cast<const double2*>(sp + j * G::CLS + cl);
+    st[0][j] = P2d{v.x, v.y};                 // r ≡ j (mod 3)
+#pragma unroll
+    for (int t = 1; t <= K; ++t) {
+      if (CHECK && r < 2 * t) break;          // level t not yet computable
+      const int p = c.qbase + r - t;          // row computed at level t
+      // ρ(p) was loaded with level-0 row r-t+1 (this stage or the previous one)
+      constexpr int dummy = 0;
+      (void)dummy;
+      const int e = j - t + 1;
+      const double* rp = (e >= 0) ? (sp + (R + e) * G::CLS) : (pp + (R + R + e) * G::CLS);
+      const double2 f = *reinterpret_cast<const double2*>(rp + cl);
+      double o0, o1, r0, r1;
+      lvl_update<ST, P2>(st[t - 1][m3(j - t - 1)], st[t - 1][m3(j - t)], st[t - 1][m3(j - t + 1)], f,
+                         a.scale, a.lambda, o0, o1, r0, r1);
+      if (FIX) {
+        const bool fy = (p < 0 && x.fix[1][0]) || (p >= a.ny && x.fix[1][1]);
+        if (fy || c.fx0) o0 = st[t - 1][m3(j - t)].a;
+        if (fy || c.fx1) o1 = st[t - 1][m3(j - t)].b;
+      }
+      const bool prow = !CHECK || (p >= c.y0 && p < c.y1);
+      if (act[t - 1] && prow) {
+        if (c.own0) {
+          mx[t - 1] = umax64(mx[t - 1], (unsigned long long)__double_as_longlong(fabs(r0)));
+          ss[t - 1] = fma(r0, r0, ss[t - 1]);
+        }
+        if (c.own1) {
+          mx[t - 1] = umax64(mx[t - 1], (unsigned long long)__double_as_longlong(fabs(r1)));
+          ss[t - 1] = fma(r1, r1, ss[t - 1]);
+        }
+      }
+      if (t == K) {
+        if (prow) {
+          double* dp = a.dst + (int64_t)p * a.ld_dst + c.xg;
+          if (c.own0 && c.own1) {
+            *reinterpret_cast<double2*>(dp) = make_double2(o0, o1);
+          } else {
+            if (c.own0) dp[0] = o0;
+            if (c.own1) dp[1] = o1;
+          }
+          if (a.gs.g > 0) {
+            const int Y = p + a.gs.o[1];
+            if (c.xface || Y < a.gs.g || Y >= a.gs.n[1] - a.gs.g) {
+              if (c.own0) images(a, c.xg, p, o0);
+              if (c.own1) images(a, c.xg + 1, p, o1);
+            }
+          }
+        }
+      } else {
+        st[t][m3(j - t)] = P2d{o0, o1};
+      }
+    }
+  }
+}
+
+template <int ST, int K, int NW, int P2, int FIX>
+__global__ void __maxnreg__(112)
+    k_tb(const StreamLaunch a, const TbLaunch x, int nstrips, int nitems, int crows) {
+  using G = Geom<K, NW>;
+  extern __shared__ __align__(128) double smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NST * G::STAGE);
+  uint64_t* empty = full + NST;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mb_init(&full[s], 1);
+      mb_init(&empty[s], NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  unsigned long long mx[K];
+  double ss[K];
+  bool act[K];
+#pragma unroll
+  for (int t = 0; t < K; ++t) {
+    mx[t] = 0ull;
+    ss[t] = 0.0;
+    act[t] = x.lvl[t].out_max != nullptr;
+  }
+
+  if (warp == NW) {
+    // ------------- producer: level-0 rows of φ and the rows of ρ -------------
+    if (lane == 0) {
+      uint64_t pol;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      int slot = 0;
+      uint32_t phase = 0;
+      for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+        const int sidx = it % nstrips, k = it / nstrips;
+        const int cload = sidx * G::CO - K;
+        const int wcopy = min(G::CL, a.nx + K - cload);  // even (cload, nx, K even)
+        const uint32_t rb = (uint32_t)wcopy * 8u;
+        const int y0 = k * crows, y1 = min(a.ny, y0 + crows);
+        const int qbase = y0 - K, nrows = y1 - y0 + 2 * K;
+        const int nst = (nrows + R - 1) / R;
+        for (int s = 0; s < nst; ++s) {
+          mb_wait(&empty[slot], phase ^ 1u);
+          double* sp = smem + (size_t)slot * G::STAGE;
+          int n = 0;
+          for (int j = 0; j < R; ++j) {
+            const int r = s * R + j;
+            if (r < nrows) n += (r >= 2) ? 2 : 1;
+          }
+          mb_expect(&full[slot], rb * (uint32_t)n);
+          for (int j = 0; j < R; ++j) {
+            const int r = s * R + j;
+            if (r >= nrows) break;
+            const int q = qbase + r;
+            g2s(sp + j * G::CLS, a.src + (int64_t)q * a.ld_src + cload, rb, &full[slot], pol);
+            if (r >= 2)  // ρ row q-1: rows y0-K+1 .. y1+K-2 are the ones the levels use
+              g2s(sp + (R + j) * G::CLS, a.rhs + (int64_t)(q - 1) * a.ld_rhs + cload, rb, &full[slot], pol);
+          }
+          if (++slot == NST) {
+            slot = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+  } else {
+    // ---------------------------- consumers ----------------------------
+    const int cl = warp * G::WO + 2 * lane;
+    const bool own = (2 * lane >= K) && (2 * lane + 1 < 64 - K);
+    int slot = 0, prev = -1;
+    uint32_t phase = 0;
+    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+      const int sidx = it % nstrips, k = it / nstrips;
+      TbCtx c;
+      const int cload = sidx * G::CO - K;
+      c.xg = cload + cl;
+      c.own0 = own && c.xg >= 0 && c.xg < a.nx;
+      c.own1 = own && c.xg + 1 >= 0 && c.xg + 1 < a.nx;
+      c.fx0 = FIX && ((c.xg < 0 && x.fix[0][0]) || (c.xg >= a.nx && x.fix[0][1]));
+      c.fx1 = FIX && ((c.xg + 1 < 0 && x.fix[0][0]) || (c.xg + 1 >= a.nx && x.fix[0][1]));
+      {
+        const int X0 = c.xg + a.gs.o[0];
+        c.xface = (X0 < a.gs.g + 1) || (X0 + 1 >= a.gs.n[0] - a.gs.g - 1);
+      }
+      c.y0 = k * crows;
+      c.y1 = min(a.ny, c.y0 + crows);
+      c.qbase = c.y0 - K;
+      c.nrows = c.y1 - c.y0 + 2 * K;
+      const int nst = (c.nrows + R - 1) / R;
+      P2d st[K][3];
+#pragma unroll
+      for (int t = 0; t < K; ++t)
+#pragma unroll
+        for (int u = 0; u < 3; ++u) st[t][u] = P2d{0.0, 0.0};
+      const double* pp = smem;  // previous stage (valid from s = 1)
+      for (int s = 0; s < nst; ++s) {
+        mb_wait(&full[slot], phase);
+        const double* sp = smem + (size_t)slot * G::STAGE;
+        const bool steady = (s * R >= 2 * K) && (s * R + R - 1 < c.nrows - K);
+        if (steady)
+          tb_stage<ST, K, NW, P2, FIX, false>(a, x, c, s, sp, pp, cl, st, mx, ss, act);
+        else
+          tb_stage<ST, K, NW, P2, FIX, true>(a, x, c, s, sp, pp, cl, st, mx, ss, act);
+        __syncwarp();
+        if (prev >= 0 && lane == 0) mb_arrive(&empty[prev]);  // stage s-1 no longer needed
+        prev = slot;
+        pp = sp;
+        if (++slot == NST) {
+          slot = 0;
+          phase ^= 1u;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mb_arrive(&empty[prev]);  // the item's last stage
+      prev = -1;
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < K; ++t) {
+    if (act[t]) {
+      reduce_norms(x.lvl[t], mx[t], ss[t]);
+      __syncthreads();
+    }
+  }
+}
+
+// ------------------------------------------------------------------ host
+static int tb_nsm() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+struct TbPlan {
+  int nstrips, nitems, crows, grid;
+};
+
+static int tb_nw() {
+  static int nw = 0;
+  if (!nw) {
+    const char* e = getenv("PROTOX_TB_NW");  // A/B knob: 8 (2 CTAs/SM) or 16 (1 CTA/SM)
+    nw = (e && atoi(e) == 8) ? 8 : 16;
+  }
+  return nw;
+}
+
+static TbPlan tb_plan(int K, int nx, int ny) {
+  TbPlan g;
+  const int NW = tb_nw();
+  const int CO = NW * (64 - 2 * K);
+  const int RK = 3 * K / (K % 3 == 0 ? 3 : 1);  // chunk rows: multiple of R (=3)
+  g.nstrips = (nx + CO - 1) / CO;
+  const int cps = NW == 8 ? 2 : 1;
+  const int gmax = cps * tb_nsm() < BULK_MAX_GRID ? cps * tb_nsm() : BULK_MAX_GRID;
+  const int c0 = (ny + CHUNK_ROWS - 1) / CHUNK_ROWS;
+  double best = 1e30;
+  int bestc = c0;
+  for (int c = c0; c <= 2 * c0 && c <= ny; ++c) {
+    int rows = (ny + c - 1) / c;
+    rows = (rows + 2) / 3 * 3;  // whole stages of R = 3 rows
+    const int cc = (ny + rows - 1) / rows;
+    const int items = g.nstrips * cc;
+    const int waves = (items + gmax - 1) / gmax;
+    const double cost = (double)waves * (rows + 2 * K);
+    if (cost < best - 1e-9) {
+      best = cost;
+      bestc = cc;
+    }
+  }
+  g.crows = (ny + bestc - 1) / bestc;
+  g.crows = (g.crows + 2) / 3 * 3;
+  (void)RK;
+  const int nch = (ny + g.crows - 1) / g.crows;
+  g.nitems = g.nstrips * nch;
+  g.grid = g.nitems < gmax ? g.nitems : gmax;
+  return g;
+}
+
+int32_t tb_blocks(int K, const StreamLaunch& a) { return tb_plan(K, a.nx, a.ny).grid; }
+
+static bool pow2(double v) {
+  if (!(v > 0.0) || !std::isfinite(v)) return false;
+  int e;
+  return std::frexp(v, &e) == 0.5;
+}
+
+template <int ST, int K, int NW, int P2, int FIX>
+static cudaError_t tb_launch_nw(const StreamLaunch& a, const TbLaunch& x, cudaStream_t s) {
+  using G = Geom<K, NW>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_tb<ST, K, NW, P2, FIX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)G::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const TbPlan g = tb_plan(K, a.nx, a.ny);
+  k_tb<ST, K, NW, P2, FIX><<<g.grid, G::THREADS, G::SMEM, s>>>(a, x, g.nstrips, g.nitems, g.crows);
+  return cudaGetLastError();
+}
+
+template <int ST, int K, int P2, int FIX>
+static cudaError_t tb_launch_t(const StreamLaunch& a, const TbLaunch& x, cudaStream_t s) {
+  return tb_nw() == 8 ? tb_launch_nw<ST, K, 8, P2, FIX>(a, x, s) : tb_launch_nw<ST, K, 16, P2, FIX>(a, x, s);
+}
+
+template <int ST, int K, int P2>
+static cudaError_t tb_fix(const StreamLaunch& a, const TbLaunch& x, cudaStream_t s) {
+  const bool fix = x.fix[0][0] || x.fix[0][1] || x.fix[1][0] || x.fix[1][1];
+  return fix ? tb_launch_t<ST, K, P2, 1>(a, x, s) : tb_launch_t<ST, K, P2, 0>(a, x, s);
+}
+
+px_status launch_tb(int stencil, int K, const StreamLaunch& a, const TbLaunch& x, cudaStream_t s) {
+  if (a.phase != 0 || (a.nx & 1)) return fail(PX_ERR_ALIGN, "temporal blocking needs an aligned, even-width slab");
+  const bool p2 = stencil == 0 && pow2(a.scale) && pow2(a.lambda);
+  cudaError_t e;
+  const int key = (stencil * 8 + K) * 2 + (p2 ? 1 : 0);
+  switch (key) {
+    case (0 * 8 + 2) * 2 + 0: e = tb_fix<0, 2, 0>(a, x, s); break;
+    case (0 * 8 + 2) * 2 + 1: e = tb_fix<0, 2, 1>(a, x, s); break;
+    case (0 * 8 + 4) * 2 + 0: e = tb_fix<0, 4, 0>(a, x, s); break;
+    case (0 * 8 + 4) * 2 + 1: e = tb_fix<0, 4, 1>(a, x, s); break;
+    case (1 * 8 + 2) * 2 + 0: e = tb_fix<1, 2, 0>(a, x, s); break;
+    case (1 * 8 + 4) * 2 + 0: e = tb_fix<1, 4, 0>(a, x, s); break;
+    default: return fail(PX_ERR_UNSUPPORTED, "temporal_k=%d not built (2 or 4)", K);
+  }
+  count_launches(1);
+  return cuda_check(e, "temporal-blocking kernel launch");
+}
+
+}  // namespace px

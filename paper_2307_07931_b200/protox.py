@@ -83,7 +83,7 @@ EXPORTS = [
     "px_box_size", "px_box_is_empty", "px_box_grow", "px_box_intersect", "px_box_ordinal",
     "px_layout_create", "px_layout_destroy", "px_layout_num_boxes", "px_layout_box",
     "px_layout_local", "px_layout_patch", "px_layout_halo_plan", "px_norm_buffer_len",
-    "px_stencil_apply", "px_relax_step", "px_residual_norm", "px_mehrstellen_rhs",
+    "px_stencil_apply", "px_relax_step", "px_relax_block", "px_residual_norm", "px_mehrstellen_rhs",
     "px_init_field", "px_fill_ghosts",
     "px_comm_unique_id", "px_comm_create", "px_comm_destroy", "px_comm_allreduce_norms",
     "px_exchange_ghosts", "px_exchange_ghosts_local",
@@ -136,6 +136,8 @@ def lib():
     L.px_stencil_apply.argtypes = [i32, ctypes.c_double, P(px_patch), P(px_patch), px_box, vp]
     L.px_relax_step.restype = st
     L.px_relax_step.argtypes = [P(px_relax_params), P(px_patch), P(px_patch), P(px_patch), px_box, vp, vp]
+    L.px_relax_block.restype = st
+    L.px_relax_block.argtypes = [P(px_relax_params), i32, P(px_patch), P(px_patch), P(px_patch), px_box, vp, vp]
     L.px_residual_norm.restype = st
     L.px_residual_norm.argtypes = [P(px_relax_params), P(px_patch), P(px_patch), px_box, vp, vp]
     L.px_mehrstellen_rhs.restype = st
@@ -312,6 +314,13 @@ def relax_step(p: px_relax_params, phi_in: px_patch, phi_out: px_patch, rhs: px_
                                ctypes.byref(rhs), region, _ptr(norms), _stream(stream)))
 
 
+def relax_block(p: px_relax_params, k: int, phi_in: px_patch, phi_out: px_patch, rhs: px_patch,
+                region: px_box, norms=None, stream=None):
+    """px_relax_block: k sweeps in one pass (temporal blocking)."""
+    _check(lib().px_relax_block(ctypes.byref(p), k, ctypes.byref(phi_in), ctypes.byref(phi_out),
+                                ctypes.byref(rhs), region, _ptr(norms), _stream(stream)))
+
+
 def residual_norm(p: px_relax_params, phi: px_patch, rhs: px_patch, region: px_box, norms,
                   stream=None):
     _check(lib().px_residual_norm(ctypes.byref(p), ctypes.byref(phi), ctypes.byref(rhs), region,
@@ -402,7 +411,7 @@ def solve(layout: Layout, comm: Comm | None, rank: int, p: px_relax_params, nswe
 
 def solve_host(layout: Layout, p: px_relax_params, nsweeps: int, norm_every: int,
                phi0: np.ndarray, rho: np.ndarray, out: np.ndarray | None = None,
-               use_graph: bool = False, stream=None):
+               use_graph: bool = False, stream=None, temporal_k: int = 1):
     """px_solve_host: numpy (n1, n0) float64 host arrays (pinned torch CPU
     tensors also accepted via .numpy()).  Returns (phi_N, norms)."""
     phi0 = np.ascontiguousarray(phi0, dtype=np.float64)
@@ -412,7 +421,7 @@ def solve_host(layout: Layout, p: px_relax_params, nsweeps: int, norm_every: int
     cap = 0 if norm_every < 0 else ((nsweeps + norm_every - 1) // norm_every if norm_every > 0 else 0) + 1
     norms = np.zeros((max(cap, 1), 2), dtype=np.float64)
     nw = ctypes.c_int32(0)
-    opts = px_solve_opts(nsweeps, norm_every, 1, int(use_graph))
+    opts = px_solve_opts(nsweeps, norm_every, temporal_k, int(use_graph))
     _check(lib().px_solve_host(layout.h, ctypes.byref(p), ctypes.byref(opts),
                                phi0.ctypes.data_as(ctypes.c_void_p), rho.ctypes.data_as(ctypes.c_void_p),
                                out.ctypes.data_as(ctypes.c_void_p),

@@ -45,7 +45,7 @@ def _check_norms(gpu, orc):
 
 
 def run_gpu_solve(n0, n1, h, lam, bc, st, N, E, phi0_g, rho_g, g=1, box=None, nranks=1,
-                  graph=True, corr=False):
+                  graph=True, corr=False, tk=1):
     """Solve on the GPU; nranks > 1 runs all slabs on this device (local transport)."""
     dom = P.box(0, 0, n0 - 1, n1 - 1)
     lay = P.Layout(dom, box or (n0, n1 // nranks), g, bc, nranks)
@@ -63,12 +63,16 @@ def run_gpu_solve(n0, n1, h, lam, bc, st, N, E, phi0_g, rho_g, g=1, box=None, nr
             P.mehrstellen_rhs(lay.patch(r, rhss[r]), lay.patch(r, f), lay.local(r).owned)
             fs.append(f)
         rhss = fs
+    if tk > 1:
+        # temporal blocking advances ghost cells too: ρ needs its ghosts (depth >= k)
+        P.exchange_ghosts_local(lay, [lay.patch(r, t) for r, t in enumerate(rhss)])
     stream = torch.cuda.Stream()
     stream.wait_stream(torch.cuda.current_stream())  # allocations/copies ran on the current stream
     res = P.solve(lay, None, 0, P.relax_params(h, lam, st), N, E,
                   [lay.patch(r, t) for r, t in enumerate(phis)],
                   [lay.patch(r, t) for r, t in enumerate(scrs)],
-                  [lay.patch(r, t) for r, t in enumerate(rhss)], use_graph=graph, stream=stream)
+                  [lay.patch(r, t) for r, t in enumerate(rhss)], use_graph=graph, stream=stream,
+                  temporal_k=tk)
     out_t = scrs if res.in_scratch else phis
     out = np.concatenate([owned_to_host(lay, r, out_t[r]) for r in range(nranks)], axis=0)
     return out, res.norms, lay
@@ -413,3 +417,76 @@ def test_solve_bulk_kernel_bitwise(nranks, bc, st):
     ref, rn = oracle.solve(_orc_problem(n0, n1, h, lam, bc, st, N, E), phi0, rho)
     assert bits_equal(out, ref[1:-1, 1:-1]), ulp_diff(out, ref[1:-1, 1:-1])
     _check_norms(norms, rn)
+
+
+# ------------------------------------------------- temporal blocking (a7)
+@pytest.mark.parametrize("tk", [2, 4])
+@pytest.mark.parametrize("bc", [P.PX_BC_PERIODIC, P.PX_BC_FIXED_GHOSTS])
+@pytest.mark.parametrize("st", [P.PX_LAPLACE_5PT, P.PX_MEHRSTELLEN_9PT])
+@pytest.mark.parametrize("nranks,hinv", [(1, 1024), (3, 1000)])
+def test_solve_temporal_blocking_bitwise(tk, bc, st, nranks, hinv):
+    """k sweeps per pass (ghost width 4) == k plain sweeps, bit for bit: ragged
+    strips (1000 = 2 x 448 + 104 columns), several row chunks, 3 slabs with
+    local transport, an odd sweep count (2 or 4-blocks + plain sweeps),
+    power-of-two h (fused multiply-add path) and h = 1/1000 (separate ops)."""
+    n0, n1, N, E = 1000, 300, 11, 3
+    h = 1.0 / hinv
+    lam = h * h / 8 if st == 0 else 3 * h * h / 16
+    g = 4
+    phi0, rho = _fields(n0, n1, g, 40 + tk + bc + st, bc)
+    out, norms, _ = run_gpu_solve(n0, n1, h, lam, bc, st, N, E, phi0, rho, g=g, box=(50, 50),
+                                  nranks=nranks, tk=tk)
+    ref, rn = oracle.solve(_orc_problem(n0, n1, h, lam, bc, st, N, E, g=g), phi0, rho)
+    assert bits_equal(out, ref[g:-g, g:-g]), ulp_diff(out, ref[g:-g, g:-g])
+    _check_norms(norms, rn)
+
+
+def test_temporal_blocking_large_tall():
+    """Bulk-sized temporal blocking (many chunks per strip), k = 4, periodic."""
+    n0, n1, N, E = 2048, 2560, 8, 1
+    h = 1.0 / 2048
+    lam = h * h / 8
+    g = 4
+    phi0, rho = _fields(n0, n1, g, 77, P.PX_BC_PERIODIC)
+    out, norms, _ = run_gpu_solve(n0, n1, h, lam, P.PX_BC_PERIODIC, 0, N, E, phi0, rho, g=g, box=(256, 256),
+                                  tk=4)
+    ref, rn = oracle.solve(_orc_problem(n0, n1, h, lam, P.PX_BC_PERIODIC, 0, N, E, g=g), phi0, rho)
+    assert bits_equal(out, ref[g:-g, g:-g]), ulp_diff(out, ref[g:-g, g:-g])
+    _check_norms(norms, rn)
+
+
+def test_temporal_blocking_unsupported_cases():
+    lay = P.Layout(P.box(0, 0, 127, 127), (64, 64), 2, P.PX_BC_DIRICHLET_CC, 1)
+    a, b, r = lay.alloc(0), lay.alloc(0), lay.alloc(0)
+    with pytest.raises(P.PxError, match="DIRICHLET"):
+        P.solve(lay, None, 0, P.relax_params(1 / 128, 1e-6), 4, 1, lay.patch(0, a), lay.patch(0, b),
+                lay.patch(0, r), temporal_k=2)
+    with pytest.raises(P.PxError, match="exceeds the ghost width"):
+        P.solve(lay, None, 0, P.relax_params(1 / 128, 1e-6), 4, 1, lay.patch(0, a), lay.patch(0, b),
+                lay.patch(0, r), temporal_k=4)
+
+
+@pytest.mark.parametrize("k", [2, 4])
+@pytest.mark.parametrize("st", [P.PX_LAPLACE_5PT, P.PX_MEHRSTELLEN_9PT])
+def test_relax_block_bitwise(k, st):
+    """px_relax_block: k sweeps in one pass == k plain sweeps (periodic ghosts
+    filled to depth 4 for φ and ρ); norms = residual of φ_in."""
+    n0, n1, g = 1500, 700, 4
+    h = 1.0 / 2048
+    lam = h * h / 8 if st == 0 else 3 * h * h / 16
+    phi0, rho = _fields(n0, n1, g, 91 + k + st, P.PX_BC_PERIODIC)
+    lay = P.Layout(P.box(0, 0, n0 - 1, n1 - 1), (n0, n1), g, P.PX_BC_PERIODIC, 1)
+    a = to_device_ghosted(lay, 0, phi0, g)
+    b = lay.alloc(0)
+    r = to_device_ghosted(lay, 0, rho, g)
+    P.fill_ghosts(lay, 0, lay.patch(0, a))
+    P.fill_ghosts(lay, 0, lay.patch(0, r))
+    nb = P.norm_buffer(lay.local(0).owned)
+    P.relax_block(P.relax_params(h, lam, st), k, lay.patch(0, a), lay.patch(0, b), lay.patch(0, r),
+                  lay.local(0).owned, nb)
+    torch.cuda.synchronize()
+    ref, rn = oracle.solve(_orc_problem(n0, n1, h, lam, P.PX_BC_PERIODIC, st, k, k, g=g), phi0, rho)
+    out = owned_to_host(lay, 0, b)
+    assert bits_equal(out, ref[g:-g, g:-g]), ulp_diff(out, ref[g:-g, g:-g])
+    assert nb[0].item() == rn[0, 0]
+    assert abs(nb[1].item() - rn[0, 1]) <= SUM_RTOL * rn[0, 1]
