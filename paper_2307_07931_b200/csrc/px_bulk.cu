@@ -28,15 +28,13 @@ namespace px {
 
 namespace bulk {
 
-constexpr int W = 512;                   // strip width (columns)
-constexpr int PAIRS = W / 2;             // consumer threads
-constexpr int NCW = PAIRS / 32;          // consumer warps (8)
-constexpr int THREADS = PAIRS + 32;      // + producer warp
+// NC consumer warps (a strip of W = 64*NC columns, one column pair per
+// thread) + 1 producer warp.
 constexpr int CHUNK_ROWS = 1024;         // nominal rows per work item
 // ring of NST stages of R rows of φ and of the rhs (R * 8 KB per stage)
-template <int NST, int R>
+template <int NST, int R, int NC>
 constexpr size_t smem_bytes() {
-  return (size_t)NST * (R * 2 * W) * sizeof(double) + 2 * NST * sizeof(uint64_t);
+  return (size_t)NST * (R * 2 * 64 * NC) * sizeof(double) + 2 * NST * sizeof(uint64_t);
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -84,6 +82,7 @@ struct Item {
   int y0, y1;  // rows computed: [y0, y1)
 };
 
+template <int W>
 __device__ __forceinline__ Item item_of(const StreamLaunch& a, int it, int nstrips, int crows) {
   Item t;
   const int s = it % nstrips, k = it / nstrips;
@@ -103,9 +102,10 @@ using namespace bulk;
 
 
 // NST stages of R rows per CTA, CPS CTAs per SM.
-template <int MODE, int ST, int NST, int R, int CPS>
-__global__ void __launch_bounds__(THREADS, CPS) k_bulk(const StreamLaunch a, int nstrips, int nitems,
-                                                       int crows) {
+template <int MODE, int ST, int NST, int R, int CPS, int NC>
+__global__ void __launch_bounds__(NC * 32 + 32, CPS) k_bulk(const StreamLaunch a, int nstrips, int nitems,
+                                                            int crows) {
+  constexpr int W = 64 * NC, NCW = NC;
   constexpr int STAGE_DOUBLES = R * 2 * W;
   extern __shared__ __align__(128) double smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NST * STAGE_DOUBLES);
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(THREADS, CPS) k_bulk(const StreamLaunch a, int
       int slot = 0;
       uint32_t phase = 0;
       for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
-        const Item t = item_of(a, it, nstrips, crows);
+        const Item t = item_of<W>(a, it, nstrips, crows);
         const int nst = item_stages<R>(t);
         const uint32_t rowbytes = (uint32_t)t.w * 8u;
         for (int st = 0; st < nst; ++st) {
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(THREADS, CPS) k_bulk(const StreamLaunch a, int
     int it = blockIdx.x;
     Item t;
     if (it < nitems) {
-      t = item_of(a, it, nstrips, crows);
+      t = item_of<W>(a, it, nstrips, crows);
       load_halo(t, 0);
     }
     for (; it < nitems; it += gridDim.x) {
@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(THREADS, CPS) k_bulk(const StreamLaunch a, int
         if (st + 1 < nst) {
           load_halo(t, st + 1);
         } else if (it + (int)gridDim.x < nitems) {
-          load_halo(item_of(a, it + gridDim.x, nstrips, crows), 0);
+          load_halo(item_of<W>(a, it + gridDim.x, nstrips, crows), 0);
         }
         mbar_wait(&full[slot], phase);
         const double* sp = smem + (size_t)slot * STAGE_DOUBLES;
@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(THREADS, CPS) k_bulk(const StreamLaunch a, int
           phase ^= 1u;
         }
       }
-      if (it + (int)gridDim.x < nitems) t = item_of(a, it + gridDim.x, nstrips, crows);
+      if (it + (int)gridDim.x < nitems) t = item_of<W>(a, it + gridDim.x, nstrips, crows);
     }
   }
   if (a.norms.out_max) reduce_norms(a.norms, mx, ss);
@@ -303,11 +303,15 @@ static int num_sms() {
 // PROTOX_BULK_CFG=<index> selects another for A/B, PROTOX_BULK_CHUNK the
 // nominal rows per work item.
 struct BulkCfg {
-  int nst, r, cps;
+  int nst, r, cps, nc;
 };
-// measured at 16384² (GB/s): {3,2,3} 6132, {4,2,3} 6038, {3,4,2} 5917, {6,2,2} 5727,
-// {5,4,1} 5433 (profiles/round1_bulk_configs.json)
-static const BulkCfg kCfgs[] = {{3, 2, 3}, {3, 4, 2}, {5, 4, 1}, {7, 4, 1}, {6, 2, 2}, {4, 2, 3}};
+// {stages, rows per stage, CTAs per SM, consumer warps}; measured at 16384²
+// (GB/s, profiles/round1_bulk_configs.json): {3,2,3,7} 6171, {3,2,3,8} 6118-6132,
+// {4,2,3,7} 6136, {3,4,2,8} 5917, {5,4,1,8} 5433, {3,2,4,7} 4633 (spills).
+// 8-warp blocks (7 consumers + producer) keep 6 warps per SM sub-partition
+// at 80 registers without spills.
+static const BulkCfg kCfgs[] = {{3, 2, 3, 7}, {3, 2, 3, 8}, {3, 4, 2, 8}, {5, 4, 1, 8},
+                                 {3, 2, 4, 7}, {4, 2, 3, 7}};
 static const BulkCfg& bulk_cfg() {
   static int idx = -1;
   if (idx < 0) {
@@ -356,7 +360,7 @@ struct BulkGeom {
 };
 static BulkGeom bulk_geom(const StreamLaunch& a) {
   BulkGeom g;
-  g.nstrips = (a.nx + W - 1) / W;
+  g.nstrips = (a.nx + 64 * bulk_cfg().nc - 1) / (64 * bulk_cfg().nc);
   const BulkCfg& cfg = bulk_cfg();
   const int per_sm = cfg.cps;
   int gmax = num_sms() * per_sm < BULK_MAX_GRID ? num_sms() * per_sm : BULK_MAX_GRID;
@@ -384,29 +388,33 @@ static BulkGeom bulk_geom(const StreamLaunch& a) {
 
 int32_t bulk_blocks(const StreamLaunch& a) { return bulk_geom(a).grid; }
 
-template <int MODE, int ST, int NST, int R, int CPS>
+template <int MODE, int ST, int NST, int R, int CPS, int NC>
 static cudaError_t launch_b(const StreamLaunch& a, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_bulk<MODE, ST, NST, R, CPS>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<NST, R>());
+    cudaError_t e = cudaFuncSetAttribute(k_bulk<MODE, ST, NST, R, CPS, NC>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem_bytes<NST, R, NC>());
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const BulkGeom g = bulk_geom(a);
-  k_bulk<MODE, ST, NST, R, CPS><<<g.grid, THREADS, smem_bytes<NST, R>(), s>>>(a, g.nstrips, g.nitems, g.crows);
+  k_bulk<MODE, ST, NST, R, CPS, NC><<<g.grid, NC * 32 + 32, smem_bytes<NST, R, NC>(), s>>>(a, g.nstrips, g.nitems,
+                                                                                       g.crows);
   return cudaGetLastError();
 }
 
 template <int MODE, int ST>
 static cudaError_t launch_cfg(const StreamLaunch& a, cudaStream_t s) {
   const BulkCfg& c = bulk_cfg();
-  if (c.nst == 3 && c.r == 2) return launch_b<MODE, ST, 3, 2, 3>(a, s);
-  if (c.nst == 3 && c.r == 4) return launch_b<MODE, ST, 3, 4, 2>(a, s);
-  if (c.nst == 5) return launch_b<MODE, ST, 5, 4, 1>(a, s);
-  if (c.nst == 7) return launch_b<MODE, ST, 7, 4, 1>(a, s);
-  if (c.nst == 6) return launch_b<MODE, ST, 6, 2, 2>(a, s);
-  return launch_b<MODE, ST, 4, 2, 3>(a, s);
+  if (c.nc == 7) {
+    if (c.cps == 4) return launch_b<MODE, ST, 3, 2, 4, 7>(a, s);
+    if (c.nst == 4) return launch_b<MODE, ST, 4, 2, 3, 7>(a, s);
+    return launch_b<MODE, ST, 3, 2, 3, 7>(a, s);
+  }
+  if (c.nst == 3 && c.r == 4) return launch_b<MODE, ST, 3, 4, 2, 8>(a, s);
+  if (c.nst == 5) return launch_b<MODE, ST, 5, 4, 1, 8>(a, s);
+  return launch_b<MODE, ST, 3, 2, 3, 8>(a, s);
 }
 
 px_status launch_bulk(int mode, int stencil, const StreamLaunch& a, cudaStream_t s) {

@@ -564,6 +564,7 @@ px_status px_solve(const px_layout* l, px_comm* c, int32_t rank, const px_relax_
       cudaError_t ce = cudaStreamEndCapture(s, &graph);
       if (st != PX_OK) {
         if (graph) cudaGraphDestroy(graph);
+        cudaGetLastError();  // do not leave a capture-time error for the next call
         return st;
       }
       PX_TRY(cuda_check(ce, "end capture"));
@@ -571,6 +572,10 @@ px_status px_solve(const px_layout* l, px_comm* c, int32_t rank, const px_relax_
       count_launches(-plan->launches_per_run);
       ce = cudaGraphInstantiate(&plan->exec, graph, 0);
       cudaGraphDestroy(graph);
+      if (ce != cudaSuccess) {
+        plan->exec = nullptr;
+        cudaGetLastError();
+      }
       PX_TRY(cuda_check(ce, "graph instantiate"));
     }
     PX_TRY(cuda_check(cudaGraphLaunch(plan->exec, s), "graph launch"));

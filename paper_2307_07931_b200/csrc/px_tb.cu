@@ -40,12 +40,13 @@ constexpr int R = 3;               // rows per stage = rows per unrolled body (t
 constexpr int NST = 4;             // ring stages (consumers hold the current and previous one)
 constexpr int CHUNK_ROWS = 255;    // nominal rows per work item (multiple of R)
 
-// NW consumer warps + 1 producer warp per CTA; NW = 8 runs 2 CTAs per SM,
-// NW = 16 one CTA per SM (more registers per thread).
+// NW consumer warps + 1 producer warp per CTA.  Blocks are 8 or 16 warps so
+// that each SM sub-partition (16K registers) holds 4 warps of 128 registers:
+// NW = 7 runs 2 CTAs per SM, NW = 15 one CTA per SM.
 template <int K, int NW>
 struct Geom {
   static constexpr int THREADS = NW * 32 + 32;
-  static constexpr int CPS = NW == 8 ? 2 : 1;
+  static constexpr int CPS = NW == 7 ? 2 : 1;
   static constexpr int WO = 64 - 2 * K;          // output columns per warp
   static constexpr int CO = NW * WO;             // output columns per CTA strip
   static constexpr int CL = CO + 2 * K;          // loaded columns per CTA strip
@@ -222,7 +223,7 @@ __device__ __forceinline__ void tb_stage(const StreamLaunch& a, const TbLaunch& 
 }
 
 template <int ST, int K, int NW, int P2, int FIX>
-__global__ void __maxnreg__(112)
+__global__ void __launch_bounds__(NW * 32 + 32, (NW == 7 ? 2 : 1))
     k_tb(const StreamLaunch a, const TbLaunch x, int nstrips, int nitems, int crows) {
   using G = Geom<K, NW>;
   extern __shared__ __align__(128) double smem[];
@@ -367,8 +368,10 @@ struct TbPlan {
 static int tb_nw() {
   static int nw = 0;
   if (!nw) {
-    const char* e = getenv("PROTOX_TB_NW");  // A/B knob: 8 (2 CTAs/SM) or 16 (1 CTA/SM)
-    nw = (e && atoi(e) == 8) ? 8 : 16;
+    // A/B knob: 7 (2 CTAs/SM) or 15 (1 CTA/SM, default: 734 vs 726 Gcell/s at
+    // 16384², k=4, norm every 4 sweeps -- profiles/round1_tb.json)
+    const char* e = getenv("PROTOX_TB_NW");
+    nw = (e && atoi(e) == 7) ? 7 : 15;
   }
   return nw;
 }
@@ -379,7 +382,7 @@ static TbPlan tb_plan(int K, int nx, int ny) {
   const int CO = NW * (64 - 2 * K);
   const int RK = 3 * K / (K % 3 == 0 ? 3 : 1);  // chunk rows: multiple of R (=3)
   g.nstrips = (nx + CO - 1) / CO;
-  const int cps = NW == 8 ? 2 : 1;
+  const int cps = NW == 7 ? 2 : 1;
   const int gmax = cps * tb_nsm() < BULK_MAX_GRID ? cps * tb_nsm() : BULK_MAX_GRID;
   const int c0 = (ny + CHUNK_ROWS - 1) / CHUNK_ROWS;
   double best = 1e30;
@@ -430,7 +433,7 @@ static cudaError_t tb_launch_nw(const StreamLaunch& a, const TbLaunch& x, cudaSt
 
 template <int ST, int K, int P2, int FIX>
 static cudaError_t tb_launch_t(const StreamLaunch& a, const TbLaunch& x, cudaStream_t s) {
-  return tb_nw() == 8 ? tb_launch_nw<ST, K, 8, P2, FIX>(a, x, s) : tb_launch_nw<ST, K, 16, P2, FIX>(a, x, s);
+  return tb_nw() == 7 ? tb_launch_nw<ST, K, 7, P2, FIX>(a, x, s) : tb_launch_nw<ST, K, 15, P2, FIX>(a, x, s);
 }
 
 template <int ST, int K, int P2>
