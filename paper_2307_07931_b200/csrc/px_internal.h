@@ -113,6 +113,24 @@ struct TbLaunch {
 int32_t tb_blocks(int K, const StreamLaunch& a);
 px_status launch_tb(int stencil, int K, const StreamLaunch& a, const TbLaunch& x, cudaStream_t s);
 
+// A whole single-box solve in one launch (px_smallbox.cu, K9).
+struct SmallBox {
+  const double* phi_in;   // cell (0,0) of the input patch
+  double* phi_out;        // cell (0,0) of the output patch (may equal phi_in)
+  const double* rhs;      // cell (0,0) of the rhs patch
+  int64_t ld_in, ld_out, ld_rhs;
+  int nx, ny, g;
+  int bc;
+  int stencil;
+  double scale, lambda;
+  int nsweeps, every;     // norms of φ^s for s % every == 0 (every <= 0: none)
+  int final_norm;         // record the residual of φ^N
+  double* d_max;          // norm ring
+  double* d_sum;
+};
+bool smallbox_fits(int nx, int ny);
+px_status launch_smallbox(const SmallBox& b, cudaStream_t s);
+
 // upper bound of the thread blocks a relax/residual launch over a region uses
 constexpr int32_t BULK_MAX_GRID = 512;
 int32_t stream_blocks(int32_t nx, int32_t ny, int32_t phase);

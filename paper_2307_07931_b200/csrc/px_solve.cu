@@ -275,11 +275,50 @@ static px_status copy_face_ghosts(const px_layout* l, int32_t rank, const px_pat
   return PX_OK;
 }
 
+// Whole single-box solve in one launch (K9) when the box fits in shared memory.
+static bool smallbox_path(const SolveCtx& x) {
+  if (x.c || x.nparts != 1 || x.l->nranks != 1 || x.l->ghost != 1) return false;
+  if (x.o->temporal_k > 1) return false;
+  const int32_t nx = ext(x.l->domain, 0), ny = ext(x.l->domain, 1);
+  return nx * ny <= 16384 && smallbox_fits(nx, ny);
+}
+
+static px_status enqueue_smallbox(const SolveCtx& x) {
+  px_local_info li;
+  PX_TRY(local_info(x.l, 0, &li));
+  const int32_t N = x.o->nsweeps, E = x.o->norm_every;
+  SmallBox b;
+  std::memset(&b, 0, sizeof b);
+  const int32_t x0 = li.owned.lo.c[0], y0 = li.owned.lo.c[1];
+  const px_patch& out = (N % 2) ? x.scr[0] : x.phi[0];  // the buffer the sweep-by-sweep path ends in
+  b.phi_in = at(x.phi[0], x0, y0);
+  b.phi_out = at(out, x0, y0);
+  b.rhs = at(x.rhs[0], x0, y0);
+  b.ld_in = x.phi[0].ld;
+  b.ld_out = out.ld;
+  b.ld_rhs = x.rhs[0].ld;
+  b.nx = ext(li.owned, 0);
+  b.ny = ext(li.owned, 1);
+  b.g = 1;
+  b.bc = x.l->bc;
+  b.stencil = x.p->stencil;
+  b.scale = stencil_scale(x.p->stencil, x.p->h);
+  b.lambda = x.p->lambda;
+  b.nsweeps = N;
+  b.every = E;
+  b.final_norm = E >= 0;
+  b.d_max = x.plan->d_max;
+  b.d_sum = x.plan->d_sum;
+  if (!contains(x.rhs[0].box, li.owned)) return fail(PX_ERR_SHAPE, "rhs does not cover the box");
+  return launch_smallbox(b, x.s);
+}
+
 // Enqueue the whole solve on x.s (directly, or under graph capture).
 static px_status enqueue_solve(const SolveCtx& x) {
   const int32_t N = x.o->nsweeps, E = x.o->norm_every;
   Plan* plan = x.plan;
   const bool nccl_multi = x.c && x.l->nranks > 1;
+  if (smallbox_path(x)) return enqueue_smallbox(x);
   // exchange ghosts of φ^0
   PX_TRY(exchange_all(x, x.phi));
   // FIXED_GHOSTS: the caller's ghost cells at domain faces belong to every

@@ -490,3 +490,35 @@ def test_relax_block_bitwise(k, st):
     assert bits_equal(out, ref[g:-g, g:-g]), ulp_diff(out, ref[g:-g, g:-g])
     assert nb[0].item() == rn[0, 0]
     assert abs(nb[1].item() - rn[0, 1]) <= SUM_RTOL * rn[0, 1]
+
+
+@pytest.mark.parametrize("st", [P.PX_LAPLACE_5PT, P.PX_MEHRSTELLEN_9PT])
+def test_truncation_ladder_matches_oracle(st):
+    """BASELINE config 5 ladder at oracle-feasible sizes: τ_h from the GPU
+    residual kernel equals the oracle's (max-norm bit for bit), ratio 4 / 16."""
+    taus = []
+    for n in (15, 31, 63, 127):
+        h = 1.0 / (n + 1)
+        xi = np.arange(-1, n + 1) * h + h
+        X, Y = np.meshgrid(xi, xi, indexing="xy")
+        phi = np.cos(np.pi * X) * np.sin(np.pi * Y) * np.exp(Y)
+        lap = -np.pi**2 * phi + np.cos(np.pi * X) * ((1 - np.pi**2) * np.sin(np.pi * Y) * np.exp(Y)
+                                                    + 2 * np.pi * np.cos(np.pi * Y) * np.exp(Y))
+        lay = P.Layout(P.box(0, 0, n - 1, n - 1), (n, n), 1, P.PX_BC_FIXED_GHOSTS, 1)
+        a, r = lay.alloc(0), lay.alloc(0)
+        lay.view(0, a, ghosts=True).copy_(torch.from_numpy(phi))
+        lay.view(0, r, ghosts=True).copy_(torch.from_numpy(lap))
+        rhs = r
+        if st == 1:
+            rhs = lay.alloc(0)
+            P.mehrstellen_rhs(lay.patch(0, r), lay.patch(0, rhs), lay.local(0).owned)
+        nb = P.norm_buffer(lay.local(0).owned)
+        P.residual_norm(P.relax_params(h, 0.0, st), lay.patch(0, a), lay.patch(0, rhs), lay.local(0).owned, nb)
+        torch.cuda.synchronize()
+        ref = oracle.residual(oracle.Problem(n, n, h, 0.0, bc=oracle.BC_FIXED, stencil=st, rhs_correction=(st == 1)),
+                              phi, lap)
+        assert nb[0].item() == ref[0]
+        taus.append(ref[0])
+    ratios = [taus[i] / taus[i + 1] for i in range(3)]
+    lo, hi = (3.8, 4.2) if st == 0 else (14.0, 17.5)
+    assert all(lo < q < hi for q in ratios), ratios
