@@ -33,17 +33,39 @@ constexpr int SW_ROWS = 32;
 constexpr int SW_PF = 4;                  // prefetch distance in rows (= ring slots)
 constexpr unsigned FULL = 0xffffffffu;
 
+static int ldg_nsm() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
+  }
+  return n;
+}
+
+// Rows per CTA: SW_ROWS, reduced in steps of SW_PF (down to SW_PF) until the
+// grid has >= 4 CTAs per SM -- small (L2-resident) problems such as 1024²
+// would otherwise leave most SMs idle.
+static int32_t ldg_rows(int32_t nx, int32_t ny, int32_t phase) {
+  const int64_t gx = (nx + phase + SW_COLS - 1) / SW_COLS;
+  const int64_t target = 4 * (int64_t)ldg_nsm();
+  int32_t rows = SW_ROWS;
+  while (rows > SW_PF && gx * ((ny + rows - 1) / rows) < target) rows -= SW_PF;
+  return rows;
+}
+
 static int32_t ldg_blocks(int32_t nx, int32_t ny, int32_t phase) {
   if (nx <= 0 || ny <= 0) return 0;
-  int32_t gx = (nx + phase + SW_COLS - 1) / SW_COLS;
-  int32_t gy = (ny + SW_ROWS - 1) / SW_ROWS;
-  return gx * gy;
+  const int32_t rows = ldg_rows(nx, ny, phase);
+  return ((nx + phase + SW_COLS - 1) / SW_COLS) * ((ny + rows - 1) / rows);
 }
 
 // upper bound of the blocks any relax/residual launch over the region uses
-// (sizes norm buffers; host-only)
+// (sizes norm buffers; host-only: no device query)
 int32_t stream_blocks(int32_t nx, int32_t ny, int32_t phase) {
-  const int32_t b = ldg_blocks(nx, ny, phase);
+  if (nx <= 0 || ny <= 0) return BULK_MAX_GRID;
+  const int32_t b = ((nx + phase + SW_COLS - 1) / SW_COLS) * ((ny + SW_PF - 1) / SW_PF);
   return b > BULK_MAX_GRID ? b : BULK_MAX_GRID;
 }
 
@@ -125,11 +147,11 @@ __device__ __forceinline__ void taps(const Fin& S, const Fin& C, const Fin& N, d
 
 // ------------------------------------------------------- the stream kernel
 template <int MODE, int ST>
-__global__ void __launch_bounds__(SW_THREADS, 2) k_stream(const StreamLaunch a) {
+__global__ void __launch_bounds__(SW_THREADS, 2) k_stream(const StreamLaunch a, const int rows) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = -a.phase + (blockIdx.x * SW_WARPS + warp) * 64 + 2 * lane;
-  const int r0 = blockIdx.y * SW_ROWS;
-  const int rend = min(a.ny, r0 + SW_ROWS);   // rows computed: [r0, rend)
+  const int r0 = blockIdx.y * rows;
+  const int rend = min(a.ny, r0 + rows);      // rows computed: [r0, rend)
   const int rlast = rend;                      // last φ row needed (N of rend-1)
   const bool need_rhs = (MODE == MODE_RELAX || MODE == MODE_RESID);
   const bool warp_live = (-a.phase + (int)(blockIdx.x * SW_WARPS + warp) * 64) < a.nx;
@@ -167,7 +189,7 @@ __global__ void __launch_bounds__(SW_THREADS, 2) k_stream(const StreamLaunch a) 
     }
 
 #pragma unroll 1
-    for (int i0 = 0; i0 < SW_ROWS; i0 += SW_PF) {
+    for (int i0 = 0; i0 < rows; i0 += SW_PF) {
 #pragma unroll
     for (int jj = 0; jj < SW_PF; ++jj) {
       const int i = i0 + jj;
@@ -244,13 +266,14 @@ px_status cuda_check(cudaError_t e, const char* what) {
 
 template <int MODE, int ST>
 static void launch_t(const StreamLaunch& a, dim3 grid, cudaStream_t s) {
-  k_stream<MODE, ST><<<grid, SW_THREADS, 0, s>>>(a);
+  k_stream<MODE, ST><<<grid, SW_THREADS, 0, s>>>(a, ldg_rows(a.nx, a.ny, a.phase));
 }
 
 px_status launch_stream(int mode, int stencil, const StreamLaunch& a, cudaStream_t s) {
   if (a.nx <= 0 || a.ny <= 0) return PX_OK;
   if (bulk_eligible(mode, a)) return launch_bulk(mode, stencil, a, s);
-  dim3 grid((a.nx + a.phase + SW_COLS - 1) / SW_COLS, (a.ny + SW_ROWS - 1) / SW_ROWS);
+  const int32_t rows = ldg_rows(a.nx, a.ny, a.phase);
+  dim3 grid((a.nx + a.phase + SW_COLS - 1) / SW_COLS, (a.ny + rows - 1) / rows);
   if (grid.y > 65535) return fail(PX_ERR_UNSUPPORTED, "region too tall (%d rows)", a.ny);
   switch (mode * 2 + stencil) {
     case MODE_RELAX * 2 + 0: launch_t<MODE_RELAX, 0>(a, grid, s); break;

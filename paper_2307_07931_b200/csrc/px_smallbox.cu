@@ -115,18 +115,26 @@ __global__ void __launch_bounds__(SB_THREADS, 1) k_smallbox(const SmallBox b) {
   __syncthreads();
   const double scale = b.scale, lambda = b.lambda;
   int entry = 0;
+  // thread -> fixed column, rows strided: no integer division in the sweep loop
+  const int tpr = b.nx < nt ? b.nx : nt;           // threads per row
+  const int rstride = nt / tpr;                    // rows handled per pass
+  const int tx = tid % tpr, ty = tid / tpr;
+  const bool active = ty < rstride;
   for (int s = 0; s < b.nsweeps; ++s) {
     const bool rec = b.every > 0 && s % b.every == 0;
     unsigned long long mx = 0ull;
     double ss = 0.0;
-    for (int k = tid; k < ncell; k += nt) {
-      const int x = k % b.nx, y = k / b.nx;
-      const int i = (x + 1) + (y + 1) * P;
-      const double L = sb_taps<ST>(A, P, i);
-      const double r = __dsub_rn(__dmul_rn(scale, L), F[k]);
-      B[i] = __dadd_rn(A[i], __dmul_rn(lambda, r));
-      mx = umax64(mx, (unsigned long long)__double_as_longlong(fabs(r)));
-      ss = fma(r, r, ss);
+    if (active) {
+      for (int y = ty; y < b.ny; y += rstride) {
+        for (int x = tx; x < b.nx; x += tpr) {
+          const int i = (x + 1) + (y + 1) * P;
+          const double L = sb_taps<ST>(A, P, i);
+          const double r = __dsub_rn(__dmul_rn(scale, L), F[x + y * b.nx]);
+          B[i] = __dadd_rn(A[i], __dmul_rn(lambda, r));
+          mx = umax64(mx, (unsigned long long)__double_as_longlong(fabs(r)));
+          ss = fma(r, r, ss);
+        }
+      }
     }
     __syncthreads();
     fill_ring(B);
