@@ -129,6 +129,20 @@ struct SmallBox {
   double* d_sum;
 };
 bool smallbox_fits(int nx, int ny);
+
+// All sweeps of a single-rank solve in one cooperative launch (px_kernels.cu).
+struct PersistLaunch {
+  StreamLaunch a0, a1;     // RELAX A -> B (even sweeps), B -> A (odd sweeps)
+  StreamLaunch r0, r1;     // RESID on A, on B (final residual)
+  int nsweeps, every, final_norm;
+  double* d_max;
+  double* d_sum;
+  double* partials;        // 2 x 2 x grid doubles
+  int rows, gx, gy;        // tile grid (SW_COLS columns x rows)
+};
+int32_t persist_rows(int32_t nx, int32_t ny, int32_t grid);
+int32_t persist_grid();
+px_status launch_persist(int stencil, const PersistLaunch& p, int grid, cudaStream_t s);
 px_status launch_smallbox(const SmallBox& b, cudaStream_t s);
 
 // upper bound of the thread blocks a relax/residual launch over a region uses

@@ -21,8 +21,12 @@
 #include <climits>
 #include <cstdint>
 
+#include <cooperative_groups.h>
+
 #include "px_internal.h"
 #include "px_device.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace px {
 
@@ -146,18 +150,18 @@ __device__ __forceinline__ void taps(const Fin& S, const Fin& C, const Fin& N, d
 }
 
 // ------------------------------------------------------- the stream kernel
+// One tile (column group bx x row chunk by) of a sweep; accumulates the
+// residual norms of the tile's cells into mx / ss.
 template <int MODE, int ST>
-__global__ void __launch_bounds__(SW_THREADS, 2) k_stream(const StreamLaunch a, const int rows) {
+__device__ __forceinline__ void stream_tile(const StreamLaunch& a, const int bx, const int by, const int rows,
+                                            unsigned long long& mx, double& ss) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int c = -a.phase + (blockIdx.x * SW_WARPS + warp) * 64 + 2 * lane;
-  const int r0 = blockIdx.y * rows;
+  const int c = -a.phase + (bx * SW_WARPS + warp) * 64 + 2 * lane;
+  const int r0 = by * rows;
   const int rend = min(a.ny, r0 + rows);      // rows computed: [r0, rend)
   const int rlast = rend;                      // last φ row needed (N of rend-1)
   const bool need_rhs = (MODE == MODE_RELAX || MODE == MODE_RESID);
-  const bool warp_live = (-a.phase + (int)(blockIdx.x * SW_WARPS + warp) * 64) < a.nx;
-
-  unsigned long long mx = 0ull;
-  double ss = 0.0;
+  const bool warp_live = (-a.phase + (int)(bx * SW_WARPS + warp) * 64) < a.nx;
 
   if (warp_live) {
     // Ring of SW_PF raw φ rows and SW_PF rhs rows in flight.  φ row
@@ -251,8 +255,110 @@ __global__ void __launch_bounds__(SW_THREADS, 2) k_stream(const StreamLaunch a, 
     }
     }
   }
+}
+
+template <int MODE, int ST>
+__global__ void __launch_bounds__(SW_THREADS, 2) k_stream(const StreamLaunch a, const int rows) {
+  unsigned long long mx = 0ull;
+  double ss = 0.0;
+  stream_tile<MODE, ST>(a, blockIdx.x, blockIdx.y, rows, mx, ss);
   if (MODE == MODE_RELAX || MODE == MODE_RESID) {
     if (a.norms.out_max) reduce_norms(a.norms, mx, ss);
+  }
+}
+
+// Block 0 reduces n per-CTA partials in fixed order into *out_max / *out_sum.
+__device__ void reduce_partials(const double* part, int n, double* out_max, double* out_sum,
+                                unsigned long long* s_mx, double* s_ss) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long m = 0ull;
+  double t = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    m = umax64(m, (unsigned long long)__double_as_longlong(__ldcg(part + 2 * i)));
+    t = t + __ldcg(part + 2 * i + 1);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    m = umax64(m, __shfl_xor_sync(FULL_MASK, m, o));
+    t = t + __shfl_xor_sync(FULL_MASK, t, o);
+  }
+  if (lane == 0) {
+    s_mx[warp] = m;
+    s_ss[warp] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    m = s_mx[0];
+    t = s_ss[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      m = umax64(m, s_mx[w]);
+      t = t + s_ss[w];
+    }
+    *out_max = __longlong_as_double((long long)m);
+    *out_sum = t;
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------- persistent whole-solve kernel
+// All sweeps of a single-rank solve in ONE cooperative launch (C2-sized,
+// L2-resident problems, where one launch per sweep is latency): each CTA
+// sweeps its tiles, then the grid synchronises (the fused ghost images of
+// the new iterate become visible) and the two buffers swap.  Norms of a
+// recorded sweep: each CTA's fixed-order partial, then CTA 0 reduces them in
+// fixed order after the barrier (partials double-buffered by entry parity).
+template <int ST>
+__global__ void __launch_bounds__(SW_THREADS, 2) k_persist(const PersistLaunch p) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ unsigned long long s_mx[32];
+  __shared__ double s_ss[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ntiles = p.gx * p.gy;
+  auto block_partial = [&](unsigned long long mx, double ss, double* part) {
+    for (int o = 16; o > 0; o >>= 1) {
+      mx = umax64(mx, __shfl_xor_sync(FULL_MASK, mx, o));
+      ss = ss + __shfl_xor_sync(FULL_MASK, ss, o);
+    }
+    if (lane == 0) {
+      s_mx[warp] = mx;
+      s_ss[warp] = ss;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long m = s_mx[0];
+      double t = s_ss[0];
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+        m = umax64(m, s_mx[w]);
+        t = t + s_ss[w];
+      }
+      part[2 * blockIdx.x] = __longlong_as_double((long long)m);
+      part[2 * blockIdx.x + 1] = t;
+    }
+    __syncthreads();
+  };
+  int entry = 0;
+  for (int s = 0; s < p.nsweeps; ++s) {
+    const StreamLaunch& a = (s & 1) ? p.a1 : p.a0;
+    const bool rec = p.every > 0 && s % p.every == 0;
+    unsigned long long mx = 0ull;
+    double ss = 0.0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) stream_tile<MODE_RELAX, ST>(a, t % p.gx, t / p.gx, p.rows, mx, ss);
+    double* part = p.partials + (size_t)(entry & 1) * 2 * gridDim.x;
+    if (rec) block_partial(mx, ss, part);
+    grid.sync();
+    if (rec) {
+      if (blockIdx.x == 0) reduce_partials(part, gridDim.x, p.d_max + entry, p.d_sum + entry, s_mx, s_ss);
+      ++entry;
+    }
+  }
+  if (p.final_norm) {
+    const StreamLaunch& a = (p.nsweeps & 1) ? p.r1 : p.r0;
+    unsigned long long mx = 0ull;
+    double ss = 0.0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) stream_tile<MODE_RESID, ST>(a, t % p.gx, t / p.gx, p.rows, mx, ss);
+    double* part = p.partials + (size_t)(entry & 1) * 2 * gridDim.x;
+    block_partial(mx, ss, part);
+    grid.sync();
+    if (blockIdx.x == 0) reduce_partials(part, gridDim.x, p.d_max + entry, p.d_sum + entry, s_mx, s_ss);
   }
 }
 
@@ -287,6 +393,47 @@ px_status launch_stream(int mode, int stencil, const StreamLaunch& a, cudaStream
   }
   count_launches(1);
   return cuda_check(cudaGetLastError(), "stream kernel launch");
+}
+
+int32_t persist_rows(int32_t nx, int32_t ny, int32_t grid) {
+  const int64_t gx = (nx + SW_COLS - 1) / SW_COLS;
+  int32_t rows = (int32_t)((gx * ny + grid - 1) / grid);
+  rows = (rows + SW_PF - 1) / SW_PF * SW_PF;
+  return rows < SW_PF ? SW_PF : rows;
+}
+
+// co-resident grid of the persistent kernel (cooperative launch limit)
+int32_t persist_grid() {
+  static int g = 0;
+  if (!g) {
+    int per = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_persist<0>, SW_THREADS, 0) != cudaSuccess ||
+        per < 1)
+      per = 1;
+    int per9 = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per9, k_persist<1>, SW_THREADS, 0) != cudaSuccess ||
+        per9 < 1)
+      per9 = 1;
+    g = ldg_nsm() * (per < per9 ? per : per9);
+  }
+  return g;
+}
+
+px_status launch_persist(int stencil, const PersistLaunch& p, int grid, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(SW_THREADS);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = stencil ? cudaLaunchKernelEx(&cfg, k_persist<1>, p) : cudaLaunchKernelEx(&cfg, k_persist<0>, p);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  count_launches(1);
+  return cuda_check(e, "persistent solve kernel launch");
 }
 
 // ------------------------------------------------------------ ghost fill

@@ -332,6 +332,37 @@ static px_status enqueue_solve(const SolveCtx& x) {
   const int32_t K = x.o->temporal_k > 1 ? x.o->temporal_k : 1;
   int32_t it = 0;
   // temporal blocking: K sweeps per pass, ghost exchange every K sweeps
+  // single-rank problems below the TMA kernel's size: all sweeps in one
+  // cooperative launch (launch latency would dominate one kernel per sweep)
+  if (K == 1 && !x.c && x.nparts == 1 && x.l->nranks == 1 && N > 0) {
+    px_local_info li;
+    PX_TRY(local_info(x.l, 0, &li));
+    const int32_t nx = ext(li.owned, 0), ny = ext(li.owned, 1);
+    if ((int64_t)nx * ny < (int64_t)4 * 1024 * 1024) {
+      PersistLaunch pl;
+      std::memset(&pl, 0, sizeof pl);
+      const double scale = stencil_scale(x.p->stencil, x.p->h);
+      px_patch A = x.phi[0], B = x.scr[0];
+      PX_TRY(make_stream_launch(MODE_RELAX, x.p->stencil, scale, x.p->lambda, &A, &x.rhs[0], &B, li.owned, &pl.a0));
+      PX_TRY(make_stream_launch(MODE_RELAX, x.p->stencil, scale, x.p->lambda, &B, &x.rhs[0], &A, li.owned, &pl.a1));
+      PX_TRY(make_stream_launch(MODE_RESID, x.p->stencil, scale, 0.0, &A, &x.rhs[0], nullptr, li.owned, &pl.r0));
+      PX_TRY(make_stream_launch(MODE_RESID, x.p->stencil, scale, 0.0, &B, &x.rhs[0], nullptr, li.owned, &pl.r1));
+      if (pl.a0.phase == pl.a1.phase) {
+        pl.a0.gs = pl.a1.gs = ghost_spec(x.l, li, li.owned, true);
+        const int32_t grid = persist_grid();
+        pl.nsweeps = N;
+        pl.every = E;
+        pl.final_norm = E >= 0;
+        pl.d_max = plan->d_max;
+        pl.d_sum = plan->d_sum;
+        pl.partials = ws_region(plan, 0);
+        pl.gx = (nx + pl.a0.phase + 511) / 512;
+        pl.rows = persist_rows(nx + pl.a0.phase, ny, grid);
+        pl.gy = (ny + pl.rows - 1) / pl.rows;
+        return launch_persist(x.p->stencil, pl, grid, x.s);
+      }
+    }
+  }
   while (K > 1 && it + K <= N) {
     std::vector<StreamLaunch> la(x.nparts);
     std::vector<TbLaunch> tl(x.nparts);
@@ -581,7 +612,7 @@ px_status px_solve(const px_layout* l, px_comm* c, int32_t rank, const px_relax_
       // split launches add at most 2 extra partial rows of blocks
       maxblocks += stream_blocks(ext(lj.owned, 0), ext(lj.owned, 1), 1) + 2 * stream_blocks(ext(lj.owned, 0), 1, 1);
     }
-    np->ws_stride = 2 + 2 * maxblocks;
+    np->ws_stride = std::max<int64_t>(2 + 2 * maxblocks, 4 * 1024);  // >= 4 x persistent grid
     np->ws_len = np->ws_stride * (o->temporal_k > 1 ? o->temporal_k : 1);
     PX_TRY(cuda_check(cudaMalloc(&np->d_max, ne * sizeof(double)), "cudaMalloc ring"));
     PX_TRY(cuda_check(cudaMalloc(&np->d_sum, ne * sizeof(double)), "cudaMalloc ring"));
