@@ -274,6 +274,9 @@ __global__ void __launch_bounds__(NC * 32 + 32, CPS) k_bulk(const StreamLaunch a
           w_s = w_c; a_s = a_c; b_s = b_c; e_s = e_c;
           w_c = w_n; a_c = a_n; b_c = b_n; e_c = e_n;
         }
+        // order this warp's shared-memory reads of the stage before the
+        // producer's next TMA write into it (generic -> async proxy)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
         if (++slot == NST) {

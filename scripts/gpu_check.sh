@@ -1,7 +1,6 @@
 #!/bin/bash
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
-timeout 1800 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
-for c in C1 C2; do
-  timeout 900 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err
-done
+CS=/usr/local/cuda/bin/compute-sanitizer
+timeout 900 $CS --tool racecheck --print-limit 10 python scripts/sanitize_cases.py bulk_relax > gpurun_out/sanitize_racecheck_bulk.log 2>&1
+timeout 200 python scripts/ab_relax.py --n 16384 --reps 25 > gpurun_out/ab_fence.jsonl 2>&1

@@ -1,0 +1,87 @@
+"""Small invocations of every libprotox kernel, for compute-sanitizer
+(memcheck / racecheck / synccheck / initcheck):
+
+    compute-sanitizer --tool memcheck python scripts/sanitize_cases.py
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np
+import torch
+
+from paper_2307_07931_b200 import inputs
+from paper_2307_07931_b200 import protox as P
+
+
+def fields(lay, rank=0):
+    a, b, r = lay.alloc(rank), lay.alloc(rank), lay.alloc(rank)
+    P.init_field(lay, rank, lay.patch(rank, r), P.PX_FIELD_HASH, 1)
+    P.init_field(lay, rank, lay.patch(rank, a), P.PX_FIELD_HASH, 2)
+    return a, b, r
+
+
+def case(name, fn):
+    fn()
+    torch.cuda.synchronize()
+    print("ok", name, flush=True)
+
+
+def relax(n0, n1, g=1, st=0, bc=P.PX_BC_PERIODIC, k=1):
+    lay = P.Layout(P.box(0, 0, n0 - 1, n1 - 1), (n0, n1), g, bc, 1)
+    a, b, r = fields(lay)
+    P.fill_ghosts(lay, 0, lay.patch(0, a))
+    P.fill_ghosts(lay, 0, lay.patch(0, r))
+    nb = P.norm_buffer(lay.local(0).owned)
+    prm = P.relax_params(1.0 / n0, (1.0 / n0) ** 2 / 8, st)
+    if k == 1:
+        P.relax_step(prm, lay.patch(0, a), lay.patch(0, b), lay.patch(0, r), lay.local(0).owned, nb)
+        P.residual_norm(prm, lay.patch(0, a), lay.patch(0, r), lay.local(0).owned, nb)
+    else:
+        P.relax_block(prm, k, lay.patch(0, a), lay.patch(0, b), lay.patch(0, r), lay.local(0).owned, nb)
+
+
+def solve(n0, n1, nranks=1, g=1, st=0, bc=P.PX_BC_PERIODIC, N=5, E=2, tk=1, graph=False):
+    lay = P.Layout(P.box(0, 0, n0 - 1, n1 - 1), (n0, n1 // nranks), g, bc, nranks)
+    parts = [fields(lay, r) for r in range(nranks)]
+    if tk > 1:
+        P.exchange_ghosts_local(lay, [lay.patch(r, parts[r][2]) for r in range(nranks)])
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    P.solve(lay, None, 0, P.relax_params(1.0 / n0, (1.0 / n0) ** 2 / 8, st), N, E,
+            [lay.patch(r, p[0]) for r, p in enumerate(parts)], [lay.patch(r, p[1]) for r, p in enumerate(parts)],
+            [lay.patch(r, p[2]) for r, p in enumerate(parts)], temporal_k=tk, use_graph=graph, stream=s)
+
+
+def other():
+    lay = P.Layout(P.box(0, 0, 199, 99), (200, 100), 1, P.PX_BC_DIRICHLET_CC, 1)
+    a, b, r = fields(lay)
+    P.fill_ghosts(lay, 0, lay.patch(0, a))
+    P.mehrstellen_rhs(lay.patch(0, a), lay.patch(0, b), lay.local(0).owned)
+    P.stencil_apply(1, 2.0, lay.patch(0, a), lay.patch(0, b), lay.local(0).owned)
+    x = torch.rand(4096, dtype=torch.float64, device="cuda")
+    y = torch.rand(4096, dtype=torch.float64, device="cuda")
+    z = torch.empty(4096, dtype=torch.float64, device="cuda")
+    P.stream_ceiling(x, y, z, 0)
+    P.stream_ceiling(x, None, z, 1)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1] if len(sys.argv) > 1 else "all"
+    cases = {
+        "ldg_relax": lambda: relax(300, 70, st=0),
+        "ldg_relax9": lambda: relax(130, 41, st=1, bc=P.PX_BC_DIRICHLET_CC),
+        "bulk_relax": lambda: relax(2048, 2048),
+        "bulk_relax9": lambda: relax(2050, 2048, st=1),
+        "tb_relax_block": lambda: relax(1000, 300, g=4, k=4),
+        "smallbox_solve": lambda: solve(64, 64, bc=P.PX_BC_DIRICHLET_CC),
+        "persist_solve": lambda: solve(600, 90, st=1),
+        "local_multipart_solve": lambda: solve(256, 150, nranks=3, bc=P.PX_BC_FIXED_GHOSTS),
+        "tb_solve": lambda: solve(1000, 300, nranks=3, g=4, tk=4, N=9, E=3),
+        "graph_solve": lambda: solve(600, 90, N=4, E=1, graph=True),
+        "other_kernels": other,
+    }
+    for name, fn in cases.items():
+        if which in ("all", name):
+            case(name, fn)
