@@ -18,6 +18,7 @@
 // a chunk is re-read once per chunk (2 rows per CHUNK_ROWS).
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdint>
 #include <cstdlib>
 
@@ -102,10 +103,13 @@ using namespace bulk;
 
 
 // NST stages of R rows per CTA, CPS CTAs per SM.
-template <int MODE, int ST, int NST, int R, int CPS, int NC>
+// PW bit 0: scale is a power of two, bit 1: λ is a power of two (exact
+// products, so fused multiply-adds are bit-identical to the separate ops).
+template <int MODE, int ST, int NST, int R, int CPS, int NC, int PW>
 __global__ void __launch_bounds__(NC * 32 + 32, CPS) k_bulk(const StreamLaunch a, int nstrips, int nitems,
                                                             int crows) {
   constexpr int W = 64 * NC, NCW = NC;
+  constexpr bool P2 = (PW & 1) != 0, PL = (PW & 2) != 0;
   constexpr int STAGE_DOUBLES = R * 2 * W;
   extern __shared__ __align__(128) double smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NST * STAGE_DOUBLES);
@@ -229,23 +233,24 @@ __global__ void __launch_bounds__(NC * 32 + 32, CPS) k_bulk(const StreamLaunch a
           if (r >= t.y0 && live) {
             double L0, L1;
             if (ST == 0) {
-              L0 = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(w_c, b_c), a_s), a_n), __dmul_rn(-4.0, a_c));
-              L1 = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(a_c, e_c), b_s), b_n), __dmul_rn(-4.0, b_c));
+              // -4·C is exact, so the fused multiply-add rounds like the separate ops
+              L0 = fma(-4.0, a_c, __dadd_rn(__dadd_rn(__dadd_rn(w_c, b_c), a_s), a_n));
+              L1 = fma(-4.0, b_c, __dadd_rn(__dadd_rn(__dadd_rn(a_c, e_c), b_s), b_n));
             } else {
               double q;
               q = __dmul_rn(4.0, w_c);
-              q = __dadd_rn(q, __dmul_rn(4.0, b_c));
-              q = __dadd_rn(q, __dmul_rn(4.0, a_s));
-              q = __dadd_rn(q, __dmul_rn(4.0, a_n));
+              q = fma(4.0, b_c, q);  // 4·x exact: fma == separate ops
+              q = fma(4.0, a_s, q);
+              q = fma(4.0, a_n, q);
               q = __dadd_rn(q, w_s);
               q = __dadd_rn(q, b_s);
               q = __dadd_rn(q, w_n);
               q = __dadd_rn(q, b_n);
               L0 = __dadd_rn(q, __dmul_rn(-20.0, a_c));
               q = __dmul_rn(4.0, a_c);
-              q = __dadd_rn(q, __dmul_rn(4.0, e_c));
-              q = __dadd_rn(q, __dmul_rn(4.0, b_s));
-              q = __dadd_rn(q, __dmul_rn(4.0, b_n));
+              q = fma(4.0, e_c, q);
+              q = fma(4.0, b_s, q);
+              q = fma(4.0, b_n, q);
               q = __dadd_rn(q, a_s);
               q = __dadd_rn(q, e_s);
               q = __dadd_rn(q, a_n);
@@ -253,15 +258,16 @@ __global__ void __launch_bounds__(NC * 32 + 32, CPS) k_bulk(const StreamLaunch a
               L1 = __dadd_rn(q, __dmul_rn(-20.0, b_c));
             }
             const double2 f = *reinterpret_cast<const double2*>(sp + (R + i) * W + c0);
-            const double d0 = __dmul_rn(a.scale, L0), d1 = __dmul_rn(a.scale, L1);
-            const double e0 = __dsub_rn(d0, f.x), e1 = __dsub_rn(d1, f.y);
+            // scale, λ powers of two (P2): the products are exact, fma rounds like the separate ops
+            const double e0 = P2 ? fma(a.scale, L0, -f.x) : __dsub_rn(__dmul_rn(a.scale, L0), f.x);
+            const double e1 = P2 ? fma(a.scale, L1, -f.y) : __dsub_rn(__dmul_rn(a.scale, L1), f.y);
             mx = umax64(mx, (unsigned long long)__double_as_longlong(fabs(e0)));
             mx = umax64(mx, (unsigned long long)__double_as_longlong(fabs(e1)));
             ss = fma(e0, e0, ss);
             ss = fma(e1, e1, ss);
             if (MODE == MODE_RELAX) {
-              const double o0 = __dadd_rn(a_c, __dmul_rn(a.lambda, e0));
-              const double o1 = __dadd_rn(b_c, __dmul_rn(a.lambda, e1));
+              const double o0 = PL ? fma(a.lambda, e0, a_c) : __dadd_rn(a_c, __dmul_rn(a.lambda, e0));
+              const double o1 = PL ? fma(a.lambda, e1, b_c) : __dadd_rn(b_c, __dmul_rn(a.lambda, e1));
               const int x = t.c + c0;
               double* dp = a.dst + (int64_t)r * a.ld_dst + x;
               *reinterpret_cast<double2*>(dp) = make_double2(o0, o1);
@@ -313,8 +319,7 @@ struct BulkCfg {
 // {4,2,3,7} 6136, {3,4,2,8} 5917, {5,4,1,8} 5433, {3,2,4,7} 4633 (spills).
 // 8-warp blocks (7 consumers + producer) keep 6 warps per SM sub-partition
 // at 80 registers without spills.
-static const BulkCfg kCfgs[] = {{3, 2, 3, 7}, {3, 2, 3, 8}, {3, 4, 2, 8}, {5, 4, 1, 8},
-                                 {3, 2, 4, 7}, {4, 2, 3, 7}};
+static const BulkCfg kCfgs[] = {{3, 2, 3, 7}, {3, 2, 3, 8}, {5, 4, 1, 8}};
 static const BulkCfg& bulk_cfg() {
   static int idx = -1;
   if (idx < 0) {
@@ -391,33 +396,45 @@ static BulkGeom bulk_geom(const StreamLaunch& a) {
 
 int32_t bulk_blocks(const StreamLaunch& a) { return bulk_geom(a).grid; }
 
-template <int MODE, int ST, int NST, int R, int CPS, int NC>
+template <int MODE, int ST, int NST, int R, int CPS, int NC, int PW>
 static cudaError_t launch_b(const StreamLaunch& a, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_bulk<MODE, ST, NST, R, CPS, NC>,
+    cudaError_t e = cudaFuncSetAttribute(k_bulk<MODE, ST, NST, R, CPS, NC, PW>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem_bytes<NST, R, NC>());
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const BulkGeom g = bulk_geom(a);
-  k_bulk<MODE, ST, NST, R, CPS, NC><<<g.grid, NC * 32 + 32, smem_bytes<NST, R, NC>(), s>>>(a, g.nstrips, g.nitems,
-                                                                                       g.crows);
+  k_bulk<MODE, ST, NST, R, CPS, NC, PW><<<g.grid, NC * 32 + 32, smem_bytes<NST, R, NC>(), s>>>(
+      a, g.nstrips, g.nitems, g.crows);
   return cudaGetLastError();
+}
+
+static bool is_pow2(double v) {
+  if (!(v > 0.0) || !std::isfinite(v)) return false;
+  int e;
+  return std::frexp(v, &e) == 0.5;
+}
+
+template <int MODE, int ST, int PW>
+static cudaError_t launch_pw(const StreamLaunch& a, cudaStream_t s) {
+  const BulkCfg& c = bulk_cfg();
+  if (c.nc == 8 && c.nst == 3) return launch_b<MODE, ST, 3, 2, 3, 8, PW>(a, s);
+  if (c.nst == 5) return launch_b<MODE, ST, 5, 4, 1, 8, PW>(a, s);
+  return launch_b<MODE, ST, 3, 2, 3, 7, PW>(a, s);
 }
 
 template <int MODE, int ST>
 static cudaError_t launch_cfg(const StreamLaunch& a, cudaStream_t s) {
-  const BulkCfg& c = bulk_cfg();
-  if (c.nc == 7) {
-    if (c.cps == 4) return launch_b<MODE, ST, 3, 2, 4, 7>(a, s);
-    if (c.nst == 4) return launch_b<MODE, ST, 4, 2, 3, 7>(a, s);
-    return launch_b<MODE, ST, 3, 2, 3, 7>(a, s);
+  const int pw = (is_pow2(a.scale) ? 1 : 0) | (is_pow2(a.lambda) ? 2 : 0);
+  switch (pw) {
+    case 3: return launch_pw<MODE, ST, 3>(a, s);
+    case 2: return launch_pw<MODE, ST, 2>(a, s);
+    case 1: return launch_pw<MODE, ST, 1>(a, s);
+    default: return launch_pw<MODE, ST, 0>(a, s);
   }
-  if (c.nst == 3 && c.r == 4) return launch_b<MODE, ST, 3, 4, 2, 8>(a, s);
-  if (c.nst == 5) return launch_b<MODE, ST, 5, 4, 1, 8>(a, s);
-  return launch_b<MODE, ST, 3, 2, 3, 8>(a, s);
 }
 
 px_status launch_bulk(int mode, int stencil, const StreamLaunch& a, cudaStream_t s) {

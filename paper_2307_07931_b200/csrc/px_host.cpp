@@ -186,11 +186,20 @@ px_status px_layout_patch(const px_layout* l, int32_t rank, double* alloc_base, 
 }
 
 px_status px_layout_halo_plan(const px_layout* l, int32_t rank, px_halo_op ops[4], int32_t* nops) {
+  return halo_plan(l, rank, ops, nops, false);
+}
+
+}  // extern "C"
+
+namespace px {
+// allow_self: a one-rank periodic layout exchanges with itself (used by the
+// NCCL self-exchange test mode, px_comm_create with PROTOX_NCCL_SELF_EXCHANGE=1)
+px_status halo_plan(const px_layout* l, int32_t rank, px_halo_op ops[4], int32_t* nops, bool allow_self) {
   if (!ops || !nops) return fail(PX_ERR_ARG, "null argument");
   px_local_info li;
   PX_TRY(local_info(l, rank, &li));
   *nops = 0;
-  if (l->nranks == 1) return PX_OK;
+  if (l->nranks == 1 && !(allow_self && l->bc == PX_BC_PERIODIC)) return PX_OK;
   const int32_t g = l->ghost;
   const int64_t count = (int64_t)(g - 1) * li.ld + ext(li.alloc, 0);
   auto off = [&](int32_t y) { return (int64_t)(y - li.alloc.lo.c[1]) * li.ld; };
@@ -209,6 +218,9 @@ px_status px_layout_halo_plan(const px_layout* l, int32_t rank, px_halo_op ops[4
   if (li.nbr_hi >= 0) add(li.nbr_hi, 1, li.owned.hi.c[1] + 1);
   return PX_OK;
 }
+}  // namespace px
+
+extern "C" {
 
 int64_t px_norm_buffer_len(px_box region) {
   // results (2) + counter slot (2) + 2 partials per block, for any phase

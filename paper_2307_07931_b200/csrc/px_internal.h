@@ -170,5 +170,6 @@ px_status make_stream_launch(int mode, int stencil, double scale, double lambda,
                              px_box region, StreamLaunch* a);
 double stencil_scale(int stencil, double h);
 uint64_t layout_generation(const px_layout* l);
+px_status halo_plan(const px_layout* l, int32_t rank, px_halo_op ops[4], int32_t* nops, bool allow_self);
 
 }  // namespace px

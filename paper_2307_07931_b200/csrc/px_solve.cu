@@ -19,6 +19,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -29,6 +30,7 @@ struct px_comm {
   ncclComm_t nccl = nullptr;
   int32_t nranks = 1, rank = 0, device = 0;
   cudaStream_t stream = nullptr;
+  bool self_exchange = false;  // 1 rank, periodic: exchange ghost rows with itself over NCCL (test mode)
 };
 
 namespace px {
@@ -52,11 +54,16 @@ static px_status check_rank_patch(const px_layout* l, int32_t rank, const px_pat
 
 // NCCL row exchange of one rank (y-ghost rows from the neighbours), posted
 // in the order of px_layout_halo_plan inside one group.
+// Does this (layout, communicator) pair exchange ghost rows over NCCL?
+static bool comm_exchanges(const px_layout* l, const px_comm* c) {
+  return c && (l->nranks > 1 || (c->self_exchange && l->bc == PX_BC_PERIODIC));
+}
+
 static px_status nccl_rows(const px_layout* l, px_comm* c, int32_t rank, const px_patch& p,
                            cudaStream_t s) {
   px_halo_op ops[4];
   int32_t n = 0;
-  PX_TRY(px_layout_halo_plan(l, rank, ops, &n));
+  PX_TRY(halo_plan(l, rank, ops, &n, c->self_exchange));
   PX_TRY(nccl_check(ncclGroupStart(), "ncclGroupStart"));
   for (int32_t i = 0; i < n; ++i) {
     double* buf = p.data + ops[i].offset;
@@ -203,7 +210,7 @@ static px_status build_part_launches(const SolveCtx& x, int32_t part, const px_p
     px_patch outp = out;
     PX_TRY(make_stream_launch(resid ? MODE_RESID : MODE_RELAX, x.p->stencil, scale, x.p->lambda,
                               &in, &x.rhs[part], resid ? nullptr : &outp, rg, &sl.a));
-    if (!resid) sl.a.gs = ghost_spec(x.l, li, rg, x.l->nranks == 1);
+    if (!resid) sl.a.gs = ghost_spec(x.l, li, rg, x.l->nranks == 1 && !comm_exchanges(x.l, x.c));
     sl.blocks = launch_blocks(resid ? MODE_RESID : MODE_RELAX, sl.a);
     v.push_back(sl);
   }
@@ -237,7 +244,7 @@ static void set_slot(std::vector<SweepLaunch>& v, size_t first, Plan* plan, int3
 static px_status exchange_all(const SolveCtx& x, const px_patch* parts) {
   if (x.c) {
     PX_TRY(launch_fill_ghosts(x.l, x.rank, parts[0], x.s));
-    if (x.l->nranks > 1) {
+    if (comm_exchanges(x.l, x.c)) {
       PX_TRY(cuda_check(cudaEventRecord(x.plan->ev_bnd, x.s), "event record"));
       PX_TRY(cuda_check(cudaStreamWaitEvent(x.c->stream, x.plan->ev_bnd, 0), "stream wait"));
       PX_TRY(nccl_rows(x.l, x.c, x.rank, parts[0], x.c->stream));
@@ -317,7 +324,7 @@ static px_status enqueue_smallbox(const SolveCtx& x) {
 static px_status enqueue_solve(const SolveCtx& x) {
   const int32_t N = x.o->nsweeps, E = x.o->norm_every;
   Plan* plan = x.plan;
-  const bool nccl_multi = x.c && x.l->nranks > 1;
+  const bool nccl_multi = comm_exchanges(x.l, x.c);
   if (smallbox_path(x)) return enqueue_smallbox(x);
   // exchange ghosts of φ^0
   PX_TRY(exchange_all(x, x.phi));
@@ -375,7 +382,7 @@ static px_status enqueue_solve(const SolveCtx& x) {
       px_patch outp = nxt[part];
       PX_TRY(make_stream_launch(MODE_RELAX, x.p->stencil, stencil_scale(x.p->stencil, x.p->h),
                                 x.p->lambda, &cur[part], &x.rhs[part], &outp, li.owned, &la[part]));
-      la[part].gs = ghost_spec(x.l, li, li.owned, x.l->nranks == 1);
+      la[part].gs = ghost_spec(x.l, li, li.owned, x.l->nranks == 1 && !nccl_multi);
       std::memset(&tl[part], 0, sizeof(TbLaunch));
       const bool fixed = x.l->bc == PX_BC_FIXED_GHOSTS;
       tl[part].fix[0][0] = tl[part].fix[0][1] = fixed;
@@ -487,6 +494,10 @@ px_status px_comm_create(const uint8_t id[128], int32_t nranks, int32_t rank, in
   ncclUniqueId u;
   std::memcpy(&u, id, 128);
   PX_TRY(nccl_check(ncclCommInitRank(&c->nccl, nranks, u, rank), "ncclCommInitRank"));
+  if (nranks == 1) {
+    const char* e = getenv("PROTOX_NCCL_SELF_EXCHANGE");
+    c->self_exchange = e && e[0] == '1';
+  }
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
   PX_TRY(cuda_check(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, hi),
@@ -526,7 +537,7 @@ px_status px_exchange_ghosts(const px_layout* l, px_comm* c, int32_t rank, px_pa
                 c->nranks);
   cudaStream_t s = (cudaStream_t)stream;
   PX_TRY(launch_fill_ghosts(l, rank, *phi, s));
-  if (c && l->nranks > 1) PX_TRY(nccl_rows(l, c, rank, *phi, s));
+  if (comm_exchanges(l, c)) PX_TRY(nccl_rows(l, c, rank, *phi, s));
   return PX_OK;
 }
 

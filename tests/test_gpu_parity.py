@@ -522,3 +522,51 @@ def test_truncation_ladder_matches_oracle(st):
     ratios = [taus[i] / taus[i + 1] for i in range(3)]
     lo, hi = (3.8, 4.2) if st == 0 else (14.0, 17.5)
     assert all(lo < q < hi for q in ratios), ratios
+
+
+# ------------------------------------------ NCCL path on one GPU (self-exchange)
+@pytest.mark.parametrize("tk,graph", [(1, True), (1, False), (4, True)])
+def test_nccl_self_exchange_solve(tk, graph, monkeypatch):
+    """The multi-GPU code path on one GPU: a one-rank NCCL communicator in
+    self-exchange mode sends the periodic ghost rows to itself with the
+    library's grouped send/recv (halo plan), on the comm stream, overlapped
+    with the interior kernel, captured in a CUDA graph; the norm ring goes
+    through ncclAllReduce.  Bit-identical to the oracle."""
+    monkeypatch.setenv("PROTOX_NCCL_SELF_EXCHANGE", "1")
+    n0, n1, N, E, g = 2048, 2304, 9, 2, max(1, tk)
+    h = 1.0 / 2048
+    lam = h * h / 8
+    phi0, rho = _fields(n0, n1, g, 300 + tk, P.PX_BC_PERIODIC)
+    lay = P.Layout(P.box(0, 0, n0 - 1, n1 - 1), (256, 256), g, P.PX_BC_PERIODIC, 1)
+    comm = P.Comm(P.comm_unique_id(), 1, 0, torch.cuda.current_device())
+    try:
+        a = to_device_ghosted(lay, 0, phi0, g)
+        b = lay.alloc(0)
+        r = to_device_ghosted(lay, 0, rho, g)
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        if tk > 1:
+            P.exchange_ghosts(lay, comm, 0, lay.patch(0, r), stream=s)
+        before = P.kernel_launch_count()
+        res = P.solve(lay, comm, 0, P.relax_params(h, lam), N, E, lay.patch(0, a), lay.patch(0, b),
+                      lay.patch(0, r), use_graph=graph, stream=s, temporal_k=tk)
+        assert P.kernel_launch_count() - before >= (3 * N if tk == 1 else 2)  # boundary + interior launches
+        out = owned_to_host(lay, 0, b if res.in_scratch else a)
+    finally:
+        comm.close()
+    ref, rn = oracle.solve(_orc_problem(n0, n1, h, lam, P.PX_BC_PERIODIC, 0, N, E, g=g), phi0, rho)
+    assert bits_equal(out, ref[g:-g, g:-g]), ulp_diff(out, ref[g:-g, g:-g])
+    _check_norms(res.norms, rn)
+
+
+def test_nccl_allreduce_norms_single_rank():
+    comm = P.Comm(P.comm_unique_id(), 1, 0, torch.cuda.current_device())
+    try:
+        m = torch.tensor([1.0, 3.0, float("nan")], dtype=torch.float64, device="cuda")
+        s2 = torch.tensor([2.0, 4.0, 5.0], dtype=torch.float64, device="cuda")
+        P.comm_allreduce_norms(comm, m, s2, 3)
+        torch.cuda.synchronize()
+        assert s2.tolist() == [2.0, 4.0, 5.0]
+        assert m[:2].tolist() == [1.0, 3.0]
+    finally:
+        comm.close()
