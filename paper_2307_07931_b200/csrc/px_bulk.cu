@@ -375,7 +375,9 @@ static BulkGeom bulk_geom(const StreamLaunch& a) {
   const int c0 = (a.ny + bulk_chunk() - 1) / bulk_chunk();
   double best = 1e30;
   g.nchunks = c0;
-  for (int c = c0; c <= 2 * c0 && c <= a.ny; ++c) {
+  // up to twice the nominal chunk count, or enough chunks to give every CTA an item
+  const int cmax = 2 * c0 > (gmax + g.nstrips - 1) / g.nstrips ? 2 * c0 : (gmax + g.nstrips - 1) / g.nstrips;
+  for (int c = c0; c <= cmax && c <= a.ny; ++c) {
     const int rows = (a.ny + c - 1) / c;
     const int cc = (a.ny + rows - 1) / rows;       // chunks actually produced
     const int items = g.nstrips * cc;

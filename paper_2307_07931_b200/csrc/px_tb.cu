@@ -387,7 +387,8 @@ static TbPlan tb_plan(int K, int nx, int ny) {
   const int c0 = (ny + CHUNK_ROWS - 1) / CHUNK_ROWS;
   double best = 1e30;
   int bestc = c0;
-  for (int c = c0; c <= 2 * c0 && c <= ny; ++c) {
+  const int cmax = 2 * c0 > (gmax + g.nstrips - 1) / g.nstrips ? 2 * c0 : (gmax + g.nstrips - 1) / g.nstrips;
+  for (int c = c0; c <= cmax && c <= ny; ++c) {
     int rows = (ny + c - 1) / c;
     rows = (rows + 2) / 3 * 3;  // whole stages of R = 3 rows
     const int cc = (ny + rows - 1) / rows;

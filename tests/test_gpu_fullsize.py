@@ -117,3 +117,34 @@ def test_config5_fullsize_mehrstellen_sampled_bitwise():
     g = 1 + lam * mu9
     fmax = torch.max(torch.abs(lay.view(0, f))).item()
     np.testing.assert_allclose(res.norms[:, 0], g ** np.arange(N + 1) * fmax, rtol=1e-12)
+
+
+def test_config4_fullsize_temporal_blocking_sampled_bitwise():
+    """BASELINE config 4 in the bench's launch configuration: 32768², 256²
+    boxes, ghost width 4, temporal blocking k = 4, norm every exchange,
+    CUDA graph; sampled cells bit-identical to the oracle's window runs."""
+    n, N, E, K = 32768, 100, 4, 4
+    h = 1.0 / n
+    lam = h * h / 8
+    lay = P.Layout(P.box(0, 0, n - 1, n - 1), (256, 256), K, P.PX_BC_PERIODIC, 1)
+    phi, scr, rho = lay.alloc(0), lay.alloc(0), lay.alloc(0)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    P.init_field(lay, 0, lay.patch(0, rho), P.PX_FIELD_HASH, inputs.DEFAULT_SEED, stream=s)
+    P.fill_ghosts(lay, 0, lay.patch(0, rho), stream=s)
+    res = P.solve(lay, None, 0, P.relax_params(h, lam), N, E, lay.patch(0, phi), lay.patch(0, scr),
+                  lay.patch(0, rho), use_graph=True, stream=s, temporal_k=K)
+    out = lay.view(0, scr if res.in_scratch else phi)
+    R = N
+    for (x, y) in _samples(n, 6, 11):
+        win = inputs.hash_window(n, n, x - R - 1, y - R - 1, 2 * R + 3, 2 * R + 3)
+        want = _window_value(win, N, h, lam)
+        got = out[y, x].item()
+        assert np.float64(got).view(np.uint64) == np.float64(want).view(np.uint64), (x, y, got, want)
+    rv = lay.view(0, rho)
+    assert res.norms.shape == (N // E + 1, 2)
+    assert res.norms[0, 0] == torch.max(torch.abs(rv)).item()
+    ss = torch.sum(rv * rv).item()
+    assert abs(res.norms[0, 1] - ss) <= 1e-12 * ss
+    del phi, scr, rho
+    torch.cuda.empty_cache()

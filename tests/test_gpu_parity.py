@@ -185,13 +185,13 @@ def test_solve_ragged_multibox(bc, st, graph):
     _check_norms(norms, rn)
 
 
-@pytest.mark.parametrize("nranks", [2, 3, 5])
+@pytest.mark.parametrize("nranks", [2, 3, 4, 5, 8])
 @pytest.mark.parametrize("bc", [P.PX_BC_PERIODIC, P.PX_BC_DIRICHLET_CC, P.PX_BC_FIXED_GHOSTS])
 @pytest.mark.parametrize("st", [P.PX_LAPLACE_5PT, P.PX_MEHRSTELLEN_9PT])
 def test_slab_decomposition_local_transport(nranks, bc, st):
     """Slabs of box-rows on one device exchanging by D2D copies: identical
-    to the undecomposed oracle (decomposition invariance, P12)."""
-    n0, n1, N, E = 256, 150, 12, 4
+    to the undecomposed oracle (decomposition invariance, P12), P = 2..8."""
+    n0, n1, N, E = 256, 160, 12, 4
     h = 1.0 / 256
     lam = h * h / 8 if st == 0 else 3 * h * h / 16
     phi0, rho = _fields(n0, n1, 1, 5 + nranks, bc)
