@@ -61,6 +61,9 @@ def parse():
     ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--halo", default="nccl", choices=["nccl", "p2p"],
+                    help="multi-GPU ghost exchange: NCCL grouped send/recv (default) or the fused "
+                         "peer-memory push (px_comm_enable_p2p)")
     return ap.parse_args()
 
 
@@ -232,11 +235,14 @@ def run_native(args):
             P.exchange_ghosts(lay, comm, rank, lay.patch(rank, rhs), stream=stream)
     stream.synchronize()
     pa, pb, pr = lay.patch(rank, phi), lay.patch(rank, scr), lay.patch(rank, rhs)
+    if comm is not None and args.halo == "p2p" and tk == 1:
+        P.comm_enable_p2p(comm, lay, rank, pa, pb)
 
     bufs = [pa, pb]
 
     def step():
-        # each step continues the relaxation from the previous step's iterate
+        # each step continues the relaxation from the previous step's iterate (S is even,
+        # so with k = 1 the result is back in phi and the registered p2p buffer order holds)
         r = P.solve(lay, comm, rank, prm, S, E, bufs[0], bufs[1], pr, use_graph=True, stream=stream,
                     temporal_k=tk)
         if r.in_scratch:
@@ -360,7 +366,7 @@ def run_native(args):
             "warmup": max(args.warmup, 3), "ms_per_step": t_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["desc"], "n": n, "sweeps_per_step": S, "norm_every": E,
-                       "temporal_k": tk, "ghost": ghost,
+                       "temporal_k": tk, "ghost": ghost, "halo": args.halo if world > 1 else "local",
                        "steps_continue": "each step continues from the previous step's iterate",
                        "box": box, "partition": f"slabs x{world}", "rho": cfg["rho"], "h": h, "lambda": lam,
                        "l2": "inputs (3 x %.2f GB) exceed L2; no flush" % (lay.local(0).alloc_elems * 8 / 1e9)

@@ -246,6 +246,24 @@ void px_comm_destroy(px_comm* c);
 px_status px_comm_allreduce_norms(px_comm* c, double* d_max, double* d_sum, int32_t n,
                                   void* stream);
 
+/* Fused halo push over peer memory (NVLink / NVSwitch): register this rank's
+ * two solve buffers (φ and its scratch, as later passed to px_solve) with the
+ * communicator.  The ranks exchange CUDA IPC handles of the allocations
+ * (all-gather over NCCL) and map their slab neighbours' buffers.  Afterwards
+ * px_solve (temporal_k = 1) computes each sweep's boundary rows in a kernel
+ * that also stores them -- with their x images, so corners are right --
+ * into the neighbours' ghost rows and then increments the neighbour's
+ * arrival counter (release, system scope); the next sweep's boundary kernel
+ * waits for its own counter (acquire) before reading ghost rows.  Counters
+ * are cumulative per solve epoch (never reset), so repeated solves and CUDA
+ * graph replay are safe as long as all ranks run the same sequence of
+ * solves.  No NCCL call or comm-stream hop per sweep; the norm all-reduce
+ * stays an ncclAllReduce at the end.  Collective: every rank calls it.
+ * Buffers must outlive the communicator.  A one-rank periodic layout in
+ * self-exchange mode (PROTOX_NCCL_SELF_EXCHANGE=1) pushes to itself (test). */
+px_status px_comm_enable_p2p(px_comm* c, const px_layout* l, int32_t rank, const px_patch* phi,
+                             const px_patch* phi_scratch);
+
 /* Full ghost exchange of rank `rank`'s patch: px_fill_ghosts, then the
  * y-ghost rows from the neighbour ranks over NCCL (full padded rows, so
  * corners are right).  c may be NULL only if the layout has one rank. */

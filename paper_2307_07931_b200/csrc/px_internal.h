@@ -92,6 +92,20 @@ struct NormSlot {
   int32_t expected;
 };
 
+// Fused halo push over peer memory (px_solve P2P mode): a
+// boundary-row launch also stores its cells (and their x images) into the
+// neighbour's ghost rows and then bumps the neighbour's arrival counter; a
+// launch that reads ghost rows first waits until its own arrival counter
+// reaches the expected count (epoch-based, so counters never reset).
+struct RemoteSpec {
+  double* rdst;                    // neighbour cell matching region.lo (null: no push)
+  unsigned long long* rflag;       // neighbour's arrival counter to bump
+  unsigned long long* wflag;       // own arrival counter to wait on (null: no wait)
+  const unsigned long long* epoch; // own solve epoch (1 for the first solve)
+  unsigned long long per_epoch;    // arrivals per solve
+  unsigned long long wcount;       // arrivals needed within this solve
+};
+
 struct StreamLaunch {
   const double* src;  // φ_in at region.lo
   const double* rhs;  // rhs at region.lo (may be null in APPLY mode)
@@ -103,6 +117,7 @@ struct StreamLaunch {
   double scale, lambda;
   GhostSpec gs;
   NormSlot norms;     // norms.out_max == null: none
+  RemoteSpec rs;      // fused halo push / wait (k_stream only)
 };
 
 // Extra launch state of a temporal-blocking pass (px_tb.cu).
@@ -141,6 +156,10 @@ struct PersistLaunch {
   int rows, gx, gy;        // tile grid (SW_COLS columns x rows)
 };
 int32_t persist_rows(int32_t nx, int32_t ny, int32_t grid);
+int32_t stream_launch_blocks_ldg(const StreamLaunch& a);
+px_status launch_stream_ldg(int mode, int stencil, const StreamLaunch& a, cudaStream_t s);
+px_status launch_wait(const RemoteSpec& rs, cudaStream_t s);
+px_status launch_epoch_bump(unsigned long long* epoch, cudaStream_t s);
 int32_t persist_grid();
 px_status launch_persist(int stencil, const PersistLaunch& p, int grid, cudaStream_t s);
 px_status launch_smallbox(const SmallBox& b, cudaStream_t s);

@@ -74,7 +74,7 @@ int32_t stream_blocks(int32_t nx, int32_t ny, int32_t phase) {
 }
 
 int32_t launch_blocks(int mode, const StreamLaunch& a) {
-  if (bulk_eligible(mode, a)) return bulk_blocks(a);
+  if (bulk_eligible(mode, a) && !a.rs.rdst && !a.rs.wflag) return bulk_blocks(a);
   return ldg_blocks(a.nx, a.ny, a.phase);
 }
 
@@ -150,6 +150,27 @@ __device__ __forceinline__ void taps(const Fin& S, const Fin& C, const Fin& N, d
 }
 
 // ------------------------------------------------------- the stream kernel
+// Spin until *flag >= (epoch-1)*per_epoch + count (system-scope acquire).
+__device__ __forceinline__ void rs_wait(const RemoteSpec& rs) {
+  const unsigned long long target = (*rs.epoch - 1ull) * rs.per_epoch + rs.wcount;
+  unsigned long long v;
+  do {
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(rs.wflag) : "memory");
+  } while (v < target);
+}
+
+// Store a cell (and its x images) into the neighbour's ghost rows.
+__device__ __forceinline__ void rs_push(const StreamLaunch& a, int x, int y, double v) {
+  double* rp = a.rs.rdst + (int64_t)y * a.ld_dst;
+  rp[x] = v;
+  const GhostSpec& g = a.gs;
+  const int X = x + g.o[0];
+  if (X < g.g && g.mode[0][0] != GH_NONE)
+    rp[(g.mode[0][0] == GH_WRAP ? X + g.n[0] : -X - 1) - g.o[0]] = g.mode[0][0] == GH_REFLECT ? -v : v;
+  if (X >= g.n[0] - g.g && g.mode[0][1] != GH_NONE)
+    rp[(g.mode[0][1] == GH_WRAP ? X - g.n[0] : 2 * g.n[0] - 1 - X) - g.o[0]] = g.mode[0][1] == GH_REFLECT ? -v : v;
+}
+
 // One tile (column group bx x row chunk by) of a sweep; accumulates the
 // residual norms of the tile's cells into mx / ss.
 template <int MODE, int ST>
@@ -249,6 +270,10 @@ __device__ __forceinline__ void stream_tile(const StreamLaunch& a, const int bx,
           if (va) images(a, c, r, o0);
           if (vb) images(a, c + 1, r, o1);
         }
+        if (MODE == MODE_RELAX && a.rs.rdst) {
+          if (va) rs_push(a, c, r, o0);
+          if (vb) rs_push(a, c + 1, r, o1);
+        }
       }
       fS = fC;
       fC = fN;
@@ -261,7 +286,17 @@ template <int MODE, int ST>
 __global__ void __launch_bounds__(SW_THREADS, 2) k_stream(const StreamLaunch a, const int rows) {
   unsigned long long mx = 0ull;
   double ss = 0.0;
+  if (a.rs.wflag) {  // the ghost rows this launch reads arrive over peer memory
+    if (threadIdx.x == 0) rs_wait(a.rs);
+    __syncthreads();
+  }
   stream_tile<MODE, ST>(a, blockIdx.x, blockIdx.y, rows, mx, ss);
+  if (a.rs.rdst) {   // publish this CTA's pushed cells, then count its arrival
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0)
+      asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(a.rs.rflag), "l"(1ull) : "memory");
+  }
   if (MODE == MODE_RELAX || MODE == MODE_RESID) {
     if (a.norms.out_max) reduce_norms(a.norms, mx, ss);
   }
@@ -377,7 +412,29 @@ static void launch_t(const StreamLaunch& a, dim3 grid, cudaStream_t s) {
 
 px_status launch_stream(int mode, int stencil, const StreamLaunch& a, cudaStream_t s) {
   if (a.nx <= 0 || a.ny <= 0) return PX_OK;
-  if (bulk_eligible(mode, a)) return launch_bulk(mode, stencil, a, s);
+  if (bulk_eligible(mode, a) && !a.rs.rdst && !a.rs.wflag) return launch_bulk(mode, stencil, a, s);
+  return launch_stream_ldg(mode, stencil, a, s);
+}
+
+int32_t stream_launch_blocks_ldg(const StreamLaunch& a) { return ldg_blocks(a.nx, a.ny, a.phase); }
+
+__global__ void k_wait(const RemoteSpec rs) { rs_wait(rs); }
+__global__ void k_epoch_bump(unsigned long long* e) { *e += 1ull; }
+
+px_status launch_wait(const RemoteSpec& rs, cudaStream_t s) {
+  k_wait<<<1, 1, 0, s>>>(rs);
+  count_launches(1);
+  return cuda_check(cudaGetLastError(), "wait kernel launch");
+}
+
+px_status launch_epoch_bump(unsigned long long* epoch, cudaStream_t s) {
+  k_epoch_bump<<<1, 1, 0, s>>>(epoch);
+  count_launches(1);
+  return cuda_check(cudaGetLastError(), "epoch kernel launch");
+}
+
+px_status launch_stream_ldg(int mode, int stencil, const StreamLaunch& a, cudaStream_t s) {
+  if (a.nx <= 0 || a.ny <= 0) return PX_OK;
   const int32_t rows = ldg_rows(a.nx, a.ny, a.phase);
   dim3 grid((a.nx + a.phase + SW_COLS - 1) / SW_COLS, (a.ny + rows - 1) / rows);
   if (grid.y > 65535) return fail(PX_ERR_UNSUPPORTED, "region too tall (%d rows)", a.ny);

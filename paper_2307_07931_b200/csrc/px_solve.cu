@@ -26,11 +26,27 @@
 
 #include "px_internal.h"
 
+// Peer-memory halo state (px_comm_enable_p2p).
+struct P2PState {
+  bool enabled = false;
+  uint64_t layout_gen = 0;
+  int32_t rank = 0;
+  const double* bufs[2] = {nullptr, nullptr};   // own registered φ (A) and scratch (B)
+  double* peer_lo[2] = {nullptr, nullptr};      // lower neighbour's A, B (patch data pointers)
+  double* peer_hi[2] = {nullptr, nullptr};      // upper neighbour's A, B
+  unsigned long long* flags = nullptr;          // own: [0] arrivals from below, [1] from above
+  unsigned long long* peer_flags_lo = nullptr;  // lower neighbour's flags
+  unsigned long long* peer_flags_hi = nullptr;  // upper neighbour's flags
+  unsigned long long* epoch = nullptr;          // own solve counter
+  std::vector<void*> opened;                    // IPC-mapped peer allocations
+};
+
 struct px_comm {
   ncclComm_t nccl = nullptr;
   int32_t nranks = 1, rank = 0, device = 0;
   cudaStream_t stream = nullptr;
-  bool self_exchange = false;  // 1 rank, periodic: exchange ghost rows with itself over NCCL (test mode)
+  bool self_exchange = false;  // 1 rank, periodic: exchange ghost rows with itself (test mode)
+  P2PState p2p;
 };
 
 namespace px {
@@ -421,13 +437,47 @@ static px_status enqueue_solve(const SolveCtx& x) {
     std::swap(cur, nxt);
     it += K;
   }
+  // Fused halo push over peer memory (px_comm_enable_p2p): the boundary-row
+  // launches store their rows into the neighbours' ghost rows and count their
+  // arrival; the next sweep's boundary launches wait for it.  No NCCL call
+  // and no comm stream per sweep.
+  px_local_info pli;
+  PX_TRY(local_info(x.l, x.rank, &pli));
+  const bool p2p = nccl_multi && K == 1 && x.c->p2p.enabled && x.c->p2p.layout_gen == layout_generation(x.l) &&
+                   x.c->p2p.rank == x.rank && x.phi[0].data == x.c->p2p.bufs[0] &&
+                   x.scr[0].data == x.c->p2p.bufs[1] && ext(pli.owned, 1) > 2 * x.l->ghost && it < N;
+  unsigned long long G = 0;
+  if (p2p) PX_TRY(launch_epoch_bump(x.c->p2p.epoch, x.s));
   for (; it < N; ++it) {
     const int32_t slot = (E > 0 && it % E == 0) ? it / E : -1;
     std::vector<SweepLaunch> v;
     for (int32_t part = 0; part < x.nparts; ++part)
       PX_TRY(build_part_launches(x, part, cur[part], nxt[part], false, nccl_multi, v));
     set_slot(v, 0, plan, slot);
-    if (nccl_multi) {
+    if (p2p) {
+      const P2PState& st = x.c->p2p;
+      const int nb = (it & 1) ? 0 : 1;  // the neighbours' buffer this sweep writes (their "next")
+      const int32_t g = x.l->ghost, x0 = pli.owned.lo.c[0];
+      G = (unsigned long long)stream_launch_blocks_ldg(v[0].a);
+      for (int side = 0; side < 2; ++side) {
+        StreamLaunch& a = v[side].a;
+        const int32_t pr = side == 0 ? pli.nbr_lo : pli.nbr_hi;
+        if (pr < 0) continue;
+        px_local_info nli;
+        PX_TRY(local_info(x.l, pr, &nli));
+        const int32_t ty = side == 0 ? nli.owned.hi.c[1] + 1 : nli.owned.lo.c[1] - g;  // their ghost rows
+        double* base = side == 0 ? st.peer_lo[nb] : st.peer_hi[nb];
+        a.rs.rdst = base + (int64_t)(x0 - nli.alloc.lo.c[0]) + (int64_t)(ty - nli.alloc.lo.c[1]) * nli.ld;
+        a.rs.rflag = side == 0 ? st.peer_flags_lo + 1 : st.peer_flags_hi + 0;
+        a.rs.epoch = st.epoch;
+        a.rs.per_epoch = (unsigned long long)N * G;
+        if (it >= 1) {
+          a.rs.wflag = st.flags + side;
+          a.rs.wcount = (unsigned long long)it * G;
+        }
+      }
+      for (auto& sl : v) PX_TRY(launch_stream(MODE_RELAX, x.p->stencil, sl.a, x.s));
+    } else if (nccl_multi) {
       // boundary rows, exchange on the comm stream, interior concurrently
       const bool split = v.size() == 3;
       PX_TRY(launch_stream(MODE_RELAX, x.p->stencil, v[0].a, x.s));
@@ -445,6 +495,18 @@ static px_status enqueue_solve(const SolveCtx& x) {
     std::swap(cur, nxt);
   }
   const int32_t entry = plan->n_entries - 1;
+  if (p2p) {  // φ^N's ghost rows: the last sweep's pushes must have arrived
+    for (int side = 0; side < 2; ++side) {
+      if ((side == 0 ? pli.nbr_lo : pli.nbr_hi) < 0) continue;
+      RemoteSpec w;
+      std::memset(&w, 0, sizeof w);
+      w.wflag = x.c->p2p.flags + side;
+      w.epoch = x.c->p2p.epoch;
+      w.per_epoch = (unsigned long long)N * G;
+      w.wcount = (unsigned long long)N * G;
+      PX_TRY(launch_wait(w, x.s));
+    }
+  }
   if (E >= 0) {
     std::vector<SweepLaunch> v;
     for (int32_t part = 0; part < x.nparts; ++part)
@@ -512,9 +574,113 @@ void px_comm_destroy(px_comm* c) {
   auto& v = plans();
   v.erase(std::remove_if(v.begin(), v.end(), [c](const std::unique_ptr<Plan>& p) { return p->key.comm == c; }),
           v.end());
+  for (void* b : c->p2p.opened) cudaIpcCloseMemHandle(b);
+  if (c->p2p.flags) cudaFree(c->p2p.flags);
   if (c->nccl) ncclCommDestroy(c->nccl);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
+}
+
+// base address of the allocation containing p (driver API, fetched at run
+// time so the library does not link libcuda)
+typedef int (*MemGetAddressRangeFn)(unsigned long long*, size_t*, unsigned long long);
+static px_status alloc_base(const void* p, void** base, size_t* off) {
+  static MemGetAddressRangeFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess || !f)
+      return fail(PX_ERR_CUDA, "cuMemGetAddressRange entry point unavailable");
+    fn = (MemGetAddressRangeFn)f;
+  }
+  unsigned long long b = 0;
+  size_t sz = 0;
+  if (fn(&b, &sz, (unsigned long long)(uintptr_t)p) != 0) return fail(PX_ERR_CUDA, "cuMemGetAddressRange failed");
+  *base = (void*)(uintptr_t)b;
+  *off = (size_t)((uintptr_t)p - (uintptr_t)b);
+  return PX_OK;
+}
+
+struct P2PExport {
+  cudaIpcMemHandle_t h[3];   // A, B, flags
+  uint64_t off[3];
+};
+
+px_status px_comm_enable_p2p(px_comm* c, const px_layout* l, int32_t rank, const px_patch* phi,
+                             const px_patch* phi_scratch) {
+  if (!c || !l || !phi || !phi_scratch) return fail(PX_ERR_ARG, "null argument");
+  if (c->nranks != l->nranks || c->rank != rank)
+    return fail(PX_ERR_STATE, "communicator (rank %d of %d) does not match layout/rank", c->rank, c->nranks);
+  px_local_info li;
+  PX_TRY(check_rank_patch(l, rank, phi, "phi", &li));
+  PX_TRY(check_rank_patch(l, rank, phi_scratch, "phi_scratch", &li));
+  if (!comm_exchanges(l, c))
+    return fail(PX_ERR_UNSUPPORTED, "peer halo push needs a multi-rank layout (or the 1-rank periodic self-exchange mode)");
+  P2PState& st = c->p2p;
+  for (void* b : st.opened) cudaIpcCloseMemHandle(b);
+  st.opened.clear();
+  if (!st.flags) {
+    PX_TRY(cuda_check(cudaMalloc(&st.flags, 4 * sizeof(unsigned long long)), "cudaMalloc flags"));
+  }
+  PX_TRY(cuda_check(cudaMemset(st.flags, 0, 4 * sizeof(unsigned long long)), "memset flags"));
+  st.epoch = st.flags + 2;
+  st.bufs[0] = phi->data;
+  st.bufs[1] = phi_scratch->data;
+  st.layout_gen = layout_generation(l);
+  st.rank = rank;
+  if (c->nranks == 1) {  // self-exchange: the neighbour is this rank
+    for (int b = 0; b < 2; ++b) st.peer_lo[b] = st.peer_hi[b] = const_cast<double*>(st.bufs[b]);
+    st.peer_flags_lo = st.peer_flags_hi = st.flags;
+    st.enabled = true;
+    return PX_OK;
+  }
+  // export (allocation handle, offset) of A, B and the flags; all-gather over NCCL
+  P2PExport mine;
+  std::memset(&mine, 0, sizeof mine);
+  const void* ptrs[3] = {phi->data, phi_scratch->data, st.flags};
+  for (int i = 0; i < 3; ++i) {
+    void* base = nullptr;
+    size_t off = 0;
+    PX_TRY(alloc_base(ptrs[i], &base, &off));
+    PX_TRY(cuda_check(cudaIpcGetMemHandle(&mine.h[i], base), "cudaIpcGetMemHandle"));
+    mine.off[i] = off;
+  }
+  const size_t sz = sizeof(P2PExport);
+  uint8_t* d = nullptr;
+  PX_TRY(cuda_check(cudaMalloc(&d, sz * (c->nranks + 1)), "cudaMalloc exchange"));
+  std::vector<P2PExport> all(c->nranks);
+  px_status stt = cuda_check(cudaMemcpy(d + sz * c->nranks, &mine, sz, cudaMemcpyHostToDevice), "H2D");
+  if (stt == PX_OK)
+    stt = nccl_check(ncclAllGather(d + sz * c->nranks, d, sz, ncclUint8, c->nccl, c->stream), "ncclAllGather");
+  if (stt == PX_OK) stt = cuda_check(cudaStreamSynchronize(c->stream), "all-gather");
+  if (stt == PX_OK) stt = cuda_check(cudaMemcpy(all.data(), d, sz * c->nranks, cudaMemcpyDeviceToHost), "D2H");
+  cudaFree(d);
+  PX_TRY(stt);
+  int32_t peers[2] = {li.nbr_lo, li.nbr_hi};
+  void* mapped[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
+  for (int side = 0; side < 2; ++side) {
+    const int32_t pr = peers[side];
+    if (pr < 0) continue;
+    if (side == 1 && pr == peers[0]) {  // same neighbour on both sides (P = 2): map once
+      for (int i = 0; i < 3; ++i) mapped[1][i] = mapped[0][i];
+      continue;
+    }
+    for (int i = 0; i < 3; ++i) {
+      void* b = nullptr;
+      PX_TRY(cuda_check(cudaIpcOpenMemHandle(&b, all[pr].h[i], cudaIpcMemLazyEnablePeerAccess),
+                        "cudaIpcOpenMemHandle"));
+      st.opened.push_back(b);
+      mapped[side][i] = (uint8_t*)b + all[pr].off[i];
+    }
+  }
+  for (int b = 0; b < 2; ++b) {
+    st.peer_lo[b] = (double*)mapped[0][b];
+    st.peer_hi[b] = (double*)mapped[1][b];
+  }
+  st.peer_flags_lo = (unsigned long long*)mapped[0][2];
+  st.peer_flags_hi = (unsigned long long*)mapped[1][2];
+  st.enabled = true;
+  return PX_OK;
 }
 
 px_status px_comm_allreduce_norms(px_comm* c, double* d_max, double* d_sum, int32_t n,

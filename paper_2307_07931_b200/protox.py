@@ -86,6 +86,7 @@ EXPORTS = [
     "px_stencil_apply", "px_relax_step", "px_relax_block", "px_residual_norm", "px_mehrstellen_rhs",
     "px_init_field", "px_fill_ghosts",
     "px_comm_unique_id", "px_comm_create", "px_comm_destroy", "px_comm_allreduce_norms",
+    "px_comm_enable_p2p",
     "px_exchange_ghosts", "px_exchange_ghosts_local",
     "px_solve", "px_solve_host", "px_release_cached", "px_kernel_launch_count",
     "px_relax_variant", "px_stream_ceiling",
@@ -152,6 +153,8 @@ def lib():
     L.px_comm_create.argtypes = [ctypes.c_char_p, i32, i32, i32, P(vp)]
     L.px_comm_destroy.restype = None
     L.px_comm_destroy.argtypes = [vp]
+    L.px_comm_enable_p2p.restype = st
+    L.px_comm_enable_p2p.argtypes = [vp, vp, i32, P(px_patch), P(px_patch)]
     L.px_comm_allreduce_norms.restype = st
     L.px_comm_allreduce_norms.argtypes = [vp, vp, vp, i32, vp]
     L.px_exchange_ghosts.restype = st
@@ -364,6 +367,11 @@ def comm_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(lib().px_comm_unique_id(buf))
     return buf.raw
+
+
+def comm_enable_p2p(comm: Comm, layout: Layout, rank: int, phi: px_patch, phi_scratch: px_patch):
+    """px_comm_enable_p2p: fused halo push over peer memory for px_solve."""
+    _check(lib().px_comm_enable_p2p(comm.h, layout.h, rank, ctypes.byref(phi), ctypes.byref(phi_scratch)))
 
 
 def comm_allreduce_norms(comm: Comm, d_max, d_sum, n: int, stream=None):

@@ -570,3 +570,38 @@ def test_nccl_allreduce_norms_single_rank():
         assert m[:2].tolist() == [1.0, 3.0]
     finally:
         comm.close()
+
+
+@pytest.mark.parametrize("graph", [True, False])
+def test_p2p_halo_push_self_exchange(graph, monkeypatch):
+    """Fused halo push over peer memory (px_comm_enable_p2p), self-exchange
+    mode on one GPU: the boundary-row kernels store their rows (and x images)
+    into the 'neighbour's' ghost rows and count arrivals; the next sweep's
+    boundary kernels wait for them.  Two consecutive solves (epoch counters),
+    graph and non-graph: bit-identical to 2N oracle sweeps."""
+    monkeypatch.setenv("PROTOX_NCCL_SELF_EXCHANGE", "1")
+    n0, n1, N, E = 1536, 2304, 8, 2
+    h = 1.0 / 2048
+    lam = h * h / 8
+    phi0, rho = _fields(n0, n1, 1, 404, P.PX_BC_PERIODIC)
+    lay = P.Layout(P.box(0, 0, n0 - 1, n1 - 1), (256, 256), 1, P.PX_BC_PERIODIC, 1)
+    comm = P.Comm(P.comm_unique_id(), 1, 0, torch.cuda.current_device())
+    try:
+        a = to_device_ghosted(lay, 0, phi0, 1)
+        b = lay.alloc(0)
+        r = to_device_ghosted(lay, 0, rho, 1)
+        pa, pb, pr = lay.patch(0, a), lay.patch(0, b), lay.patch(0, r)
+        P.comm_enable_p2p(comm, lay, 0, pa, pb)
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        r1 = P.solve(lay, comm, 0, P.relax_params(h, lam), N, E, pa, pb, pr, use_graph=graph, stream=s)
+        assert not r1.in_scratch
+        r2 = P.solve(lay, comm, 0, P.relax_params(h, lam), N, E, pa, pb, pr, use_graph=graph, stream=s)
+        out = owned_to_host(lay, 0, a)
+    finally:
+        comm.close()
+    ref, rn = oracle.solve(_orc_problem(n0, n1, h, lam, P.PX_BC_PERIODIC, 0, 2 * N, E), phi0, rho)
+    assert bits_equal(out, ref[1:-1, 1:-1]), ulp_diff(out, ref[1:-1, 1:-1])
+    # norms: first solve's entries are φ^0..φ^6, final φ^8; second continues from φ^8
+    _check_norms(r1.norms[:-1], rn[: N // E])
+    _check_norms(r2.norms, rn[N // E:])
