@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(NC * 32 + 32, CPS) k_bulk(const StreamLaunch a
                                                             int crows) {
   constexpr int W = 64 * NC, NCW = NC;
   constexpr bool P2 = (PW & 1) != 0, PL = (PW & 2) != 0;
+  static_assert(R % 3 == 0, "rows live in slots indexed by row mod 3");
   constexpr int STAGE_DOUBLES = R * 2 * W;
   extern __shared__ __align__(128) double smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NST * STAGE_DOUBLES);
@@ -199,8 +200,12 @@ __global__ void __launch_bounds__(NC * 32 + 32, CPS) k_bulk(const StreamLaunch a
       const bool live = c0 < t.w;
       const bool left = (j == 0);
       const bool edge_r = (c0 + 2 == t.w);        // this pair ends the strip
-      double w_s = 0, a_s = 0, b_s = 0, e_s = 0;  // row S
-      double w_c = 0, a_c = 0, b_c = 0, e_c = 0;  // row C
+      // the pair's cells lie within g of an x face (ghost images)
+      const int X0 = t.c + c0 + a.gs.o[0];
+      const bool xface = a.gs.g > 0 && ((X0 < a.gs.g) || (X0 + 1 >= a.gs.n[0] - a.gs.g));
+      // rows in three register slots indexed by (row - (y0-1)) mod 3: R is a
+      // multiple of 3, so the S/C/N roles are compile-time and nothing moves
+      double rw[3] = {0, 0, 0}, ra[3] = {0, 0, 0}, rb[3] = {0, 0, 0}, re[3] = {0, 0, 0};
       for (int st = 0; st < nst; ++st) {
         double hw[R], he[R];
 #pragma unroll
@@ -216,26 +221,36 @@ __global__ void __launch_bounds__(NC * 32 + 32, CPS) k_bulk(const StreamLaunch a
         }
         mbar_wait(&full[slot], phase);
         const double* sp = smem + (size_t)slot * STAGE_DOUBLES;
+        const bool full_stage = (t.y0 - 1 + st * R + R - 1 <= t.y1) && (t.y0 - 1 + st * R - 1 >= t.y0);
 #pragma unroll
         for (int i = 0; i < R; ++i) {
+          constexpr int dummy = 0;
+          (void)dummy;
+          const int n_ = i % 3, c_ = (i + 2) % 3, s_ = (i + 1) % 3;  // N, C, S slots
           const int yf = t.y0 - 1 + st * R + i;
-          if (yf > t.y1) break;
+          if (!full_stage && yf > t.y1) break;
           // row N = φ row yf, from shared memory
-          double w_n = 0, a_n = 0, b_n = 0, e_n = 0;
           if (live) {
             const double2 pr = *reinterpret_cast<const double2*>(sp + i * W + c0);
-            a_n = pr.x;
-            b_n = pr.y;
-            w_n = left ? hw[i] : sp[i * W + c0 - 1];
-            e_n = edge_r ? he[i] : sp[i * W + c0 + 2];
+            ra[n_] = pr.x;
+            rb[n_] = pr.y;
+            rw[n_] = left ? hw[i] : sp[i * W + c0 - 1];
+            re[n_] = edge_r ? he[i] : sp[i * W + c0 + 2];
           }
           const int r = yf - 1;  // the row computed now
-          if (r >= t.y0 && live) {
+          if (live && (full_stage || r >= t.y0)) {
+            const double w_c = rw[c_], a_c = ra[c_], b_c = rb[c_], e_c = re[c_];
+            const double w_s = rw[s_], a_s = ra[s_], b_s = rb[s_], e_s = re[s_];
+            const double w_n = rw[n_], a_n = ra[n_], b_n = rb[n_], e_n = re[n_];
             double L0, L1;
             if (ST == 0) {
               // -4·C is exact, so the fused multiply-add rounds like the separate ops
               L0 = fma(-4.0, a_c, __dadd_rn(__dadd_rn(__dadd_rn(w_c, b_c), a_s), a_n));
               L1 = fma(-4.0, b_c, __dadd_rn(__dadd_rn(__dadd_rn(a_c, e_c), b_s), b_n));
+              (void)w_s;
+              (void)e_s;
+              (void)w_n;
+              (void)e_n;
             } else {
               double q;
               q = __dmul_rn(4.0, w_c);
@@ -272,13 +287,14 @@ __global__ void __launch_bounds__(NC * 32 + 32, CPS) k_bulk(const StreamLaunch a
               double* dp = a.dst + (int64_t)r * a.ld_dst + x;
               *reinterpret_cast<double2*>(dp) = make_double2(o0, o1);
               if (a.gs.g > 0) {
-                images(a, x, r, o0);
-                images(a, x + 1, r, o1);
+                const int Y = r + a.gs.o[1];
+                if (xface || Y < a.gs.g || Y >= a.gs.n[1] - a.gs.g) {
+                  images(a, x, r, o0);
+                  images(a, x + 1, r, o1);
+                }
               }
             }
           }
-          w_s = w_c; a_s = a_c; b_s = b_c; e_s = e_c;
-          w_c = w_n; a_c = a_n; b_c = b_n; e_c = e_n;
         }
         // order this warp's shared-memory reads of the stage before the
         // producer's next TMA write into it (generic -> async proxy)
@@ -315,11 +331,12 @@ struct BulkCfg {
   int nst, r, cps, nc;
 };
 // {stages, rows per stage, CTAs per SM, consumer warps}; measured at 16384²
-// (GB/s, profiles/round1_bulk_configs.json): {3,2,3,7} 6171, {3,2,3,8} 6118-6132,
-// {4,2,3,7} 6136, {3,4,2,8} 5917, {5,4,1,8} 5433, {3,2,4,7} 4633 (spills).
-// 8-warp blocks (7 consumers + producer) keep 6 warps per SM sub-partition
-// at 80 registers without spills.
-static const BulkCfg kCfgs[] = {{3, 2, 3, 7}, {3, 2, 3, 8}, {5, 4, 1, 8}};
+// (GB/s, profiles/round1_bulk_configs.json).  Rows live in 3 register slots
+// (row mod 3), so R is a multiple of 3: {3,3,2,8} 6244, {4,3,2,8} 6208,
+// {4,3,1,15} 6202, {3,3,3,7} 5769 (spills at 80 registers).  Earlier R = 2
+// variants with register moves: {3,2,3,7} 6171-6195, {3,2,3,8} 6118-6132,
+// {3,4,2,8} 5917, {5,4,1,8} 5433.
+static const BulkCfg kCfgs[] = {{3, 3, 2, 8}, {4, 3, 2, 8}, {4, 3, 1, 15}, {3, 3, 3, 7}, {5, 3, 1, 8}};
 static const BulkCfg& bulk_cfg() {
   static int idx = -1;
   if (idx < 0) {
@@ -423,9 +440,11 @@ static bool is_pow2(double v) {
 template <int MODE, int ST, int PW>
 static cudaError_t launch_pw(const StreamLaunch& a, cudaStream_t s) {
   const BulkCfg& c = bulk_cfg();
-  if (c.nc == 8 && c.nst == 3) return launch_b<MODE, ST, 3, 2, 3, 8, PW>(a, s);
-  if (c.nst == 5) return launch_b<MODE, ST, 5, 4, 1, 8, PW>(a, s);
-  return launch_b<MODE, ST, 3, 2, 3, 7, PW>(a, s);
+  if (c.nc == 8 && c.nst == 4) return launch_b<MODE, ST, 4, 3, 2, 8, PW>(a, s);
+  if (c.nc == 15) return launch_b<MODE, ST, 4, 3, 1, 15, PW>(a, s);
+  if (c.nc == 7) return launch_b<MODE, ST, 3, 3, 3, 7, PW>(a, s);
+  if (c.nst == 5) return launch_b<MODE, ST, 5, 3, 1, 8, PW>(a, s);
+  return launch_b<MODE, ST, 3, 3, 2, 8, PW>(a, s);
 }
 
 template <int MODE, int ST>
