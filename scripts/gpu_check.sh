@@ -1,7 +1,8 @@
 #!/bin/bash
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
-rm -f gpurun_out/ab.jsonl
-for c in 0 1 2 3; do echo -n "{\"cfg\": $c, \"r\": " >> gpurun_out/ab.jsonl; PROTOX_BULK_CFG=$c timeout 200 python scripts/ab_relax.py --n 16384 --reps 40 >> gpurun_out/ab.jsonl 2>>gpurun_out/ab.err || echo null >> gpurun_out/ab.jsonl; sed -i '$ s/$/}/' gpurun_out/ab.jsonl; done
-for c in 0 1 2; do echo -n "{\"cfg9_8192\": $c, \"r\": " >> gpurun_out/ab.jsonl; PROTOX_BULK_CFG=$c timeout 200 python scripts/ab_relax.py --n 8192 --reps 40 --stencil 1 >> gpurun_out/ab.jsonl 2>>gpurun_out/ab.err || echo null >> gpurun_out/ab.jsonl; sed -i '$ s/$/}/' gpurun_out/ab.jsonl; done
-for c in 0 1 2; do echo -n "{\"cfg_solve\": $c, \"r\": " >> gpurun_out/ab.jsonl; PROTOX_BULK_CFG=$c timeout 200 python scripts/ab_solve.py --n 16384 --tk 1 --reps 5 >> gpurun_out/ab.jsonl 2>>gpurun_out/ab.err || echo null >> gpurun_out/ab.jsonl; sed -i '$ s/$/}/' gpurun_out/ab.jsonl; done
+timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke exit $?" >> gpurun_out/smoke.log
+timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err
+for c in C4 C5 C2 C1; do timeout 900 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; done
+bash scripts/gpu_profiles.sh

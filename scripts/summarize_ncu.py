@@ -71,10 +71,11 @@ def summarize(name, rep, key=None, alg_bytes=None):
         out["sass_mnemonics_present"] = sorted({k for k in mix if k.startswith(("UBLKCP", "SYNCS", "UTMA", "LDS", "STG", "LDG"))})
     rd = out["metrics"].get("dram__bytes_read.sum", {}).get("value")
     wr = out["metrics"].get("dram__bytes_write.sum", {}).get("value")
-    unit = out["metrics"].get("dram__bytes_read.sum", {}).get("unit", "")
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    urd = scale.get(out["metrics"].get("dram__bytes_read.sum", {}).get("unit", ""), 1)
+    uwr = scale.get(out["metrics"].get("dram__bytes_write.sum", {}).get("unit", ""), 1)
     if rd is not None and wr is not None:
-        out["dram_bytes_per_launch"] = (rd + wr) * scale
+        out["dram_bytes_per_launch"] = rd * urd + wr * uwr
         if alg_bytes:
             out["algorithmic_bytes_per_launch"] = alg_bytes
             out["traffic_over_algorithmic"] = out["dram_bytes_per_launch"] / alg_bytes
