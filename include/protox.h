@@ -317,6 +317,26 @@ px_status px_solve(const px_layout* l, px_comm* c, int32_t rank, const px_relax_
 px_status px_solve_host(const px_layout* l, const px_relax_params* p, const px_solve_opts* o,
                         const double* h_phi0, const double* h_rho, double* h_phi_out,
                         double* h_norms, int32_t cap, int32_t* n_written, void* stream);
+/* Pipelined end-to-end solves of nprob independent problems on HOST arrays
+ * (single rank, same layout / parameters / options for all): the H2D of
+ * problem i+1 and the D2H of problem i-1 run on the copy engines (two
+ * library streams) while problem i is solved on `stream`, over three
+ * library-owned device buffer sets (cached like px_solve_host's).
+ *   h_phi0[i]  n1 x n0 interior, dim-0 fastest; h_phi0 == NULL or
+ *              h_phi0[i] == NULL: φ^0 = 0 (zero-filled on the device)
+ *   h_rho[i]   right-hand side, same shape (required)
+ *   h_phi_out[i] receives φ^N (required)
+ *   h_norms    nprob * cap (max|r|, Σr²) pairs, problem i at h_norms[2*cap*i]
+ *              (as px_solve); n_written: nprob counts, or NULL
+ * Host buffers should be page-locked (cudaHostAlloc / cudaHostRegister) for
+ * the copies to overlap the solves; pageable memory is correct but
+ * serialises.  `stream` must be a non-default stream; work already on it
+ * precedes the batch, and on return (host-synchronous) it is idle.
+ * Results are bit-identical to nprob calls of px_solve_host. */
+px_status px_solve_host_batch(const px_layout* l, const px_relax_params* p, const px_solve_opts* o,
+                              int32_t nprob, const double* const* h_phi0, const double* const* h_rho,
+                              double* const* h_phi_out, double* h_norms, int32_t cap, int32_t* n_written,
+                              void* stream);
 void px_release_cached(void);
 
 /* Diagnostics: number of kernel launches libprotox enqueued so far in this

@@ -156,6 +156,29 @@ struct PersistLaunch {
   int rows, gx, gy;        // tile grid (SW_COLS columns x rows)
 };
 int32_t persist_rows(int32_t nx, int32_t ny, int32_t grid);
+
+// All sweeps of a single-rank solve with the iterate resident in shared
+// memory (px_resident.cu): CTA c of G owns rows [c*ny/G, (c+1)*ny/G) and
+// exchanges only its first and last row with its two neighbours per sweep
+// through L2 (flag handshake, no grid barrier).
+struct ResidentLaunch {
+  const double* phi_in;   // cell (0,0) of φ^0 (ghost ring filled)
+  double* phi_out;        // cell (0,0) of the buffer that receives φ^N (+ ghost ring)
+  const double* rhs;      // cell (0,0) of the right-hand side
+  int64_t ld_in, ld_out, ld_rhs;
+  int nx, ny, rmax;       // extent; max rows per CTA
+  int xmode[2], ymode[2]; // GH_WRAP / GH_REFLECT / GH_NONE (fixed ghosts)
+  double scale, lambda;
+  int nsweeps, every, final_norm, n_entries;
+  double* d_max;
+  double* d_sum;
+  double* ws;             // resident_ws_doubles(...) doubles, zero not required
+};
+size_t resident_ws_doubles(int nx, int grid, int n_entries);
+// CTAs and dynamic shared memory of the resident kernel for an nx x ny
+// problem; false if it does not fit (or nx is odd).
+bool resident_plan(int nx, int ny, int* grid, int* rmax, size_t* smem);
+px_status launch_resident(int stencil, const ResidentLaunch& r, int grid, size_t smem, cudaStream_t s);
 int32_t stream_launch_blocks_ldg(const StreamLaunch& a);
 px_status launch_stream_ldg(int mode, int stencil, const StreamLaunch& a, cudaStream_t s);
 px_status launch_wait(const RemoteSpec& rs, cudaStream_t s);

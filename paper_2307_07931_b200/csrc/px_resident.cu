@@ -1,0 +1,314 @@
+// px_resident.cu -- all sweeps of an L2-sized single-rank solve with the
+// iterate RESIDENT IN SHARED MEMORY (BASELINE config 2: 1024², 1000 sweeps;
+// SURVEY §8(d) "C2 is L2-bound and launch-bound").
+//
+// One cooperative launch of G <= #SM CTAs.  CTA c owns the rows
+// [c·ny/G, (c+1)·ny/G) and keeps them in shared memory for the whole solve:
+// two copies of its rows plus one halo row above and below (with the ghost
+// columns), and its rows of the right-hand side.  A sweep reads and writes
+// shared memory only; then the CTA publishes its first and last new row to
+// L2 (double-buffered by sweep parity), raises its flag (release), waits for
+// the flags of its two neighbours (acquire) and copies their rows into its
+// halo.  No grid-wide barrier per sweep: a CTA synchronises with its two
+// neighbours only.  Domain faces: periodic wrap (the ring of CTAs), odd
+// reflection (halo row = −own row), fixed ghosts (kept from φ^0); the ghost
+// columns of every row follow the x rule after each exchange.
+//
+// Per cell the oracle's expression tree with every * and + rounded
+// separately (bit-identical).  Norms: per thread in row order, per CTA in
+// fixed warp order into partials[entry][cta]; after the last sweep one grid
+// barrier, then entry e is reduced over the CTAs in fixed order by CTA
+// e mod G.  Deterministic for a given (nx, ny, #SM).
+//
+// Safety of the two publication slots: CTA c writes φ^{s+1} rows into slot
+// (s+1)&1 during sweep s; it can write slot (s+1)&1 again (φ^{s+3}) only
+// after both neighbours raised flag s+2, i.e. after they copied φ^{s+1}.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "px_device.cuh"
+#include "px_internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace px {
+
+constexpr int RS_THREADS = 512;
+
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Canonical tap sums (oracle order, each op rounded).
+template <int ST>
+__device__ __forceinline__ double rs_taps(double w, double e, double s, double n, double c, double sw,
+                                          double se, double nw, double ne) {
+  if (ST == 0) return __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(w, e), s), n), __dmul_rn(-4.0, c));
+  double q = __dmul_rn(4.0, w);
+  q = __dadd_rn(q, __dmul_rn(4.0, e));
+  q = __dadd_rn(q, __dmul_rn(4.0, s));
+  q = __dadd_rn(q, __dmul_rn(4.0, n));
+  q = __dadd_rn(q, sw);
+  q = __dadd_rn(q, se);
+  q = __dadd_rn(q, nw);
+  q = __dadd_rn(q, ne);
+  return __dadd_rn(q, __dmul_rn(-20.0, c));
+}
+
+// Rows 1..R of the CTA's shared block: B = A + λ(scale·L(A) − F) (WRITE), or
+// residual norms of A only.  A thread walks a column pair down the rows with
+// the S/C rows (and their outer neighbours) in registers.
+template <int ST, bool WRITE>
+__device__ __forceinline__ void rs_rows(const double* A, double* B, const double* F, int P, int nx, int R,
+                                        double scale, double lambda, unsigned long long& mx, double& ss) {
+  for (int q = threadIdx.x; q < nx / 2; q += blockDim.x) {
+    const int x = 2 * q + 2;  // shared index of column 2q
+    double2 S = *reinterpret_cast<const double2*>(A + x);
+    double2 C = *reinterpret_cast<const double2*>(A + P + x);
+    double sw = A[x - 1], se = A[x + 2], cw = A[P + x - 1], ce = A[P + x + 2];
+    for (int r = 1; r <= R; ++r) {
+      const double* an = A + (size_t)(r + 1) * P + x;
+      const double2 N = *reinterpret_cast<const double2*>(an);
+      const double nw = an[-1], ne = an[2];
+      const double L0 = rs_taps<ST>(cw, C.y, S.x, N.x, C.x, sw, S.y, nw, N.y);
+      const double L1 = rs_taps<ST>(C.x, ce, S.y, N.y, C.y, S.x, se, N.x, ne);
+      const double2 f = *reinterpret_cast<const double2*>(F + (size_t)(r - 1) * nx + (x - 2));
+      const double r0 = __dsub_rn(__dmul_rn(scale, L0), f.x);
+      const double r1 = __dsub_rn(__dmul_rn(scale, L1), f.y);
+      if (WRITE) {
+        double2 o;
+        o.x = __dadd_rn(C.x, __dmul_rn(lambda, r0));
+        o.y = __dadd_rn(C.y, __dmul_rn(lambda, r1));
+        *reinterpret_cast<double2*>(B + (size_t)r * P + x) = o;
+      }
+      mx = umax64(mx, (unsigned long long)__double_as_longlong(fabs(r0)));
+      ss = fma(r0, r0, ss);
+      mx = umax64(mx, (unsigned long long)__double_as_longlong(fabs(r1)));
+      ss = fma(r1, r1, ss);
+      S = C;
+      sw = cw;
+      se = ce;
+      C = N;
+      cw = nw;
+      ce = ne;
+    }
+  }
+}
+
+// fixed-order block reduction of (max bits, Σ) into out[0..1] (thread 0)
+__device__ __forceinline__ void rs_block_reduce(unsigned long long mx, double ss, double* out) {
+  __shared__ unsigned long long s_mx[RS_THREADS / 32];
+  __shared__ double s_ss[RS_THREADS / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = umax64(mx, __shfl_xor_sync(FULL_MASK, mx, o));
+    ss = ss + __shfl_xor_sync(FULL_MASK, ss, o);
+  }
+  if (lane == 0) {
+    s_mx[warp] = mx;
+    s_ss[warp] = ss;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long m = s_mx[0];
+    double t = s_ss[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      m = umax64(m, s_mx[w]);
+      t = t + s_ss[w];
+    }
+    out[0] = __longlong_as_double((long long)m);
+    out[1] = t;
+  }
+  __syncthreads();
+}
+
+// ghost columns -1 and nx of one shared row (x rule; GH_NONE keeps them)
+__device__ __forceinline__ void rs_xghost(double* row, int nx, const int (&xm)[2]) {
+  if (xm[0] == GH_WRAP) row[1] = row[nx + 1];
+  else if (xm[0] == GH_REFLECT) row[1] = -row[2];
+  if (xm[1] == GH_WRAP) row[nx + 2] = row[2];
+  else if (xm[1] == GH_REFLECT) row[nx + 2] = -row[nx + 1];
+}
+
+template <int ST>
+__global__ void __launch_bounds__(RS_THREADS, 1) k_resident(const ResidentLaunch p) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double sm[];
+  const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  const int nx = p.nx, P = nx + 4;
+  const int y0 = (int)((int64_t)c * p.ny / G), y1 = (int)((int64_t)(c + 1) * p.ny / G), R = y1 - y0;
+  double* A = sm;
+  double* B = A + (size_t)(p.rmax + 2) * P;
+  double* F = B + (size_t)(p.rmax + 2) * P;
+  unsigned long long* flags = reinterpret_cast<unsigned long long*>(p.ws);
+  double* pub = p.ws + G;                          // [slot][cta][first, last][nx]
+  double* part = pub + (size_t)2 * G * 2 * nx;     // [entry][cta][max, sum]
+  const int up = c > 0 ? c - 1 : G - 1, dn = c < G - 1 ? c + 1 : 0;
+  const bool top_x = c > 0 || p.ymode[0] == GH_WRAP;      // halo row 0 from CTA `up`
+  const bool bot_x = c < G - 1 || p.ymode[1] == GH_WRAP;  // halo row R+1 from CTA `dn`
+  const int xm[2] = {p.xmode[0], p.xmode[1]};
+
+  // φ^0 rows y0-1 .. y1 with their ghost columns (ghost ring filled by the
+  // caller's exchange) into both copies; the rhs rows.
+  for (int r = 0; r < R + 2; ++r) {
+    const double* src = p.phi_in + (int64_t)(y0 - 1 + r) * p.ld_in;
+    for (int x = tid - 1; x <= nx; x += nt) {
+      const double v = src[x];
+      A[(size_t)r * P + x + 2] = v;
+      B[(size_t)r * P + x + 2] = v;
+    }
+  }
+  for (int r = 0; r < R; ++r)
+    for (int x = tid; x < nx; x += nt) F[(size_t)r * nx + x] = p.rhs[(int64_t)(y0 + r) * p.ld_rhs + x];
+  if (tid == 0) flags[c] = 0ull;
+  __threadfence();
+  grid.sync();
+
+  int entry = 0;
+  for (int s = 0; s < p.nsweeps; ++s) {
+    const bool rec = p.every > 0 && s % p.every == 0;
+    unsigned long long mx = 0ull;
+    double ss = 0.0;
+    rs_rows<ST, true>(A, B, F, P, nx, R, p.scale, p.lambda, mx, ss);
+    if (rec) {
+      rs_block_reduce(mx, ss, part + ((size_t)entry * G + c) * 2);
+      ++entry;
+    } else {
+      __syncthreads();
+    }
+    // publish the first and last new rows; raise the flag
+    const int slot = (s + 1) & 1;
+    double* mine = pub + (size_t)(slot * G + c) * 2 * nx;
+    for (int x = tid; x < nx; x += nt) {
+      __stcg(mine + x, B[P + x + 2]);
+      __stcg(mine + nx + x, B[(size_t)R * P + x + 2]);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      st_release(flags + c, (unsigned long long)(s + 1));
+    }
+    // wait for the neighbours' rows of φ^{s+1}
+    if (tid == 0 && top_x)
+      while (ld_acquire(flags + up) < (unsigned long long)(s + 1)) {
+      }
+    if (tid == 32 && bot_x)
+      while (ld_acquire(flags + dn) < (unsigned long long)(s + 1)) {
+      }
+    __syncthreads();
+    const double* fu = pub + ((size_t)(slot * G + up) * 2 + 1) * nx;  // up's last row
+    const double* fd = pub + ((size_t)(slot * G + dn) * 2) * nx;      // dn's first row
+    for (int x = tid; x < nx; x += nt) {
+      if (top_x) B[x + 2] = __ldcg(fu + x);
+      else if (p.ymode[0] == GH_REFLECT) B[x + 2] = -B[P + x + 2];
+      if (bot_x) B[(size_t)(R + 1) * P + x + 2] = __ldcg(fd + x);
+      else if (p.ymode[1] == GH_REFLECT) B[(size_t)(R + 1) * P + x + 2] = -B[(size_t)R * P + x + 2];
+    }
+    __syncthreads();
+    for (int r = tid; r < R + 2; r += nt) rs_xghost(B + (size_t)r * P, nx, xm);
+    __syncthreads();
+    double* t = A;
+    A = B;
+    B = t;
+  }
+  if (p.final_norm) {
+    unsigned long long mx = 0ull;
+    double ss = 0.0;
+    rs_rows<ST, false>(A, nullptr, F, P, nx, R, p.scale, p.lambda, mx, ss);
+    rs_block_reduce(mx, ss, part + ((size_t)entry * G + c) * 2);
+    ++entry;
+  }
+  __threadfence();
+  grid.sync();
+  // entries reduced over the CTAs in fixed order
+  for (int e = c; e < entry; e += G) {
+    unsigned long long m = 0ull;
+    double t = 0.0;
+    for (int i = tid; i < G; i += nt) {
+      m = umax64(m, (unsigned long long)__double_as_longlong(__ldcg(part + ((size_t)e * G + i) * 2)));
+      t = t + __ldcg(part + ((size_t)e * G + i) * 2 + 1);
+    }
+    double out[2];
+    rs_block_reduce(m, t, out);
+    if (tid == 0) {
+      p.d_max[e] = out[0];
+      p.d_sum[e] = out[1];
+    }
+  }
+  // φ^N (with its ghost columns) back to HBM; the face ghost rows too
+  for (int r = 1; r <= R; ++r) {
+    double* dst = p.phi_out + (int64_t)(y0 - 1 + r) * p.ld_out;
+    for (int x = tid - 1; x <= nx; x += nt) dst[x] = A[(size_t)r * P + x + 2];
+  }
+  if (c == 0)
+    for (int x = tid - 1; x <= nx; x += nt) p.phi_out[-p.ld_out + x] = A[x + 2];
+  if (c == G - 1)
+    for (int x = tid - 1; x <= nx; x += nt) p.phi_out[(int64_t)p.ny * p.ld_out + x] = A[(size_t)(R + 1) * P + x + 2];
+}
+
+size_t resident_ws_doubles(int nx, int grid, int n_entries) {
+  return (size_t)grid + (size_t)2 * grid * 2 * nx + (size_t)(n_entries > 0 ? n_entries : 1) * grid * 2;
+}
+
+static int rs_nsm(int* smem_optin) {
+  static int n = 0, opt = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    if (cudaDeviceGetAttribute(&opt, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || opt <= 0)
+      opt = 227 * 1024;
+    cudaGetLastError();
+  }
+  *smem_optin = opt;
+  return n;
+}
+
+bool resident_plan(int nx, int ny, int* grid, int* rmax, size_t* smem) {
+  if (nx < 2 || ny < 1 || (nx & 1)) return false;
+  int optin = 0;
+  const int nsm = rs_nsm(&optin);
+  const int G = ny < nsm ? ny : nsm;
+  const int R = (ny + G - 1) / G;
+  const size_t bytes = ((size_t)2 * (R + 2) * (nx + 4) + (size_t)R * nx) * sizeof(double);
+  // leave room for the static shared arrays of the reduction
+  if (bytes + 1024 > (size_t)optin) return false;
+  *grid = G;
+  *rmax = R;
+  *smem = bytes;
+  return true;
+}
+
+px_status launch_resident(int stencil, const ResidentLaunch& r, int grid, size_t smem, cudaStream_t s) {
+  static size_t attr_set[2] = {0, 0};
+  const int k = stencil ? 1 : 0;
+  if (attr_set[k] < smem) {
+    cudaError_t e = k ? cudaFuncSetAttribute(k_resident<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                      : cudaFuncSetAttribute(k_resident<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_check(e, "resident kernel smem attribute");
+    attr_set[k] = smem;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(RS_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = k ? cudaLaunchKernelEx(&cfg, k_resident<1>, r) : cudaLaunchKernelEx(&cfg, k_resident<0>, r);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  count_launches(1);
+  return cuda_check(e, "resident solve kernel launch");
+}
+
+}  // namespace px

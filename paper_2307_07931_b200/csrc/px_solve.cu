@@ -148,7 +148,9 @@ struct Plan {
   cudaGraphExec_t exec = nullptr;
   int64_t launches_per_run = 0;
   cudaEvent_t ev_bnd = nullptr, ev_comm = nullptr;
+  double* d_res = nullptr;      // shared-memory-resident solve: flags, row mailboxes, partials
   ~Plan() {
+    if (d_res) cudaFree(d_res);
     if (exec) cudaGraphExecDestroy(exec);
     if (d_max) cudaFree(d_max);
     if (d_sum) cudaFree(d_sum);
@@ -157,6 +159,17 @@ struct Plan {
     if (ev_comm) cudaEventDestroy(ev_comm);
   }
 };
+
+// PROTOX_RESIDENT=0 (read once) disables the shared-memory-resident solve
+// (A/B against the L2 persistent kernel).
+static bool resident_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PROTOX_RESIDENT");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
 
 static std::vector<std::unique_ptr<Plan>>& plans() {
   static std::vector<std::unique_ptr<Plan>> v;
@@ -361,6 +374,37 @@ static px_status enqueue_solve(const SolveCtx& x) {
     px_local_info li;
     PX_TRY(local_info(x.l, 0, &li));
     const int32_t nx = ext(li.owned, 0), ny = ext(li.owned, 1);
+    int rgrid = 0, rmax = 0;
+    size_t rsmem = 0;
+    if (resident_enabled() && resident_plan(nx, ny, &rgrid, &rmax, &rsmem)) {
+      // the iterate fits in the SMs' shared memory: it stays there for all N sweeps
+      ResidentLaunch rl;
+      std::memset(&rl, 0, sizeof rl);
+      const px_patch& A = x.phi[0];
+      const px_patch& B = (N & 1) ? x.scr[0] : x.phi[0];
+      rl.phi_in = at(A, li.owned.lo.c[0], li.owned.lo.c[1]);
+      rl.phi_out = at(B, li.owned.lo.c[0], li.owned.lo.c[1]);
+      rl.rhs = at(x.rhs[0], li.owned.lo.c[0], li.owned.lo.c[1]);
+      rl.ld_in = A.ld;
+      rl.ld_out = B.ld;
+      rl.ld_rhs = x.rhs[0].ld;
+      rl.nx = nx;
+      rl.ny = ny;
+      rl.rmax = rmax;
+      const int m = x.l->bc == PX_BC_PERIODIC ? GH_WRAP : x.l->bc == PX_BC_DIRICHLET_CC ? GH_REFLECT : GH_NONE;
+      rl.xmode[0] = rl.xmode[1] = rl.ymode[0] = rl.ymode[1] = m;
+      rl.scale = stencil_scale(x.p->stencil, x.p->h);
+      rl.lambda = x.p->lambda;
+      rl.nsweeps = N;
+      rl.every = E;
+      rl.final_norm = E >= 0;
+      rl.n_entries = plan->n_entries;
+      rl.d_max = plan->d_max;
+      rl.d_sum = plan->d_sum;
+      if (!plan->d_res) return fail(PX_ERR_STATE, "resident workspace missing from the plan");
+      rl.ws = plan->d_res;
+      return launch_resident(x.p->stencil, rl, rgrid, rsmem, x.s);
+    }
     if ((int64_t)nx * ny < (int64_t)4 * 1024 * 1024) {
       PersistLaunch pl;
       std::memset(&pl, 0, sizeof pl);
@@ -716,10 +760,15 @@ px_status px_exchange_ghosts_local(const px_layout* l, const px_patch* parts, vo
   return local_rows(l, parts, s);
 }
 
-px_status px_solve(const px_layout* l, px_comm* c, int32_t rank, const px_relax_params* p,
-                   const px_solve_opts* o, px_patch* phi, px_patch* phi_scratch,
-                   const px_patch* rhs, double* h_norms, int32_t cap, int32_t* n_written,
-                   int32_t* in_scratch, void* stream) {
+}  // extern "C"
+
+// Validate, find or build the plan, and enqueue the N sweeps on `stream`
+// (graph replay or direct launches).  Nothing is synchronised: the recorded
+// norms are in plan->d_max/d_sum and φ^N is in phi_scratch iff *odd.
+static px_status solve_enqueue(const px_layout* l, px_comm* c, int32_t rank, const px_relax_params* p,
+                               const px_solve_opts* o, px_patch* phi, px_patch* phi_scratch,
+                               const px_patch* rhs, void* stream, Plan** plan_out, bool* odd_out,
+                               int32_t* nparts_out) {
   if (!l || !p || !o || !phi || !phi_scratch || !rhs) return fail(PX_ERR_ARG, "null argument");
   if (o->nsweeps < 0) return fail(PX_ERR_ARG, "nsweeps must be >= 0");
   if (!(p->h > 0.0)) return fail(PX_ERR_ARG, "h must be positive");
@@ -736,7 +785,6 @@ px_status px_solve(const px_layout* l, px_comm* c, int32_t rank, const px_relax_
     if (ext(l->domain, 0) % 2)
       return fail(PX_ERR_UNSUPPORTED, "temporal blocking needs an even domain width");
   }
-  if (cap < 0 || (cap > 0 && !h_norms)) return fail(PX_ERR_ARG, "bad norm output");
   int32_t nparts = 1;
   if (c) {
     if (c->nranks != l->nranks || c->rank != rank)
@@ -795,6 +843,17 @@ px_status px_solve(const px_layout* l, px_comm* c, int32_t rank, const px_relax_
     PX_TRY(cuda_check(cudaMalloc(&np->d_sum, ne * sizeof(double)), "cudaMalloc ring"));
     PX_TRY(cuda_check(cudaMalloc(&np->d_ws, np->ws_len * sizeof(double)), "cudaMalloc ws"));
     PX_TRY(cuda_check(cudaMemset(np->d_ws, 0, np->ws_len * sizeof(double)), "memset ws"));
+    {  // workspace of the shared-memory-resident solve (allocated here: not during graph capture)
+      px_local_info l0;
+      PX_TRY(local_info(l, c ? rank : 0, &l0));
+      int rg = 0, rm = 0;
+      size_t rsm = 0;
+      if (!c && nparts == 1 && l->nranks == 1 && o->temporal_k <= 1 && o->nsweeps > 0 &&
+          resident_plan(ext(l0.owned, 0), ext(l0.owned, 1), &rg, &rm, &rsm))
+        PX_TRY(cuda_check(cudaMalloc(&np->d_res, resident_ws_doubles(ext(l0.owned, 0), rg, np->n_entries) *
+                                                     sizeof(double)),
+                          "cudaMalloc resident workspace"));
+    }
     PX_TRY(cuda_check(cudaEventCreateWithFlags(&np->ev_bnd, cudaEventDisableTiming), "event"));
     PX_TRY(cuda_check(cudaEventCreateWithFlags(&np->ev_comm, cudaEventDisableTiming), "event"));
     plan = np.get();
@@ -830,17 +889,34 @@ px_status px_solve(const px_layout* l, px_comm* c, int32_t rank, const px_relax_
   } else {
     PX_TRY(enqueue_solve(x));
   }
+  // φ^N is in the buffer the last pass wrote: one buffer swap per sweep, or
+  // per temporal-blocking pass of K sweeps plus one per remaining sweep.
+  const int32_t K = o->temporal_k > 1 ? o->temporal_k : 1;
+  const int32_t nswaps = K > 1 ? o->nsweeps / K + o->nsweeps % K : o->nsweeps;
+  *plan_out = plan;
+  *odd_out = (nswaps % 2) == 1;
+  *nparts_out = nparts;
+  return PX_OK;
+}
+
+extern "C" {
+
+px_status px_solve(const px_layout* l, px_comm* c, int32_t rank, const px_relax_params* p,
+                   const px_solve_opts* o, px_patch* phi, px_patch* phi_scratch,
+                   const px_patch* rhs, double* h_norms, int32_t cap, int32_t* n_written,
+                   int32_t* in_scratch, void* stream) {
+  if (cap < 0 || (cap > 0 && !h_norms)) return fail(PX_ERR_ARG, "bad norm output");
+  Plan* plan = nullptr;
+  bool odd = false;
+  int32_t nparts = 1;
+  PX_TRY(solve_enqueue(l, c, rank, p, o, phi, phi_scratch, rhs, stream, &plan, &odd, &nparts));
+  cudaStream_t s = (cudaStream_t)stream;
   const int32_t ne = plan->n_entries;
   std::vector<double> hm(ne), hs(ne);
   if (ne > 0) {
     PX_TRY(cuda_check(cudaMemcpyAsync(hm.data(), plan->d_max, ne * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H norms"));
     PX_TRY(cuda_check(cudaMemcpyAsync(hs.data(), plan->d_sum, ne * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H norms"));
   }
-  // φ^N is in the buffer the last pass wrote: one buffer swap per sweep, or
-  // per temporal-blocking pass of K sweeps plus one per remaining sweep.
-  const int32_t K = o->temporal_k > 1 ? o->temporal_k : 1;
-  const int32_t nswaps = K > 1 ? o->nsweeps / K + o->nsweeps % K : o->nsweeps;
-  const bool odd = (nswaps % 2) == 1;
   if (odd && !in_scratch) {
     for (int32_t i = 0; i < nparts; ++i) {
       const px_patch& a = phi_scratch[i];
@@ -922,9 +998,168 @@ px_status px_solve_host(const px_layout* l, const px_relax_params* p, const px_s
   return cuda_check(cudaStreamSynchronize(s), "solve_host");
 }
 
+// Pipelined host path: NSET device buffer sets; the copy-in stream, the
+// compute stream and the copy-out stream are ordered by events so that the
+// H2D of problem i+1 and the D2H of problem i-1 run on the copy engines
+// while problem i is being solved.  Three sets let the H2D of problem i+1
+// and the D2H of problem i-1 run at the same time (full-duplex PCIe).
+constexpr int NSET = 3;
+struct BatchBufs {
+  uint64_t gen = 0;
+  int64_t elems = 0;
+  int32_t ne = 0;
+  double* d[NSET][3] = {};  // phi, scr, rhs per set
+  double* h_ring[NSET] = {};  // pinned (max, sum) staging per set
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_in[NSET] = {}, ev_done[NSET] = {}, ev_free[NSET] = {};
+  void release_fields() {
+    for (auto& set : d)
+      for (auto& q : set) {
+        if (q) cudaFree(q);
+        q = nullptr;
+      }
+    for (auto& h : h_ring) {
+      if (h) cudaFreeHost(h);
+      h = nullptr;
+    }
+    elems = 0;
+    gen = 0;
+    ne = 0;
+  }
+  void release() {
+    release_fields();
+    if (s_in) cudaStreamDestroy(s_in);
+    if (s_out) cudaStreamDestroy(s_out);
+    s_in = s_out = nullptr;
+    auto destroy = [](cudaEvent_t& e) {
+      if (e) cudaEventDestroy(e);
+      e = nullptr;
+    };
+    destroy(ev_start);
+    for (int b = 0; b < NSET; ++b) {
+      destroy(ev_in[b]);
+      destroy(ev_done[b]);
+      destroy(ev_free[b]);
+    }
+  }
+};
+static BatchBufs g_batch;
+
+px_status px_solve_host_batch(const px_layout* l, const px_relax_params* p, const px_solve_opts* o,
+                              int32_t nprob, const double* const* h_phi0, const double* const* h_rho,
+                              double* const* h_phi_out, double* h_norms, int32_t cap, int32_t* n_written,
+                              void* stream) {
+  if (!l || !p || !o || !h_rho || !h_phi_out) return fail(PX_ERR_ARG, "null argument");
+  if (nprob < 0) return fail(PX_ERR_ARG, "nprob must be >= 0");
+  if (cap < 0 || (cap > 0 && !h_norms)) return fail(PX_ERR_ARG, "bad norm output");
+  if (l->nranks != 1) return fail(PX_ERR_UNSUPPORTED, "px_solve_host_batch needs a single-rank layout");
+  if (!stream) return fail(PX_ERR_ARG, "px_solve_host_batch needs a non-default compute stream");
+  for (int32_t i = 0; i < nprob; ++i)
+    if (!h_rho[i] || !h_phi_out[i]) return fail(PX_ERR_ARG, "null host buffer for problem %d", i);
+  if (nprob == 0) return PX_OK;
+  px_local_info li;
+  PX_TRY(local_info(l, 0, &li));
+  BatchBufs& B = g_batch;
+  const int32_t ne = count_entries(o->nsweeps, o->norm_every);
+  if (!B.s_in) {
+    PX_TRY(cuda_check(cudaStreamCreateWithFlags(&B.s_in, cudaStreamNonBlocking), "stream"));
+    PX_TRY(cuda_check(cudaStreamCreateWithFlags(&B.s_out, cudaStreamNonBlocking), "stream"));
+    PX_TRY(cuda_check(cudaEventCreateWithFlags(&B.ev_start, cudaEventDisableTiming), "event"));
+    for (int b = 0; b < NSET; ++b) {
+      PX_TRY(cuda_check(cudaEventCreateWithFlags(&B.ev_in[b], cudaEventDisableTiming), "event"));
+      PX_TRY(cuda_check(cudaEventCreateWithFlags(&B.ev_done[b], cudaEventDisableTiming), "event"));
+      PX_TRY(cuda_check(cudaEventCreateWithFlags(&B.ev_free[b], cudaEventDisableTiming), "event"));
+    }
+  }
+  if (B.elems != li.alloc_elems || B.gen != layout_generation(l) || B.ne < ne) {
+    PX_TRY(cuda_check(cudaDeviceSynchronize(), "sync before realloc"));
+    B.release_fields();
+    const size_t b = li.alloc_elems * sizeof(double);
+    for (auto& set : B.d)
+      for (auto& q : set) {
+        PX_TRY(cuda_check(cudaMalloc(&q, b), "cudaMalloc"));
+        PX_TRY(cuda_check(cudaMemset(q, 0, b), "memset"));
+      }
+    for (auto& h : B.h_ring)
+      PX_TRY(cuda_check(cudaMallocHost(&h, 2 * (size_t)std::max(ne, 1) * sizeof(double)), "cudaMallocHost"));
+    B.elems = li.alloc_elems;
+    B.gen = layout_generation(l);
+    B.ne = std::max(ne, 1);
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const int32_t n0 = ext(li.owned, 0), n1 = ext(li.owned, 1);
+  const size_t w = n0 * sizeof(double), dp = li.ld * sizeof(double);
+  const size_t alloc_bytes = li.alloc_elems * sizeof(double);
+  // the copy streams start after the work already on the compute stream
+  PX_TRY(cuda_check(cudaEventRecord(B.ev_start, s), "event"));
+  PX_TRY(cuda_check(cudaStreamWaitEvent(B.s_in, B.ev_start, 0), "wait"));
+  PX_TRY(cuda_check(cudaStreamWaitEvent(B.s_out, B.ev_start, 0), "wait"));
+  bool pending[NSET] = {};
+  int32_t pend_i[NSET] = {};
+  auto harvest = [&](int b) -> px_status {  // host side of problem pend_i[b]: norms out of staging
+    if (!pending[b]) return PX_OK;
+    PX_TRY(cuda_check(cudaEventSynchronize(B.ev_free[b]), "batch D2H"));
+    const int32_t i = pend_i[b];
+    const int32_t nw = std::min(ne, cap);
+    for (int32_t j = 0; j < nw; ++j) {
+      h_norms[(size_t)i * 2 * cap + 2 * j] = B.h_ring[b][j];
+      h_norms[(size_t)i * 2 * cap + 2 * j + 1] = B.h_ring[b][B.ne + j];
+    }
+    if (n_written) n_written[i] = nw;
+    pending[b] = false;
+    return PX_OK;
+  };
+  for (int32_t i = 0; i < nprob; ++i) {
+    const int b = i % NSET;
+    PX_TRY(harvest(b));  // problem i-NSET has left set b (host wait: its D2H is done)
+    px_patch ph, sc, rh;
+    PX_TRY(px_layout_patch(l, 0, B.d[b][0], &ph));
+    PX_TRY(px_layout_patch(l, 0, B.d[b][1], &sc));
+    PX_TRY(px_layout_patch(l, 0, B.d[b][2], &rh));
+    // ---- copy in (s_in)
+    if (h_phi0 && h_phi0[i]) {
+      PX_TRY(cuda_check(cudaMemcpy2DAsync(at(ph, li.owned.lo.c[0], li.owned.lo.c[1]), dp, h_phi0[i], w, w, n1,
+                                          cudaMemcpyHostToDevice, B.s_in), "H2D phi"));
+    } else {
+      PX_TRY(cuda_check(cudaMemsetAsync(B.d[b][0], 0, alloc_bytes, B.s_in), "zero phi"));
+    }
+    PX_TRY(cuda_check(cudaMemcpy2DAsync(at(rh, li.owned.lo.c[0], li.owned.lo.c[1]), dp, h_rho[i], w, w, n1,
+                                        cudaMemcpyHostToDevice, B.s_in), "H2D rho"));
+    PX_TRY(cuda_check(cudaEventRecord(B.ev_in[b], B.s_in), "event"));
+    // ---- solve (compute stream)
+    PX_TRY(cuda_check(cudaStreamWaitEvent(s, B.ev_in[b], 0), "wait"));
+    if (o->temporal_k > 1) PX_TRY(launch_fill_ghosts(l, 0, rh, s));
+    Plan* plan = nullptr;
+    bool odd = false;
+    int32_t nparts = 1;
+    PX_TRY(solve_enqueue(l, nullptr, 0, p, o, &ph, &sc, &rh, stream, &plan, &odd, &nparts));
+    PX_TRY(cuda_check(cudaEventRecord(B.ev_done[b], s), "event"));
+    // ---- copy out (s_out)
+    PX_TRY(cuda_check(cudaStreamWaitEvent(B.s_out, B.ev_done[b], 0), "wait"));
+    const px_patch& res = odd ? sc : ph;
+    PX_TRY(cuda_check(cudaMemcpy2DAsync(h_phi_out[i], w, at(res, li.owned.lo.c[0], li.owned.lo.c[1]), dp, w, n1,
+                                        cudaMemcpyDeviceToHost, B.s_out), "D2H phi"));
+    if (plan->n_entries > 0) {
+      PX_TRY(cuda_check(cudaMemcpyAsync(B.h_ring[b], plan->d_max, plan->n_entries * sizeof(double),
+                                        cudaMemcpyDeviceToHost, B.s_out), "D2H norms"));
+      PX_TRY(cuda_check(cudaMemcpyAsync(B.h_ring[b] + B.ne, plan->d_sum, plan->n_entries * sizeof(double),
+                                        cudaMemcpyDeviceToHost, B.s_out), "D2H norms"));
+    }
+    PX_TRY(cuda_check(cudaEventRecord(B.ev_free[b], B.s_out), "event"));
+    pending[b] = true;
+    pend_i[b] = i;
+  }
+  // join: the compute stream ends after the last copy out
+  for (int b = 0; b < NSET; ++b)
+    if (pending[b]) PX_TRY(cuda_check(cudaStreamWaitEvent(s, B.ev_free[b], 0), "wait"));
+  for (int b = 0; b < NSET; ++b) PX_TRY(harvest(b));
+  return cuda_check(cudaStreamSynchronize(s), "solve_host_batch");
+}
+
 void px_release_cached(void) {
   plans().clear();
   g_host.release();
+  g_batch.release();
 }
 
 }  // extern "C"

@@ -152,16 +152,26 @@ struct TbCtx {
   bool own0, own1;  // lane writes / counts these cells
   bool fx0, fx1;    // FIXED ghost columns (keep level-0 values)
   bool xface;       // a written cell is within g of an x face (ghost images)
+  bool img;         // some written cell of this item may have ghost images
 };
+
+// Which time levels record residual norms in this launch: NM = 0 none,
+// 1 level 0 only (a norm every E >= K sweeps, passes aligned to E), 2 any
+// (runtime mask).  Compile-time for 0 / 1 so the steady body carries no
+// per-level tests.
+template <int NM>
+__device__ __forceinline__ bool lvl_act(const bool (&act)[4], int t) {
+  return NM == 2 ? act[t] : (NM == 1 && t == 0);
+}
 
 // Process the R rows of one stage.  CHECK: warm-up / drain stage (row-range
 // conditions evaluated); otherwise every level is computable and every row
 // is an output row (steady state, no per-row conditions).
-template <int ST, int K, int NW, int P2, int FIX, bool CHECK>
+template <int ST, int K, int NW, int P2, int FIX, int NM, bool CHECK>
 __device__ __forceinline__ void tb_stage(const StreamLaunch& a, const TbLaunch& x, const TbCtx& c,
                                          int s, const double* sp, const double* pp, int cl,
                                          P2d (&st)[K][3], unsigned long long (&mx)[K], double (&ss)[K],
-                                         const bool (&act)[K]) {
+                                         const bool (&act)[4]) {
   using G = Geom<K, NW>;
 #pragma unroll
   for (int j = 0; j < R; ++j) {
@@ -188,15 +198,15 @@ __device__ __forceinline__ void tb_stage(const StreamLaunch& a, const TbLaunch& 
         if (fy || c.fx1) o1 = st[t - 1][m3(j - t)].b;
       }
       const bool prow = !CHECK || (p >= c.y0 && p < c.y1);
-      if (act[t - 1] && prow) {
-        if (c.own0) {
-          mx[t - 1] = umax64(mx[t - 1], (unsigned long long)__double_as_longlong(fabs(r0)));
-          ss[t - 1] = fma(r0, r0, ss[t - 1]);
-        }
-        if (c.own1) {
-          mx[t - 1] = umax64(mx[t - 1], (unsigned long long)__double_as_longlong(fabs(r1)));
-          ss[t - 1] = fma(r1, r1, ss[t - 1]);
-        }
+      if (lvl_act<NM>(act, t - 1)) {
+        // branch-free: a cell the lane does not own contributes r = 0
+        // (umax with +0 bits and fma(0, 0, Σ) leave both unchanged)
+        const double q0 = (c.own0 && prow) ? r0 : 0.0;
+        const double q1 = (c.own1 && prow) ? r1 : 0.0;
+        mx[t - 1] = umax64(mx[t - 1], (unsigned long long)__double_as_longlong(fabs(q0)));
+        ss[t - 1] = fma(q0, q0, ss[t - 1]);
+        mx[t - 1] = umax64(mx[t - 1], (unsigned long long)__double_as_longlong(fabs(q1)));
+        ss[t - 1] = fma(q1, q1, ss[t - 1]);
       }
       if (t == K) {
         if (prow) {
@@ -207,7 +217,7 @@ __device__ __forceinline__ void tb_stage(const StreamLaunch& a, const TbLaunch& 
             if (c.own0) dp[0] = o0;
             if (c.own1) dp[1] = o1;
           }
-          if (a.gs.g > 0) {
+          if (c.img) {
             const int Y = p + a.gs.o[1];
             if (c.xface || Y < a.gs.g || Y >= a.gs.n[1] - a.gs.g) {
               if (c.own0) images(a, c.xg, p, o0);
@@ -222,7 +232,7 @@ __device__ __forceinline__ void tb_stage(const StreamLaunch& a, const TbLaunch& 
   }
 }
 
-template <int ST, int K, int NW, int P2, int FIX>
+template <int ST, int K, int NW, int P2, int FIX, int NM>
 __global__ void __launch_bounds__(NW * 32 + 32, (NW == 7 ? 2 : 1))
     k_tb(const StreamLaunch a, const TbLaunch x, int nstrips, int nitems, int crows) {
   using G = Geom<K, NW>;
@@ -241,7 +251,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, (NW == 7 ? 2 : 1))
 
   unsigned long long mx[K];
   double ss[K];
-  bool act[K];
+  bool act[4];
 #pragma unroll
   for (int t = 0; t < K; ++t) {
     mx[t] = 0ull;
@@ -309,6 +319,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, (NW == 7 ? 2 : 1))
       }
       c.y0 = k * crows;
       c.y1 = min(a.ny, c.y0 + crows);
+      c.img = a.gs.g > 0 && (c.xface || c.y0 + a.gs.o[1] < a.gs.g || c.y1 - 1 + a.gs.o[1] >= a.gs.n[1] - a.gs.g);
       c.qbase = c.y0 - K;
       c.nrows = c.y1 - c.y0 + 2 * K;
       const int nst = (c.nrows + R - 1) / R;
@@ -323,9 +334,9 @@ __global__ void __launch_bounds__(NW * 32 + 32, (NW == 7 ? 2 : 1))
         const double* sp = smem + (size_t)slot * G::STAGE;
         const bool steady = (s * R >= 2 * K) && (s * R + R - 1 < c.nrows - K);
         if (steady)
-          tb_stage<ST, K, NW, P2, FIX, false>(a, x, c, s, sp, pp, cl, st, mx, ss, act);
+          tb_stage<ST, K, NW, P2, FIX, NM, false>(a, x, c, s, sp, pp, cl, st, mx, ss, act);
         else
-          tb_stage<ST, K, NW, P2, FIX, true>(a, x, c, s, sp, pp, cl, st, mx, ss, act);
+          tb_stage<ST, K, NW, P2, FIX, NM, true>(a, x, c, s, sp, pp, cl, st, mx, ss, act);
         __syncwarp();
         if (prev >= 0 && lane == 0) mb_arrive(&empty[prev]);  // stage s-1 no longer needed
         prev = slot;
@@ -342,7 +353,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, (NW == 7 ? 2 : 1))
   }
 #pragma unroll
   for (int t = 0; t < K; ++t) {
-    if (act[t]) {
+    if (lvl_act<NM>(act, t)) {
       reduce_norms(x.lvl[t], mx[t], ss[t]);
       __syncthreads();
     }
@@ -417,19 +428,29 @@ static bool pow2(double v) {
   return std::frexp(v, &e) == 0.5;
 }
 
-template <int ST, int K, int NW, int P2, int FIX>
-static cudaError_t tb_launch_nw(const StreamLaunch& a, const TbLaunch& x, cudaStream_t s) {
+template <int ST, int K, int NW, int P2, int FIX, int NM>
+static cudaError_t tb_launch_nm(const StreamLaunch& a, const TbLaunch& x, cudaStream_t s) {
   using G = Geom<K, NW>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_tb<ST, K, NW, P2, FIX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_tb<ST, K, NW, P2, FIX, NM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)G::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const TbPlan g = tb_plan(K, a.nx, a.ny);
-  k_tb<ST, K, NW, P2, FIX><<<g.grid, G::THREADS, G::SMEM, s>>>(a, x, g.nstrips, g.nitems, g.crows);
+  k_tb<ST, K, NW, P2, FIX, NM><<<g.grid, G::THREADS, G::SMEM, s>>>(a, x, g.nstrips, g.nitems, g.crows);
   return cudaGetLastError();
+}
+
+template <int ST, int K, int NW, int P2, int FIX>
+static cudaError_t tb_launch_nw(const StreamLaunch& a, const TbLaunch& x, cudaStream_t s) {
+  unsigned mask = 0;
+  for (int t = 0; t < K; ++t)
+    if (x.lvl[t].out_max) mask |= 1u << t;
+  if (mask == 0) return tb_launch_nm<ST, K, NW, P2, FIX, 0>(a, x, s);
+  if (mask == 1) return tb_launch_nm<ST, K, NW, P2, FIX, 1>(a, x, s);
+  return tb_launch_nm<ST, K, NW, P2, FIX, 2>(a, x, s);
 }
 
 template <int ST, int K, int P2, int FIX>

@@ -88,7 +88,7 @@ EXPORTS = [
     "px_comm_unique_id", "px_comm_create", "px_comm_destroy", "px_comm_allreduce_norms",
     "px_comm_enable_p2p",
     "px_exchange_ghosts", "px_exchange_ghosts_local",
-    "px_solve", "px_solve_host", "px_release_cached", "px_kernel_launch_count",
+    "px_solve", "px_solve_host", "px_solve_host_batch", "px_release_cached", "px_kernel_launch_count",
     "px_relax_variant", "px_stream_ceiling",
 ]
 
@@ -167,6 +167,9 @@ def lib():
     L.px_solve_host.restype = st
     L.px_solve_host.argtypes = [vp, P(px_relax_params), P(px_solve_opts), vp, vp, vp,
                                 P(ctypes.c_double), i32, P(i32), vp]
+    L.px_solve_host_batch.restype = st
+    L.px_solve_host_batch.argtypes = [vp, P(px_relax_params), P(px_solve_opts), i32, vp, vp, vp,
+                                      P(ctypes.c_double), i32, P(i32), vp]
     L.px_release_cached.restype = None
     L.px_kernel_launch_count.restype = i64
     L.px_stream_ceiling.restype = st
@@ -436,6 +439,39 @@ def solve_host(layout: Layout, p: px_relax_params, nsweeps: int, norm_every: int
                                norms.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), cap,
                                ctypes.byref(nw), _stream(stream)))
     return out, norms[: nw.value].copy()
+
+
+def solve_host_batch(layout: Layout, p: px_relax_params, nsweeps: int, norm_every: int,
+                     rhos, outs, phi0s=None, use_graph: bool = True, stream=None, temporal_k: int = 1):
+    """px_solve_host_batch: len(rhos) independent problems from host arrays,
+    copies overlapped with the solves.  rhos/outs/phi0s: lists of (n1, n0)
+    float64 numpy arrays (pinned torch CPU tensors via .numpy() for overlap);
+    phi0s None (or None entries) = zero initial guess.  Returns the list of
+    per-problem norm arrays."""
+    n = len(rhos)
+    if len(outs) != n or (phi0s is not None and len(phi0s) != n):
+        raise ValueError("rhos, outs and phi0s must have the same length")
+    keep = [np.ascontiguousarray(r, dtype=np.float64) for r in rhos]
+    for o in outs:
+        if not (o.flags.c_contiguous and o.dtype == np.float64):
+            raise ValueError("outs must be C-contiguous float64 arrays")
+    VP = ctypes.c_void_p * max(n, 1)
+    a_rho = VP(*[r.ctypes.data for r in keep])
+    a_out = VP(*[o.ctypes.data for o in outs])
+    a_phi = None
+    if phi0s is not None:
+        keep0 = [None if q is None else np.ascontiguousarray(q, dtype=np.float64) for q in phi0s]
+        a_phi = VP(*[None if q is None else q.ctypes.data for q in keep0])
+    cap = 0 if norm_every < 0 else ((nsweeps + norm_every - 1) // norm_every if norm_every > 0 else 0) + 1
+    norms = np.zeros((max(n, 1), max(cap, 1), 2), dtype=np.float64)
+    nw = (ctypes.c_int32 * max(n, 1))()
+    opts = px_solve_opts(nsweeps, norm_every, temporal_k, int(use_graph))
+    _check(lib().px_solve_host_batch(layout.h, ctypes.byref(p), ctypes.byref(opts), n,
+                                     ctypes.cast(a_phi, ctypes.c_void_p) if a_phi is not None else None,
+                                     ctypes.cast(a_rho, ctypes.c_void_p), ctypes.cast(a_out, ctypes.c_void_p),
+                                     norms.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), cap, nw,
+                                     _stream(stream)))
+    return [norms[i, : nw[i]].copy() for i in range(n)]
 
 
 def release_cached():

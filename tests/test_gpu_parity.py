@@ -185,6 +185,38 @@ def test_solve_ragged_multibox(bc, st, graph):
     _check_norms(norms, rn)
 
 
+@pytest.mark.parametrize("shape", [(130, 400), (1022, 149), (4, 5000)])
+@pytest.mark.parametrize("bc", [P.PX_BC_PERIODIC, P.PX_BC_DIRICHLET_CC, P.PX_BC_FIXED_GHOSTS])
+@pytest.mark.parametrize("st", [P.PX_LAPLACE_5PT, P.PX_MEHRSTELLEN_9PT])
+def test_solve_resident_shapes(shape, bc, st):
+    """Shared-memory-resident solve (k_resident): uneven rows per CTA, one
+    row per CTA, 34 rows x 2 column pairs per CTA; even and odd sweep counts;
+    norms every 4."""
+    n0, n1 = shape
+    h = 1.0 / 1024
+    lam = h * h / 8 if st == 0 else 3 * h * h / 16
+    phi0, rho = _fields(n0, n1, 1, 17, bc)
+    for N in (10, 13):
+        out, norms, _ = run_gpu_solve(n0, n1, h, lam, bc, st, N, 4, phi0, rho)
+        ref, rn = oracle.solve(_orc_problem(n0, n1, h, lam, bc, st, N, 4), phi0, rho)
+        assert bits_equal(out, ref[1:-1, 1:-1]), ulp_diff(out, ref[1:-1, 1:-1])
+        _check_norms(norms, rn)
+
+
+@pytest.mark.parametrize("bc", [P.PX_BC_PERIODIC, P.PX_BC_DIRICHLET_CC, P.PX_BC_FIXED_GHOSTS])
+def test_solve_persistent_path(bc):
+    """2500 x 300 does not fit the SMs' shared memory and is below the TMA
+    kernel's size: the L2 persistent cooperative kernel (k_persist) runs."""
+    n0, n1, N, E = 2500, 300, 9, 2
+    h = 1.0 / 2048
+    lam = h * h / 8
+    phi0, rho = _fields(n0, n1, 1, 23, bc)
+    out, norms, _ = run_gpu_solve(n0, n1, h, lam, bc, 0, N, E, phi0, rho, box=(500, 100))
+    ref, rn = oracle.solve(_orc_problem(n0, n1, h, lam, bc, 0, N, E, b0=500, b1=100), phi0, rho)
+    assert bits_equal(out, ref[1:-1, 1:-1]), ulp_diff(out, ref[1:-1, 1:-1])
+    _check_norms(norms, rn)
+
+
 @pytest.mark.parametrize("nranks", [2, 3, 4, 5, 8])
 @pytest.mark.parametrize("bc", [P.PX_BC_PERIODIC, P.PX_BC_DIRICHLET_CC, P.PX_BC_FIXED_GHOSTS])
 @pytest.mark.parametrize("st", [P.PX_LAPLACE_5PT, P.PX_MEHRSTELLEN_9PT])
@@ -256,6 +288,44 @@ def test_solve_host_e2e_matches_oracle():
     ref, rn = oracle.solve(_orc_problem(n0, n1, h, lam, P.PX_BC_PERIODIC, 0, N, 5), phi0, rho)
     assert bits_equal(out, ref[1:-1, 1:-1])
     _check_norms(norms, rn)
+
+
+@pytest.mark.parametrize("tk", [1, 4])
+def test_solve_host_batch_matches_oracle(tk):
+    """Pipelined host-buffer batch: each problem bit-identical to its own
+    oracle solve; φ0 = NULL means zero; an odd sweep count leaves φ^N in the
+    scratch buffer (the D2H must pick it)."""
+    n0, n1, N, E = 256, 96, 19, 4
+    g = 4 if tk > 1 else 1
+    h = 1.0 / 256
+    lam = h * h / 8
+    lay = P.Layout(P.box(0, 0, n0 - 1, n1 - 1), (64, 32), g, P.PX_BC_PERIODIC, 1)
+    probs = [_fields(n0, n1, g, 40 + i, P.PX_BC_PERIODIC) for i in range(5)]
+    phi0s = [None if i % 2 == 0 else probs[i][0] for i in range(5)]
+    rhos = [torch.from_numpy(np.ascontiguousarray(pr[1][g:g + n1, g:g + n0])).pin_memory() for pr in probs]
+    outs = [torch.empty((n1, n0), dtype=torch.float64).pin_memory() for _ in probs]
+    p0 = [None if q is None else np.ascontiguousarray(q[g:g + n1, g:g + n0]) for q in phi0s]
+    s = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    for rep in range(2):  # second call replays the cached plans / buffers
+        norms = P.solve_host_batch(lay, P.relax_params(h, lam), N, E, [r.numpy() for r in rhos],
+                                   [o.numpy() for o in outs], p0, stream=s, temporal_k=tk)
+        for i, (phi0, rho) in enumerate(probs):
+            if phi0s[i] is None:
+                phi0 = np.zeros_like(phi0)
+            ref, rn = oracle.solve(_orc_problem(n0, n1, h, lam, P.PX_BC_PERIODIC, 0, N, E, b0=64, b1=32, g=g),
+                                   phi0, rho)
+            assert bits_equal(outs[i].numpy(), ref[g:g + n1, g:g + n0]), (rep, i)
+            _check_norms(norms[i], rn)
+
+
+def test_solve_host_batch_errors():
+    lay = P.Layout(P.box(0, 0, 63, 63), (64, 64), 1, P.PX_BC_PERIODIC, 1)
+    a = np.zeros((64, 64))
+    with pytest.raises(P.PxError):
+        P.solve_host_batch(lay, P.relax_params(1 / 64, 1 / 64 ** 2 / 8), 4, 1, [a], [a.copy()], stream=0)
+    assert P.solve_host_batch(lay, P.relax_params(1 / 64, 1 / 64 ** 2 / 8), 4, 1, [], [],
+                              stream=torch.cuda.Stream()) == []
 
 
 # ------------------------------------------------------------ other ops
