@@ -339,6 +339,35 @@ px_status px_solve_host_batch(const px_layout* l, const px_relax_params* p, cons
                               void* stream);
 void px_release_cached(void);
 
+/* Multigrid V-cycle with the fused relax sweep as smoother (SURVEY §8(f)
+ * NEXT rank 2; multigrid is a Proto use of stencils, and ProtoX
+ * future work; the cycle itself is DESIGN.md readings
+ * R-MG1..R-MG6).  Levels l = 0..levels-1 with (n0 >> l) x (n1 >> l) cells,
+ * h_l = 2^l h, λ_l = 4^l λ, the stencil of p and the layout's boundary rule
+ * (homogeneous on l >= 1).  V(l): on the coarsest level nu_coarse sweeps;
+ * else nu1 sweeps, f_{l+1} = −R(scale·S(φ_l) − f_l) (2x2 average),
+ * φ_{l+1} = 0, V(l+1), φ_l += P φ_{l+1} (cell-centred bilinear), nu2 sweeps.
+ * Single-rank layout, PERIODIC or DIRICHLET_CC; n0, n1 divisible by
+ * 2^(levels-1), else PX_ERR_SHAPE.  phi holds φ^0 on entry (ghosts need not
+ * be filled) and the result (with its ghost ring) on return; phi_scratch is
+ * a second caller buffer of the same layout; rhs holds f on the owned cells.
+ * Coarse-level buffers are library-owned, cached per (layout, params, opts,
+ * pointers, stream) with the CUDA graph of the whole solve (use_graph),
+ * freed by px_mg_release / px_release_cached.  h_norms[2k], [2k+1] =
+ * (max|r|, Σr²) of the finest iterate after k cycles, k = 0..ncycles.
+ * Host-synchronous.  Bit-identical to the oracle's orc_mg_solve. */
+typedef struct {
+  int32_t levels;
+  int32_t nu1, nu2;
+  int32_t nu_coarse;
+  int32_t ncycles;
+  int32_t use_graph;
+} px_mg_opts;
+px_status px_mg_solve(const px_layout* l, const px_relax_params* p, const px_mg_opts* o, px_patch* phi,
+                      px_patch* phi_scratch, const px_patch* rhs, double* h_norms, int32_t cap,
+                      int32_t* n_written, void* stream);
+void px_mg_release(void);
+
 /* Diagnostics: number of kernel launches libprotox enqueued so far in this
  * process (graph replays count their kernel nodes). */
 int64_t px_kernel_launch_count(void);

@@ -51,6 +51,11 @@ class _Problem(ctypes.Structure):
     ]
 
 
+class _MG(ctypes.Structure):
+    _fields_ = [("levels", ctypes.c_int64), ("nu1", ctypes.c_int64), ("nu2", ctypes.c_int64),
+                ("nu_coarse", ctypes.c_int64), ("ncycles", ctypes.c_int64)]
+
+
 _lib = None
 
 
@@ -76,6 +81,9 @@ def _L():
         _lib.orc_stencil_taps.restype = i64
         _lib.orc_box_ordinal.argtypes = [i64] * 6
         _lib.orc_box_ordinal.restype = i64
+        _lib.orc_mg_solve.argtypes = [P, ctypes.POINTER(_MG), d, d, d, d, i64, ctypes.POINTER(i64)]
+        _lib.orc_mg_restrict.argtypes = [i64, i64, d, d]
+        _lib.orc_mg_prolong.argtypes = [i64, i64, ctypes.c_int32, d, d]
         _lib.orc_neumaier_sum.argtypes = [d, i64]
         _lib.orc_neumaier_sum.restype = ctypes.c_double
     return _lib
@@ -227,3 +235,48 @@ def box_ordinal(lo, hi, p) -> int:
 def neumaier_sum(x: np.ndarray) -> float:
     x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1)
     return float(_L().orc_neumaier_sum(_dp(x), x.size))
+
+
+# --------------------------------------------------------------- multigrid
+@dataclass
+class MG:
+    """V(nu1, nu2)-cycle options (readings R-MG1..R-MG6)."""
+    levels: int
+    nu1: int = 2
+    nu2: int = 2
+    nu_coarse: int = 4
+    ncycles: int = 1
+
+
+def mg_solve(p: Problem, m: MG, phi0_g: np.ndarray, rho_g: np.ndarray):
+    """m.ncycles V-cycles.  Returns (phi_g, norms) with norms[k] = (max|r|,
+    sum r^2) of the finest iterate after k cycles, k = 0..ncycles."""
+    phi0_g = np.ascontiguousarray(phi0_g, dtype=np.float64)
+    rho_g = np.ascontiguousarray(rho_g, dtype=np.float64)
+    assert phi0_g.shape == p.gshape and rho_g.shape == p.gshape
+    out = np.zeros(p.gshape, dtype=np.float64)
+    norms = np.zeros((m.ncycles + 1, 2), dtype=np.float64)
+    nw = ctypes.c_int64(0)
+    pc, mc = p.c(), _MG(m.levels, m.nu1, m.nu2, m.nu_coarse, m.ncycles)
+    _check(_L().orc_mg_solve(ctypes.byref(pc), ctypes.byref(mc), _dp(phi0_g), _dp(rho_g), _dp(out),
+                             _dp(norms), m.ncycles + 1, ctypes.byref(nw)))
+    return out, norms[: nw.value]
+
+
+def mg_restrict(d: np.ndarray) -> np.ndarray:
+    """-R d: minus the 2x2 average of a fine (n1, n0) array."""
+    d = np.ascontiguousarray(d, dtype=np.float64)
+    n1, n0 = d.shape
+    out = np.zeros((n1 // 2, n0 // 2), dtype=np.float64)
+    _check(_L().orc_mg_restrict(n0, n1, _dp(d), _dp(out)))
+    return out
+
+
+def mg_prolong(e: np.ndarray, fine: np.ndarray, bc: int) -> np.ndarray:
+    """fine + P e (cell-centred bilinear, coarse ghosts by the rule bc)."""
+    e = np.ascontiguousarray(e, dtype=np.float64)
+    f = np.array(fine, dtype=np.float64, order="C", copy=True)
+    nc1, nc0 = e.shape
+    assert f.shape == (2 * nc1, 2 * nc0)
+    _check(_L().orc_mg_prolong(nc0, nc1, bc, _dp(e), _dp(f)))
+    return f

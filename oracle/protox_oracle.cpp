@@ -43,6 +43,7 @@
  * brute force, spectral N-sweep closed form, exact trajectories, truncation
  * and discretisation order ladders, exchange vs flat periodic array).
  */
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -349,6 +350,100 @@ static void jacobi_iteration(const Stencil& st, Level& phi, const Level& f, doub
   }
 }
 
+/* ------------------------------------------------------------------------
+ * Multigrid V-cycle with the Jacobi sweep as smoother (SURVEY §8(f) NEXT
+ * rank 2; the paper names multigrid as a Proto use of stencils, PAPER.md:25,
+ * and as future work for ProtoX, without defining one).  The
+ * definition written out here is DESIGN.md readings R-MG1..R-MG6:
+ *   levels ℓ = 0..L-1, n_ℓ = n/2^ℓ cells, h_ℓ = 2^ℓ h, same stencil and
+ *   boundary rule on every level (homogeneous on ℓ >= 1), λ_ℓ = 4^ℓ λ;
+ *   V(ℓ): ℓ = L-1: ν_c Jacobi iterations; else ν1 iterations,
+ *         f_{ℓ+1} = −R d_ℓ  with d_ℓ = scale_ℓ·S(φ_ℓ) − f_ℓ (Eq.7),
+ *         φ_{ℓ+1} = 0, V(ℓ+1), φ_ℓ += P φ_{ℓ+1}, ν2 iterations;
+ *   R: average of the 2x2 children, summed in the order (0,0),(1,0),(0,1),(1,1);
+ *   P: cell-centred bilinear, fine cell (2I+a, 2J+b) gets
+ *      (9·e(I,J) + 3·e(I±1,J) + 3·e(I,J±1) + e(I±1,J±1)) / 16, the ± towards
+ *      the fine cell, summed left to right, coarse ghosts by the level's rule.
+ * ---------------------------------------------------------------------- */
+struct MGLevel {
+  Layout L;
+  Stencil st;
+  double lambda = 0.0;
+  std::vector<Level> phi, f;  // one element each (Level holds a pointer to L)
+};
+
+static double level_at(const Level& lev, Point p) {
+  return lev.data[(size_t)lev.L->owner(p)].at(p);
+}
+static double& level_ref(Level& lev, Point p) { return lev.data[(size_t)lev.L->owner(p)].at(p); }
+
+/* f_{ℓ+1} = −R d_ℓ */
+static void restrict_defect(MGLevel& fine, MGLevel& coarse) {
+  Level& phi = fine.phi[0];
+  exchange(phi);
+  const int64_t n0 = fine.L.n[0], n1 = fine.L.n[1];
+  std::vector<double> d((size_t)(n0 * n1));
+  for (size_t ib = 0; ib < fine.L.boxes.size(); ++ib) {
+    const Box& B = fine.L.boxes[ib];
+    for (int64_t y = B.lo.c[1]; y <= B.hi.c[1]; ++y)
+      for (int64_t x = B.lo.c[0]; x <= B.hi.c[0]; ++x) {
+        Point q = pt(x, y);
+        double L = tap_sum(fine.st, phi.data[ib], q);
+        d[(size_t)(x + y * n0)] = fine.st.scale * L - fine.f[0].data[ib].at(q);
+      }
+  }
+  Level& fc = coarse.f[0];
+  for (int64_t J = 0; J < coarse.L.n[1]; ++J)
+    for (int64_t I = 0; I < coarse.L.n[0]; ++I) {
+      const double* r0 = &d[(size_t)(2 * I + 2 * J * n0)];
+      double t = r0[0] + r0[1];
+      t = t + r0[n0];
+      t = t + r0[n0 + 1];
+      level_ref(fc, pt(I, J)) = -0.25 * t;
+    }
+}
+
+/* φ_ℓ += P φ_{ℓ+1} */
+static void prolong_correct(MGLevel& coarse, MGLevel& fine) {
+  Level& e = coarse.phi[0];
+  exchange(e);
+  const BoxData& E = e.data[0];  // coarse levels are one box
+  for (size_t ib = 0; ib < fine.L.boxes.size(); ++ib) {
+    const Box& B = fine.L.boxes[ib];
+    for (int64_t y = B.lo.c[1]; y <= B.hi.c[1]; ++y)
+      for (int64_t x = B.lo.c[0]; x <= B.hi.c[0]; ++x) {
+        const int64_t I = x / 2, J = y / 2;
+        const int64_t xn = (x % 2) ? I + 1 : I - 1, yn = (y % 2) ? J + 1 : J - 1;
+        double t = 9.0 * E.at(pt(I, J));
+        t = t + 3.0 * E.at(pt(xn, J));
+        t = t + 3.0 * E.at(pt(I, yn));
+        t = t + E.at(pt(xn, yn));
+        double v = 0.0625 * t;
+        Point q = pt(x, y);
+        fine.phi[0].data[ib].at(q) = fine.phi[0].data[ib].at(q) + v;
+      }
+  }
+}
+
+struct MGOpts {
+  int64_t levels, nu1, nu2, nu_coarse, ncycles;
+};
+
+static void vcycle(std::vector<MGLevel>& lv, size_t l, const MGOpts& m) {
+  MGLevel& F = lv[l];
+  if (l + 1 == lv.size()) {
+    for (int64_t k = 0; k < m.nu_coarse; ++k) jacobi_iteration(F.st, F.phi[0], F.f[0], F.lambda);
+    return;
+  }
+  for (int64_t k = 0; k < m.nu1; ++k) jacobi_iteration(F.st, F.phi[0], F.f[0], F.lambda);
+  MGLevel& C = lv[l + 1];
+  restrict_defect(F, C);
+  for (BoxData& bd : C.phi[0].data) std::fill(bd.v.begin(), bd.v.end(), 0.0);
+  vcycle(lv, l + 1, m);
+  prolong_correct(C, F);
+  for (int64_t k = 0; k < m.nu2; ++k) jacobi_iteration(F.st, F.phi[0], F.f[0], F.lambda);
+}
+
 }  // namespace orc
 
 using namespace orc;
@@ -562,6 +657,121 @@ int64_t orc_box_ordinal(int64_t lo0, int64_t lo1, int64_t hi0, int64_t hi1, int6
   Box b = mkbox(lo0, lo1, hi0, hi1);
   if (!b.contains(pt(p0, p1))) return -1;
   return b.ordinal(pt(p0, p1));
+}
+
+/* ---- multigrid (readings R-MG1..R-MG6) ---- */
+typedef struct {
+  int64_t levels, nu1, nu2, nu_coarse, ncycles;
+} orc_mg;
+
+/* V-cycles on the problem p (bc PERIODIC or DIRICHLET_CC; n0, n1 divisible
+ * by 2^(levels-1)).  phi0 / rho / phi_out as orc_solve; norms[2k], [2k+1] =
+ * (max|r|, Σr²) of the finest iterate after k cycles, k = 0..ncycles. */
+int orc_mg_solve(const orc_problem* p, const orc_mg* m, const double* phi0, const double* rho,
+                 double* phi_out, double* norms, int64_t cap, int64_t* nwritten) {
+  if (!p || !m) {
+    g_err = "null argument";
+    return 1;
+  }
+  if (m->levels < 1 || m->nu1 < 0 || m->nu2 < 0 || m->nu_coarse < 0 || m->ncycles < 0) {
+    g_err = "bad multigrid options";
+    return 1;
+  }
+  if (p->bc == BC_FIXED) {
+    g_err = "multigrid needs PERIODIC or DIRICHLET_CC";
+    return 1;
+  }
+  const int64_t div = (int64_t)1 << (m->levels - 1);
+  if (p->n0 % div || p->n1 % div) {
+    g_err = "n must be divisible by 2^(levels-1)";
+    return 1;
+  }
+  MGOpts o{m->levels, m->nu1, m->nu2, m->nu_coarse, m->ncycles};
+  std::vector<MGLevel> lv((size_t)m->levels);
+  for (int64_t l = 0; l < m->levels; ++l) {
+    MGLevel& M = lv[(size_t)l];
+    const int64_t s = (int64_t)1 << l;
+    const double h = p->h * (double)s;
+    bool ok = (l == 0) ? make_layout(p->n0, p->n1, p->b0, p->b1, p->ghost, p->bc, M.L)
+                       : make_layout(p->n0 / s, p->n1 / s, p->n0 / s, p->n1 / s, 1, p->bc, M.L);
+    if (!ok) return 1;
+    M.st = (p->stencil == 1) ? mehrstellen9(h) : laplace5(h);
+    M.lambda = p->lambda * (double)(s * s);
+  }
+  for (MGLevel& M : lv) {  // after the vector is final: Level keeps &M.L
+    M.phi.emplace_back(M.L);
+    M.f.emplace_back(M.L);
+  }
+  orc_problem p0 = *p;
+  Layout L0;
+  Stencil st0;
+  if (!build(&p0, L0, st0)) return 1;
+  scatter_global(phi0, lv[0].phi[0]);
+  make_rhs(p, lv[0].L, rho, lv[0].f[0]);
+  int64_t nw = 0;
+  auto record = [&]() {
+    double r[2];
+    residual(lv[0].st, lv[0].phi[0], lv[0].f[0], r);
+    if (nw < cap && norms) {
+      norms[2 * nw] = r[0];
+      norms[2 * nw + 1] = r[1];
+    }
+    ++nw;
+  };
+  record();
+  for (int64_t k = 0; k < m->ncycles; ++k) {
+    vcycle(lv, 0, o);
+    record();
+  }
+  exchange(lv[0].phi[0]);
+  if (phi_out) gather_global(lv[0].phi[0], phi_out);
+  if (nwritten) *nwritten = nw;
+  return 0;
+}
+
+/* Components, for the pins: coarse (n0/2 x n1/2) = −R d of a fine interior
+ * array d (n0 x n1); fine (2nc0 x 2nc1 interior) += P e for a coarse
+ * interior array e with the boundary rule bc. */
+int orc_mg_restrict(int64_t n0, int64_t n1, const double* d, double* coarse) {
+  if (n0 % 2 || n1 % 2) {
+    g_err = "odd extent";
+    return 1;
+  }
+  MGLevel F, C;
+  make_layout(n0, n1, n0, n1, 1, BC_PERIODIC, F.L);
+  make_layout(n0 / 2, n1 / 2, n0 / 2, n1 / 2, 1, BC_PERIODIC, C.L);
+  /* restrict_defect takes d = scale·S(φ) − f: with φ = 0 and f = −d it is d */
+  F.st = laplace5(1.0);
+  F.phi.emplace_back(F.L);
+  F.f.emplace_back(F.L);
+  C.phi.emplace_back(C.L);
+  C.f.emplace_back(C.L);
+  for (int64_t y = 0; y < n1; ++y)
+    for (int64_t x = 0; x < n0; ++x) F.f[0].data[0].at(pt(x, y)) = -d[x + y * n0];
+  restrict_defect(F, C);
+  for (int64_t y = 0; y < n1 / 2; ++y)
+    for (int64_t x = 0; x < n0 / 2; ++x) coarse[x + y * (n0 / 2)] = C.f[0].data[0].at(pt(x, y));
+  return 0;
+}
+
+int orc_mg_prolong(int64_t nc0, int64_t nc1, int32_t bc, const double* e, double* fine) {
+  if (bc == BC_FIXED) {
+    g_err = "prolongation needs PERIODIC or DIRICHLET_CC";
+    return 1;
+  }
+  MGLevel F, C;
+  make_layout(2 * nc0, 2 * nc1, 2 * nc0, 2 * nc1, 1, bc, F.L);
+  make_layout(nc0, nc1, nc0, nc1, 1, bc, C.L);
+  F.phi.emplace_back(F.L);
+  C.phi.emplace_back(C.L);
+  for (int64_t y = 0; y < nc1; ++y)
+    for (int64_t x = 0; x < nc0; ++x) C.phi[0].data[0].at(pt(x, y)) = e[x + y * nc0];
+  for (int64_t y = 0; y < 2 * nc1; ++y)
+    for (int64_t x = 0; x < 2 * nc0; ++x) F.phi[0].data[0].at(pt(x, y)) = fine[x + y * 2 * nc0];
+  prolong_correct(C, F);
+  for (int64_t y = 0; y < 2 * nc1; ++y)
+    for (int64_t x = 0; x < 2 * nc0; ++x) fine[x + y * 2 * nc0] = F.phi[0].data[0].at(pt(x, y));
+  return 0;
 }
 
 double orc_neumaier_sum(const double* x, int64_t n) {

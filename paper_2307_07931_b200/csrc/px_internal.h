@@ -199,6 +199,11 @@ px_status launch_bulk(int mode, int stencil, const StreamLaunch& a, cudaStream_t
 // launchers (px_kernels.cu); return PX_ERR_CUDA on launch failure
 px_status launch_stream(int mode, int stencil, const StreamLaunch& a, cudaStream_t s);
 px_status launch_fill_ghosts(const px_layout* l, int32_t rank, const px_patch& p, cudaStream_t s);
+// ghost fill of an nx x ny region at o (cell (0,0)), depth g: x faces by mode
+// mx for rows [0,ny), then y faces by my_lo / my_hi over the full padded rows
+// (corners by the product rule)
+px_status launch_fill_ghosts_raw(double* o, int64_t ld, int nx, int ny, int g, int mx, int my_lo, int my_hi,
+                                 cudaStream_t s);
 px_status launch_init_field(const px_layout* l, int32_t rank, const px_patch& p, int kind,
                             uint64_t seed, int k, int lw, cudaStream_t s);
 px_status cuda_check(cudaError_t e, const char* what);

@@ -539,15 +539,20 @@ px_status launch_fill_ghosts(const px_layout* l, int32_t rank, const px_patch& p
   if (li.nbr_lo < 0 && l->bc == PX_BC_DIRICHLET_CC) my_lo = GH_REFLECT;
   if (li.nbr_hi < 0 && l->bc == PX_BC_DIRICHLET_CC) my_hi = GH_REFLECT;
   if (l->bc == PX_BC_PERIODIC && l->nranks == 1) my_lo = my_hi = GH_WRAP;
+  return launch_fill_ghosts_raw(o, p.ld, nx, ny, g, mx, my_lo, my_hi, s);
+}
+
+px_status launch_fill_ghosts_raw(double* o, int64_t ld, int nx, int ny, int g, int mx, int my_lo, int my_hi,
+                                 cudaStream_t s) {
   if (mx != GH_NONE) {
     int64_t n = (int64_t)ny * g * 2;
-    k_ghost_x<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(o, p.ld, nx, ny, g, mx, mx);
+    k_ghost_x<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(o, ld, nx, ny, g, mx, mx);
     count_launches(1);
     PX_TRY(cuda_check(cudaGetLastError(), "ghost x launch"));
   }
   if (my_lo != GH_NONE || my_hi != GH_NONE) {
     int64_t n = (int64_t)(nx + 2 * g) * g * 2;
-    k_ghost_y<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(o, p.ld, nx, ny, g, my_lo, my_hi);
+    k_ghost_y<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(o, ld, nx, ny, g, my_lo, my_hi);
     count_launches(1);
     PX_TRY(cuda_check(cudaGetLastError(), "ghost y launch"));
   }

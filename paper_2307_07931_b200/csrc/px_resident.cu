@@ -6,11 +6,12 @@
 // [c·ny/G, (c+1)·ny/G) and keeps them in shared memory for the whole solve:
 // two copies of its rows plus one halo row above and below (with the ghost
 // columns), and its rows of the right-hand side.  A sweep reads and writes
-// shared memory only; then the CTA publishes its first and last new row to
-// L2 (double-buffered by sweep parity), raises its flag (release), waits for
-// the flags of its two neighbours (acquire) and copies their rows into its
-// halo.  No grid-wide barrier per sweep: a CTA synchronises with its two
-// neighbours only.  Domain faces: periodic wrap (the ring of CTAs), odd
+// shared memory only.  The CTA sweeps its first and last row first,
+// publishes them to L2 (double-buffered by sweep parity) and raises its flag
+// (release), sweeps its inner rows while they travel, then waits for the
+// flags of its two neighbours (acquire) and copies their rows into its halo.
+// No grid-wide barrier per sweep: a CTA synchronises with its two neighbours
+// only.  Domain faces: periodic wrap (the ring of CTAs), odd
 // reflection (halo row = −own row), fixed ghosts (kept from φ^0); the ghost
 // columns of every row follow the x rule after each exchange.
 //
@@ -62,18 +63,20 @@ __device__ __forceinline__ double rs_taps(double w, double e, double s, double n
   return __dadd_rn(q, __dmul_rn(-20.0, c));
 }
 
-// Rows 1..R of the CTA's shared block: B = A + λ(scale·L(A) − F) (WRITE), or
-// residual norms of A only.  A thread walks a column pair down the rows with
-// the S/C rows (and their outer neighbours) in registers.
+// Rows rlo..rhi of the CTA's shared block: B = A + λ(scale·L(A) − F)
+// (WRITE), or residual norms of A only.  A thread walks a column pair down
+// the rows with the S/C rows (and their outer neighbours) in registers.
 template <int ST, bool WRITE>
-__device__ __forceinline__ void rs_rows(const double* A, double* B, const double* F, int P, int nx, int R,
-                                        double scale, double lambda, unsigned long long& mx, double& ss) {
+__device__ __forceinline__ void rs_rows(const double* A, double* B, const double* F, int P, int nx, int rlo,
+                                        int rhi, double scale, double lambda, unsigned long long& mx,
+                                        double& ss) {
   for (int q = threadIdx.x; q < nx / 2; q += blockDim.x) {
     const int x = 2 * q + 2;  // shared index of column 2q
-    double2 S = *reinterpret_cast<const double2*>(A + x);
-    double2 C = *reinterpret_cast<const double2*>(A + P + x);
-    double sw = A[x - 1], se = A[x + 2], cw = A[P + x - 1], ce = A[P + x + 2];
-    for (int r = 1; r <= R; ++r) {
+    const double* a0 = A + (size_t)(rlo - 1) * P + x;
+    double2 S = *reinterpret_cast<const double2*>(a0);
+    double2 C = *reinterpret_cast<const double2*>(a0 + P);
+    double sw = a0[-1], se = a0[2], cw = a0[P - 1], ce = a0[P + 2];
+    for (int r = rlo; r <= rhi; ++r) {
       const double* an = A + (size_t)(r + 1) * P + x;
       const double2 N = *reinterpret_cast<const double2*>(an);
       const double nw = an[-1], ne = an[2];
@@ -176,14 +179,11 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resident(const ResidentLaunch
     const bool rec = p.every > 0 && s % p.every == 0;
     unsigned long long mx = 0ull;
     double ss = 0.0;
-    rs_rows<ST, true>(A, B, F, P, nx, R, p.scale, p.lambda, mx, ss);
-    if (rec) {
-      rs_block_reduce(mx, ss, part + ((size_t)entry * G + c) * 2);
-      ++entry;
-    } else {
-      __syncthreads();
-    }
-    // publish the first and last new rows; raise the flag
+    // the first and last rows first: they go to the neighbours, whose copy
+    // overlaps the sweep of the inner rows
+    rs_rows<ST, true>(A, B, F, P, nx, 1, 1, p.scale, p.lambda, mx, ss);
+    if (R > 1) rs_rows<ST, true>(A, B, F, P, nx, R, R, p.scale, p.lambda, mx, ss);
+    __syncthreads();
     const int slot = (s + 1) & 1;
     double* mine = pub + (size_t)(slot * G + c) * 2 * nx;
     for (int x = tid; x < nx; x += nt) {
@@ -191,9 +191,13 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resident(const ResidentLaunch
       __stcg(mine + nx + x, B[(size_t)R * P + x + 2]);
     }
     __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      st_release(flags + c, (unsigned long long)(s + 1));
+    // release at gpu scope: the CTA's row stores (ordered before it by the
+    // barrier) are visible to whoever acquires the flag
+    if (tid == 0) st_release(flags + c, (unsigned long long)(s + 1));
+    if (R > 2) rs_rows<ST, true>(A, B, F, P, nx, 2, R - 1, p.scale, p.lambda, mx, ss);
+    if (rec) {
+      rs_block_reduce(mx, ss, part + ((size_t)entry * G + c) * 2);
+      ++entry;
     }
     // wait for the neighbours' rows of φ^{s+1}
     if (tid == 0 && top_x)
@@ -221,7 +225,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resident(const ResidentLaunch
   if (p.final_norm) {
     unsigned long long mx = 0ull;
     double ss = 0.0;
-    rs_rows<ST, false>(A, nullptr, F, P, nx, R, p.scale, p.lambda, mx, ss);
+    rs_rows<ST, false>(A, nullptr, F, P, nx, 1, R, p.scale, p.lambda, mx, ss);
     rs_block_reduce(mx, ss, part + ((size_t)entry * G + c) * 2);
     ++entry;
   }

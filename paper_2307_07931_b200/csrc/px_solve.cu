@@ -1157,6 +1157,7 @@ px_status px_solve_host_batch(const px_layout* l, const px_relax_params* p, cons
 }
 
 void px_release_cached(void) {
+  px_mg_release();
   plans().clear();
   g_host.release();
   g_batch.release();

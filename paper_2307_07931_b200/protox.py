@@ -65,6 +65,11 @@ class px_solve_opts(ctypes.Structure):
                 ("temporal_k", ctypes.c_int32), ("use_graph", ctypes.c_int32)]
 
 
+class px_mg_opts(ctypes.Structure):
+    _fields_ = [("levels", ctypes.c_int32), ("nu1", ctypes.c_int32), ("nu2", ctypes.c_int32),
+                ("nu_coarse", ctypes.c_int32), ("ncycles", ctypes.c_int32), ("use_graph", ctypes.c_int32)]
+
+
 def point(x, y) -> px_point:
     p = px_point()
     p.c[0], p.c[1] = int(x), int(y)
@@ -88,7 +93,7 @@ EXPORTS = [
     "px_comm_unique_id", "px_comm_create", "px_comm_destroy", "px_comm_allreduce_norms",
     "px_comm_enable_p2p",
     "px_exchange_ghosts", "px_exchange_ghosts_local",
-    "px_solve", "px_solve_host", "px_solve_host_batch", "px_release_cached", "px_kernel_launch_count",
+    "px_solve", "px_solve_host", "px_solve_host_batch", "px_release_cached", "px_mg_solve", "px_mg_release", "px_kernel_launch_count",
     "px_relax_variant", "px_stream_ceiling",
 ]
 
@@ -170,6 +175,10 @@ def lib():
     L.px_solve_host_batch.restype = st
     L.px_solve_host_batch.argtypes = [vp, P(px_relax_params), P(px_solve_opts), i32, vp, vp, vp,
                                       P(ctypes.c_double), i32, P(i32), vp]
+    L.px_mg_solve.restype = st
+    L.px_mg_solve.argtypes = [vp, P(px_relax_params), P(px_mg_opts), P(px_patch), P(px_patch), P(px_patch),
+                              P(ctypes.c_double), i32, P(i32), vp]
+    L.px_mg_release.restype = None
     L.px_release_cached.restype = None
     L.px_kernel_launch_count.restype = i64
     L.px_stream_ceiling.restype = st
@@ -418,6 +427,23 @@ def solve(layout: Layout, comm: Comm | None, rank: int, p: px_relax_params, nswe
                           ctypes.byref(nw), ctypes.byref(ins) if keep_in_scratch else None,
                           _stream(stream)))
     return SolveResult(norms[: nw.value].copy(), bool(ins.value))
+
+
+def mg_solve(layout: Layout, p: px_relax_params, levels: int, ncycles: int, phi: px_patch,
+             phi_scratch: px_patch, rhs: px_patch, nu1: int = 2, nu2: int = 2, nu_coarse: int = 8,
+             use_graph: bool = False, stream=None) -> np.ndarray:
+    """px_mg_solve: ncycles V(nu1, nu2)-cycles; the result is in phi.
+    Returns norms[k] = (max|r|, sum r^2) after k cycles, k = 0..ncycles."""
+    opts = px_mg_opts(levels, nu1, nu2, nu_coarse, ncycles, int(use_graph))
+    cap = ncycles + 1
+    norms = np.zeros((cap, 2), dtype=np.float64)
+    nw = ctypes.c_int32(0)
+    ph, sc, rh = px_patch(phi.data, phi.box, phi.ld), px_patch(phi_scratch.data, phi_scratch.box, phi_scratch.ld), \
+        px_patch(rhs.data, rhs.box, rhs.ld)
+    _check(lib().px_mg_solve(layout.h, ctypes.byref(p), ctypes.byref(opts), ctypes.byref(ph), ctypes.byref(sc),
+                             ctypes.byref(rh), norms.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), cap,
+                             ctypes.byref(nw), _stream(stream)))
+    return norms[: nw.value].copy()
 
 
 def solve_host(layout: Layout, p: px_relax_params, nsweeps: int, norm_every: int,

@@ -543,3 +543,158 @@ def test_fault_injection_sign_flip_breaks_spectral_pin():
     p = Problem(n, n, h, -lam, bc=BC_PERIODIC, nsweeps=N, norm_every=-1)
     out, _ = oracle.solve(p, oracle.ghosted(p, phi0), oracle.ghosted(p, rho))
     assert rel_max(out[1:-1, 1:-1], ref) > 1e-3
+
+
+# ------------------------------------------------ multigrid V-cycle (R-MG)
+# The paper names multigrid but defines none; the V-cycle
+# is DESIGN.md readings R-MG1..R-MG6.  Pins: exactness of the transfer
+# operators on polynomials, an 8x8 dense brute-force V-cycle built here from
+# matrices, and the fixed point = the discrete solution (spectral closed form).
+def test_mg_restrict_linear_exact():
+    """-R of a linear cell-centred field is minus the field at the coarse
+    centres, exactly (dyadic coefficients)."""
+    n = 16
+    x = (np.arange(n) + 0.5) / n
+    d = 0.75 + 0.5 * x[None, :] - 0.25 * x[:, None]
+    X = (np.arange(n // 2) + 0.5) / (n // 2)
+    want = -(0.75 + 0.5 * X[None, :] - 0.25 * X[:, None])
+    assert np.array_equal(oracle.mg_restrict(d), want)
+    # and it is minus the 2x2 average for arbitrary data
+    rng = np.random.default_rng(3)
+    r = rng.uniform(-1, 1, (6, 10))
+    np.testing.assert_allclose(oracle.mg_restrict(r), -0.25 * (r[0::2, 0::2] + r[0::2, 1::2] + r[1::2, 0::2] + r[1::2, 1::2]),
+                               rtol=0, atol=4e-16)
+
+
+def test_mg_prolong_linear_and_walls():
+    """Bilinear cell-centred prolongation reproduces a linear field at every
+    fine cell away from the walls; periodic constants everywhere; with odd
+    reflection a constant c gives c/2 in the fine cells next to a wall and
+    c/4 in the corner cells (the interpolant vanishes on the wall)."""
+    nc = 8
+    X = (np.arange(nc) + 0.5) / nc
+    e = 0.5 + 0.25 * X[None, :] + 0.125 * X[:, None]
+    out = oracle.mg_prolong(e, np.zeros((2 * nc, 2 * nc)), BC_DIRICHLET_CC)
+    x = (np.arange(2 * nc) + 0.5) / (2 * nc)
+    want = 0.5 + 0.25 * x[None, :] + 0.125 * x[:, None]
+    assert np.array_equal(out[1:-1, 1:-1], want[1:-1, 1:-1])
+    c = 0.75
+    per = oracle.mg_prolong(np.full((nc, nc), c), np.ones((2 * nc, 2 * nc)), BC_PERIODIC)
+    assert np.array_equal(per, np.full((2 * nc, 2 * nc), 1.0 + c))
+    dc = oracle.mg_prolong(np.full((nc, nc), c), np.zeros((2 * nc, 2 * nc)), BC_DIRICHLET_CC)
+    assert np.array_equal(dc[1:-1, 1:-1], np.full((2 * nc - 2, 2 * nc - 2), c))
+    assert np.array_equal(dc[0, 1:-1], np.full(2 * nc - 2, c / 2))
+    assert np.array_equal(dc[1:-1, -1], np.full(2 * nc - 2, c / 2))
+    assert dc[0, 0] == c / 4 and dc[-1, -1] == c / 4
+
+
+def _dense_prolong(nc, bc):
+    """(2nc)² x nc² bilinear prolongation with the boundary rule folded in."""
+    nf = 2 * nc
+    Pm = np.zeros((nf * nf, nc * nc))
+    for y in range(nf):
+        for x in range(nf):
+            I, J = x // 2, y // 2
+            xn = I + 1 if x % 2 else I - 1
+            yn = J + 1 if y % 2 else J - 1
+            for (qx, qy, w) in [(I, J, 9), (xn, J, 3), (I, yn, 3), (xn, yn, 1)]:
+                s = 1.0
+                if bc == BC_PERIODIC:
+                    qx, qy = qx % nc, qy % nc
+                else:
+                    if qx < 0 or qx >= nc:
+                        qx, s = (-qx - 1 if qx < 0 else 2 * nc - 1 - qx), -s
+                    if qy < 0 or qy >= nc:
+                        qy, s = (-qy - 1 if qy < 0 else 2 * nc - 1 - qy), -s
+                Pm[x + y * nf, qx + qy * nc] += s * w / 16.0
+    return Pm
+
+
+def _dense_restrict(nc):
+    nf = 2 * nc
+    Rm = np.zeros((nc * nc, nf * nf))
+    for J in range(nc):
+        for I in range(nc):
+            for a in (0, 1):
+                for b in (0, 1):
+                    Rm[I + J * nc, (2 * I + a) + (2 * J + b) * nf] = 0.25
+    return Rm
+
+
+@pytest.mark.parametrize("bc", [BC_PERIODIC, BC_DIRICHLET_CC])
+@pytest.mark.parametrize("kind", [ST_LAPLACE5, ST_MEHRSTELLEN9])
+def test_mg_dense_8x8_vcycle_bruteforce(bc, kind):
+    """Two V(2,2)-cycles, 3 levels (8, 4, 2), 3 coarse sweeps: dense matrices
+    A_l (Eq.1 with the BC), R (2x2 average), P (bilinear), the recursion
+    written with them; the oracle agrees to rounding."""
+    n, levels, nu1, nu2, nuc, cyc = 8, 3, 2, 2, 3, 2
+    h = 1.0 / n
+    lam = h * h / 8 if kind == ST_LAPLACE5 else 3 * h * h / 16
+    A = [_dense_matrix(n >> l, bc, h * 2**l, kind) for l in range(levels)]
+    lamv = [lam * 4**l for l in range(levels)]
+    Rm = [_dense_restrict(n >> (l + 1)) for l in range(levels - 1)]
+    Pm = [_dense_prolong(n >> (l + 1), bc) for l in range(levels - 1)]
+
+    def V(l, v, f):
+        if l == levels - 1:
+            for _ in range(nuc):
+                v = v + lamv[l] * (A[l] @ v - f)
+            return v
+        for _ in range(nu1):
+            v = v + lamv[l] * (A[l] @ v - f)
+        fc = Rm[l] @ (f - A[l] @ v)
+        e = V(l + 1, np.zeros(fc.size), fc)
+        v = v + Pm[l] @ e
+        for _ in range(nu2):
+            v = v + lamv[l] * (A[l] @ v - f)
+        return v
+
+    rng = np.random.default_rng(5 + bc + 2 * kind)
+    phi0, rho = rng.uniform(-1, 1, (n, n)), rng.uniform(-1, 1, (n, n))
+    v, f = phi0.reshape(-1).copy(), rho.reshape(-1)
+    res = []
+    r = A[0] @ v - f
+    res.append((np.max(np.abs(r)), np.sum(r * r)))
+    for _ in range(cyc):
+        v = V(0, v, f)
+        r = A[0] @ v - f
+        res.append((np.max(np.abs(r)), np.sum(r * r)))
+    p = Problem(n, n, h, lam, bc=bc, stencil=kind, b0=4, b1=8)
+    out, norms = oracle.mg_solve(p, oracle.MG(levels, nu1, nu2, nuc, cyc), oracle.ghosted(p, phi0),
+                                 oracle.ghosted(p, rho))
+    assert rel_max(out[1:-1, 1:-1].reshape(-1), v) < 1e-13
+    np.testing.assert_allclose(norms, np.array(res), rtol=1e-12)
+
+
+@pytest.mark.parametrize("kind", [ST_LAPLACE5, ST_MEHRSTELLEN9])
+def test_mg_converges_to_discrete_solution(kind):
+    """Fixed point: V-cycles drive φ to A⁻¹ρ.  Dirichlet-CC sine mode: φ* =
+    ρ/μ₁₁ in closed form; periodic random zero-mean ρ: the FFT solve.  Per
+    cycle the residual drops by < 0.35 (V(2,2), ω = 1/2 Jacobi smoother)."""
+    n = 32
+    h = 1.0 / n
+    lam = h * h / 8 if kind == ST_LAPLACE5 else 3 * h * h / 16
+    x = (np.arange(n) + 0.5) * h
+    rho = np.outer(np.sin(np.pi * x), np.sin(np.pi * x))
+    a = -4 * math.sin(math.pi * h / 2) ** 2
+    mu = (_mu5 if kind == ST_LAPLACE5 else _mu9)(a, a, h)
+    p = Problem(n, n, h, lam, bc=BC_DIRICHLET_CC, stencil=kind)
+    out, norms = oracle.mg_solve(p, oracle.MG(5, 2, 2, 8, 30), np.zeros(p.gshape), oracle.ghosted(p, rho))
+    assert rel_max(out[1:-1, 1:-1], rho / mu) < 1e-12
+    ratios = norms[1:12, 0] / norms[:11, 0]
+    assert np.all(ratios < 0.35), ratios
+    # periodic, random zero-mean right-hand side
+    rng = np.random.default_rng(9)
+    f = rng.uniform(-1, 1, (n, n))
+    f -= f.mean()
+    pp = Problem(n, n, h, lam, bc=BC_PERIODIC, stencil=kind, b0=8, b1=16)
+    out, norms = oracle.mg_solve(pp, oracle.MG(5, 2, 2, 8, 40), np.zeros(pp.gshape), oracle.ghosted(pp, f))
+    k = np.arange(n)
+    ak = -4 * np.sin(np.pi * k / n) ** 2
+    ay, ax = np.meshgrid(ak, ak, indexing="ij")
+    muk = (_mu5 if kind == ST_LAPLACE5 else _mu9)(ax, ay, h)
+    F = np.fft.fft2(f)
+    S = np.where(muk == 0, 0, F / np.where(muk == 0, 1, muk))
+    want = np.real(np.fft.ifft2(S))
+    assert rel_max(out[1:-1, 1:-1] - out[1:-1, 1:-1].mean(), want) < 1e-10
+    assert norms[-1, 0] < 1e-11 * norms[0, 0]
