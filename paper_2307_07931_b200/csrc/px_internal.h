@@ -124,6 +124,8 @@ struct StreamLaunch {
 struct TbLaunch {
   NormSlot lvl[4];   // norms of the residual computed at level t (iterate base+t-1)
   int32_t fix[2][2]; // FIXED faces: ghost cells there keep their level-0 value
+  int32_t refl[2][2]; // DIRICHLET_CC faces: the first ghost column / row of every
+                      // level is re-derived by odd reflection (wide kernel only)
 };
 int32_t tb_blocks(int K, const StreamLaunch& a);
 px_status launch_tb(int stencil, int K, const StreamLaunch& a, const TbLaunch& x, cudaStream_t s);

@@ -448,6 +448,10 @@ static px_status enqueue_solve(const SolveCtx& x) {
       tl[part].fix[0][0] = tl[part].fix[0][1] = fixed;
       tl[part].fix[1][0] = fixed && li.nbr_lo < 0;
       tl[part].fix[1][1] = fixed && li.nbr_hi < 0;
+      const bool dir = x.l->bc == PX_BC_DIRICHLET_CC;  // per-level odd reflection at domain faces
+      tl[part].refl[0][0] = tl[part].refl[0][1] = dir;
+      tl[part].refl[1][0] = dir && li.nbr_lo < 0;
+      tl[part].refl[1][1] = dir && li.nbr_hi < 0;
       blocks[part] = tb_blocks(K, la[part]);
       total += blocks[part];
     }
@@ -780,8 +784,6 @@ static px_status solve_enqueue(const px_layout* l, px_comm* c, int32_t rank, con
       return fail(PX_ERR_UNSUPPORTED, "temporal_k=%d not built (1, 2 or 4)", o->temporal_k);
     if (o->temporal_k > l->ghost)
       return fail(PX_ERR_UNSUPPORTED, "temporal_k=%d exceeds the ghost width %d", o->temporal_k, l->ghost);
-    if (l->bc == PX_BC_DIRICHLET_CC)
-      return fail(PX_ERR_UNSUPPORTED, "temporal blocking with DIRICHLET_CC (per-level reflection) not built");
     if (ext(l->domain, 0) % 2)
       return fail(PX_ERR_UNSUPPORTED, "temporal blocking needs an even domain width");
   }

@@ -491,14 +491,17 @@ def test_solve_bulk_kernel_bitwise(nranks, bc, st):
 
 # ------------------------------------------------- temporal blocking (a7)
 @pytest.mark.parametrize("tk", [2, 4])
-@pytest.mark.parametrize("bc", [P.PX_BC_PERIODIC, P.PX_BC_FIXED_GHOSTS])
+@pytest.mark.parametrize("bc", [P.PX_BC_PERIODIC, P.PX_BC_FIXED_GHOSTS, P.PX_BC_DIRICHLET_CC])
 @pytest.mark.parametrize("st", [P.PX_LAPLACE_5PT, P.PX_MEHRSTELLEN_9PT])
 @pytest.mark.parametrize("nranks,hinv", [(1, 1024), (3, 1000)])
 def test_solve_temporal_blocking_bitwise(tk, bc, st, nranks, hinv):
     """k sweeps per pass (ghost width 4) == k plain sweeps, bit for bit: ragged
-    strips (1000 = 2 x 448 + 104 columns), several row chunks, 3 slabs with
+    strips (1000 columns = one full CTA strip + a ragged one), several row chunks, 3 slabs with
     local transport, an odd sweep count (2 or 4-blocks + plain sweeps),
-    power-of-two h (fused multiply-add path) and h = 1/1000 (separate ops)."""
+    power-of-two h (fused multiply-add path) and h = 1/1000 (separate ops).
+    DIRICHLET_CC: every level re-derives its first ghost column / row by odd
+    reflection (corners by the product rule), as the oracle's exchange does
+    between sweeps."""
     n0, n1, N, E = 1000, 300, 11, 3
     h = 1.0 / hinv
     lam = h * h / 8 if st == 0 else 3 * h * h / 16
@@ -511,16 +514,18 @@ def test_solve_temporal_blocking_bitwise(tk, bc, st, nranks, hinv):
     _check_norms(norms, rn)
 
 
-def test_temporal_blocking_large_tall():
-    """Bulk-sized temporal blocking (many chunks per strip), k = 4, periodic."""
+@pytest.mark.parametrize("bc,st", [(P.PX_BC_PERIODIC, P.PX_LAPLACE_5PT), (P.PX_BC_DIRICHLET_CC, P.PX_LAPLACE_5PT),
+                                   (P.PX_BC_DIRICHLET_CC, P.PX_MEHRSTELLEN_9PT)])
+def test_temporal_blocking_large_tall(bc, st):
+    """Bulk-sized temporal blocking (many chunks per strip, several strips), k = 4."""
     n0, n1, N, E = 2048, 2560, 8, 1
     h = 1.0 / 2048
-    lam = h * h / 8
+    lam = h * h / 8 if st == 0 else 3 * h * h / 16
     g = 4
-    phi0, rho = _fields(n0, n1, g, 77, P.PX_BC_PERIODIC)
-    out, norms, _ = run_gpu_solve(n0, n1, h, lam, P.PX_BC_PERIODIC, 0, N, E, phi0, rho, g=g, box=(256, 256),
+    phi0, rho = _fields(n0, n1, g, 77, bc)
+    out, norms, _ = run_gpu_solve(n0, n1, h, lam, bc, st, N, E, phi0, rho, g=g, box=(256, 256),
                                   tk=4)
-    ref, rn = oracle.solve(_orc_problem(n0, n1, h, lam, P.PX_BC_PERIODIC, 0, N, E, g=g), phi0, rho)
+    ref, rn = oracle.solve(_orc_problem(n0, n1, h, lam, bc, st, N, E, g=g), phi0, rho)
     assert bits_equal(out, ref[g:-g, g:-g]), ulp_diff(out, ref[g:-g, g:-g])
     _check_norms(norms, rn)
 
@@ -528,9 +533,9 @@ def test_temporal_blocking_large_tall():
 def test_temporal_blocking_unsupported_cases():
     lay = P.Layout(P.box(0, 0, 127, 127), (64, 64), 2, P.PX_BC_DIRICHLET_CC, 1)
     a, b, r = lay.alloc(0), lay.alloc(0), lay.alloc(0)
-    with pytest.raises(P.PxError, match="DIRICHLET"):
+    with pytest.raises(P.PxError, match="not built"):
         P.solve(lay, None, 0, P.relax_params(1 / 128, 1e-6), 4, 1, lay.patch(0, a), lay.patch(0, b),
-                lay.patch(0, r), temporal_k=2)
+                lay.patch(0, r), temporal_k=3)
     with pytest.raises(P.PxError, match="exceeds the ghost width"):
         P.solve(lay, None, 0, P.relax_params(1 / 128, 1e-6), 4, 1, lay.patch(0, a), lay.patch(0, b),
                 lay.patch(0, r), temporal_k=4)
