@@ -302,7 +302,7 @@ def run_native(args):
     traffic = load_traffic(args.config) if world == 1 else None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
-                "kernel": (f"k_tb<5pt,K={tk}> (temporal blocking: one launch = {tk} sweeps, "
+                "kernel": (f"k_tbw<5pt,K={tk}> (temporal blocking, skewed wavefront: one launch = {tk} sweeps, "
                            f"{BYTES_PER_CELL_UPDATE}/{tk} B per cell-update)") if tk > 1 else
                           ("k_bulk<RELAX,5pt> (TMA bulk-copy pipeline)" if cfg["stencil"] == 0 else "k_bulk<RELAX,9pt>"),
                 "kernel_ms": k_ms, "algorithmic_bytes_per_launch": BYTES_PER_CELL_UPDATE * local_cells,

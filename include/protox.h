@@ -279,8 +279,10 @@ px_status px_exchange_ghosts_local(const px_layout* l, const px_patch* parts, vo
  * norm_every = E: record the global residual norms of φ^(jE) for every
  * jE < N (computed inside the sweep that consumes φ^(jE)), plus a final
  * entry for φ^N; E = 0: final entry only; E < 0: no norms.
- * temporal_k: sweeps per ghost exchange (1, or k <= ghost width: temporal
- * blocking).  use_graph: capture the sweep sequence in a CUDA
+ * temporal_k: sweeps per ghost exchange (1, or k in {2, 4} with k <= ghost
+ * width: temporal blocking; every BC -- DIRICHLET_CC faces
+ * re-derive their first ghost column/row by odd reflection after each of the
+ * k levels, so a pass is exactly k plain sweeps).  use_graph: capture the sweep sequence in a CUDA
  * graph cached per (layout, comm, params, opts, pointers, stream); the
  * captured pointers must stay valid while the layout lives.
  *

@@ -680,3 +680,21 @@ def test_p2p_halo_push_self_exchange(graph, monkeypatch):
     # norms: first solve's entries are φ^0..φ^6, final φ^8; second continues from φ^8
     _check_norms(r1.norms[:-1], rn[: N // E])
     _check_norms(r2.norms, rn[N // E:])
+
+
+@pytest.mark.gpu
+def test_temporal_blocking_narrow_kernel_subprocess():
+    """The narrow temporal-blocking kernel (2 columns per lane, A/B baseline,
+    PROTOX_TB_IMPL=narrow is read once per process) stays bit-identical:
+    periodic and FIXED_GHOSTS cases re-run in a child process."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    ids = [f"tests/test_gpu_parity.py::test_solve_temporal_blocking_bitwise[{c}]"
+           for c in ("1-1024-0-0-4", "1-1024-1-2-2", "3-1000-0-2-4", "3-1000-1-0-2")]
+    ids.append("tests/test_gpu_parity.py::test_temporal_blocking_large_tall[0-0]")
+    env = dict(os.environ, PROTOX_TB_IMPL="narrow")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-m", "gpu", *ids],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
