@@ -23,6 +23,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "protox_oracle.cpp")
+_SRC3 = os.path.join(_HERE, "protox_oracle3d.cpp")
 _LIB = os.path.join(_HERE, "liborc.so")
 
 BC_PERIODIC, BC_DIRICHLET_CC, BC_FIXED = 0, 1, 2
@@ -33,9 +34,10 @@ _CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c++17", "-fPIC", 
 
 def build(force: bool = False) -> str:
     """Compile the oracle with g++ (plain -O2, -ffp-contract=off)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(os.path.getmtime(_SRC),
+                                                                          os.path.getmtime(_SRC3)):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["g++", *_CFLAGS, _SRC, "-o", tmp])
+        subprocess.check_call(["g++", *_CFLAGS, _SRC, _SRC3, "-o", tmp])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -46,6 +48,15 @@ class _Problem(ctypes.Structure):
         ("b0", ctypes.c_int64), ("b1", ctypes.c_int64),
         ("ghost", ctypes.c_int32), ("bc", ctypes.c_int32),
         ("stencil", ctypes.c_int32), ("rhs_correction", ctypes.c_int32),
+        ("h", ctypes.c_double), ("lam", ctypes.c_double),
+        ("nsweeps", ctypes.c_int64), ("norm_every", ctypes.c_int64),
+    ]
+
+
+class _Problem3(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_int64 * 3), ("b", ctypes.c_int64 * 3),
+        ("ghost", ctypes.c_int32), ("bc", ctypes.c_int32),
         ("h", ctypes.c_double), ("lam", ctypes.c_double),
         ("nsweeps", ctypes.c_int64), ("norm_every", ctypes.c_int64),
     ]
@@ -86,6 +97,11 @@ def _L():
         _lib.orc_mg_prolong.argtypes = [i64, i64, ctypes.c_int32, d, d]
         _lib.orc_neumaier_sum.argtypes = [d, i64]
         _lib.orc_neumaier_sum.restype = ctypes.c_double
+        P3 = ctypes.POINTER(_Problem3)
+        _lib.orc3_last_error.restype = ctypes.c_char_p
+        _lib.orc3_solve.argtypes = [P3, d, d, d, d, i64, ctypes.POINTER(i64)]
+        _lib.orc3_apply_laplacian.argtypes = [P3, d, d]
+        _lib.orc3_exchange.argtypes = [P3, d]
     return _lib
 
 
@@ -280,3 +296,80 @@ def mg_prolong(e: np.ndarray, fine: np.ndarray, bc: int) -> np.ndarray:
     assert f.shape == (2 * nc1, 2 * nc0)
     _check(_L().orc_mg_prolong(nc0, nc1, bc, _dp(e), _dp(f)))
     return f
+
+
+# ------------------------------------------------------------------------ 3D
+# (protox_oracle3d.cpp, readings R-3D1..R-3D3)
+# A global ghosted 3D array has shape (n2 + 2g, n1 + 2g, n0 + 2g); element
+# [z + g, y + g, x + g] is cell (x, y, z) (dimension 0 fastest in memory).
+
+def _check3(rc: int):
+    if rc != 0:
+        raise OracleError(_L().orc3_last_error().decode())
+
+
+@dataclass
+class Problem3:
+    """3D relaxation problem: domain n = (n0, n1, n2) split into boxes b."""
+    n: tuple
+    h: float
+    lam: float
+    b: tuple | None = None
+    ghost: int = 1
+    bc: int = BC_PERIODIC
+    nsweeps: int = 0
+    norm_every: int = 0
+
+    def c(self) -> _Problem3:
+        b = self.b or self.n
+        return _Problem3((ctypes.c_int64 * 3)(*self.n), (ctypes.c_int64 * 3)(*b), self.ghost, self.bc,
+                         self.h, self.lam, self.nsweeps, self.norm_every)
+
+    @property
+    def gshape(self):
+        g = self.ghost
+        return (self.n[2] + 2 * g, self.n[1] + 2 * g, self.n[0] + 2 * g)
+
+    def n_norms(self) -> int:
+        if self.norm_every < 0:
+            return 0
+        k = (self.nsweeps + self.norm_every - 1) // self.norm_every if self.norm_every > 0 else 0
+        return k + 1
+
+
+def ghosted3(p: Problem3, interior: np.ndarray, ghost_values: float | np.ndarray = 0.0) -> np.ndarray:
+    g = p.ghost
+    out = np.empty(p.gshape, dtype=np.float64)
+    out[...] = ghost_values
+    out[g:g + p.n[2], g:g + p.n[1], g:g + p.n[0]] = interior
+    return out
+
+
+def solve3(p: Problem3, phi0_g: np.ndarray, rho_g: np.ndarray):
+    """p.nsweeps iterations of figure `Proto` in 3D.  Returns (phi_g, norms)."""
+    phi0_g = np.ascontiguousarray(phi0_g, dtype=np.float64)
+    rho_g = np.ascontiguousarray(rho_g, dtype=np.float64)
+    assert phi0_g.shape == p.gshape and rho_g.shape == p.gshape
+    out = np.zeros(p.gshape, dtype=np.float64)
+    cap = max(p.n_norms(), 1)
+    norms = np.zeros((cap, 2), dtype=np.float64)
+    nw = ctypes.c_int64(0)
+    pc = p.c()
+    _check3(_L().orc3_solve(ctypes.byref(pc), _dp(phi0_g), _dp(rho_g), _dp(out), _dp(norms), cap,
+                            ctypes.byref(nw)))
+    return out, norms[: nw.value]
+
+
+def apply_laplacian3(p: Problem3, phi_g: np.ndarray) -> np.ndarray:
+    phi_g = np.ascontiguousarray(phi_g, dtype=np.float64)
+    out = np.zeros((p.n[2], p.n[1], p.n[0]), dtype=np.float64)
+    pc = p.c()
+    _check3(_L().orc3_apply_laplacian(ctypes.byref(pc), _dp(phi_g), _dp(out)))
+    return out
+
+
+def exchange3(p: Problem3, glob: np.ndarray) -> np.ndarray:
+    g = np.array(glob, dtype=np.float64, order="C", copy=True)
+    pc = p.c()
+    _check3(_L().orc3_exchange(ctypes.byref(pc), _dp(g)))
+    return g
