@@ -10,7 +10,7 @@ every sweep, replayed from a CUDA graph; the multi-GPU run splits the same
 16384² domain into slabs over N ranks (strong scaling) with a per-sweep
 NCCL ghost exchange and the residual all-reduce.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3|C2|C1|C5]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3|C2|C1|C4|C5|C3D]
     python bench.py --impl reference ...   # the CPU oracle on a bounded sample
 
 Prints ONE JSON line on rank 0.  Inputs (3 x 2.15 GB) exceed the 126 MB L2,
@@ -49,6 +49,9 @@ CONFIGS = {
                desc="BASELINE config 1: 64x64 box + 1 ghost layer, Dirichlet, 100 sweeps"),
     "C5": dict(n=8192, box=256, bc=1, stencil=1, sweeps=100, norm_every=1, rho="sine",
                desc="BASELINE config 5: 8192x8192 Mehrstellen 9-point, Dirichlet-CC"),
+    "C3D": dict(n=512, box=512, bc=0, stencil=2, sweeps=100, norm_every=1, rho="hash", dims=3,
+                desc="3D extension (SURVEY 8(f) rank 3, not a BASELINE config): 3D Poisson 512^3 fp64, "
+                     "periodic, 7-point, norms every sweep"),
 }
 
 
@@ -160,11 +163,46 @@ def oracle_sample(cfg, n_sample: int, sweeps: int):
     return n * n * sweeps / dt / 1e9, dt
 
 
+def oracle_sample3(cfg, n_sample: int, sweeps: int):
+    """The 3D oracle on an n_sample³ sample of the same recipe."""
+    import numpy as np
+
+    import oracle
+    from paper_2307_07931_b200 import inputs
+    n = n_sample
+    h = 1.0 / n
+    p = oracle.Problem3((n, n, n), h, h * h / 12, bc=oracle.BC_PERIODIC, nsweeps=sweeps,
+                        norm_every=cfg["norm_every"])
+    rho_g = oracle.ghosted3(p, inputs.hash_field3(n, n, n))
+    phi_g = np.zeros_like(rho_g)
+    t0 = time.perf_counter()
+    oracle.solve3(p, phi_g, rho_g)
+    dt = time.perf_counter() - t0
+    return n ** 3 * sweeps / dt / 1e9, dt
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     cfg = CONFIGS[args.config]
+    if cfg.get("dims") == 3:
+        n_s, sweeps = 128, 20
+        rates, times = [], []
+        for i in range(args.warmup + args.steps):
+            r, dt = oracle_sample3(cfg, n_s, sweeps)
+            if i >= args.warmup:
+                times.append(dt)
+        total = n_s ** 3 * sweeps * args.steps / sum(times) / 1e9
+        sample = f"3D oracle (single-threaded C++, unfused Proto order) on {n_s}^3, {sweeps} sweeps per step"
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": total, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": cfg["desc"], "sample": sample},
+            "cpu_baseline": {"value": total, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": total, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return 0
     n_s = min(cfg["n"], 2048)
     sweeps = 10 if cfg["n"] > 2048 else cfg["sweeps"]
     for _ in range(args.warmup):
@@ -189,6 +227,142 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------- native arm
+def run_native3d(args):
+    """C3D: the 3D relaxation (px3_solve).  N > 1: independent replicas (the
+    3D path is single-device; weak scaling, no data-path collective)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2307_07931_b200 import inputs
+    from paper_2307_07931_b200 import protox as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = CONFIGS[args.config]
+    n, S, E = cfg["n"], cfg["sweeps"], cfg["norm_every"]
+    h = 1.0 / n
+    lam = h * h / 12  # λ = h²/(4D), D = 3 (PAPER.md:138)
+    grid = P.Grid3((n, n, n), 1)
+    phi, scr, rho = grid.alloc(dev), grid.alloc(dev), grid.alloc(dev)
+    stream = torch.cuda.Stream(device=dev)
+    stream.wait_stream(torch.cuda.current_stream(dev))
+    prm = P.relax_params(h, lam, P.PX_LAPLACE_7PT_3D)
+    P.init_field3(grid, rho, 1, inputs.DEFAULT_SEED, stream=stream)
+    stream.synchronize()
+    bufs = [phi, scr]
+
+    def step():
+        r = P.solve3(grid, cfg["bc"], prm, S, E, bufs[0], bufs[1], rho, use_graph=True, stream=stream)
+        if r.in_scratch:
+            bufs.reverse()
+        return r
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 3)):
+        res = step()
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = P.kernel_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        res = step()
+    ev1.record(stream)
+    barrier()
+    launches = P.kernel_launch_count() - launches0
+    clk = clocks.stop()
+    t = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_ms = float(t.item())
+    value = world * n ** 3 * S * args.steps / (t_ms * 1e-3) / 1e9
+
+    # roofline of k3_relax (px3_relax_step, same launch geometry), CUDA events on its stream
+    nb = P.norm_buffer3(dev)
+    stream.wait_stream(torch.cuda.current_stream(dev))
+    reps = 20
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for i in range(reps):
+        src, dst = (bufs[0], bufs[1]) if i % 2 == 0 else (bufs[1], bufs[0])
+        P.fill_ghosts3(grid, cfg["bc"], src, stream=stream)
+        evs[i][0].record(stream)
+        P.relax_step3(prm, grid, src, dst, rho, nb, stream=stream)
+        evs[i][1].record(stream)
+    stream.synchronize()
+    k_ms = statistics.mean(a.elapsed_time(b) for a, b in evs[2:])
+    alg = BYTES_PER_CELL_UPDATE * n ** 3
+    peak, peak_src = load_peaks()
+    roofline = {"bound": "hbm", "achieved": alg / (k_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                "frac": alg / (k_ms * 1e-3) / 1e9 / peak, "traffic": load_traffic(args.config) if world == 1 else None,
+                "kernel": "k3_relax<RELAX> (3D 7-point, TMA tensor tiles marching in z)", "kernel_ms": k_ms,
+                "algorithmic_bytes_per_launch": alg, "peak_source": peak_src,
+                "whole_step_GBps": BYTES_PER_CELL_UPDATE * value / world}
+
+    # e2e: pinned host ρ -> device, solve from φ0 = 0, φ^N back to pinned host, every step
+    e2e = None
+    if not args.no_e2e:
+        h_rho = grid.view(rho).cpu().pin_memory()
+        h_out = torch.empty_like(h_rho).pin_memory()
+        d_phi, d_scr, d_rhs = grid.alloc(dev), grid.alloc(dev), grid.alloc(dev)
+        stream.wait_stream(torch.cuda.current_stream(dev))
+
+        def e2e_step():
+            with torch.cuda.stream(stream):
+                grid.view(d_phi).zero_()
+                grid.view(d_rhs).copy_(h_rho, non_blocking=True)
+            r = P.solve3(grid, cfg["bc"], prm, S, E, d_phi, d_scr, d_rhs, use_graph=True, stream=stream)
+            with torch.cuda.stream(stream):
+                h_out.copy_(grid.view(d_scr if r.in_scratch else d_phi), non_blocking=True)
+            stream.synchronize()
+
+        e2e_step()
+        barrier()
+        ke = max(3, min(args.steps, 6))
+        w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w0.record(stream)
+        for _ in range(ke):
+            e2e_step()
+        w1.record(stream)
+        barrier()
+        te = torch.tensor([w0.elapsed_time(w1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        n_norm = (S + E - 1) // E + 1 if E > 0 else 1
+        e2e = {"value": world * n ** 3 * S * ke / (te.item() * 1e-3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": n ** 3 * 8, "d2h_bytes_per_step": n ** 3 * 8 + 16 * n_norm, "steps": ke,
+               "api": "torch pinned copy of rho + px3_solve (phi0 = 0 zero-filled on the device) + D2H phi^N"}
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        r, dt = oracle_sample3(cfg, 160, 20)
+        cpu = {"value": r, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"single-threaded C++ 3D oracle, 160^3 of the same recipe, 20 sweeps, {dt:.1f} s"}
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["desc"], "n": n, "sweeps_per_step": S, "norm_every": E, "ghost": 1,
+                       "replicas": world, "rho": cfg["rho"], "h": h, "lambda": lam,
+                       "steps_continue": "each step continues from the previous step's iterate",
+                       "l2": "inputs (3 x %.2f GB) exceed L2; no flush" % (grid.alloc_elems * 8 / 1e9)},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+            "final_residual_max": float(res.norms[-1, 0]) if len(res.norms) else None}))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def run_native(args):
     import torch
     import torch.distributed as dist
@@ -398,6 +572,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if CONFIGS[args.config].get("dims") == 3:
+        return run_native3d(args)
     return run_native(args)
 
 

@@ -155,7 +155,7 @@ typedef struct {
 px_status px_layout_halo_plan(const px_layout* l, int32_t rank, px_halo_op ops[4], int32_t* nops);
 
 /* ----------------------------------------------------------------- kernels */
-typedef enum { PX_LAPLACE_5PT = 0, PX_MEHRSTELLEN_9PT = 1 } px_stencil;
+typedef enum { PX_LAPLACE_5PT = 0, PX_MEHRSTELLEN_9PT = 1, PX_LAPLACE_7PT_3D = 2 } px_stencil;
 /* stencil: taps in the fixed order W,E,S,N(1),C(-4) for 5-point; W,E,S,N(4),
  * SW,SE,NW,NE(1),C(-20) for Mehrstellen (not in the paper, BASELINE config 5).
  * scale = 1/(h*h) (5-point) or 1/(6*h*h) (9-point), computed in double on the
@@ -369,6 +369,58 @@ px_status px_mg_solve(const px_layout* l, const px_relax_params* p, const px_mg_
                       px_patch* phi_scratch, const px_patch* rhs, double* h_norms, int32_t cap,
                       int32_t* n_written, void* stream);
 void px_mg_release(void);
+
+/* ---------------------------------------------------------------------- 3D
+ * The 3D relaxation.  The paper's Point and Box
+ * are dimension-generic (Z^D), λ = h²/(4D);
+ * the stencil PX_LAPLACE_7PT_3D has taps W,E,S,N,B,T (offsets −x,+x,−y,+y,
+ * −z,+z; weight 1) and C (−6) in that order, scale = 1/(h·h) (DESIGN.md
+ * R-3D1); per cell r = scale·L − rhs, φ' = φ + λ·r, every operation rounded
+ * once -- bit-identical to the oracle's orc3_solve.  Single device.
+ *
+ * A 3D patch over CALLER-OWNED device memory: cell (x, y, z) at
+ * data[x + y·ld + z·plane], data pointing at cell (0,0,0); n = extents,
+ * ghost = g (1..16).  The memory must cover cells (−2 .. n0+1, −g .. n1+g−1,
+ * −g .. n2+g−1) (the TMA boxes read one column beyond the ghost layer);
+ * data 16-byte aligned, ld and plane even; PX_ERR_ALIGN / PX_ERR_SHAPE
+ * otherwise.  px3_layout gives a conforming layout: ld, plane, the element
+ * offset of cell (0,0,0) in an allocation of alloc_elems doubles. */
+typedef struct {
+  double* data;
+  int32_t n[3];
+  int32_t ghost;
+  int64_t ld, plane;
+} px_patch3;
+px_status px3_layout(const int32_t n[3], int32_t ghost, int64_t* ld, int64_t* plane, int64_t* origin,
+                     int64_t* alloc_elems);
+/* Norm buffer of px3_norm_buffer_len() doubles, zero-initialised once, with
+ * the 2D norm-buffer protocol (buf[0] = max|r|, buf[1] = Σr²). */
+int64_t px3_norm_buffer_len(void);
+/* Synthetic field on the owned cells: kind 0 zeros, 1 the counter hash
+ * u = splitmix64(seed ^ (x + n0·(y + n1·z))), ((u >> 11)·2^-53)·2 − 1. */
+px_status px3_init_field(px_patch3* p, int32_t kind, uint64_t seed, void* stream);
+/* Ghost layer by the boundary rule (R-3D2): PERIODIC wrap,
+ * DIRICHLET_CC odd reflection, phased x, y, z (edges and corners by the
+ * product rule); FIXED_GHOSTS: nothing.  g <= every extent. */
+px_status px3_fill_ghosts(px_bc bc, px_patch3* p, void* stream);
+/* One fused sweep over all cells (ghosts of φ_in must be valid): φ_out =
+ * φ_in + λ(scale·S(φ_in) − rhs); d_norms (optional, px3 norm buffer) gets
+ * the residual norms of φ_in.  phi_in, phi_out, rhs: same extents and ghost
+ * width; φ_in and φ_out must differ.  Asynchronous on stream. */
+px_status px3_relax_step(const px_relax_params* p, const px_patch3* phi_in, px_patch3* phi_out,
+                         const px_patch3* rhs, double* d_norms, void* stream);
+/* Residual norms of φ as given (Eq.7; ghosts must be valid) into d_norms. */
+px_status px3_residual_norm(const px_relax_params* p, const px_patch3* phi, const px_patch3* rhs,
+                            double* d_norms, void* stream);
+/* N-sweep solve (figure `Proto` in 3D, fused): per sweep the ghost fill of bc
+ * then one fused sweep; norm schedule, h_norms / cap / n_written / in_scratch
+ * exactly as px_solve (temporal_k must be <= 1).  use_graph: the sequence is
+ * captured once into a CUDA graph cached per (bc, params, opts, patches,
+ * stream) until px3_release.  Host-synchronous. */
+px_status px3_solve(px_bc bc, const px_relax_params* p, const px_solve_opts* o, px_patch3* phi,
+                    px_patch3* phi_scratch, const px_patch3* rhs, double* h_norms, int32_t cap,
+                    int32_t* n_written, int32_t* in_scratch, void* stream);
+void px3_release(void);
 
 /* Diagnostics: number of kernel launches libprotox enqueued so far in this
  * process (graph replays count their kernel nodes). */

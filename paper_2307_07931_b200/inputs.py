@@ -73,3 +73,20 @@ def random_field(n0: int, n1: int, seed: int) -> np.ndarray:
     """Plain numpy-seeded uniform [-1, 1) field (for parity stress inputs)."""
     rng = np.random.default_rng(seed)
     return rng.uniform(-1.0, 1.0, size=(n1, n0))
+
+
+def hash_values3(ix, iy, iz, n0: int, n1: int, seed: int = DEFAULT_SEED) -> np.ndarray:
+    """3D counter hash: ρ at global cells (ix, iy, iz) of an n0 x n1 x n2 domain,
+    u = splitmix64(seed XOR (i + n0*(j + n1*k))) (the 2D recipe in 3D; the
+    device initialiser px3_init_field implements it independently)."""
+    idx = (np.asarray(ix, dtype=np.uint64) + np.uint64(n0) * (np.asarray(iy, dtype=np.uint64)
+                                                              + np.uint64(n1) * np.asarray(iz, dtype=np.uint64)))
+    u = splitmix64(idx ^ np.uint64(seed))
+    return ((u >> np.uint64(11)).astype(np.float64) * 2.0 ** -53) * 2.0 - 1.0
+
+
+def hash_field3(n0: int, n1: int, n2: int, seed: int = DEFAULT_SEED) -> np.ndarray:
+    """Full (n2, n1, n0) interior field of the 3D counter hash."""
+    iz, iy, ix = np.meshgrid(np.arange(n2, dtype=np.uint64), np.arange(n1, dtype=np.uint64),
+                             np.arange(n0, dtype=np.uint64), indexing="ij")
+    return hash_values3(ix, iy, iz, n0, n1, seed)

@@ -22,7 +22,7 @@ PX_OK, PX_ERR_ARG, PX_ERR_SHAPE, PX_ERR_DOMAIN, PX_ERR_ALIGN = 0, 1, 2, 3, 4
 PX_ERR_UNSUPPORTED, PX_ERR_CUDA, PX_ERR_NCCL, PX_ERR_STATE = 5, 6, 7, 8
 PX_BC_PERIODIC, PX_BC_DIRICHLET_CC, PX_BC_FIXED_GHOSTS = 0, 1, 2
 PX_PART_SLABS = 0
-PX_LAPLACE_5PT, PX_MEHRSTELLEN_9PT = 0, 1
+PX_LAPLACE_5PT, PX_MEHRSTELLEN_9PT, PX_LAPLACE_7PT_3D = 0, 1, 2
 PX_FIELD_ZERO, PX_FIELD_HASH, PX_FIELD_SINE = 0, 1, 2
 
 
@@ -65,6 +65,11 @@ class px_solve_opts(ctypes.Structure):
                 ("temporal_k", ctypes.c_int32), ("use_graph", ctypes.c_int32)]
 
 
+class px_patch3(ctypes.Structure):
+    _fields_ = [("data", ctypes.c_void_p), ("n", ctypes.c_int32 * 3), ("ghost", ctypes.c_int32),
+                ("ld", ctypes.c_int64), ("plane", ctypes.c_int64)]
+
+
 class px_mg_opts(ctypes.Structure):
     _fields_ = [("levels", ctypes.c_int32), ("nu1", ctypes.c_int32), ("nu2", ctypes.c_int32),
                 ("nu_coarse", ctypes.c_int32), ("ncycles", ctypes.c_int32), ("use_graph", ctypes.c_int32)]
@@ -95,6 +100,8 @@ EXPORTS = [
     "px_exchange_ghosts", "px_exchange_ghosts_local",
     "px_solve", "px_solve_host", "px_solve_host_batch", "px_release_cached", "px_mg_solve", "px_mg_release", "px_kernel_launch_count",
     "px_relax_variant", "px_stream_ceiling",
+    "px3_layout", "px3_norm_buffer_len", "px3_init_field", "px3_fill_ghosts", "px3_relax_step",
+    "px3_residual_norm", "px3_solve", "px3_release",
 ]
 
 
@@ -183,6 +190,21 @@ def lib():
     L.px_kernel_launch_count.restype = i64
     L.px_stream_ceiling.restype = st
     L.px_stream_ceiling.argtypes = [vp, vp, vp, i64, i32, vp]
+    L.px3_layout.restype = st
+    L.px3_layout.argtypes = [P(i32), i32, P(i64), P(i64), P(i64), P(i64)]
+    L.px3_norm_buffer_len.restype = i64
+    L.px3_init_field.restype = st
+    L.px3_init_field.argtypes = [P(px_patch3), i32, ctypes.c_uint64, vp]
+    L.px3_fill_ghosts.restype = st
+    L.px3_fill_ghosts.argtypes = [st, P(px_patch3), vp]
+    L.px3_relax_step.restype = st
+    L.px3_relax_step.argtypes = [P(px_relax_params), P(px_patch3), P(px_patch3), P(px_patch3), vp, vp]
+    L.px3_residual_norm.restype = st
+    L.px3_residual_norm.argtypes = [P(px_relax_params), P(px_patch3), P(px_patch3), vp, vp]
+    L.px3_solve.restype = st
+    L.px3_solve.argtypes = [st, P(px_relax_params), P(px_solve_opts), P(px_patch3), P(px_patch3), P(px_patch3),
+                            P(ctypes.c_double), i32, P(i32), P(i32), vp]
+    L.px3_release.restype = None
     L.px_relax_variant.restype = i32
     L.px_relax_variant.argtypes = [P(px_patch), P(px_patch), P(px_patch), px_box]
     _lib = L
@@ -516,3 +538,76 @@ def stream_ceiling(a, b, c, variant: int = 0, stream=None):
 
 def kernel_launch_count() -> int:
     return lib().px_kernel_launch_count()
+
+
+# ---------------------------------------------------------------------- 3D
+class Grid3:
+    """A 3D single-device field layout (px3_layout): allocation size and the
+    view of cell (0,0,0) of caller-owned torch float64 tensors."""
+
+    def __init__(self, n, ghost: int = 1):
+        self.n = tuple(int(v) for v in n)
+        self.ghost = int(ghost)
+        ld, plane, org, tot = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().px3_layout((ctypes.c_int32 * 3)(*self.n), self.ghost, ctypes.byref(ld), ctypes.byref(plane),
+                                ctypes.byref(org), ctypes.byref(tot)))
+        self.ld, self.plane, self.origin, self.alloc_elems = ld.value, plane.value, org.value, tot.value
+
+    def alloc(self, device=None):
+        import torch
+        return torch.zeros(self.alloc_elems, dtype=torch.float64, device=device or "cuda")
+
+    def patch(self, t) -> px_patch3:
+        return px_patch3(t.data_ptr() + 8 * self.origin, (ctypes.c_int32 * 3)(*self.n), self.ghost, self.ld,
+                         self.plane)
+
+    def view(self, t, ghosts: bool = False):
+        """(n2[+2g], n1[+2g], n0[+2g]) strided view of the cells of t."""
+        g = self.ghost if ghosts else 0
+        n0, n1, n2 = self.n
+        start = self.origin - g * (1 + self.ld + self.plane)
+        return t.as_strided((n2 + 2 * g, n1 + 2 * g, n0 + 2 * g), (self.plane, self.ld, 1), start)
+
+
+def norm_buffer3(device=None):
+    import torch
+    return torch.zeros(lib().px3_norm_buffer_len(), dtype=torch.float64, device=device or "cuda")
+
+
+def init_field3(grid: Grid3, t, kind: int, seed: int = 0, stream=None):
+    p = grid.patch(t)
+    _check(lib().px3_init_field(ctypes.byref(p), kind, seed, _stream(stream)))
+
+
+def fill_ghosts3(grid: Grid3, bc: int, t, stream=None):
+    p = grid.patch(t)
+    _check(lib().px3_fill_ghosts(bc, ctypes.byref(p), _stream(stream)))
+
+
+def relax_step3(p: px_relax_params, grid: Grid3, phi_in, phi_out, rhs, norms=None, stream=None):
+    a, b, r = grid.patch(phi_in), grid.patch(phi_out), grid.patch(rhs)
+    _check(lib().px3_relax_step(ctypes.byref(p), ctypes.byref(a), ctypes.byref(b), ctypes.byref(r), _ptr(norms),
+                                _stream(stream)))
+
+
+def residual_norm3(p: px_relax_params, grid: Grid3, phi, rhs, norms, stream=None):
+    a, r = grid.patch(phi), grid.patch(rhs)
+    _check(lib().px3_residual_norm(ctypes.byref(p), ctypes.byref(a), ctypes.byref(r), _ptr(norms), _stream(stream)))
+
+
+def solve3(grid: Grid3, bc: int, p: px_relax_params, nsweeps: int, norm_every: int, phi, phi_scratch, rhs,
+           use_graph: bool = False, stream=None, keep_in_scratch: bool = True) -> SolveResult:
+    """px3_solve on torch tensors allocated by grid.alloc()."""
+    opts = px_solve_opts(nsweeps, norm_every, 1, int(use_graph))
+    cap = 0 if norm_every < 0 else ((nsweeps + norm_every - 1) // norm_every if norm_every > 0 else 0) + 1
+    norms = np.zeros((max(cap, 1), 2), dtype=np.float64)
+    nw, ins = ctypes.c_int32(0), ctypes.c_int32(0)
+    a, b, r = grid.patch(phi), grid.patch(phi_scratch), grid.patch(rhs)
+    _check(lib().px3_solve(bc, ctypes.byref(p), ctypes.byref(opts), ctypes.byref(a), ctypes.byref(b), ctypes.byref(r),
+                           norms.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), max(cap, 1), ctypes.byref(nw),
+                           ctypes.byref(ins) if keep_in_scratch else None, _stream(stream)))
+    return SolveResult(norms[: nw.value].copy(), bool(ins.value))
+
+
+def release3():
+    lib().px3_release()

@@ -15,7 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def header_functions():
     src = open(os.path.join(ROOT, "include", "protox.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(px_[a-z_0-9]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(px3?_[a-z_0-9]+)\s*\(", src)))
 
 
 def test_library_exports_every_header_function():

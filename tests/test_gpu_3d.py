@@ -1,0 +1,216 @@
+"""GPU parity of the 3D relaxation (px3_*) against
+the 3D oracle (oracle/protox_oracle3d.cpp, pinned in tests/test_oracle_pins3d.py)
+on the same seeded inputs: φ bit-identical, max-norms bit-identical, Σr²
+within 1e-12 relative (different summation order, R16).  Shapes
+span several 64 x 32 tiles with ragged tails in every dimension, several z
+chunks, all three boundary rules and the norm schedules; the full-size case
+(512³, the bench's launch configuration) is checked on sampled cells by
+oracle windows around them."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2307_07931_b200 import inputs
+from paper_2307_07931_b200 import protox as P
+
+from helpers import BC_MAP, bits_equal, ulp_diff
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+SUM_RTOL = 1e-12
+BCS = [P.PX_BC_PERIODIC, P.PX_BC_DIRICHLET_CC, P.PX_BC_FIXED_GHOSTS]
+
+
+def _upload(grid, glob):
+    t = grid.alloc()
+    grid.view(t, ghosts=True).copy_(torch.from_numpy(np.ascontiguousarray(glob)))
+    return t
+
+
+def _fields(n, g, seed):
+    rng = np.random.default_rng(seed)
+    shape = (n[2] + 2 * g, n[1] + 2 * g, n[0] + 2 * g)
+    return rng.uniform(-1, 1, shape), rng.uniform(-1, 1, shape)
+
+
+def _check_norms(gpu, orc):
+    assert gpu.shape == orc.shape, (gpu.shape, orc.shape)
+    assert bits_equal(gpu[:, 0], orc[:, 0]), (gpu[:, 0], orc[:, 0])
+    np.testing.assert_allclose(gpu[:, 1], orc[:, 1], rtol=SUM_RTOL, atol=0)
+
+
+def run3(n, bc, N, E, seed=1, graph=True, g=1, h=None, lam=None, phi0=None, rho=None):
+    h = h or 1.0 / max(n)
+    lam = lam if lam is not None else h * h / 12  # λ = h²/(4D), D = 3
+    if phi0 is None:
+        phi0, rho = _fields(n, g, seed)
+    grid = P.Grid3(n, g)
+    a, b, r = _upload(grid, phi0), grid.alloc(), _upload(grid, rho)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    res = P.solve3(grid, bc, P.relax_params(h, lam, P.PX_LAPLACE_7PT_3D), N, E, a, b, r, use_graph=graph,
+                   stream=s)
+    out = grid.view(b if res.in_scratch else a).cpu().numpy()
+    p = oracle.Problem3(n, h, lam, ghost=g, bc=BC_MAP[bc], nsweeps=N, norm_every=E)
+    ref, rn = oracle.solve3(p, phi0, rho)
+    return out, res.norms, ref[g:-g, g:-g, g:-g], rn
+
+
+@pytest.mark.parametrize("bc", BCS)
+@pytest.mark.parametrize("n", [(64, 32, 6), (70, 37, 13), (130, 65, 9), (5, 3, 2), (1, 1, 1)])
+def test_solve3_bitwise(bc, n):
+    out, norms, ref, rn = run3(n, bc, 7, 2, seed=sum(n) + bc)
+    assert bits_equal(out, ref), ulp_diff(out, ref)
+    _check_norms(norms, rn)
+
+
+@pytest.mark.parametrize("E", [-1, 0, 1, 3])
+@pytest.mark.parametrize("graph", [True, False])
+def test_solve3_norm_schedules_and_graph(E, graph):
+    n = (96, 40, 11)
+    out, norms, ref, rn = run3(n, P.PX_BC_PERIODIC, 6, E, seed=7 + E, graph=graph)
+    assert bits_equal(out, ref)
+    if E >= 0:
+        _check_norms(norms, rn)
+    else:
+        assert norms.shape[0] == 0
+
+
+def test_solve3_many_z_chunks_and_ghost2():
+    """z extent large enough that the planner splits columns into several z
+    chunks (each re-reads its first plane); ghost width 2; non-pow2 h."""
+    n = (64, 64, 150)
+    out, norms, ref, rn = run3(n, P.PX_BC_DIRICHLET_CC, 5, 1, seed=3, g=2, h=1.0 / 150)
+    assert bits_equal(out, ref), ulp_diff(out, ref)
+    _check_norms(norms, rn)
+
+
+def test_solve3_repeat_replays_cached_graph():
+    n = (66, 34, 8)
+    phi0, rho = _fields(n, 1, 5)
+    grid = P.Grid3(n, 1)
+    a, b, r = _upload(grid, phi0), grid.alloc(), _upload(grid, rho)
+    prm = P.relax_params(1 / 66, (1 / 66) ** 2 / 12, P.PX_LAPLACE_7PT_3D)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    r1 = P.solve3(grid, P.PX_BC_PERIODIC, prm, 4, 1, a, b, r, use_graph=True, stream=s)
+    r2 = P.solve3(grid, P.PX_BC_PERIODIC, prm, 4, 1, a, b, r, use_graph=True, stream=s)  # continues from φ^4
+    p = oracle.Problem3(n, 1 / 66, (1 / 66) ** 2 / 12, nsweeps=8, norm_every=1)
+    ref, rn = oracle.solve3(p, phi0, rho)
+    out = grid.view(b if r2.in_scratch else a).cpu().numpy()
+    assert bits_equal(out, ref[1:-1, 1:-1, 1:-1])
+    assert bits_equal(np.concatenate([r1.norms[:4, 0], r2.norms[:, 0]]), rn[:, 0])
+
+
+def test_relax_step3_and_residual_vs_oracle():
+    n = (100, 50, 7)
+    h = 1 / 100
+    lam = h * h / 12
+    phi0, rho = _fields(n, 1, 9)
+    grid = P.Grid3(n, 1)
+    a, b, r = _upload(grid, phi0), grid.alloc(), _upload(grid, rho)
+    prm = P.relax_params(h, lam, P.PX_LAPLACE_7PT_3D)
+    nb, nb2 = P.norm_buffer3(), P.norm_buffer3()
+    P.fill_ghosts3(grid, P.PX_BC_PERIODIC, a)
+    P.relax_step3(prm, grid, a, b, r, nb)
+    P.fill_ghosts3(grid, P.PX_BC_PERIODIC, b)
+    P.residual_norm3(prm, grid, b, r, nb2)
+    torch.cuda.synchronize()
+    p = oracle.Problem3(n, h, lam, nsweeps=1, norm_every=1)
+    ref, rn = oracle.solve3(p, phi0, rho)
+    assert bits_equal(grid.view(b).cpu().numpy(), ref[1:-1, 1:-1, 1:-1])
+    got = np.array([nb[:2].cpu().numpy(), nb2[:2].cpu().numpy()])
+    _check_norms(got, rn)
+
+
+@pytest.mark.parametrize("bc", [P.PX_BC_PERIODIC, P.PX_BC_DIRICHLET_CC])
+@pytest.mark.parametrize("g", [1, 2])
+def test_fill_ghosts3_matches_oracle_exchange(bc, g):
+    n = (9, 6, 5)
+    rng = np.random.default_rng(4)
+    glob = rng.uniform(-1, 1, (n[2] + 2 * g, n[1] + 2 * g, n[0] + 2 * g))
+    grid = P.Grid3(n, g)
+    t = _upload(grid, glob)
+    P.fill_ghosts3(grid, bc, t)
+    torch.cuda.synchronize()
+    want = oracle.exchange3(oracle.Problem3(n, 1.0, 0.0, ghost=g, bc=BC_MAP[bc]), glob)
+    assert bits_equal(grid.view(t, ghosts=True).cpu().numpy(), want)
+
+
+def test_init_field3_hash_bitwise():
+    n = (37, 20, 11)
+    grid = P.Grid3(n, 1)
+    t = grid.alloc()
+    P.init_field3(grid, t, 1, inputs.DEFAULT_SEED)
+    torch.cuda.synchronize()
+    assert bits_equal(grid.view(t).cpu().numpy(), inputs.hash_field3(*n))
+
+
+def test_nan_propagates3():
+    n = (64, 32, 4)
+    phi0, rho = _fields(n, 1, 2)
+    phi0[2, 5, 9] = np.nan
+    out, norms, ref, rn = run3(n, P.PX_BC_PERIODIC, 1, 1, phi0=phi0, rho=rho)
+    assert math.isnan(norms[0, 0]) and math.isnan(rn[0, 0])
+
+
+def test_errors3():
+    grid = P.Grid3((16, 8, 4), 1)
+    a, b, r = grid.alloc(), grid.alloc(), grid.alloc()
+    with pytest.raises(P.PxError, match="PX_LAPLACE_7PT_3D"):
+        P.solve3(grid, 0, P.relax_params(1 / 16, 1e-4, P.PX_LAPLACE_5PT), 2, 1, a, b, r)
+    with pytest.raises(P.PxError, match="differ"):
+        P.solve3(grid, 0, P.relax_params(1 / 16, 1e-4, P.PX_LAPLACE_7PT_3D), 2, 1, a, a, r)
+    g2 = P.Grid3((16, 8, 5), 1)
+    c = g2.alloc()
+    pa, pc = grid.patch(a), g2.patch(c)
+    import ctypes
+    nb = P.norm_buffer3()
+    st = P.lib().px3_relax_step(ctypes.byref(P.relax_params(1 / 16, 1e-4, P.PX_LAPLACE_7PT_3D)), ctypes.byref(pa),
+                                ctypes.byref(pc), ctypes.byref(pa), ctypes.c_void_p(nb.data_ptr()), None)
+    assert st == P.PX_ERR_SHAPE
+    bad = grid.patch(a)
+    bad.data += 8  # misaligned cell (0,0,0)
+    st = P.lib().px3_fill_ghosts(0, ctypes.byref(bad), None)
+    assert st == P.PX_ERR_ALIGN
+
+
+# ------------------------------------------------------------ full size (512³)
+def test_full_size_512_sampled_windows():
+    """512³ periodic, hash ρ (device generator), φ⁰ = 0, N = 12 sweeps in the
+    bench's launch configuration: each sampled cell is recomputed by the
+    oracle on the (2N+1)³ window around it (FIXED ghosts one layer further
+    out cannot reach the centre in N sweeps) -- bit-identical; the recorded
+    norm of φ⁰ equals the closed form r(0) = −ρ."""
+    n = (512, 512, 512)
+    N = 12
+    h = 1 / 512
+    lam = h * h / 12
+    grid = P.Grid3(n, 1)
+    a, b, r = grid.alloc(), grid.alloc(), grid.alloc()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    P.init_field3(grid, r, 1, inputs.DEFAULT_SEED, stream=s)
+    res = P.solve3(grid, P.PX_BC_PERIODIC, P.relax_params(h, lam, P.PX_LAPLACE_7PT_3D), N, 1, a, b, r,
+                   use_graph=True, stream=s)
+    out_t = b if res.in_scratch else a
+    vw = grid.view(out_t)
+    assert res.norms[0, 0] == float(grid.view(r).abs().max().item())  # r(φ⁰ = 0) = −ρ
+    rng = np.random.default_rng(12)
+    samples = [(0, 0, 0), (511, 511, 511), (255, 3, 509)] + [tuple(int(v) for v in rng.integers(0, 512, 3))
+                                                             for _ in range(3)]
+    w = N  # window half-width
+    m = 2 * w + 1
+    for (x, y, z) in samples:
+        idx = [(np.arange(c - w - 1, c + w + 2) % 512) for c in (x, y, z)]
+        iz, iy, ix = np.meshgrid(idx[2], idx[1], idx[0], indexing="ij")
+        rho_g = inputs.hash_values3(ix, iy, iz, n[0], n[1])
+        p = oracle.Problem3((m, m, m), h, lam, bc=oracle.BC_FIXED, nsweeps=N, norm_every=-1)
+        ref, _ = oracle.solve3(p, np.zeros(p.gshape), np.ascontiguousarray(rho_g))
+        got = float(vw[z, y, x].item())
+        want = ref[w + 1, w + 1, w + 1]
+        assert np.float64(got).view(np.uint64) == np.float64(want).view(np.uint64), ((x, y, z), got, want)
