@@ -29,6 +29,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -44,12 +45,13 @@ constexpr int BXW = TX + 4, BYH = TY + 2;   // φ box: columns x0-2 .. x0+TX+1, 
 constexpr int NWC = 8;                      // consumer warps, warp w: tile rows 4w .. 4w+3
 constexpr int RPW = TY / NWC;               // rows per warp (4)
 constexpr int THREADS = NWC * 32 + 32;
-constexpr int NST = 4;
+constexpr int NST_MAX = 6;  // ring stages: template parameter, default 4 (PROTOX_K3_NST A/B)
 constexpr int PHI_PAD = (BXW * BYH + 15) / 16 * 16;  // 128-byte aligned ρ tile
 constexpr int STAGE = PHI_PAD + TX * TY;             // doubles
 constexpr uint32_t PHI_BYTES = BXW * BYH * 8u;
 constexpr uint32_t RHO_BYTES = TX * TY * 8u;
-constexpr size_t SMEM = (size_t)NST * STAGE * sizeof(double) + 2 * NST * sizeof(uint64_t);
+template <int NST>
+constexpr size_t smem_bytes() { return (size_t)NST * STAGE * sizeof(double) + 2 * NST * sizeof(uint64_t); }
 constexpr int MAX_GRID = 512;
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -91,12 +93,13 @@ struct Relax3 {
   int32_t nitems;
   double scale, lambda;
   NormSlot norms;
+  int32_t policy;         // L2 policies (A/B knob PROTOX_K3_POLICY): 0 ρ evict_first + φ evict_last
 };
 
 // The map's origin is cell (-2, -g, -g) of the patch, so tensor coordinate
 // (c0, c1, c2) is cell (c0 - 2, c1 - g, c2 - g).
-template <int MODE>
-__global__ void __launch_bounds__(k3::THREADS, 1)
+template <int MODE, int NST>
+__global__ void __launch_bounds__(k3::THREADS, NST == 3 ? 2 : 1)
     k3_relax(const __grid_constant__ CUtensorMap mphi, const __grid_constant__ CUtensorMap mrho, const Relax3 a,
              int g) {
   using namespace k3;
@@ -119,10 +122,17 @@ __global__ void __launch_bounds__(k3::THREADS, 1)
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mphi)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mrho)) : "memory");
-      uint64_t pol;
-      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-      uint64_t pol_halo;  // the φ planes: their halo rows are re-read by the neighbouring tiles
-      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_halo));
+      uint64_t pol, pol_halo;  // ρ: read once; φ planes: their halo rows are re-read by the neighbouring tiles
+      if (a.policy == 0) {
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_halo));
+      } else if (a.policy == 1) {
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+        pol_halo = pol;
+      } else {
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_halo));
+      }
       int slot = 0;
       uint32_t phase = 0;
       for (int it = blockIdx.x; it < a.nitems; it += gridDim.x) {
@@ -332,19 +342,39 @@ static px_status make_map(const px_patch3& p, uint32_t bx, uint32_t by, CUtensor
   cuuint64_t strides[2] = {(cuuint64_t)p.ld * 8, (cuuint64_t)p.plane * 8};
   cuuint32_t box[3] = {bx, by, 1};
   cuuint32_t es[3] = {1, 1, 1};
+  static int promo = -1;  // A/B knob PROTOX_K3_PROMO: 0 none, 1 64B, 2 128B (default), 3 256B
+  if (promo < 0) {
+    const char* ev = getenv("PROTOX_K3_PROMO");
+    promo = ev ? atoi(ev) : 2;
+    if (promo < 0 || promo > 3) promo = 2;
+  }
+  const CUtensorMapL2promotion pr[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
+                                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  CU_TENSOR_MAP_SWIZZLE_NONE, pr[promo], CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(PX_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return PX_OK;
 }
 
 // z chunks: items = tiles x chunks; minimise waves x (planes per chunk + 2)
+// ring stages and CTAs per SM: 4 stages x 1 CTA (default) or 3 stages x 2 CTAs
+// (PROTOX_K3_NST=3 selects the latter; 6 = six stages x 1 CTA), A/B knob
+static int k3_nst() {
+  static int nst = -1;
+  if (nst < 0) {
+    const char* ev = getenv("PROTOX_K3_NST");
+    nst = ev ? atoi(ev) : 4;
+    if (nst != 3 && nst != 6) nst = 4;
+  }
+  return nst;
+}
+
 static void plan3(const int32_t n[3], Relax3& a, int* grid) {
   a.ntx = (n[0] + k3::TX - 1) / k3::TX;
   a.nty = (n[1] + k3::TY - 1) / k3::TY;
   const int tiles = a.ntx * a.nty;
-  const int gmax = k3_nsm() < k3::MAX_GRID ? k3_nsm() : k3::MAX_GRID;
+  const int cps = k3_nst() == 3 ? 2 : 1;
+  const int gmax = cps * k3_nsm() < k3::MAX_GRID ? cps * k3_nsm() : k3::MAX_GRID;
   double best = 1e30;
   int bc = 1;
   for (int c = 1; c <= n[2] && c <= 64; ++c) {
@@ -391,6 +421,20 @@ static px_status same_shape3(const px_patch3& a, const px_patch3& b, const char*
 
 static bool pow2_ok(double h) { return h > 0.0 && std::isfinite(h); }
 
+template <int MODE, int NST>
+static cudaError_t k3_go(const CUtensorMap& mphi, const CUtensorMap& mrho, const Relax3& a, int g, int grid,
+                         cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k3_relax<MODE, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)k3::smem_bytes<NST>());
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  k3_relax<MODE, NST><<<grid, k3::THREADS, k3::smem_bytes<NST>(), s>>>(mphi, mrho, a, g);
+  return cudaSuccess;
+}
+
 static px_status launch_relax3(int mode, const px_relax_params& prm, const px_patch3& in, const px_patch3* out,
                                const px_patch3& rhs, const NormSlot& ns, cudaStream_t s) {
   CUtensorMap mphi, mrho;
@@ -407,24 +451,22 @@ static px_status launch_relax3(int mode, const px_relax_params& prm, const px_pa
   a.scale = 1.0 / (prm.h * prm.h);
   a.lambda = prm.lambda;
   a.norms = ns;
-  cudaError_t e;
-  if (mode == MODE_RELAX) {
-    static bool attr = false;
-    if (!attr) {
-      e = cudaFuncSetAttribute(k3_relax<MODE_RELAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k3::SMEM);
-      if (e != cudaSuccess) return cuda_check(e, "3D relax attribute");
-      attr = true;
-    }
-    k3_relax<MODE_RELAX><<<grid, k3::THREADS, k3::SMEM, s>>>(mphi, mrho, a, in.ghost);
-  } else {
-    static bool attr = false;
-    if (!attr) {
-      e = cudaFuncSetAttribute(k3_relax<MODE_RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k3::SMEM);
-      if (e != cudaSuccess) return cuda_check(e, "3D residual attribute");
-      attr = true;
-    }
-    k3_relax<MODE_RESID><<<grid, k3::THREADS, k3::SMEM, s>>>(mphi, mrho, a, in.ghost);
+  static int policy = -1;
+  if (policy < 0) {
+    const char* ev = getenv("PROTOX_K3_POLICY");
+    policy = ev ? atoi(ev) : 0;
   }
+  a.policy = policy;
+  const int nst = k3_nst();
+  cudaError_t e = cudaSuccess;
+  if (mode == MODE_RELAX) {
+    if (nst == 3) e = k3_go<MODE_RELAX, 3>(mphi, mrho, a, in.ghost, grid, s);
+    else if (nst == 6) e = k3_go<MODE_RELAX, 6>(mphi, mrho, a, in.ghost, grid, s);
+    else e = k3_go<MODE_RELAX, 4>(mphi, mrho, a, in.ghost, grid, s);
+  } else {
+    e = k3_go<MODE_RESID, 4>(mphi, mrho, a, in.ghost, grid, s);
+  }
+  if (e != cudaSuccess) return cuda_check(e, "3D relax attribute");
   count_launches(1);
   return cuda_check(cudaGetLastError(), "3D relax launch");
 }
