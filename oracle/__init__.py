@@ -57,6 +57,7 @@ class _Problem3(ctypes.Structure):
     _fields_ = [
         ("n", ctypes.c_int64 * 3), ("b", ctypes.c_int64 * 3),
         ("ghost", ctypes.c_int32), ("bc", ctypes.c_int32),
+        ("stencil", ctypes.c_int32), ("rhs_correction", ctypes.c_int32),
         ("h", ctypes.c_double), ("lam", ctypes.c_double),
         ("nsweeps", ctypes.c_int64), ("norm_every", ctypes.c_int64),
     ]
@@ -102,6 +103,7 @@ def _L():
         _lib.orc3_solve.argtypes = [P3, d, d, d, d, i64, ctypes.POINTER(i64)]
         _lib.orc3_apply_laplacian.argtypes = [P3, d, d]
         _lib.orc3_exchange.argtypes = [P3, d]
+        _lib.orc3_rhs.argtypes = [P3, d, d]
     return _lib
 
 
@@ -319,11 +321,14 @@ class Problem3:
     bc: int = BC_PERIODIC
     nsweeps: int = 0
     norm_every: int = 0
+    stencil: int = 0            # 0 = 7-point, 1 = 27-point Mehrstellen
+    rhs_correction: bool = False
 
     def c(self) -> _Problem3:
         b = self.b or self.n
         return _Problem3((ctypes.c_int64 * 3)(*self.n), (ctypes.c_int64 * 3)(*b), self.ghost, self.bc,
-                         self.h, self.lam, self.nsweeps, self.norm_every)
+                         self.stencil, int(self.rhs_correction), self.h, self.lam, self.nsweeps,
+                         self.norm_every)
 
     @property
     def gshape(self):
@@ -373,3 +378,12 @@ def exchange3(p: Problem3, glob: np.ndarray) -> np.ndarray:
     pc = p.c()
     _check3(_L().orc3_exchange(ctypes.byref(pc), _dp(g)))
     return g
+
+
+def rhs3(p: Problem3, rho_g: np.ndarray) -> np.ndarray:
+    """The right-hand side the 3D solve uses: ρ, or ρ + S7(ρ)/12 (27-point with correction)."""
+    rho_g = np.ascontiguousarray(rho_g, dtype=np.float64)
+    out = np.zeros((p.n[2], p.n[1], p.n[0]), dtype=np.float64)
+    pc = p.c()
+    _check3(_L().orc3_rhs(ctypes.byref(pc), _dp(rho_g), _dp(out)))
+    return out

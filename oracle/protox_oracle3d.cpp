@@ -28,6 +28,9 @@
  *        reflection per dimension (a ghost outside Ω in several dimensions
  *        gets the product of the signs), FIXED_GHOSTS (ghosts outside Ω are
  *        the caller's and never change).
+ *  R-3D4 27-point compact Mehrstellen variant (the 3D counterpart of
+ *        BASELINE config 5): faces 14, edges 3, corners 1, centre -128,
+ *        scale 1/(30h²); fourth order with f = ρ + (1/12)·S7(ρ).
  *  R-3D3 layout: a global ghosted array of (n0+2g)(n1+2g)(n2+2g) doubles,
  *        dimension 0 fastest, then 1, then 2; the domain is split into
  *        b0 x b1 x b2 boxes, each with its own ghost ring (BoxData).
@@ -94,6 +97,26 @@ struct Tap3 {
 static std::vector<Tap3> laplace7() {
   return {{p3(-1, 0, 0), 1.0}, {p3(1, 0, 0), 1.0}, {p3(0, -1, 0), 1.0}, {p3(0, 1, 0), 1.0},
           {p3(0, 0, -1), 1.0}, {p3(0, 0, 1), 1.0}, {p3(0, 0, 0), -6.0}};
+}
+
+/* 27-point compact fourth-order Mehrstellen operator (reading R-3D4; the 3D
+ * counterpart of the BASELINE config-5 9-point stencil, not in the paper):
+ * scale 1/(30h²), faces 14, edges 3, corners 1, centre -128, in the order
+ * faces W,E,S,N,B,T; edges xy (-1,-1),(1,-1),(-1,1),(1,1), xz (-1,·,-1),
+ * (1,·,-1),(-1,·,1),(1,·,1), yz (·,-1,-1),(·,1,-1),(·,-1,1),(·,1,1);
+ * corners z-major then y then x; centre. */
+static std::vector<Tap3> mehrstellen27() {
+  std::vector<Tap3> t = {{p3(-1, 0, 0), 14.0}, {p3(1, 0, 0), 14.0}, {p3(0, -1, 0), 14.0},
+                         {p3(0, 1, 0), 14.0},  {p3(0, 0, -1), 14.0}, {p3(0, 0, 1), 14.0}};
+  const int e2[4][2] = {{-1, -1}, {1, -1}, {-1, 1}, {1, 1}};
+  for (auto& e : e2) t.push_back({p3(e[0], e[1], 0), 3.0});
+  for (auto& e : e2) t.push_back({p3(e[0], 0, e[1]), 3.0});
+  for (auto& e : e2) t.push_back({p3(0, e[0], e[1]), 3.0});
+  for (int z = -1; z <= 1; z += 2)
+    for (int y = -1; y <= 1; y += 2)
+      for (int x = -1; x <= 1; x += 2) t.push_back({p3(x, y, z), 1.0});
+  t.push_back({p3(0, 0, 0), -128.0});
+  return t;
 }
 
 static double tap_sum3(const std::vector<Tap3>& taps, const BoxData3& src, P3 i) {
@@ -291,9 +314,48 @@ typedef struct {
   int64_t b[3];   /* box size per dimension (must divide n) */
   int32_t ghost;  /* ghost width g >= 1 */
   int32_t bc;     /* 0 periodic, 1 dirichlet-cc, 2 fixed ghosts */
+  int32_t stencil;         /* 0 = 7-point, 1 = 27-point Mehrstellen */
+  int32_t rhs_correction;  /* 27-point only: f = rho + (1/12) S7(rho) */
   double h, lambda;
   int64_t nsweeps, norm_every;
 } orc3_problem;
+
+static bool setup3(const orc3_problem* p, std::vector<Tap3>& taps, double& scale) {
+  if (p->stencil == 0) {
+    taps = laplace7();
+    scale = 1.0 / (p->h * p->h);
+  } else if (p->stencil == 1) {
+    taps = mehrstellen27();
+    scale = 1.0 / (30.0 * p->h * p->h);
+  } else {
+    g_err3 = "stencil must be 0 (7-point) or 1 (27-point Mehrstellen)";
+    return false;
+  }
+  return true;
+}
+
+/* f = ρ on the interior; with the 27-point stencil and rhs_correction,
+ * f = ρ + (1/12)·S7(ρ) with ρ's ghosts filled by the boundary rule (R-3D4). */
+static void make_rhs3(const orc3_problem* p, const double* rho_g, Level3& f) {
+  scatter3(rho_g, f);
+  if (p->stencil != 1 || !p->rhs_correction) return;
+  exchange3(f);
+  const std::vector<Tap3> s7 = laplace7();
+  const double c12 = 1.0 / 12.0;
+  for (size_t ib = 0; ib < f.L->boxes.size(); ++ib) {
+    const Box3& B = f.L->boxes[ib];
+    BoxData3 corr(B);
+    for (int64_t z = B.lo.c[2]; z <= B.hi.c[2]; ++z)
+      for (int64_t y = B.lo.c[1]; y <= B.hi.c[1]; ++y)
+        for (int64_t x = B.lo.c[0]; x <= B.hi.c[0]; ++x) corr.at(p3(x, y, z)) = tap_sum3(s7, f.data[ib], p3(x, y, z));
+    for (int64_t z = B.lo.c[2]; z <= B.hi.c[2]; ++z)
+      for (int64_t y = B.lo.c[1]; y <= B.hi.c[1]; ++y)
+        for (int64_t x = B.lo.c[0]; x <= B.hi.c[0]; ++x) {
+          const P3 q = p3(x, y, z);
+          f.data[ib].at(q) = f.data[ib].at(q) + c12 * corr.at(q);
+        }
+  }
+}
 
 const char* orc3_last_error(void) { return g_err3.c_str(); }
 
@@ -312,11 +374,12 @@ int orc3_solve(const orc3_problem* p, const double* phi0, const double* rho, dou
   }
   Layout3 L;
   if (!make_layout3(p->n, p->b, p->ghost, p->bc, L)) return 1;
-  const std::vector<Tap3> taps = laplace7();
-  const double scale = 1.0 / (p->h * p->h);
+  std::vector<Tap3> taps;
+  double scale;
+  if (!setup3(p, taps, scale)) return 1;
   Level3 phi(L), f(L);
   scatter3(phi0, phi);
-  scatter3(rho, f);
+  make_rhs3(p, rho, f);
   int64_t nw = 0;
   auto record = [&]() {
     double r[2];
@@ -342,8 +405,9 @@ int orc3_solve(const orc3_problem* p, const double* phi0, const double* rho, dou
 int orc3_apply_laplacian(const orc3_problem* p, const double* phi_g, double* out) {
   Layout3 L;
   if (!make_layout3(p->n, p->b, p->ghost, p->bc, L)) return 1;
-  const std::vector<Tap3> taps = laplace7();
-  const double scale = 1.0 / (p->h * p->h);
+  std::vector<Tap3> taps;
+  double scale;
+  if (!setup3(p, taps, scale)) return 1;
   Level3 phi(L);
   scatter3(phi_g, phi);
   exchange3(phi);
@@ -353,6 +417,21 @@ int orc3_apply_laplacian(const orc3_problem* p, const double* phi_g, double* out
       for (int64_t y = B.lo.c[1]; y <= B.hi.c[1]; ++y)
         for (int64_t x = B.lo.c[0]; x <= B.hi.c[0]; ++x)
           out[x + L.n[0] * (y + L.n[1] * z)] = scale * tap_sum3(taps, phi.data[ib], p3(x, y, z));
+  }
+  return 0;
+}
+
+/* the right-hand side the solve uses (f = ρ, or ρ + S7(ρ)/12), interior n2 x n1 x n0 */
+int orc3_rhs(const orc3_problem* p, const double* rho_g, double* out) {
+  Layout3 L;
+  if (!make_layout3(p->n, p->b, p->ghost, p->bc, L)) return 1;
+  Level3 f(L);
+  make_rhs3(p, rho_g, f);
+  for (size_t ib = 0; ib < L.boxes.size(); ++ib) {
+    const Box3& B = L.boxes[ib];
+    for (int64_t z = B.lo.c[2]; z <= B.hi.c[2]; ++z)
+      for (int64_t y = B.lo.c[1]; y <= B.hi.c[1]; ++y)
+        for (int64_t x = B.lo.c[0]; x <= B.hi.c[0]; ++x) out[x + L.n[0] * (y + L.n[1] * z)] = f.data[ib].at(p3(x, y, z));
   }
   return 0;
 }

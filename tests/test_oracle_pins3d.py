@@ -253,3 +253,132 @@ def test_nan_propagates():
     phi0[2, 2, 2] = np.nan
     _, norms = oracle.solve3(p, phi0, rho)
     assert math.isnan(norms[0, 0]) and math.isnan(norms[-1, 0])
+
+
+# ------------------------------------------------------- 27-point Mehrstellen (R-3D4)
+def test_mehrstellen27_exact_on_integer_quadratics():
+    n = (6, 5, 7)
+    p = oracle.Problem3(n, 1.0, 0.0, bc=BC_FIXED, ghost=1, stencil=1)
+    z, y, x = np.meshgrid(np.arange(-1, n[2] + 1), np.arange(-1, n[1] + 1), np.arange(-1, n[0] + 1),
+                          indexing="ij")
+    x, y, z = x.astype(float), y.astype(float), z.astype(float)
+    for (a, b, c, d, e, f) in [(1, 0, 0, 0, 0, 0), (0, 0, 1, 0, 0, 0), (2, -1, 5, 3, -7, 4), (0, 0, 0, 1, 1, 1)]:
+        phi = a * x * x + b * y * y + c * z * z + d * x * y + e * y * z + f * z * x + 3 * x - 2 * y + z + 11
+        lap = oracle.apply_laplacian3(p, phi)  # = fl(1/30) * (60 (a+b+c)) exactly up to that one rounding
+        np.testing.assert_allclose(lap, 2 * (a + b + c), rtol=2e-16, atol=0)
+    assert np.all(oracle.apply_laplacian3(p, np.full(p.gshape, 3.5)) == 0.0)
+
+
+def _mu27(c, h):
+    """Eigenvalue of the 27-point operator on a separable cosine/sine mode with
+    per-dimension factors c_d = cos(θ_d)."""
+    cx, cy, cz = c
+    return (-128 + 28 * (cx + cy + cz) + 12 * (cx * cy + cy * cz + cz * cx) + 8 * cx * cy * cz) / (30 * h * h)
+
+
+@pytest.mark.parametrize("k", [(1, 0, 0), (1, 2, 3), (3, 1, 2)])
+def test_mehrstellen27_periodic_eigenvalues(k):
+    n = (8, 12, 16)
+    h = 1.0 / 8
+    p = oracle.Problem3(n, h, 0.0, bc=BC_PERIODIC, stencil=1)
+    Z, Y, X = np.meshgrid(*[np.arange(m) for m in n[::-1]], indexing="ij")
+    v = np.cos(2 * np.pi * (k[0] * X / n[0] + k[1] * Y / n[1] + k[2] * Z / n[2]))
+    mu = _mu27([math.cos(2 * math.pi * k[d] / n[d]) for d in range(3)], h)
+    lap = oracle.apply_laplacian3(p, oracle.ghosted3(p, v))
+    np.testing.assert_allclose(lap, mu * v, rtol=0, atol=1e-11 * abs(mu))
+
+
+@pytest.mark.parametrize("k", [(1, 1, 1), (2, 1, 3)])
+def test_mehrstellen27_dirichlet_eigenvalues(k):
+    n = (8, 6, 10)
+    h = 1.0 / 8
+    p = oracle.Problem3(n, h, 0.0, bc=BC_DIRICHLET_CC, stencil=1)
+    xs = [np.sin(k[d] * np.pi * (np.arange(n[d]) + 0.5) / n[d]) for d in range(3)]
+    v = xs[2][:, None, None] * xs[1][None, :, None] * xs[0][None, None, :]
+    mu = _mu27([math.cos(k[d] * math.pi / n[d]) for d in range(3)], h)
+    lap = oracle.apply_laplacian3(p, oracle.ghosted3(p, v))
+    np.testing.assert_allclose(lap, mu * v, rtol=0, atol=1e-11 * abs(mu))
+
+
+def _shift(m, s, bc):
+    """1D shift (u_{i+s}) with the boundary rule folded in (s = -1, 0, 1)."""
+    if s == 0:
+        return np.eye(m)
+    S = np.eye(m, k=s)
+    if bc == BC_PERIODIC:
+        S[(0 if s < 0 else m - 1), (m - 1 if s < 0 else 0)] = 1.0
+    elif bc == BC_DIRICHLET_CC:
+        i = 0 if s < 0 else m - 1
+        S[i, i] = -1.0
+    return S
+
+
+def _dense27(n, h, bc):
+    w = {0: -128.0, 1: 14.0, 2: 3.0, 3: 1.0}
+    A = np.zeros((n[0] * n[1] * n[2],) * 2)
+    for dz in (-1, 0, 1):
+        for dy in (-1, 0, 1):
+            for dx in (-1, 0, 1):
+                A += w[abs(dx) + abs(dy) + abs(dz)] * np.kron(_shift(n[2], dz, bc),
+                                                            np.kron(_shift(n[1], dy, bc), _shift(n[0], dx, bc)))
+    return A / (30 * h * h)
+
+
+@pytest.mark.parametrize("bc", [BC_PERIODIC, BC_DIRICHLET_CC])
+def test_mehrstellen27_dense_bruteforce(bc):
+    n = (4, 4, 5)
+    h = 1.0 / 4
+    lam = h * h / 12
+    N = 6
+    p = oracle.Problem3(n, h, lam, b=(2, 2, 5), bc=bc, nsweeps=N, norm_every=1, stencil=1)
+    phi0, rho = _rand(p, 31 + bc)
+    out, norms = oracle.solve3(p, phi0, rho)
+    A = _dense27(n, h, bc)
+    x = _interior(p, phi0).reshape(-1).copy()
+    f = _interior(p, rho).reshape(-1)
+    want = []
+    for _ in range(N):
+        r = A @ x - f
+        want.append((np.max(np.abs(r)), np.sum(r * r)))
+        x = x + lam * r
+    r = A @ x - f
+    want.append((np.max(np.abs(r)), np.sum(r * r)))
+    np.testing.assert_allclose(_interior(p, out).reshape(-1), x, rtol=0, atol=1e-13 * np.max(np.abs(x)))
+    np.testing.assert_allclose(norms, np.array(want), rtol=1e-12)
+
+
+def test_mehrstellen27_rhs_correction_is_rho_plus_s7_over_12():
+    n = (6, 5, 4)
+    p = oracle.Problem3(n, 0.1, 0.0, bc=BC_PERIODIC, stencil=1, rhs_correction=True)
+    rng = np.random.default_rng(8)
+    rho = rng.uniform(-1, 1, (n[2], n[1], n[0]))
+    pad = np.pad(rho, 1, mode="wrap")
+    s7 = (pad[1:-1, 1:-1, :-2] + pad[1:-1, 1:-1, 2:] + pad[1:-1, :-2, 1:-1] + pad[1:-1, 2:, 1:-1]
+          + pad[:-2, 1:-1, 1:-1] + pad[2:, 1:-1, 1:-1] - 6 * rho)
+    np.testing.assert_allclose(oracle.rhs3(p, oracle.ghosted3(p, rho)), rho + s7 / 12, rtol=0, atol=1e-15)
+
+
+def _truncation(n, stencil, corr):
+    """max |Δ_h φ*(cells) − f_h| with φ* = sin πx sin πy sin πz, ρ = Δφ* = −3π²φ*
+    and FIXED ghosts holding φ*, ρ sampled (cell centres, h = 1/n)."""
+    h = 1.0 / n
+    c = (np.arange(-1, n + 1) + 0.5) * h
+    s = np.sin(np.pi * c)
+    phi = s[:, None, None] * s[None, :, None] * s[None, None, :]
+    rho = -3 * np.pi**2 * phi
+    p = oracle.Problem3((n, n, n), h, 0.0, bc=BC_FIXED, stencil=stencil, rhs_correction=corr, nsweeps=0,
+                        norm_every=0)
+    _, norms = oracle.solve3(p, phi, rho)
+    return norms[0, 0]
+
+
+def test_truncation_order_ladder():
+    """7-point: τ_h ratio 4 as h halves (second order); 27-point Mehrstellen
+    with f = ρ + S7(ρ)/12: ratio 16 (fourth order); without the correction it
+    drops back to 4."""
+    t7 = [_truncation(n, 0, False) for n in (16, 32, 64)]
+    t27 = [_truncation(n, 1, True) for n in (16, 32, 64)]
+    t27n = [_truncation(n, 1, False) for n in (16, 32, 64)]
+    for t, lo, hi in ((t7, 3.9, 4.1), (t27, 15.5, 16.5), (t27n, 3.9, 4.1)):
+        r = [t[i] / t[i + 1] for i in range(2)]
+        assert all(lo < q < hi for q in r), (t, r)
