@@ -155,7 +155,12 @@ typedef struct {
 px_status px_layout_halo_plan(const px_layout* l, int32_t rank, px_halo_op ops[4], int32_t* nops);
 
 /* ----------------------------------------------------------------- kernels */
-typedef enum { PX_LAPLACE_5PT = 0, PX_MEHRSTELLEN_9PT = 1, PX_LAPLACE_7PT_3D = 2 } px_stencil;
+typedef enum {
+  PX_LAPLACE_5PT = 0,
+  PX_MEHRSTELLEN_9PT = 1,
+  PX_LAPLACE_7PT_3D = 2,
+  PX_MEHRSTELLEN_27PT_3D = 3
+} px_stencil;
 /* stencil: taps in the fixed order W,E,S,N(1),C(-4) for 5-point; W,E,S,N(4),
  * SW,SE,NW,NE(1),C(-20) for Mehrstellen (not in the paper, BASELINE config 5).
  * scale = 1/(h*h) (5-point) or 1/(6*h*h) (9-point), computed in double on the
@@ -373,7 +378,7 @@ void px_mg_release(void);
 /* ---------------------------------------------------------------------- 3D
  * The 3D relaxation.  The paper's Point and Box
  * are dimension-generic (Z^D), λ = h²/(4D);
- * the stencil PX_LAPLACE_7PT_3D has taps W,E,S,N,B,T (offsets −x,+x,−y,+y,
+ * the stencil PX_LAPLACE_7PT_3D (or PX_MEHRSTELLEN_27PT_3D, below) has taps W,E,S,N,B,T (offsets −x,+x,−y,+y,
  * −z,+z; weight 1) and C (−6) in that order, scale = 1/(h·h) (DESIGN.md
  * R-3D1); per cell r = scale·L − rhs, φ' = φ + λ·r, every operation rounded
  * once -- bit-identical to the oracle's orc3_solve.  Single device.
@@ -399,6 +404,13 @@ int64_t px3_norm_buffer_len(void);
 /* Synthetic field on the owned cells: kind 0 zeros, 1 the counter hash
  * u = splitmix64(seed ^ (x + n0·(y + n1·z))), ((u >> 11)·2^-53)·2 − 1. */
 px_status px3_init_field(px_patch3* p, int32_t kind, uint64_t seed, void* stream);
+/* 27-point variant (PX_MEHRSTELLEN_27PT_3D, R-3D4; not in the
+ * paper -- the 3D counterpart of the BASELINE config-5 Mehrstellen stencil):
+ * taps faces W,E,S,N,B,T (14), edges xy, xz, yz (3), corners z-major (1),
+ * centre (−128), scale = 1/(30·h·h); fourth order with the right-hand side
+ * f = ρ + (1/12)·S7(ρ) from px3_mehrstellen_rhs (ρ's ghosts filled; rho and
+ * f distinct patches of one layout). */
+px_status px3_mehrstellen_rhs(const px_patch3* rho, px_patch3* f, void* stream);
 /* Ghost layer by the boundary rule (R-3D2): PERIODIC wrap,
  * DIRICHLET_CC odd reflection, phased x, y, z (edges and corners by the
  * product rule); FIXED_GHOSTS: nothing.  g <= every extent. */

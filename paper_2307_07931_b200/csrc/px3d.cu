@@ -96,9 +96,70 @@ struct Relax3 {
   int32_t policy;         // L2 policies (A/B knob PROTOX_K3_POLICY): 0 ρ evict_first + φ evict_last
 };
 
+// r = scale·L − ρ, φ' = φ + λr for the pair, store, accumulate the norms
+template <int MODE>
+__device__ __forceinline__ void k3_finish(const Relax3& a, const double* tp, int brow, int lane, int cx, int y0,
+                                          int z, bool ox0, bool ox1, double2 C, double L0, double L1,
+                                          unsigned long long& mx, double& ss) {
+  using namespace k3;
+  const double2 f = *reinterpret_cast<const double2*>(tp + PHI_PAD + (brow - 1) * TX + 2 * lane);
+  const double r0 = __dsub_rn(__dmul_rn(a.scale, L0), f.x);
+  const double r1 = __dsub_rn(__dmul_rn(a.scale, L1), f.y);
+  const int y = y0 + brow - 1;
+  const bool oy = y < a.n[1];
+  const bool w0 = ox0 && oy, w1 = ox1 && oy;
+  if (MODE == MODE_RELAX) {
+    const double o0 = __dadd_rn(C.x, __dmul_rn(a.lambda, r0));
+    const double o1 = __dadd_rn(C.y, __dmul_rn(a.lambda, r1));
+    double* dp = a.dst + cx + (int64_t)y * a.ld + (int64_t)z * a.plane;
+    if (w0 && w1)
+      *reinterpret_cast<double2*>(dp) = make_double2(o0, o1);
+    else if (w0)
+      dp[0] = o0;
+  }
+  const double q0 = w0 ? r0 : 0.0, q1 = w1 ? r1 : 0.0;
+  mx = umax64(mx, (unsigned long long)__double_as_longlong(fabs(q0)));
+  ss = fma(q0, q0, ss);
+  mx = umax64(mx, (unsigned long long)__double_as_longlong(fabs(q1)));
+  ss = fma(q1, q1, ss);
+}
+
+// Undivided 27-point Mehrstellen sum (R-3D4) of one cell, v(q, dy, dx) the
+// value at plane z+q-1: the oracle's tap order, every product and sum rounded.
+template <class V>
+__device__ __forceinline__ double m27(const V& v) {
+  double acc = __dmul_rn(14.0, v(1, 0, -1));  // faces W, E, S, N, B, T
+  acc = __dadd_rn(acc, __dmul_rn(14.0, v(1, 0, 1)));
+  acc = __dadd_rn(acc, __dmul_rn(14.0, v(1, -1, 0)));
+  acc = __dadd_rn(acc, __dmul_rn(14.0, v(1, 1, 0)));
+  acc = __dadd_rn(acc, __dmul_rn(14.0, v(0, 0, 0)));
+  acc = __dadd_rn(acc, __dmul_rn(14.0, v(2, 0, 0)));
+  acc = __dadd_rn(acc, __dmul_rn(3.0, v(1, -1, -1)));  // edges xy
+  acc = __dadd_rn(acc, __dmul_rn(3.0, v(1, -1, 1)));
+  acc = __dadd_rn(acc, __dmul_rn(3.0, v(1, 1, -1)));
+  acc = __dadd_rn(acc, __dmul_rn(3.0, v(1, 1, 1)));
+  acc = __dadd_rn(acc, __dmul_rn(3.0, v(0, 0, -1)));  // edges xz
+  acc = __dadd_rn(acc, __dmul_rn(3.0, v(0, 0, 1)));
+  acc = __dadd_rn(acc, __dmul_rn(3.0, v(2, 0, -1)));
+  acc = __dadd_rn(acc, __dmul_rn(3.0, v(2, 0, 1)));
+  acc = __dadd_rn(acc, __dmul_rn(3.0, v(0, -1, 0)));  // edges yz
+  acc = __dadd_rn(acc, __dmul_rn(3.0, v(0, 1, 0)));
+  acc = __dadd_rn(acc, __dmul_rn(3.0, v(2, -1, 0)));
+  acc = __dadd_rn(acc, __dmul_rn(3.0, v(2, 1, 0)));
+  acc = __dadd_rn(acc, v(0, -1, -1));  // corners, z-major
+  acc = __dadd_rn(acc, v(0, -1, 1));
+  acc = __dadd_rn(acc, v(0, 1, -1));
+  acc = __dadd_rn(acc, v(0, 1, 1));
+  acc = __dadd_rn(acc, v(2, -1, -1));
+  acc = __dadd_rn(acc, v(2, -1, 1));
+  acc = __dadd_rn(acc, v(2, 1, -1));
+  acc = __dadd_rn(acc, v(2, 1, 1));
+  return __dadd_rn(acc, __dmul_rn(-128.0, v(1, 0, 0)));
+}
+
 // The map's origin is cell (-2, -g, -g) of the patch, so tensor coordinate
 // (c0, c1, c2) is cell (c0 - 2, c1 - g, c2 - g).
-template <int MODE, int NST>
+template <int MODE, int NST, int ST>
 __global__ void __launch_bounds__(k3::THREADS, NST == 3 ? 2 : 1)
     k3_relax(const __grid_constant__ CUtensorMap mphi, const __grid_constant__ CUtensorMap mrho, const Relax3 a,
              int g) {
@@ -165,16 +226,18 @@ __global__ void __launch_bounds__(k3::THREADS, NST == 3 ? 2 : 1)
       const int cx = x0 + 2 * lane;
       const bool ox0 = cx < a.n[0], ox1 = cx + 1 < a.n[0];
       double2 Bv[RPW];
-      // stage 0: plane z0-1 -> B
+      // stage 0: plane z0-1 -> B (7-point: its pair values in registers, the
+      // stage released at once; 27-point: the whole box is held as the B plane)
       mb_wait(&full[slot], phase);
-      {
+      int bslot = slot;
+      if (ST == 0) {
         const double* sp = smem + (size_t)slot * STAGE;
 #pragma unroll
         for (int i = 0; i < RPW; ++i)
           Bv[i] = *reinterpret_cast<const double2*>(sp + (RPW * warp + i + 1) * BXW + bc);
+        __syncwarp();
+        if (lane == 0) mb_arrive(&empty[slot]);
       }
-      __syncwarp();
-      if (lane == 0) mb_arrive(&empty[slot]);
       if (++slot == NST) {
         slot = 0;
         phase ^= 1u;
@@ -190,57 +253,80 @@ __global__ void __launch_bounds__(k3::THREADS, NST == 3 ? 2 : 1)
         mb_wait(&full[slot], phase);  // plane z+1 and ρ(z)
         const double* cp = smem + (size_t)cslot * STAGE;
         const double* tp = smem + (size_t)slot * STAGE;
-        double2 r[RPW + 2];
+        if (ST == 0) {
+          double2 r[RPW + 2];
 #pragma unroll
-        for (int i = 0; i < RPW + 2; ++i) r[i] = *reinterpret_cast<const double2*>(cp + (RPW * warp + i) * BXW + bc);
+          for (int i = 0; i < RPW + 2; ++i) r[i] = *reinterpret_cast<const double2*>(cp + (RPW * warp + i) * BXW + bc);
 #pragma unroll
-        for (int i = 0; i < RPW; ++i) {
-          const int brow = RPW * warp + i + 1;
-          const double2 C = r[i + 1], S = r[i], N = r[i + 2];
-          const double W = cp[brow * BXW + bc - 1], E = cp[brow * BXW + bc + 2];
-          const double2 T = *reinterpret_cast<const double2*>(tp + brow * BXW + bc);
-          const double2 f = *reinterpret_cast<const double2*>(tp + PHI_PAD + (brow - 1) * TX + 2 * lane);
-          const double2 B = Bv[i];
-          double L0 = __dadd_rn(W, C.y);
-          L0 = __dadd_rn(L0, S.x);
-          L0 = __dadd_rn(L0, N.x);
-          L0 = __dadd_rn(L0, B.x);
-          L0 = __dadd_rn(L0, T.x);
-          L0 = __dadd_rn(L0, __dmul_rn(-6.0, C.x));
-          double L1 = __dadd_rn(C.x, E);
-          L1 = __dadd_rn(L1, S.y);
-          L1 = __dadd_rn(L1, N.y);
-          L1 = __dadd_rn(L1, B.y);
-          L1 = __dadd_rn(L1, T.y);
-          L1 = __dadd_rn(L1, __dmul_rn(-6.0, C.y));
-          const double r0 = __dsub_rn(__dmul_rn(a.scale, L0), f.x);
-          const double r1 = __dsub_rn(__dmul_rn(a.scale, L1), f.y);
-          const int y = y0 + brow - 1;
-          const bool oy = y < a.n[1];
-          const bool w0 = ox0 && oy, w1 = ox1 && oy;
-          if (MODE == MODE_RELAX) {
-            const double o0 = __dadd_rn(C.x, __dmul_rn(a.lambda, r0));
-            const double o1 = __dadd_rn(C.y, __dmul_rn(a.lambda, r1));
-            double* dp = a.dst + cx + (int64_t)y * a.ld + (int64_t)z * a.plane;
-            if (w0 && w1)
-              *reinterpret_cast<double2*>(dp) = make_double2(o0, o1);
-            else if (w0)
-              dp[0] = o0;
+          for (int i = 0; i < RPW; ++i) {
+            const int brow = RPW * warp + i + 1;
+            const double2 C = r[i + 1], S = r[i], N = r[i + 2];
+            const double W = cp[brow * BXW + bc - 1], E = cp[brow * BXW + bc + 2];
+            const double2 T = *reinterpret_cast<const double2*>(tp + brow * BXW + bc);
+            const double2 B = Bv[i];
+            double L0 = __dadd_rn(W, C.y);
+            L0 = __dadd_rn(L0, S.x);
+            L0 = __dadd_rn(L0, N.x);
+            L0 = __dadd_rn(L0, B.x);
+            L0 = __dadd_rn(L0, T.x);
+            L0 = __dadd_rn(L0, __dmul_rn(-6.0, C.x));
+            double L1 = __dadd_rn(C.x, E);
+            L1 = __dadd_rn(L1, S.y);
+            L1 = __dadd_rn(L1, N.y);
+            L1 = __dadd_rn(L1, B.y);
+            L1 = __dadd_rn(L1, T.y);
+            L1 = __dadd_rn(L1, __dmul_rn(-6.0, C.y));
+            k3_finish<MODE>(a, tp, brow, lane, cx, y0, z, ox0, ox1, C, L0, L1, mx, ss);
+            Bv[i] = C;
           }
-          const double q0 = w0 ? r0 : 0.0, q1 = w1 ? r1 : 0.0;
-          mx = umax64(mx, (unsigned long long)__double_as_longlong(fabs(q0)));
-          ss = fma(q0, q0, ss);
-          mx = umax64(mx, (unsigned long long)__double_as_longlong(fabs(q1)));
-          ss = fma(q1, q1, ss);
-          Bv[i] = C;
+        } else {
+          // 27-point: rows 4w .. 4w+5 of the B, C, T plane boxes (pairs and the
+          // W / E neighbours), then the taps in the oracle's order (R-3D4)
+          const double* bp = smem + (size_t)bslot * STAGE;
+          const double* pl[3] = {bp, cp, tp};
+          double2 P[3][RPW + 2];
+          double Wv[3][RPW + 2], Ev[3][RPW + 2];
+#pragma unroll
+          for (int q = 0; q < 3; ++q)
+#pragma unroll
+            for (int i = 0; i < RPW + 2; ++i) {
+              const double* rp = pl[q] + (RPW * warp + i) * BXW + bc;
+              P[q][i] = *reinterpret_cast<const double2*>(rp);
+              Wv[q][i] = rp[-1];
+              Ev[q][i] = rp[2];
+            }
+#pragma unroll
+          for (int i = 0; i < RPW; ++i) {
+            const int brow = RPW * warp + i + 1;
+            // value of (plane q = dz+1, dy, dx) for the pair's cell 0 / cell 1
+            auto v0 = [&](int q, int dy, int dx) {
+              const int k = i + 1 + dy;
+              return dx < 0 ? Wv[q][k] : (dx == 0 ? P[q][k].x : P[q][k].y);
+            };
+            auto v1 = [&](int q, int dy, int dx) {
+              const int k = i + 1 + dy;
+              return dx < 0 ? P[q][k].x : (dx == 0 ? P[q][k].y : Ev[q][k]);
+            };
+            const double L0 = m27(v0), L1 = m27(v1);
+            k3_finish<MODE>(a, tp, brow, lane, cx, y0, z, ox0, ox1, P[1][i + 1], L0, L1, mx, ss);
+          }
+          __syncwarp();
+          if (lane == 0) mb_arrive(&empty[bslot]);  // plane z-1 no longer needed
+          bslot = cslot;
         }
-        __syncwarp();
-        if (lane == 0) mb_arrive(&empty[cslot]);  // plane z no longer needed
+        if (ST == 0) {
+          __syncwarp();
+          if (lane == 0) mb_arrive(&empty[cslot]);  // plane z no longer needed
+        }
         cslot = slot;
         if (++slot == NST) {
           slot = 0;
           phase ^= 1u;
         }
+      }
+      if (ST == 1) {
+        __syncwarp();
+        if (lane == 0) mb_arrive(&empty[bslot]);
       }
       __syncwarp();
       if (lane == 0) mb_arrive(&empty[cslot]);  // the item's last plane
@@ -281,6 +367,26 @@ __global__ void k3_ghost(double* o, int64_t ld, int64_t plane, int n0, int n1, i
     }
     const double v = o[s[0] + (int64_t)s[1] * ld + (int64_t)s[2] * plane];
     o[c[0] + (int64_t)c[1] * ld + (int64_t)c[2] * plane] = sign * v;
+  }
+}
+
+// f = ρ + c12·S7(ρ) over the owned cells (27-point right-hand side, R-3D4);
+// ρ's ghosts must be filled.  S7 in the canonical order W,E,S,N,B,T, −6C.
+__global__ void k3_mrhs(const double* rho, double* f, int64_t ld, int64_t plane, int n0, int n1, int n2,
+                        double c12) {
+  const int64_t total = (int64_t)n0 * n1 * n2;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int x = (int)(i % n0);
+    const int64_t r = i / n0;
+    const int y = (int)(r % n1), z = (int)(r / n1);
+    const double* c = rho + x + (int64_t)y * ld + (int64_t)z * plane;
+    double L = __dadd_rn(c[-1], c[1]);
+    L = __dadd_rn(L, c[-ld]);
+    L = __dadd_rn(L, c[ld]);
+    L = __dadd_rn(L, c[-plane]);
+    L = __dadd_rn(L, c[plane]);
+    L = __dadd_rn(L, __dmul_rn(-6.0, c[0]));
+    f[x + (int64_t)y * ld + (int64_t)z * plane] = __dadd_rn(c[0], __dmul_rn(c12, L));
   }
 }
 
@@ -369,11 +475,11 @@ static int k3_nst() {
   return nst;
 }
 
-static void plan3(const int32_t n[3], Relax3& a, int* grid) {
+static void plan3(const int32_t n[3], Relax3& a, int* grid, int stencil = PX_LAPLACE_7PT_3D) {
   a.ntx = (n[0] + k3::TX - 1) / k3::TX;
   a.nty = (n[1] + k3::TY - 1) / k3::TY;
   const int tiles = a.ntx * a.nty;
-  const int cps = k3_nst() == 3 ? 2 : 1;
+  const int cps = (k3_nst() == 3 && stencil == PX_LAPLACE_7PT_3D) ? 2 : 1;
   const int gmax = cps * k3_nsm() < k3::MAX_GRID ? cps * k3_nsm() : k3::MAX_GRID;
   double best = 1e30;
   int bc = 1;
@@ -394,10 +500,10 @@ static void plan3(const int32_t n[3], Relax3& a, int* grid) {
   *grid = a.nitems < gmax ? a.nitems : gmax;
 }
 
-int32_t relax3_blocks(const int32_t n[3]) {
+int32_t relax3_blocks(const int32_t n[3], int stencil) {
   Relax3 a;
   int grid = 0;
-  plan3(n, a, &grid);
+  plan3(n, a, &grid, stencil);
   return grid;
 }
 
@@ -421,17 +527,17 @@ static px_status same_shape3(const px_patch3& a, const px_patch3& b, const char*
 
 static bool pow2_ok(double h) { return h > 0.0 && std::isfinite(h); }
 
-template <int MODE, int NST>
+template <int MODE, int NST, int ST>
 static cudaError_t k3_go(const CUtensorMap& mphi, const CUtensorMap& mrho, const Relax3& a, int g, int grid,
                          cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k3_relax<MODE, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k3_relax<MODE, NST, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)k3::smem_bytes<NST>());
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  k3_relax<MODE, NST><<<grid, k3::THREADS, k3::smem_bytes<NST>(), s>>>(mphi, mrho, a, g);
+  k3_relax<MODE, NST, ST><<<grid, k3::THREADS, k3::smem_bytes<NST>(), s>>>(mphi, mrho, a, g);
   return cudaSuccess;
 }
 
@@ -444,11 +550,11 @@ static px_status launch_relax3(int mode, const px_relax_params& prm, const px_pa
   std::memset(&a, 0, sizeof a);
   for (int d = 0; d < 3; ++d) a.n[d] = in.n[d];
   int grid = 0;
-  plan3(a.n, a, &grid);
+  plan3(a.n, a, &grid, prm.stencil);
   a.dst = out ? out->data : nullptr;
   a.ld = out ? out->ld : 0;
   a.plane = out ? out->plane : 0;
-  a.scale = 1.0 / (prm.h * prm.h);
+  a.scale = prm.stencil == PX_MEHRSTELLEN_27PT_3D ? 1.0 / (30.0 * prm.h * prm.h) : 1.0 / (prm.h * prm.h);
   a.lambda = prm.lambda;
   a.norms = ns;
   static int policy = -1;
@@ -459,12 +565,15 @@ static px_status launch_relax3(int mode, const px_relax_params& prm, const px_pa
   a.policy = policy;
   const int nst = k3_nst();
   cudaError_t e = cudaSuccess;
-  if (mode == MODE_RELAX) {
-    if (nst == 3) e = k3_go<MODE_RELAX, 3>(mphi, mrho, a, in.ghost, grid, s);
-    else if (nst == 6) e = k3_go<MODE_RELAX, 6>(mphi, mrho, a, in.ghost, grid, s);
-    else e = k3_go<MODE_RELAX, 4>(mphi, mrho, a, in.ghost, grid, s);
+  if (prm.stencil == PX_MEHRSTELLEN_27PT_3D) {  // three planes held: 5 stages
+    e = mode == MODE_RELAX ? k3_go<MODE_RELAX, 5, 1>(mphi, mrho, a, in.ghost, grid, s)
+                           : k3_go<MODE_RESID, 5, 1>(mphi, mrho, a, in.ghost, grid, s);
+  } else if (mode == MODE_RELAX) {
+    if (nst == 3) e = k3_go<MODE_RELAX, 3, 0>(mphi, mrho, a, in.ghost, grid, s);
+    else if (nst == 6) e = k3_go<MODE_RELAX, 6, 0>(mphi, mrho, a, in.ghost, grid, s);
+    else e = k3_go<MODE_RELAX, 4, 0>(mphi, mrho, a, in.ghost, grid, s);
   } else {
-    e = k3_go<MODE_RESID, 4>(mphi, mrho, a, in.ghost, grid, s);
+    e = k3_go<MODE_RESID, 4, 0>(mphi, mrho, a, in.ghost, grid, s);
   }
   if (e != cudaSuccess) return cuda_check(e, "3D relax attribute");
   count_launches(1);
@@ -494,7 +603,8 @@ static px_status launch_ghost3(px_bc bc, const px_patch3& p, cudaStream_t s) {
 
 static px_status check_params3(const px_relax_params* p) {
   if (!p) return fail(PX_ERR_ARG, "null params");
-  if (p->stencil != PX_LAPLACE_7PT_3D) return fail(PX_ERR_UNSUPPORTED, "3D calls take stencil PX_LAPLACE_7PT_3D");
+  if (p->stencil != PX_LAPLACE_7PT_3D && p->stencil != PX_MEHRSTELLEN_27PT_3D)
+    return fail(PX_ERR_UNSUPPORTED, "3D calls take stencil PX_LAPLACE_7PT_3D or PX_MEHRSTELLEN_27PT_3D");
   if (!pow2_ok(p->h)) return fail(PX_ERR_ARG, "h must be positive and finite");
   return PX_OK;
 }
@@ -551,7 +661,7 @@ static bool same_key(const Plan3& p, px_bc bc, const px_relax_params& prm, const
 
 static px_status enqueue_solve3(Plan3& P) {
   const int N = P.opts.nsweeps, E = P.opts.norm_every;
-  const int32_t blocks = relax3_blocks(P.a.n);
+  const int32_t blocks = relax3_blocks(P.a.n, P.prm.stencil);
   const px_patch3* cur = &P.a;
   const px_patch3* nxt = &P.b;
   int entry = 0;
@@ -610,6 +720,19 @@ px_status px3_init_field(px_patch3* p, int32_t kind, uint64_t seed, void* stream
   return cuda_check(cudaGetLastError(), "3D init launch");
 }
 
+px_status px3_mehrstellen_rhs(const px_patch3* rho, px_patch3* f, void* stream) {
+  clear_error();
+  PX_TRY(check3(rho, "rho"));
+  PX_TRY(check3(f, "f"));
+  PX_TRY(same_shape3(*rho, *f, "f"));
+  if (rho->ld != f->ld || rho->plane != f->plane) return fail(PX_ERR_SHAPE, "rho and f must share ld and plane");
+  if (rho->data == f->data) return fail(PX_ERR_ARG, "rho and f must differ");
+  k3_mrhs<<<2048, 256, 0, (cudaStream_t)stream>>>(rho->data, f->data, rho->ld, rho->plane, rho->n[0], rho->n[1],
+                                                  rho->n[2], 1.0 / 12.0);
+  count_launches(1);
+  return cuda_check(cudaGetLastError(), "3D Mehrstellen rhs launch");
+}
+
 px_status px3_fill_ghosts(px_bc bc, px_patch3* p, void* stream) {
   clear_error();
   PX_TRY(check3(p, "phi"));
@@ -628,7 +751,7 @@ px_status px3_relax_step(const px_relax_params* p, const px_patch3* phi_in, px_p
   PX_TRY(same_shape3(*phi_in, *phi_out, "phi_out"));
   PX_TRY(same_shape3(*phi_in, *rhs, "rhs"));
   if (phi_in->data == phi_out->data) return fail(PX_ERR_ARG, "phi_in and phi_out must not overlap");
-  return launch_relax3(MODE_RELAX, *p, *phi_in, phi_out, *rhs, slot_from(d_norms, relax3_blocks(phi_in->n)),
+  return launch_relax3(MODE_RELAX, *p, *phi_in, phi_out, *rhs, slot_from(d_norms, relax3_blocks(phi_in->n, p->stencil)),
                        (cudaStream_t)stream);
 }
 
@@ -640,7 +763,7 @@ px_status px3_residual_norm(const px_relax_params* p, const px_patch3* phi, cons
   PX_TRY(check3(rhs, "rhs"));
   PX_TRY(same_shape3(*phi, *rhs, "rhs"));
   if (!d_norms) return fail(PX_ERR_ARG, "d_norms is required");
-  return launch_relax3(MODE_RESID, *p, *phi, nullptr, *rhs, slot_from(d_norms, relax3_blocks(phi->n)),
+  return launch_relax3(MODE_RESID, *p, *phi, nullptr, *rhs, slot_from(d_norms, relax3_blocks(phi->n, p->stencil)),
                        (cudaStream_t)stream);
 }
 

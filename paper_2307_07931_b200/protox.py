@@ -22,7 +22,7 @@ PX_OK, PX_ERR_ARG, PX_ERR_SHAPE, PX_ERR_DOMAIN, PX_ERR_ALIGN = 0, 1, 2, 3, 4
 PX_ERR_UNSUPPORTED, PX_ERR_CUDA, PX_ERR_NCCL, PX_ERR_STATE = 5, 6, 7, 8
 PX_BC_PERIODIC, PX_BC_DIRICHLET_CC, PX_BC_FIXED_GHOSTS = 0, 1, 2
 PX_PART_SLABS = 0
-PX_LAPLACE_5PT, PX_MEHRSTELLEN_9PT, PX_LAPLACE_7PT_3D = 0, 1, 2
+PX_LAPLACE_5PT, PX_MEHRSTELLEN_9PT, PX_LAPLACE_7PT_3D, PX_MEHRSTELLEN_27PT_3D = 0, 1, 2, 3
 PX_FIELD_ZERO, PX_FIELD_HASH, PX_FIELD_SINE = 0, 1, 2
 
 
@@ -101,7 +101,7 @@ EXPORTS = [
     "px_solve", "px_solve_host", "px_solve_host_batch", "px_release_cached", "px_mg_solve", "px_mg_release", "px_kernel_launch_count",
     "px_relax_variant", "px_stream_ceiling",
     "px3_layout", "px3_norm_buffer_len", "px3_init_field", "px3_fill_ghosts", "px3_relax_step",
-    "px3_residual_norm", "px3_solve", "px3_release",
+    "px3_residual_norm", "px3_solve", "px3_release", "px3_mehrstellen_rhs",
 ]
 
 
@@ -205,6 +205,8 @@ def lib():
     L.px3_solve.argtypes = [st, P(px_relax_params), P(px_solve_opts), P(px_patch3), P(px_patch3), P(px_patch3),
                             P(ctypes.c_double), i32, P(i32), P(i32), vp]
     L.px3_release.restype = None
+    L.px3_mehrstellen_rhs.restype = st
+    L.px3_mehrstellen_rhs.argtypes = [P(px_patch3), P(px_patch3), vp]
     L.px_relax_variant.restype = i32
     L.px_relax_variant.argtypes = [P(px_patch), P(px_patch), P(px_patch), px_box]
     _lib = L
@@ -607,6 +609,12 @@ def solve3(grid: Grid3, bc: int, p: px_relax_params, nsweeps: int, norm_every: i
                            norms.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), max(cap, 1), ctypes.byref(nw),
                            ctypes.byref(ins) if keep_in_scratch else None, _stream(stream)))
     return SolveResult(norms[: nw.value].copy(), bool(ins.value))
+
+
+def mehrstellen_rhs3(grid: Grid3, rho, f, stream=None):
+    """px3_mehrstellen_rhs: f = ρ + S7(ρ)/12 (ρ's ghosts filled)."""
+    a, b = grid.patch(rho), grid.patch(f)
+    _check(lib().px3_mehrstellen_rhs(ctypes.byref(a), ctypes.byref(b), _stream(stream)))
 
 
 def release3():

@@ -214,3 +214,49 @@ def test_full_size_512_sampled_windows():
         got = float(vw[z, y, x].item())
         want = ref[w + 1, w + 1, w + 1]
         assert np.float64(got).view(np.uint64) == np.float64(want).view(np.uint64), ((x, y, z), got, want)
+
+
+# ------------------------------------------------------- 27-point Mehrstellen (R-3D4)
+@pytest.mark.parametrize("bc", BCS)
+@pytest.mark.parametrize("n", [(64, 32, 5), (70, 37, 9), (3, 2, 2)])
+def test_solve3_mehrstellen27_bitwise(bc, n):
+    h = 1.0 / max(n)
+    lam = h * h / 12
+    phi0, rho = _fields(n, 1, 100 + sum(n) + bc)
+    grid = P.Grid3(n, 1)
+    a, b, r = _upload(grid, phi0), grid.alloc(), _upload(grid, rho)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    res = P.solve3(grid, bc, P.relax_params(h, lam, P.PX_MEHRSTELLEN_27PT_3D), 5, 2, a, b, r, use_graph=True,
+                   stream=s)
+    out = grid.view(b if res.in_scratch else a).cpu().numpy()
+    p = oracle.Problem3(n, h, lam, bc=BC_MAP[bc], nsweeps=5, norm_every=2, stencil=1)
+    ref, rn = oracle.solve3(p, phi0, rho)
+    assert bits_equal(out, ref[1:-1, 1:-1, 1:-1]), ulp_diff(out, ref[1:-1, 1:-1, 1:-1])
+    _check_norms(res.norms, rn)
+
+
+@pytest.mark.parametrize("bc", [P.PX_BC_PERIODIC, P.PX_BC_DIRICHLET_CC])
+def test_mehrstellen27_corrected_rhs_and_solve(bc):
+    """px3_mehrstellen_rhs (ρ ghosts by the BC rule) then the 27-point solve ==
+    the oracle with rhs_correction, bit for bit; several z chunks."""
+    n = (66, 40, 70)
+    h = 1.0 / 70
+    lam = h * h / 12
+    phi0, rho = _fields(n, 1, 55 + bc)
+    grid = P.Grid3(n, 1)
+    a, b, r = _upload(grid, phi0), grid.alloc(), _upload(grid, rho)
+    f = grid.alloc()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    P.fill_ghosts3(grid, bc, r, stream=s)
+    P.mehrstellen_rhs3(grid, r, f, stream=s)
+    s.synchronize()
+    p = oracle.Problem3(n, h, lam, bc=BC_MAP[bc], nsweeps=6, norm_every=1, stencil=1, rhs_correction=True)
+    assert bits_equal(grid.view(f).cpu().numpy(), oracle.rhs3(p, rho))
+    res = P.solve3(grid, bc, P.relax_params(h, lam, P.PX_MEHRSTELLEN_27PT_3D), 6, 1, a, b, f, use_graph=False,
+                   stream=s)
+    out = grid.view(b if res.in_scratch else a).cpu().numpy()
+    ref, rn = oracle.solve3(p, phi0, rho)
+    assert bits_equal(out, ref[1:-1, 1:-1, 1:-1]), ulp_diff(out, ref[1:-1, 1:-1, 1:-1])
+    _check_norms(res.norms, rn)
