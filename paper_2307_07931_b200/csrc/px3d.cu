@@ -45,7 +45,6 @@ constexpr int BXW = TX + 4, BYH = TY + 2;   // φ box: columns x0-2 .. x0+TX+1, 
 constexpr int NWC = 8;                      // consumer warps, warp w: tile rows 4w .. 4w+3
 constexpr int RPW = TY / NWC;               // rows per warp (4)
 constexpr int THREADS = NWC * 32 + 32;
-constexpr int NST_MAX = 6;  // ring stages: template parameter, default 4 (PROTOX_K3_NST A/B)
 constexpr int PHI_PAD = (BXW * BYH + 15) / 16 * 16;  // 128-byte aligned ρ tile
 constexpr int STAGE = PHI_PAD + TX * TY;             // doubles
 constexpr uint32_t PHI_BYTES = BXW * BYH * 8u;
@@ -160,7 +159,7 @@ __device__ __forceinline__ double m27(const V& v) {
 // The map's origin is cell (-2, -g, -g) of the patch, so tensor coordinate
 // (c0, c1, c2) is cell (c0 - 2, c1 - g, c2 - g).
 template <int MODE, int NST, int ST>
-__global__ void __launch_bounds__(k3::THREADS, NST == 3 ? 2 : 1)
+__global__ void __maxnreg__(ST == 1 ? 168 : 112)  // 9 warps: 3 share a sub-partition (16K regs)
     k3_relax(const __grid_constant__ CUtensorMap mphi, const __grid_constant__ CUtensorMap mrho, const Relax3 a,
              int g) {
   using namespace k3;
@@ -283,32 +282,35 @@ __global__ void __launch_bounds__(k3::THREADS, NST == 3 ? 2 : 1)
           // 27-point: rows 4w .. 4w+5 of the B, C, T plane boxes (pairs and the
           // W / E neighbours), then the taps in the oracle's order (R-3D4)
           const double* bp = smem + (size_t)bslot * STAGE;
-          const double* pl[3] = {bp, cp, tp};
-          double2 P[3][RPW + 2];
-          double Wv[3][RPW + 2], Ev[3][RPW + 2];
+          // rolling window of three rows per plane (slot = row mod 3)
+          double2 P[3][3];
+          double Wv[3][3], Ev[3][3];
+          auto load_row = [&](int k) {
 #pragma unroll
-          for (int q = 0; q < 3; ++q)
-#pragma unroll
-            for (int i = 0; i < RPW + 2; ++i) {
-              const double* rp = pl[q] + (RPW * warp + i) * BXW + bc;
-              P[q][i] = *reinterpret_cast<const double2*>(rp);
-              Wv[q][i] = rp[-1];
-              Ev[q][i] = rp[2];
+            for (int q = 0; q < 3; ++q) {
+              const double* rp = (q == 0 ? bp : (q == 1 ? cp : tp)) + (RPW * warp + k) * BXW + bc;
+              P[q][k % 3] = *reinterpret_cast<const double2*>(rp);
+              Wv[q][k % 3] = rp[-1];
+              Ev[q][k % 3] = rp[2];
             }
+          };
+          load_row(0);
+          load_row(1);
 #pragma unroll
           for (int i = 0; i < RPW; ++i) {
+            load_row(i + 2);
             const int brow = RPW * warp + i + 1;
             // value of (plane q = dz+1, dy, dx) for the pair's cell 0 / cell 1
             auto v0 = [&](int q, int dy, int dx) {
-              const int k = i + 1 + dy;
+              const int k = (i + 1 + dy) % 3;
               return dx < 0 ? Wv[q][k] : (dx == 0 ? P[q][k].x : P[q][k].y);
             };
             auto v1 = [&](int q, int dy, int dx) {
-              const int k = i + 1 + dy;
+              const int k = (i + 1 + dy) % 3;
               return dx < 0 ? P[q][k].x : (dx == 0 ? P[q][k].y : Ev[q][k]);
             };
             const double L0 = m27(v0), L1 = m27(v1);
-            k3_finish<MODE>(a, tp, brow, lane, cx, y0, z, ox0, ox1, P[1][i + 1], L0, L1, mx, ss);
+            k3_finish<MODE>(a, tp, brow, lane, cx, y0, z, ox0, ox1, P[1][(i + 1) % 3], L0, L1, mx, ss);
           }
           __syncwarp();
           if (lane == 0) mb_arrive(&empty[bslot]);  // plane z-1 no longer needed
