@@ -54,6 +54,21 @@ def solve(n0, n1, nranks=1, g=1, st=0, bc=P.PX_BC_PERIODIC, N=5, E=2, tk=1, grap
             [lay.patch(r, p[2]) for r, p in enumerate(parts)], temporal_k=tk, use_graph=graph, stream=s)
 
 
+def solve3(n, st=P.PX_LAPLACE_7PT_3D, bc=P.PX_BC_PERIODIC, N=3, E=1):
+    g = P.Grid3(n, 1)
+    a, b, r = g.alloc(), g.alloc(), g.alloc()
+    P.init_field3(g, r, 1, 1)
+    P.init_field3(g, a, 1, 2)
+    if st == P.PX_MEHRSTELLEN_27PT_3D:
+        P.fill_ghosts3(g, bc, r)
+        f = g.alloc()
+        P.mehrstellen_rhs3(g, r, f)
+        r = f
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    P.solve3(g, bc, P.relax_params(1.0 / n[0], (1.0 / n[0]) ** 2 / 12, st), N, E, a, b, r, stream=s)
+
+
 def other():
     lay = P.Layout(P.box(0, 0, 199, 99), (200, 100), 1, P.PX_BC_DIRICHLET_CC, 1)
     a, b, r = fields(lay)
@@ -80,6 +95,10 @@ if __name__ == "__main__":
         "local_multipart_solve": lambda: solve(256, 150, nranks=3, bc=P.PX_BC_FIXED_GHOSTS),
         "tb_solve": lambda: solve(1000, 300, nranks=3, g=4, tk=4, N=9, E=3),
         "graph_solve": lambda: solve(600, 90, N=4, E=1, graph=True),
+        "tb_dirichlet9_solve": lambda: solve(1000, 300, g=4, tk=4, N=8, E=4, st=1, bc=P.PX_BC_DIRICHLET_CC),
+        "tb_fixed_k2_solve": lambda: solve(500, 120, g=2, tk=2, N=4, E=1, bc=P.PX_BC_FIXED_GHOSTS),
+        "relax3_solve": lambda: solve3((70, 37, 13)),
+        "relax3_27_solve": lambda: solve3((66, 34, 9), st=P.PX_MEHRSTELLEN_27PT_3D, bc=P.PX_BC_DIRICHLET_CC),
         "other_kernels": other,
     }
     for name, fn in cases.items():
