@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "px_device.cuh"
 #include "px_internal.h"
@@ -257,8 +258,233 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resident(const ResidentLaunch
     for (int x = tid - 1; x <= nx; x += nt) p.phi_out[(int64_t)p.ny * p.ld_out + x] = A[(size_t)(R + 1) * P + x + 2];
 }
 
+// ---------------------------------------------------------------------------
+// k_resident_tb<ST, K>: the same resident solve with TEMPORAL BLOCKING of the
+// row exchange -- K sweeps per neighbour handshake.  CTA c keeps its rows and
+// K halo rows on each neighbour side (shared rows i = 0 .. R+2K-1, owned
+// i = K .. K+R-1, global row y0-K+i).  A round of K levels computes, at level
+// t, the rows whose inputs are still valid: on a side exchanged with a
+// neighbour the valid range shrinks by one row per level (redundant halo
+// compute -- the halo rows are advanced exactly like the neighbour advances
+// its own rows, so the owned results are bit-identical); on a reflecting or
+// fixed domain face the owned rows are computed at every level and the
+// first ghost row is re-derived (reflection) or kept (fixed).  Then the CTA
+// publishes its first and last K owned rows and copies its neighbours' into
+// its halo: one handshake per K sweeps instead of one per sweep.  The
+// right-hand side is read from global memory (L2-resident) so that the two
+// copies of the taller row block fit in shared memory.
+constexpr int RT_MAXROWS = 16;  // rows a thread walks per level (ρ prefetched into registers)
+template <int ST, bool WRITE>
+__device__ __forceinline__ void rt_rows(const double* A, double* B, const double* rhs, int64_t ld_rhs, int P, int nx,
+                                        int rlo, int rhi, int y_of_i0, int ny, bool wrap, double scale,
+                                        double lambda, bool norm, int nlo, int nhi, unsigned long long& mx,
+                                        double& ss) {
+  for (int q = threadIdx.x; q < nx / 2; q += blockDim.x) {
+    const int x = 2 * q + 2;
+    // the right-hand side of the whole column walk first: one L2 round trip
+    // per level instead of one per row
+    double2 fr[RT_MAXROWS];
+#pragma unroll
+    for (int j = 0; j < RT_MAXROWS; ++j) {
+      const int r = rlo + j;
+      if (r <= rhi) {
+        int y = y_of_i0 + r;
+        if (wrap) y = y < 0 ? y + ny : (y >= ny ? y - ny : y);
+        fr[j] = __ldg(reinterpret_cast<const double2*>(rhs + (int64_t)y * ld_rhs + (x - 2)));
+      }
+    }
+    const double* a0 = A + (size_t)(rlo - 1) * P + x;
+    double2 S = *reinterpret_cast<const double2*>(a0);
+    double2 C = *reinterpret_cast<const double2*>(a0 + P);
+    double sw = a0[-1], se = a0[2], cw = a0[P - 1], ce = a0[P + 2];
+#pragma unroll
+    for (int j = 0; j < RT_MAXROWS; ++j) {
+      const int r = rlo + j;
+      if (r > rhi) break;
+      const double* an = A + (size_t)(r + 1) * P + x;
+      const double2 N = *reinterpret_cast<const double2*>(an);
+      const double nw = an[-1], ne = an[2];
+      const double L0 = rs_taps<ST>(cw, C.y, S.x, N.x, C.x, sw, S.y, nw, N.y);
+      const double L1 = rs_taps<ST>(C.x, ce, S.y, N.y, C.y, S.x, se, N.x, ne);
+      const double2 f = fr[j];
+      const double r0 = __dsub_rn(__dmul_rn(scale, L0), f.x);
+      const double r1 = __dsub_rn(__dmul_rn(scale, L1), f.y);
+      if (WRITE) {
+        double2 o;
+        o.x = __dadd_rn(C.x, __dmul_rn(lambda, r0));
+        o.y = __dadd_rn(C.y, __dmul_rn(lambda, r1));
+        *reinterpret_cast<double2*>(B + (size_t)r * P + x) = o;
+      }
+      if (norm && r >= nlo && r <= nhi) {
+        mx = umax64(mx, (unsigned long long)__double_as_longlong(fabs(r0)));
+        ss = fma(r0, r0, ss);
+        mx = umax64(mx, (unsigned long long)__double_as_longlong(fabs(r1)));
+        ss = fma(r1, r1, ss);
+      }
+      S = C;
+      sw = cw;
+      se = ce;
+      C = N;
+      cw = nw;
+      ce = ne;
+    }
+  }
+}
+
+template <int ST, int K>
+__global__ void __launch_bounds__(RS_THREADS, 1) k_resident_tb(const ResidentLaunch p) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double sm[];
+  const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  const int nx = p.nx, ny = p.ny, P = nx + 4;
+  const int y0 = (int)((int64_t)c * ny / G), y1 = (int)((int64_t)(c + 1) * ny / G), R = y1 - y0;
+  const int NR = R + 2 * K;  // shared rows
+  double* A = sm;
+  double* B = A + (size_t)(p.rmax + 2 * K) * P;
+  unsigned long long* flags = reinterpret_cast<unsigned long long*>(p.ws);
+  double* pub = p.ws + G;                                // [slot][cta][first, last][K][nx]
+  double* part = pub + (size_t)2 * G * 2 * K * nx;       // [entry][cta][max, sum]
+  const int up = c > 0 ? c - 1 : G - 1, dn = c < G - 1 ? c + 1 : 0;
+  const bool wrap = p.ymode[0] == GH_WRAP;
+  const bool top_x = c > 0 || wrap;       // halo rows 0..K-1 from CTA `up`
+  const bool bot_x = c < G - 1 || wrap;   // halo rows R+K..R+2K-1 from CTA `dn`
+  const int xm[2] = {p.xmode[0], p.xmode[1]};
+  const int yb = y0 - K;                  // global row of shared row 0
+
+  // φ^0: owned rows, the neighbour halos (global rows, wrapped on the
+  // periodic ring) and the first ghost row at a domain face, into both copies
+  for (int i = 0; i < NR; ++i) {
+    int y = yb + i;
+    const bool own = i >= K && i < K + R;
+    bool load = own || (i < K && top_x) || (i >= K + R && bot_x) || (i == K - 1 && !top_x) || (i == K + R && !bot_x);
+    if (!load) continue;
+    if (wrap) y = y < 0 ? y + ny : (y >= ny ? y - ny : y);
+    const double* src = p.phi_in + (int64_t)y * p.ld_in;
+    for (int x = tid - 1; x <= nx; x += nt) {
+      const double v = src[x];
+      A[(size_t)i * P + x + 2] = v;
+      B[(size_t)i * P + x + 2] = v;
+    }
+  }
+  if (tid == 0) flags[c] = 0ull;
+  __threadfence();
+  grid.sync();
+
+  int entry = 0, s = 0, round = 0;
+  while (s < p.nsweeps) {
+    const int kk = p.nsweeps - s < K ? p.nsweeps - s : K;  // levels of this round
+    for (int t = 1; t <= kk; ++t) {
+      // valid range at level t (shrinks on exchanged sides only)
+      const int lo = top_x ? t : K, hi = bot_x ? NR - 1 - t : K + R - 1;
+      const bool rec = p.every > 0 && (s % p.every) == 0;
+      unsigned long long mx = 0ull;
+      double ss = 0.0;
+      rt_rows<ST, true>(A, B, p.rhs, p.ld_rhs, P, nx, lo, hi, yb, ny, wrap, p.scale, p.lambda, rec, K, K + R - 1,
+                        mx, ss);
+      __syncthreads();
+      // domain faces: the first ghost row by reflection (fixed: kept)
+      for (int x = tid; x < nx; x += nt) {
+        if (!top_x && p.ymode[0] == GH_REFLECT) B[(size_t)(K - 1) * P + x + 2] = -B[(size_t)K * P + x + 2];
+        if (!bot_x && p.ymode[1] == GH_REFLECT) B[(size_t)(K + R) * P + x + 2] = -B[(size_t)(K + R - 1) * P + x + 2];
+      }
+      __syncthreads();
+      const int glo = top_x ? lo : K - 1, ghi = bot_x ? hi : K + R;
+      for (int r = glo + tid; r <= ghi; r += nt) rs_xghost(B + (size_t)r * P, nx, xm);
+      if (rec) {
+        rs_block_reduce(mx, ss, part + ((size_t)entry * G + c) * 2);
+        ++entry;
+      } else {
+        __syncthreads();
+      }
+      double* tmp = A;
+      A = B;
+      B = tmp;
+      ++s;
+    }
+    // handshake: publish the first and last K owned rows, take the neighbours'
+    const int slot = (round + 1) & 1;
+    double* mine = pub + (size_t)(slot * G + c) * 2 * K * nx;
+    for (int j = 0; j < K; ++j)
+      for (int x = tid; x < nx; x += nt) {
+        __stcg(mine + (size_t)j * nx + x, A[(size_t)(K + j) * P + x + 2]);
+        __stcg(mine + (size_t)(K + j) * nx + x, A[(size_t)(R + j) * P + x + 2]);
+      }
+    __syncthreads();
+    ++round;
+    if (tid == 0) st_release(flags + c, (unsigned long long)round);
+    if (tid == 0 && top_x)
+      while (ld_acquire(flags + up) < (unsigned long long)round) {
+      }
+    if (tid == 32 && bot_x)
+      while (ld_acquire(flags + dn) < (unsigned long long)round) {
+      }
+    __syncthreads();
+    const double* fu = pub + ((size_t)(slot * G + up) * 2 + 1) * K * nx;  // up's last K rows
+    const double* fd = pub + ((size_t)(slot * G + dn) * 2) * K * nx;      // dn's first K rows
+    for (int j = 0; j < K; ++j)
+      for (int x = tid; x < nx; x += nt) {
+        if (top_x) A[(size_t)j * P + x + 2] = __ldcg(fu + (size_t)j * nx + x);
+        if (bot_x) A[(size_t)(K + R + j) * P + x + 2] = __ldcg(fd + (size_t)j * nx + x);
+      }
+    __syncthreads();
+    for (int r = tid; r < NR; r += nt)
+      if ((r < K && top_x) || (r >= K + R && bot_x)) rs_xghost(A + (size_t)r * P, nx, xm);
+    __syncthreads();
+  }
+  if (p.final_norm) {
+    unsigned long long mx = 0ull;
+    double ss = 0.0;
+    rt_rows<ST, false>(A, nullptr, p.rhs, p.ld_rhs, P, nx, K, K + R - 1, yb, ny, wrap, p.scale, p.lambda, true, K,
+                       K + R - 1, mx, ss);
+    rs_block_reduce(mx, ss, part + ((size_t)entry * G + c) * 2);
+    ++entry;
+  }
+  __threadfence();
+  grid.sync();
+  for (int e = c; e < entry; e += G) {
+    unsigned long long m = 0ull;
+    double t = 0.0;
+    for (int i = tid; i < G; i += nt) {
+      m = umax64(m, (unsigned long long)__double_as_longlong(__ldcg(part + ((size_t)e * G + i) * 2)));
+      t = t + __ldcg(part + ((size_t)e * G + i) * 2 + 1);
+    }
+    double out[2];
+    rs_block_reduce(m, t, out);
+    if (tid == 0) {
+      p.d_max[e] = out[0];
+      p.d_sum[e] = out[1];
+    }
+  }
+  for (int i = K; i < K + R; ++i) {
+    double* dst = p.phi_out + (int64_t)(yb + i) * p.ld_out;
+    for (int x = tid - 1; x <= nx; x += nt) dst[x] = A[(size_t)i * P + x + 2];
+  }
+  if (c == 0)
+    for (int x = tid - 1; x <= nx; x += nt) p.phi_out[-p.ld_out + x] = A[(size_t)(K - 1) * P + x + 2];
+  if (c == G - 1)
+    for (int x = tid - 1; x <= nx; x += nt) p.phi_out[(int64_t)ny * p.ld_out + x] = A[(size_t)(K + R) * P + x + 2];
+}
+
+// rounds of the temporally blocked resident solve: K sweeps per handshake
+// (PROTOX_RESIDENT_K = 1, 2 or 3), limited by shared memory and by the rows a
+// CTA owns.  Default 1: measured at BASELINE config 2 (1024², 1000 sweeps)
+// K = 1 / 2 / 3 run at 252 / 207 / 218 Gcell-updates/s -- the per-level
+// barriers and the redundant halo rows cost more than the saved handshakes
+// (DESIGN.md §6), so the blocked variant is an A/B option only.
+constexpr int RS_KMAX = 3;
+static int rs_k_env() {
+  static int k = -1;
+  if (k < 0) {
+    const char* e = getenv("PROTOX_RESIDENT_K");
+    k = e ? atoi(e) : 1;
+    if (k < 1) k = 1;
+    if (k > RS_KMAX) k = RS_KMAX;
+  }
+  return k;
+}
+
 size_t resident_ws_doubles(int nx, int grid, int n_entries) {
-  return (size_t)grid + (size_t)2 * grid * 2 * nx + (size_t)(n_entries > 0 ? n_entries : 1) * grid * 2;
+  return (size_t)grid + (size_t)2 * grid * 2 * RS_KMAX * nx + (size_t)(n_entries > 0 ? n_entries : 1) * grid * 2;
 }
 
 static int rs_nsm(int* smem_optin) {
@@ -275,30 +501,62 @@ static int rs_nsm(int* smem_optin) {
   return n;
 }
 
-bool resident_plan(int nx, int ny, int* grid, int* rmax, size_t* smem) {
-  if (nx < 2 || ny < 1 || (nx & 1)) return false;
+// K of the resident solve of an nx x ny problem (0: does not fit)
+static int resident_k(int nx, int ny, int* grid, int* rmax, size_t* smem) {
+  if (nx < 2 || ny < 1 || (nx & 1)) return 0;
   int optin = 0;
   const int nsm = rs_nsm(&optin);
   const int G = ny < nsm ? ny : nsm;
   const int R = (ny + G - 1) / G;
-  const size_t bytes = ((size_t)2 * (R + 2) * (nx + 4) + (size_t)R * nx) * sizeof(double);
-  // leave room for the static shared arrays of the reduction
-  if (bytes + 1024 > (size_t)optin) return false;
-  *grid = G;
-  *rmax = R;
-  *smem = bytes;
-  return true;
+  const int Rmin = ny / G;  // the smallest block: it publishes K owned rows
+  for (int K = rs_k_env(); K >= 1; --K) {
+    if (K > 1 && R + 2 * K - 2 > RT_MAXROWS) continue;  // rows per level walk
+    size_t bytes;
+    if (K == 1)
+      bytes = ((size_t)2 * (R + 2) * (nx + 4) + (size_t)R * nx) * sizeof(double);
+    else
+      bytes = (size_t)2 * (R + 2 * K) * (nx + 4) * sizeof(double);
+    // leave room for the static shared arrays of the reduction
+    if (bytes + 1024 > (size_t)optin || (K > 1 && Rmin < K)) continue;
+    *grid = G;
+    *rmax = R;
+    *smem = bytes;
+    return K;
+  }
+  return 0;
+}
+
+bool resident_plan(int nx, int ny, int* grid, int* rmax, size_t* smem) {
+  return resident_k(nx, ny, grid, rmax, smem) > 0;
+}
+
+template <typename F>
+static cudaError_t rs_attr(F* fn, size_t smem, size_t& set) {
+  if (set >= smem) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) set = smem;
+  return e;
 }
 
 px_status launch_resident(int stencil, const ResidentLaunch& r, int grid, size_t smem, cudaStream_t s) {
-  static size_t attr_set[2] = {0, 0};
+  int g2 = 0, rm = 0;
+  size_t sm2 = 0;
+  const int K = resident_k(r.nx, r.ny, &g2, &rm, &sm2);
+  if (K < 1 || g2 != grid || sm2 != smem) return fail(PX_ERR_STATE, "resident plan changed");
+  static size_t attr_set[2][RS_KMAX] = {};
   const int k = stencil ? 1 : 0;
-  if (attr_set[k] < smem) {
-    cudaError_t e = k ? cudaFuncSetAttribute(k_resident<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
-                      : cudaFuncSetAttribute(k_resident<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return cuda_check(e, "resident kernel smem attribute");
-    attr_set[k] = smem;
+  void* fn = nullptr;
+  cudaError_t e = cudaSuccess;
+  switch (k * 4 + K) {
+    case 1: e = rs_attr(k_resident<0>, smem, attr_set[0][0]); fn = (void*)k_resident<0>; break;
+    case 2: e = rs_attr(k_resident_tb<0, 2>, smem, attr_set[0][1]); fn = (void*)k_resident_tb<0, 2>; break;
+    case 3: e = rs_attr(k_resident_tb<0, 3>, smem, attr_set[0][2]); fn = (void*)k_resident_tb<0, 3>; break;
+    case 5: e = rs_attr(k_resident<1>, smem, attr_set[1][0]); fn = (void*)k_resident<1>; break;
+    case 6: e = rs_attr(k_resident_tb<1, 2>, smem, attr_set[1][1]); fn = (void*)k_resident_tb<1, 2>; break;
+    case 7: e = rs_attr(k_resident_tb<1, 3>, smem, attr_set[1][2]); fn = (void*)k_resident_tb<1, 3>; break;
+    default: return fail(PX_ERR_STATE, "bad resident configuration");
   }
+  if (e != cudaSuccess) return cuda_check(e, "resident kernel smem attribute");
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(RS_THREADS);
@@ -309,7 +567,8 @@ px_status launch_resident(int stencil, const ResidentLaunch& r, int grid, size_t
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = k ? cudaLaunchKernelEx(&cfg, k_resident<1>, r) : cudaLaunchKernelEx(&cfg, k_resident<0>, r);
+  void* args[] = {const_cast<ResidentLaunch*>(&r)};
+  e = cudaLaunchKernelExC(&cfg, fn, args);
   if (e == cudaSuccess) e = cudaGetLastError();
   count_launches(1);
   return cuda_check(e, "resident solve kernel launch");

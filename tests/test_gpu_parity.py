@@ -698,3 +698,20 @@ def test_temporal_blocking_narrow_kernel_subprocess():
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-m", "gpu", *ids],
                        cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.gpu
+def test_resident_temporal_blocking_variant_subprocess():
+    """The temporally blocked resident solve (A/B option PROTOX_RESIDENT_K=2,3,
+    read once per process) stays bit-identical: the resident-path tests re-run
+    in child processes."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for k in ("2", "3"):
+        env = dict(os.environ, PROTOX_RESIDENT_K=k)
+        r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-m", "gpu",
+                            "tests/test_gpu_parity.py", "-k", "resident_shapes or config2_full"],
+                           cwd=root, env=env, capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, (k, r.stdout[-3000:] + r.stderr[-2000:])
