@@ -94,6 +94,40 @@ def load_traffic(config):
         return None
 
 
+def k12_ceiling(P, torch, dev, elems: int, stream) -> float:
+    """K12: the box's own 2-read/1-write fp64 streaming ceiling
+    (c = a + b over arrays of the sweep's size, px_stream_ceiling), GB/s,
+    CUDA events on the launching stream, median of 7 after 2 warm-ups."""
+    a = torch.empty(elems, dtype=torch.float64, device=dev).fill_(1.0)
+    b = torch.empty_like(a).fill_(2.0)
+    c = torch.empty_like(a)
+    stream.wait_stream(torch.cuda.current_stream(dev))
+    ms = []
+    for i in range(9):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        P.stream_ceiling(a, b, c, 0, stream=stream)
+        e1.record(stream)
+        stream.synchronize()
+        if i >= 2:
+            ms.append(e0.elapsed_time(e1))
+    del a, b, c
+    return 24 * elems / (statistics.median(ms) * 1e-3) / 1e9
+
+
+def roofline_extras(roof: dict, cells_per_launch: int, ceiling_gbps: float | None):
+    """The three denominators of SURVEY §8(d) and the effective bytes per cell."""
+    ach = roof["achieved"]
+    roof["frac_vs_spec_8000"] = ach / 8000.0
+    roof["frac_vs_measured_copy_6546"] = ach / 6546.2
+    if ceiling_gbps:
+        roof["k12_ceiling_GBps"] = ceiling_gbps
+        roof["frac_vs_k12_ceiling"] = ach / ceiling_gbps
+    if roof.get("traffic"):
+        roof["effective_bytes_per_cell_per_launch"] = roof["traffic"] / cells_per_launch
+    return roof
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons during the timed region."""
 
@@ -319,6 +353,7 @@ def run_native3d(args):
                           % ("7pt" if cfg["stencil"] == P.PX_LAPLACE_7PT_3D else "27pt"), "kernel_ms": k_ms,
                 "algorithmic_bytes_per_launch": alg, "peak_source": peak_src,
                 "whole_step_GBps": BYTES_PER_CELL_UPDATE * value / world}
+    roofline_extras(roofline, n ** 3, k12_ceiling(P, torch, dev, n ** 3, stream))
 
     # e2e: pinned host ρ -> device, solve from φ0 = 0, φ^N back to pinned host, every step
     e2e = None
@@ -492,6 +527,8 @@ def run_native(args):
                           ("k_bulk<RELAX,5pt> (TMA bulk-copy pipeline)" if cfg["stencil"] == 0 else "k_bulk<RELAX,9pt>"),
                 "kernel_ms": k_ms, "algorithmic_bytes_per_launch": BYTES_PER_CELL_UPDATE * local_cells,
                 "peak_source": peak_src, "whole_step_GBps": BYTES_PER_CELL_UPDATE * value}
+    ceil = k12_ceiling(P, torch, dev, min(local_cells, 1 << 28), stream) if local_cells >= (1 << 22) else None
+    roofline_extras(roofline, local_cells, ceil)
 
     # ---- end to end through the public host API (pinned host buffers; every
     # step's H2D of ρ and D2H of φ^N and its norms are inside the timed region).
