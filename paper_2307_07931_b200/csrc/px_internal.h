@@ -146,6 +146,9 @@ struct SmallBox {
   double* d_sum;
 };
 bool smallbox_fits(int nx, int ny);
+// the same solve on a cluster of 8 CTAs with DSMEM halo exchange (px_cluster.cu)
+bool cluster_box_eligible(int nx, int ny);
+px_status launch_cluster_box(const SmallBox& b, cudaStream_t s);
 
 // All sweeps of a single-rank solve in one cooperative launch (px_kernels.cu).
 struct PersistLaunch {

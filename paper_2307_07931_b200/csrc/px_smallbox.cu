@@ -173,6 +173,8 @@ size_t smallbox_smem(int nx, int ny) {
 bool smallbox_fits(int nx, int ny) { return nx >= 1 && ny >= 1 && smallbox_smem(nx, ny) <= 200 * 1024; }
 
 px_status launch_smallbox(const SmallBox& b, cudaStream_t s) {
+  // 16+ rows: spread the box over a cluster of 8 SMs (px_cluster.cu)
+  if (cluster_box_eligible(b.nx, b.ny)) return launch_cluster_box(b, s);
   const size_t smem = smallbox_smem(b.nx, b.ny);
   cudaError_t e;
   if (b.stencil == 0) {
