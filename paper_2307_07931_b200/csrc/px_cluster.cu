@@ -102,8 +102,8 @@ __global__ void __cluster_dims__(CB_CL, 1, 1) __launch_bounds__(CB_THREADS, 1) k
   for (int k = tid; k < R * nx; k += nt) F[k] = b.rhs[(k % nx) + (int64_t)(y0 + k / nx) * b.ld_rhs];
   __syncthreads();
 
-  // halo rows of buffer D from the neighbours' buffer D (or the face rule),
-  // then the x ghosts of the halo rows; D's own rows must be final
+  // halo rows of buffer D from the neighbours' buffer D (or the face rule);
+  // D's own rows and their x ghosts must be final in every CTA
   auto halo = [&](int d) {
     double* D = bufs[d];
     cluster.sync();  // every CTA's rows of D (and their x ghosts) are complete
@@ -140,7 +140,17 @@ __global__ void __cluster_dims__(CB_CL, 1, 1) __launch_bounds__(CB_THREADS, 1) k
       const int i = (x + 1) + (r + 1) * P;
       const double L = cb_taps<ST>(A, P, i);
       const double rr = __dsub_rn(__dmul_rn(scale, L), F[k]);
-      B[i] = __dadd_rn(A[i], __dmul_rn(lambda, rr));
+      const double o = __dadd_rn(A[i], __dmul_rn(lambda, rr));
+      B[i] = o;
+      // the row's x ghost images of this cell (wrap / odd reflection)
+      if (x == 0) {
+        if (b.bc == PX_BC_PERIODIC) B[i + nx] = o;
+        else if (b.bc == PX_BC_DIRICHLET_CC) B[i - 1] = -o;
+      }
+      if (x == nx - 1) {
+        if (b.bc == PX_BC_PERIODIC) B[i - nx] = o;
+        else if (b.bc == PX_BC_DIRICHLET_CC) B[i + 1] = -o;
+      }
       mx = umax64(mx, (unsigned long long)__double_as_longlong(fabs(rr)));
       ss = fma(rr, rr, ss);
       x += sx;
@@ -151,11 +161,9 @@ __global__ void __cluster_dims__(CB_CL, 1, 1) __launch_bounds__(CB_THREADS, 1) k
       }
     }
     if (rec) warp_partial(mx, ss, entry++);
-    __syncthreads();
-    for (int r = 1 + tid; r <= R; r += nt) cb_xghost(B + (size_t)r * P, nx, b.bc);
+    // halo rows: copied with their ghost columns (set by their owner), or the
+    // negated own row at a Dirichlet face (product rule at the corners)
     halo(cur ^ 1);
-    if (tid < 2) cb_xghost(B + (size_t)(tid == 0 ? 0 : R + 1) * P, nx, b.bc);
-    __syncthreads();
     cur ^= 1;
   }
   if (b.final_norm) {
