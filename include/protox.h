@@ -444,6 +444,16 @@ int64_t px_kernel_launch_count(void);
 int32_t px_relax_variant(const px_patch* phi_in, const px_patch* phi_out, const px_patch* rhs,
                          px_box region);
 
+/* Proto's UNFUSED pointwise update (forallInPlace(jacobiUpdate), figure
+ * `Proto`; Eq.3): φ ← φ + λ(temp − rhs) in place over region,
+ * with temp = scale·S(φ) from px_stencil_apply.  With px_stencil_apply and
+ * px_residual_norm it forms the unfused Proto sequence that the fused sweep
+ * replaces -- a measurement baseline (the paper's fused-vs-unfused
+ * comparison, on the GPU), bit-identical to px_relax_step.
+ * PX_ERR_DOMAIN if region is not inside every patch.  Asynchronous. */
+px_status px_pointwise_update(px_patch* phi, const px_patch* temp, const px_patch* rhs, double lambda,
+                              px_box region, void* stream);
+
 /* Measurement helper (not part of the method): the streaming ceiling of the
  * GPU for the sweep's access pattern.  variant 0: c[i] = a[i] + b[i] (2 reads,
  * 1 write, like the fused sweep); variant 1: c[i] = a[i] (copy).  n even,

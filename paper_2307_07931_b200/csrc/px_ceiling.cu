@@ -65,3 +65,44 @@ extern "C" px_status px_stream_ceiling(const double* a, const double* b, double*
   count_launches(1);
   return cuda_check(cudaGetLastError(), "ceiling kernel launch");
 }
+
+// ---------------------------------------------------------------------------
+// K10: Proto's UNFUSED pointwise update, forallInPlace(jacobiUpdate, φ, temp,
+// ρ, λ) of figure `Proto` (Eq.3): φ ← φ + λ(temp − ρ) in place,
+// temp = laplace(φ, wgt) from px_stencil_apply.  Together with
+// px_stencil_apply and px_residual_norm it is the unfused Proto sequence the
+// fused sweep replaces (the paper's own comparison, re-run on
+// the GPU: scripts/fusion_gpu.py).  Every operation rounded as in the oracle,
+// so the sequence is bit-identical to the fused sweep.  Baseline only.
+namespace px {
+__global__ void __launch_bounds__(256) k_update(double* phi, const double* temp, const double* rhs, int64_t ldp,
+                                                int64_t ldt, int64_t ldr, int nx, int ny, double lambda) {
+  for (int y = blockIdx.y; y < ny; y += gridDim.y) {
+    double* p = phi + (int64_t)y * ldp;
+    const double* t = temp + (int64_t)y * ldt;
+    const double* f = rhs + (int64_t)y * ldr;
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < nx; x += gridDim.x * blockDim.x)
+      p[x] = __dadd_rn(p[x], __dmul_rn(lambda, __dsub_rn(t[x], f[x])));
+  }
+}
+}  // namespace px
+
+extern "C" px_status px_pointwise_update(px_patch* phi, const px_patch* temp, const px_patch* rhs, double lambda,
+                                         px_box region, void* stream) {
+  using namespace px;
+  clear_error();
+  PX_TRY(check_patch(phi, "phi"));
+  PX_TRY(check_patch(temp, "temp"));
+  PX_TRY(check_patch(rhs, "rhs"));
+  if (empty(region)) return PX_OK;
+  if (!contains(phi->box, region) || !contains(temp->box, region) || !contains(rhs->box, region))
+    return fail(PX_ERR_DOMAIN, "px_pointwise_update: region outside a patch");
+  const int nx = ext(region, 0), ny = ext(region, 1);
+  const int gx = (nx + 255) / 256 < 4 ? (nx + 255) / 256 : 4;
+  const int gy = ny < 4096 ? ny : 4096;
+  k_update<<<dim3(gx, gy), 256, 0, (cudaStream_t)stream>>>(
+      at(*phi, region.lo.c[0], region.lo.c[1]), at(*temp, region.lo.c[0], region.lo.c[1]),
+      at(*rhs, region.lo.c[0], region.lo.c[1]), phi->ld, temp->ld, rhs->ld, nx, ny, lambda);
+  count_launches(1);
+  return cuda_check(cudaGetLastError(), "update kernel launch");
+}

@@ -99,7 +99,7 @@ EXPORTS = [
     "px_comm_enable_p2p",
     "px_exchange_ghosts", "px_exchange_ghosts_local",
     "px_solve", "px_solve_host", "px_solve_host_batch", "px_release_cached", "px_mg_solve", "px_mg_release", "px_kernel_launch_count",
-    "px_relax_variant", "px_stream_ceiling",
+    "px_relax_variant", "px_stream_ceiling", "px_pointwise_update",
     "px3_layout", "px3_norm_buffer_len", "px3_init_field", "px3_fill_ghosts", "px3_relax_step",
     "px3_residual_norm", "px3_solve", "px3_release", "px3_mehrstellen_rhs",
 ]
@@ -190,6 +190,8 @@ def lib():
     L.px_kernel_launch_count.restype = i64
     L.px_stream_ceiling.restype = st
     L.px_stream_ceiling.argtypes = [vp, vp, vp, i64, i32, vp]
+    L.px_pointwise_update.restype = st
+    L.px_pointwise_update.argtypes = [P(px_patch), P(px_patch), P(px_patch), ctypes.c_double, px_box, vp]
     L.px3_layout.restype = st
     L.px3_layout.argtypes = [P(i32), i32, P(i64), P(i64), P(i64), P(i64)]
     L.px3_norm_buffer_len.restype = i64
@@ -536,6 +538,12 @@ def relax_variant(phi_in: px_patch, phi_out: px_patch, rhs: px_patch, region: px
 def stream_ceiling(a, b, c, variant: int = 0, stream=None):
     """K12 measurement helper: c = a + b (variant 0) or c = a (variant 1)."""
     _check(lib().px_stream_ceiling(_ptr(a), _ptr(b), _ptr(c), c.numel(), variant, _stream(stream)))
+
+
+def pointwise_update(phi: px_patch, temp: px_patch, rhs: px_patch, lam: float, region: px_box, stream=None):
+    """px_pointwise_update: Proto's unfused forallInPlace update (baseline)."""
+    _check(lib().px_pointwise_update(ctypes.byref(phi), ctypes.byref(temp), ctypes.byref(rhs), lam, region,
+                                     _stream(stream)))
 
 
 def kernel_launch_count() -> int:

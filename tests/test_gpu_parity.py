@@ -715,3 +715,30 @@ def test_resident_temporal_blocking_variant_subprocess():
                             "tests/test_gpu_parity.py", "-k", "resident_shapes or config2_full"],
                            cwd=root, env=env, capture_output=True, text=True, timeout=900)
         assert r.returncode == 0, (k, r.stdout[-3000:] + r.stderr[-2000:])
+
+
+@pytest.mark.gpu
+def test_unfused_proto_sequence_bitwise():
+    """Proto's unfused sequence (px_stencil_apply -> px_pointwise_update, then
+    px_residual_norm of the updated iterate) equals the oracle bit
+    for bit -- the baseline of the fused-vs-unfused measurement."""
+    n0, n1, N = 300, 170, 5
+    h = 1.0 / 256
+    lam = h * h / 8
+    phi0, rho = _fields(n0, n1, 1, 5, P.PX_BC_PERIODIC)
+    lay = P.Layout(P.box(0, 0, n0 - 1, n1 - 1), (n0, n1), 1, P.PX_BC_PERIODIC, 1)
+    li = lay.local(0)
+    a, t, r = to_device_ghosted(lay, 0, phi0, 1), lay.alloc(0), to_device_ghosted(lay, 0, rho, 1)
+    pa, pt, pr = lay.patch(0, a), lay.patch(0, t), lay.patch(0, r)
+    nb = P.norm_buffer(li.owned)
+    got = []
+    for _ in range(N):
+        P.fill_ghosts(lay, 0, pa)
+        P.stencil_apply(0, 1.0 / (h * h), pa, pt, li.owned)
+        P.pointwise_update(pa, pt, pr, lam, li.owned)
+        P.fill_ghosts(lay, 0, pa)
+        P.residual_norm(P.relax_params(h, lam), pa, pr, li.owned, nb)
+        got.append(nb[:2].cpu().numpy())
+    ref, rn = oracle.solve(_orc_problem(n0, n1, h, lam, P.PX_BC_PERIODIC, 0, N, 1), phi0, rho)
+    assert bits_equal(owned_to_host(lay, 0, a), ref[1:-1, 1:-1])
+    _check_norms(np.array(got), rn[1:])
