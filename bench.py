@@ -266,8 +266,9 @@ def run_reference(args):
 
 # ----------------------------------------------------------------- native arm
 def run_native3d(args):
-    """C3D: the 3D relaxation (px3_solve).  N > 1: independent replicas (the
-    3D path is single-device; weak scaling, no data-path collective)."""
+    """C3D / C3D27: the 3D relaxation (px3_solve).  N > 1: the n³ domain in
+    z-slabs over the ranks (px3_solve_comm: z ghost planes over NCCL, norms
+    all-reduced at the end) -- strong scaling."""
     import torch
     import torch.distributed as dist
 
@@ -285,7 +286,17 @@ def run_native3d(args):
     n, S, E = cfg["n"], cfg["sweeps"], cfg["norm_every"]
     h = 1.0 / n
     lam = h * h / 12  # λ = h²/(4D), D = 3
-    grid = P.Grid3((n, n, n), 1)
+    comm = None
+    nzl = n
+    if world > 1 and cfg["stencil"] != P.PX_LAPLACE_7PT_3D:
+        raise SystemExit("C3D27 runs on one GPU (its corrected right-hand side needs exchanged rho planes)")
+    if world > 1:
+        z0, z1 = P.slab3(n, world, rank)
+        nzl = z1 - z0
+        obj = [P.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = P.Comm(obj[0], world, rank, local)
+    grid = P.Grid3((n, n, nzl), 1)
     phi, scr, rho = grid.alloc(dev), grid.alloc(dev), grid.alloc(dev)
     stream = torch.cuda.Stream(device=dev)
     stream.wait_stream(torch.cuda.current_stream(dev))
@@ -300,8 +311,13 @@ def run_native3d(args):
     stream.synchronize()
     bufs = [phi, scr]
 
+    def solve_any(a, b, r_):
+        if comm is not None:
+            return P.solve3_comm(comm, grid, cfg["bc"], prm, S, E, a, b, r_, use_graph=True, stream=stream)
+        return P.solve3(grid, cfg["bc"], prm, S, E, a, b, r_, use_graph=True, stream=stream)
+
     def step():
-        r = P.solve3(grid, cfg["bc"], prm, S, E, bufs[0], bufs[1], rho, use_graph=True, stream=stream)
+        r = solve_any(bufs[0], bufs[1], rho)
         if r.in_scratch:
             bufs.reverse()
         return r
@@ -330,7 +346,7 @@ def run_native3d(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_ms = float(t.item())
-    value = world * n ** 3 * S * args.steps / (t_ms * 1e-3) / 1e9
+    value = n ** 3 * S * args.steps / (t_ms * 1e-3) / 1e9
 
     # roofline of k3_relax (px3_relax_step, same launch geometry), CUDA events on its stream
     nb = P.norm_buffer3(dev)
@@ -345,7 +361,7 @@ def run_native3d(args):
         evs[i][1].record(stream)
     stream.synchronize()
     k_ms = statistics.mean(a.elapsed_time(b) for a, b in evs[2:])
-    alg = BYTES_PER_CELL_UPDATE * n ** 3
+    alg = BYTES_PER_CELL_UPDATE * n * n * nzl
     peak, peak_src = load_peaks()
     roofline = {"bound": "hbm", "achieved": alg / (k_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
                 "frac": alg / (k_ms * 1e-3) / 1e9 / peak, "traffic": load_traffic(args.config) if world == 1 else None,
@@ -353,7 +369,7 @@ def run_native3d(args):
                           % ("7pt" if cfg["stencil"] == P.PX_LAPLACE_7PT_3D else "27pt"), "kernel_ms": k_ms,
                 "algorithmic_bytes_per_launch": alg, "peak_source": peak_src,
                 "whole_step_GBps": BYTES_PER_CELL_UPDATE * value / world}
-    roofline_extras(roofline, n ** 3, k12_ceiling(P, torch, dev, n ** 3, stream))
+    roofline_extras(roofline, n * n * nzl, k12_ceiling(P, torch, dev, n * n * nzl, stream))
 
     # e2e: pinned host ρ -> device, solve from φ0 = 0, φ^N back to pinned host, every step
     e2e = None
@@ -367,7 +383,7 @@ def run_native3d(args):
             with torch.cuda.stream(stream):
                 grid.view(d_phi).zero_()
                 grid.view(d_rhs).copy_(h_rho, non_blocking=True)
-            r = P.solve3(grid, cfg["bc"], prm, S, E, d_phi, d_scr, d_rhs, use_graph=True, stream=stream)
+            r = solve_any(d_phi, d_scr, d_rhs)
             with torch.cuda.stream(stream):
                 h_out.copy_(grid.view(d_scr if r.in_scratch else d_phi), non_blocking=True)
             stream.synchronize()
@@ -385,8 +401,9 @@ def run_native3d(args):
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         n_norm = (S + E - 1) // E + 1 if E > 0 else 1
-        e2e = {"value": world * n ** 3 * S * ke / (te.item() * 1e-3) / 1e9, "unit": UNIT,
-               "h2d_bytes_per_step": n ** 3 * 8, "d2h_bytes_per_step": n ** 3 * 8 + 16 * n_norm, "steps": ke,
+        e2e = {"value": n ** 3 * S * ke / (te.item() * 1e-3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": n * n * nzl * 8, "d2h_bytes_per_step": n * n * nzl * 8 + 16 * n_norm,
+               "steps": ke,
                "api": "torch pinned copy of rho + px3_solve (phi0 = 0 zero-filled on the device) + D2H phi^N"}
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -397,13 +414,18 @@ def run_native3d(args):
         print(json.dumps({
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": t_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["desc"], "n": n, "sweeps_per_step": S, "norm_every": E, "ghost": 1,
-                       "replicas": world, "rho": cfg["rho"], "h": h, "lambda": lam,
+                       "partition": f"z-slabs x{world}",
+                       "rho": cfg["rho"] if world == 1 else "hash of each rank's local cell index",
+                       "h": h, "lambda": lam,
                        "steps_continue": "each step continues from the previous step's iterate",
                        "l2": "inputs (3 x %.2f GB) exceed L2; no flush" % (grid.alloc_elems * 8 / 1e9)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
             "final_residual_max": float(res.norms[-1, 0]) if len(res.norms) else None}))
+    if comm is not None:
+        P.release3()
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
     return 0

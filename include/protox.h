@@ -432,6 +432,21 @@ px_status px3_residual_norm(const px_relax_params* p, const px_patch3* phi, cons
 px_status px3_solve(px_bc bc, const px_relax_params* p, const px_solve_opts* o, px_patch3* phi,
                     px_patch3* phi_scratch, const px_patch3* rhs, double* h_norms, int32_t cap,
                     int32_t* n_written, int32_t* in_scratch, void* stream);
+/* z-slab decomposition of a 3D domain (n2 planes) over nranks ranks, the 3D
+ * counterpart of the 2D slab partitioner: rank r owns planes
+ * [z0, z1) = [r·n2/P, (r+1)·n2/P).  PX_ERR_SHAPE if n2 < nranks. */
+px_status px3_slab(int32_t n2, int32_t nranks, int32_t rank, int32_t* z0, int32_t* z1);
+/* px3_solve on this rank's z-slab of a domain split over the communicator's
+ * ranks (patches hold the rank's n2 = z1 - z0 planes): per sweep the x / y
+ * ghosts locally, the z ghost planes from the slab neighbours in one NCCL
+ * group (send up, send down, recv down, recv up) -- a periodic ring, or the
+ * boundary rule at the global z faces -- then the fused sweep; the recorded
+ * norms are all-reduced over the ranks once at the end (ncclMax, ncclSum).
+ * A one-rank communicator created with PROTOX_NCCL_SELF_EXCHANGE=1 exchanges
+ * its periodic z planes with itself (test mode). */
+px_status px3_solve_comm(px_comm* c, px_bc bc, const px_relax_params* p, const px_solve_opts* o, px_patch3* phi,
+                         px_patch3* phi_scratch, const px_patch3* rhs, double* h_norms, int32_t cap,
+                         int32_t* n_written, int32_t* in_scratch, void* stream);
 void px3_release(void);
 
 /* Diagnostics: number of kernel launches libprotox enqueued so far in this

@@ -26,6 +26,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
+#include <nccl.h>
 
 #include <cmath>
 #include <cstdint>
@@ -341,7 +342,8 @@ __global__ void __maxnreg__(ST == 1 ? 168 : 112)  // 9 warps: 3 share a sub-part
 // (mode 2) of the owned cells; dimensions before D cover their ghosts too
 // (phased x, y, z: edges and corners by the product rule).
 template <int D>
-__global__ void k3_ghost(double* o, int64_t ld, int64_t plane, int n0, int n1, int n2, int g, int mode) {
+__global__ void k3_ghost(double* o, int64_t ld, int64_t plane, int n0, int n1, int n2, int g, int mode,
+                         int sides) {
   const int n[3] = {n0, n1, n2};
   // extents of the face set: dims < D padded, D ghost-only (2g), dims > D interior
   int e[3];
@@ -361,6 +363,7 @@ __global__ void k3_ghost(double* o, int64_t ld, int64_t plane, int n0, int n1, i
     int s[3] = {c[0], c[1], c[2]};
     double sign = 1.0;
     const int cd = c[D];
+    if (!(sides & (cd < 0 ? 1 : 2))) continue;  // bit 0: lower face, bit 1: upper face
     if (mode == GH_WRAP) {
       s[D] = cd < 0 ? cd + n[D] : cd - n[D];
     } else {
@@ -582,7 +585,10 @@ static px_status launch_relax3(int mode, const px_relax_params& prm, const px_pa
   return cuda_check(cudaGetLastError(), "3D relax launch");
 }
 
-static px_status launch_ghost3(px_bc bc, const px_patch3& p, cudaStream_t s) {
+// ghost layers: dimensions x, y (both sides) and z on the `zsides` faces
+// (bit 0 lower, bit 1 upper): the slab solve fills the inter-rank z faces by
+// exchange
+static px_status launch_ghost3(px_bc bc, const px_patch3& p, cudaStream_t s, int zsides = 3) {
   if (bc == PX_BC_FIXED_GHOSTS) return PX_OK;
   const int mode = bc == PX_BC_PERIODIC ? GH_WRAP : GH_REFLECT;
   const int g = p.ghost;
@@ -596,10 +602,13 @@ static px_status launch_ghost3(px_bc bc, const px_patch3& p, cudaStream_t s) {
   const int64_t f0 = (int64_t)2 * g * p.n[1] * p.n[2];
   const int64_t f1 = (int64_t)(p.n[0] + 2 * g) * 2 * g * p.n[2];
   const int64_t f2 = (int64_t)(p.n[0] + 2 * g) * (p.n[1] + 2 * g) * 2 * g;
-  k3_ghost<0><<<blocks(f0), T, 0, s>>>(p.data, p.ld, p.plane, p.n[0], p.n[1], p.n[2], g, mode);
-  k3_ghost<1><<<blocks(f1), T, 0, s>>>(p.data, p.ld, p.plane, p.n[0], p.n[1], p.n[2], g, mode);
-  k3_ghost<2><<<blocks(f2), T, 0, s>>>(p.data, p.ld, p.plane, p.n[0], p.n[1], p.n[2], g, mode);
-  count_launches(3);
+  k3_ghost<0><<<blocks(f0), T, 0, s>>>(p.data, p.ld, p.plane, p.n[0], p.n[1], p.n[2], g, mode, 3);
+  k3_ghost<1><<<blocks(f1), T, 0, s>>>(p.data, p.ld, p.plane, p.n[0], p.n[1], p.n[2], g, mode, 3);
+  count_launches(2);
+  if (zsides) {
+    k3_ghost<2><<<blocks(f2), T, 0, s>>>(p.data, p.ld, p.plane, p.n[0], p.n[1], p.n[2], g, mode, zsides);
+    count_launches(1);
+  }
   return cuda_check(cudaGetLastError(), "3D ghost fill launch");
 }
 
@@ -635,6 +644,7 @@ static double* start3(const px_patch3& p) { return p.data - 2 - (int64_t)p.ghost
 // ------------------------------------------------------------ solve plan
 struct Plan3 {
   // key
+  px_comm* comm = nullptr;
   px_bc bc;
   px_relax_params prm;
   px_solve_opts opts;
@@ -654,11 +664,54 @@ struct Plan3 {
 };
 static std::unique_ptr<Plan3> g_plan3;
 
-static bool same_key(const Plan3& p, px_bc bc, const px_relax_params& prm, const px_solve_opts& o,
+static bool same_key(const Plan3& p, px_comm* comm, px_bc bc, const px_relax_params& prm, const px_solve_opts& o,
                      const px_patch3& a, const px_patch3& b, const px_patch3& r, cudaStream_t s) {
-  return p.bc == bc && std::memcmp(&p.prm, &prm, sizeof prm) == 0 && std::memcmp(&p.opts, &o, sizeof o) == 0 &&
+  return p.comm == comm && p.bc == bc && std::memcmp(&p.prm, &prm, sizeof prm) == 0 && std::memcmp(&p.opts, &o, sizeof o) == 0 &&
          std::memcmp(&p.a, &a, sizeof a) == 0 && std::memcmp(&p.b, &b, sizeof b) == 0 &&
          std::memcmp(&p.r, &r, sizeof r) == 0 && p.s == s;
+}
+
+static px_status nccl3(ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return PX_OK;
+  return fail(PX_ERR_NCCL, "%s: %s", what, ncclGetErrorString(r));
+}
+
+// z-slab neighbours of this rank (-1: a domain face handled locally)
+static void slab_nbrs(const Plan3& P, int* lo, int* hi) {
+  *lo = *hi = -1;
+  if (!P.comm) return;
+  const int np = comm_nranks(P.comm), r = comm_rank(P.comm);
+  const bool per = P.bc == PX_BC_PERIODIC;
+  if (np == 1) {
+    if (per && comm_self_exchange(P.comm)) *lo = *hi = 0;  // test mode: the rank is its own neighbour
+    return;
+  }
+  *lo = r > 0 ? r - 1 : (per ? np - 1 : -1);
+  *hi = r < np - 1 ? r + 1 : (per ? 0 : -1);
+}
+
+// ghost fill of one iterate: x, y locally; z planes from the slab neighbours
+// (one NCCL group, posted send-up, send-down, recv-down, recv-up -- NCCL
+// matches a peer pair's sends and receives in posting order, so two ranks on
+// a periodic ring pair the right planes) or locally at a domain face.
+static px_status exchange3(const Plan3& P, const px_patch3& p) {
+  int lo, hi;
+  slab_nbrs(P, &lo, &hi);
+  const int zs = (lo < 0 ? 1 : 0) | (hi < 0 ? 2 : 0);
+  if (!P.comm) return launch_ghost3(P.bc, p, P.s, 3);
+  PX_TRY(launch_ghost3(P.bc, p, P.s, zs));
+  if (lo < 0 && hi < 0) return PX_OK;
+  // a full plane, cells (-2 .. n0+1, -g .. n1+g-1) of plane z
+  const int g = p.ghost, nz = p.n[2];
+  const size_t cnt = (size_t)(p.n[1] + 2 * g - 1) * p.ld + p.n[0] + 4;
+  auto plane_at = [&](int z) { return p.data + (int64_t)z * p.plane - (int64_t)g * p.ld - 2; };
+  ncclComm_t nc = (ncclComm_t)comm_nccl(P.comm);
+  PX_TRY(nccl3(ncclGroupStart(), "ncclGroupStart"));
+  if (hi >= 0) PX_TRY(nccl3(ncclSend(plane_at(nz - 1), cnt, ncclDouble, hi, nc, P.s), "ncclSend up"));
+  if (lo >= 0) PX_TRY(nccl3(ncclSend(plane_at(0), cnt, ncclDouble, lo, nc, P.s), "ncclSend down"));
+  if (lo >= 0) PX_TRY(nccl3(ncclRecv(plane_at(-1), cnt, ncclDouble, lo, nc, P.s), "ncclRecv down"));
+  if (hi >= 0) PX_TRY(nccl3(ncclRecv(plane_at(nz), cnt, ncclDouble, hi, nc, P.s), "ncclRecv up"));
+  return nccl3(ncclGroupEnd(), "ncclGroupEnd");
 }
 
 static px_status enqueue_solve3(Plan3& P) {
@@ -670,8 +723,8 @@ static px_status enqueue_solve3(Plan3& P) {
   auto slot = [&](int e) {
     NormSlot ns;
     std::memset(&ns, 0, sizeof ns);
-    ns.out_max = P.d_ring + 2 * e;
-    ns.out_sum = P.d_ring + 2 * e + 1;
+    ns.out_max = P.d_ring + e;  // ring: max[ne] then sum[ne] (all-reduced as two arrays)
+    ns.out_sum = P.d_ring + (P.n_entries > 0 ? P.n_entries : 1) + e;
     ns.counter = reinterpret_cast<unsigned int*>(P.d_ws);
     ns.partials = P.d_ws + 2;
     ns.offset = 0;
@@ -679,15 +732,23 @@ static px_status enqueue_solve3(Plan3& P) {
     return ns;
   };
   for (int it = 0; it < N; ++it) {
-    PX_TRY(launch_ghost3(P.bc, *cur, P.s));
+    PX_TRY(exchange3(P, *cur));
     NormSlot ns;
     std::memset(&ns, 0, sizeof ns);
     if (E > 0 && it % E == 0) ns = slot(entry++);
     PX_TRY(launch_relax3(MODE_RELAX, P.prm, *cur, nxt, P.r, ns, P.s));
     std::swap(cur, nxt);
   }
-  PX_TRY(launch_ghost3(P.bc, *cur, P.s));
+  PX_TRY(exchange3(P, *cur));
   if (E >= 0) PX_TRY(launch_relax3(MODE_RESID, P.prm, *cur, nullptr, P.r, slot(entry++), P.s));
+  if (P.comm && E >= 0) {  // the residual norms over all ranks, once per solve (R14)
+    const int ne = P.n_entries;
+    ncclComm_t nc = (ncclComm_t)comm_nccl(P.comm);
+    PX_TRY(nccl3(ncclGroupStart(), "ncclGroupStart"));
+    PX_TRY(nccl3(ncclAllReduce(P.d_ring, P.d_ring, ne, ncclDouble, ncclMax, nc, P.s), "ncclAllReduce max"));
+    PX_TRY(nccl3(ncclAllReduce(P.d_ring + ne, P.d_ring + ne, ne, ncclDouble, ncclSum, nc, P.s), "ncclAllReduce sum"));
+    PX_TRY(nccl3(ncclGroupEnd(), "ncclGroupEnd"));
+  }
   return PX_OK;
 }
 
@@ -769,10 +830,12 @@ px_status px3_residual_norm(const px_relax_params* p, const px_patch3* phi, cons
                        (cudaStream_t)stream);
 }
 
-px_status px3_solve(px_bc bc, const px_relax_params* p, const px_solve_opts* o, px_patch3* phi,
-                    px_patch3* phi_scratch, const px_patch3* rhs, double* h_norms, int32_t cap,
-                    int32_t* n_written, int32_t* in_scratch, void* stream) {
-  clear_error();
+}  // extern "C"
+
+namespace px {
+static px_status solve3_impl(px_comm* comm, px_bc bc, const px_relax_params* p, const px_solve_opts* o,
+                             px_patch3* phi, px_patch3* phi_scratch, const px_patch3* rhs, double* h_norms,
+                             int32_t cap, int32_t* n_written, int32_t* in_scratch, void* stream) {
   PX_TRY(check_params3(p));
   if (!o) return fail(PX_ERR_ARG, "null options");
   if (o->nsweeps < 0) return fail(PX_ERR_ARG, "nsweeps must be >= 0");
@@ -794,9 +857,10 @@ px_status px3_solve(px_bc bc, const px_relax_params* p, const px_solve_opts* o, 
                                       cudaMemcpyDeviceToDevice, s),
                       "fixed ghost copy"));
   }
-  if (!g_plan3 || !same_key(*g_plan3, bc, *p, *o, *phi, *phi_scratch, *rhs, s)) {
+  if (!g_plan3 || !same_key(*g_plan3, comm, bc, *p, *o, *phi, *phi_scratch, *rhs, s)) {
     g_plan3.reset(new Plan3());
     Plan3& P = *g_plan3;
+    P.comm = comm;
     P.bc = bc;
     P.prm = *p;
     P.opts = *o;
@@ -836,9 +900,9 @@ px_status px3_solve(px_bc bc, const px_relax_params* p, const px_solve_opts* o, 
                       "norms D2H"));
   PX_TRY(cuda_check(cudaStreamSynchronize(s), "solve sync"));
   const int nw = n_entries < cap ? n_entries : cap;
-  for (int j = 0; j < nw; ++j) {
-    h_norms[2 * j] = ring[2 * j];
-    h_norms[2 * j + 1] = ring[2 * j + 1];
+  for (int j = 0; j < nw; ++j) {  // ring: max[n_entries] then sum[n_entries]
+    h_norms[2 * j] = ring[j];
+    h_norms[2 * j + 1] = ring[n_entries + j];
   }
   if (n_written) *n_written = n_entries;
   const bool odd = (N & 1) != 0;
@@ -853,6 +917,46 @@ px_status px3_solve(px_bc bc, const px_relax_params* p, const px_solve_opts* o, 
   return PX_OK;
 }
 
+}  // namespace px
+
+extern "C" {
+
+px_status px3_solve(px_bc bc, const px_relax_params* p, const px_solve_opts* o, px_patch3* phi,
+                    px_patch3* phi_scratch, const px_patch3* rhs, double* h_norms, int32_t cap,
+                    int32_t* n_written, int32_t* in_scratch, void* stream) {
+  clear_error();
+  return solve3_impl(nullptr, bc, p, o, phi, phi_scratch, rhs, h_norms, cap, n_written, in_scratch, stream);
+}
+
+px_status px3_slab(int32_t n2, int32_t nranks, int32_t rank, int32_t* z0, int32_t* z1) {
+  clear_error();
+  if (!z0 || !z1) return fail(PX_ERR_ARG, "null argument");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(PX_ERR_ARG, "bad rank %d of %d", rank, nranks);
+  if (n2 < nranks) return fail(PX_ERR_SHAPE, "n2 = %d planes for %d ranks", n2, nranks);
+  *z0 = (int32_t)((int64_t)rank * n2 / nranks);
+  *z1 = (int32_t)((int64_t)(rank + 1) * n2 / nranks);
+  return PX_OK;
+}
+
+px_status px3_solve_comm(px_comm* c, px_bc bc, const px_relax_params* p, const px_solve_opts* o, px_patch3* phi,
+                         px_patch3* phi_scratch, const px_patch3* rhs, double* h_norms, int32_t cap,
+                         int32_t* n_written, int32_t* in_scratch, void* stream) {
+  clear_error();
+  if (!c) return fail(PX_ERR_ARG, "null communicator");
+  return solve3_impl(c, bc, p, o, phi, phi_scratch, rhs, h_norms, cap, n_written, in_scratch, stream);
+}
+
 void px3_release(void) { g_plan3.reset(); }
+
+}  // extern "C"
+
+namespace px {
+// drop the cached 3D plan of a communicator being destroyed (px_comm_destroy)
+void release3_for_comm(const px_comm* c) {
+  if (g_plan3 && g_plan3->comm == c) g_plan3.reset();
+}
+}  // namespace px
+
+extern "C" {
 
 }  // extern "C"

@@ -214,6 +214,13 @@ px_status launch_init_field(const px_layout* l, int32_t rank, const px_patch& p,
 px_status cuda_check(cudaError_t e, const char* what);
 void count_launches(int64_t n);
 
+// communicator accessors (px_solve.cu) for the 3D slab solve (px3d.cu)
+void* comm_nccl(const px_comm* c);  // ncclComm_t
+int32_t comm_nranks(const px_comm* c);
+int32_t comm_rank(const px_comm* c);
+bool comm_self_exchange(const px_comm* c);
+void release3_for_comm(const px_comm* c);  // px3d.cu
+
 // validation helpers (px_host.cpp)
 px_status check_patch(const px_patch* p, const char* name);
 px_status local_info(const px_layout* l, int32_t rank, px_local_info* out);

@@ -580,6 +580,14 @@ static int32_t count_entries(int32_t N, int32_t E) {
 
 using namespace px;
 
+namespace px {
+// accessors for the 3D slab solve (px3d.cu)
+void* comm_nccl(const px_comm* c) { return (void*)c->nccl; }
+int32_t comm_nranks(const px_comm* c) { return c->nranks; }
+int32_t comm_rank(const px_comm* c) { return c->rank; }
+bool comm_self_exchange(const px_comm* c) { return c->self_exchange; }
+}  // namespace px
+
 extern "C" {
 
 px_status px_comm_unique_id(uint8_t id[128]) {
@@ -618,6 +626,7 @@ px_status px_comm_create(const uint8_t id[128], int32_t nranks, int32_t rank, in
 
 void px_comm_destroy(px_comm* c) {
   if (!c) return;
+  px::release3_for_comm(c);
   // drop plans that reference this communicator
   auto& v = plans();
   v.erase(std::remove_if(v.begin(), v.end(), [c](const std::unique_ptr<Plan>& p) { return p->key.comm == c; }),

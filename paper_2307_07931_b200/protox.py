@@ -101,7 +101,7 @@ EXPORTS = [
     "px_solve", "px_solve_host", "px_solve_host_batch", "px_release_cached", "px_mg_solve", "px_mg_release", "px_kernel_launch_count",
     "px_relax_variant", "px_stream_ceiling", "px_pointwise_update",
     "px3_layout", "px3_norm_buffer_len", "px3_init_field", "px3_fill_ghosts", "px3_relax_step",
-    "px3_residual_norm", "px3_solve", "px3_release", "px3_mehrstellen_rhs",
+    "px3_residual_norm", "px3_solve", "px3_release", "px3_mehrstellen_rhs", "px3_slab", "px3_solve_comm",
 ]
 
 
@@ -207,6 +207,11 @@ def lib():
     L.px3_solve.argtypes = [st, P(px_relax_params), P(px_solve_opts), P(px_patch3), P(px_patch3), P(px_patch3),
                             P(ctypes.c_double), i32, P(i32), P(i32), vp]
     L.px3_release.restype = None
+    L.px3_slab.restype = st
+    L.px3_slab.argtypes = [i32, i32, i32, P(i32), P(i32)]
+    L.px3_solve_comm.restype = st
+    L.px3_solve_comm.argtypes = [vp, st, P(px_relax_params), P(px_solve_opts), P(px_patch3), P(px_patch3),
+                                 P(px_patch3), P(ctypes.c_double), i32, P(i32), P(i32), vp]
     L.px3_mehrstellen_rhs.restype = st
     L.px3_mehrstellen_rhs.argtypes = [P(px_patch3), P(px_patch3), vp]
     L.px_relax_variant.restype = i32
@@ -623,6 +628,27 @@ def mehrstellen_rhs3(grid: Grid3, rho, f, stream=None):
     """px3_mehrstellen_rhs: f = ρ + S7(ρ)/12 (ρ's ghosts filled)."""
     a, b = grid.patch(rho), grid.patch(f)
     _check(lib().px3_mehrstellen_rhs(ctypes.byref(a), ctypes.byref(b), _stream(stream)))
+
+
+def slab3(n2: int, nranks: int, rank: int):
+    """px3_slab: the planes [z0, z1) rank owns of an n2-plane domain."""
+    z0, z1 = ctypes.c_int32(), ctypes.c_int32()
+    _check(lib().px3_slab(n2, nranks, rank, ctypes.byref(z0), ctypes.byref(z1)))
+    return z0.value, z1.value
+
+
+def solve3_comm(comm, grid: Grid3, bc: int, p: px_relax_params, nsweeps: int, norm_every: int, phi, phi_scratch,
+                rhs, use_graph: bool = False, stream=None, keep_in_scratch: bool = True) -> SolveResult:
+    """px3_solve_comm: this rank's z-slab (grid.n[2] = its planes) of a domain split over comm."""
+    opts = px_solve_opts(nsweeps, norm_every, 1, int(use_graph))
+    cap = 0 if norm_every < 0 else ((nsweeps + norm_every - 1) // norm_every if norm_every > 0 else 0) + 1
+    norms = np.zeros((max(cap, 1), 2), dtype=np.float64)
+    nw, ins = ctypes.c_int32(0), ctypes.c_int32(0)
+    a, b, r = grid.patch(phi), grid.patch(phi_scratch), grid.patch(rhs)
+    _check(lib().px3_solve_comm(comm.h, bc, ctypes.byref(p), ctypes.byref(opts), ctypes.byref(a), ctypes.byref(b),
+                                ctypes.byref(r), norms.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), max(cap, 1),
+                                ctypes.byref(nw), ctypes.byref(ins) if keep_in_scratch else None, _stream(stream)))
+    return SolveResult(norms[: nw.value].copy(), bool(ins.value))
 
 
 def release3():

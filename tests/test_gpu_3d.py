@@ -260,3 +260,36 @@ def test_mehrstellen27_corrected_rhs_and_solve(bc):
     ref, rn = oracle.solve3(p, phi0, rho)
     assert bits_equal(out, ref[1:-1, 1:-1, 1:-1]), ulp_diff(out, ref[1:-1, 1:-1, 1:-1])
     _check_norms(res.norms, rn)
+
+
+# ------------------------------------------------------- z slabs over NCCL
+@pytest.mark.parametrize("st,bc,graph", [(P.PX_LAPLACE_7PT_3D, P.PX_BC_PERIODIC, True),
+                                         (P.PX_LAPLACE_7PT_3D, P.PX_BC_PERIODIC, False),
+                                         (P.PX_MEHRSTELLEN_27PT_3D, P.PX_BC_PERIODIC, True),
+                                         (P.PX_LAPLACE_7PT_3D, P.PX_BC_DIRICHLET_CC, True)])
+def test_solve3_comm_nccl_self_exchange(st, bc, graph, monkeypatch):
+    """px3_solve_comm with a one-rank NCCL communicator: in self-exchange mode
+    (periodic) the z ghost planes travel through ncclSend/ncclRecv to the rank
+    itself with the slab plan's posting order, inside the CUDA graph, and the
+    norms are all-reduced -- bit-identical to the oracle; Dirichlet: local faces."""
+    monkeypatch.setenv("PROTOX_NCCL_SELF_EXCHANGE", "1")
+    n = (70, 37, 13)
+    h = 1.0 / 70
+    lam = h * h / 12
+    phi0, rho = _fields(n, 1, 300 + st + bc)
+    grid = P.Grid3(n, 1)
+    a, b, r = _upload(grid, phi0), grid.alloc(), _upload(grid, rho)
+    comm = P.Comm(P.comm_unique_id(), 1, 0, torch.cuda.current_device())
+    try:
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        res = P.solve3_comm(comm, grid, bc, P.relax_params(h, lam, st), 6, 2, a, b, r, use_graph=graph, stream=s)
+        out = grid.view(b if res.in_scratch else a).cpu().numpy()
+    finally:
+        P.release3()
+        comm.close()
+    p = oracle.Problem3(n, h, lam, bc=BC_MAP[bc], nsweeps=6, norm_every=2,
+                        stencil=0 if st == P.PX_LAPLACE_7PT_3D else 1)
+    ref, rn = oracle.solve3(p, phi0, rho)
+    assert bits_equal(out, ref[1:-1, 1:-1, 1:-1]), ulp_diff(out, ref[1:-1, 1:-1, 1:-1])
+    _check_norms(res.norms, rn)
