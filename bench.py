@@ -301,7 +301,7 @@ def run_native3d(args):
     stream = torch.cuda.Stream(device=dev)
     stream.wait_stream(torch.cuda.current_stream(dev))
     prm = P.relax_params(h, lam, cfg["stencil"])
-    P.init_field3(grid, rho, 1, inputs.DEFAULT_SEED, stream=stream)
+    P.init_field3(grid, rho, 1, inputs.DEFAULT_SEED, stream=stream, z0=z0 if world > 1 else 0)
     if cfg["stencil"] == P.PX_MEHRSTELLEN_27PT_3D:  # f = ρ + S7(ρ)/12 (ρ ghosts by the BC rule)
         P.fill_ghosts3(grid, cfg["bc"], rho, stream=stream)
         f = grid.alloc(dev)
@@ -417,7 +417,7 @@ def run_native3d(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["desc"], "n": n, "sweeps_per_step": S, "norm_every": E, "ghost": 1,
                        "partition": f"z-slabs x{world}",
-                       "rho": cfg["rho"] if world == 1 else "hash of each rank's local cell index",
+                       "rho": cfg["rho"],
                        "h": h, "lambda": lam,
                        "steps_continue": "each step continues from the previous step's iterate",
                        "l2": "inputs (3 x %.2f GB) exceed L2; no flush" % (grid.alloc_elems * 8 / 1e9)},

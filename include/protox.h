@@ -402,8 +402,10 @@ px_status px3_layout(const int32_t n[3], int32_t ghost, int64_t* ld, int64_t* pl
  * the 2D norm-buffer protocol (buf[0] = max|r|, buf[1] = Σr²). */
 int64_t px3_norm_buffer_len(void);
 /* Synthetic field on the owned cells: kind 0 zeros, 1 the counter hash
- * u = splitmix64(seed ^ (x + n0·(y + n1·z))), ((u >> 11)·2^-53)·2 − 1. */
-px_status px3_init_field(px_patch3* p, int32_t kind, uint64_t seed, void* stream);
+ * u = splitmix64(seed ^ (x + n0·(y + n1·(z + z0)))), ((u >> 11)·2^-53)·2 − 1,
+ * z0 = the global index of the patch's first plane (a z-slab's px3_slab z0;
+ * 0 for a whole domain), so every decomposition gets the same field. */
+px_status px3_init_field(px_patch3* p, int32_t kind, uint64_t seed, int32_t z0, void* stream);
 /* 27-point variant (PX_MEHRSTELLEN_27PT_3D, R-3D4; not in the
  * paper -- the 3D counterpart of the BASELINE config-5 Mehrstellen stencil):
  * taps faces W,E,S,N,B,T (14), edges xy, xz, yz (3), corners z-major (1),

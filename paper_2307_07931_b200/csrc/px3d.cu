@@ -403,8 +403,10 @@ __device__ __forceinline__ uint64_t splitmix64_3(uint64_t x) {
 }
 
 // synthetic fields: kind 0 zero, 1 counter hash of the global cell index
-// x + n0 (y + n1 z) (the 2D recipe in 3D), owned cells only
-__global__ void k3_init(double* o, int64_t ld, int64_t plane, int n0, int n1, int n2, int kind, uint64_t seed) {
+// x + n0 (y + n1 (z + z0)) (the 2D recipe in 3D; z0 = the slab's first
+// global plane), owned cells only
+__global__ void k3_init(double* o, int64_t ld, int64_t plane, int n0, int n1, int n2, int kind, uint64_t seed,
+                        int z0) {
   const int64_t total = (int64_t)n0 * n1 * n2;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int x = (int)(i % n0);
@@ -412,7 +414,7 @@ __global__ void k3_init(double* o, int64_t ld, int64_t plane, int n0, int n1, in
     const int y = (int)(r % n1), z = (int)(r / n1);
     double v = 0.0;
     if (kind == 1) {
-      const uint64_t u = splitmix64_3(seed ^ (uint64_t)i);
+      const uint64_t u = splitmix64_3(seed ^ (uint64_t)(i + (int64_t)z0 * n0 * n1));
       v = ((double)(u >> 11) * 0x1p-53) * 2.0 - 1.0;
     }
     o[x + (int64_t)y * ld + (int64_t)z * plane] = v;
@@ -774,11 +776,13 @@ px_status px3_layout(const int32_t n[3], int32_t ghost, int64_t* ld, int64_t* pl
 
 int64_t px3_norm_buffer_len(void) { return 4 + 2 * (int64_t)k3::MAX_GRID; }
 
-px_status px3_init_field(px_patch3* p, int32_t kind, uint64_t seed, void* stream) {
+px_status px3_init_field(px_patch3* p, int32_t kind, uint64_t seed, int32_t z0, void* stream) {
   clear_error();
   PX_TRY(check3(p, "field"));
   if (kind != 0 && kind != 1) return fail(PX_ERR_ARG, "kind must be 0 (zero) or 1 (hash)");
-  k3_init<<<1024, 256, 0, (cudaStream_t)stream>>>(p->data, p->ld, p->plane, p->n[0], p->n[1], p->n[2], kind, seed);
+  if (z0 < 0) return fail(PX_ERR_ARG, "z0 must be >= 0");
+  k3_init<<<1024, 256, 0, (cudaStream_t)stream>>>(p->data, p->ld, p->plane, p->n[0], p->n[1], p->n[2], kind, seed,
+                                                  z0);
   count_launches(1);
   return cuda_check(cudaGetLastError(), "3D init launch");
 }

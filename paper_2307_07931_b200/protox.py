@@ -196,7 +196,7 @@ def lib():
     L.px3_layout.argtypes = [P(i32), i32, P(i64), P(i64), P(i64), P(i64)]
     L.px3_norm_buffer_len.restype = i64
     L.px3_init_field.restype = st
-    L.px3_init_field.argtypes = [P(px_patch3), i32, ctypes.c_uint64, vp]
+    L.px3_init_field.argtypes = [P(px_patch3), i32, ctypes.c_uint64, i32, vp]
     L.px3_fill_ghosts.restype = st
     L.px3_fill_ghosts.argtypes = [st, P(px_patch3), vp]
     L.px3_relax_step.restype = st
@@ -589,9 +589,10 @@ def norm_buffer3(device=None):
     return torch.zeros(lib().px3_norm_buffer_len(), dtype=torch.float64, device=device or "cuda")
 
 
-def init_field3(grid: Grid3, t, kind: int, seed: int = 0, stream=None):
+def init_field3(grid: Grid3, t, kind: int, seed: int = 0, stream=None, z0: int = 0):
+    """px3_init_field (z0: the global index of the patch's first plane)."""
     p = grid.patch(t)
-    _check(lib().px3_init_field(ctypes.byref(p), kind, seed, _stream(stream)))
+    _check(lib().px3_init_field(ctypes.byref(p), kind, seed, z0, _stream(stream)))
 
 
 def fill_ghosts3(grid: Grid3, bc: int, t, stream=None):

@@ -293,3 +293,16 @@ def test_solve3_comm_nccl_self_exchange(st, bc, graph, monkeypatch):
     ref, rn = oracle.solve3(p, phi0, rho)
     assert bits_equal(out, ref[1:-1, 1:-1, 1:-1]), ulp_diff(out, ref[1:-1, 1:-1, 1:-1])
     _check_norms(res.norms, rn)
+
+
+def test_init_field3_hash_slab_offset():
+    """A z-slab's hash field (z0 = its first global plane) is the matching
+    planes of the whole-domain field: every decomposition sees one ρ."""
+    n = (20, 9, 12)
+    full = inputs.hash_field3(*n)
+    for z0, z1 in (P.slab3(12, 3, r) for r in range(3)):
+        g = P.Grid3((n[0], n[1], z1 - z0), 1)
+        t = g.alloc()
+        P.init_field3(g, t, 1, inputs.DEFAULT_SEED, z0=z0)
+        torch.cuda.synchronize()
+        assert bits_equal(g.view(t).cpu().numpy(), full[z0:z1])
