@@ -532,7 +532,7 @@ static px_status same_shape3(const px_patch3& a, const px_patch3& b, const char*
   return PX_OK;
 }
 
-static bool pow2_ok(double h) { return h > 0.0 && std::isfinite(h); }
+static bool positive_finite(double h) { return h > 0.0 && std::isfinite(h); }
 
 template <int MODE, int NST, int ST>
 static cudaError_t k3_go(const CUtensorMap& mphi, const CUtensorMap& mrho, const Relax3& a, int g, int grid,
@@ -618,7 +618,7 @@ static px_status check_params3(const px_relax_params* p) {
   if (!p) return fail(PX_ERR_ARG, "null params");
   if (p->stencil != PX_LAPLACE_7PT_3D && p->stencil != PX_MEHRSTELLEN_27PT_3D)
     return fail(PX_ERR_UNSUPPORTED, "3D calls take stencil PX_LAPLACE_7PT_3D or PX_MEHRSTELLEN_27PT_3D");
-  if (!pow2_ok(p->h)) return fail(PX_ERR_ARG, "h must be positive and finite");
+  if (!positive_finite(p->h)) return fail(PX_ERR_ARG, "h must be positive and finite");
   return PX_OK;
 }
 
