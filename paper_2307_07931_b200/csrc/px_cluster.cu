@@ -6,20 +6,20 @@
 // keeps rows [c·ny/CL, (c+1)·ny/CL) of φ (two copies) and of the right-hand
 // side in its shared memory, plus one halo row above and below.  Per sweep
 // every CTA updates its rows (the oracle's expression tree, every operation
-// rounded -- bit-identical), sets the x ghost columns of its rows, and after
-// ONE cluster barrier (barrier.cluster arrive.release / wait.acquire) copies
-// its neighbours' new boundary rows straight out of their shared memory
-// (distributed shared memory, ld.shared::cluster through mapped addresses)
-// into its halo rows -- or derives them at a domain face (periodic: the ring
-// of CTAs; Dirichlet: odd reflection; fixed: kept).  No global-memory
+// rounded -- bit-identical) with their x ghost columns, pushes its first and
+// last new rows straight into its two neighbours' halo rows (distributed
+// shared memory stores through mapped addresses) and release-arrives on
+// their mbarriers (mbarrier.arrive.release.cluster on a mapa address); it
+// then waits only for its own two neighbours -- no cluster-wide barrier per
+// sweep.  Domain faces: periodic = the ring of CTAs; Dirichlet: odd
+// reflection; fixed: kept.  No global-memory
 // traffic inside the sweep loop.  Residual norms: per CTA in fixed order per
 // recorded sweep, kept in shared memory; at the end CTA 0 reduces every entry
 // over the CTAs in rank order through DSMEM.
 //
-// Buffer reuse: a CTA writes buffer X at sweeps s and s+2 and its neighbours
-// read X's boundary rows between the barrier of sweep s and their compute of
-// sweep s+1, which precedes the barrier of sweep s+1 -- so one cluster barrier
-// per sweep orders every read before the next write.
+// Buffer reuse: a neighbour pushes its sweep-s rows into our buffer (s+1)&1
+// after it received our sweep-(s-1) push, i.e. after we finished reading
+// that buffer in sweep s-1; the halo it fills is read in sweep s+1.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -60,6 +60,22 @@ __device__ __forceinline__ void cb_xghost(double* row, int nx, int bc) {
     row[0] = -row[1];
     row[nx + 1] = -row[nx];
   }
+}
+
+// release-arrive on the mbarrier at the same shared-memory offset in CTA `rank` of the cluster
+__device__ __forceinline__ void mb_arrive_remote(uint64_t* bar, int rank) {
+  uint32_t local = (uint32_t)__cvta_generic_to_shared(bar), remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+// wait (acquire at cluster scope) for the phase with parity `par` to complete
+__device__ __forceinline__ void mb_wait_cluster(uint64_t* bar, uint32_t par) {
+  asm volatile(
+      "{\n.reg .pred P1;\nW_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra W_%=;\n}\n" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
+      "r"(par)
+      : "memory");
 }
 
 template <int ST>
@@ -118,6 +134,20 @@ __global__ void __cluster_dims__(CB_CL, 1, 1) __launch_bounds__(CB_THREADS, 1) k
     }
     __syncthreads();
   };
+  // neighbour-to-neighbour halo barrier: one arrival per pushing neighbour
+  const bool has_up = !top_face || b.bc == PX_BC_PERIODIC, has_dn = !bot_face || b.bc == PX_BC_PERIODIC;
+  const int nexp = (has_up ? 1 : 0) + (has_dn ? 1 : 0);
+  // two barriers, alternating by sweep parity: a neighbour may run one sweep
+  // ahead (it depends on us, not on our other neighbour), so its next
+  // arrival must not count toward the phase we are still waiting for
+  __shared__ __align__(8) uint64_t hbar[2];
+  if (tid == 0 && nexp) {
+    for (int k = 0; k < 2; ++k)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(&hbar[k])),
+                   "r"(nexp)
+                   : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   // the given ghost ring may be stale for periodic / Dirichlet: re-derive it
   for (int r = 1 + tid; r <= R; r += nt) cb_xghost(bufs[0] + (size_t)r * P, nx, b.bc);
   __syncthreads();
@@ -160,10 +190,34 @@ __global__ void __cluster_dims__(CB_CL, 1, 1) __launch_bounds__(CB_THREADS, 1) k
         ++r;
       }
     }
-    if (rec) warp_partial(mx, ss, entry++);
-    // halo rows: copied with their ghost columns (set by their owner), or the
-    // negated own row at a Dirichlet face (product rule at the corners)
-    halo(cur ^ 1);
+    __syncthreads();  // the CTA's new rows (and their x ghosts) are complete
+    // halo rows, neighbour-to-neighbour: push the first / last new row (with
+    // its ghost columns) straight into the neighbours' halo rows of the same
+    // buffer (DSMEM stores), then release-arrive on their barriers; at a
+    // Dirichlet face the halo row is the negated own row (corners by the
+    // product rule); fixed faces keep theirs.  A neighbour is at least at
+    // the end of its sweep s-1 compute (it pushed to us before we started
+    // sweep s), so its copy of this buffer is no longer being read.
+    {
+      double* Bu = cluster.map_shared_rank(B, up);  // up's buffer: its last halo row R_up+1
+      double* Bd = cluster.map_shared_rank(B, dn);  // dn's buffer: its halo row 0
+      const int Ru = (up + 1) * ny / CB_CL - up * ny / CB_CL;
+      for (int x = tid; x < P; x += nt) {
+        if (has_up) Bu[(size_t)(Ru + 1) * P + x] = B[P + x];
+        else if (b.bc == PX_BC_DIRICHLET_CC) B[x] = -B[P + x];
+        if (has_dn) Bd[x] = B[(size_t)R * P + x];
+        else if (b.bc == PX_BC_DIRICHLET_CC) B[(size_t)(R + 1) * P + x] = -B[(size_t)R * P + x];
+      }
+      __syncthreads();
+      if (tid == 0) {
+        if (has_up) mb_arrive_remote(&hbar[s & 1], up);
+        if (has_dn) mb_arrive_remote(&hbar[s & 1], dn);
+      }
+      // the norm's warp reduction overlaps the neighbours' arrival latency
+      if (rec) warp_partial(mx, ss, entry++);
+      // both neighbours' rows of this sweep have arrived in our halo
+      if (nexp) mb_wait_cluster(&hbar[s & 1], (uint32_t)((s >> 1) & 1));
+    }
     cur ^= 1;
   }
   if (b.final_norm) {
