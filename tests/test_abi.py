@@ -158,3 +158,24 @@ def test_validation_rejects_bad_patches_before_any_launch():
 def test_norm_buffer_len_positive():
     assert P.norm_buffer_len(P.box(0, 0, 16383, 16383)) > 4
     assert P.norm_buffer_len(P.box(0, 0, 0, 0)) >= 6
+
+
+def test_px3_layout_and_slabs_host_only():
+    """3D host-side geometry without a GPU: the layout pitches (x origin at
+    element 16, 16-aligned rows) and the z-slab partitioner."""
+    g = P.Grid3((70, 37, 13), 1)
+    assert g.ld % 16 == 0 and g.ld >= 70 + 32
+    assert g.plane == g.ld * (37 + 2)
+    assert g.origin == 16 + g.ld + g.plane
+    assert g.alloc_elems == g.plane * (13 + 2)
+    for world in (1, 2, 3, 8):
+        spans = [P.slab3(512, world, r) for r in range(world)]
+        assert spans[0][0] == 0 and spans[-1][1] == 512
+        assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+        assert max(b - a for a, b in spans) - min(b - a for a, b in spans) <= 1
+    with pytest.raises(P.PxError, match="planes"):
+        P.slab3(2, 3, 0)
+    with pytest.raises(P.PxError):
+        P.slab3(16, 2, 2)
+    with pytest.raises(P.PxError):
+        P.Grid3((0, 4, 4), 1)
