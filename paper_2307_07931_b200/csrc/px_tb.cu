@@ -385,6 +385,9 @@ __global__ void __launch_bounds__(NW * 32 + 32, (NW == 7 ? 2 : 1))
 // ghost column / row is re-derived from the level's own interior by odd
 // reflection (corners by the product rule), so a pass of K levels is exactly
 // K plain sweeps with the ghost fill in between (oracle R5).
+#ifndef PX_TBW_SWZ
+#define PX_TBW_SWZ 0
+#endif
 namespace tbw {
 constexpr int NW = 7;
 constexpr int NST = 5;
@@ -412,10 +415,21 @@ struct Ctx {
   int xl, xh;        // DIR: position of column -1 / column nx in this lane (-1: none)
   bool ylo, yhi;     // DIR: reflecting y faces of the region
 };
+// A lane's four doubles sit 32 B after its left neighbour's, so two plain
+// 16-B loads put lanes k and k+4 on the same banks (8 wavefronts per load
+// instead of 4).  Lanes with bit 2 set fetch their upper half first: the
+// eight lanes of each quarter-warp then cover all eight 16-B bank groups.
 __device__ __forceinline__ Q4 lds4(const double* p) {
+#if PX_TBW_SWZ
+  const int sw = (threadIdx.x >> 1) & 2;  // 2 for lanes with bit 2 set
+  const double2 u = *reinterpret_cast<const double2*>(p + sw);
+  const double2 w = *reinterpret_cast<const double2*>(p + (2 - sw));
+  return sw ? Q4{{w.x, w.y, u.x, u.y}} : Q4{{u.x, u.y, w.x, w.y}};
+#else
   const double2 u = *reinterpret_cast<const double2*>(p);
   const double2 w = *reinterpret_cast<const double2*>(p + 2);
   return Q4{{u.x, u.y, w.x, w.y}};
+#endif
 }
 }  // namespace tbw
 
