@@ -236,7 +236,7 @@ def run_reference(args):
         print(json.dumps({
             "impl": "reference", "metric": METRIC, "value": total, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": cfg["desc"], "sample": sample},
             "cpu_baseline": {"value": total, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": total, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
