@@ -56,3 +56,21 @@ def test_reference_arm_torchrun_two_ranks():
     assert len(lines) == 1  # rank 0 only
     _check(lines[0])
     assert lines[0]["n_gpus"] == 2
+
+
+def test_native_arm_fails_loudly_without_gpu():
+    """The product path has no CPU fallback: with no GPU the native arm exits non-zero
+    and prints no bench line."""
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
+    p = subprocess.run([sys.executable, "bench.py", "--steps", "1", "--warmup", "3"], cwd=ROOT, env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert p.returncode != 0
+    assert _lines(p.stdout) == []
+
+
+def test_binding_raises_when_library_missing(monkeypatch):
+    from paper_2307_07931_b200 import protox as P
+    monkeypatch.setattr(P, "_lib", None)
+    monkeypatch.setattr(P, "LIB_PATH", os.path.join(ROOT, "no_such_dir", "libprotox.so"))
+    with pytest.raises(RuntimeError, match="not built"):
+        P.lib()
