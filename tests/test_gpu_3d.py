@@ -80,6 +80,37 @@ def test_solve3_norm_schedules_and_graph(E, graph):
         assert norms.shape[0] == 0
 
 
+@pytest.mark.parametrize("N,E", [(0, 1), (0, 0), (3, 5), (4, 4), (1, 1)])
+def test_solve3_zero_sweeps_and_sparse_norms(N, E):
+    """N = 0 returns φ⁰ untouched in φ (and the norm of φ⁰ when E >= 0); norm
+    periods longer than the solve report only the final sweep's norm."""
+    n = (40, 24, 5)
+    out, norms, ref, rn = run3(n, P.PX_BC_DIRICHLET_CC, N, E, seed=40 + N + E)
+    assert bits_equal(out, ref)
+    _check_norms(norms, rn)
+
+
+@pytest.mark.parametrize("N,E", [(0, 0), (4, 3), (6, -1)])
+def test_solve3_mehrstellen27_norm_schedules(N, E):
+    n = (48, 20, 6)
+    h = 1.0 / 48
+    lam = h * h / 12
+    phi0, rho = _fields(n, 1, 77 + N)
+    grid = P.Grid3(n, 1)
+    a, b, r = _upload(grid, phi0), grid.alloc(), _upload(grid, rho)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    res = P.solve3(grid, P.PX_BC_PERIODIC, P.relax_params(h, lam, P.PX_MEHRSTELLEN_27PT_3D), N, E, a, b, r,
+                   use_graph=False, stream=s)
+    out = grid.view(b if res.in_scratch else a).cpu().numpy()
+    ref, rn = oracle.solve3(oracle.Problem3(n, h, lam, nsweeps=N, norm_every=E, stencil=1), phi0, rho)
+    assert bits_equal(out, ref[1:-1, 1:-1, 1:-1])
+    if E < 0:
+        assert res.norms.shape[0] == 0
+    else:
+        _check_norms(res.norms, rn)
+
+
 def test_solve3_many_z_chunks_and_ghost2():
     """z extent large enough that the planner splits columns into several z
     chunks (each re-reads its first plane); ghost width 2; non-pow2 h."""
