@@ -449,6 +449,22 @@ px_status px3_slab(int32_t n2, int32_t nranks, int32_t rank, int32_t* z0, int32_
 px_status px3_solve_comm(px_comm* c, px_bc bc, const px_relax_params* p, const px_solve_opts* o, px_patch3* phi,
                          px_patch3* phi_scratch, const px_patch3* rhs, double* h_norms, int32_t cap,
                          int32_t* n_written, int32_t* in_scratch, void* stream);
+/* px3_solve for nprob independent problems given as HOST arrays -- the 3D
+ * counterpart of px_solve_host_batch.  Every array is a dense (n[2], n[1],
+ * n[0]) fp64 block of owned cells, x fastest; h_rho[i] is read, h_phi_out[i]
+ * (φ^N) written; h_phi0 NULL (or a NULL entry) = zero initial guess.  The
+ * library owns three device buffer sets (fields with `ghost` ghost layers,
+ * px3_layout pitches), each with its own cached plan / CUDA graph, so problem
+ * i's H2D and problem i-1's D2H (two internal copy streams) overlap problem
+ * i's solve on `stream` (required, non-default).  Norms: h_norms[i·2·cap + 2j
+ * + {0,1}] and n_written[i] as px3_solve.  bc PERIODIC or DIRICHLET_CC
+ * (host arrays carry no ghosts: PX_ERR_UNSUPPORTED for FIXED_GHOSTS).  Host
+ * buffers should be pinned for the copies to overlap.  Host-synchronous;
+ * px3_release frees the buffers. */
+px_status px3_solve_host_batch(px_bc bc, const px_relax_params* p, const px_solve_opts* o, const int32_t n[3],
+                               int32_t ghost, int32_t nprob, const double* const* h_phi0,
+                               const double* const* h_rho, double* const* h_phi_out, double* h_norms, int32_t cap,
+                               int32_t* n_written, void* stream);
 void px3_release(void);
 
 /* Diagnostics: number of kernel launches libprotox enqueued so far in this

@@ -950,7 +950,223 @@ px_status px3_solve_comm(px_comm* c, px_bc bc, const px_relax_params* p, const p
   return solve3_impl(c, bc, p, o, phi, phi_scratch, rhs, h_norms, cap, n_written, in_scratch, stream);
 }
 
-void px3_release(void) { g_plan3.reset(); }
+// ---------------------------------------------------------------- host batch
+// Three device buffer sets, each with its own cached plan (and graph): problem
+// i's H2D (s_in) and problem i-1's D2H (s_out) overlap problem i's solve.
+namespace {
+struct Batch3 {
+  static constexpr int NSET = 3;
+  int32_t n[3] = {0, 0, 0};
+  int32_t ghost = 0;
+  int64_t ld = 0, plane = 0, origin = 0, alloc = 0;
+  double* d[NSET][3] = {};
+  double* h_ring[NSET] = {};
+  int ne = 0;
+  std::unique_ptr<Plan3> plan[NSET];
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_in[NSET] = {}, ev_done[NSET] = {}, ev_free[NSET] = {};
+  void release_fields() {
+    for (auto& pl : plan) pl.reset();
+    for (auto& set : d)
+      for (auto& q : set) {
+        if (q) cudaFree(q);
+        q = nullptr;
+      }
+    for (auto& h : h_ring) {
+      if (h) cudaFreeHost(h);
+      h = nullptr;
+    }
+    alloc = 0;
+    ne = 0;
+  }
+  void release() {
+    release_fields();
+    if (s_in) cudaStreamDestroy(s_in);
+    if (s_out) cudaStreamDestroy(s_out);
+    s_in = s_out = nullptr;
+    auto destroy = [](cudaEvent_t& e) {
+      if (e) cudaEventDestroy(e);
+      e = nullptr;
+    };
+    destroy(ev_start);
+    for (int b = 0; b < NSET; ++b) {
+      destroy(ev_in[b]);
+      destroy(ev_done[b]);
+      destroy(ev_free[b]);
+    }
+  }
+  px_patch3 patch(int b, int k) const {
+    px_patch3 q;
+    q.data = d[b][k] + origin;
+    for (int i = 0; i < 3; ++i) q.n[i] = n[i];
+    q.ghost = ghost;
+    q.ld = ld;
+    q.plane = plane;
+    return q;
+  }
+};
+Batch3 g_batch3;
+
+// dense host (n2, n1, n0) <-> the owned cells of a padded device field
+cudaMemcpy3DParms copy3(const Batch3& B, double* dev_origin, double* host, bool h2d) {
+  cudaMemcpy3DParms c;
+  std::memset(&c, 0, sizeof c);
+  cudaPitchedPtr hp = make_cudaPitchedPtr(host, B.n[0] * sizeof(double), B.n[0] * sizeof(double), B.n[1]);
+  cudaPitchedPtr dp = make_cudaPitchedPtr(dev_origin, B.ld * sizeof(double), B.n[0] * sizeof(double),
+                                          B.n[1] + 2 * B.ghost);
+  c.srcPtr = h2d ? hp : dp;
+  c.dstPtr = h2d ? dp : hp;
+  c.extent = make_cudaExtent(B.n[0] * sizeof(double), B.n[1], B.n[2]);
+  c.kind = h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+  return c;
+}
+}  // namespace
+
+px_status px3_solve_host_batch(px_bc bc, const px_relax_params* p, const px_solve_opts* o, const int32_t n[3],
+                               int32_t ghost, int32_t nprob, const double* const* h_phi0,
+                               const double* const* h_rho, double* const* h_phi_out, double* h_norms, int32_t cap,
+                               int32_t* n_written, void* stream) {
+  clear_error();
+  if (!p || !o || !n || !h_rho || !h_phi_out) return fail(PX_ERR_ARG, "null argument");
+  PX_TRY(check_params3(p));
+  if (nprob < 0) return fail(PX_ERR_ARG, "nprob must be >= 0");
+  if (o->nsweeps < 0) return fail(PX_ERR_ARG, "nsweeps must be >= 0");
+  if (o->temporal_k > 1) return fail(PX_ERR_UNSUPPORTED, "3D temporal blocking not built");
+  if (bc != PX_BC_PERIODIC && bc != PX_BC_DIRICHLET_CC)
+    return fail(PX_ERR_UNSUPPORTED, "px3_solve_host_batch takes PERIODIC or DIRICHLET_CC (host arrays carry no ghosts)");
+  if (!stream) return fail(PX_ERR_ARG, "px3_solve_host_batch needs a non-default compute stream");
+  const int E = o->norm_every, N = o->nsweeps;
+  const int ne = E < 0 ? 0 : (E > 0 ? (N + E - 1) / E : 0) + 1;
+  if (ne > 0 && (!h_norms || cap < 1)) return fail(PX_ERR_ARG, "h_norms / cap required for norm entries");
+  for (int32_t i = 0; i < nprob; ++i)
+    if (!h_rho[i] || !h_phi_out[i]) return fail(PX_ERR_ARG, "null host buffer for problem %d", i);
+  int64_t ld, plane, origin, alloc;
+  PX_TRY(px3_layout(n, ghost, &ld, &plane, &origin, &alloc));
+  if (nprob == 0) return PX_OK;
+  Batch3& B = g_batch3;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!B.s_in) {
+    PX_TRY(cuda_check(cudaStreamCreateWithFlags(&B.s_in, cudaStreamNonBlocking), "stream"));
+    PX_TRY(cuda_check(cudaStreamCreateWithFlags(&B.s_out, cudaStreamNonBlocking), "stream"));
+    PX_TRY(cuda_check(cudaEventCreateWithFlags(&B.ev_start, cudaEventDisableTiming), "event"));
+    for (int b = 0; b < Batch3::NSET; ++b) {
+      PX_TRY(cuda_check(cudaEventCreateWithFlags(&B.ev_in[b], cudaEventDisableTiming), "event"));
+      PX_TRY(cuda_check(cudaEventCreateWithFlags(&B.ev_done[b], cudaEventDisableTiming), "event"));
+      PX_TRY(cuda_check(cudaEventCreateWithFlags(&B.ev_free[b], cudaEventDisableTiming), "event"));
+    }
+  }
+  if (B.alloc != alloc || B.ld != ld || B.ghost != ghost || std::memcmp(B.n, n, sizeof B.n) != 0 || B.ne < ne) {
+    PX_TRY(cuda_check(cudaDeviceSynchronize(), "sync before realloc"));
+    B.release_fields();
+    for (auto& set : B.d)
+      for (auto& q : set) {
+        PX_TRY(cuda_check(cudaMalloc(&q, alloc * sizeof(double)), "cudaMalloc"));
+        PX_TRY(cuda_check(cudaMemset(q, 0, alloc * sizeof(double)), "memset"));
+      }
+    B.ne = ne > 0 ? ne : 1;
+    for (auto& h : B.h_ring) PX_TRY(cuda_check(cudaMallocHost(&h, 2 * (size_t)B.ne * sizeof(double)), "cudaMallocHost"));
+    std::memcpy(B.n, n, sizeof B.n);
+    B.ghost = ghost;
+    B.ld = ld;
+    B.plane = plane;
+    B.origin = origin;
+    B.alloc = alloc;
+  }
+  // one plan (norm ring, workspace, graph) per buffer set
+  for (int b = 0; b < Batch3::NSET; ++b) {
+    const px_patch3 a = B.patch(b, 0), c = B.patch(b, 1), r = B.patch(b, 2);
+    if (B.plan[b] && same_key(*B.plan[b], nullptr, bc, *p, *o, a, c, r, s)) continue;
+    B.plan[b].reset(new Plan3());
+    Plan3& P = *B.plan[b];
+    P.bc = bc;
+    P.prm = *p;
+    P.opts = *o;
+    P.a = a;
+    P.b = c;
+    P.r = r;
+    P.s = s;
+    P.n_entries = ne;
+    PX_TRY(cuda_check(cudaMalloc(&P.d_ring, sizeof(double) * 2 * (ne > 0 ? ne : 1)), "norm ring"));
+    PX_TRY(cuda_check(cudaMalloc(&P.d_ws, sizeof(double) * (2 + 2 * k3::MAX_GRID)), "norm workspace"));
+    PX_TRY(cuda_check(cudaMemset(P.d_ws, 0, sizeof(double) * (2 + 2 * k3::MAX_GRID)), "norm workspace"));
+    if (o->use_graph) {
+      cudaGraph_t graph;
+      const int64_t before = px_kernel_launch_count();
+      PX_TRY(cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture"));
+      px_status st = enqueue_solve3(P);
+      cudaError_t ce = cudaStreamEndCapture(s, &graph);
+      P.launches_per_run = px_kernel_launch_count() - before;
+      count_launches(-P.launches_per_run);
+      if (st != PX_OK) return st;
+      PX_TRY(cuda_check(ce, "end capture"));
+      ce = cudaGraphInstantiate(&P.exec, graph, 0);
+      cudaGraphDestroy(graph);
+      PX_TRY(cuda_check(ce, "graph instantiate"));
+    }
+  }
+  PX_TRY(cuda_check(cudaEventRecord(B.ev_start, s), "event"));
+  PX_TRY(cuda_check(cudaStreamWaitEvent(B.s_in, B.ev_start, 0), "wait"));
+  PX_TRY(cuda_check(cudaStreamWaitEvent(B.s_out, B.ev_start, 0), "wait"));
+  bool pending[Batch3::NSET] = {};
+  int32_t pend_i[Batch3::NSET] = {};
+  auto harvest = [&](int b) -> px_status {
+    if (!pending[b]) return PX_OK;
+    PX_TRY(cuda_check(cudaEventSynchronize(B.ev_free[b]), "batch D2H"));
+    const int32_t i = pend_i[b];
+    const int32_t nw = ne < cap ? ne : cap;
+    for (int32_t j = 0; j < nw; ++j) {  // ring: max[ne] then sum[ne]
+      h_norms[(size_t)i * 2 * cap + 2 * j] = B.h_ring[b][j];
+      h_norms[(size_t)i * 2 * cap + 2 * j + 1] = B.h_ring[b][ne + j];
+    }
+    if (n_written) n_written[i] = nw;
+    pending[b] = false;
+    return PX_OK;
+  };
+  const bool odd = (N & 1) != 0;
+  for (int32_t i = 0; i < nprob; ++i) {
+    const int b = i % Batch3::NSET;
+    PX_TRY(harvest(b));  // problem i-NSET has left set b
+    Plan3& P = *B.plan[b];
+    // ---- copy in (s_in)
+    if (h_phi0 && h_phi0[i]) {
+      cudaMemcpy3DParms c = copy3(B, P.a.data, const_cast<double*>(h_phi0[i]), true);
+      PX_TRY(cuda_check(cudaMemcpy3DAsync(&c, B.s_in), "H2D phi"));
+    } else {
+      PX_TRY(cuda_check(cudaMemsetAsync(B.d[b][0], 0, alloc * sizeof(double), B.s_in), "zero phi"));
+    }
+    cudaMemcpy3DParms cr = copy3(B, P.r.data, const_cast<double*>(h_rho[i]), true);
+    PX_TRY(cuda_check(cudaMemcpy3DAsync(&cr, B.s_in), "H2D rho"));
+    PX_TRY(cuda_check(cudaEventRecord(B.ev_in[b], B.s_in), "event"));
+    // ---- solve (compute stream)
+    PX_TRY(cuda_check(cudaStreamWaitEvent(s, B.ev_in[b], 0), "wait"));
+    if (P.exec) {
+      PX_TRY(cuda_check(cudaGraphLaunch(P.exec, s), "graph launch"));
+      count_launches(P.launches_per_run);
+    } else {
+      PX_TRY(enqueue_solve3(P));
+    }
+    PX_TRY(cuda_check(cudaEventRecord(B.ev_done[b], s), "event"));
+    // ---- copy out (s_out)
+    PX_TRY(cuda_check(cudaStreamWaitEvent(B.s_out, B.ev_done[b], 0), "wait"));
+    cudaMemcpy3DParms co = copy3(B, odd ? P.b.data : P.a.data, h_phi_out[i], false);
+    PX_TRY(cuda_check(cudaMemcpy3DAsync(&co, B.s_out), "D2H phi"));
+    if (ne > 0)
+      PX_TRY(cuda_check(cudaMemcpyAsync(B.h_ring[b], P.d_ring, 2 * ne * sizeof(double), cudaMemcpyDeviceToHost,
+                                        B.s_out), "D2H norms"));
+    PX_TRY(cuda_check(cudaEventRecord(B.ev_free[b], B.s_out), "event"));
+    pending[b] = true;
+    pend_i[b] = i;
+  }
+  for (int b = 0; b < Batch3::NSET; ++b)
+    if (pending[b]) PX_TRY(cuda_check(cudaStreamWaitEvent(s, B.ev_free[b], 0), "wait"));
+  for (int b = 0; b < Batch3::NSET; ++b) PX_TRY(harvest(b));
+  return cuda_check(cudaStreamSynchronize(s), "px3_solve_host_batch");
+}
+
+void px3_release(void) {
+  g_plan3.reset();
+  g_batch3.release();
+}
 
 }  // extern "C"
 

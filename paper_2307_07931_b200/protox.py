@@ -101,7 +101,7 @@ EXPORTS = [
     "px_solve", "px_solve_host", "px_solve_host_batch", "px_release_cached", "px_mg_solve", "px_mg_release", "px_kernel_launch_count",
     "px_relax_variant", "px_stream_ceiling", "px_pointwise_update",
     "px3_layout", "px3_norm_buffer_len", "px3_init_field", "px3_fill_ghosts", "px3_relax_step",
-    "px3_residual_norm", "px3_solve", "px3_release", "px3_mehrstellen_rhs", "px3_slab", "px3_solve_comm",
+    "px3_residual_norm", "px3_solve", "px3_solve_host_batch", "px3_release", "px3_mehrstellen_rhs", "px3_slab", "px3_solve_comm",
 ]
 
 
@@ -206,6 +206,9 @@ def lib():
     L.px3_solve.restype = st
     L.px3_solve.argtypes = [st, P(px_relax_params), P(px_solve_opts), P(px_patch3), P(px_patch3), P(px_patch3),
                             P(ctypes.c_double), i32, P(i32), P(i32), vp]
+    L.px3_solve_host_batch.restype = st
+    L.px3_solve_host_batch.argtypes = [st, P(px_relax_params), P(px_solve_opts), P(i32), i32, i32, vp, vp, vp,
+                                       P(ctypes.c_double), i32, P(i32), vp]
     L.px3_release.restype = None
     L.px3_slab.restype = st
     L.px3_slab.argtypes = [i32, i32, i32, P(i32), P(i32)]
@@ -623,6 +626,43 @@ def solve3(grid: Grid3, bc: int, p: px_relax_params, nsweeps: int, norm_every: i
                            norms.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), max(cap, 1), ctypes.byref(nw),
                            ctypes.byref(ins) if keep_in_scratch else None, _stream(stream)))
     return SolveResult(norms[: nw.value].copy(), bool(ins.value))
+
+
+def solve3_host_batch(n, ghost: int, bc: int, p: px_relax_params, nsweeps: int, norm_every: int, rhos, outs,
+                      phi0s=None, use_graph: bool = True, stream=None):
+    """px3_solve_host_batch: len(rhos) independent 3D problems from host arrays
+    (dense (n2, n1, n0) float64; pinned torch CPU tensors via .numpy() for
+    overlap), copies overlapped with the solves.  phi0s None (or None entries)
+    = zero initial guess.  Returns the list of per-problem norm arrays."""
+    k = len(rhos)
+    if len(outs) != k or (phi0s is not None and len(phi0s) != k):
+        raise ValueError("rhos, outs and phi0s must have the same length")
+    shape = (n[2], n[1], n[0])
+    keep = [np.ascontiguousarray(r, dtype=np.float64) for r in rhos]
+    for a in keep + list(outs) + [q for q in (phi0s or []) if q is not None]:
+        if tuple(a.shape) != shape:
+            raise ValueError(f"host arrays must have shape {shape}")
+    for o in outs:
+        if not (o.flags.c_contiguous and o.dtype == np.float64):
+            raise ValueError("outs must be C-contiguous float64 arrays")
+    VP = ctypes.c_void_p * max(k, 1)
+    a_rho = VP(*[r.ctypes.data for r in keep])
+    a_out = VP(*[o.ctypes.data for o in outs])
+    a_phi = None
+    if phi0s is not None:
+        keep0 = [None if q is None else np.ascontiguousarray(q, dtype=np.float64) for q in phi0s]
+        a_phi = VP(*[None if q is None else q.ctypes.data for q in keep0])
+    cap = 0 if norm_every < 0 else ((nsweeps + norm_every - 1) // norm_every if norm_every > 0 else 0) + 1
+    norms = np.zeros((max(k, 1), max(cap, 1), 2), dtype=np.float64)
+    nw = (ctypes.c_int32 * max(k, 1))()
+    opts = px_solve_opts(nsweeps, norm_every, 1, int(use_graph))
+    nn = (ctypes.c_int32 * 3)(*n)
+    _check(lib().px3_solve_host_batch(bc, ctypes.byref(p), ctypes.byref(opts), nn, ghost, k,
+                                      ctypes.cast(a_phi, ctypes.c_void_p) if a_phi is not None else None,
+                                      ctypes.cast(a_rho, ctypes.c_void_p), ctypes.cast(a_out, ctypes.c_void_p),
+                                      norms.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), max(cap, 1), nw,
+                                      _stream(stream)))
+    return [norms[i, : nw[i]].copy() for i in range(k)]
 
 
 def mehrstellen_rhs3(grid: Grid3, rho, f, stream=None):

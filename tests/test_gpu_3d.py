@@ -337,3 +337,45 @@ def test_init_field3_hash_slab_offset():
         P.init_field3(g, t, 1, inputs.DEFAULT_SEED, z0=z0)
         torch.cuda.synchronize()
         assert bits_equal(g.view(t).cpu().numpy(), full[z0:z1])
+
+
+@pytest.mark.parametrize("st,bc,graph", [(P.PX_LAPLACE_7PT_3D, P.PX_BC_PERIODIC, True),
+                                         (P.PX_LAPLACE_7PT_3D, P.PX_BC_DIRICHLET_CC, False),
+                                         (P.PX_MEHRSTELLEN_27PT_3D, P.PX_BC_DIRICHLET_CC, True)])
+def test_solve3_host_batch_bitwise(st, bc, graph):
+    """px3_solve_host_batch: five problems (two with φ⁰ from the host, three from
+    zero) through the three rotating buffer sets, each bit-identical to its
+    own oracle solve; odd N (result in the scratch field)."""
+    n, N, E = (70, 37, 9), 5, 2
+    h = 1.0 / 70
+    lam = h * h / 12
+    probs = []
+    for i in range(5):
+        phi0, rho = _fields(n, 1, 500 + i)
+        if i % 2:
+            phi0 = np.zeros_like(phi0)
+        probs.append((phi0, rho))
+    outs = [torch.empty((n[2], n[1], n[0]), dtype=torch.float64).pin_memory().numpy() for _ in probs]
+    rhos = [np.ascontiguousarray(r[1:-1, 1:-1, 1:-1]) for _, r in probs]
+    phi0s = [None if i % 2 else np.ascontiguousarray(f[1:-1, 1:-1, 1:-1]) for i, (f, _) in enumerate(probs)]
+    torch.cuda.synchronize()
+    norms = P.solve3_host_batch(n, 1, bc, P.relax_params(h, lam, st), N, E, rhos, outs, phi0s, use_graph=graph,
+                                stream=torch.cuda.Stream())
+    for i, (phi0, rho) in enumerate(probs):
+        # the oracle starts from the same owned cells (its ghosts are refilled every sweep)
+        p = oracle.Problem3(n, h, lam, bc=BC_MAP[bc], nsweeps=N, norm_every=E,
+                            stencil=0 if st == P.PX_LAPLACE_7PT_3D else 1)
+        ref, rn = oracle.solve3(p, phi0, rho)
+        assert bits_equal(outs[i], ref[1:-1, 1:-1, 1:-1]), (i, ulp_diff(outs[i], ref[1:-1, 1:-1, 1:-1]))
+        _check_norms(norms[i], rn)
+
+
+def test_solve3_host_batch_rejects_fixed_ghosts_and_bad_shapes():
+    n = (8, 8, 4)
+    z = np.zeros((4, 8, 8))
+    prm = P.relax_params(1 / 8, 1 / 768, P.PX_LAPLACE_7PT_3D)
+    with pytest.raises(P.PxError):
+        P.solve3_host_batch(n, 1, P.PX_BC_FIXED_GHOSTS, prm, 2, 1, [z], [z.copy()], stream=torch.cuda.Stream())
+    with pytest.raises(ValueError):
+        P.solve3_host_batch(n, 1, P.PX_BC_PERIODIC, prm, 2, 1, [np.zeros((8, 8, 4))], [z.copy()],
+                            stream=torch.cuda.Stream())
