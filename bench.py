@@ -43,9 +43,11 @@ CONFIGS = {
                desc="BASELINE config 4: 2D Poisson 32768x32768 fp64, periodic, 5-point, 256x256-box "
                     "DisjointBoxLayout, temporal blocking k=4 sweeps per halo exchange (norm per exchange)"),
     "C2": dict(n=1024, box=1024, bc=0, stencil=0, sweeps=1000, norm_every=10, rho="hash",
+               solve_kernel="k_resident (iterate resident in shared memory, all sweeps in one launch)",
                desc="BASELINE config 2: 2D Poisson 1024x1024 single box, 1000 sweeps, "
                     "max-norm every 10 (L2-resident)"),
     "C1": dict(n=64, box=64, bc=1, stencil=0, sweeps=100, norm_every=1, rho="sine",
+               solve_kernel="k_cluster_box (whole solve on an 8-CTA cluster, DSMEM halos, one launch)",
                desc="BASELINE config 1: 64x64 box + 1 ghost layer, Dirichlet, 100 sweeps"),
     "C5": dict(n=8192, box=256, bc=1, stencil=1, sweeps=100, norm_every=1, rho="sine",
                desc="BASELINE config 5: 8192x8192 Mehrstellen 9-point, Dirichlet-CC"),
@@ -551,6 +553,7 @@ def run_native(args):
         evs[i][1].record(stream)
     stream.synchronize()
     k_ms = statistics.mean(a.elapsed_time(b) for a, b in evs[2:])
+    variant = P.relax_variant(qa, qb, pr, li.owned)
     local_cells = (li.owned.hi.c[0] - li.owned.lo.c[0] + 1) * (li.owned.hi.c[1] - li.owned.lo.c[1] + 1)
     achieved = BYTES_PER_CELL_UPDATE * local_cells / (k_ms * 1e-3) / 1e9
     peak, peak_src = load_peaks()
@@ -559,11 +562,23 @@ def run_native(args):
                 "frac": achieved / peak, "traffic": traffic,
                 "kernel": (f"k_tbw<5pt,K={tk}> (temporal blocking, skewed wavefront: one launch = {tk} sweeps, "
                            f"{BYTES_PER_CELL_UPDATE}/{tk} B per cell-update)") if tk > 1 else
-                          ("k_bulk<RELAX,5pt> (TMA bulk-copy pipeline)" if cfg["stencil"] == 0 else "k_bulk<RELAX,9pt>"),
+                          ("%s<RELAX,%s>%s" % ("k_bulk" if variant == 1 else "k_stream", "5pt" if cfg["stencil"] == 0
+                                               else "9pt", " (TMA bulk-copy pipeline)" if variant == 1 else
+                                               " (register-streaming LDG.128)")),
                 "kernel_ms": k_ms, "algorithmic_bytes_per_launch": BYTES_PER_CELL_UPDATE * local_cells,
                 "peak_source": peak_src, "whole_step_GBps": BYTES_PER_CELL_UPDATE * value}
     ceil = k12_ceiling(P, torch, dev, min(local_cells, 1 << 28), stream) if local_cells >= (1 << 22) else None
     roofline_extras(roofline, local_cells, ceil)
+    if cfg.get("solve_kernel") and world == 1 and tk == 1:
+        # small configs: px_solve runs the whole solve in one kernel whose iterate never
+        # leaves the chip, so the timed step is that kernel; the fields above describe
+        # a single k = 1 sweep launch for comparison with the large configs
+        per_step = launches / args.steps
+        roofline["solve_kernel"] = {
+            "name": cfg["solve_kernel"], "launches_per_step": per_step, "ms_per_step": t_ms / args.steps,
+            "us_per_sweep": 1e3 * t_ms / args.steps / S,
+            "bound": "latency (on-chip iterate: block barriers and neighbour handshakes per sweep)",
+            "equivalent_GBps_at_24B": BYTES_PER_CELL_UPDATE * value}
 
     # ---- end to end through the public host API (pinned host buffers; every
     # step's H2D of ρ and D2H of φ^N and its norms are inside the timed region).
