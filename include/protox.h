@@ -449,8 +449,8 @@ px_status px3_slab(int32_t n2, int32_t nranks, int32_t rank, int32_t* z0, int32_
 px_status px3_solve_comm(px_comm* c, px_bc bc, const px_relax_params* p, const px_solve_opts* o, px_patch3* phi,
                          px_patch3* phi_scratch, const px_patch3* rhs, double* h_norms, int32_t cap,
                          int32_t* n_written, int32_t* in_scratch, void* stream);
-/* px3_solve for nprob independent problems given as HOST arrays -- the 3D
- * counterpart of px_solve_host_batch.  Every array is a dense (n[2], n[1],
+/* px3_solve (figure `Proto`, per problem) for nprob independent
+ * problems given as HOST arrays -- the 3D counterpart of px_solve_host_batch.  Every array is a dense (n[2], n[1],
  * n[0]) fp64 block of owned cells, x fastest; h_rho[i] is read, h_phi_out[i]
  * (φ^N) written; h_phi0 NULL (or a NULL entry) = zero initial guess.  The
  * library owns three device buffer sets (fields with `ghost` ghost layers,
