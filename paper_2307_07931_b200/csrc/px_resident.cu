@@ -67,7 +67,8 @@ __device__ __forceinline__ double rs_taps(double w, double e, double s, double n
 // Rows rlo..rhi of the CTA's shared block: B = A + λ(scale·L(A) − F)
 // (WRITE), or residual norms of A only.  A thread walks a column pair down
 // the rows with the S/C rows (and their outer neighbours) in registers.
-template <int ST, bool WRITE>
+// NORM = false: a sweep whose norm is not recorded skips the accumulation.
+template <int ST, bool WRITE, bool NORM = true>
 __device__ __forceinline__ void rs_rows(const double* A, double* B, const double* F, int P, int nx, int rlo,
                                         int rhi, double scale, double lambda, unsigned long long& mx,
                                         double& ss) {
@@ -92,10 +93,12 @@ __device__ __forceinline__ void rs_rows(const double* A, double* B, const double
         o.y = __dadd_rn(C.y, __dmul_rn(lambda, r1));
         *reinterpret_cast<double2*>(B + (size_t)r * P + x) = o;
       }
-      mx = umax64(mx, (unsigned long long)__double_as_longlong(fabs(r0)));
-      ss = fma(r0, r0, ss);
-      mx = umax64(mx, (unsigned long long)__double_as_longlong(fabs(r1)));
-      ss = fma(r1, r1, ss);
+      if (NORM) {
+        mx = umax64(mx, (unsigned long long)__double_as_longlong(fabs(r0)));
+        ss = fma(r0, r0, ss);
+        mx = umax64(mx, (unsigned long long)__double_as_longlong(fabs(r1)));
+        ss = fma(r1, r1, ss);
+      }
       S = C;
       sw = cw;
       se = ce;
@@ -182,8 +185,12 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resident(const ResidentLaunch
     double ss = 0.0;
     // the first and last rows first: they go to the neighbours, whose copy
     // overlaps the sweep of the inner rows
-    rs_rows<ST, true>(A, B, F, P, nx, 1, 1, p.scale, p.lambda, mx, ss);
-    if (R > 1) rs_rows<ST, true>(A, B, F, P, nx, R, R, p.scale, p.lambda, mx, ss);
+    auto sweep = [&](int lo, int hi) {
+      if (rec) rs_rows<ST, true, true>(A, B, F, P, nx, lo, hi, p.scale, p.lambda, mx, ss);
+      else rs_rows<ST, true, false>(A, B, F, P, nx, lo, hi, p.scale, p.lambda, mx, ss);
+    };
+    sweep(1, 1);
+    if (R > 1) sweep(R, R);
     __syncthreads();
     const int slot = (s + 1) & 1;
     double* mine = pub + (size_t)(slot * G + c) * 2 * nx;
@@ -195,7 +202,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resident(const ResidentLaunch
     // release at gpu scope: the CTA's row stores (ordered before it by the
     // barrier) are visible to whoever acquires the flag
     if (tid == 0) st_release(flags + c, (unsigned long long)(s + 1));
-    if (R > 2) rs_rows<ST, true>(A, B, F, P, nx, 2, R - 1, p.scale, p.lambda, mx, ss);
+    if (R > 2) sweep(2, R - 1);
     if (rec) {
       rs_block_reduce(mx, ss, part + ((size_t)entry * G + c) * 2);
       ++entry;
