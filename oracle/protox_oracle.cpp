@@ -292,7 +292,7 @@ static void gather_global(const Level& lev, double* glob) {
   }
 }
 
-/* Neumaier-compensated sum accumulator (reading R26). */
+/* Neumaier-compensated sum accumulator (reading R26; non-finite sums: R6). */
 struct Neumaier {
   double s = 0.0, c = 0.0;
   void add(double x) {
@@ -303,7 +303,11 @@ struct Neumaier {
       c += (x - t) + s;
     s = t;
   }
-  double value() const { return s + c; }
+  // The compensation only refines a finite sum.  With an infinite term the
+  // plain running sum is +inf (every term r*r >= 0) or NaN (a NaN term), and
+  // that is the value of the sum (reading R6: Σr² is the plain sum of the
+  // squares); (s - t) would turn inf into a spurious NaN in c.
+  double value() const { return std::isfinite(s) ? s + c : s; }
 };
 
 /* computeMaxResidualAcrossProcs and Eq.7:

@@ -249,7 +249,11 @@ struct Neumaier3 {
       c += (x - t) + s;
     s = t;
   }
-  double value() const { return s + c; }
+  // The compensation only refines a finite sum.  With an infinite term the
+  // plain running sum is +inf (every term r*r >= 0) or NaN (a NaN term), and
+  // that is the value of the sum (reading R6: Σr² is the plain sum of the
+  // squares); (s - t) would turn inf into a spurious NaN in c.
+  double value() const { return std::isfinite(s) ? s + c : s; }
 };
 
 /* Eq.7: exchange, r = scale*S(φ) − ρ over every interior point, max |r|

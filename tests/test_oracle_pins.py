@@ -532,6 +532,25 @@ def test_max_norm_propagates_nan():
     assert math.isnan(r[0])
 
 
+def test_norms_of_infinite_residual():
+    """Σr² is the plain sum of the squares (reading R6): one r = ±inf makes it
+    +inf (every term is >= 0), not the NaN a compensation term (inf - inf)
+    would produce; max|r| is inf.  A NaN term makes both NaN.  The rest of the
+    field is finite, so only the definition fixes these values."""
+    n = 8
+    p = Problem(n, n, 1.0 / n, 0.0, bc=BC_PERIODIC)
+    phi = np.random.default_rng(3).uniform(-1, 1, (n, n))
+    rho = np.ones((n, n))
+    rho[2, 5] = np.inf
+    m, s = oracle.residual(p, oracle.ghosted(p, phi), oracle.ghosted(p, rho))
+    assert m == np.inf and s == np.inf
+    rho[6, 1] = np.nan
+    m, s = oracle.residual(p, oracle.ghosted(p, phi), oracle.ghosted(p, rho))
+    assert math.isnan(m) and math.isnan(s)
+    assert oracle.neumaier_sum(np.array([1.0, np.inf, 2.0])) == np.inf
+    assert math.isnan(oracle.neumaier_sum(np.array([1.0, np.inf, np.nan])))
+
+
 def test_fault_injection_sign_flip_breaks_spectral_pin():
     """SPEC S:447 idea: a flipped λ sign must fail the closed-form check."""
     n, N = 16, 20

@@ -255,6 +255,17 @@ def test_nan_propagates():
     assert math.isnan(norms[0, 0]) and math.isnan(norms[-1, 0])
 
 
+def test_infinite_residual_sum_is_inf():
+    """Reading R6: Σr² is the plain sum of squares -- +inf with one infinite
+    residual (not the NaN an inf - inf compensation term would give)."""
+    n = (4, 4, 4)
+    p = oracle.Problem3(n, 0.25, 0.25**2 / 12, nsweeps=0, norm_every=1)
+    phi0, rho = _rand(p, 3)
+    rho[2, 2, 2] = np.inf
+    _, norms = oracle.solve3(p, phi0, rho)
+    assert norms[0, 0] == np.inf and norms[0, 1] == np.inf
+
+
 # ------------------------------------------------------- 27-point Mehrstellen (R-3D4)
 def test_mehrstellen27_exact_on_integer_quadratics():
     n = (6, 5, 7)
