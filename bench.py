@@ -456,8 +456,6 @@ def run_native(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus and world > 1:
-        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -666,8 +664,50 @@ def run_native(args):
     return 0
 
 
+def free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def ensure_ranks(args):
+    """One process per GPU.  Under torchrun WORLD_SIZE must equal --gpus.
+    Outside torchrun, --gpus N > 1 re-launches this script under
+    torch.distributed.run with N ranks (127.0.0.1) and returns its exit code,
+    so a scaling run can never silently measure one rank; the native arm
+    refuses (exit 2) when fewer than N GPUs are visible.  Returns None when the
+    current process should run the benchmark itself."""
+    world = os.environ.get("WORLD_SIZE")
+    if world is not None:
+        if int(world) != args.gpus:
+            sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}\n")
+            return 2
+        return None
+    if args.gpus <= 1:
+        return None
+    if args.impl == "native":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            sys.stderr.write(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}; "
+                             "refusing to measure fewer ranks\n")
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    sys.stderr.write("bench.py: launching %d ranks: %s\n" % (args.gpus, " ".join(cmd)))
+    sys.stderr.flush()
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    rc = ensure_ranks(args)
+    if rc is not None:
+        return rc
     if args.impl == "reference":
         return run_reference(args)
     if CONFIGS[args.config].get("dims") == 3:

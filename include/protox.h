@@ -247,7 +247,12 @@ px_status px_comm_create(const uint8_t id[128], int32_t nranks, int32_t rank, in
                          px_comm** out);
 void px_comm_destroy(px_comm* c);
 /* Global all-reduce of n residual norms in device memory: d_max[i] by max,
- * d_sum[i] by sum (computeMaxResidualAcrossProcs). */
+ * d_sum[i] by sum (computeMaxResidualAcrossProcs).  d_max must hold
+ * non-negative values (|r|, NaN with the sign bit clear): the max is taken
+ * over their IEEE-754 bit patterns as uint64 (ncclUint64, ncclMax), which
+ * orders non-negative doubles exactly and puts NaN above +inf, so a NaN on
+ * any rank makes the global max NaN (reading R7; ncclMax on ncclDouble
+ * gives no NaN guarantee).  Σr² is summed as doubles (NaN propagates). */
 px_status px_comm_allreduce_norms(px_comm* c, double* d_max, double* d_sum, int32_t n,
                                   void* stream);
 
@@ -470,6 +475,13 @@ void px3_release(void);
 /* Diagnostics: number of kernel launches libprotox enqueued so far in this
  * process (graph replays count their kernel nodes). */
 int64_t px_kernel_launch_count(void);
+/* Diagnostics: the sweep kernels the calling thread's last px_solve (or
+ * px_solve_host / px_solve_host_batch) enqueued, '+'-separated in launch
+ * order, e.g. "k_bulk", "k_stream+k_bulk" (boundary rows + interior),
+ * "k_tbw", "k_resident", "k_persist", "k_cluster_box", "k_smallbox".  The
+ * string is library-owned and valid until the thread's next solve; "" before
+ * the first. */
+const char* px_last_solve_kernels(void);
 /* Diagnostics: which relax kernel a px_relax_step over `region` would run:
  * 1 = TMA bulk-copy pipeline (16-byte aligned region start, even width,
  * >= 4M cells), 0 = register-streaming LDG.128 kernel, <0 = invalid args.

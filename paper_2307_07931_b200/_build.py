@@ -36,23 +36,54 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every source to an object in parallel (one nvcc per file), then
+    link libprotox.so.  Objects go to a per-process temp dir; nothing is cached
+    between builds except the finished library."""
     if not force and not needs_build():
         return LIB
+    import concurrent.futures as cf
+    import shutil
+    import tempfile
     nccl = nccl_dir()
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = ["nvcc", "-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC", "-shared",
-           "-Xptxas", "-v", f"-I{INCLUDE}", f"-I{CSRC}", f"-I{nccl}/include", *sources(),
-           f"-L{nccl}/lib", "-l:libnccl.so.2", f"-Xlinker=-rpath,{nccl}/lib", "-o", tmp]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    common = ["nvcc", "-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC",
+              f"-I{INCLUDE}", f"-I{CSRC}", f"-I{nccl}/include"]
+    odir = tempfile.mkdtemp(prefix="protox_build_")
     log = os.path.join(PKG, "build.log")
-    with open(log, "w") as f:
-        f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
-    if r.returncode != 0:
-        sys.stderr.write(r.stderr[-6000:])
-        raise RuntimeError(f"nvcc failed (see {log})")
-    os.replace(tmp, LIB)
+    try:
+        def compile_one(src):
+            obj = os.path.join(odir, os.path.basename(src) + ".o")
+            cmd = [*common, "-Xptxas", "-v", "-c", src, "-o", obj]
+            r = subprocess.run(cmd, capture_output=True, text=True)
+            return src, obj, cmd, r
+        srcs = sources()
+        with cf.ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
+            results = list(ex.map(compile_one, srcs))
+        text = []
+        failed = []
+        for src, obj, cmd, r in results:
+            text.append(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+            if r.returncode != 0:
+                failed.append((src, r.stderr))
+        if not failed:
+            tmp = LIB + f".tmp{os.getpid()}"
+            cmd = ["nvcc", *ARCH, "-shared", *[o for _, o, _, _ in results], f"-L{nccl}/lib", "-l:libnccl.so.2",
+                   f"-Xlinker=-rpath,{nccl}/lib", "-o", tmp]
+            r = subprocess.run(cmd, capture_output=True, text=True)
+            text.append(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+            if r.returncode != 0:
+                failed.append(("link", r.stderr))
+        with open(log, "w") as f:
+            f.write("\n".join(text))
+        if failed:
+            for src, err in failed:
+                sys.stderr.write(f"--- {src}\n{err[-6000:]}\n")
+            raise RuntimeError(f"nvcc failed (see {log})")
+        os.replace(tmp, LIB)
+    finally:
+        shutil.rmtree(odir, ignore_errors=True)
     if verbose:
-        print(r.stderr)
+        with open(log) as f:
+            print(f.read())
     return LIB
 
 

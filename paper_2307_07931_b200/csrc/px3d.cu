@@ -747,7 +747,8 @@ static px_status enqueue_solve3(Plan3& P) {
     const int ne = P.n_entries;
     ncclComm_t nc = (ncclComm_t)comm_nccl(P.comm);
     PX_TRY(nccl3(ncclGroupStart(), "ncclGroupStart"));
-    PX_TRY(nccl3(ncclAllReduce(P.d_ring, P.d_ring, ne, ncclDouble, ncclMax, nc, P.s), "ncclAllReduce max"));
+    // max|r| as u64 bit patterns (non-negative doubles: exact, NaN-propagating, R7)
+    PX_TRY(nccl3(ncclAllReduce(P.d_ring, P.d_ring, ne, ncclUint64, ncclMax, nc, P.s), "ncclAllReduce max"));
     PX_TRY(nccl3(ncclAllReduce(P.d_ring + ne, P.d_ring + ne, ne, ncclDouble, ncclSum, nc, P.s), "ncclAllReduce sum"));
     PX_TRY(nccl3(ncclGroupEnd(), "ncclGroupEnd"));
   }
@@ -908,7 +909,7 @@ static px_status solve3_impl(px_comm* comm, px_bc bc, const px_relax_params* p, 
     h_norms[2 * j] = ring[j];
     h_norms[2 * j + 1] = ring[n_entries + j];
   }
-  if (n_written) *n_written = n_entries;
+  if (n_written) *n_written = nw;
   const bool odd = (N & 1) != 0;
   if (in_scratch) {
     *in_scratch = odd ? 1 : 0;

@@ -467,6 +467,7 @@ px_status launch_bulk(int mode, int stencil, const StreamLaunch& a, cudaStream_t
     case MODE_RESID * 2 + 1: e = launch_cfg<MODE_RESID, 1>(a, s); break;
     default: return fail(PX_ERR_ARG, "bulk kernel: bad mode");
   }
+  if (mode == MODE_RELAX) note_kernel("k_bulk");
   count_launches(1);
   return cuda_check(e, "bulk relax kernel launch");
 }

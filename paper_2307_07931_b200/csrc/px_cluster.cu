@@ -263,23 +263,34 @@ __global__ void __cluster_dims__(CB_CL, 1, 1) __launch_bounds__(CB_THREADS, 1) k
   cluster.sync();  // no CTA leaves while CTA 0 may still read its partials
 }
 
-bool cluster_box_eligible(int nx, int ny) {
+static int cluster_box_entries(const SmallBox& b) {
+  const int n_entries = (b.every > 0 ? (b.nsweeps + b.every - 1) / b.every : 0) + (b.final_norm ? 1 : 0);
+  return n_entries > 0 ? n_entries : 1;
+}
+
+// dynamic shared memory of k_cluster_box: two row buffers with halo rows, the
+// CTA's rhs rows, and the per-warp norm partials of every recorded entry
+static size_t cluster_box_smem(int nx, int ny, int ne) {
+  const int rmax = (ny + CB_CL - 1) / CB_CL;
+  return ((size_t)2 * (rmax + 2) * (nx + 2) + (size_t)rmax * nx) * sizeof(double) +
+         (size_t)ne * (CB_THREADS / 32) * (sizeof(unsigned long long) + sizeof(double));
+}
+
+bool cluster_box_eligible(const SmallBox& b) {
   static int en = -1;
   if (en < 0) {
     const char* e = getenv("PROTOX_SMALLBOX_CLUSTER");
     en = (e && e[0] == '0') ? 0 : 1;
   }
-  if (!en || nx < 1 || ny < 2 * CB_CL) return false;
-  const int rmax = (ny + CB_CL - 1) / CB_CL;
-  return ((size_t)2 * (rmax + 2) * (nx + 2) + (size_t)rmax * nx) * sizeof(double) + 4096 <= 160 * 1024;
+  if (!en || b.nx < 1 || b.ny < 2 * CB_CL) return false;
+  // the norm partials of every recorded entry live in shared memory too: a
+  // long solve with many recorded norms falls back to k_smallbox (global ring)
+  return cluster_box_smem(b.nx, b.ny, cluster_box_entries(b)) <= 200 * 1024;
 }
 
 px_status launch_cluster_box(const SmallBox& b, cudaStream_t s) {
-  const int n_entries = (b.every > 0 ? (b.nsweeps + b.every - 1) / b.every : 0) + (b.final_norm ? 1 : 0);
-  const int ne = n_entries > 0 ? n_entries : 1;
-  const int rmax = (b.ny + CB_CL - 1) / CB_CL;
-  const size_t smem = ((size_t)2 * (rmax + 2) * (b.nx + 2) + (size_t)rmax * b.nx) * sizeof(double) +
-                      (size_t)ne * (CB_THREADS / 32) * (sizeof(unsigned long long) + sizeof(double));
+  const int ne = cluster_box_entries(b);
+  const size_t smem = cluster_box_smem(b.nx, b.ny, ne);
   if (smem > 200 * 1024) return fail(PX_ERR_UNSUPPORTED, "cluster box too large");
   cudaError_t e;
   if (b.stencil == 0) {
@@ -297,6 +308,7 @@ px_status launch_cluster_box(const SmallBox& b, cudaStream_t s) {
     }
     k_cluster_box<1><<<CB_CL, CB_THREADS, smem, s>>>(b, ne);
   }
+  note_kernel("k_cluster_box");
   e = cudaGetLastError();
   count_launches(1);
   return cuda_check(e, "cluster box kernel launch");

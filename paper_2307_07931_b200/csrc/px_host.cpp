@@ -147,7 +147,11 @@ px_status px_layout_create(px_box domain, px_point box_size, int32_t ghost, px_b
   return PX_OK;
 }
 
-void px_layout_destroy(px_layout* l) { delete l; }
+void px_layout_destroy(px_layout* l) {
+  if (!l) return;
+  px::drop_layout_plans(l->gen);  // cached solve plans built for this layout
+  delete l;
+}
 
 px_status px_layout_num_boxes(const px_layout* l, int32_t* n) {
   if (!l || !n) return fail(PX_ERR_ARG, "null argument");

@@ -4,8 +4,10 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -96,13 +98,13 @@ struct NormSlot {
 // boundary-row launch also stores its cells (and their x images) into the
 // neighbour's ghost rows and then bumps the neighbour's arrival counter; a
 // launch that reads ghost rows first waits until its own arrival counter
-// reaches the expected count (epoch-based, so counters never reset).
+// reaches base + the count expected within this solve (counters never reset;
+// the base advances by each solve's own arrivals, so solves may differ in N).
 struct RemoteSpec {
   double* rdst;                    // neighbour cell matching region.lo (null: no push)
   unsigned long long* rflag;       // neighbour's arrival counter to bump
   unsigned long long* wflag;       // own arrival counter to wait on (null: no wait)
-  const unsigned long long* epoch; // own solve epoch (1 for the first solve)
-  unsigned long long per_epoch;    // arrivals per solve
+  const unsigned long long* epoch; // own arrival base (arrivals of all earlier solves)
   unsigned long long wcount;       // arrivals needed within this solve
 };
 
@@ -147,7 +149,7 @@ struct SmallBox {
 };
 bool smallbox_fits(int nx, int ny);
 // the same solve on a cluster of 8 CTAs with DSMEM halo exchange (px_cluster.cu)
-bool cluster_box_eligible(int nx, int ny);
+bool cluster_box_eligible(const SmallBox& b);  // incl. its norm partials
 px_status launch_cluster_box(const SmallBox& b, cudaStream_t s);
 
 // All sweeps of a single-rank solve in one cooperative launch (px_kernels.cu).
@@ -187,7 +189,7 @@ px_status launch_resident(int stencil, const ResidentLaunch& r, int grid, size_t
 int32_t stream_launch_blocks_ldg(const StreamLaunch& a);
 px_status launch_stream_ldg(int mode, int stencil, const StreamLaunch& a, cudaStream_t s);
 px_status launch_wait(const RemoteSpec& rs, cudaStream_t s);
-px_status launch_epoch_bump(unsigned long long* epoch, cudaStream_t s);
+px_status launch_epoch_bump(unsigned long long* epoch, unsigned long long per_solve, cudaStream_t s);
 int32_t persist_grid();
 px_status launch_persist(int stencil, const PersistLaunch& p, int grid, cudaStream_t s);
 px_status launch_smallbox(const SmallBox& b, cudaStream_t s);
@@ -213,6 +215,30 @@ px_status launch_init_field(const px_layout* l, int32_t rank, const px_patch& p,
                             uint64_t seed, int k, int lw, cudaStream_t s);
 px_status cuda_check(cudaError_t e, const char* what);
 void count_launches(int64_t n);
+// sweep-kernel names of the current solve (px_last_solve_kernels)
+void note_kernel(const char* name);
+std::string take_noted_kernels();
+
+// ---- bounded plan caches (px_solve, px_mg_solve) --------------------------
+// A cached plan owns device workspace, events and a CUDA graph exec.  The
+// caches keep the most recently used plans only (PROTOX_PLAN_CACHE, default
+// 32); a plan is also dropped when its layout is destroyed.
+int plan_cache_cap();
+// Move `p` to the most-recently-used end of `v` and evict the least recently
+// used plans beyond the cap (after a device synchronisation: an evicted plan's
+// graph may still be in flight).
+template <class T>
+void plan_touch(std::vector<std::unique_ptr<T>>& v, T* p) {
+  auto it = std::find_if(v.begin(), v.end(), [p](const std::unique_ptr<T>& q) { return q.get() == p; });
+  if (it != v.end() && it + 1 != v.end()) std::rotate(it, it + 1, v.end());
+  const size_t cap = (size_t)plan_cache_cap();
+  if (v.size() > cap) {
+    cudaDeviceSynchronize();
+    v.erase(v.begin(), v.begin() + (v.size() - cap));
+  }
+}
+void drop_layout_plans(uint64_t layout_gen);     // px_solve.cu (all caches)
+void mg_drop_layout_plans(uint64_t layout_gen);  // px_mg.cu
 
 // communicator accessors (px_solve.cu) for the 3D slab solve (px3d.cu)
 void* comm_nccl(const px_comm* c);  // ncclComm_t

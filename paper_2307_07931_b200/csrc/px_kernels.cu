@@ -150,9 +150,10 @@ __device__ __forceinline__ void taps(const Fin& S, const Fin& C, const Fin& N, d
 }
 
 // ------------------------------------------------------- the stream kernel
-// Spin until *flag >= (epoch-1)*per_epoch + count (system-scope acquire).
+// Spin until *flag >= base + count (system-scope acquire); base = the
+// neighbour's arrivals of all earlier solves (advanced by k_epoch_bump).
 __device__ __forceinline__ void rs_wait(const RemoteSpec& rs) {
-  const unsigned long long target = (*rs.epoch - 1ull) * rs.per_epoch + rs.wcount;
+  const unsigned long long target = *rs.epoch + rs.wcount;
   unsigned long long v;
   do {
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(rs.wflag) : "memory");
@@ -400,6 +401,19 @@ __global__ void __launch_bounds__(SW_THREADS, 2) k_persist(const PersistLaunch p
 static int64_t g_launches = 0;
 void count_launches(int64_t n) { g_launches += n; }
 
+// names of the sweep kernels enqueued since the last take (px_last_solve_kernels)
+static thread_local std::string tl_kernels;
+void note_kernel(const char* name) {
+  if (tl_kernels.find(name) != std::string::npos) return;
+  if (!tl_kernels.empty()) tl_kernels += "+";
+  tl_kernels += name;
+}
+std::string take_noted_kernels() {
+  std::string s;
+  s.swap(tl_kernels);
+  return s;
+}
+
 px_status cuda_check(cudaError_t e, const char* what) {
   if (e == cudaSuccess) return PX_OK;
   return fail(PX_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
@@ -419,7 +433,12 @@ px_status launch_stream(int mode, int stencil, const StreamLaunch& a, cudaStream
 int32_t stream_launch_blocks_ldg(const StreamLaunch& a) { return ldg_blocks(a.nx, a.ny, a.phase); }
 
 __global__ void k_wait(const RemoteSpec rs) { rs_wait(rs); }
-__global__ void k_epoch_bump(unsigned long long* e) { *e += 1ull; }
+// e[0] = arrival base of this solve, e[1] = arrivals per side of the previous
+// solve: every solve adds its own count, so solves of different lengths mix.
+__global__ void k_epoch_bump(unsigned long long* e, unsigned long long per_solve) {
+  e[0] += e[1];
+  e[1] = per_solve;
+}
 
 px_status launch_wait(const RemoteSpec& rs, cudaStream_t s) {
   k_wait<<<1, 1, 0, s>>>(rs);
@@ -427,8 +446,8 @@ px_status launch_wait(const RemoteSpec& rs, cudaStream_t s) {
   return cuda_check(cudaGetLastError(), "wait kernel launch");
 }
 
-px_status launch_epoch_bump(unsigned long long* epoch, cudaStream_t s) {
-  k_epoch_bump<<<1, 1, 0, s>>>(epoch);
+px_status launch_epoch_bump(unsigned long long* epoch, unsigned long long per_solve, cudaStream_t s) {
+  k_epoch_bump<<<1, 1, 0, s>>>(epoch, per_solve);
   count_launches(1);
   return cuda_check(cudaGetLastError(), "epoch kernel launch");
 }
@@ -448,6 +467,7 @@ px_status launch_stream_ldg(int mode, int stencil, const StreamLaunch& a, cudaSt
     case MODE_MRHS * 2 + 0: launch_t<MODE_MRHS, 0>(a, grid, s); break;
     default: return fail(PX_ERR_ARG, "bad stream mode %d / stencil %d", mode, stencil);
   }
+  if (mode == MODE_RELAX) note_kernel("k_stream");
   count_launches(1);
   return cuda_check(cudaGetLastError(), "stream kernel launch");
 }
@@ -488,6 +508,7 @@ px_status launch_persist(int stencil, const PersistLaunch& p, int grid, cudaStre
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaError_t e = stencil ? cudaLaunchKernelEx(&cfg, k_persist<1>, p) : cudaLaunchKernelEx(&cfg, k_persist<0>, p);
+  note_kernel("k_persist");
   if (e == cudaSuccess) e = cudaGetLastError();
   count_launches(1);
   return cuda_check(e, "persistent solve kernel launch");

@@ -103,10 +103,13 @@ struct MgKey {
   double h, lambda;
   px_mg_opts o;
   const double *phi, *scr, *rhs;
+  px_box rbox;       // rhs patch geometry (offsets baked into the captured launches)
+  int64_t rld;
   cudaStream_t s;
   bool operator==(const MgKey& k) const {
     return gen == k.gen && stencil == k.stencil && h == k.h && lambda == k.lambda &&
-           std::memcmp(&o, &k.o, sizeof o) == 0 && phi == k.phi && scr == k.scr && rhs == k.rhs && s == k.s;
+           std::memcmp(&o, &k.o, sizeof o) == 0 && phi == k.phi && scr == k.scr && rhs == k.rhs &&
+           std::memcmp(&rbox, &k.rbox, sizeof rbox) == 0 && rld == k.rld && s == k.s;
   }
 };
 
@@ -266,6 +269,15 @@ px_status mg_enqueue(MgPlan& P, int stencil, const px_mg_opts& o, int ghost, cud
 }
 
 }  // namespace
+
+void mg_drop_layout_plans(uint64_t gen) {
+  auto& v = mg_plans();
+  auto dead = [gen](const std::unique_ptr<MgPlan>& p) { return p->key.gen == gen; };
+  if (std::any_of(v.begin(), v.end(), dead)) {
+    cudaDeviceSynchronize();
+    v.erase(std::remove_if(v.begin(), v.end(), dead), v.end());
+  }
+}
 }  // namespace px
 
 using namespace px;
@@ -300,7 +312,8 @@ px_status px_mg_solve(const px_layout* l, const px_relax_params* p, const px_mg_
   cudaStream_t s = (cudaStream_t)stream;
   if (o->use_graph && !s) return fail(PX_ERR_ARG, "use_graph needs a non-default stream");
 
-  MgKey key{layout_generation(l), p->stencil, p->h, p->lambda, *o, phi->data, phi_scratch->data, rhs->data, s};
+  MgKey key{layout_generation(l), p->stencil, p->h, p->lambda, *o, phi->data, phi_scratch->data, rhs->data,
+            rhs->box, rhs->ld, s};
   MgPlan* P = nullptr;
   for (auto& q : mg_plans())
     if (q->key == key) P = q.get();
@@ -352,6 +365,7 @@ px_status px_mg_solve(const px_layout* l, const px_relax_params* p, const px_mg_
     P = np.get();
     mg_plans().push_back(std::move(np));
   }
+  plan_touch(mg_plans(), P);
   if (o->use_graph) {
     if (!P->exec) {
       const int64_t before = px_kernel_launch_count();

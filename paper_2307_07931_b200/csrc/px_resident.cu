@@ -577,6 +577,7 @@ px_status launch_resident(int stencil, const ResidentLaunch& r, int grid, size_t
   void* args[] = {const_cast<ResidentLaunch*>(&r)};
   e = cudaLaunchKernelExC(&cfg, fn, args);
   if (e == cudaSuccess) e = cudaGetLastError();
+  note_kernel(K == 1 ? "k_resident" : "k_resident_tb");
   count_launches(1);
   return cuda_check(e, "resident solve kernel launch");
 }

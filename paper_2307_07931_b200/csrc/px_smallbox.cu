@@ -174,7 +174,7 @@ bool smallbox_fits(int nx, int ny) { return nx >= 1 && ny >= 1 && smallbox_smem(
 
 px_status launch_smallbox(const SmallBox& b, cudaStream_t s) {
   // 16+ rows: spread the box over a cluster of 8 SMs (px_cluster.cu)
-  if (cluster_box_eligible(b.nx, b.ny)) return launch_cluster_box(b, s);
+  if (cluster_box_eligible(b)) return launch_cluster_box(b, s);
   const size_t smem = smallbox_smem(b.nx, b.ny);
   cudaError_t e;
   if (b.stencil == 0) {
@@ -192,6 +192,7 @@ px_status launch_smallbox(const SmallBox& b, cudaStream_t s) {
     }
     k_smallbox<1><<<1, SB_THREADS, smem, s>>>(b);
   }
+  note_kernel("k_smallbox");
   e = cudaGetLastError();
   count_launches(1);
   return cuda_check(e, "small-box kernel launch");

@@ -37,7 +37,7 @@ struct P2PState {
   unsigned long long* flags = nullptr;          // own: [0] arrivals from below, [1] from above
   unsigned long long* peer_flags_lo = nullptr;  // lower neighbour's flags
   unsigned long long* peer_flags_hi = nullptr;  // upper neighbour's flags
-  unsigned long long* epoch = nullptr;          // own solve counter
+  unsigned long long* epoch = nullptr;          // own [arrival base, previous solve arrivals]
   std::vector<void*> opened;                    // IPC-mapped peer allocations
 };
 
@@ -130,11 +130,12 @@ struct PlanKey {
   int32_t rank, stencil, nsweeps, norm_every, k, nparts;
   double h, lambda;
   std::vector<const double*> ptrs;
+  std::vector<int64_t> rhs_geom;  // per part: rhs box lo/hi and ld (baked into captured launches)
   cudaStream_t stream;
   bool operator==(const PlanKey& o) const {
     return layout_gen == o.layout_gen && comm == o.comm && rank == o.rank && stencil == o.stencil &&
            nsweeps == o.nsweeps && norm_every == o.norm_every && k == o.k && nparts == o.nparts &&
-           h == o.h && lambda == o.lambda && ptrs == o.ptrs && stream == o.stream;
+           h == o.h && lambda == o.lambda && ptrs == o.ptrs && rhs_geom == o.rhs_geom && stream == o.stream;
   }
 };
 
@@ -148,6 +149,7 @@ struct Plan {
   cudaGraphExec_t exec = nullptr;
   int64_t launches_per_run = 0;
   cudaEvent_t ev_bnd = nullptr, ev_comm = nullptr;
+  std::string kernels;          // sweep kernels the solve enqueues (px_last_solve_kernels)
   double* d_res = nullptr;      // shared-memory-resident solve: flags, row mailboxes, partials
   ~Plan() {
     if (d_res) cudaFree(d_res);
@@ -174,6 +176,27 @@ static bool resident_enabled() {
 static std::vector<std::unique_ptr<Plan>>& plans() {
   static std::vector<std::unique_ptr<Plan>> v;
   return v;
+}
+
+int plan_cache_cap() {
+  static int cap = 0;
+  if (!cap) {
+    const char* e = getenv("PROTOX_PLAN_CACHE");
+    cap = e ? atoi(e) : 32;
+    if (cap < 1) cap = 1;
+  }
+  return cap;
+}
+
+void drop_layout_plans(uint64_t gen) {
+  auto& v = plans();
+  const bool any = std::any_of(v.begin(), v.end(), [gen](const std::unique_ptr<Plan>& p) { return p->key.layout_gen == gen; });
+  if (any) {
+    cudaDeviceSynchronize();  // a dropped plan's graph may still be in flight
+    v.erase(std::remove_if(v.begin(), v.end(), [gen](const std::unique_ptr<Plan>& p) { return p->key.layout_gen == gen; }),
+            v.end());
+  }
+  mg_drop_layout_plans(gen);
 }
 
 struct SolveCtx {
@@ -495,7 +518,7 @@ static px_status enqueue_solve(const SolveCtx& x) {
                    x.c->p2p.rank == x.rank && x.phi[0].data == x.c->p2p.bufs[0] &&
                    x.scr[0].data == x.c->p2p.bufs[1] && ext(pli.owned, 1) > 2 * x.l->ghost && it < N;
   unsigned long long G = 0;
-  if (p2p) PX_TRY(launch_epoch_bump(x.c->p2p.epoch, x.s));
+  const int32_t it0 = it;
   for (; it < N; ++it) {
     const int32_t slot = (E > 0 && it % E == 0) ? it / E : -1;
     std::vector<SweepLaunch> v;
@@ -507,6 +530,8 @@ static px_status enqueue_solve(const SolveCtx& x) {
       const int nb = (it & 1) ? 0 : 1;  // the neighbours' buffer this sweep writes (their "next")
       const int32_t g = x.l->ghost, x0 = pli.owned.lo.c[0];
       G = (unsigned long long)stream_launch_blocks_ldg(v[0].a);
+      // arrival base of this solve += the previous solve's arrivals per side
+      if (it == it0) PX_TRY(launch_epoch_bump(st.epoch, (unsigned long long)(N - it0) * G, x.s));
       for (int side = 0; side < 2; ++side) {
         StreamLaunch& a = v[side].a;
         const int32_t pr = side == 0 ? pli.nbr_lo : pli.nbr_hi;
@@ -518,10 +543,9 @@ static px_status enqueue_solve(const SolveCtx& x) {
         a.rs.rdst = base + (int64_t)(x0 - nli.alloc.lo.c[0]) + (int64_t)(ty - nli.alloc.lo.c[1]) * nli.ld;
         a.rs.rflag = side == 0 ? st.peer_flags_lo + 1 : st.peer_flags_hi + 0;
         a.rs.epoch = st.epoch;
-        a.rs.per_epoch = (unsigned long long)N * G;
-        if (it >= 1) {
+        if (it > it0) {
           a.rs.wflag = st.flags + side;
-          a.rs.wcount = (unsigned long long)it * G;
+          a.rs.wcount = (unsigned long long)(it - it0) * G;
         }
       }
       for (auto& sl : v) PX_TRY(launch_stream(MODE_RELAX, x.p->stencil, sl.a, x.s));
@@ -550,8 +574,7 @@ static px_status enqueue_solve(const SolveCtx& x) {
       std::memset(&w, 0, sizeof w);
       w.wflag = x.c->p2p.flags + side;
       w.epoch = x.c->p2p.epoch;
-      w.per_epoch = (unsigned long long)N * G;
-      w.wcount = (unsigned long long)N * G;
+      w.wcount = (unsigned long long)(N - it0) * G;
       PX_TRY(launch_wait(w, x.s));
     }
   }
@@ -563,7 +586,10 @@ static px_status enqueue_solve(const SolveCtx& x) {
     for (auto& sl : v) PX_TRY(launch_stream(MODE_RESID, x.p->stencil, sl.a, x.s));
   }
   if (nccl_multi && plan->n_entries > 0) {
-    PX_TRY(nccl_check(ncclAllReduce(plan->d_max, plan->d_max, plan->n_entries, ncclDouble,
+    // max|r| as u64 bit patterns (|r| >= 0, so the order of the patterns is the
+    // order of the values, and a NaN -- exponent all ones, sign clear -- is
+    // above +inf): exact and NaN-propagating on every rank (R7).
+    PX_TRY(nccl_check(ncclAllReduce(plan->d_max, plan->d_max, plan->n_entries, ncclUint64,
                                     ncclMax, x.c->nccl, x.s), "ncclAllReduce(max)"));
     PX_TRY(nccl_check(ncclAllReduce(plan->d_sum, plan->d_sum, plan->n_entries, ncclDouble,
                                     ncclSum, x.c->nccl, x.s), "ncclAllReduce(sum)"));
@@ -745,7 +771,8 @@ px_status px_comm_allreduce_norms(px_comm* c, double* d_max, double* d_sum, int3
   if (!c || !d_max || !d_sum || n < 0) return fail(PX_ERR_ARG, "bad argument");
   cudaStream_t s = (cudaStream_t)stream;
   PX_TRY(nccl_check(ncclGroupStart(), "ncclGroupStart"));
-  PX_TRY(nccl_check(ncclAllReduce(d_max, d_max, n, ncclDouble, ncclMax, c->nccl, s), "ncclAllReduce"));
+  // max as u64 bit patterns of non-negative doubles (NaN-propagating, R7)
+  PX_TRY(nccl_check(ncclAllReduce(d_max, d_max, n, ncclUint64, ncclMax, c->nccl, s), "ncclAllReduce"));
   PX_TRY(nccl_check(ncclAllReduce(d_sum, d_sum, n, ncclDouble, ncclSum, c->nccl, s), "ncclAllReduce"));
   return nccl_check(ncclGroupEnd(), "ncclGroupEnd");
 }
@@ -774,6 +801,8 @@ px_status px_exchange_ghosts_local(const px_layout* l, const px_patch* parts, vo
 }
 
 }  // extern "C"
+
+static thread_local std::string tl_last_kernels;  // px_last_solve_kernels
 
 // Validate, find or build the plan, and enqueue the N sweeps on `stream`
 // (graph replay or direct launches).  Nothing is synchronised: the recorded
@@ -831,6 +860,11 @@ static px_status solve_enqueue(const px_layout* l, px_comm* c, int32_t rank, con
     key.ptrs.push_back(phi[i].data);
     key.ptrs.push_back(phi_scratch[i].data);
     key.ptrs.push_back(rhs[i].data);
+    for (int d = 0; d < 2; ++d) {
+      key.rhs_geom.push_back(rhs[i].box.lo.c[d]);
+      key.rhs_geom.push_back(rhs[i].box.hi.c[d]);
+    }
+    key.rhs_geom.push_back(rhs[i].ld);
   }
   key.stream = s;
   Plan* plan = nullptr;
@@ -870,13 +904,16 @@ static px_status solve_enqueue(const px_layout* l, px_comm* c, int32_t rank, con
     plan = np.get();
     plans().push_back(std::move(np));
   }
+  plan_touch(plans(), plan);
   SolveCtx x{l, c, rank, p, o, nparts, phi, phi_scratch, rhs, plan, s};
   if (o->use_graph && !s) return fail(PX_ERR_ARG, "use_graph needs a non-default stream");
+  take_noted_kernels();
   if (o->use_graph) {
     if (!plan->exec) {
       const int64_t before = px_kernel_launch_count();
       PX_TRY(cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture"));
       px_status st = enqueue_solve(x);
+      plan->kernels = take_noted_kernels();
       cudaGraph_t graph = nullptr;
       cudaError_t ce = cudaStreamEndCapture(s, &graph);
       if (st != PX_OK) {
@@ -899,7 +936,9 @@ static px_status solve_enqueue(const px_layout* l, px_comm* c, int32_t rank, con
     count_launches(plan->launches_per_run);
   } else {
     PX_TRY(enqueue_solve(x));
+    plan->kernels = take_noted_kernels();
   }
+  tl_last_kernels = plan->kernels;
   // φ^N is in the buffer the last pass wrote: one buffer swap per sweep, or
   // per temporal-blocking pass of K sweeps plus one per remaining sweep.
   const int32_t K = o->temporal_k > 1 ? o->temporal_k : 1;
@@ -1166,6 +1205,8 @@ px_status px_solve_host_batch(const px_layout* l, const px_relax_params* p, cons
   for (int b = 0; b < NSET; ++b) PX_TRY(harvest(b));
   return cuda_check(cudaStreamSynchronize(s), "solve_host_batch");
 }
+
+const char* px_last_solve_kernels(void) { return tl_last_kernels.c_str(); }
 
 void px_release_cached(void) {
   px_mg_release();

@@ -948,6 +948,7 @@ px_status launch_tb(int stencil, int K, const StreamLaunch& a, const TbLaunch& x
     case (1 * 8 + 4) * 2 + 0: e = tb_fix<1, 4, 0>(a, x, s); break;
     default: return fail(PX_ERR_UNSUPPORTED, "temporal_k=%d not built (2 or 4)", K);
   }
+  note_kernel(tb_wide() ? "k_tbw" : "k_tb");
   count_launches(1);
   return cuda_check(e, "temporal-blocking kernel launch");
 }

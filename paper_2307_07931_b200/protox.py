@@ -99,6 +99,7 @@ EXPORTS = [
     "px_comm_enable_p2p",
     "px_exchange_ghosts", "px_exchange_ghosts_local",
     "px_solve", "px_solve_host", "px_solve_host_batch", "px_release_cached", "px_mg_solve", "px_mg_release", "px_kernel_launch_count",
+    "px_last_solve_kernels",
     "px_relax_variant", "px_stream_ceiling", "px_pointwise_update",
     "px3_layout", "px3_norm_buffer_len", "px3_init_field", "px3_fill_ghosts", "px3_relax_step",
     "px3_residual_norm", "px3_solve", "px3_solve_host_batch", "px3_release", "px3_mehrstellen_rhs", "px3_slab", "px3_solve_comm",
@@ -188,6 +189,7 @@ def lib():
     L.px_mg_release.restype = None
     L.px_release_cached.restype = None
     L.px_kernel_launch_count.restype = i64
+    L.px_last_solve_kernels.restype = ctypes.c_char_p
     L.px_stream_ceiling.restype = st
     L.px_stream_ceiling.argtypes = [vp, vp, vp, i64, i32, vp]
     L.px_pointwise_update.restype = st
@@ -556,6 +558,11 @@ def pointwise_update(phi: px_patch, temp: px_patch, rhs: px_patch, lam: float, r
 
 def kernel_launch_count() -> int:
     return lib().px_kernel_launch_count()
+
+
+def last_solve_kernels() -> str:
+    """px_last_solve_kernels: the sweep kernels this thread's last solve enqueued."""
+    return lib().px_last_solve_kernels().decode()
 
 
 # ---------------------------------------------------------------------- 3D

@@ -74,3 +74,37 @@ def test_binding_raises_when_library_missing(monkeypatch):
     monkeypatch.setattr(P, "LIB_PATH", os.path.join(ROOT, "no_such_dir", "libprotox.so"))
     with pytest.raises(RuntimeError, match="not built"):
         P.lib()
+
+
+def test_gpus_flag_spawns_ranks_itself():
+    """`bench.py --gpus 2` outside torchrun re-launches itself with two ranks
+    (torch.distributed.run): the reference arm (no GPU needed) then prints one
+    line from rank 0 with n_gpus = 2 -- never a silent one-rank measurement."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    p = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "C1", "--gpus", "2",
+                        "--steps", "1", "--warmup", "3"], cwd=ROOT, env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    assert "launching 2 ranks" in p.stderr
+    lines = _lines(p.stdout)
+    assert len(lines) == 1 and lines[0]["n_gpus"] == 2
+
+
+def test_native_multi_gpu_refuses_without_enough_gpus():
+    """The native arm with --gpus 2 and fewer visible GPUs exits non-zero with
+    a message and no bench line."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    p = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--steps", "1", "--warmup", "3"], cwd=ROOT,
+                       env=env, capture_output=True, text=True, timeout=300)
+    assert p.returncode == 2
+    assert "refusing" in p.stderr
+    assert _lines(p.stdout) == []
+
+
+def test_world_size_mismatch_refused():
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0", CUDA_VISIBLE_DEVICES="")
+    p = subprocess.run([sys.executable, "bench.py", "--gpus", "4", "--impl", "reference", "--config", "C1"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=300)
+    assert p.returncode == 2 and "WORLD_SIZE" in p.stderr

@@ -101,12 +101,12 @@ def _worker(rank, world, port, bc, q):
                                 norm_every=1 if (it < N and it % E == 0) or it == N else -1)
             out, nm = oracle.solve3(p, a, f)
             if len(nm):
-                t = torch.tensor([nm[0, 0], nm[0, 1]], dtype=torch.float64)
-                mx = t[:1].clone()
-                sm = t[1:].clone()
+                # max over the bit patterns of |r| as integers, as px3d.cu does (ncclUint64)
+                mx = torch.from_numpy(np.array([nm[0, 0]], dtype=np.float64).view(np.int64).copy())
+                sm = torch.tensor([nm[0, 1]], dtype=torch.float64)
                 dist.all_reduce(mx, op=dist.ReduceOp.MAX)
                 dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-                norms.append((mx.item(), sm.item()))
+                norms.append((float(mx.numpy().view(np.float64)[0]), sm.item()))
             if it < N:
                 a[1:nz + 1] = out[1:nz + 1]
         parts = [None] * world

@@ -5,7 +5,15 @@ of px_layout_halo_plan (NCCL's in-order send/recv matching emulated with
 per-peer tags), all-reduces the residual norms (max / sum), and advances its
 slab with the oracle.  The gathered result must be bit-identical to the
 undecomposed oracle run: this checks the partitioner, neighbour ranks, span
-offsets/counts and posting order the GPU path uses over NCCL."""
+offsets/counts and posting order the GPU path uses over NCCL.
+
+The max-norm all-reduce is emulated exactly as libprotox performs it
+(px_solve.cu, px_comm_allreduce_norms): a max over the IEEE-754 bit patterns
+of the non-negative |r| values as integers (ncclUint64 / ncclMax there,
+int64 MAX here -- identical for patterns below 2^63), which keeps a NaN of any
+rank (reading R7).  `test_nan_norm_allreduce_over_gloo` puts a NaN in one
+rank's slab only and checks that every rank's reduced norms are NaN exactly
+where the undecomposed oracle's are."""
 import os
 import socket
 
@@ -26,7 +34,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, bc, g, st, q):
+def _worker(rank, world, port, bc, g, st, q, nan_cell=None):
     import sys
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -43,6 +51,8 @@ def _worker(rank, world, port, bc, g, st, q):
         rng = np.random.default_rng(42)
         phi0 = rng.uniform(-1, 1, (n1 + 2 * g, n0 + 2 * g))
         rho = rng.uniform(-1, 1, (n1 + 2 * g, n0 + 2 * g))
+        if nan_cell is not None:  # (y, x) of an interior cell of phi0 (ghosted indexing)
+            phi0[nan_cell] = np.nan
         lay = P.Layout(P.box(0, 0, n0 - 1, n1 - 1), (12, 10), g, bc, world)
         li = lay.local(rank)
         ld, off = li.ld, li.patch_offset
@@ -102,11 +112,12 @@ def _worker(rank, world, port, bc, g, st, q):
         def residual_allreduce():
             exchange(flat)
             m, s = oracle.residual(local, win(flat), win(rhs_flat))
-            t = torch.tensor([m], dtype=torch.float64)
+            # the library's max: over the bit patterns of |r| >= 0 as integers
+            t = torch.from_numpy(np.array([m], dtype=np.float64).view(np.int64).copy())
             u = torch.tensor([s], dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dist.all_reduce(u, op=dist.ReduceOp.SUM)
-            return t.item(), u.item()
+            return float(t.numpy().view(np.float64)[0]), u.item(), bool(np.isnan(m))
 
         norms = []
         for it in range(N):
@@ -119,15 +130,19 @@ def _worker(rank, world, port, bc, g, st, q):
         got = [None] * world if rank == 0 else None
         dist.gather_object(win(flat)[g:g + ny, g:g + n0].copy(), got, dst=0)
         if rank == 0:
-            full = np.concatenate(got, 0)
+            full = np.ascontiguousarray(np.concatenate(got, 0))
             p = oracle.Problem(n0, n1, h, lam, b0=12, b1=10, ghost=g, bc=BC_MAP[bc], stencil=st,
                                nsweeps=N, norm_every=E)
             ref, rn = oracle.solve(p, phi0, rho)
-            ok = np.array_equal(full, ref[g:g + n1, g:g + n0])
-            nm = np.array(norms)
-            ok_max = np.array_equal(nm[:, 0], rn[:, 0])
-            ok_sum = np.allclose(nm[:, 1], rn[:, 1], rtol=1e-12, atol=0)
-            q.put((ok, ok_max, ok_sum, float(np.max(np.abs(full - ref[g:g + n1, g:g + n0])))))
+            refi = np.ascontiguousarray(ref[g:g + n1, g:g + n0])
+            ok = np.array_equal(full.view(np.uint64), refi.view(np.uint64))  # NaN-aware, bitwise
+            nm = np.array([x[:2] for x in norms])
+            local_nan = [x[2] for x in norms]
+            ok_max = (np.array_equal(np.isnan(nm[:, 0]), np.isnan(rn[:, 0])) and
+                      np.array_equal(nm[:, 0].view(np.uint64), rn[:, 0].view(np.uint64)))
+            ok_sum = np.allclose(nm[:, 1], rn[:, 1], rtol=1e-12, atol=0, equal_nan=True)
+            q.put((ok, ok_max, ok_sum, float(np.nanmax(np.abs(full - refi))), int(np.isnan(rn[:, 0]).sum()),
+                   int(sum(local_nan))))
         dist.barrier()
         dist.destroy_process_group()
     except Exception as e:  # report instead of hanging the parent
@@ -150,6 +165,30 @@ def test_slab_exchange_over_gloo(world, bc, g, st):
     for p in procs:
         p.join(timeout=60)
     assert res[0] != "error", res
-    ok, ok_max, ok_sum, d = res
+    ok, ok_max, ok_sum, d = res[:4]
     assert ok, d
     assert ok_max and ok_sum
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_nan_norm_allreduce_over_gloo(world):
+    """A NaN in the LAST rank's slab only: rank 0's own residuals stay finite
+    for the first recorded iterates (the NaN needs sweeps to cross slabs), yet
+    the reduced max must be NaN in every entry where the undecomposed oracle's
+    is (all of them here), and the field bit-identical (NaN payloads included)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    n1 = 60
+    cell = (n1 - 3, 20)  # ghosted (y, x): interior row n1-4, inside the last slab for world 2 and 3
+    procs = [ctx.Process(target=_worker, args=(r, world, port, 0, 1, 0, q, cell)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+    assert res[0] != "error", res
+    ok, ok_max, ok_sum, _, n_nan_ref, n_nan_rank0 = res
+    assert n_nan_ref == 5  # N = 7, E = 2: entries for phi^0, ^2, ^4, ^6 and phi^7 -- all NaN
+    assert n_nan_rank0 < n_nan_ref  # rank 0 alone saw finite maxima: the reduction carried the NaN
+    assert ok and ok_max and ok_sum
