@@ -69,9 +69,12 @@ def parse():
     ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--halo", default="nccl", choices=["nccl", "p2p"],
-                    help="multi-GPU ghost exchange: NCCL grouped send/recv (default) or the fused "
-                         "peer-memory push (px_comm_enable_p2p)")
+    ap.add_argument("--halo", default="p2p", choices=["nccl", "p2p"],
+                    help="multi-GPU ghost exchange: the fused peer-memory push inside the relax kernel "
+                         "(px_comm_enable_p2p, default; self-checked against NCCL at start-up, NCCL if it "
+                         "fails) or NCCL grouped send/recv on a comm stream")
+    ap.add_argument("--no-halo-proxy", action="store_true",
+                    help="N = 1: skip the one-GPU halo-path measurement at the 8-rank slab shape")
     return ap.parse_args()
 
 
@@ -118,10 +121,11 @@ def k12_ceiling(P, torch, dev, elems: int, stream) -> float:
 
 
 def roofline_extras(roof: dict, cells_per_launch: int, ceiling_gbps: float | None):
-    """The three denominators of SURVEY §8(d) and the effective bytes per cell."""
+    """The three denominators of SURVEY §8(d) and the effective bytes per cell:
+    the 8 TB/s spec, the measured copy bandwidth (MEASURED_PEAKS.json, = the
+    line's `peak`), the live K12 streaming ceiling."""
     ach = roof["achieved"]
     roof["frac_vs_spec_8000"] = ach / 8000.0
-    roof["frac_vs_measured_copy_6546"] = ach / 6546.2
     if ceiling_gbps:
         roof["k12_ceiling_GBps"] = ceiling_gbps
         roof["frac_vs_k12_ceiling"] = ach / ceiling_gbps
@@ -322,6 +326,7 @@ def run_native3d(args):
         r = solve_any(bufs[0], bufs[1], rho)
         if r.in_scratch:
             bufs.reverse()
+            tens.reverse()
         return r
 
     def barrier():
@@ -490,18 +495,26 @@ def run_native(args):
             P.exchange_ghosts(lay, comm, rank, lay.patch(rank, rhs), stream=stream)
     stream.synchronize()
     pa, pb, pr = lay.patch(rank, phi), lay.patch(rank, scr), lay.patch(rank, rhs)
+    halo_mode = "local" if world == 1 else "nccl"
+    scomm = comm  # the communicator px_solve uses
     if comm is not None and args.halo == "p2p" and tk == 1:
-        P.comm_enable_p2p(comm, lay, rank, pa, pb)
+        pcomm, why = p2p_setup(P, torch, dist, lay, rank, world, local, comm, prm, S, pa, pb, pr, phi, stream)
+        if pcomm is not None:
+            scomm, halo_mode = pcomm, "p2p"
+        else:
+            halo_mode = f"nccl (p2p refused: {why})"
 
     bufs = [pa, pb]
+    tens = [phi, scr]  # the tensors behind bufs
 
     def step():
         # each step continues the relaxation from the previous step's iterate (S is even,
         # so with k = 1 the result is back in phi and the registered p2p buffer order holds)
-        r = P.solve(lay, comm, rank, prm, S, E, bufs[0], bufs[1], pr, use_graph=True, stream=stream,
+        r = P.solve(lay, scomm, rank, prm, S, E, bufs[0], bufs[1], pr, use_graph=True, stream=stream,
                     temporal_k=tk)
         if r.in_scratch:
             bufs.reverse()
+            tens.reverse()
         return r
 
     def barrier():
@@ -551,6 +564,11 @@ def run_native(args):
         evs[i][1].record(stream)
     stream.synchronize()
     k_ms = statistics.mean(a.elapsed_time(b) for a, b in evs[2:])
+    halo = None
+    if world > 1:
+        kt = torch.tensor([k_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(kt, op=dist.ReduceOp.MAX)
+        halo = halo_metrics(halo_mode, n, ghost, tk, S, t_ms / args.steps, float(kt.item()))
     variant = P.relax_variant(qa, qb, pr, li.owned)
     local_cells = (li.owned.hi.c[0] - li.owned.lo.c[0] + 1) * (li.owned.hi.c[1] - li.owned.lo.c[1] + 1)
     achieved = BYTES_PER_CELL_UPDATE * local_cells / (k_ms * 1e-3) / 1e9
@@ -596,23 +614,25 @@ def run_native(args):
                                                   [h_outs[i % 2].numpy() for i in range(k)], None,
                                                   use_graph=True, stream=stream, temporal_k=tk)
         else:
+            # the bench's own (registered) buffers: φ0 and ρ copied in every step
             h_phi0 = torch.zeros((ny, n), dtype=torch.float64).pin_memory()
             h_out = h_outs[0]
-            d_phi, d_scr, d_rhs = lay.alloc(rank, dev), lay.alloc(rank, dev), lay.alloc(rank, dev)
-            stream.wait_stream(torch.cuda.current_stream(dev))
-            qa, qb, qr = lay.patch(rank, d_phi), lay.patch(rank, d_scr), lay.patch(rank, d_rhs)
+            d_rhs = rho if cfg["stencil"] == 0 else rhs
 
             def e2e_step():
                 with torch.cuda.stream(stream):
-                    lay.view(rank, d_phi).copy_(h_phi0, non_blocking=True)
+                    lay.view(rank, tens[0]).copy_(h_phi0, non_blocking=True)
                     lay.view(rank, d_rhs).copy_(h_rho, non_blocking=True)
                 if tk > 1:
-                    P.exchange_ghosts(lay, comm, rank, qr, stream=stream)
-                r = P.solve(lay, comm, rank, prm, S, E, qa, qb, qr, use_graph=True, stream=stream,
+                    P.exchange_ghosts(lay, comm, rank, pr, stream=stream)
+                r = P.solve(lay, scomm, rank, prm, S, E, bufs[0], bufs[1], pr, use_graph=True, stream=stream,
                             temporal_k=tk)
                 with torch.cuda.stream(stream):
-                    h_out.copy_(lay.view(rank, d_scr if r.in_scratch else d_phi), non_blocking=True)
+                    h_out.copy_(lay.view(rank, tens[1] if r.in_scratch else tens[0]), non_blocking=True)
                 stream.synchronize()
+                if r.in_scratch:
+                    bufs.reverse()
+                    tens.reverse()
 
             def e2e_run(k):
                 for _ in range(k):
@@ -633,13 +653,18 @@ def run_native(args):
                "d2h_bytes_per_step": n * n * 8 + 16 * n_norm, "steps": ke,
                "api": ("px_solve_host_batch (one problem per step: H2D rho, solve, D2H phi^N + norms; "
                        "phi0 = 0 zero-filled on the device; copies overlap the neighbouring steps' solves)")
-               if world == 1 else "torch pinned copies of phi0 and rho + px_solve + D2H phi^N"}
+               if world == 1 else f"torch pinned copies of phi0 and rho + px_solve ({halo_mode} halo) + D2H phi^N"}
+
+    halo_proxy = None
+    if world == 1 and tk == 1 and n >= 16384 and not args.no_halo_proxy and cfg["bc"] == 0:
+        halo_proxy = measure_halo_proxy(P, torch, dev, stream, prm, n, 8, S)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        n_s, sw = (min(n, 4096), 40) if n > 1024 else (n, S)
+        # C1/C2 in full, C3/C5 at full size for >= 10 sweeps, C4 at 8192² (host RAM)
+        n_s, sw = (n, 10) if n <= 16384 and n > 1024 else ((8192, 4) if n > 16384 else (n, S))
         r, dt = oracle_sample(cfg, n_s, sw)
-        cpu = {"value": r, "unit": UNIT, "cores": 1, "kind": "oracle",
+        cpu = {"value": r, "unit": UNIT, "cores": 1, "kind": "oracle", "host": host_info(),
                "sample": f"single-threaded C++ oracle, {n_s}x{n_s} of the same recipe, {sw} sweeps, {dt:.1f} s"}
 
     if rank == 0:
@@ -648,7 +673,7 @@ def run_native(args):
             "warmup": max(args.warmup, 3), "ms_per_step": t_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["desc"], "n": n, "sweeps_per_step": S, "norm_every": E,
-                       "temporal_k": tk, "ghost": ghost, "halo": args.halo if world > 1 else "local",
+                       "temporal_k": tk, "ghost": ghost, "halo": halo_mode,
                        "steps_continue": "each step continues from the previous step's iterate",
                        "box": box, "partition": f"slabs x{world}", "rho": cfg["rho"], "h": h, "lambda": lam,
                        "l2": "inputs (3 x %.2f GB) exceed L2; no flush" % (lay.local(0).alloc_elems * 8 / 1e9)
@@ -656,12 +681,134 @@ def run_native(args):
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk, "final_residual_max": float(res.norms[-1, 0]) if len(res.norms) else None,
         }
+        if halo is not None:
+            line["halo"] = halo
+        if halo_proxy is not None:
+            line["halo_proxy"] = halo_proxy
         print(json.dumps(line))
+    if scomm is not None and scomm is not comm:
+        scomm.close()
     if comm is not None:
         comm.close()
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def host_info() -> dict:
+    """The GPU box's host: core count and CPU model (the oracle's context)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu": model}
+
+
+def p2p_setup(P, torch, dist, lay, rank, world, local, comm, prm, S, pa, pb, pr, phi, stream):
+    """The fused peer-memory push on a peer-memory communicator (records
+    all-gathered over the torch process group), self-checked before use: a
+    short solve from φ = 0 through the NCCL path and through the push path
+    must give the same bits on every rank.  Returns (communicator, None) or
+    (None, reason); φ is left zeroed."""
+    def run(c):
+        phi.zero_()
+        torch.cuda.synchronize()
+        r = P.solve(lay, c, rank, prm, 4, 1, pa, pb, pr, use_graph=False, stream=stream)
+        return phi.clone(), r.norms.copy()
+    try:
+        ref, rn = run(comm)
+        pcomm = P.Comm(None, world, rank, local)
+        recs = [None] * world
+        dist.all_gather_object(recs, P.comm_p2p_export(pcomm, lay, rank, pa, pb))
+        P.comm_p2p_import(pcomm, lay, recs)
+        got, gn = run(pcomm)
+        ok = bool(torch.equal(lay.view(rank, got), lay.view(rank, ref))) and bool((gn[:, 0] == rn[:, 0]).all())
+        why = "self-check differs from NCCL"
+    except Exception as e:  # noqa: BLE001 -- reported in config.halo, the NCCL path runs instead
+        pcomm, ok, why = None, False, f"{type(e).__name__}: {e}"[:200]
+    flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=phi.device)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    phi.zero_()
+    torch.cuda.synchronize()
+    if flag.item() == 1:
+        return pcomm, None
+    if pcomm is not None:
+        pcomm.close()
+    return None, why if not ok else "another rank's self-check failed"
+
+
+def halo_metrics(mode, n, g, tk, S, ms_per_step, kernel_ms):
+    """SURVEY §8(d) multi-GPU halo figures from the device-timed step and the
+    sweep kernel alone (max over ranks).  Per sweep each rank sends g full
+    padded rows to each of its two slab neighbours."""
+    row_bytes = (n + 2 * g) * 8
+    per_dir = g * row_bytes
+    sweep_ms = ms_per_step / S * tk  # per exchange
+    over_ms = max(sweep_ms - kernel_ms, 0.0)
+    return {"path": mode, "bytes_per_neighbour_direction": per_dir, "bytes_sent_per_exchange_per_rank": 2 * per_dir,
+            "exchange_every_sweeps": tk, "kernel_ms": kernel_ms, "ms_per_exchange_period": sweep_ms,
+            "unoverlapped_us_per_exchange": 1e3 * over_ms, "unoverlapped_frac": over_ms / sweep_ms,
+            "halo_GBps_per_direction_avg": per_dir / (sweep_ms * 1e-3) / 1e9,
+            "nvlink_frac_of_900GBps": per_dir / (sweep_ms * 1e-3) / 900e9,
+            "note": "push path: the halo stores are issued inside the sweep kernel, so the exchange has no span "
+                    "of its own; the unoverlapped time is what the step adds over the sweep kernel alone"}
+
+
+def measure_halo_proxy(P, torch, dev, stream, prm, n, p, S):
+    """One-GPU proxy of the multi-GPU halo paths (N = 1 runs only): the slab
+    of a p-rank split of the n² domain (n x n/p rows, periodic) solved for S
+    sweeps with norms every sweep, graph replay, as (a) one rank with fused
+    wrap images, (b) its own neighbour over NCCL send/recv (comm stream,
+    boundary rows first) and (c) its own neighbour through the fused
+    peer-memory push -- ms per sweep and overhead over the sweep kernel."""
+    from paper_2307_07931_b200 import inputs
+    os.environ["PROTOX_NCCL_SELF_EXCHANGE"] = "1"
+    n1 = n // p
+    lay = P.Layout(P.box(0, 0, n - 1, n1 - 1), (256, 256), 1, P.PX_BC_PERIODIC, 1)
+    li = lay.local(0)
+    a, b, r = lay.alloc(0, dev), lay.alloc(0, dev), lay.alloc(0, dev)
+    stream.wait_stream(torch.cuda.current_stream(dev))
+    P.init_field(lay, 0, lay.patch(0, r), P.PX_FIELD_HASH, inputs.DEFAULT_SEED, stream=stream)
+    pa, pb, pr = lay.patch(0, a), lay.patch(0, b), lay.patch(0, r)
+    nb = P.norm_buffer(li.owned, dev)
+    stream.wait_stream(torch.cuda.current_stream(dev))
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(23)]
+    for i, (e0, e1) in enumerate(evs):
+        src, dst = (pa, pb) if i % 2 == 0 else (pb, pa)
+        e0.record(stream)
+        P.relax_step(prm, src, dst, pr, li.owned, nb, stream=stream)
+        e1.record(stream)
+    stream.synchronize()
+    out = {"slab": [n, n1], "ranks_emulated": p, "sweeps": S,
+           "kernel_ms": statistics.mean(e0.elapsed_time(e1) for e0, e1 in evs[3:])}
+    for mode in ("local", "nccl", "p2p"):
+        comm = None
+        if mode == "nccl":
+            comm = P.Comm(P.comm_unique_id(), 1, 0, dev.index)
+        elif mode == "p2p":
+            comm = P.Comm(None, 1, 0, dev.index)
+            P.comm_p2p_import(comm, lay, [P.comm_p2p_export(comm, lay, 0, pa, pb)])
+        P.solve(lay, comm, 0, prm, S, 1, pa, pb, pr, use_graph=True, stream=stream)
+        kern = P.last_solve_kernels()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(3):
+            P.solve(lay, comm, 0, prm, S, 1, pa, pb, pr, use_graph=True, stream=stream)
+        e1.record(stream)
+        stream.synchronize()
+        ms = e0.elapsed_time(e1) / (3 * S)
+        out[mode] = {"ms_per_sweep": ms, "overhead_frac": ms / out["kernel_ms"] - 1, "sweep_kernels": kern}
+        if comm is not None:
+            comm.close()
+    P.release_cached()
+    del a, b, r
+    torch.cuda.empty_cache()
+    return out
 
 
 def free_port() -> int:

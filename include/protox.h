@@ -247,7 +247,9 @@ px_status px_comm_create(const uint8_t id[128], int32_t nranks, int32_t rank, in
                          px_comm** out);
 void px_comm_destroy(px_comm* c);
 /* Global all-reduce of n residual norms in device memory: d_max[i] by max,
- * d_sum[i] by sum (computeMaxResidualAcrossProcs).  d_max must hold
+ * d_sum[i] by sum (computeMaxResidualAcrossProcs).  NCCL on an NCCL
+ * communicator; over peer memory on a px_comm_create_peer one (after
+ * px_comm_p2p_import; Σ then in rank order).  d_max must hold
  * non-negative values (|r|, NaN with the sign bit clear): the max is taken
  * over their IEEE-754 bit patterns as uint64 (ncclUint64, ncclMax), which
  * orders non-negative doubles exactly and puts NaN above +inf, so a NaN on
@@ -256,21 +258,59 @@ void px_comm_destroy(px_comm* c);
 px_status px_comm_allreduce_norms(px_comm* c, double* d_max, double* d_sum, int32_t n,
                                   void* stream);
 
-/* Fused halo push over peer memory (NVLink / NVSwitch): register this rank's
- * two solve buffers (φ and its scratch, as later passed to px_solve) with the
- * communicator.  The ranks exchange CUDA IPC handles of the allocations
- * (all-gather over NCCL) and map their slab neighbours' buffers.  Afterwards
- * px_solve (temporal_k = 1) computes each sweep's boundary rows in a kernel
- * that also stores them -- with their x images, so corners are right --
- * into the neighbours' ghost rows and then increments the neighbour's
- * arrival counter (release, system scope); the next sweep's boundary kernel
- * waits for its own counter (acquire) before reading ghost rows.  Counters
- * are cumulative per solve epoch (never reset), so repeated solves and CUDA
- * graph replay are safe as long as all ranks run the same sequence of
- * solves.  No NCCL call or comm-stream hop per sweep; the norm all-reduce
- * stays an ncclAllReduce at the end.  Collective: every rank calls it.
- * Buffers must outlive the communicator.  A one-rank periodic layout in
- * self-exchange mode (PROTOX_NCCL_SELF_EXCHANGE=1) pushes to itself (test). */
+/* Peer-memory communicator: no NCCL.  Its ranks exchange ghost rows and
+ * residual norms only through the fused peer-memory push below
+ * (px_comm_p2p_export / px_comm_p2p_import), so px_solve with it needs push
+ * mode (registered buffers, temporal_k = 1, even slab width, more than 2g
+ * rows per slab; else PX_ERR_UNSUPPORTED), and px_exchange_ghosts /
+ * px3_solve_comm refuse it.  Lets ranks that share one GPU (tests) or run
+ * without NCCL use the path.  At most 16 ranks. */
+px_status px_comm_create_peer(int32_t nranks, int32_t rank, int32_t device, px_comm** out);
+
+/* Fused halo push over peer memory (NVLink / NVSwitch; "information is
+ * exchanged between the boxes", P:173 computeMaxResidualAcrossProcs).
+ *
+ * Registration is two calls so the caller can move the records over any
+ * process group:
+ *   px_comm_p2p_export: register this rank's two solve buffers (φ and its
+ *     scratch, as later passed to px_solve, in either order) and write this
+ *     rank's PX_P2P_BLOB_BYTES record (CUDA IPC handles of the allocations
+ *     holding them and of a library-owned control block; offsets; slab
+ *     pitch).  Resets this rank's arrival counters, so every rank must
+ *     export before any rank imports.
+ *   px_comm_p2p_import: blobs = the nranks records in rank order (an
+ *     all-gather of the exports); maps the slab neighbours' buffers and every
+ *     rank's control block.  PX_ERR_ARG / PX_ERR_SHAPE if a record is not the
+ *     matching rank's export for this layout.
+ * px_comm_enable_p2p = export + NCCL all-gather + import (NCCL communicator).
+ *
+ * Afterwards px_solve (temporal_k = 1) runs ONE relax kernel per sweep over
+ * the whole slab.  Its work items holding the first and last g rows are
+ * scheduled first (each is the first item of its thread block) and, at their
+ * end, store those rows of φ' -- with their x images, so corners are right --
+ * straight into the neighbours' ghost rows (16-byte stores over NVLink).  The
+ * next sweep's kernel publishes them: its first block counts one arrival per
+ * side on the neighbours' counters (relaxed, system scope: the pushing grid
+ * has completed, so its stores are performed -- no system-scope fence inside
+ * a sweep), and its boundary blocks wait for their own counter (acquire)
+ * before any thread reads a ghost row.  φ^0's rows are pushed by one small
+ * kernel at the start; the norm ring is all-reduced over peer memory at the
+ * end (every rank publishes its ring in its control block, reads all of them
+ * in rank order: max over the u64 bit patterns -- NaN-propagating --, Σ in
+ * rank order, so every rank gets the same bits).  No NCCL call and no
+ * comm-stream hop in the solve.  Counters are cumulative (never reset after
+ * export), so repeated solves of any lengths and CUDA graph replay are safe
+ * as long as all ranks run the same sequence of solves.  Push mode needs an
+ * even slab width, more than 2g rows per slab and a slab no wider than
+ * 148 x 512 columns (else px_solve uses the NCCL exchange, or fails with
+ * PX_ERR_UNSUPPORTED on a peer-memory communicator).  Buffers must outlive
+ * the registration.  A one-rank periodic layout in self-exchange mode
+ * (PROTOX_NCCL_SELF_EXCHANGE=1)
+ * pushes to itself (test).  DIRICHLET_CC, PERIODIC and FIXED_GHOSTS. */
+#define PX_P2P_BLOB_BYTES 256
+px_status px_comm_p2p_export(px_comm* c, const px_layout* l, int32_t rank, const px_patch* phi,
+                             const px_patch* phi_scratch, uint8_t* blob);
+px_status px_comm_p2p_import(px_comm* c, const px_layout* l, const uint8_t* blobs);
 px_status px_comm_enable_p2p(px_comm* c, const px_layout* l, int32_t rank, const px_patch* phi,
                              const px_patch* phi_scratch);
 

@@ -37,23 +37,36 @@ def needs_build() -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     """Compile every source to an object in parallel (one nvcc per file), then
-    link libprotox.so.  Objects go to a per-process temp dir; nothing is cached
-    between builds except the finished library."""
+    link libprotox.so.  Objects are cached in build/ under a hash of the
+    source, every header and the command line (force=True recompiles all)."""
     if not force and not needs_build():
         return LIB
     import concurrent.futures as cf
-    import shutil
-    import tempfile
+    import hashlib
     nccl = nccl_dir()
     common = ["nvcc", "-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC",
               f"-I{INCLUDE}", f"-I{CSRC}", f"-I{nccl}/include"]
-    odir = tempfile.mkdtemp(prefix="protox_build_")
+    odir = os.path.join(PKG, "build")
+    os.makedirs(odir, exist_ok=True)
     log = os.path.join(PKG, "build.log")
+    hdrs = b"".join(open(h, "rb").read() for h in sorted(glob.glob(os.path.join(CSRC, "*.h")) +
+                                                         glob.glob(os.path.join(CSRC, "*.cuh")) +
+                                                         [os.path.join(INCLUDE, "protox.h")]))
+    tmp = None
     try:
         def compile_one(src):
-            obj = os.path.join(odir, os.path.basename(src) + ".o")
-            cmd = [*common, "-Xptxas", "-v", "-c", src, "-o", obj]
+            key = hashlib.sha1(open(src, "rb").read() + hdrs + " ".join(common).encode()).hexdigest()[:16]
+            base = os.path.basename(src)
+            obj = os.path.join(odir, f"{base}.{key}.o")
+            cmd = [*common, "-Xptxas", "-v", "-c", src, "-o", obj + ".part"]
+            if os.path.exists(obj) and not force:
+                return src, obj, cmd, subprocess.CompletedProcess(cmd, 0, "(cached)\n", "")
             r = subprocess.run(cmd, capture_output=True, text=True)
+            if r.returncode == 0:
+                os.replace(obj + ".part", obj)
+                for old in glob.glob(os.path.join(odir, f"{base}.*.o")):
+                    if old != obj:
+                        os.remove(old)
             return src, obj, cmd, r
         srcs = sources()
         with cf.ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
@@ -80,7 +93,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError(f"nvcc failed (see {log})")
         os.replace(tmp, LIB)
     finally:
-        shutil.rmtree(odir, ignore_errors=True)
+        if tmp and os.path.exists(tmp):
+            os.remove(tmp)
     if verbose:
         with open(log) as f:
             print(f.read())

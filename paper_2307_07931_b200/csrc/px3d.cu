@@ -948,6 +948,7 @@ px_status px3_solve_comm(px_comm* c, px_bc bc, const px_relax_params* p, const p
                          int32_t* n_written, int32_t* in_scratch, void* stream) {
   clear_error();
   if (!c) return fail(PX_ERR_ARG, "null communicator");
+  if (!comm_nccl(c)) return fail(PX_ERR_UNSUPPORTED, "px3_solve_comm needs an NCCL communicator (px_comm_create)");
   return solve3_impl(c, bc, p, o, phi, phi_scratch, rhs, h_norms, cap, n_written, in_scratch, stream);
 }
 

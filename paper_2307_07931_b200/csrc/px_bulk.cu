@@ -77,16 +77,71 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
   return p;
 }
 
+// ---- fused halo push over peer memory (PushSpec, px_internal.h) ----
+// spin until own arrival counter `side` reaches base + wcount (acquire, system scope)
+__device__ __forceinline__ void ps_wait(const PushSpec& ps, int side) {
+  const unsigned long long target = *ps.epoch + ps.wcount;
+  unsigned long long v;
+  do {
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(ps.wflag[side]) : "memory");
+  } while (v < target);
+}
+// The pair (x, x+1) of a row pushed into the neighbour's ghost row rp, with
+// the x images of the pair's cells at the domain's x faces (corners).  Rare
+// (2g rows per sweep): out of line, scalar arguments only, so the kernel's
+// inner loop keeps its registers.
+static __device__ __noinline__ void ps_push(double* rp, int x, double v0, double v1, int X0, int g, int n0,
+                                            int m0, int m1) {
+  *reinterpret_cast<double2*>(rp + x) = make_double2(v0, v1);
+  for (int q = 0; q < 2; ++q) {
+    const int X = X0 + q;
+    const double v = q ? v1 : v0;
+    const int o = x + q - X;  // region-relative column of global column 0
+    if (X < g && m0 != GH_NONE) rp[(m0 == GH_WRAP ? X + n0 : -X - 1) + o] = m0 == GH_REFLECT ? -v : v;
+    if (X >= n0 - g && m1 != GH_NONE) rp[(m1 == GH_WRAP ? X - n0 : 2 * n0 - 1 - X) + o] = m1 == GH_REFLECT ? -v : v;
+  }
+}
+// End of a boundary item: push its rows [0,g) (lo side) and/or [ny-g,ny) (hi
+// side) of φ' -- read back from this thread's own stores -- into the
+// neighbours' ghost rows (plain stores; their arrival is counted by the next
+// kernel, see k_bulk).  Outside the per-stage loop, out of line: the sweep's
+// inner loop is untouched.
+static __device__ __noinline__ void push_rows(const StreamLaunch& a, int x, bool lo, bool hi, bool live, bool xface,
+                                              int X0) {
+  const int g = a.ps.g;
+  for (int side = 0; side < 2; ++side) {
+    if (!(side ? hi : lo) || !a.ps.rdst[side]) continue;
+    const int p0 = side ? a.ny - g : 0;
+    if (live) {
+      for (int r = 0; r < g; ++r) {
+        const double2 v = *reinterpret_cast<const double2*>(a.dst + (int64_t)(p0 + r) * a.ld_dst + x);
+        double* rp = a.ps.rdst[side] + (int64_t)r * a.ld_dst;
+        if (xface)
+          ps_push(rp, x, v.x, v.y, X0, a.gs.g, a.gs.n[0], a.gs.mode[0][0], a.gs.mode[0][1]);
+        else
+          *reinterpret_cast<double2*>(rp + x) = v;
+      }
+    }
+  }
+}
+
 struct Item {
   int c;       // first column of the strip (relative to region.lo)
   int w;       // strip width (even)
   int y0, y1;  // rows computed: [y0, y1)
 };
 
-template <int W>
+template <int W, int PUSH>
 __device__ __forceinline__ Item item_of(const StreamLaunch& a, int it, int nstrips, int crows) {
   Item t;
-  const int s = it % nstrips, k = it / nstrips;
+  const int s = it % nstrips;
+  int k = it / nstrips;
+  if (PUSH && k > 0) {
+    // push mode: the first and the last row chunk (the ones that push rows to
+    // and read ghost rows from the neighbours) are the first two chunks run
+    const int nchunks = (a.ny + crows - 1) / crows;
+    k = (k == 1) ? nchunks - 1 : k - 1;
+  }
   t.c = s * W;
   t.w = min(W, a.nx - t.c);
   t.y0 = k * crows;
@@ -105,7 +160,8 @@ using namespace bulk;
 // NST stages of R rows per CTA, CPS CTAs per SM.
 // PW bit 0: scale is a power of two, bit 1: λ is a power of two (exact
 // products, so fused multiply-adds are bit-identical to the separate ops).
-template <int MODE, int ST, int NST, int R, int CPS, int NC, int PW>
+// PUSH: fused peer-memory halo push (PushSpec; px_solve P2P mode)
+template <int MODE, int ST, int NST, int R, int CPS, int NC, int PW, int PUSH>
 __global__ void __launch_bounds__(NC * 32 + 32, CPS) k_bulk(const StreamLaunch a, int nstrips, int nitems,
                                                             int crows) {
   constexpr int W = 64 * NC, NCW = NC;
@@ -122,6 +178,27 @@ __global__ void __launch_bounds__(NC * 32 + 32, CPS) k_bulk(const StreamLaunch a
       mbar_init(&empty[s], NCW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (PUSH && blockIdx.x == 0 && a.ps.rel) {
+      // the previous sweep's pushes into the neighbours' ghost rows are
+      // complete: that kernel has finished (stream order; a finished grid's
+      // stores, peer stores included, are performed), so one relaxed count
+      // per side publishes them -- no system-scope fence in the sweep
+      for (int side = 0; side < 2; ++side)
+        if (a.ps.rflag[side])
+          asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(a.ps.rflag[side]), "l"(1ull) : "memory");
+    }
+    if (PUSH && blockIdx.x < nitems) {
+      // push mode: the boundary items (first and last row chunk) are every
+      // CTA's FIRST item (they are scheduled first and the grid covers them,
+      // bulk_geom), so the ghost rows the neighbours push are awaited once,
+      // here, before any thread of the CTA touches them: the acquire plus the
+      // CTA barrier below order every consumer load after the neighbours'
+      // stores, and the proxy fence orders the producer's TMA reads.
+      const Item t = item_of<W, PUSH>(a, blockIdx.x, nstrips, crows);
+      if (t.y0 == 0 && a.ps.wflag[0]) ps_wait(a.ps, 0);
+      if (t.y1 == a.ny && a.ps.wflag[1]) ps_wait(a.ps, 1);
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
   }
   __syncthreads();
 
@@ -135,7 +212,7 @@ __global__ void __launch_bounds__(NC * 32 + 32, CPS) k_bulk(const StreamLaunch a
       int slot = 0;
       uint32_t phase = 0;
       for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
-        const Item t = item_of<W>(a, it, nstrips, crows);
+        const Item t = item_of<W, PUSH>(a, it, nstrips, crows);
         const int nst = item_stages<R>(t);
         const uint32_t rowbytes = (uint32_t)t.w * 8u;
         for (int st = 0; st < nst; ++st) {
@@ -192,7 +269,7 @@ __global__ void __launch_bounds__(NC * 32 + 32, CPS) k_bulk(const StreamLaunch a
     int it = blockIdx.x;
     Item t;
     if (it < nitems) {
-      t = item_of<W>(a, it, nstrips, crows);
+      t = item_of<W, PUSH>(a, it, nstrips, crows);
       load_halo(t, 0);
     }
     for (; it < nitems; it += gridDim.x) {
@@ -217,7 +294,7 @@ __global__ void __launch_bounds__(NC * 32 + 32, CPS) k_bulk(const StreamLaunch a
         if (st + 1 < nst) {
           load_halo(t, st + 1);
         } else if (it + (int)gridDim.x < nitems) {
-          load_halo(item_of<W>(a, it + gridDim.x, nstrips, crows), 0);
+          load_halo(item_of<W, PUSH>(a, it + gridDim.x, nstrips, crows), 0);
         }
         mbar_wait(&full[slot], phase);
         const double* sp = smem + (size_t)slot * STAGE_DOUBLES;
@@ -306,7 +383,9 @@ __global__ void __launch_bounds__(NC * 32 + 32, CPS) k_bulk(const StreamLaunch a
           phase ^= 1u;
         }
       }
-      if (it + (int)gridDim.x < nitems) t = item_of<W>(a, it + gridDim.x, nstrips, crows);
+      if (PUSH && ((t.y0 == 0 && a.ps.rdst[0]) || (t.y1 == a.ny && a.ps.rdst[1])))
+        push_rows(a, t.c + c0, t.y0 == 0, t.y1 == a.ny, live, xface, X0);
+      if (it + (int)gridDim.x < nitems) t = item_of<W, PUSH>(a, it + gridDim.x, nstrips, crows);
     }
   }
   if (a.norms.out_max) reduce_norms(a.norms, mx, ss);
@@ -348,6 +427,9 @@ static const BulkCfg& bulk_cfg() {
   }
   return kCfgs[idx];
 }
+// the fused push always runs the default configuration (its arrival count
+// depends on the strip width)
+static const BulkCfg& cfg_for(const StreamLaunch& a) { return a.ps.on ? kCfgs[0] : bulk_cfg(); }
 static int bulk_chunk() {
   static int c = 0;
   if (!c) {
@@ -369,8 +451,10 @@ bool bulk_eligible(int mode, const StreamLaunch& a) {
   if (disabled) return false;
   if (mode != MODE_RELAX && mode != MODE_RESID) return false;
   if (a.phase != 0 || (a.nx & 1) || a.nx <= 0 || a.ny <= 0) return false;
-  // small (L2-resident, launch-bound) problems cannot fill a persistent grid
-  if ((int64_t)a.nx * a.ny < (int64_t)4 * 1024 * 1024) return false;
+  // small (L2-resident, launch-bound) problems cannot fill a persistent grid;
+  // the fused peer-memory push runs in this kernel at any size
+  if (!a.ps.on && (int64_t)a.nx * a.ny < (int64_t)4 * 1024 * 1024) return false;
+  if (a.ps.on && (mode != MODE_RELAX || a.ps.g < 1 || a.ny < a.ps.g)) return false;
   if ((a.ld_src & 1) || (mode == MODE_RELAX && (a.ld_dst & 1)) || (a.ld_rhs & 1)) return false;
   // bulk copies need 16-byte aligned row starts
   if (((uintptr_t)a.src & 15) || ((uintptr_t)a.rhs & 15)) return false;
@@ -385,18 +469,20 @@ struct BulkGeom {
 };
 static BulkGeom bulk_geom(const StreamLaunch& a) {
   BulkGeom g;
-  g.nstrips = (a.nx + 64 * bulk_cfg().nc - 1) / (64 * bulk_cfg().nc);
-  const BulkCfg& cfg = bulk_cfg();
+  const BulkCfg& cfg = cfg_for(a);
+  g.nstrips = (a.nx + 64 * cfg.nc - 1) / (64 * cfg.nc);
   const int per_sm = cfg.cps;
   int gmax = num_sms() * per_sm < BULK_MAX_GRID ? num_sms() * per_sm : BULK_MAX_GRID;
   const int c0 = (a.ny + bulk_chunk() - 1) / bulk_chunk();
   double best = 1e30;
-  g.nchunks = c0;
+  g.nchunks = a.ps.on ? 1 : c0;
   // up to twice the nominal chunk count, or enough chunks to give every CTA an item
   const int cmax = 2 * c0 > (gmax + g.nstrips - 1) / g.nstrips ? 2 * c0 : (gmax + g.nstrips - 1) / g.nstrips;
   for (int c = c0; c <= cmax && c <= a.ny; ++c) {
     const int rows = (a.ny + c - 1) / c;
     const int cc = (a.ny + rows - 1) / rows;       // chunks actually produced
+    // push mode: each pushed block of g boundary rows lies within one chunk
+    if (a.ps.on && (rows < a.ps.g || a.ny - (cc - 1) * rows < a.ps.g)) continue;
     const int items = g.nstrips * cc;
     const int waves = (items + gmax - 1) / gmax;
     // time ~ waves * (rows + 2): balance and per-chunk halo overhead
@@ -415,18 +501,26 @@ static BulkGeom bulk_geom(const StreamLaunch& a) {
 
 int32_t bulk_blocks(const StreamLaunch& a) { return bulk_geom(a).grid; }
 
-template <int MODE, int ST, int NST, int R, int CPS, int NC, int PW>
+int32_t bulk_push_arrivals(const StreamLaunch& a) {
+  if (!a.ps.on || !bulk_eligible(MODE_RELAX, a)) return 0;
+  const BulkGeom g = bulk_geom(a);
+  // every boundary item must be some CTA's first item (the kernel-start wait)
+  if ((g.nchunks > 1 ? 2 : 1) * g.nstrips > g.grid) return 0;
+  return 1;  // one count per side per sweep (CTA 0 of the next kernel)
+}
+
+template <int MODE, int ST, int NST, int R, int CPS, int NC, int PW, int PUSH = 0>
 static cudaError_t launch_b(const StreamLaunch& a, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_bulk<MODE, ST, NST, R, CPS, NC, PW>,
+    cudaError_t e = cudaFuncSetAttribute(k_bulk<MODE, ST, NST, R, CPS, NC, PW, PUSH>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem_bytes<NST, R, NC>());
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const BulkGeom g = bulk_geom(a);
-  k_bulk<MODE, ST, NST, R, CPS, NC, PW><<<g.grid, NC * 32 + 32, smem_bytes<NST, R, NC>(), s>>>(
+  k_bulk<MODE, ST, NST, R, CPS, NC, PW, PUSH><<<g.grid, NC * 32 + 32, smem_bytes<NST, R, NC>(), s>>>(
       a, g.nstrips, g.nitems, g.crows);
   return cudaGetLastError();
 }
@@ -439,6 +533,9 @@ static bool is_pow2(double v) {
 
 template <int MODE, int ST, int PW>
 static cudaError_t launch_pw(const StreamLaunch& a, cudaStream_t s) {
+  if constexpr (MODE == MODE_RELAX) {
+    if (a.ps.on) return launch_b<MODE, ST, 3, 3, 2, 8, PW, 1>(a, s);  // = kCfgs[0]
+  }
   const BulkCfg& c = bulk_cfg();
   if (c.nc == 8 && c.nst == 4) return launch_b<MODE, ST, 4, 3, 2, 8, PW>(a, s);
   if (c.nc == 15) return launch_b<MODE, ST, 4, 3, 1, 15, PW>(a, s);

@@ -94,18 +94,27 @@ struct NormSlot {
   int32_t expected;
 };
 
-// Fused halo push over peer memory (px_solve P2P mode): a
-// boundary-row launch also stores its cells (and their x images) into the
-// neighbour's ghost rows and then bumps the neighbour's arrival counter; a
-// launch that reads ghost rows first waits until its own arrival counter
-// reaches base + the count expected within this solve (counters never reset;
-// the base advances by each solve's own arrivals, so solves may differ in N).
-struct RemoteSpec {
-  double* rdst;                    // neighbour cell matching region.lo (null: no push)
-  unsigned long long* rflag;       // neighbour's arrival counter to bump
-  unsigned long long* wflag;       // own arrival counter to wait on (null: no wait)
+// Fused halo push over peer memory (px_solve P2P mode).  ONE
+// k_bulk launch per sweep over the whole owned slab.  Its work items of the
+// first and last row chunk run first (every one is some CTA's first item); at
+// their end they store rows [0,g) and [ny-g,ny) of φ' (with their x images,
+// so corners are right) straight into the lo / hi neighbour's ghost rows
+// (16-byte stores over NVLink).  The NEXT sweep's kernel publishes them: its
+// CTA 0 counts one arrival per side on the neighbours' counters (relaxed,
+// system scope -- the pushing grid has completed, so its stores are
+// performed), and its boundary CTAs wait until their own counter reaches
+// base + wcount (acquire) before any thread reads a ghost row.  Counters never
+// reset: the base (*epoch) advances by each solve's own arrivals, so solves
+// may differ in N.  Side 0 = lo (rank below), 1 = hi.
+struct PushSpec {
+  double* rdst[2];                 // neighbour's ghost-row cell matching region.lo.x (null: no push)
+  unsigned long long* rflag[2];    // neighbour's arrival counter to bump
+  unsigned long long* wflag[2];    // own arrival counter to wait on (null: no wait)
   const unsigned long long* epoch; // own arrival base (arrivals of all earlier solves)
-  unsigned long long wcount;       // arrivals needed within this solve
+  unsigned long long wcount;       // arrivals needed within this solve, per side
+  int32_t g;                       // rows pushed per side (the ghost width)
+  int32_t on;                      // any push / wait: boundary chunks are scheduled first
+  int32_t rel;                     // publish the previous sweep's pushes (CTA 0, at kernel start)
 };
 
 struct StreamLaunch {
@@ -119,7 +128,7 @@ struct StreamLaunch {
   double scale, lambda;
   GhostSpec gs;
   NormSlot norms;     // norms.out_max == null: none
-  RemoteSpec rs;      // fused halo push / wait (k_stream only)
+  PushSpec ps;        // fused halo push / wait (k_bulk only)
 };
 
 // Extra launch state of a temporal-blocking pass (px_tb.cu).
@@ -188,7 +197,46 @@ bool resident_plan(int nx, int ny, int* grid, int* rmax, size_t* smem);
 px_status launch_resident(int stencil, const ResidentLaunch& r, int grid, size_t smem, cudaStream_t s);
 int32_t stream_launch_blocks_ldg(const StreamLaunch& a);
 px_status launch_stream_ldg(int mode, int stencil, const StreamLaunch& a, cudaStream_t s);
-px_status launch_wait(const RemoteSpec& rs, cudaStream_t s);
+// arrivals a push-mode k_bulk launch of `a` counts per side (1); 0 if the
+// launch cannot push (not bulk-eligible, or its boundary items would not all
+// be first items of its CTAs)
+int32_t bulk_push_arrivals(const StreamLaunch& a);
+// publish the last sweep's pushes (ps.rel), then wait (on the device) until
+// both own counters of `ps` reach base + wcount
+px_status launch_wait(const PushSpec& ps, cudaStream_t s);
+// copy the full padded rows [0,g) / [ny-g,ny) of a slab (x ghosts included)
+// into the neighbours' ghost rows of both their buffers, then count
+// PX_PUSH_INIT_CTAS arrivals per side (the exchange of φ^0 in push mode)
+constexpr int PX_PUSH_INIT_CTAS = 32;
+struct PushInit {
+  const double* src_lo;            // own padded row 0 (x = -g)
+  const double* src_hi;            // own padded row ny-g
+  double* dst[2][2];               // [side][buffer]: neighbour's ghost row start (x = -g)
+  unsigned long long* rflag[2];
+  int64_t ld;
+  int32_t row_len, g;
+};
+px_status launch_push_init(const PushInit& pi, cudaStream_t s);
+// Norm all-reduce over peer memory (one CTA): every rank publishes its ring
+// in its mailbox, counts an arrival on every peer, reads all mailboxes in
+// rank order (max over the u64 bit patterns, Σ in rank order: every rank gets
+// the same bits), then counts a "done" on every peer before its mailbox may
+// be reused.
+constexpr int PX_PEER_MAX = 16;
+constexpr int PX_MBOX_ENTRIES = 2048;
+struct PeerAllreduce {
+  double* d_max;
+  double* d_sum;
+  int32_t n, nranks, rank;
+  double* mbox_own;                          // 2 * PX_MBOX_ENTRIES doubles
+  const double* mbox[PX_PEER_MAX];           // every rank's mailbox (own included)
+  unsigned long long* arrive[PX_PEER_MAX];   // every rank's arrive counter
+  unsigned long long* done[PX_PEER_MAX];     // every rank's done counter
+  unsigned long long* own_arrive;
+  unsigned long long* own_done;
+  unsigned long long* round;                 // own round counter
+};
+px_status launch_peer_allreduce(const PeerAllreduce& ar, cudaStream_t s);
 px_status launch_epoch_bump(unsigned long long* epoch, unsigned long long per_solve, cudaStream_t s);
 int32_t persist_grid();
 px_status launch_persist(int stencil, const PersistLaunch& p, int grid, cudaStream_t s);

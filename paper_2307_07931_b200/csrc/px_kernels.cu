@@ -74,7 +74,7 @@ int32_t stream_blocks(int32_t nx, int32_t ny, int32_t phase) {
 }
 
 int32_t launch_blocks(int mode, const StreamLaunch& a) {
-  if (bulk_eligible(mode, a) && !a.rs.rdst && !a.rs.wflag) return bulk_blocks(a);
+  if (bulk_eligible(mode, a)) return bulk_blocks(a);
   return ldg_blocks(a.nx, a.ny, a.phase);
 }
 
@@ -150,28 +150,6 @@ __device__ __forceinline__ void taps(const Fin& S, const Fin& C, const Fin& N, d
 }
 
 // ------------------------------------------------------- the stream kernel
-// Spin until *flag >= base + count (system-scope acquire); base = the
-// neighbour's arrivals of all earlier solves (advanced by k_epoch_bump).
-__device__ __forceinline__ void rs_wait(const RemoteSpec& rs) {
-  const unsigned long long target = *rs.epoch + rs.wcount;
-  unsigned long long v;
-  do {
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(rs.wflag) : "memory");
-  } while (v < target);
-}
-
-// Store a cell (and its x images) into the neighbour's ghost rows.
-__device__ __forceinline__ void rs_push(const StreamLaunch& a, int x, int y, double v) {
-  double* rp = a.rs.rdst + (int64_t)y * a.ld_dst;
-  rp[x] = v;
-  const GhostSpec& g = a.gs;
-  const int X = x + g.o[0];
-  if (X < g.g && g.mode[0][0] != GH_NONE)
-    rp[(g.mode[0][0] == GH_WRAP ? X + g.n[0] : -X - 1) - g.o[0]] = g.mode[0][0] == GH_REFLECT ? -v : v;
-  if (X >= g.n[0] - g.g && g.mode[0][1] != GH_NONE)
-    rp[(g.mode[0][1] == GH_WRAP ? X - g.n[0] : 2 * g.n[0] - 1 - X) - g.o[0]] = g.mode[0][1] == GH_REFLECT ? -v : v;
-}
-
 // One tile (column group bx x row chunk by) of a sweep; accumulates the
 // residual norms of the tile's cells into mx / ss.
 template <int MODE, int ST>
@@ -271,10 +249,6 @@ __device__ __forceinline__ void stream_tile(const StreamLaunch& a, const int bx,
           if (va) images(a, c, r, o0);
           if (vb) images(a, c + 1, r, o1);
         }
-        if (MODE == MODE_RELAX && a.rs.rdst) {
-          if (va) rs_push(a, c, r, o0);
-          if (vb) rs_push(a, c + 1, r, o1);
-        }
       }
       fS = fC;
       fC = fN;
@@ -287,17 +261,7 @@ template <int MODE, int ST>
 __global__ void __launch_bounds__(SW_THREADS, 2) k_stream(const StreamLaunch a, const int rows) {
   unsigned long long mx = 0ull;
   double ss = 0.0;
-  if (a.rs.wflag) {  // the ghost rows this launch reads arrive over peer memory
-    if (threadIdx.x == 0) rs_wait(a.rs);
-    __syncthreads();
-  }
   stream_tile<MODE, ST>(a, blockIdx.x, blockIdx.y, rows, mx, ss);
-  if (a.rs.rdst) {   // publish this CTA's pushed cells, then count its arrival
-    __threadfence_system();
-    __syncthreads();
-    if (threadIdx.x == 0)
-      asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(a.rs.rflag), "l"(1ull) : "memory");
-  }
   if (MODE == MODE_RELAX || MODE == MODE_RESID) {
     if (a.norms.out_max) reduce_norms(a.norms, mx, ss);
   }
@@ -426,13 +390,30 @@ static void launch_t(const StreamLaunch& a, dim3 grid, cudaStream_t s) {
 
 px_status launch_stream(int mode, int stencil, const StreamLaunch& a, cudaStream_t s) {
   if (a.nx <= 0 || a.ny <= 0) return PX_OK;
-  if (bulk_eligible(mode, a) && !a.rs.rdst && !a.rs.wflag) return launch_bulk(mode, stencil, a, s);
+  if (bulk_eligible(mode, a)) return launch_bulk(mode, stencil, a, s);
+  if (a.ps.on) return fail(PX_ERR_UNSUPPORTED, "peer-memory push needs the TMA kernel (even width, aligned rows)");
   return launch_stream_ldg(mode, stencil, a, s);
 }
 
 int32_t stream_launch_blocks_ldg(const StreamLaunch& a) { return ldg_blocks(a.nx, a.ny, a.phase); }
 
-__global__ void k_wait(const RemoteSpec rs) { rs_wait(rs); }
+// ---- fused halo push over peer memory: per-solve helpers (px_solve P2P mode)
+__device__ __forceinline__ void spin_until(const unsigned long long* flag, unsigned long long target) {
+  unsigned long long v;
+  do {
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+  } while (v < target);
+}
+
+__global__ void k_wait(const PushSpec ps) {
+  if (ps.rel)  // the previous kernel (the last sweep) has completed: its pushes are performed
+    for (int side = 0; side < 2; ++side)
+      if (ps.rflag[side])
+        asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(ps.rflag[side]), "l"(1ull) : "memory");
+  const unsigned long long target = *ps.epoch + ps.wcount;
+  for (int side = 0; side < 2; ++side)
+    if (ps.wflag[side]) spin_until(ps.wflag[side], target);
+}
 // e[0] = arrival base of this solve, e[1] = arrivals per side of the previous
 // solve: every solve adds its own count, so solves of different lengths mix.
 __global__ void k_epoch_bump(unsigned long long* e, unsigned long long per_solve) {
@@ -440,10 +421,94 @@ __global__ void k_epoch_bump(unsigned long long* e, unsigned long long per_solve
   e[1] = per_solve;
 }
 
-px_status launch_wait(const RemoteSpec& rs, cudaStream_t s) {
-  k_wait<<<1, 1, 0, s>>>(rs);
+// φ^0's boundary rows (full padded rows) into both buffers of each neighbour.
+// CTA b copies a column slice of every row; then it counts one arrival per
+// side (PX_PUSH_INIT_CTAS arrivals per side in all).
+__global__ void __launch_bounds__(256) k_push_init(const PushInit pi) {
+  const int per = (pi.row_len + gridDim.x - 1) / gridDim.x;
+  const int i0 = blockIdx.x * per, i1 = min(pi.row_len, i0 + per);
+  for (int side = 0; side < 2; ++side) {
+    const double* src = side ? pi.src_hi : pi.src_lo;
+    for (int b = 0; b < 2; ++b) {
+      double* dst = pi.dst[side][b];
+      if (!dst) continue;
+      for (int r = 0; r < pi.g; ++r)
+        for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x)
+          dst[(int64_t)r * pi.ld + i] = src[(int64_t)r * pi.ld + i];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int side = 0; side < 2; ++side)
+      if (pi.rflag[side])
+        asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(pi.rflag[side]), "l"(1ull) : "memory");
+  }
+}
+
+// Norm all-reduce over peer memory (PeerAllreduce, px_internal.h); one CTA.
+__global__ void __launch_bounds__(256) k_peer_allreduce(const PeerAllreduce ar) {
+  __shared__ unsigned long long q;
+  const int P = ar.nranks;
+  for (int c0 = 0; c0 < ar.n; c0 += PX_MBOX_ENTRIES) {
+    const int m = min(PX_MBOX_ENTRIES, ar.n - c0);
+    if (threadIdx.x == 0) q = ++*ar.round;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+      ar.mbox_own[2 * i] = ar.d_max[c0 + i];
+      ar.mbox_own[2 * i + 1] = ar.d_sum[c0 + i];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      for (int p = 0; p < P; ++p)
+        if (p != ar.rank)
+          asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(ar.arrive[p]), "l"(1ull) : "memory");
+      spin_until(ar.own_arrive, q * (unsigned long long)(P - 1));
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+      // every rank combines the mailboxes in rank order: identical bits everywhere
+      unsigned long long mx = 0ull;
+      double ss = 0.0;
+      for (int p = 0; p < P; ++p) {
+        const double* mb = ar.mbox[p];
+        const double vm = __ldcv(mb + 2 * i), vs = __ldcv(mb + 2 * i + 1);
+        const unsigned long long bits = (unsigned long long)__double_as_longlong(vm);
+        mx = bits > mx ? bits : mx;  // |r| >= 0 (or NaN, sign clear): the bit order is the value order
+        ss = p == 0 ? vs : __dadd_rn(ss, vs);
+      }
+      ar.d_max[c0 + i] = __longlong_as_double((long long)mx);
+      ar.d_sum[c0 + i] = ss;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // every peer has read this mailbox before the next round rewrites it
+      __threadfence_system();
+      for (int p = 0; p < P; ++p)
+        if (p != ar.rank)
+          asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(ar.done[p]), "l"(1ull) : "memory");
+      spin_until(ar.own_done, q * (unsigned long long)(P - 1));
+    }
+    __syncthreads();
+  }
+}
+
+px_status launch_wait(const PushSpec& ps, cudaStream_t s) {
+  k_wait<<<1, 1, 0, s>>>(ps);
   count_launches(1);
   return cuda_check(cudaGetLastError(), "wait kernel launch");
+}
+
+px_status launch_push_init(const PushInit& pi, cudaStream_t s) {
+  k_push_init<<<PX_PUSH_INIT_CTAS, 256, 0, s>>>(pi);
+  count_launches(1);
+  return cuda_check(cudaGetLastError(), "push-init kernel launch");
+}
+
+px_status launch_peer_allreduce(const PeerAllreduce& ar, cudaStream_t s) {
+  if (ar.n <= 0 || ar.nranks <= 1) return PX_OK;
+  k_peer_allreduce<<<1, 256, 0, s>>>(ar);
+  count_launches(1);
+  return cuda_check(cudaGetLastError(), "peer all-reduce kernel launch");
 }
 
 px_status launch_epoch_bump(unsigned long long* epoch, unsigned long long per_solve, cudaStream_t s) {

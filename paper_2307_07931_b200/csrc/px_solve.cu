@@ -24,25 +24,56 @@
 #include <memory>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges for nsys timelines, no link dependency
+
 #include "px_internal.h"
 
-// Peer-memory halo state (px_comm_enable_p2p).
+// NVTX range for the scope (host side: marks the enqueue of a solve phase
+// and, in px_solve, the whole host-synchronous call)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
+// Peer-memory halo state (px_comm_p2p_export / _import, px_comm_enable_p2p).
+// Control block of a rank (one cudaMalloc, exported over CUDA IPC), u64 words:
+enum : int {
+  CTL_FROM_LO = 0,    // arrivals pushed by the rank below
+  CTL_FROM_HI = 1,    // arrivals pushed by the rank above
+  CTL_EPOCH = 2,      // [2] arrival base of the current solve, [3] previous solve's arrivals
+  CTL_AR_ARRIVE = 4,  // peer norm all-reduce: mailboxes published by peers
+  CTL_AR_DONE = 5,    //   mailboxes read by peers
+  CTL_AR_ROUND = 6,   //   own round counter
+  CTL_MBOX = 8,       // mailbox: 2 * PX_MBOX_ENTRIES doubles
+};
+static constexpr size_t CTL_BYTES = (CTL_MBOX + 2 * px::PX_MBOX_ENTRIES) * sizeof(unsigned long long);
+
 struct P2PState {
-  bool enabled = false;
+  bool exported = false, enabled = false;
   uint64_t layout_gen = 0;
   int32_t rank = 0;
   const double* bufs[2] = {nullptr, nullptr};   // own registered φ (A) and scratch (B)
   double* peer_lo[2] = {nullptr, nullptr};      // lower neighbour's A, B (patch data pointers)
   double* peer_hi[2] = {nullptr, nullptr};      // upper neighbour's A, B
-  unsigned long long* flags = nullptr;          // own: [0] arrivals from below, [1] from above
-  unsigned long long* peer_flags_lo = nullptr;  // lower neighbour's flags
-  unsigned long long* peer_flags_hi = nullptr;  // upper neighbour's flags
-  unsigned long long* epoch = nullptr;          // own [arrival base, previous solve arrivals]
+  unsigned long long* ctl = nullptr;            // own control block
+  std::vector<unsigned long long*> ctl_of;      // every rank's control block (mapped; own at [rank])
   std::vector<void*> opened;                    // IPC-mapped peer allocations
 };
 
+// One 256-byte record per rank (px_comm_p2p_export): IPC handles of the
+// allocations holding A, B and the control block, and the offsets into them.
+struct P2PBlob {
+  uint32_t magic;
+  int32_t rank, nranks, pad;
+  int64_t ld, n0;                 // slab pitch and width (checked on import)
+  cudaIpcMemHandle_t h[3];        // A, B, control block
+  uint64_t off[3];
+};
+static_assert(sizeof(P2PBlob) <= PX_P2P_BLOB_BYTES, "P2P blob size");
+static constexpr uint32_t P2P_MAGIC = 0x50583250u;  // "PX2P"
+
 struct px_comm {
-  ncclComm_t nccl = nullptr;
+  ncclComm_t nccl = nullptr;   // null: peer-memory-only communicator (px_comm_create_peer)
   int32_t nranks = 1, rank = 0, device = 0;
   cudaStream_t stream = nullptr;
   bool self_exchange = false;  // 1 rank, periodic: exchange ghost rows with itself (test mode)
@@ -372,14 +403,108 @@ static px_status enqueue_smallbox(const SolveCtx& x) {
   return launch_smallbox(b, x.s);
 }
 
+// Norm all-reduce over peer memory (control blocks of every rank mapped).
+static px_status peer_allreduce(const px_comm* c, double* d_max, double* d_sum, int32_t n, cudaStream_t s) {
+  const P2PState& st = c->p2p;
+  if (c->nranks > PX_PEER_MAX) return fail(PX_ERR_UNSUPPORTED, "peer all-reduce: more than %d ranks", PX_PEER_MAX);
+  PeerAllreduce ar;
+  std::memset(&ar, 0, sizeof ar);
+  ar.d_max = d_max;
+  ar.d_sum = d_sum;
+  ar.n = n;
+  ar.nranks = c->nranks;
+  ar.rank = c->rank;
+  ar.mbox_own = reinterpret_cast<double*>(st.ctl + CTL_MBOX);
+  for (int32_t r = 0; r < c->nranks; ++r) {
+    ar.mbox[r] = reinterpret_cast<const double*>(st.ctl_of[r] + CTL_MBOX);
+    ar.arrive[r] = st.ctl_of[r] + CTL_AR_ARRIVE;
+    ar.done[r] = st.ctl_of[r] + CTL_AR_DONE;
+  }
+  ar.own_arrive = st.ctl + CTL_AR_ARRIVE;
+  ar.own_done = st.ctl + CTL_AR_DONE;
+  ar.round = st.ctl + CTL_AR_ROUND;
+  return launch_peer_allreduce(ar, s);
+}
+
+// Does this solve run in the fused peer-memory push mode?  Needs registered
+// buffers (either order), k = 1 and a slab the TMA kernel can push from.
+// *G = arrivals per side per sweep, *swap = phi is the registered scratch.
+static bool p2p_mode(const SolveCtx& x, int32_t* G, bool* swap) {
+  if (!x.c || !comm_exchanges(x.l, x.c) || x.nparts != 1) return false;
+  const P2PState& st = x.c->p2p;
+  if (!st.enabled || st.layout_gen != layout_generation(x.l) || st.rank != x.rank) return false;
+  if (x.o->temporal_k > 1 || x.o->nsweeps <= 0) return false;
+  if (x.phi[0].data == st.bufs[0] && x.scr[0].data == st.bufs[1]) {
+    *swap = false;
+  } else if (x.phi[0].data == st.bufs[1] && x.scr[0].data == st.bufs[0]) {
+    *swap = true;
+  } else {
+    return false;
+  }
+  px_local_info li;
+  if (local_info(x.l, x.rank, &li) != PX_OK) return false;
+  if (ext(li.owned, 1) <= 2 * x.l->ghost) return false;
+  StreamLaunch a;
+  px_patch outp = x.scr[0];
+  if (make_stream_launch(MODE_RELAX, x.p->stencil, stencil_scale(x.p->stencil, x.p->h), x.p->lambda, &x.phi[0],
+                         &x.rhs[0], &outp, li.owned, &a) != PX_OK)
+    return false;
+  a.ps.on = 1;
+  a.ps.g = x.l->ghost;
+  *G = bulk_push_arrivals(a);
+  return *G > 0;
+}
+
+// Push-mode exchange of φ^0: local ghost fill, then the boundary rows (full
+// padded rows) into both buffers of each neighbour, one arrival per side.
+static px_status push_init(const SolveCtx& x, const px_local_info& li) {
+  PX_TRY(launch_fill_ghosts(x.l, x.rank, x.phi[0], x.s));
+  const P2PState& st = x.c->p2p;
+  const int32_t g = x.l->ghost, x0 = li.owned.lo.c[0];
+  PushInit pi;
+  std::memset(&pi, 0, sizeof pi);
+  pi.src_lo = at(x.phi[0], x0 - g, li.owned.lo.c[1]);
+  pi.src_hi = at(x.phi[0], x0 - g, li.owned.hi.c[1] - g + 1);
+  pi.ld = x.phi[0].ld;
+  pi.row_len = ext(li.owned, 0) + 2 * g;
+  pi.g = g;
+  for (int side = 0; side < 2; ++side) {
+    const int32_t pr = side == 0 ? li.nbr_lo : li.nbr_hi;
+    if (pr < 0) continue;
+    px_local_info nli;
+    PX_TRY(local_info(x.l, pr, &nli));
+    const int32_t ty = side == 0 ? nli.owned.hi.c[1] + 1 : nli.owned.lo.c[1] - g;  // their ghost rows
+    const int64_t off = (int64_t)(x0 - g - nli.alloc.lo.c[0]) + (int64_t)(ty - nli.alloc.lo.c[1]) * nli.ld;
+    for (int b = 0; b < 2; ++b) pi.dst[side][b] = (side == 0 ? st.peer_lo[b] : st.peer_hi[b]) + off;
+    pi.rflag[side] = st.ctl_of[pr] + (side == 0 ? CTL_FROM_HI : CTL_FROM_LO);
+  }
+  return launch_push_init(pi, x.s);
+}
+
 // Enqueue the whole solve on x.s (directly, or under graph capture).
 static px_status enqueue_solve(const SolveCtx& x) {
   const int32_t N = x.o->nsweeps, E = x.o->norm_every;
   Plan* plan = x.plan;
   const bool nccl_multi = comm_exchanges(x.l, x.c);
   if (smallbox_path(x)) return enqueue_smallbox(x);
+  // fused peer-memory push (px_comm_p2p_import): no NCCL call in the solve
+  int32_t G = 0;
+  bool swap = false;
+  const bool p2p = p2p_mode(x, &G, &swap);
+  if (x.c && !x.c->nccl && !p2p && comm_exchanges(x.l, x.c))
+    return fail(PX_ERR_UNSUPPORTED,
+                "a peer-memory communicator solves only in push mode (registered buffers, temporal_k = 1, "
+                "even slab width, more than 2g rows)");
+  px_local_info pli;
+  PX_TRY(local_info(x.l, x.c ? x.rank : 0, &pli));
   // exchange ghosts of φ^0
-  PX_TRY(exchange_all(x, x.phi));
+  NvtxRange r_ex(p2p ? "protox/exchange_phi0 (peer push)" : "protox/exchange_phi0");
+  if (p2p) {
+    PX_TRY(launch_epoch_bump(x.c->p2p.ctl + CTL_EPOCH, PX_PUSH_INIT_CTAS + (unsigned long long)x.o->nsweeps * G, x.s));
+    PX_TRY(push_init(x, pli));
+  } else {
+    PX_TRY(exchange_all(x, x.phi));
+  }
   // FIXED_GHOSTS: the caller's ghost cells at domain faces belong to every
   // iterate (oracle R5); copy them into the scratch buffer once.
   if (x.l->bc == PX_BC_FIXED_GHOSTS) {
@@ -508,47 +633,52 @@ static px_status enqueue_solve(const SolveCtx& x) {
     std::swap(cur, nxt);
     it += K;
   }
-  // Fused halo push over peer memory (px_comm_enable_p2p): the boundary-row
-  // launches store their rows into the neighbours' ghost rows and count their
-  // arrival; the next sweep's boundary launches wait for it.  No NCCL call
-  // and no comm stream per sweep.
-  px_local_info pli;
-  PX_TRY(local_info(x.l, x.rank, &pli));
-  const bool p2p = nccl_multi && K == 1 && x.c->p2p.enabled && x.c->p2p.layout_gen == layout_generation(x.l) &&
-                   x.c->p2p.rank == x.rank && x.phi[0].data == x.c->p2p.bufs[0] &&
-                   x.scr[0].data == x.c->p2p.bufs[1] && ext(pli.owned, 1) > 2 * x.l->ghost && it < N;
-  unsigned long long G = 0;
-  const int32_t it0 = it;
+  // Fused halo push over peer memory: ONE k_bulk launch per sweep stores the
+  // slab's boundary rows into the neighbours' ghost rows and counts arrivals;
+  // its boundary items wait for the neighbours' pushes of the previous sweep
+  // (φ^0's rows: push_init).  No NCCL call and no comm stream per sweep.
+  PushSpec ps;
+  std::memset(&ps, 0, sizeof ps);
+  if (p2p) {
+    const P2PState& st = x.c->p2p;
+    ps.on = 1;
+    ps.g = x.l->ghost;
+    ps.epoch = st.ctl + CTL_EPOCH;
+    for (int side = 0; side < 2; ++side) {
+      const int32_t pr = side == 0 ? pli.nbr_lo : pli.nbr_hi;
+      if (pr < 0) continue;
+      ps.rflag[side] = st.ctl_of[pr] + (side == 0 ? CTL_FROM_HI : CTL_FROM_LO);
+      ps.wflag[side] = st.ctl + (side == 0 ? CTL_FROM_LO : CTL_FROM_HI);
+    }
+  }
+  NvtxRange r_sw(p2p ? "protox/sweeps (fused push)" : nccl_multi ? "protox/sweeps (NCCL halo)" : "protox/sweeps");
   for (; it < N; ++it) {
     const int32_t slot = (E > 0 && it % E == 0) ? it / E : -1;
     std::vector<SweepLaunch> v;
     for (int32_t part = 0; part < x.nparts; ++part)
-      PX_TRY(build_part_launches(x, part, cur[part], nxt[part], false, nccl_multi, v));
+      PX_TRY(build_part_launches(x, part, cur[part], nxt[part], false, nccl_multi && !p2p, v));
+    if (p2p) {  // the push-mode launch has its own geometry: count its blocks for the norm slot
+      v[0].a.ps = ps;
+      v[0].blocks = launch_blocks(MODE_RELAX, v[0].a);
+    }
     set_slot(v, 0, plan, slot);
     if (p2p) {
       const P2PState& st = x.c->p2p;
-      const int nb = (it & 1) ? 0 : 1;  // the neighbours' buffer this sweep writes (their "next")
+      const int nb = ((swap ? 1 : 0) + it + 1) & 1;  // the neighbours' buffer this sweep writes (their "next")
       const int32_t g = x.l->ghost, x0 = pli.owned.lo.c[0];
-      G = (unsigned long long)stream_launch_blocks_ldg(v[0].a);
-      // arrival base of this solve += the previous solve's arrivals per side
-      if (it == it0) PX_TRY(launch_epoch_bump(st.epoch, (unsigned long long)(N - it0) * G, x.s));
+      StreamLaunch& a = v[0].a;
+      a.ps.wcount = PX_PUSH_INIT_CTAS + (unsigned long long)it * G;
+      a.ps.rel = it > 0;  // publish sweep it-1's pushes
       for (int side = 0; side < 2; ++side) {
-        StreamLaunch& a = v[side].a;
         const int32_t pr = side == 0 ? pli.nbr_lo : pli.nbr_hi;
         if (pr < 0) continue;
         px_local_info nli;
         PX_TRY(local_info(x.l, pr, &nli));
         const int32_t ty = side == 0 ? nli.owned.hi.c[1] + 1 : nli.owned.lo.c[1] - g;  // their ghost rows
         double* base = side == 0 ? st.peer_lo[nb] : st.peer_hi[nb];
-        a.rs.rdst = base + (int64_t)(x0 - nli.alloc.lo.c[0]) + (int64_t)(ty - nli.alloc.lo.c[1]) * nli.ld;
-        a.rs.rflag = side == 0 ? st.peer_flags_lo + 1 : st.peer_flags_hi + 0;
-        a.rs.epoch = st.epoch;
-        if (it > it0) {
-          a.rs.wflag = st.flags + side;
-          a.rs.wcount = (unsigned long long)(it - it0) * G;
-        }
+        a.ps.rdst[side] = base + (int64_t)(x0 - nli.alloc.lo.c[0]) + (int64_t)(ty - nli.alloc.lo.c[1]) * nli.ld;
       }
-      for (auto& sl : v) PX_TRY(launch_stream(MODE_RELAX, x.p->stencil, sl.a, x.s));
+      PX_TRY(launch_stream(MODE_RELAX, x.p->stencil, a, x.s));
     } else if (nccl_multi) {
       // boundary rows, exchange on the comm stream, interior concurrently
       const bool split = v.size() == 3;
@@ -568,15 +698,10 @@ static px_status enqueue_solve(const SolveCtx& x) {
   }
   const int32_t entry = plan->n_entries - 1;
   if (p2p) {  // φ^N's ghost rows: the last sweep's pushes must have arrived
-    for (int side = 0; side < 2; ++side) {
-      if ((side == 0 ? pli.nbr_lo : pli.nbr_hi) < 0) continue;
-      RemoteSpec w;
-      std::memset(&w, 0, sizeof w);
-      w.wflag = x.c->p2p.flags + side;
-      w.epoch = x.c->p2p.epoch;
-      w.wcount = (unsigned long long)(N - it0) * G;
-      PX_TRY(launch_wait(w, x.s));
-    }
+    PushSpec w = ps;
+    w.wcount = PX_PUSH_INIT_CTAS + (unsigned long long)N * G;
+    w.rel = 1;  // publish the last sweep's pushes
+    PX_TRY(launch_wait(w, x.s));
   }
   if (E >= 0) {
     std::vector<SweepLaunch> v;
@@ -585,7 +710,10 @@ static px_status enqueue_solve(const SolveCtx& x) {
     set_slot(v, 0, plan, entry);
     for (auto& sl : v) PX_TRY(launch_stream(MODE_RESID, x.p->stencil, sl.a, x.s));
   }
-  if (nccl_multi && plan->n_entries > 0) {
+  NvtxRange r_ar("protox/norm_allreduce");
+  if (p2p && plan->n_entries > 0) {
+    PX_TRY(peer_allreduce(x.c, plan->d_max, plan->d_sum, plan->n_entries, x.s));
+  } else if (nccl_multi && plan->n_entries > 0) {
     // max|r| as u64 bit patterns (|r| >= 0, so the order of the patterns is the
     // order of the values, and a NaN -- exponent all ones, sign clear -- is
     // above +inf): exact and NaN-propagating on every rank (R7).
@@ -625,6 +753,12 @@ px_status px_comm_unique_id(uint8_t id[128]) {
   return PX_OK;
 }
 
+static px_status comm_streams(px_comm* c) {
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  return cuda_check(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, hi), "comm stream");
+}
+
 px_status px_comm_create(const uint8_t id[128], int32_t nranks, int32_t rank, int32_t device,
                          px_comm** out) {
   if (!id || !out) return fail(PX_ERR_ARG, "null argument");
@@ -642,12 +776,35 @@ px_status px_comm_create(const uint8_t id[128], int32_t nranks, int32_t rank, in
     const char* e = getenv("PROTOX_NCCL_SELF_EXCHANGE");
     c->self_exchange = e && e[0] == '1';
   }
-  int lo = 0, hi = 0;
-  cudaDeviceGetStreamPriorityRange(&lo, &hi);
-  PX_TRY(cuda_check(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, hi),
-                    "comm stream"));
+  PX_TRY(comm_streams(c.get()));
   *out = c.release();
   return PX_OK;
+}
+
+px_status px_comm_create_peer(int32_t nranks, int32_t rank, int32_t device, px_comm** out) {
+  if (!out) return fail(PX_ERR_ARG, "null argument");
+  *out = nullptr;
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(PX_ERR_ARG, "bad rank/nranks");
+  if (nranks > PX_PEER_MAX) return fail(PX_ERR_UNSUPPORTED, "peer communicator: at most %d ranks", PX_PEER_MAX);
+  PX_TRY(cuda_check(cudaSetDevice(device), "cudaSetDevice"));
+  std::unique_ptr<px_comm> c(new px_comm());
+  c->nranks = nranks;
+  c->rank = rank;
+  c->device = device;
+  if (nranks == 1) {
+    const char* e = getenv("PROTOX_NCCL_SELF_EXCHANGE");
+    c->self_exchange = e && e[0] == '1';
+  }
+  PX_TRY(comm_streams(c.get()));
+  *out = c.release();
+  return PX_OK;
+}
+
+static void p2p_close(P2PState& st) {
+  for (void* b : st.opened) cudaIpcCloseMemHandle(b);
+  st.opened.clear();
+  st.ctl_of.clear();
+  st.enabled = false;
 }
 
 void px_comm_destroy(px_comm* c) {
@@ -657,8 +814,8 @@ void px_comm_destroy(px_comm* c) {
   auto& v = plans();
   v.erase(std::remove_if(v.begin(), v.end(), [c](const std::unique_ptr<Plan>& p) { return p->key.comm == c; }),
           v.end());
-  for (void* b : c->p2p.opened) cudaIpcCloseMemHandle(b);
-  if (c->p2p.flags) cudaFree(c->p2p.flags);
+  p2p_close(c->p2p);
+  if (c->p2p.ctl) cudaFree(c->p2p.ctl);
   if (c->nccl) ncclCommDestroy(c->nccl);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -684,14 +841,9 @@ static px_status alloc_base(const void* p, void** base, size_t* off) {
   return PX_OK;
 }
 
-struct P2PExport {
-  cudaIpcMemHandle_t h[3];   // A, B, flags
-  uint64_t off[3];
-};
-
-px_status px_comm_enable_p2p(px_comm* c, const px_layout* l, int32_t rank, const px_patch* phi,
-                             const px_patch* phi_scratch) {
-  if (!c || !l || !phi || !phi_scratch) return fail(PX_ERR_ARG, "null argument");
+px_status px_comm_p2p_export(px_comm* c, const px_layout* l, int32_t rank, const px_patch* phi,
+                             const px_patch* phi_scratch, uint8_t* blob) {
+  if (!c || !l || !phi || !phi_scratch || !blob) return fail(PX_ERR_ARG, "null argument");
   if (c->nranks != l->nranks || c->rank != rank)
     return fail(PX_ERR_STATE, "communicator (rank %d of %d) does not match layout/rank", c->rank, c->nranks);
   px_local_info li;
@@ -699,77 +851,138 @@ px_status px_comm_enable_p2p(px_comm* c, const px_layout* l, int32_t rank, const
   PX_TRY(check_rank_patch(l, rank, phi_scratch, "phi_scratch", &li));
   if (!comm_exchanges(l, c))
     return fail(PX_ERR_UNSUPPORTED, "peer halo push needs a multi-rank layout (or the 1-rank periodic self-exchange mode)");
+  if (phi->data == phi_scratch->data) return fail(PX_ERR_ARG, "phi and phi_scratch must differ");
   P2PState& st = c->p2p;
-  for (void* b : st.opened) cudaIpcCloseMemHandle(b);
-  st.opened.clear();
-  if (!st.flags) {
-    PX_TRY(cuda_check(cudaMalloc(&st.flags, 4 * sizeof(unsigned long long)), "cudaMalloc flags"));
-  }
-  PX_TRY(cuda_check(cudaMemset(st.flags, 0, 4 * sizeof(unsigned long long)), "memset flags"));
-  st.epoch = st.flags + 2;
+  p2p_close(st);
+  if (!st.ctl) PX_TRY(cuda_check(cudaMalloc(&st.ctl, CTL_BYTES), "cudaMalloc control block"));
+  // counters restart at zero: no peer can push before it imports this record
+  PX_TRY(cuda_check(cudaMemset(st.ctl, 0, CTL_BYTES), "memset control block"));
+  PX_TRY(cuda_check(cudaDeviceSynchronize(), "memset control block"));
   st.bufs[0] = phi->data;
   st.bufs[1] = phi_scratch->data;
   st.layout_gen = layout_generation(l);
   st.rank = rank;
+  P2PBlob mine;
+  std::memset(&mine, 0, sizeof mine);
+  mine.magic = P2P_MAGIC;
+  mine.rank = rank;
+  mine.nranks = c->nranks;
+  mine.ld = li.ld;
+  mine.n0 = ext(li.owned, 0);
+  if (c->nranks > 1) {
+    const void* ptrs[3] = {phi->data, phi_scratch->data, st.ctl};
+    for (int i = 0; i < 3; ++i) {
+      void* base = nullptr;
+      size_t off = 0;
+      PX_TRY(alloc_base(ptrs[i], &base, &off));
+      PX_TRY(cuda_check(cudaIpcGetMemHandle(&mine.h[i], base), "cudaIpcGetMemHandle"));
+      mine.off[i] = off;
+    }
+  }
+  std::memset(blob, 0, PX_P2P_BLOB_BYTES);
+  std::memcpy(blob, &mine, sizeof mine);
+  st.exported = true;
+  return PX_OK;
+}
+
+px_status px_comm_p2p_import(px_comm* c, const px_layout* l, const uint8_t* blobs) {
+  if (!c || !l || !blobs) return fail(PX_ERR_ARG, "null argument");
+  P2PState& st = c->p2p;
+  if (!st.exported || st.layout_gen != layout_generation(l))
+    return fail(PX_ERR_STATE, "px_comm_p2p_import before px_comm_p2p_export of this layout");
+  p2p_close(st);
+  std::vector<P2PBlob> all(c->nranks);
+  px_local_info li;
+  PX_TRY(local_info(l, st.rank, &li));
+  for (int32_t r = 0; r < c->nranks; ++r) {
+    std::memcpy(&all[r], blobs + (size_t)r * PX_P2P_BLOB_BYTES, sizeof(P2PBlob));
+    if (all[r].magic != P2P_MAGIC || all[r].rank != r || all[r].nranks != c->nranks)
+      return fail(PX_ERR_ARG, "p2p record %d is not rank %d's export for %d ranks", r, r, c->nranks);
+    if (all[r].ld != li.ld || all[r].n0 != ext(li.owned, 0))
+      return fail(PX_ERR_SHAPE, "p2p record %d: slab pitch/width differ from this rank's layout", r);
+  }
+  st.ctl_of.assign(c->nranks, nullptr);
+  st.ctl_of[st.rank] = st.ctl;
   if (c->nranks == 1) {  // self-exchange: the neighbour is this rank
     for (int b = 0; b < 2; ++b) st.peer_lo[b] = st.peer_hi[b] = const_cast<double*>(st.bufs[b]);
-    st.peer_flags_lo = st.peer_flags_hi = st.flags;
     st.enabled = true;
     return PX_OK;
   }
-  // export (allocation handle, offset) of A, B and the flags; all-gather over NCCL
-  P2PExport mine;
-  std::memset(&mine, 0, sizeof mine);
-  const void* ptrs[3] = {phi->data, phi_scratch->data, st.flags};
-  for (int i = 0; i < 3; ++i) {
-    void* base = nullptr;
-    size_t off = 0;
-    PX_TRY(alloc_base(ptrs[i], &base, &off));
-    PX_TRY(cuda_check(cudaIpcGetMemHandle(&mine.h[i], base), "cudaIpcGetMemHandle"));
-    mine.off[i] = off;
+  auto open = [&](int32_t r, int i, void** out) -> px_status {
+    void* b = nullptr;
+    PX_TRY(cuda_check(cudaIpcOpenMemHandle(&b, all[r].h[i], cudaIpcMemLazyEnablePeerAccess),
+                      "cudaIpcOpenMemHandle"));
+    st.opened.push_back(b);
+    *out = (uint8_t*)b + all[r].off[i];
+    return PX_OK;
+  };
+  px_status stt = PX_OK;
+  for (int32_t r = 0; r < c->nranks && stt == PX_OK; ++r) {  // every rank's control block (all-reduce)
+    if (r == st.rank) continue;
+    void* p = nullptr;
+    stt = open(r, 2, &p);
+    st.ctl_of[r] = (unsigned long long*)p;
   }
-  const size_t sz = sizeof(P2PExport);
-  uint8_t* d = nullptr;
-  PX_TRY(cuda_check(cudaMalloc(&d, sz * (c->nranks + 1)), "cudaMalloc exchange"));
-  std::vector<P2PExport> all(c->nranks);
-  px_status stt = cuda_check(cudaMemcpy(d + sz * c->nranks, &mine, sz, cudaMemcpyHostToDevice), "H2D");
-  if (stt == PX_OK)
-    stt = nccl_check(ncclAllGather(d + sz * c->nranks, d, sz, ncclUint8, c->nccl, c->stream), "ncclAllGather");
-  if (stt == PX_OK) stt = cuda_check(cudaStreamSynchronize(c->stream), "all-gather");
-  if (stt == PX_OK) stt = cuda_check(cudaMemcpy(all.data(), d, sz * c->nranks, cudaMemcpyDeviceToHost), "D2H");
-  cudaFree(d);
-  PX_TRY(stt);
-  int32_t peers[2] = {li.nbr_lo, li.nbr_hi};
-  void* mapped[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
-  for (int side = 0; side < 2; ++side) {
+  const int32_t peers[2] = {li.nbr_lo, li.nbr_hi};
+  double* mapped[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  for (int side = 0; side < 2 && stt == PX_OK; ++side) {
     const int32_t pr = peers[side];
     if (pr < 0) continue;
     if (side == 1 && pr == peers[0]) {  // same neighbour on both sides (P = 2): map once
-      for (int i = 0; i < 3; ++i) mapped[1][i] = mapped[0][i];
+      mapped[1][0] = mapped[0][0];
+      mapped[1][1] = mapped[0][1];
       continue;
     }
-    for (int i = 0; i < 3; ++i) {
-      void* b = nullptr;
-      PX_TRY(cuda_check(cudaIpcOpenMemHandle(&b, all[pr].h[i], cudaIpcMemLazyEnablePeerAccess),
-                        "cudaIpcOpenMemHandle"));
-      st.opened.push_back(b);
-      mapped[side][i] = (uint8_t*)b + all[pr].off[i];
+    for (int i = 0; i < 2 && stt == PX_OK; ++i) {
+      void* p = nullptr;
+      stt = open(pr, i, &p);
+      mapped[side][i] = (double*)p;
     }
   }
-  for (int b = 0; b < 2; ++b) {
-    st.peer_lo[b] = (double*)mapped[0][b];
-    st.peer_hi[b] = (double*)mapped[1][b];
+  if (stt != PX_OK) {
+    p2p_close(st);
+    return stt;
   }
-  st.peer_flags_lo = (unsigned long long*)mapped[0][2];
-  st.peer_flags_hi = (unsigned long long*)mapped[1][2];
+  for (int b = 0; b < 2; ++b) {
+    st.peer_lo[b] = mapped[0][b];
+    st.peer_hi[b] = mapped[1][b];
+  }
   st.enabled = true;
   return PX_OK;
+}
+
+px_status px_comm_enable_p2p(px_comm* c, const px_layout* l, int32_t rank, const px_patch* phi,
+                             const px_patch* phi_scratch) {
+  if (!c) return fail(PX_ERR_ARG, "null argument");
+  std::vector<uint8_t> all((size_t)PX_P2P_BLOB_BYTES * c->nranks);
+  uint8_t* mine = all.data() + (size_t)PX_P2P_BLOB_BYTES * rank;
+  PX_TRY(px_comm_p2p_export(c, l, rank, phi, phi_scratch, mine));
+  if (c->nranks > 1) {
+    if (!c->nccl) return fail(PX_ERR_STATE, "px_comm_enable_p2p needs NCCL; use px_comm_p2p_export/_import");
+    // all-gather the records over NCCL
+    const size_t sz = PX_P2P_BLOB_BYTES;
+    uint8_t* d = nullptr;
+    PX_TRY(cuda_check(cudaMalloc(&d, sz * (c->nranks + 1)), "cudaMalloc exchange"));
+    px_status stt = cuda_check(cudaMemcpy(d + sz * c->nranks, mine, sz, cudaMemcpyHostToDevice), "H2D");
+    if (stt == PX_OK)
+      stt = nccl_check(ncclAllGather(d + sz * c->nranks, d, sz, ncclUint8, c->nccl, c->stream), "ncclAllGather");
+    if (stt == PX_OK) stt = cuda_check(cudaStreamSynchronize(c->stream), "all-gather");
+    if (stt == PX_OK) stt = cuda_check(cudaMemcpy(all.data(), d, sz * c->nranks, cudaMemcpyDeviceToHost), "D2H");
+    cudaFree(d);
+    PX_TRY(stt);
+  }
+  return px_comm_p2p_import(c, l, all.data());
 }
 
 px_status px_comm_allreduce_norms(px_comm* c, double* d_max, double* d_sum, int32_t n,
                                   void* stream) {
   if (!c || !d_max || !d_sum || n < 0) return fail(PX_ERR_ARG, "bad argument");
   cudaStream_t s = (cudaStream_t)stream;
+  if (!c->nccl) {
+    if (c->nranks == 1) return PX_OK;
+    if (!c->p2p.enabled) return fail(PX_ERR_STATE, "peer communicator: px_comm_p2p_import first");
+    return peer_allreduce(c, d_max, d_sum, n, s);
+  }
   PX_TRY(nccl_check(ncclGroupStart(), "ncclGroupStart"));
   // max as u64 bit patterns of non-negative doubles (NaN-propagating, R7)
   PX_TRY(nccl_check(ncclAllReduce(d_max, d_max, n, ncclUint64, ncclMax, c->nccl, s), "ncclAllReduce"));
@@ -786,6 +999,8 @@ px_status px_exchange_ghosts(const px_layout* l, px_comm* c, int32_t rank, px_pa
     return fail(PX_ERR_STATE, "communicator (rank %d of %d) does not match layout/rank", c->rank,
                 c->nranks);
   cudaStream_t s = (cudaStream_t)stream;
+  if (comm_exchanges(l, c) && !c->nccl)
+    return fail(PX_ERR_UNSUPPORTED, "px_exchange_ghosts: the peer-memory communicator exchanges inside px_solve only");
   PX_TRY(launch_fill_ghosts(l, rank, *phi, s));
   if (comm_exchanges(l, c)) PX_TRY(nccl_rows(l, c, rank, *phi, s));
   return PX_OK;
@@ -956,6 +1171,7 @@ px_status px_solve(const px_layout* l, px_comm* c, int32_t rank, const px_relax_
                    const px_patch* rhs, double* h_norms, int32_t cap, int32_t* n_written,
                    int32_t* in_scratch, void* stream) {
   if (cap < 0 || (cap > 0 && !h_norms)) return fail(PX_ERR_ARG, "bad norm output");
+  NvtxRange r_solve("protox/px_solve");
   Plan* plan = nullptr;
   bool odd = false;
   int32_t nparts = 1;

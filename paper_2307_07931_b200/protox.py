@@ -9,13 +9,15 @@ call raises.
 from __future__ import annotations
 
 import ctypes
+import types
 import os
 from dataclasses import dataclass
 
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libprotox.so")
+# PROTOX_LIB: another build of the same library (A/B measurements only)
+LIB_PATH = os.environ.get("PROTOX_LIB") or os.path.join(_PKG, "libprotox.so")
 
 # ---------------------------------------------------------------- constants
 PX_OK, PX_ERR_ARG, PX_ERR_SHAPE, PX_ERR_DOMAIN, PX_ERR_ALIGN = 0, 1, 2, 3, 4
@@ -96,7 +98,7 @@ EXPORTS = [
     "px_stencil_apply", "px_relax_step", "px_relax_block", "px_residual_norm", "px_mehrstellen_rhs",
     "px_init_field", "px_fill_ghosts",
     "px_comm_unique_id", "px_comm_create", "px_comm_destroy", "px_comm_allreduce_norms",
-    "px_comm_enable_p2p",
+    "px_comm_enable_p2p", "px_comm_create_peer", "px_comm_p2p_export", "px_comm_p2p_import",
     "px_exchange_ghosts", "px_exchange_ghosts_local",
     "px_solve", "px_solve_host", "px_solve_host_batch", "px_release_cached", "px_mg_solve", "px_mg_release", "px_kernel_launch_count",
     "px_last_solve_kernels",
@@ -104,6 +106,19 @@ EXPORTS = [
     "px3_layout", "px3_norm_buffer_len", "px3_init_field", "px3_fill_ghosts", "px3_relax_step",
     "px3_residual_norm", "px3_solve", "px3_solve_host_batch", "px3_release", "px3_mehrstellen_rhs", "px3_slab", "px3_solve_comm",
 ]
+
+
+class _Older:
+    """Attribute sink over an older libprotox build (PROTOX_LIB A/B runs)."""
+
+    def __init__(self, L):
+        self._L = L
+
+    def __getattr__(self, name):
+        try:
+            return getattr(self._L, name)
+        except AttributeError:
+            return types.SimpleNamespace()
 
 
 def lib():
@@ -114,6 +129,9 @@ def lib():
     if not os.path.exists(LIB_PATH):
         raise RuntimeError(f"libprotox.so not built ({LIB_PATH}); run __graft_entry__.build()")
     L = ctypes.CDLL(LIB_PATH)
+    real = L
+    if os.environ.get("PROTOX_LIB"):
+        L = _Older(L)  # an older build (A/B): symbols it lacks are skipped
     st, i32, i64, vp = ctypes.c_int, ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p
     P = ctypes.POINTER
     L.px_status_str.restype = ctypes.c_char_p
@@ -168,6 +186,12 @@ def lib():
     L.px_comm_destroy.argtypes = [vp]
     L.px_comm_enable_p2p.restype = st
     L.px_comm_enable_p2p.argtypes = [vp, vp, i32, P(px_patch), P(px_patch)]
+    L.px_comm_create_peer.restype = st
+    L.px_comm_create_peer.argtypes = [i32, i32, i32, P(vp)]
+    L.px_comm_p2p_export.restype = st
+    L.px_comm_p2p_export.argtypes = [vp, vp, i32, P(px_patch), P(px_patch), ctypes.c_char_p]
+    L.px_comm_p2p_import.restype = st
+    L.px_comm_p2p_import.argtypes = [vp, vp, ctypes.c_char_p]
     L.px_comm_allreduce_norms.restype = st
     L.px_comm_allreduce_norms.argtypes = [vp, vp, vp, i32, vp]
     L.px_exchange_ghosts.restype = st
@@ -221,8 +245,8 @@ def lib():
     L.px3_mehrstellen_rhs.argtypes = [P(px_patch3), P(px_patch3), vp]
     L.px_relax_variant.restype = i32
     L.px_relax_variant.argtypes = [P(px_patch), P(px_patch), P(px_patch), px_box]
-    _lib = L
-    return L
+    _lib = real
+    return real
 
 
 class PxError(RuntimeError):
@@ -393,11 +417,15 @@ def fill_ghosts(layout: Layout, rank: int, phi: px_patch, stream=None):
 
 # ---------------------------------------------------------------- comm
 class Comm:
-    """NCCL communicator (one process per GPU)."""
+    """Communicator (one process per GPU): NCCL (px_comm_create), or with
+    uid=None peer memory only (px_comm_create_peer)."""
 
-    def __init__(self, uid: bytes, nranks: int, rank: int, device: int):
+    def __init__(self, uid, nranks: int, rank: int, device: int):
         h = ctypes.c_void_p()
-        _check(lib().px_comm_create(uid, nranks, rank, device, ctypes.byref(h)))
+        if uid is None:
+            _check(lib().px_comm_create_peer(nranks, rank, device, ctypes.byref(h)))
+        else:
+            _check(lib().px_comm_create(uid, nranks, rank, device, ctypes.byref(h)))
         self.h = h
         self.nranks, self.rank = nranks, rank
 
@@ -420,6 +448,24 @@ def comm_unique_id() -> bytes:
 def comm_enable_p2p(comm: Comm, layout: Layout, rank: int, phi: px_patch, phi_scratch: px_patch):
     """px_comm_enable_p2p: fused halo push over peer memory for px_solve."""
     _check(lib().px_comm_enable_p2p(comm.h, layout.h, rank, ctypes.byref(phi), ctypes.byref(phi_scratch)))
+
+
+P2P_BLOB_BYTES = 256  # PX_P2P_BLOB_BYTES
+
+
+def comm_p2p_export(comm: Comm, layout: Layout, rank: int, phi: px_patch, phi_scratch: px_patch) -> bytes:
+    """px_comm_p2p_export: register the solve buffers, return this rank's record."""
+    buf = ctypes.create_string_buffer(P2P_BLOB_BYTES)
+    _check(lib().px_comm_p2p_export(comm.h, layout.h, rank, ctypes.byref(phi), ctypes.byref(phi_scratch), buf))
+    return buf.raw
+
+
+def comm_p2p_import(comm: Comm, layout: Layout, records) -> None:
+    """px_comm_p2p_import: records = every rank's export, in rank order."""
+    blob = b"".join(bytes(r) for r in records)
+    if len(blob) != P2P_BLOB_BYTES * comm.nranks:
+        raise ValueError("need one record per rank")
+    _check(lib().px_comm_p2p_import(comm.h, layout.h, blob))
 
 
 def comm_allreduce_norms(comm: Comm, d_max, d_sum, n: int, stream=None):

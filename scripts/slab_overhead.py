@@ -41,7 +41,7 @@ for p in ps:
     P.init_field(lay, 0, lay.patch(0, r), P.PX_FIELD_HASH, inputs.DEFAULT_SEED, stream=s)
     prm = P.relax_params(h, h * h / 8)
     pa, pb, pr = lay.patch(0, a), lay.patch(0, b), lay.patch(0, r)
-    out = {"P": p, "slab": [n0, n1]}
+    out = {"P": p, "slab": [n0, n1], "lib": os.path.basename(P.LIB_PATH)}
     # the sweep kernel alone
     nb = P.norm_buffer(li.owned)
     s.wait_stream(torch.cuda.current_stream())
@@ -53,7 +53,7 @@ for p in ps:
         e1.record(s)
     s.synchronize()
     out["kernel_ms"] = sum(e0.elapsed_time(e1) for e0, e1 in evs[3:]) / 20
-    for mode in ("local", "nccl", "p2p"):
+    for mode in os.environ.get("SLAB_MODES", "local,nccl,p2p").split(","):
         comm = None
         if mode != "local":
             comm = P.Comm(P.comm_unique_id(), 1, 0, torch.cuda.current_device())

@@ -647,39 +647,62 @@ def test_nccl_allreduce_norms_single_rank():
         comm.close()
 
 
-@pytest.mark.parametrize("graph", [True, False])
-def test_p2p_halo_push_self_exchange(graph, monkeypatch):
-    """Fused halo push over peer memory (px_comm_enable_p2p), self-exchange
-    mode on one GPU: the boundary-row kernels store their rows (and x images)
-    into the 'neighbour's' ghost rows and count arrivals; the next sweep's
-    boundary kernels wait for them.  Two consecutive solves (epoch counters),
-    graph and non-graph: bit-identical to 2N oracle sweeps."""
+@pytest.mark.parametrize("graph,kind,n0,n1,N2,st", [
+    (True, "nccl", 1536, 2304, 8, 0),
+    (False, "nccl", 1536, 2304, 5, 1),
+    (True, "peer", 640, 300, 3, 0),
+    (False, "peer", 2048, 2048, 7, 1),
+])
+def test_p2p_halo_push_self_exchange(graph, kind, n0, n1, N2, st, monkeypatch):
+    """Fused halo push over peer memory, self-exchange mode on one GPU (the
+    one-rank periodic layout is its own neighbour): ONE k_bulk launch per
+    sweep stores the slab's boundary rows (and x images) into the
+    'neighbour's' ghost rows and counts arrivals; its boundary items wait for
+    them.  NCCL communicator (px_comm_enable_p2p) or peer-memory one
+    (px_comm_create_peer + export/import, no NCCL at all).  Two consecutive
+    solves of different lengths (epoch counters); the second starts from
+    whichever buffer holds the first's result (registered pair swapped).
+    Bit-identical to the oracle's N1+N2 sweeps."""
     monkeypatch.setenv("PROTOX_NCCL_SELF_EXCHANGE", "1")
-    n0, n1, N, E = 1536, 2304, 8, 2
+    N, E = 8, 2
     h = 1.0 / 2048
     lam = h * h / 8
     phi0, rho = _fields(n0, n1, 1, 404, P.PX_BC_PERIODIC)
-    lay = P.Layout(P.box(0, 0, n0 - 1, n1 - 1), (256, 256), 1, P.PX_BC_PERIODIC, 1)
-    comm = P.Comm(P.comm_unique_id(), 1, 0, torch.cuda.current_device())
+    lay = P.Layout(P.box(0, 0, n0 - 1, n1 - 1), (128, 100 if n1 == 300 else 256), 1, P.PX_BC_PERIODIC, 1)
+    uid = P.comm_unique_id() if kind == "nccl" else None
+    comm = P.Comm(uid, 1, 0, torch.cuda.current_device())
     try:
         a = to_device_ghosted(lay, 0, phi0, 1)
         b = lay.alloc(0)
         r = to_device_ghosted(lay, 0, rho, 1)
         pa, pb, pr = lay.patch(0, a), lay.patch(0, b), lay.patch(0, r)
-        P.comm_enable_p2p(comm, lay, 0, pa, pb)
+        if kind == "nccl":
+            P.comm_enable_p2p(comm, lay, 0, pa, pb)
+        else:
+            P.comm_p2p_import(comm, lay, [P.comm_p2p_export(comm, lay, 0, pa, pb)])
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
-        r1 = P.solve(lay, comm, 0, P.relax_params(h, lam), N, E, pa, pb, pr, use_graph=graph, stream=s)
+        prm = P.relax_params(h, lam, st)
+        r1 = P.solve(lay, comm, 0, prm, N, E, pa, pb, pr, use_graph=graph, stream=s)
+        assert P.last_solve_kernels() == "k_bulk"
         assert not r1.in_scratch
-        r2 = P.solve(lay, comm, 0, P.relax_params(h, lam), N, E, pa, pb, pr, use_graph=graph, stream=s)
-        out = owned_to_host(lay, 0, a)
+        r2 = P.solve(lay, comm, 0, prm, N2, E, pa, pb, pr, use_graph=graph, stream=s)
+        out = owned_to_host(lay, 0, b if r2.in_scratch else a)
+        if N2 % 2:  # continue from the scratch buffer: the registered pair in swapped order
+            r3 = P.solve(lay, comm, 0, prm, 2, E, pb, pa, pr, use_graph=graph, stream=s)
+            assert P.last_solve_kernels() == "k_bulk"
+            out = owned_to_host(lay, 0, a if r3.in_scratch else b)
     finally:
         comm.close()
-    ref, rn = oracle.solve(_orc_problem(n0, n1, h, lam, P.PX_BC_PERIODIC, 0, 2 * N, E), phi0, rho)
+    total = N + N2 + (2 if N2 % 2 else 0)
+    ref, rn = oracle.solve(_orc_problem(n0, n1, h, lam, P.PX_BC_PERIODIC, st, total, E), phi0, rho)
     assert bits_equal(out, ref[1:-1, 1:-1]), ulp_diff(out, ref[1:-1, 1:-1])
     # norms: first solve's entries are φ^0..φ^6, final φ^8; second continues from φ^8
-    _check_norms(r1.norms[:-1], rn[: N // E])
-    _check_norms(r2.norms, rn[N // E:])
+    _check_norms(r1.norms, rn[: N // E + 1])
+    if N2 % 2 == 0:
+        _check_norms(r2.norms, rn[N // E:])
+    else:
+        assert r2.norms[0, 0] == rn[N // E, 0]
 
 
 @pytest.mark.gpu
