@@ -178,7 +178,17 @@ __global__ void __launch_bounds__(NC * 32 + 32, CPS) k_bulk(const StreamLaunch a
       mbar_init(&empty[s], NCW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (PUSH && blockIdx.x == 0 && a.ps.rel) {
+  }
+  // Programmatic dependent launch (a.pdl: the sweep loop of px_solve): the
+  // next sweep's grid may be launched now -- its CTAs take SM slots as this
+  // grid's CTAs exit and run their prologue -- and this grid waits here
+  // until the previous sweep's grid has completed and its stores are
+  // visible (no-op without the launch attribute).  Every global access of
+  // the kernel (including the norm workspace) comes after the wait.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (PUSH && tid == 0) {
+    if (blockIdx.x == 0 && a.ps.rel) {
       // the previous sweep's pushes into the neighbours' ghost rows are
       // complete: that kernel has finished (stream order; a finished grid's
       // stores, peer stores included, are performed), so one relaxed count
@@ -187,7 +197,7 @@ __global__ void __launch_bounds__(NC * 32 + 32, CPS) k_bulk(const StreamLaunch a
         if (a.ps.rflag[side])
           asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(a.ps.rflag[side]), "l"(1ull) : "memory");
     }
-    if (PUSH && blockIdx.x < nitems) {
+    if (blockIdx.x < nitems) {
       // push mode: the boundary items (first and last row chunk) are every
       // CTA's FIRST item (they are scheduled first and the grid covers them,
       // bulk_geom), so the ghost rows the neighbours push are awaited once,
@@ -391,6 +401,17 @@ __global__ void __launch_bounds__(NC * 32 + 32, CPS) k_bulk(const StreamLaunch a
   if (a.norms.out_max) reduce_norms(a.norms, mx, ss);
 }
 
+// PROTOX_PDL=0 (read once) launches the sweep kernels without programmatic
+// dependent launch (A/B)
+static bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PROTOX_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 static int g_nsm = 0;
 static int num_sms() {
   if (!g_nsm) {
@@ -520,9 +541,17 @@ static cudaError_t launch_b(const StreamLaunch& a, cudaStream_t s) {
     attr = true;
   }
   const BulkGeom g = bulk_geom(a);
-  k_bulk<MODE, ST, NST, R, CPS, NC, PW, PUSH><<<g.grid, NC * 32 + 32, smem_bytes<NST, R, NC>(), s>>>(
-      a, g.nstrips, g.nitems, g.crows);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(g.grid);
+  cfg.blockDim = dim3(NC * 32 + 32);
+  cfg.dynamicSmemBytes = smem_bytes<NST, R, NC>();
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = (a.pdl && pdl_enabled()) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k_bulk<MODE, ST, NST, R, CPS, NC, PW, PUSH>, a, g.nstrips, g.nitems, g.crows);
 }
 
 static bool is_pow2(double v) {

@@ -129,6 +129,7 @@ struct StreamLaunch {
   GhostSpec gs;
   NormSlot norms;     // norms.out_max == null: none
   PushSpec ps;        // fused halo push / wait (k_bulk only)
+  int32_t pdl;        // launch as a programmatic dependent of the previous kernel (k_bulk only)
 };
 
 // Extra launch state of a temporal-blocking pass (px_tb.cu).

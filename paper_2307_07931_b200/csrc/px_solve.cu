@@ -652,6 +652,11 @@ static px_status enqueue_solve(const SolveCtx& x) {
     }
   }
   NvtxRange r_sw(p2p ? "protox/sweeps (fused push)" : nccl_multi ? "protox/sweeps (NCCL halo)" : "protox/sweeps");
+  // one launch per sweep (push mode, or one part without a NCCL exchange):
+  // each sweep kernel is a programmatic dependent of the previous one, so
+  // its launch and prologue overlap the previous sweep's tail
+  const bool one_launch = p2p || (!nccl_multi && x.nparts == 1);
+  const int32_t it_first = it;
   for (; it < N; ++it) {
     const int32_t slot = (E > 0 && it % E == 0) ? it / E : -1;
     std::vector<SweepLaunch> v;
@@ -662,6 +667,7 @@ static px_status enqueue_solve(const SolveCtx& x) {
       v[0].blocks = launch_blocks(MODE_RELAX, v[0].a);
     }
     set_slot(v, 0, plan, slot);
+    if (one_launch && v.size() == 1 && it > it_first) v[0].a.pdl = 1;
     if (p2p) {
       const P2PState& st = x.c->p2p;
       const int nb = ((swap ? 1 : 0) + it + 1) & 1;  // the neighbours' buffer this sweep writes (their "next")
