@@ -37,6 +37,7 @@
 
 #include "px_device.cuh"
 #include "px_internal.h"
+#include "px_ptx.cuh"
 
 namespace px {
 namespace k3 {
@@ -54,33 +55,7 @@ template <int NST>
 constexpr size_t smem_bytes() { return (size_t)NST * STAGE * sizeof(double) + 2 * NST * sizeof(uint64_t); }
 constexpr int MAX_GRID = 512;
 
-__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mb_init(uint64_t* b, uint32_t c) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(c) : "memory");
-}
-__device__ __forceinline__ void mb_expect(uint64_t* b, uint32_t tx) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(tx) : "memory");
-}
-__device__ __forceinline__ void mb_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
-}
-__device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t par) {
-  asm volatile(
-      "{\n.reg .pred P1;\nW_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra W_%=;\n}\n" ::"r"(su32(b)),
-      "r"(par)
-      : "memory");
-}
-// TMA tensor copy of one 3D box (global -> shared), completion on the mbarrier
-__device__ __forceinline__ void tma3(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar,
-                                     uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(su32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar)), "l"(pol)
-      : "memory");
-}
+using namespace ptx;
 
 }  // namespace k3
 
@@ -170,8 +145,8 @@ __global__ void __maxnreg__(ST == 1 ? 168 : 112)  // 9 warps: 3 share a sub-part
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) {
-      mb_init(&full[s], 1);
-      mb_init(&empty[s], NWC);
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NWC);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -185,14 +160,14 @@ __global__ void __maxnreg__(ST == 1 ? 168 : 112)  // 9 warps: 3 share a sub-part
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mrho)) : "memory");
       uint64_t pol, pol_halo;  // ρ: read once; φ planes: their halo rows are re-read by the neighbouring tiles
       if (a.policy == 0) {
-        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_halo));
+        pol = evict_first_policy();
+        pol_halo = evict_last_policy();
       } else if (a.policy == 1) {
-        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+        pol = evict_normal_policy();
         pol_halo = pol;
       } else {
-        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_halo));
+        pol = evict_first_policy();
+        pol_halo = evict_normal_policy();
       }
       int slot = 0;
       uint32_t phase = 0;
@@ -201,10 +176,10 @@ __global__ void __maxnreg__(ST == 1 ? 168 : 112)  // 9 warps: 3 share a sub-part
         const int x0 = tx * TX, y0 = ty * TY, z0 = zc * a.zlen, z1 = min(a.n[2], z0 + a.zlen);
         const int nstg = z1 - z0 + 2;
         for (int s = 0; s < nstg; ++s) {
-          mb_wait(&empty[slot], phase ^ 1u);
+          mbar_wait(&empty[slot], phase ^ 1u);
           double* sp = smem + (size_t)slot * STAGE;
           const bool rho = s >= 2;
-          mb_expect(&full[slot], PHI_BYTES + (rho ? RHO_BYTES : 0u));
+          mbar_arrive_expect_tx(&full[slot], PHI_BYTES + (rho ? RHO_BYTES : 0u));
           // φ plane z0-1+s with its halo: cells (x0-2.., y0-1.., z)
           tma3(sp, &mphi, x0, y0 - 1 + g, z0 - 1 + s + g, &full[slot], pol_halo);
           if (rho) tma3(sp + PHI_PAD, &mrho, x0 + 2, y0 + g, z0 - 2 + s + g, &full[slot], pol);
@@ -228,7 +203,7 @@ __global__ void __maxnreg__(ST == 1 ? 168 : 112)  // 9 warps: 3 share a sub-part
       double2 Bv[RPW];
       // stage 0: plane z0-1 -> B (7-point: its pair values in registers, the
       // stage released at once; 27-point: the whole box is held as the B plane)
-      mb_wait(&full[slot], phase);
+      mbar_wait(&full[slot], phase);
       int bslot = slot;
       if (ST == 0) {
         const double* sp = smem + (size_t)slot * STAGE;
@@ -236,21 +211,21 @@ __global__ void __maxnreg__(ST == 1 ? 168 : 112)  // 9 warps: 3 share a sub-part
         for (int i = 0; i < RPW; ++i)
           Bv[i] = *reinterpret_cast<const double2*>(sp + (RPW * warp + i + 1) * BXW + bc);
         __syncwarp();
-        if (lane == 0) mb_arrive(&empty[slot]);
+        if (lane == 0) mbar_arrive(&empty[slot]);
       }
       if (++slot == NST) {
         slot = 0;
         phase ^= 1u;
       }
       // stage 1: plane z0 (held: the C plane of the first step)
-      mb_wait(&full[slot], phase);
+      mbar_wait(&full[slot], phase);
       int cslot = slot;
       if (++slot == NST) {
         slot = 0;
         phase ^= 1u;
       }
       for (int z = z0; z < z1; ++z) {
-        mb_wait(&full[slot], phase);  // plane z+1 and ρ(z)
+        mbar_wait(&full[slot], phase);  // plane z+1 and ρ(z)
         const double* cp = smem + (size_t)cslot * STAGE;
         const double* tp = smem + (size_t)slot * STAGE;
         if (ST == 0) {
@@ -314,12 +289,12 @@ __global__ void __maxnreg__(ST == 1 ? 168 : 112)  // 9 warps: 3 share a sub-part
             k3_finish<MODE>(a, tp, brow, lane, cx, y0, z, ox0, ox1, P[1][(i + 1) % 3], L0, L1, mx, ss);
           }
           __syncwarp();
-          if (lane == 0) mb_arrive(&empty[bslot]);  // plane z-1 no longer needed
+          if (lane == 0) mbar_arrive(&empty[bslot]);  // plane z-1 no longer needed
           bslot = cslot;
         }
         if (ST == 0) {
           __syncwarp();
-          if (lane == 0) mb_arrive(&empty[cslot]);  // plane z no longer needed
+          if (lane == 0) mbar_arrive(&empty[cslot]);  // plane z no longer needed
         }
         cslot = slot;
         if (++slot == NST) {
@@ -329,10 +304,10 @@ __global__ void __maxnreg__(ST == 1 ? 168 : 112)  // 9 warps: 3 share a sub-part
       }
       if (ST == 1) {
         __syncwarp();
-        if (lane == 0) mb_arrive(&empty[bslot]);
+        if (lane == 0) mbar_arrive(&empty[bslot]);
       }
       __syncwarp();
-      if (lane == 0) mb_arrive(&empty[cslot]);  // the item's last plane
+      if (lane == 0) mbar_arrive(&empty[cslot]);  // the item's last plane
     }
   }
   if (a.norms.out_max) reduce_norms(a.norms, mx, ss);

@@ -6,14 +6,18 @@
 // [c·ny/G, (c+1)·ny/G) and keeps them in shared memory for the whole solve:
 // two copies of its rows plus one halo row above and below (with the ghost
 // columns), and its rows of the right-hand side.  A sweep reads and writes
-// shared memory only.  The CTA sweeps its first and last row first,
-// publishes them to L2 (double-buffered by sweep parity) and raises its flag
-// (release), sweeps its inner rows while they travel, then waits for the
-// flags of its two neighbours (acquire) and copies their rows into its halo.
-// No grid-wide barrier per sweep: a CTA synchronises with its two neighbours
-// only.  Domain faces: periodic wrap (the ring of CTAs), odd
-// reflection (halo row = −own row), fixed ghosts (kept from φ^0); the ghost
-// columns of every row follow the x rule after each exchange.
+// shared memory only.  The CTA sweeps its first and last row first; each
+// thread publishes its own cells of them to an L2 mailbox straight from
+// registers as LL entries (every 8-byte half carries the sweep tag, so the
+// data is its own flag: no barrier, fence or flag word before the
+// publication), sweeps its inner rows while they travel, then fetches its
+// cells of the neighbours' rows (spinning until both tags match) into its
+// halo rows.  One block barrier per sweep; no grid-wide barrier: a CTA
+// synchronises with its two neighbours only.  Domain faces: periodic wrap
+// (the ring of CTAs), odd reflection (halo row = −own row, written by the
+// thread that computed it), fixed ghosts (kept from φ^0); the thread holding
+// column 0 / nx−1 of a row also writes the ghost columns that copy or
+// reflect it.
 //
 // Per cell the oracle's expression tree with every * and + rounded
 // separately (bit-identical).  Norms: per thread in row order, per CTA in
@@ -22,8 +26,9 @@
 // e mod G.  Deterministic for a given (nx, ny, #SM).
 //
 // Safety of the two publication slots: CTA c writes φ^{s+1} rows into slot
-// (s+1)&1 during sweep s; it can write slot (s+1)&1 again (φ^{s+3}) only
-// after both neighbours raised flag s+2, i.e. after they copied φ^{s+1}.
+// (s+1)&1 during sweep s; it writes slot (s+1)&1 again (φ^{s+3}, sweep s+2)
+// only after it fetched its neighbours' φ^{s+2} rows, which they published
+// in their sweep s+1, i.e. after they fetched φ^{s+1}.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -144,6 +149,108 @@ __device__ __forceinline__ void rs_xghost(double* row, int nx, const int (&xm)[2
   else if (xm[1] == GH_REFLECT) row[nx + 2] = -row[nx + 1];
 }
 
+// ---- LL exchange (the row mailbox carries its own flags) -------------------
+// One double per 16-byte entry, each 8-byte half = half the double + the
+// sweep tag (NCCL's LL idea): a 16-byte store writes each 8-byte half
+// atomically, so a reader that sees the tag in both halves has the whole
+// value of that sweep -- no release fence, no flag word, no barrier before
+// the publication.
+__device__ __forceinline__ void ll_put(double* e, double v, uint32_t tag) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(e), "r"((uint32_t)b), "r"(tag),
+               "r"((uint32_t)(b >> 32)), "r"(tag)
+               : "memory");
+}
+__device__ __forceinline__ double ll_get(const double* e, uint32_t tag) {
+  uint32_t lo, t0, hi, t1;
+  do {
+    asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(lo), "=r"(t0), "=r"(hi), "=r"(t1)
+                 : "l"(e)
+                 : "memory");
+  } while (t0 != tag || t1 != tag);
+  return __longlong_as_double((long long)(((unsigned long long)hi << 32) | lo));
+}
+
+// The x images of one row's pair (columns 2q, 2q+1 at shared index x): the
+// thread holding column 0 / nx-1 also writes the ghost columns that copy or
+// reflect it (periodic: -1 <- nx-1, nx <- 0; reflection: -1 <- -0, nx <- -(nx-1)).
+__device__ __forceinline__ void ll_ximg(double* row, int x, int nx, double v0, double v1, const int (&xm)[2]) {
+  if (x == 2) {
+    if (xm[1] == GH_WRAP) row[nx + 2] = v0;
+    if (xm[0] == GH_REFLECT) row[1] = -v0;
+  }
+  if (x == nx) {
+    if (xm[0] == GH_WRAP) row[1] = v1;
+    if (xm[1] == GH_REFLECT) row[nx + 2] = -v1;
+  }
+}
+
+// Rows rlo..rhi of B = A + λ(scale·L(A) − F) (as rs_rows), with each row's x
+// images, and -- for row 1 / row R -- the row published to the mailbox (pub_first
+// / pub_last, 2 doubles per column) or, at a reflecting y face, its odd image
+// written into the halo row 0 / R+1 of B.
+template <int ST, bool NORM>
+__device__ __forceinline__ void ll_rows(const double* A, double* B, const double* F, int P, int nx, int R, int rlo,
+                                        int rhi, double scale, double lambda, const int (&xm)[2],
+                                        double* pub_first, double* pub_last, bool refl_top, bool refl_bot,
+                                        uint32_t tag, unsigned long long& mx, double& ss) {
+  for (int q = threadIdx.x; q < nx / 2; q += blockDim.x) {
+    const int x = 2 * q + 2;
+    const double* a0 = A + (size_t)(rlo - 1) * P + x;
+    double2 S = *reinterpret_cast<const double2*>(a0);
+    double2 C = *reinterpret_cast<const double2*>(a0 + P);
+    double sw = a0[-1], se = a0[2], cw = a0[P - 1], ce = a0[P + 2];
+    for (int r = rlo; r <= rhi; ++r) {
+      const double* an = A + (size_t)(r + 1) * P + x;
+      const double2 N = *reinterpret_cast<const double2*>(an);
+      const double nw = an[-1], ne = an[2];
+      const double L0 = rs_taps<ST>(cw, C.y, S.x, N.x, C.x, sw, S.y, nw, N.y);
+      const double L1 = rs_taps<ST>(C.x, ce, S.y, N.y, C.y, S.x, se, N.x, ne);
+      const double2 f = *reinterpret_cast<const double2*>(F + (size_t)(r - 1) * nx + (x - 2));
+      const double r0 = __dsub_rn(__dmul_rn(scale, L0), f.x);
+      const double r1 = __dsub_rn(__dmul_rn(scale, L1), f.y);
+      double2 o;
+      o.x = __dadd_rn(C.x, __dmul_rn(lambda, r0));
+      o.y = __dadd_rn(C.y, __dmul_rn(lambda, r1));
+      double* brow = B + (size_t)r * P;
+      *reinterpret_cast<double2*>(brow + x) = o;
+      ll_ximg(brow, x, nx, o.x, o.y, xm);
+      if (r == 1) {
+        if (pub_first) {
+          ll_put(pub_first + 2 * (x - 2), o.x, tag);
+          ll_put(pub_first + 2 * (x - 1), o.y, tag);
+        } else if (refl_top) {
+          *reinterpret_cast<double2*>(B + x) = make_double2(-o.x, -o.y);
+          ll_ximg(B, x, nx, -o.x, -o.y, xm);
+        }
+      }
+      if (r == R) {
+        if (pub_last) {
+          ll_put(pub_last + 2 * (x - 2), o.x, tag);
+          ll_put(pub_last + 2 * (x - 1), o.y, tag);
+        } else if (refl_bot) {
+          double* h = B + (size_t)(R + 1) * P;
+          *reinterpret_cast<double2*>(h + x) = make_double2(-o.x, -o.y);
+          ll_ximg(h, x, nx, -o.x, -o.y, xm);
+        }
+      }
+      if (NORM) {
+        mx = umax64(mx, (unsigned long long)__double_as_longlong(fabs(r0)));
+        ss = fma(r0, r0, ss);
+        mx = umax64(mx, (unsigned long long)__double_as_longlong(fabs(r1)));
+        ss = fma(r1, r1, ss);
+      }
+      S = C;
+      sw = cw;
+      se = ce;
+      C = N;
+      cw = nw;
+      ce = ne;
+    }
+  }
+}
+
 template <int ST>
 __global__ void __launch_bounds__(RS_THREADS, 1) k_resident(const ResidentLaunch p) {
   cg::grid_group grid = cg::this_grid();
@@ -154,9 +261,8 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resident(const ResidentLaunch
   double* A = sm;
   double* B = A + (size_t)(p.rmax + 2) * P;
   double* F = B + (size_t)(p.rmax + 2) * P;
-  unsigned long long* flags = reinterpret_cast<unsigned long long*>(p.ws);
-  double* pub = p.ws + G;                          // [slot][cta][first, last][nx]
-  double* part = pub + (size_t)2 * G * 2 * nx;     // [entry][cta][max, sum]
+  double* pub = p.ws + ((G + 1) & ~1);             // [slot][cta][first, last][nx] LL entries (16 B each)
+  double* part = pub + (size_t)2 * G * 2 * 2 * nx; // [entry][cta][max, sum]
   const int up = c > 0 ? c - 1 : G - 1, dn = c < G - 1 ? c + 1 : 0;
   const bool top_x = c > 0 || p.ymode[0] == GH_WRAP;      // halo row 0 from CTA `up`
   const bool bot_x = c < G - 1 || p.ymode[1] == GH_WRAP;  // halo row R+1 from CTA `dn`
@@ -174,57 +280,56 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resident(const ResidentLaunch
   }
   for (int r = 0; r < R; ++r)
     for (int x = tid; x < nx; x += nt) F[(size_t)r * nx + x] = p.rhs[(int64_t)(y0 + r) * p.ld_rhs + x];
-  if (tid == 0) flags[c] = 0ull;
+  // this CTA's mailbox entries start with tag 0 (a solve's tags are 1..N)
+  for (int sl = 0; sl < 2; ++sl)
+    for (int i = tid; i < 2 * 2 * nx; i += nt) pub[(size_t)(sl * G + c) * 2 * 2 * nx + i] = 0.0;
   __threadfence();
   grid.sync();
 
   int entry = 0;
+  const bool refl_top = !top_x && p.ymode[0] == GH_REFLECT, refl_bot = !bot_x && p.ymode[1] == GH_REFLECT;
   for (int s = 0; s < p.nsweeps; ++s) {
     const bool rec = p.every > 0 && s % p.every == 0;
+    const uint32_t tag = (uint32_t)s + 1u;
     unsigned long long mx = 0ull;
     double ss = 0.0;
-    // the first and last rows first: they go to the neighbours, whose copy
-    // overlaps the sweep of the inner rows
+    // the first and last rows first, each thread publishing its own cells of
+    // them straight from registers (LL entries: no barrier, no fence, no
+    // flag), so the neighbours' copies overlap the sweep of the inner rows
+    const int slot = (s + 1) & 1;
+    double* mine = pub + (size_t)(slot * G + c) * 2 * 2 * nx;
+    double* pf = top_x ? mine : nullptr;
+    double* pl = bot_x ? mine + 2 * nx : nullptr;
     auto sweep = [&](int lo, int hi) {
-      if (rec) rs_rows<ST, true, true>(A, B, F, P, nx, lo, hi, p.scale, p.lambda, mx, ss);
-      else rs_rows<ST, true, false>(A, B, F, P, nx, lo, hi, p.scale, p.lambda, mx, ss);
+      if (rec) ll_rows<ST, true>(A, B, F, P, nx, R, lo, hi, p.scale, p.lambda, xm, pf, pl, refl_top, refl_bot, tag, mx, ss);
+      else ll_rows<ST, false>(A, B, F, P, nx, R, lo, hi, p.scale, p.lambda, xm, pf, pl, refl_top, refl_bot, tag, mx, ss);
     };
     sweep(1, 1);
     if (R > 1) sweep(R, R);
-    __syncthreads();
-    const int slot = (s + 1) & 1;
-    double* mine = pub + (size_t)(slot * G + c) * 2 * nx;
-    for (int x = tid; x < nx; x += nt) {
-      __stcg(mine + x, B[P + x + 2]);
-      __stcg(mine + nx + x, B[(size_t)R * P + x + 2]);
-    }
-    __syncthreads();
-    // release at gpu scope: the CTA's row stores (ordered before it by the
-    // barrier) are visible to whoever acquires the flag
-    if (tid == 0) st_release(flags + c, (unsigned long long)(s + 1));
     if (R > 2) sweep(2, R - 1);
     if (rec) {
       rs_block_reduce(mx, ss, part + ((size_t)entry * G + c) * 2);
       ++entry;
     }
-    // wait for the neighbours' rows of φ^{s+1}
-    if (tid == 0 && top_x)
-      while (ld_acquire(flags + up) < (unsigned long long)(s + 1)) {
+    // the neighbours' rows of φ^{s+1}: each thread fetches its own cells
+    // (spinning on the tags) and writes them, with their x images, into the
+    // halo rows
+    const double* fu = pub + ((size_t)(slot * G + up) * 2 + 1) * 2 * nx;  // up's last row
+    const double* fd = pub + ((size_t)(slot * G + dn) * 2) * 2 * nx;      // dn's first row
+    for (int q = tid; q < nx / 2; q += nt) {
+      const int x = 2 * q + 2;
+      if (top_x) {
+        const double v0 = ll_get(fu + 4 * q, tag), v1 = ll_get(fu + 4 * q + 2, tag);
+        *reinterpret_cast<double2*>(B + x) = make_double2(v0, v1);
+        ll_ximg(B, x, nx, v0, v1, xm);
       }
-    if (tid == 32 && bot_x)
-      while (ld_acquire(flags + dn) < (unsigned long long)(s + 1)) {
+      if (bot_x) {
+        const double v0 = ll_get(fd + 4 * q, tag), v1 = ll_get(fd + 4 * q + 2, tag);
+        double* h = B + (size_t)(R + 1) * P;
+        *reinterpret_cast<double2*>(h + x) = make_double2(v0, v1);
+        ll_ximg(h, x, nx, v0, v1, xm);
       }
-    __syncthreads();
-    const double* fu = pub + ((size_t)(slot * G + up) * 2 + 1) * nx;  // up's last row
-    const double* fd = pub + ((size_t)(slot * G + dn) * 2) * nx;      // dn's first row
-    for (int x = tid; x < nx; x += nt) {
-      if (top_x) B[x + 2] = __ldcg(fu + x);
-      else if (p.ymode[0] == GH_REFLECT) B[x + 2] = -B[P + x + 2];
-      if (bot_x) B[(size_t)(R + 1) * P + x + 2] = __ldcg(fd + x);
-      else if (p.ymode[1] == GH_REFLECT) B[(size_t)(R + 1) * P + x + 2] = -B[(size_t)R * P + x + 2];
     }
-    __syncthreads();
-    for (int r = tid; r < R + 2; r += nt) rs_xghost(B + (size_t)r * P, nx, xm);
     __syncthreads();
     double* t = A;
     A = B;
@@ -491,7 +596,10 @@ static int rs_k_env() {
 }
 
 size_t resident_ws_doubles(int nx, int grid, int n_entries) {
-  return (size_t)grid + (size_t)2 * grid * 2 * RS_KMAX * nx + (size_t)(n_entries > 0 ? n_entries : 1) * grid * 2;
+  // flags (k_resident_tb) or padding, the row mailboxes (k_resident: 2 slots x 2 rows x nx LL entries
+  // of 2 doubles; k_resident_tb: 2 slots x 2K rows x nx), the norm partials
+  return (size_t)grid + 1 + (size_t)2 * grid * 2 * (RS_KMAX > 2 ? RS_KMAX : 2) * nx +
+         (size_t)(n_entries > 0 ? n_entries : 1) * grid * 2;
 }
 
 static int rs_nsm(int* smem_optin) {

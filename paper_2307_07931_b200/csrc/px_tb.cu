@@ -31,6 +31,7 @@
 
 #include "px_device.cuh"
 #include "px_internal.h"
+#include "px_ptx.cuh"
 
 namespace px {
 
@@ -55,45 +56,7 @@ struct Geom {
   static constexpr size_t SMEM = (size_t)NST * STAGE * sizeof(double) + 2 * NST * sizeof(uint64_t);
 };
 
-__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mb_init(uint64_t* b, uint32_t c) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(c) : "memory");
-}
-__device__ __forceinline__ void mb_expect(uint64_t* b, uint32_t tx) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(tx) : "memory");
-}
-__device__ __forceinline__ void mb_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
-}
-__device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t par) {
-  asm volatile(
-      "{\n.reg .pred P1;\nW_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra W_%=;\n}\n" ::"r"(su32(b)),
-      "r"(par)
-      : "memory");
-}
-// producer-side wait with back-off: the single producer thread would
-// otherwise spin on try_wait and take issue slots from the consumer warps
-__device__ __forceinline__ void mb_wait_sleep(uint64_t* b, uint32_t par) {
-  uint32_t ok;
-  for (;;) {
-    asm volatile(
-        "{\n.reg .pred P1;\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
-        : "=r"(ok)
-        : "r"(su32(b)), "r"(par)
-        : "memory");
-    if (ok) return;
-    __nanosleep(200);
-  }
-}
-__device__ __forceinline__ void g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          su32(dst)),
-      "l"(src), "r"(bytes), "r"(su32(bar)), "l"(pol)
-      : "memory");
-}
+using namespace ptx;
 
 struct P2d {
   double a, b;  // the lane's two cells of a row
@@ -256,8 +219,8 @@ __global__ void __launch_bounds__(NW * 32 + 32, (NW == 7 ? 2 : 1))
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) {
-      mb_init(&full[s], 1);
-      mb_init(&empty[s], NW);
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -277,7 +240,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, (NW == 7 ? 2 : 1))
     // ------------- producer: level-0 rows of φ and the rows of ρ -------------
     if (lane == 0) {
       uint64_t pol;
-      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      pol = evict_first_policy();
       int slot = 0;
       uint32_t phase = 0;
       for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
@@ -289,21 +252,21 @@ __global__ void __launch_bounds__(NW * 32 + 32, (NW == 7 ? 2 : 1))
         const int qbase = y0 - K, nrows = y1 - y0 + 2 * K;
         const int nst = (nrows + R - 1) / R;
         for (int s = 0; s < nst; ++s) {
-          mb_wait(&empty[slot], phase ^ 1u);
+          mbar_wait(&empty[slot], phase ^ 1u);
           double* sp = smem + (size_t)slot * G::STAGE;
           int n = 0;
           for (int j = 0; j < R; ++j) {
             const int r = s * R + j;
             if (r < nrows) n += (r >= 2) ? 2 : 1;
           }
-          mb_expect(&full[slot], rb * (uint32_t)n);
+          mbar_arrive_expect_tx(&full[slot], rb * (uint32_t)n);
           for (int j = 0; j < R; ++j) {
             const int r = s * R + j;
             if (r >= nrows) break;
             const int q = qbase + r;
-            g2s(sp + j * G::CLS, a.src + (int64_t)q * a.ld_src + cload, rb, &full[slot], pol);
+            bulk_g2s(sp + j * G::CLS, a.src + (int64_t)q * a.ld_src + cload, rb, &full[slot], pol);
             if (r >= 2)  // ρ row q-1: rows y0-K+1 .. y1+K-2 are the ones the levels use
-              g2s(sp + (R + j) * G::CLS, a.rhs + (int64_t)(q - 1) * a.ld_rhs + cload, rb, &full[slot], pol);
+              bulk_g2s(sp + (R + j) * G::CLS, a.rhs + (int64_t)(q - 1) * a.ld_rhs + cload, rb, &full[slot], pol);
           }
           if (++slot == NST) {
             slot = 0;
@@ -344,7 +307,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, (NW == 7 ? 2 : 1))
         for (int u = 0; u < 3; ++u) st[t][u] = P2d{0.0, 0.0};
       const double* pp = smem;  // previous stage (valid from s = 1)
       for (int s = 0; s < nst; ++s) {
-        mb_wait(&full[slot], phase);
+        mbar_wait(&full[slot], phase);
         const double* sp = smem + (size_t)slot * G::STAGE;
         const bool steady = (s * R >= 2 * K) && (s * R + R - 1 < c.nrows - K);
         if (steady)
@@ -352,7 +315,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, (NW == 7 ? 2 : 1))
         else
           tb_stage<ST, K, NW, P2, FIX, NM, true>(a, x, c, s, sp, pp, cl, st, mx, ss, act);
         __syncwarp();
-        if (prev >= 0 && lane == 0) mb_arrive(&empty[prev]);  // stage s-1 no longer needed
+        if (prev >= 0 && lane == 0) mbar_arrive(&empty[prev]);  // stage s-1 no longer needed
         prev = slot;
         pp = sp;
         if (++slot == NST) {
@@ -361,7 +324,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, (NW == 7 ? 2 : 1))
         }
       }
       __syncwarp();
-      if (lane == 0) mb_arrive(&empty[prev]);  // the item's last stage
+      if (lane == 0) mbar_arrive(&empty[prev]);  // the item's last stage
       prev = -1;
     }
   }
@@ -632,8 +595,8 @@ __global__ void __launch_bounds__(tbw::NW * 32 + 32, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < NSTG; ++s) {
-      mb_init(&full[s], 1);
-      mb_init(&empty[s], NW);
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -653,7 +616,7 @@ __global__ void __launch_bounds__(tbw::NW * 32 + 32, 1)
     // ------------- producer: level-0 rows of φ and the rows of ρ -------------
     if (lane == 0) {
       uint64_t pol;
-      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      pol = evict_first_policy();
       int slot = 0;
       uint32_t phase = 0;
       for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
@@ -665,20 +628,20 @@ __global__ void __launch_bounds__(tbw::NW * 32 + 32, 1)
         const int qbase = y0 - K, nrows = y1 - y0 + 2 * K;
         const int nst = (nrows + K - 1 + R - 1) / R;  // K-1 drain rows: the output lags 2K-1 rows
         for (int s = 0; s < nst; ++s) {
-          mb_wait_sleep(&empty[slot], phase ^ 1u);
+          mbar_wait_sleep(&empty[slot], phase ^ 1u);
           double* sp = smem + (size_t)slot * G::STAGE;
           uint32_t n = 0;
           for (int j = 0; j < R; ++j) {
             const int r = s * R + j;
             n += (r < nrows ? 1u : 0u) + (r >= 2 && r < nrows ? 1u : 0u);
           }
-          mb_expect(&full[slot], rb * n);
+          mbar_arrive_expect_tx(&full[slot], rb * n);
           for (int j = 0; j < R; ++j) {
             const int r = s * R + j;
             const int q = qbase + r;
-            if (r < nrows) g2s(sp + j * G::CLS, a.src + (int64_t)q * a.ld_src + cload, rb, &full[slot], pol);
+            if (r < nrows) bulk_g2s(sp + j * G::CLS, a.src + (int64_t)q * a.ld_src + cload, rb, &full[slot], pol);
             if (r >= 2 && r < nrows)  // ρ of relative row r-1
-              g2s(sp + (R + j) * G::CLS, a.rhs + (int64_t)(q - 1) * a.ld_rhs + cload, rb, &full[slot], pol);
+              bulk_g2s(sp + (R + j) * G::CLS, a.rhs + (int64_t)(q - 1) * a.ld_rhs + cload, rb, &full[slot], pol);
           }
           if (++slot == NSTG) {
             slot = 0;
@@ -735,7 +698,7 @@ __global__ void __launch_bounds__(tbw::NW * 32 + 32, 1)
       const int nst = (c.nrows + K - 1 + R - 1) / R;
       const int s_steady0 = (3 * K - 1 + R - 1) / R;  // first stage with every level valid
       for (int s = 0; s < nst; ++s) {
-        mb_wait(&full[slot], phase);
+        mbar_wait(&full[slot], phase);
         const double* sp = smem + (size_t)slot * G::STAGE;
         const bool steady = s >= s_steady0 && (s * R + R - 1 < c.nrows - K);
         if (steady)
@@ -743,7 +706,7 @@ __global__ void __launch_bounds__(tbw::NW * 32 + 32, 1)
         else
           tbw_stage<ST, K, P2, FIX, DIR, NM, true>(a, x, c, s, sp, pp1, pp2, cl, st, mx, ss, ia, act);
         __syncwarp();
-        if (prev2 >= 0 && lane == 0) mb_arrive(&empty[prev2]);  // stage s-2 no longer needed
+        if (prev2 >= 0 && lane == 0) mbar_arrive(&empty[prev2]);  // stage s-2 no longer needed
         prev2 = prev1;
         prev1 = slot;
         pp2 = pp1;
@@ -755,8 +718,8 @@ __global__ void __launch_bounds__(tbw::NW * 32 + 32, 1)
       }
       __syncwarp();
       if (lane == 0) {  // the item's last two stages
-        if (prev2 >= 0) mb_arrive(&empty[prev2]);
-        if (prev1 >= 0) mb_arrive(&empty[prev1]);
+        if (prev2 >= 0) mbar_arrive(&empty[prev2]);
+        if (prev1 >= 0) mbar_arrive(&empty[prev1]);
       }
       prev1 = prev2 = -1;
       if (NM == 1) {

@@ -69,6 +69,21 @@ def solve3(n, st=P.PX_LAPLACE_7PT_3D, bc=P.PX_BC_PERIODIC, N=3, E=1):
     P.solve3(g, bc, P.relax_params(1.0 / n[0], (1.0 / n[0]) ** 2 / 12, st), N, E, a, b, r, stream=s)
 
 
+def push_solve(n0, n1, N=5, E=1, st=0):
+    """Fused peer-memory push (self-exchange, peer communicator): push_init,
+    the PUSH k_bulk sweeps as programmatic dependent launches, k_wait."""
+    import os
+    os.environ["PROTOX_NCCL_SELF_EXCHANGE"] = "1"
+    lay = P.Layout(P.box(0, 0, n0 - 1, n1 - 1), (n0, n1), 1, P.PX_BC_PERIODIC, 1)
+    a, b, r = fields(lay)
+    pa, pb, pr = lay.patch(0, a), lay.patch(0, b), lay.patch(0, r)
+    comm = P.Comm(None, 1, 0, torch.cuda.current_device())
+    P.comm_p2p_import(comm, lay, [P.comm_p2p_export(comm, lay, 0, pa, pb)])
+    P.solve(lay, comm, 0, P.relax_params(1.0 / n0, 1.0 / (8.0 * n0 * n0), st), N, E, pa, pb, pr)
+    torch.cuda.synchronize()
+    comm.close()
+
+
 def other():
     lay = P.Layout(P.box(0, 0, 199, 99), (200, 100), 1, P.PX_BC_DIRICHLET_CC, 1)
     a, b, r = fields(lay)
@@ -95,6 +110,9 @@ if __name__ == "__main__":
         "local_multipart_solve": lambda: solve(256, 150, nranks=3, bc=P.PX_BC_FIXED_GHOSTS),
         "tb_solve": lambda: solve(1000, 300, nranks=3, g=4, tk=4, N=9, E=3),
         "graph_solve": lambda: solve(600, 90, N=4, E=1, graph=True),
+        "pdl_bulk_solve": lambda: solve(2048, 2050, N=4, E=1),
+        "push_solve": lambda: push_solve(1100, 70, N=5, E=1),
+        "push_solve9": lambda: push_solve(640, 300, N=4, E=2, st=1),
         "tb_dirichlet9_solve": lambda: solve(1000, 300, g=4, tk=4, N=8, E=4, st=1, bc=P.PX_BC_DIRICHLET_CC),
         "tb_fixed_k2_solve": lambda: solve(500, 120, g=2, tk=2, N=4, E=1, bc=P.PX_BC_FIXED_GHOSTS),
         "relax3_solve": lambda: solve3((70, 37, 13)),

@@ -185,13 +185,14 @@ def test_solve_ragged_multibox(bc, st, graph):
     _check_norms(norms, rn)
 
 
-@pytest.mark.parametrize("shape", [(130, 400), (1022, 149), (4, 5000)])
+@pytest.mark.parametrize("shape", [(130, 400), (1022, 149), (4, 5000), (1024, 101), (2048, 9)])
 @pytest.mark.parametrize("bc", [P.PX_BC_PERIODIC, P.PX_BC_DIRICHLET_CC, P.PX_BC_FIXED_GHOSTS])
 @pytest.mark.parametrize("st", [P.PX_LAPLACE_5PT, P.PX_MEHRSTELLEN_9PT])
 def test_solve_resident_shapes(shape, bc, st):
-    """Shared-memory-resident solve (k_resident): uneven rows per CTA, one
-    row per CTA, 34 rows x 2 column pairs per CTA; even and odd sweep counts;
-    norms every 4."""
+    """Shared-memory-resident solve (k_resident, LL row mailbox): uneven rows
+    per CTA, one row per CTA, 34 rows x 2 column pairs per CTA, an odd CTA
+    count (101, 9: the mailbox alignment), 9 CTAs of one row; even and odd sweep
+    counts; norms every 4."""
     n0, n1 = shape
     h = 1.0 / 1024
     lam = h * h / 8 if st == 0 else 3 * h * h / 16
