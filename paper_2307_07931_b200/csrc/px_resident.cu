@@ -161,15 +161,42 @@ __device__ __forceinline__ void ll_put(double* e, double v, uint32_t tag) {
                "r"((uint32_t)(b >> 32)), "r"(tag)
                : "memory");
 }
-__device__ __forceinline__ double ll_get(const double* e, uint32_t tag) {
+#ifndef LL_BACKOFF_NS
+#define LL_BACKOFF_NS 100
+#endif
+struct LL {
   uint32_t lo, t0, hi, t1;
-  do {
-    asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(lo), "=r"(t0), "=r"(hi), "=r"(t1)
-                 : "l"(e)
-                 : "memory");
-  } while (t0 != tag || t1 != tag);
-  return __longlong_as_double((long long)(((unsigned long long)hi << 32) | lo));
+};
+__device__ __forceinline__ LL ll_load(const double* e) {
+  LL v;
+  asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.lo), "=r"(v.t0), "=r"(v.hi), "=r"(v.t1)
+               : "l"(e)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ double ll_val(const LL& v) {
+  return __longlong_as_double((long long)(((unsigned long long)v.hi << 32) | v.lo));
+}
+// the n (<= 4) entries e[i], all loads in flight together; re-poll until
+// every tag matches
+template <int n>
+__device__ __forceinline__ void ll_get(const double* const (&e)[4], uint32_t tag, double (&out)[4]) {
+  LL v[4];
+#pragma unroll
+  for (int i = 0; i < n; ++i) v[i] = ll_load(e[i]);
+  for (;;) {
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < n; ++i) ok = ok && v[i].t0 == tag && v[i].t1 == tag;
+    if (ok) break;
+    if (LL_BACKOFF_NS) __nanosleep(LL_BACKOFF_NS);  // fewer polls in flight: L2 stays free for the publications
+#pragma unroll
+    for (int i = 0; i < n; ++i)
+      if (v[i].t0 != tag || v[i].t1 != tag) v[i] = ll_load(e[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < n; ++i) out[i] = ll_val(v[i]);
 }
 
 // The x images of one row's pair (columns 2q, 2q+1 at shared index x): the
@@ -318,16 +345,27 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resident(const ResidentLaunch
     const double* fd = pub + ((size_t)(slot * G + dn) * 2) * 2 * nx;      // dn's first row
     for (int q = tid; q < nx / 2; q += nt) {
       const int x = 2 * q + 2;
+      double v[4];
+      if (top_x && bot_x) {
+        const double* const e[4] = {fu + 4 * q, fu + 4 * q + 2, fd + 4 * q, fd + 4 * q + 2};
+        ll_get<4>(e, tag, v);
+      } else if (top_x || bot_x) {
+        const double* f = top_x ? fu : fd;
+        const double* const e[4] = {f + 4 * q, f + 4 * q + 2, f, f};
+        ll_get<2>(e, tag, v);
+        if (!top_x) {
+          v[2] = v[0];
+          v[3] = v[1];
+        }
+      }
       if (top_x) {
-        const double v0 = ll_get(fu + 4 * q, tag), v1 = ll_get(fu + 4 * q + 2, tag);
-        *reinterpret_cast<double2*>(B + x) = make_double2(v0, v1);
-        ll_ximg(B, x, nx, v0, v1, xm);
+        *reinterpret_cast<double2*>(B + x) = make_double2(v[0], v[1]);
+        ll_ximg(B, x, nx, v[0], v[1], xm);
       }
       if (bot_x) {
-        const double v0 = ll_get(fd + 4 * q, tag), v1 = ll_get(fd + 4 * q + 2, tag);
         double* h = B + (size_t)(R + 1) * P;
-        *reinterpret_cast<double2*>(h + x) = make_double2(v0, v1);
-        ll_ximg(h, x, nx, v0, v1, xm);
+        *reinterpret_cast<double2*>(h + x) = make_double2(v[2], v[3]);
+        ll_ximg(h, x, nx, v[2], v[3], xm);
       }
     }
     __syncthreads();
