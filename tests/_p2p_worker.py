@@ -6,7 +6,7 @@ peer-memory norm all-reduce all run for real ("information is
 exchanged between the boxes", :173 computeMaxResidualAcrossProcs).  The
 records travel over a gloo process group.
 
-    python tests/_p2p_worker.py OUT_DIR BC N0 N1 N1SWEEPS N2SWEEPS E SEED STENCIL GRAPH
+    python tests/_p2p_worker.py OUT_DIR BC N0 N1 N1SWEEPS N2SWEEPS E SEED STENCIL GRAPH [INF_AT_ROW]
 (env: RANK, WORLD_SIZE, MASTER_ADDR, MASTER_PORT)
 Writes OUT_DIR/rank{r}.npz: the owned slab of φ^(N1+N2) and both norm lists.
 """
@@ -28,6 +28,7 @@ def main():
     out, bc, n0, n1, na, nb, E, seed, st, graph = sys.argv[1:11]
     bc, n0, n1, na, nb, E, seed, st, graph = (int(bc), int(n0), int(n1), int(na), int(nb), int(E), int(seed),
                                              int(st), int(graph))
+    inf_row = int(sys.argv[11]) if len(sys.argv) > 11 else -1
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
@@ -35,6 +36,8 @@ def main():
     rng = np.random.default_rng(seed)
     phi0 = rng.uniform(-1, 1, (n1 + 2 * g, n0 + 2 * g))
     rho = rng.uniform(-1, 1, (n1 + 2 * g, n0 + 2 * g))
+    if inf_row >= 0:  # ρ = +inf at one cell of interior row inf_row (one rank's slab)
+        rho[g + inf_row, g + n0 // 3] = np.inf
     lay = P.Layout(P.box(0, 0, n0 - 1, n1 - 1), (n0, n1 // (2 * world)), g, bc, world)
     li = lay.local(rank)
 

@@ -33,13 +33,13 @@ def _port():
     return p
 
 
-def _run(tmp_path, world, bc, n0, n1, na, nb, E, seed, st, graph):
+def _run(tmp_path, world, bc, n0, n1, na, nb, E, seed, st, graph, inf_row=-1):
     port = _port()
     procs = []
     for r in range(world):
         env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         args = [sys.executable, os.path.join(ROOT, "tests", "_p2p_worker.py"), str(tmp_path), *map(str, (
-            bc, n0, n1, na, nb, E, seed, st, graph))]
+            bc, n0, n1, na, nb, E, seed, st, graph, inf_row))]
         procs.append(subprocess.Popen(args, env=env, cwd=ROOT, stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
                                       text=True, start_new_session=True))
     outs = []
@@ -89,3 +89,35 @@ def test_p2p_push_across_processes(tmp_path, world, bc, st, graph):
     assert gpu.shape == rn.shape
     assert bits_equal(gpu[:, 0], rn[:, 0]), np.max(np.abs(gpu[:, 0] - rn[:, 0]))
     np.testing.assert_allclose(gpu[:, 1], rn[:, 1], rtol=SUM_RTOL, atol=0)
+
+
+def test_p2p_inf_nan_through_peer_allreduce(tmp_path):
+    """ρ = +inf at one cell of the LAST rank's slab (3 processes): r(φ⁰) is
+    inf only there, so the peer-memory all-reduce must give max = inf on
+    every rank at entry 0, then NaN (inf - inf) from entry 1 on (reading R7,
+    P:173); the field's NaN region spreads across the slab boundaries through
+    the pushed ghost rows and must match the oracle's NaN mask exactly, every
+    other cell bit for bit."""
+    world, bc, n0, n1, na, nb, E, seed = 3, P.PX_BC_PERIODIC, 256, 288, 3, 4, 1, 77
+    inf_row = n1 - 3
+    res = _run(tmp_path, world, bc, n0, n1, na, nb, E, seed, 0, 1, inf_row)
+    g = 1
+    rng = np.random.default_rng(seed)
+    phi0 = rng.uniform(-1, 1, (n1 + 2 * g, n0 + 2 * g))
+    rho = rng.uniform(-1, 1, (n1 + 2 * g, n0 + 2 * g))
+    rho[g + inf_row, g + n0 // 3] = np.inf
+    prob = oracle.Problem(n0, n1, 1.0 / n0, 1.0 / (8.0 * n0 * n0), b0=n0, b1=n1 // (2 * world), ghost=g,
+                          bc=BC_MAP[bc], stencil=0, nsweeps=na + nb, norm_every=E)
+    ref, rn = oracle.solve(prob, phi0, rho)
+    got = np.concatenate([r["phi"] for r in sorted(res, key=lambda r: int(r["y0"]))], axis=0)
+    ref = np.ascontiguousarray(ref[1:-1, 1:-1])
+    mg, mr = np.isnan(got), np.isnan(ref)
+    assert mr.any() and np.array_equal(mg, mr), (mg.sum(), mr.sum())
+    assert bits_equal(got[~mg], ref[~mr])
+    for r in res[1:]:
+        assert bits_equal(r["n1"], res[0]["n1"]) and bits_equal(r["n2"], res[0]["n2"])
+    gn = np.concatenate([res[0]["n1"][:-1], res[0]["n2"]])
+    assert gn[0, 0] == np.inf and rn[0, 0] == np.inf
+    assert np.array_equal(np.isnan(gn[:, 0]), np.isnan(rn[:, 0])), (gn[:, 0], rn[:, 0])
+    assert np.isnan(gn[1:, 0]).all()
+    assert np.array_equal(np.isnan(gn[:, 1]), np.isnan(rn[:, 1]))
