@@ -70,21 +70,21 @@ static __device__ __noinline__ void ps_push(double* rp, int x, double v0, double
 // neighbours' ghost rows (plain stores; their arrival is counted by the next
 // kernel, see k_bulk).  Outside the per-stage loop, out of line: the sweep's
 // inner loop is untouched.
-static __device__ __noinline__ void push_rows(const StreamLaunch& a, int x, bool lo, bool hi, bool live, bool xface,
-                                              int X0) {
-  const int g = a.ps.g;
+static __device__ __noinline__ void push_rows(const double* dst, int64_t ld, double* rlo, double* rhi, int ny,
+                                              int g, int x, bool live, bool xface, int X0, int gg, int n0, int m0,
+                                              int m1) {
+  if (!live) return;
   for (int side = 0; side < 2; ++side) {
-    if (!(side ? hi : lo) || !a.ps.rdst[side]) continue;
-    const int p0 = side ? a.ny - g : 0;
-    if (live) {
-      for (int r = 0; r < g; ++r) {
-        const double2 v = *reinterpret_cast<const double2*>(a.dst + (int64_t)(p0 + r) * a.ld_dst + x);
-        double* rp = a.ps.rdst[side] + (int64_t)r * a.ld_dst;
-        if (xface)
-          ps_push(rp, x, v.x, v.y, X0, a.gs.g, a.gs.n[0], a.gs.mode[0][0], a.gs.mode[0][1]);
-        else
-          *reinterpret_cast<double2*>(rp + x) = v;
-      }
+    double* rd = side ? rhi : rlo;
+    if (!rd) continue;
+    const int p0 = side ? ny - g : 0;
+    for (int r = 0; r < g; ++r) {
+      const double2 v = *reinterpret_cast<const double2*>(dst + (int64_t)(p0 + r) * ld + x);
+      double* rp = rd + (int64_t)r * ld;
+      if (xface)
+        ps_push(rp, x, v.x, v.y, X0, gg, n0, m0, m1);
+      else
+        *reinterpret_cast<double2*>(rp + x) = v;
     }
   }
 }
@@ -358,7 +358,8 @@ __global__ void __launch_bounds__(NC * 32 + 32, CPS) k_bulk(const StreamLaunch a
         }
       }
       if (PUSH && ((t.y0 == 0 && a.ps.rdst[0]) || (t.y1 == a.ny && a.ps.rdst[1])))
-        push_rows(a, t.c + c0, t.y0 == 0, t.y1 == a.ny, live, xface, X0);
+        push_rows(a.dst, a.ld_dst, t.y0 == 0 ? a.ps.rdst[0] : nullptr, t.y1 == a.ny ? a.ps.rdst[1] : nullptr, a.ny,
+                  a.ps.g, t.c + c0, live, xface, X0, a.gs.g, a.gs.n[0], a.gs.mode[0][0], a.gs.mode[0][1]);
       if (it + (int)gridDim.x < nitems) t = item_of<W, PUSH>(a, it + gridDim.x, nstrips, crows);
     }
   }
