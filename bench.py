@@ -284,11 +284,30 @@ def run_native3d(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # PROTOX_BENCH_SHARED_GPU=1 (tests only): every rank on cuda:0, gloo process
+    # group, no NCCL communicator -- exercises the N > 1 code path (push halo,
+    # halo metrics, max-over-ranks timing, e2e) on a one-GPU box
+    shared = world > 1 and os.environ.get("PROTOX_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if shared else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     cfg = CONFIGS[args.config]
+    if shared and (cfg.get("tk", 1) > 1 or cfg["stencil"] == 1 or args.halo != "p2p"):
+        raise SystemExit("PROTOX_BENCH_SHARED_GPU: k = 1, 5-point, --halo p2p only")
     n, S, E = cfg["n"], cfg["sweeps"], cfg["norm_every"]
     h = 1.0 / n
     lam = h * h / 12  # λ = h²/(4D), D = 3
@@ -461,11 +480,30 @@ def run_native(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # PROTOX_BENCH_SHARED_GPU=1 (tests only): every rank on cuda:0, gloo process
+    # group, no NCCL communicator -- exercises the N > 1 code path (push halo,
+    # halo metrics, max-over-ranks timing, e2e) on a one-GPU box
+    shared = world > 1 and os.environ.get("PROTOX_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if shared else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     cfg = CONFIGS[args.config]
+    if shared and (cfg.get("tk", 1) > 1 or cfg["stencil"] == 1 or args.halo != "p2p"):
+        raise SystemExit("PROTOX_BENCH_SHARED_GPU: k = 1, 5-point, --halo p2p only")
     n, S, E = cfg["n"], cfg["sweeps"], cfg["norm_every"]
     h = 1.0 / n
     lam = h * h / 8
@@ -475,7 +513,7 @@ def run_native(args):
     li = lay.local(rank)
     phi, scr, rho = lay.alloc(rank, dev), lay.alloc(rank, dev), lay.alloc(rank, dev)
     comm = None
-    if world > 1:
+    if world > 1 and not shared:
         obj = [P.comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         comm = P.Comm(obj[0], world, rank, local)
@@ -497,7 +535,13 @@ def run_native(args):
     pa, pb, pr = lay.patch(rank, phi), lay.patch(rank, scr), lay.patch(rank, rhs)
     halo_mode = "local" if world == 1 else "nccl"
     scomm = comm  # the communicator px_solve uses
-    if comm is not None and args.halo == "p2p" and tk == 1:
+    if shared:  # no NCCL to check against: the push path itself is under test
+        scomm = P.Comm(None, world, rank, local)
+        recs = [None] * world
+        dist.all_gather_object(recs, P.comm_p2p_export(scomm, lay, rank, pa, pb))
+        P.comm_p2p_import(scomm, lay, recs)
+        halo_mode = "p2p (shared-GPU test mode)"
+    elif comm is not None and args.halo == "p2p" and tk == 1:
         pcomm, why = p2p_setup(P, torch, dist, lay, rank, world, local, comm, prm, S, pa, pb, pr, phi, stream)
         if pcomm is not None:
             scomm, halo_mode = pcomm, "p2p"
@@ -537,11 +581,7 @@ def run_native(args):
     barrier()
     launches = P.kernel_launch_count() - launches0
     clk = clocks.stop()
-    t_ms = ev0.elapsed_time(ev1)
-    t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    t_ms = float(t.item())
+    t_ms = max_over_ranks(ev0.elapsed_time(ev1))
     cells = n * n * S * args.steps
     value = cells / (t_ms * 1e-3) / 1e9
 
@@ -555,7 +595,8 @@ def run_native(args):
     qa, qb = bufs
     for i in range(reps):
         src, dst = (qa, qb) if i % 2 == 0 else (qb, qa)
-        P.exchange_ghosts(lay, comm, rank, src, stream=stream)
+        if comm is not None or world == 1:  # (shared-GPU test mode: stale ghost rows, timing only)
+            P.exchange_ghosts(lay, comm, rank, src, stream=stream)
         evs[i][0].record(stream)
         if tk > 1:
             P.relax_block(prm, tk, src, dst, pr, li.owned, nb, stream=stream)
@@ -566,9 +607,7 @@ def run_native(args):
     k_ms = statistics.mean(a.elapsed_time(b) for a, b in evs[2:])
     halo = None
     if world > 1:
-        kt = torch.tensor([k_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(kt, op=dist.ReduceOp.MAX)
-        halo = halo_metrics(halo_mode, n, ghost, tk, S, t_ms / args.steps, float(kt.item()))
+        halo = halo_metrics(halo_mode, n, ghost, tk, S, t_ms / args.steps, max_over_ranks(k_ms))
     variant = P.relax_variant(qa, qb, pr, li.owned)
     local_cells = (li.owned.hi.c[0] - li.owned.lo.c[0] + 1) * (li.owned.hi.c[1] - li.owned.lo.c[1] + 1)
     achieved = BYTES_PER_CELL_UPDATE * local_cells / (k_ms * 1e-3) / 1e9
@@ -644,11 +683,9 @@ def run_native(args):
         e2e_run(ke)
         w1.record(stream)
         barrier()
-        te = torch.tensor([w0.elapsed_time(w1)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        te_ms = max_over_ranks(w0.elapsed_time(w1))
         n_norm = (S + E - 1) // E + 1 if E > 0 else 1
-        e2e = {"value": n * n * S * ke / (te.item() * 1e-3) / 1e9, "unit": UNIT,
+        e2e = {"value": n * n * S * ke / (te_ms * 1e-3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": (1 if world == 1 else 2) * n * n * 8,
                "d2h_bytes_per_step": n * n * 8 + 16 * n_norm, "steps": ke,
                "api": ("px_solve_host_batch (one problem per step: H2D rho, solve, D2H phi^N + norms; "
