@@ -50,6 +50,7 @@ static constexpr size_t CTL_BYTES = (CTL_MBOX + 2 * px::PX_MBOX_ENTRIES) * sizeo
 
 struct P2PState {
   bool exported = false, enabled = false;
+  uint64_t gen = 0;                             // changes with every (re)registration: part of the plan key
   uint64_t layout_gen = 0;
   int32_t rank = 0;
   const double* bufs[2] = {nullptr, nullptr};   // own registered φ (A) and scratch (B)
@@ -158,13 +159,14 @@ static px_status local_rows(const px_layout* l, const px_patch* parts, cudaStrea
 struct PlanKey {
   uint64_t layout_gen;
   const px_comm* comm;
+  uint64_t p2p_gen;  // the communicator's peer registration (a cached graph bakes in its mode and pointers)
   int32_t rank, stencil, nsweeps, norm_every, k, nparts;
   double h, lambda;
   std::vector<const double*> ptrs;
   std::vector<int64_t> rhs_geom;  // per part: rhs box lo/hi and ld (baked into captured launches)
   cudaStream_t stream;
   bool operator==(const PlanKey& o) const {
-    return layout_gen == o.layout_gen && comm == o.comm && rank == o.rank && stencil == o.stencil &&
+    return layout_gen == o.layout_gen && comm == o.comm && p2p_gen == o.p2p_gen && rank == o.rank && stencil == o.stencil &&
            nsweeps == o.nsweeps && norm_every == o.norm_every && k == o.k && nparts == o.nparts &&
            h == o.h && lambda == o.lambda && ptrs == o.ptrs && rhs_geom == o.rhs_geom && stream == o.stream;
   }
@@ -812,11 +814,17 @@ px_status px_comm_create_peer(int32_t nranks, int32_t rank, int32_t device, px_c
   return PX_OK;
 }
 
+static uint64_t next_p2p_gen() {
+  static uint64_t g = 0;
+  return ++g;
+}
+
 static void p2p_close(P2PState& st) {
   for (void* b : st.opened) cudaIpcCloseMemHandle(b);
   st.opened.clear();
   st.ctl_of.clear();
   st.enabled = false;
+  st.gen = next_p2p_gen();
 }
 
 void px_comm_destroy(px_comm* c) {
@@ -918,6 +926,7 @@ px_status px_comm_p2p_import(px_comm* c, const px_layout* l, const uint8_t* blob
   if (c->nranks == 1) {  // self-exchange: the neighbour is this rank
     for (int b = 0; b < 2; ++b) st.peer_lo[b] = st.peer_hi[b] = const_cast<double*>(st.bufs[b]);
     st.enabled = true;
+    st.gen = next_p2p_gen();
     return PX_OK;
   }
   auto open = [&](int32_t r, int i, void** out) -> px_status {
@@ -960,6 +969,7 @@ px_status px_comm_p2p_import(px_comm* c, const px_layout* l, const uint8_t* blob
     st.peer_hi[b] = mapped[1][b];
   }
   st.enabled = true;
+  st.gen = next_p2p_gen();
   return PX_OK;
 }
 
@@ -1075,6 +1085,7 @@ static px_status solve_enqueue(const px_layout* l, px_comm* c, int32_t rank, con
   PlanKey key;
   key.layout_gen = layout_generation(l);
   key.comm = c;
+  key.p2p_gen = c ? c->p2p.gen : 0;
   key.rank = rank;
   key.stencil = p->stencil;
   key.nsweeps = o->nsweeps;

@@ -706,6 +706,39 @@ def test_p2p_halo_push_self_exchange(graph, kind, n0, n1, N2, st, monkeypatch):
         assert r2.norms[0, 0] == rn[N // E, 0]
 
 
+def test_p2p_registration_invalidates_cached_graph(monkeypatch):
+    """A solve captured as a CUDA graph in NCCL mode, then px_comm_enable_p2p
+    on the same communicator and buffers: the next identical solve must run
+    the push path (the plan key carries the peer registration), and the
+    three solves together stay bit-identical to the oracle."""
+    monkeypatch.setenv("PROTOX_NCCL_SELF_EXCHANGE", "1")
+    n0, n1, N, E = 1024, 4200, 4, 1  # interior rows x columns > 4M: the TMA kernel
+    h = 1.0 / 2048
+    lam = h * h / 8
+    phi0, rho = _fields(n0, n1, 1, 909, P.PX_BC_PERIODIC)
+    lay = P.Layout(P.box(0, 0, n0 - 1, n1 - 1), (256, 200), 1, P.PX_BC_PERIODIC, 1)
+    comm = P.Comm(P.comm_unique_id(), 1, 0, torch.cuda.current_device())
+    try:
+        a = to_device_ghosted(lay, 0, phi0, 1)
+        b = lay.alloc(0)
+        r = to_device_ghosted(lay, 0, rho, 1)
+        pa, pb, pr = lay.patch(0, a), lay.patch(0, b), lay.patch(0, r)
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        prm = P.relax_params(h, lam)
+        P.solve(lay, comm, 0, prm, N, E, pa, pb, pr, use_graph=True, stream=s)
+        assert P.last_solve_kernels() == "k_stream+k_bulk"
+        P.comm_enable_p2p(comm, lay, 0, pa, pb)
+        P.solve(lay, comm, 0, prm, N, E, pa, pb, pr, use_graph=True, stream=s)
+        assert P.last_solve_kernels() == "k_bulk"
+        P.solve(lay, comm, 0, prm, N, E, pa, pb, pr, use_graph=True, stream=s)
+        out = owned_to_host(lay, 0, a)
+    finally:
+        comm.close()
+    ref, _ = oracle.solve(_orc_problem(n0, n1, h, lam, P.PX_BC_PERIODIC, 0, 3 * N, E), phi0, rho)
+    assert bits_equal(out, ref[1:-1, 1:-1]), ulp_diff(out, ref[1:-1, 1:-1])
+
+
 @pytest.mark.gpu
 def test_temporal_blocking_narrow_kernel_subprocess():
     """The narrow temporal-blocking kernel (2 columns per lane, A/B baseline,
