@@ -148,3 +148,46 @@ def test_config4_fullsize_temporal_blocking_sampled_bitwise():
     assert abs(res.norms[0, 1] - ss) <= 1e-12 * ss
     del phi, scr, rho
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("k", [1, 4])
+def test_beyond_2_31_elements_sampled_bitwise(k):
+    """Maximum-size edge case: a 65536 x 33000 periodic domain is 2.16e9 cells
+    (> 2^31; 17.3 GB per array with its ghosts and padding, 52 GB in all), so
+    every element offset of the last ~350 rows overflows 32 bits.  k = 1 (the
+    TMA sweep kernel) and k = 4 (temporal blocking, ghost 4), 4 sweeps, norms
+    every sweep / pass: cells sampled in the first and last rows (the largest
+    offsets) bit-identical to oracle window runs; the first recorded max-norm
+    equals max|ρ| (r(φ⁰) = −ρ for φ⁰ = 0) computed by torch over the whole
+    field."""
+    n0, n1, N = 65536, 33000, 4
+    h = 1.0 / n0
+    lam = h * h / 8
+    g = 4 if k == 4 else 1
+    lay = P.Layout(P.box(0, 0, n0 - 1, n1 - 1), (256, 200), g, P.PX_BC_PERIODIC, 1)
+    li = lay.local(0)
+    assert li.alloc_elems > 2 ** 31
+    phi, scr, rho = lay.alloc(0), lay.alloc(0), lay.alloc(0)
+    try:
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        P.init_field(lay, 0, lay.patch(0, rho), P.PX_FIELD_HASH, inputs.DEFAULT_SEED, stream=s)
+        P.fill_ghosts(lay, 0, lay.patch(0, rho), stream=s)
+        res = P.solve(lay, None, 0, P.relax_params(h, lam), N, k, lay.patch(0, phi), lay.patch(0, scr),
+                      lay.patch(0, rho), use_graph=True, stream=s, temporal_k=k)
+        assert ("k_tbw" if k == 4 else "k_bulk") in P.last_solve_kernels()
+        out = lay.view(0, scr if res.in_scratch else phi)
+        R = N
+        rng = np.random.default_rng(31)
+        pts = [(0, 0), (n0 - 1, n1 - 1), (0, n1 - 1), (n0 - 1, n1 - 2), (12345, n1 - 1), (n0 // 2, n1 - 3)]
+        pts += [(int(rng.integers(0, n0)), int(rng.integers(n1 - 400, n1))) for _ in range(6)]
+        for (x, y) in pts:
+            win = inputs.hash_window(n0, n1, x - R - 1, y - R - 1, 2 * R + 3, 2 * R + 3)
+            want = _window_value(win, N, h, lam)
+            got = out[y, x].item()
+            assert np.float64(got).view(np.uint64) == np.float64(want).view(np.uint64), (x, y, got, want)
+        assert res.norms[0, 0] == torch.max(torch.abs(lay.view(0, rho))).item()
+    finally:
+        del phi, scr, rho
+        P.release_cached()
+        torch.cuda.empty_cache()
