@@ -176,7 +176,11 @@ __global__ void __launch_bounds__(NC * 32 + 32, CPS) k_bulk(const StreamLaunch a
   }
   __syncthreads();
 
-  unsigned long long mx = 0ull;
+  // max|r| as a double through fmax (one DMNMX per cell instead of a 64-bit
+  // integer compare-and-select): fmax returns one of its operands, so the
+  // max is exact; it drops NaN, but a NaN r makes Σr² NaN, which restores it
+  // below (R7)
+  double mxd = 0.0;
   double ss = 0.0;
 
   if (warp == NCW) {
@@ -273,6 +277,14 @@ __global__ void __launch_bounds__(NC * 32 + 32, CPS) k_bulk(const StreamLaunch a
         mbar_wait(&full[slot], phase);
         const double* sp = smem + (size_t)slot * STAGE_DOUBLES;
         const bool full_stage = (t.y0 - 1 + st * R + R - 1 <= t.y1) && (t.y0 - 1 + st * R - 1 >= t.y0);
+        // ghost images from this stage: the pair is at an x face, or a row of
+        // the stage lies within g of a y face (decided once per stage, so the
+        // per-row test below is skipped in the bulk of the domain)
+        bool stage_img = false;
+        if (MODE == MODE_RELAX && a.gs.g > 0) {
+          const int Ylo = t.y0 - 2 + st * R + a.gs.o[1], Yhi = Ylo + R - 1;
+          stage_img = xface || Ylo < a.gs.g || Yhi >= a.gs.n[1] - a.gs.g;
+        }
 #pragma unroll
         for (int i = 0; i < R; ++i) {
           constexpr int dummy = 0;
@@ -327,8 +339,8 @@ __global__ void __launch_bounds__(NC * 32 + 32, CPS) k_bulk(const StreamLaunch a
             // scale, λ powers of two (P2): the products are exact, fma rounds like the separate ops
             const double e0 = P2 ? fma(a.scale, L0, -f.x) : __dsub_rn(__dmul_rn(a.scale, L0), f.x);
             const double e1 = P2 ? fma(a.scale, L1, -f.y) : __dsub_rn(__dmul_rn(a.scale, L1), f.y);
-            mx = umax64(mx, (unsigned long long)__double_as_longlong(fabs(e0)));
-            mx = umax64(mx, (unsigned long long)__double_as_longlong(fabs(e1)));
+            mxd = fmax(mxd, fabs(e0));
+            mxd = fmax(mxd, fabs(e1));
             ss = fma(e0, e0, ss);
             ss = fma(e1, e1, ss);
             if (MODE == MODE_RELAX) {
@@ -337,7 +349,7 @@ __global__ void __launch_bounds__(NC * 32 + 32, CPS) k_bulk(const StreamLaunch a
               const int x = t.c + c0;
               double* dp = a.dst + (int64_t)r * a.ld_dst + x;
               *reinterpret_cast<double2*>(dp) = make_double2(o0, o1);
-              if (a.gs.g > 0) {
+              if (stage_img) {
                 const int Y = r + a.gs.o[1];
                 if (xface || Y < a.gs.g || Y >= a.gs.n[1] - a.gs.g) {
                   images(a, x, r, o0);
@@ -363,7 +375,11 @@ __global__ void __launch_bounds__(NC * 32 + 32, CPS) k_bulk(const StreamLaunch a
       if (it + (int)gridDim.x < nitems) t = item_of<W, PUSH>(a, it + gridDim.x, nstrips, crows);
     }
   }
-  if (a.norms.out_max) reduce_norms(a.norms, mx, ss);
+  if (a.norms.out_max) {
+    const unsigned long long mx =
+        isnan(ss) ? 0x7ff8000000000000ull : (unsigned long long)__double_as_longlong(mxd);
+    reduce_norms(a.norms, mx, ss);
+  }
 }
 
 // PROTOX_PDL=0 (read once) launches the sweep kernels without programmatic

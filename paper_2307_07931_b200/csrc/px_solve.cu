@@ -665,6 +665,13 @@ static px_status enqueue_solve(const SolveCtx& x) {
   // its launch and prologue overlap the previous sweep's tail
   const bool one_launch = p2p || (!nccl_multi && x.nparts == 1);
   const int32_t it_first = it;
+  // A single-rank slab of >= 64 M cells writes its ghost ring with one fill
+  // kernel per sweep instead of fused images: measured per sweep over the
+  // sweep kernel alone (profiles/round2_fill_vs_images.jsonl) fused images
+  // cost +0.1 / +3.5 / +6.9 / +5.0 % at 2048 / 4096 / 8192 / 16384 rows of
+  // 16384 columns, the separate fill +1.4 / +2.4 / +3.3 / +3.0 %.
+  const bool sep_fill = !x.c && x.nparts == 1 && x.l->nranks == 1 &&
+                        (int64_t)ext(pli.owned, 0) * ext(pli.owned, 1) >= ((int64_t)64 << 20);
   for (; it < N; ++it) {
     const int32_t slot = (E > 0 && it % E == 0) ? it / E : -1;
     std::vector<SweepLaunch> v;
@@ -705,7 +712,9 @@ static px_status enqueue_solve(const SolveCtx& x) {
       if (split) PX_TRY(launch_stream(MODE_RELAX, x.p->stencil, v[2].a, x.s));
       PX_TRY(cuda_check(cudaStreamWaitEvent(x.s, plan->ev_comm, 0), "stream wait"));
     } else {
+      if (sep_fill) v[0].a.gs.g = 0;
       for (auto& sl : v) PX_TRY(launch_stream(MODE_RELAX, x.p->stencil, sl.a, x.s));
+      if (sep_fill) PX_TRY(launch_fill_ghosts(x.l, 0, nxt[0], x.s));
       if (x.nparts > 1) PX_TRY(local_rows(x.l, nxt, x.s));
     }
     std::swap(cur, nxt);
