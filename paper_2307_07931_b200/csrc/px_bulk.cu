@@ -371,7 +371,8 @@ __global__ void __launch_bounds__(NC * 32 + 32, CPS) k_bulk(const StreamLaunch a
       }
       if (PUSH && ((t.y0 == 0 && a.ps.rdst[0]) || (t.y1 == a.ny && a.ps.rdst[1])))
         push_rows(a.dst, a.ld_dst, t.y0 == 0 ? a.ps.rdst[0] : nullptr, t.y1 == a.ny ? a.ps.rdst[1] : nullptr, a.ny,
-                  a.ps.g, t.c + c0, live, xface, X0, a.gs.g, a.gs.n[0], a.gs.mode[0][0], a.gs.mode[0][1]);
+                  a.ps.g, t.c + c0, live, a.ps.xg > 0 && (X0 < a.ps.xg || X0 + 1 >= a.ps.xn0 - a.ps.xg), X0,
+                  a.ps.xg, a.ps.xn0, a.ps.xm0, a.ps.xm1);
       if (it + (int)gridDim.x < nitems) t = item_of<W, PUSH>(a, it + gridDim.x, nstrips, crows);
     }
   }

@@ -115,6 +115,7 @@ struct PushSpec {
   int32_t g;                       // rows pushed per side (the ghost width)
   int32_t on;                      // any push / wait: boundary chunks are scheduled first
   int32_t rel;                     // publish the previous sweep's pushes (CTA 0, at kernel start)
+  int32_t xg, xn0, xm0, xm1;       // x images of pushed cells (corners): depth, owned width, lo/hi modes
 };
 
 struct StreamLaunch {

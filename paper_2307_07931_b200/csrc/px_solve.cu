@@ -483,6 +483,19 @@ static px_status push_init(const SolveCtx& x, const px_local_info& li) {
   return launch_push_init(pi, x.s);
 }
 
+// Slab size (cells) from which a k = 1 sweep fills its ghost ring with a
+// separate kernel instead of fused images (PROTOX_SEP_FILL_CELLS, read once:
+// tests lower it to reach the path at small sizes).
+static int64_t sep_fill_cells() {
+  static int64_t v = -1;
+  if (v < 0) {
+    const char* e = getenv("PROTOX_SEP_FILL_CELLS");
+    v = e ? atoll(e) : ((int64_t)64 << 20);
+    if (v < 0) v = 0;
+  }
+  return v;
+}
+
 // Enqueue the whole solve on x.s (directly, or under graph capture).
 static px_status enqueue_solve(const SolveCtx& x) {
   const int32_t N = x.o->nsweeps, E = x.o->norm_every;
@@ -652,6 +665,11 @@ static px_status enqueue_solve(const SolveCtx& x) {
     ps.on = 1;
     ps.g = x.l->ghost;
     ps.epoch = st.ctl + CTL_EPOCH;
+    const GhostSpec gsp = ghost_spec(x.l, pli, pli.owned, false);  // x images of the pushed rows
+    ps.xg = gsp.g;
+    ps.xn0 = gsp.n[0];
+    ps.xm0 = gsp.mode[0][0];
+    ps.xm1 = gsp.mode[0][1];
     for (int side = 0; side < 2; ++side) {
       const int32_t pr = side == 0 ? pli.nbr_lo : pli.nbr_hi;
       if (pr < 0) continue;
@@ -670,8 +688,9 @@ static px_status enqueue_solve(const SolveCtx& x) {
   // sweep kernel alone (profiles/round2_fill_vs_images.jsonl) fused images
   // cost +0.1 / +3.5 / +6.9 / +5.0 % at 2048 / 4096 / 8192 / 16384 rows of
   // 16384 columns, the separate fill +1.4 / +2.4 / +3.3 / +3.0 %.
-  const bool sep_fill = !x.c && x.nparts == 1 && x.l->nranks == 1 &&
-                        (int64_t)ext(pli.owned, 0) * ext(pli.owned, 1) >= ((int64_t)64 << 20);
+  // (the push path too: its pushed rows carry their corner images themselves)
+  const bool sep_fill = ((!x.c && x.nparts == 1 && x.l->nranks == 1) || p2p) &&
+                        (int64_t)ext(pli.owned, 0) * ext(pli.owned, 1) >= sep_fill_cells();
   for (; it < N; ++it) {
     const int32_t slot = (E > 0 && it % E == 0) ? it / E : -1;
     std::vector<SweepLaunch> v;
@@ -688,6 +707,7 @@ static px_status enqueue_solve(const SolveCtx& x) {
       const int nb = ((swap ? 1 : 0) + it + 1) & 1;  // the neighbours' buffer this sweep writes (their "next")
       const int32_t g = x.l->ghost, x0 = pli.owned.lo.c[0];
       StreamLaunch& a = v[0].a;
+      if (sep_fill) a.gs.g = 0;
       a.ps.wcount = PX_PUSH_INIT_CTAS + (unsigned long long)it * G;
       a.ps.rel = it > 0;  // publish sweep it-1's pushes
       for (int side = 0; side < 2; ++side) {
@@ -700,6 +720,7 @@ static px_status enqueue_solve(const SolveCtx& x) {
         a.ps.rdst[side] = base + (int64_t)(x0 - nli.alloc.lo.c[0]) + (int64_t)(ty - nli.alloc.lo.c[1]) * nli.ld;
       }
       PX_TRY(launch_stream(MODE_RELAX, x.p->stencil, a, x.s));
+      if (sep_fill) PX_TRY(launch_fill_ghosts(x.l, x.rank, nxt[0], x.s));  // own x ghosts, y faces
     } else if (nccl_multi) {
       // boundary rows, exchange on the comm stream, interior concurrently
       const bool split = v.size() == 3;

@@ -33,11 +33,12 @@ def _port():
     return p
 
 
-def _run(tmp_path, world, bc, n0, n1, na, nb, E, seed, st, graph, inf_row=-1):
+def _run(tmp_path, world, bc, n0, n1, na, nb, E, seed, st, graph, inf_row=-1, extra_env=None):
     port = _port()
     procs = []
     for r in range(world):
-        env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
+                   **(extra_env or {}))
         args = [sys.executable, os.path.join(ROOT, "tests", "_p2p_worker.py"), str(tmp_path), *map(str, (
             bc, n0, n1, na, nb, E, seed, st, graph, inf_row))]
         procs.append(subprocess.Popen(args, env=env, cwd=ROOT, stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
@@ -55,15 +56,21 @@ def _run(tmp_path, world, bc, n0, n1, na, nb, E, seed, st, graph, inf_row=-1):
     return [np.load(tmp_path / f"rank{r}.npz") for r in range(world)]
 
 
-@pytest.mark.parametrize("world,bc,st,graph", [
-    (2, P.PX_BC_PERIODIC, 0, 1),
-    (3, P.PX_BC_PERIODIC, 1, 0),
-    (2, P.PX_BC_DIRICHLET_CC, 0, 0),
-    (3, P.PX_BC_FIXED_GHOSTS, 1, 1),
+@pytest.mark.parametrize("world,bc,st,graph,sep", [
+    (2, P.PX_BC_PERIODIC, 0, 1, 0),
+    (3, P.PX_BC_PERIODIC, 1, 0, 0),
+    (2, P.PX_BC_DIRICHLET_CC, 0, 0, 0),
+    (3, P.PX_BC_FIXED_GHOSTS, 1, 1, 0),
+    (3, P.PX_BC_PERIODIC, 1, 1, 1),
+    (2, P.PX_BC_DIRICHLET_CC, 1, 0, 1),
 ])
-def test_p2p_push_across_processes(tmp_path, world, bc, st, graph):
+def test_p2p_push_across_processes(tmp_path, world, bc, st, graph, sep):
+    """sep = 1: the ghost ring by a fill kernel per sweep (the path of slabs
+    >= 64 M cells, forced here by PROTOX_SEP_FILL_CELLS=0); the pushed rows
+    then carry their corner images themselves (9-point needs them)."""
     n0, n1, na, nb, E, seed = 384, 96 * world, 7, 6, 1, 4100 + world + 10 * bc
-    res = _run(tmp_path, world, bc, n0, n1, na, nb, E, seed, st, graph)
+    res = _run(tmp_path, world, bc, n0, n1, na, nb, E, seed, st, graph,
+               extra_env={"PROTOX_SEP_FILL_CELLS": "0"} if sep else None)
     for r in res:
         assert str(r["kernels"]) == "k_bulk", str(r["kernels"])  # one sweep kernel: the push is fused
     g = 1

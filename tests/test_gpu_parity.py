@@ -758,6 +758,27 @@ def test_temporal_blocking_narrow_kernel_subprocess():
 
 
 @pytest.mark.gpu
+def test_separate_ghost_fill_subprocess():
+    """The ghost ring by fill kernels after each sweep instead of fused images
+    (the path of single-rank slabs >= 64 M cells; PROTOX_SEP_FILL_CELLS=0,
+    read once per process, forces it at test sizes): the single-rank bulk
+    solves of every BC and stencil, the ragged multi-box solves and the
+    self-exchange push re-run in a child process, bit-identical."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PROTOX_SEP_FILL_CELLS="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-m", "gpu",
+                        "tests/test_gpu_parity.py", "-k",
+                        "(test_solve_bulk_kernel_bitwise and 1-) or test_solve_ragged_multibox or "
+                        "test_p2p_halo_push_self_exchange or test_wider_ghosts_k1"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
+
+
+@pytest.mark.gpu
 def test_resident_temporal_blocking_variant_subprocess():
     """The temporally blocked resident solve (A/B option PROTOX_RESIDENT_K=2,3,
     read once per process) stays bit-identical: the resident-path tests re-run
