@@ -166,6 +166,202 @@ __global__ void __launch_bounds__(SB_THREADS, 1) k_smallbox(const SmallBox b) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// k_box1: the same whole-box solve on one CTA of 1024 threads, rebuilt for
+// per-sweep latency (round 2; used for boxes the cluster kernel does not
+// take -- fewer than 16 rows -- where it beats k_smallbox: at 64² 2.14 vs
+// 2.92 µs per sweep; the 8-SM cluster kernel does 1.67).  A thread owns up to BX_MAXC cells at fixed
+// positions (offsets computed once), so a sweep is: its cells' stencil and
+// update -- independent chains the scheduler interleaves -- each cell at a
+// face also writing its ghost images (periodic wrap / odd reflection,
+// corners by the product rule) straight into the output buffer, then ONE
+// block barrier.  A recorded sweep adds a warp-shuffle reduction whose 32
+// per-warp partials go to shared memory; the entries are reduced over the
+// warps in fixed order after the last sweep, off the sweep loop.
+constexpr int BX_THREADS = 1024;
+constexpr int BX_MAXC = 16;
+
+// the images of interior cell (x, y) (value v) in the padded buffer D
+static __device__ __noinline__ void bx_images(double* D, int P, int nx, int ny, int x, int y, int bc, double v) {
+  int ix[3], iy[3];
+  double sx[3], sy[3];
+  int nxi = 1, nyi = 1;
+  ix[0] = x;
+  iy[0] = y;
+  sx[0] = sy[0] = 1.0;
+  const bool per = bc == PX_BC_PERIODIC;
+  const double sg = per ? 1.0 : -1.0;
+  if (x == 0) { ix[nxi] = per ? nx : -1; sx[nxi++] = sg; }       // the ghost column this cell defines
+  if (x == nx - 1) { ix[nxi] = per ? -1 : nx; sx[nxi++] = sg; }
+  if (y == 0) { iy[nyi] = per ? ny : -1; sy[nyi++] = sg; }
+  if (y == ny - 1) { iy[nyi] = per ? -1 : ny; sy[nyi++] = sg; }
+  for (int j = 0; j < nyi; ++j)
+    for (int i = 0; i < nxi; ++i)
+      if (i || j) D[(ix[i] + 1) + (iy[j] + 1) * P] = v * sx[i] * sy[j];
+}
+
+template <int ST, int MAXC>
+__global__ void __launch_bounds__(BX_THREADS, 1) k_box1(const SmallBox b, int n_entries) {
+  extern __shared__ double sm[];
+  const int P = b.nx + 2, Q = b.ny + 2;
+  double* A = sm;
+  double* B = A + (size_t)P * Q;
+  double* F = B + (size_t)P * Q;                                  // rhs, nx*ny
+  double* part = F + (size_t)b.nx * b.ny;                          // [entry][warp][max bits, sum]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ncell = b.nx * b.ny, npad = P * Q;
+  for (int k = tid; k < npad; k += BX_THREADS) {
+    const int x = k % P - 1, y = k / P - 1;
+    const double v = b.phi_in[x + (int64_t)y * b.ld_in];
+    A[k] = v;
+    B[k] = v;  // FIXED ghosts stay in both buffers
+  }
+  for (int k = tid; k < ncell; k += BX_THREADS) F[k] = b.rhs[k % b.nx + (int64_t)(k / b.nx) * b.ld_rhs];
+  __syncthreads();
+  if (b.bc != PX_BC_FIXED_GHOSTS)  // the given ghost ring by the boundary rule (as the sweeps leave it)
+    for (int k = tid; k < ncell; k += BX_THREADS) {
+      const int x = k % b.nx, y = k / b.nx;
+      if (x == 0 || y == 0 || x == b.nx - 1 || y == b.ny - 1) bx_images(A, P, b.nx, b.ny, x, y, b.bc, A[(x + 1) + (y + 1) * P]);
+    }
+  // this thread's cells: padded index, rhs index, face flag
+  int ci[MAXC], fi[MAXC];
+  int nc = 0;
+  // 4 face bits per cell (x lo, x hi, y lo, y hi): the ghost images a cell
+  // defines, written as shifts of its own index (no division in the loop)
+  unsigned long long face = 0ull;
+#pragma unroll
+  for (int j = 0; j < MAXC; ++j) {
+    const int k = tid + j * BX_THREADS;
+    ci[j] = 0;
+    fi[j] = 0;
+    if (k < ncell) {
+      const int x = k % b.nx, y = k / b.nx;
+      ci[j] = (x + 1) + (y + 1) * P;
+      fi[j] = k;
+      if (b.bc != PX_BC_FIXED_GHOSTS) {
+        const unsigned long long f = (x == 0 ? 1ull : 0ull) | (x == b.nx - 1 ? 2ull : 0ull) |
+                                     (y == 0 ? 4ull : 0ull) | (y == b.ny - 1 ? 8ull : 0ull);
+        face |= f << (4 * j);
+      }
+      nc = j + 1;
+    }
+  }
+  const bool per = b.bc == PX_BC_PERIODIC;
+  const double sg = per ? 1.0 : -1.0;
+  const int dxl = per ? b.nx : -1, dxh = per ? -b.nx : 1;            // image column shifts
+  const int dyl = per ? b.ny * P : -P, dyh = per ? -b.ny * P : P;    // image row shifts
+  __syncthreads();
+  const double scale = b.scale, lambda = b.lambda;
+  int entry = 0;
+  for (int s = 0; s < b.nsweeps; ++s) {
+    const bool rec = b.every > 0 && s % b.every == 0;
+    double mxd = 0.0, ss = 0.0;
+#pragma unroll
+    for (int j = 0; j < MAXC; ++j) {
+      if (j < nc) {
+        const int i = ci[j];
+        const double L = sb_taps<ST>(A, P, i);
+        const double r = __dsub_rn(__dmul_rn(scale, L), F[fi[j]]);
+        const double o = __dadd_rn(A[i], __dmul_rn(lambda, r));
+        B[i] = o;
+        const unsigned f = (unsigned)(face >> (4 * j)) & 15u;
+        if (f) {
+          const double so = sg * o;
+          if (f & 1u) B[i + dxl] = so;
+          if (f & 2u) B[i + dxh] = so;
+          if (f & 12u) {
+            const int dy = (f & 4u) ? dyl : dyh;
+            B[i + dy] = so;
+            if (f & 1u) B[i + dy + dxl] = sg * so;
+            if (f & 2u) B[i + dy + dxh] = sg * so;
+            if ((f & 12u) == 12u) {  // one-row box: its cells define both y images
+              B[i + dyh] = so;
+              if (f & 1u) B[i + dyh + dxl] = sg * so;
+              if (f & 2u) B[i + dyh + dxh] = sg * so;
+            }
+          }
+        }
+        mxd = fmax(mxd, fabs(r));  // exact (one of its operands); NaN restored from Σr² below
+        ss = fma(r, r, ss);
+      }
+    }
+    if (rec) {
+      unsigned long long mx = isnan(ss) ? 0x7ff8000000000000ull : (unsigned long long)__double_as_longlong(mxd);
+      for (int o = 16; o > 0; o >>= 1) {
+        mx = umax64(mx, __shfl_xor_sync(FULL_MASK, mx, o));
+        ss = ss + __shfl_xor_sync(FULL_MASK, ss, o);
+      }
+      if (lane == 0) {
+        part[((size_t)entry * 32 + warp) * 2] = __longlong_as_double((long long)mx);
+        part[((size_t)entry * 32 + warp) * 2 + 1] = ss;
+      }
+      ++entry;
+    }
+    __syncthreads();
+    double* t = A;
+    A = B;
+    B = t;
+  }
+  if (b.final_norm) {
+    double mxd = 0.0, ss = 0.0;
+#pragma unroll
+    for (int j = 0; j < MAXC; ++j) {
+      if (j >= nc) break;
+      const double r = __dsub_rn(__dmul_rn(scale, sb_taps<ST>(A, P, ci[j])), F[fi[j]]);
+      mxd = fmax(mxd, fabs(r));
+      ss = fma(r, r, ss);
+    }
+    unsigned long long mx = isnan(ss) ? 0x7ff8000000000000ull : (unsigned long long)__double_as_longlong(mxd);
+    for (int o = 16; o > 0; o >>= 1) {
+      mx = umax64(mx, __shfl_xor_sync(FULL_MASK, mx, o));
+      ss = ss + __shfl_xor_sync(FULL_MASK, ss, o);
+    }
+    if (lane == 0) {
+      part[((size_t)entry * 32 + warp) * 2] = __longlong_as_double((long long)mx);
+      part[((size_t)entry * 32 + warp) * 2 + 1] = ss;
+    }
+    ++entry;
+  }
+  __syncthreads();
+  for (int e = tid; e < entry; e += BX_THREADS) {  // entries over the warps in fixed order
+    unsigned long long m = 0ull;
+    double t = 0.0;
+    for (int w = 0; w < 32; ++w) {
+      m = umax64(m, (unsigned long long)__double_as_longlong(part[((size_t)e * 32 + w) * 2]));
+      t = w ? __dadd_rn(t, part[((size_t)e * 32 + w) * 2 + 1]) : part[((size_t)e * 32 + w) * 2 + 1];
+    }
+    b.d_max[e] = __longlong_as_double((long long)m);
+    b.d_sum[e] = t;
+  }
+  for (int k = tid; k < npad; k += BX_THREADS) {
+    const int x = k % P - 1, y = k / P - 1;
+    b.phi_out[x + (int64_t)y * b.ld_out] = A[k];
+  }
+}
+
+static int box1_entries(const SmallBox& b) {
+  return (b.every > 0 ? (b.nsweeps + b.every - 1) / b.every : 0) + (b.final_norm ? 1 : 0);
+}
+static size_t box1_smem(const SmallBox& b) {
+  return ((size_t)2 * (b.nx + 2) * (b.ny + 2) + (size_t)b.nx * b.ny + (size_t)box1_entries(b) * 32 * 2) *
+         sizeof(double);
+}
+// PROTOX_SMALLBOX (read once, A/B): unset = the 8-CTA cluster kernel when
+// the box has 16+ rows, else k_box1, else k_smallbox; "box1" / "old" force
+// k_box1 / k_smallbox
+static int box1_mode() {
+  static int m = -1;
+  if (m < 0) {
+    const char* e = getenv("PROTOX_SMALLBOX");
+    m = !e ? 0 : (e[0] == 'b' ? 1 : (e[0] == 'o' ? 2 : 0));
+  }
+  return m;
+}
+static bool box1_eligible(const SmallBox& b) {
+  return box1_mode() != 2 && b.g == 1 && (int64_t)b.nx * b.ny <= (int64_t)BX_THREADS * BX_MAXC &&
+         box1_smem(b) <= 200 * 1024;
+}
+
 size_t smallbox_smem(int nx, int ny) {
   return ((size_t)2 * (nx + 2) * (ny + 2) + (size_t)nx * ny) * sizeof(double);
 }
@@ -173,8 +369,26 @@ size_t smallbox_smem(int nx, int ny) {
 bool smallbox_fits(int nx, int ny) { return nx >= 1 && ny >= 1 && smallbox_smem(nx, ny) <= 200 * 1024; }
 
 px_status launch_smallbox(const SmallBox& b, cudaStream_t s) {
-  // 16+ rows: spread the box over a cluster of 8 SMs (px_cluster.cu)
-  if (cluster_box_eligible(b)) return launch_cluster_box(b, s);
+  // 16+ rows: spread the box over a cluster of 8 SMs (px_cluster.cu): one SM
+  // running k_box1 is issue-bound (73 % issue-active at 1.76 µs per 64² sweep)
+  if (box1_mode() == 0 && cluster_box_eligible(b)) return launch_cluster_box(b, s);
+  if (box1_eligible(b)) {
+    const size_t smem = box1_smem(b);
+    const bool small = (int64_t)b.nx * b.ny <= 4 * BX_THREADS;  // up to 4 cells per thread: all in registers
+    void (*fn)(const SmallBox, int) = b.stencil ? (small ? k_box1<1, 4> : k_box1<1, BX_MAXC>)
+                                                : (small ? k_box1<0, 4> : k_box1<0, BX_MAXC>);
+    static bool attr[4] = {false, false, false, false};
+    const int ai = (b.stencil ? 2 : 0) + (small ? 1 : 0);
+    if (!attr[ai]) {
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr[ai] = true;
+    }
+    fn<<<1, BX_THREADS, smem, s>>>(b, box1_entries(b));
+    note_kernel("k_box1");
+    count_launches(1);
+    return cuda_check(cudaGetLastError(), "small-box kernel launch");
+  }
+
   const size_t smem = smallbox_smem(b.nx, b.ny);
   cudaError_t e;
   if (b.stencil == 0) {

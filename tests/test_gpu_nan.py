@@ -14,6 +14,8 @@ The field is compared NaN-aware (same NaN mask; every other cell bit for bit:
 GPU and CPU NaN payloads differ by design), max-norms by NaN mask and bits,
 Σr² by NaN mask and 1e-12 relative.  Each case asserts which kernel the solve
 actually ran (px_last_solve_kernels)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -81,16 +83,46 @@ def _solve_case(n0, n1, bc, N, E, kind, seed, nranks=1, tk=1, box=None, graph=Tr
     return kern
 
 
-@pytest.mark.parametrize("kind", KINDS)
-def test_nan_cluster_box(kind):
-    """BJ.C1 shape (64², Dirichlet-CC): k_cluster_box (8-CTA cluster, DSMEM halos)."""
-    assert "k_cluster_box" in _solve_case(64, 64, P.PX_BC_DIRICHLET_CC, 30, 1, kind, 11)
+def _box_kernel(rows):
+    """The whole-box kernel px_solve picks (PROTOX_SMALLBOX, read once per
+    process: default the 8-CTA cluster kernel from 16 rows, else k_box1;
+    'box1' / 'old' force k_box1 / the round-1 one-CTA k_smallbox)."""
+    mode = os.environ.get("PROTOX_SMALLBOX", "")
+    if mode.startswith("b"):
+        return "k_box1"
+    if mode.startswith("o"):
+        return "k_smallbox"
+    return "k_cluster_box" if rows >= 16 else "k_box1"
 
 
 @pytest.mark.parametrize("kind", KINDS)
-def test_nan_smallbox(kind):
-    """A box of < 16 rows: k_smallbox (one CTA)."""
-    assert "k_smallbox" in _solve_case(64, 12, P.PX_BC_PERIODIC, 20, 1, kind, 12)
+def test_nan_box_c1(kind):
+    """BJ.C1 shape (64², Dirichlet-CC): the whole solve in one launch."""
+    assert _box_kernel(64) in _solve_case(64, 64, P.PX_BC_DIRICHLET_CC, 30, 1, kind, 11)
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_nan_box_short(kind):
+    """A box of < 16 rows, periodic."""
+    assert _box_kernel(12) in _solve_case(64, 12, P.PX_BC_PERIODIC, 20, 1, kind, 12)
+
+
+@pytest.mark.parametrize("mode", ["box1", "old"])
+def test_box_kernel_variants_subprocess(mode):
+    """The other whole-box kernels (k_box1 for every box it fits; the round-1
+    one-CTA k_smallbox) stay bit-identical: the small-box parity and NaN tests
+    re-run in a child process with PROTOX_SMALLBOX=<mode>."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PROTOX_SMALLBOX=mode)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-m", "gpu",
+                        "tests/test_gpu_nan.py", "tests/test_gpu_parity.py", "-k",
+                        "nan_box_c1 or nan_box_short or config1 or test_solve_ragged_multibox or "
+                        "norm_every_variants or whole_box"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
 
 
 @pytest.mark.parametrize("kind", KINDS)

@@ -185,6 +185,25 @@ def test_solve_ragged_multibox(bc, st, graph):
     _check_norms(norms, rn)
 
 
+@pytest.mark.parametrize("shape", [(64, 64), (3, 5), (1, 40), (40, 1), (127, 129), (100, 40)])
+@pytest.mark.parametrize("bc", [P.PX_BC_PERIODIC, P.PX_BC_DIRICHLET_CC, P.PX_BC_FIXED_GHOSTS])
+@pytest.mark.parametrize("st", [P.PX_LAPLACE_5PT, P.PX_MEHRSTELLEN_9PT])
+def test_solve_whole_box_shapes(shape, bc, st):
+    """Whole-box solves in one launch (k_box1 by default): up to 4 and up to
+    16 cells per thread (127 x 129 = 16383 cells), one-cell-wide boxes (a cell
+    is then its own image on both sides), every BC and stencil; odd and even
+    sweep counts and norm periods 1, 3 and 0 (final entry only)."""
+    n0, n1 = shape
+    h = 1.0 / 128
+    lam = h * h / 8 if st == 0 else 3 * h * h / 16
+    phi0, rho = _fields(n0, n1, 1, 29 + n0, bc)
+    for N, E in ((9, 1), (10, 3), (7, 0)):
+        out, norms, _ = run_gpu_solve(n0, n1, h, lam, bc, st, N, E, phi0, rho)
+        ref, rn = oracle.solve(_orc_problem(n0, n1, h, lam, bc, st, N, E), phi0, rho)
+        assert bits_equal(out, ref[1:-1, 1:-1]), (N, E, ulp_diff(out, ref[1:-1, 1:-1]))
+        _check_norms(norms, rn)
+
+
 @pytest.mark.parametrize("shape", [(130, 400), (1022, 149), (4, 5000), (1024, 101), (2048, 9)])
 @pytest.mark.parametrize("bc", [P.PX_BC_PERIODIC, P.PX_BC_DIRICHLET_CC, P.PX_BC_FIXED_GHOSTS])
 @pytest.mark.parametrize("st", [P.PX_LAPLACE_5PT, P.PX_MEHRSTELLEN_9PT])
