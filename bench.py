@@ -139,7 +139,7 @@ class ClockSampler:
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_power_cap,power.draw,power.limit")
 
     def __init__(self, index: int):
         self.index = index
@@ -178,8 +178,18 @@ class ClockSampler:
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i] == "Active"})
+        def num(v):
+            try:
+                return float(v)
+            except ValueError:
+                return None
+        pw = [v for v in (num(r[7]) for r in self.rows if len(r) > 8) if v is not None]
+        pl = [v for v in (num(r[8]) for r in self.rows if len(r) > 8) if v is not None]
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows),
+                # board power under load against its limit: sw_power_cap explains a
+                # compute-heavier kernel (C4) running below max clocks
+                "power_w": statistics.median(pw) if pw else None, "power_limit_w": max(pl) if pl else None}
 
 
 # ----------------------------------------------------------------- oracle arm

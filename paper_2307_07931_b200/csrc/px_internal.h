@@ -191,6 +191,7 @@ struct ResidentLaunch {
   double* d_max;
   double* d_sum;
   double* ws;             // resident_ws_doubles(...) doubles, zero not required
+  int unroll;             // set by launch_resident: unrolled column walk (rmax <= 7)
 };
 size_t resident_ws_doubles(int nx, int grid, int n_entries);
 // CTAs and dynamic shared memory of the resident kernel for an nx x ny

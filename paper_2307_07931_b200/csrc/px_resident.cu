@@ -150,33 +150,50 @@ __device__ __forceinline__ void rs_xghost(double* row, int nx, const int (&xm)[2
 }
 
 // ---- LL exchange (the row mailbox carries its own flags) -------------------
-// One double per 16-byte entry, each 8-byte half = half the double + the
-// sweep tag (NCCL's LL idea): a 16-byte store writes each 8-byte half
-// atomically, so a reader that sees the tag in both halves has the whole
-// value of that sweep -- no release fence, no flag word, no barrier before
-// the publication.
+// One double per 16-byte entry, each 8-byte half = (sweep tag << 32) | one
+// 32-bit half of the double (NCCL's LL idea), stored as one u64 element of a
+// v2.u64 access, i.e. single-copy atomic: a reader that sees the tag in both
+// halves has the whole value of that sweep -- no release fence, no flag word,
+// no barrier before the publication.
+#ifndef PX_LL_SYS
+#define PX_LL_SYS 0  // A/B: 1 = the round-2 volatile (system-scope) mailbox accesses
+#endif
 __device__ __forceinline__ void ll_put(double* e, double v, uint32_t tag) {
   const unsigned long long b = (unsigned long long)__double_as_longlong(v);
-  asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(e), "r"((uint32_t)b), "r"(tag),
-               "r"((uint32_t)(b >> 32)), "r"(tag)
+  const unsigned long long t = (unsigned long long)tag << 32;
+#if PX_LL_SYS
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(e), "l"(t | (b & 0xffffffffull)), "l"(t | (b >> 32))
                : "memory");
+#else
+  // gpu scope (the mailbox never leaves the device): STG.STRONG.GPU, not .SYS
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(e), "l"(t | (b & 0xffffffffull)),
+               "l"(t | (b >> 32))
+               : "memory");
+#endif
 }
+#ifndef PX_RS_DIAG
+#define PX_RS_DIAG 0  // A/B diagnostics only (scripts/build_variant.py): 1 no tag wait, 2 no row compute
+#endif
 #ifndef LL_BACKOFF_NS
 #define LL_BACKOFF_NS 100
 #endif
 struct LL {
-  uint32_t lo, t0, hi, t1;
+  unsigned long long lo, hi;  // (tag << 32) | low / high half of the double
 };
 __device__ __forceinline__ LL ll_load(const double* e) {
   LL v;
-  asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(v.lo), "=r"(v.t0), "=r"(v.hi), "=r"(v.t1)
-               : "l"(e)
-               : "memory");
+#if PX_LL_SYS
+  asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(v.lo), "=l"(v.hi) : "l"(e) : "memory");
+#else
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(v.lo), "=l"(v.hi) : "l"(e) : "memory");
+#endif
   return v;
 }
+__device__ __forceinline__ bool ll_ok(const LL& v, uint32_t tag) {
+  return (uint32_t)(v.lo >> 32) == tag && (uint32_t)(v.hi >> 32) == tag;
+}
 __device__ __forceinline__ double ll_val(const LL& v) {
-  return __longlong_as_double((long long)(((unsigned long long)v.hi << 32) | v.lo));
+  return __longlong_as_double((long long)((v.hi << 32) | (v.lo & 0xffffffffull)));
 }
 // the n (<= 4) entries e[i], all loads in flight together; re-poll until
 // every tag matches
@@ -185,15 +202,19 @@ __device__ __forceinline__ void ll_get(const double* const (&e)[4], uint32_t tag
   LL v[4];
 #pragma unroll
   for (int i = 0; i < n; ++i) v[i] = ll_load(e[i]);
+#if PX_RS_DIAG == 1
+  for (int it = 0; it < 0; ++it) {  // diagnostic: take whatever the mailbox holds
+#else
   for (;;) {
+#endif
     bool ok = true;
 #pragma unroll
-    for (int i = 0; i < n; ++i) ok = ok && v[i].t0 == tag && v[i].t1 == tag;
+    for (int i = 0; i < n; ++i) ok = ok && ll_ok(v[i], tag);
     if (ok) break;
     if (LL_BACKOFF_NS) __nanosleep(LL_BACKOFF_NS);  // fewer polls in flight: L2 stays free for the publications
 #pragma unroll
     for (int i = 0; i < n; ++i)
-      if (v[i].t0 != tag || v[i].t1 != tag) v[i] = ll_load(e[i]);
+      if (!ll_ok(v[i], tag)) v[i] = ll_load(e[i]);
   }
 #pragma unroll
   for (int i = 0; i < n; ++i) out[i] = ll_val(v[i]);
@@ -245,8 +266,8 @@ __device__ __forceinline__ void ll_rows(const double* A, double* B, const double
       ll_ximg(brow, x, nx, o.x, o.y, xm);
       if (r == 1) {
         if (pub_first) {
-          ll_put(pub_first + 2 * (x - 2), o.x, tag);
-          ll_put(pub_first + 2 * (x - 1), o.y, tag);
+          ll_put(pub_first + (x - 2), o.x, tag);
+          ll_put(pub_first + (x - 2) + nx, o.y, tag);
         } else if (refl_top) {
           *reinterpret_cast<double2*>(B + x) = make_double2(-o.x, -o.y);
           ll_ximg(B, x, nx, -o.x, -o.y, xm);
@@ -254,8 +275,8 @@ __device__ __forceinline__ void ll_rows(const double* A, double* B, const double
       }
       if (r == R) {
         if (pub_last) {
-          ll_put(pub_last + 2 * (x - 2), o.x, tag);
-          ll_put(pub_last + 2 * (x - 1), o.y, tag);
+          ll_put(pub_last + (x - 2), o.x, tag);
+          ll_put(pub_last + (x - 2) + nx, o.y, tag);
         } else if (refl_bot) {
           double* h = B + (size_t)(R + 1) * P;
           *reinterpret_cast<double2*>(h + x) = make_double2(-o.x, -o.y);
@@ -278,6 +299,100 @@ __device__ __forceinline__ void ll_rows(const double* A, double* B, const double
   }
 }
 
+// Store of row r's pair o (with its x images) into B and, for row 1 / row R,
+// the publication (or the reflected halo row) -- the per-row epilogue of
+// ll_rows, shared by the unrolled walk below.
+__device__ __forceinline__ void ll_emit(double* B, int P, int nx, int R, int r, int x, double2 o,
+                                        const int (&xm)[2], double* pub_first, double* pub_last, bool refl_top,
+                                        bool refl_bot, uint32_t tag) {
+  double* brow = B + (size_t)r * P;
+  *reinterpret_cast<double2*>(brow + x) = o;
+  ll_ximg(brow, x, nx, o.x, o.y, xm);
+  if (r == 1) {
+    if (pub_first) {
+      ll_put(pub_first + (x - 2), o.x, tag);
+      ll_put(pub_first + (x - 2) + nx, o.y, tag);
+    } else if (refl_top) {
+      *reinterpret_cast<double2*>(B + x) = make_double2(-o.x, -o.y);
+      ll_ximg(B, x, nx, -o.x, -o.y, xm);
+    }
+  }
+  if (r == R) {
+    if (pub_last) {
+      ll_put(pub_last + (x - 2), o.x, tag);
+      ll_put(pub_last + (x - 2) + nx, o.y, tag);
+    } else if (refl_bot) {
+      double* h = B + (size_t)(R + 1) * P;
+      *reinterpret_cast<double2*>(h + x) = make_double2(-o.x, -o.y);
+      ll_ximg(h, x, nx, -o.x, -o.y, xm);
+    }
+  }
+}
+
+// One pair of row r from the register copies of rows r-1, r, r+1 (oracle
+// expression tree, every op rounded).
+template <int ST, bool NORM>
+__device__ __forceinline__ double2 ll_pair(double2 S, double sw, double se, double2 C, double cw, double ce,
+                                           double2 N, double nw, double ne, double2 f, double scale,
+                                           double lambda, unsigned long long& mx, double& ss) {
+  const double L0 = rs_taps<ST>(cw, C.y, S.x, N.x, C.x, sw, S.y, nw, N.y);
+  const double L1 = rs_taps<ST>(C.x, ce, S.y, N.y, C.y, S.x, se, N.x, ne);
+  const double r0 = __dsub_rn(__dmul_rn(scale, L0), f.x);
+  const double r1 = __dsub_rn(__dmul_rn(scale, L1), f.y);
+  double2 o;
+  o.x = __dadd_rn(C.x, __dmul_rn(lambda, r0));
+  o.y = __dadd_rn(C.y, __dmul_rn(lambda, r1));
+  if (NORM) {
+    mx = umax64(mx, (unsigned long long)__double_as_longlong(fabs(r0)));
+    ss = fma(r0, r0, ss);
+    mx = umax64(mx, (unsigned long long)__double_as_longlong(fabs(r1)));
+    ss = fma(r1, r1, ss);
+  }
+  return o;
+}
+
+// ll_rows for a CTA of R <= RM rows with the whole column walk UNROLLED: a
+// thread loads its pair of all R + 2 rows up front, so the R rows' expression trees are independent streams
+// the scheduler interleaves (the rolled walk of ll_rows issues one row's
+// chain at a time and shuffles its registers between rows).  Same rows in
+// the same order as ll_rows (row 1, row R, rows 2..R-1) -- same stores, same
+// publications, same per-thread norm order: bit-identical.
+template <int ST, bool NORM, int RM>
+__device__ __forceinline__ void ll_rows_u(const double* A, double* B, const double* F, int P, int nx, int R,
+                                          double scale, double lambda, const int (&xm)[2], double* pub_first,
+                                          double* pub_last, bool refl_top, bool refl_bot, uint32_t tag,
+                                          unsigned long long& mx, double& ss) {
+  for (int q = threadIdx.x; q < nx / 2; q += blockDim.x) {
+    const int x = 2 * q + 2;
+    double2 a[RM + 2];
+#pragma unroll
+    for (int i = 0; i < RM + 2; ++i)
+      if (i <= R + 1) a[i] = *reinterpret_cast<const double2*>(A + (size_t)i * P + x);
+    // the W/E neighbour columns (and ρ) are loaded where a row uses them:
+    // keeping them for every row would spill at 128 registers per thread
+#define LL_ROW(r)                                                                                            \
+  {                                                                                                          \
+    const double* ac = A + (size_t)(r) * P + x;                                                              \
+    const double sw = ST ? ac[-P - 1] : 0.0, se = ST ? ac[-P + 2] : 0.0;                                     \
+    const double nw = ST ? ac[P - 1] : 0.0, ne = ST ? ac[P + 2] : 0.0;                                       \
+    ll_emit(B, P, nx, R, r, x,                                                                               \
+            ll_pair<ST, NORM>(a[r - 1], sw, se, a[r], ac[-1], ac[2], a[r + 1], nw, ne,                       \
+                              *reinterpret_cast<const double2*>(F + (size_t)((r) - 1) * nx + (x - 2)), scale, \
+                              lambda, mx, ss),                                                               \
+            xm, pub_first, pub_last, refl_top, refl_bot, tag);                                               \
+  }
+    LL_ROW(1);
+#pragma unroll
+    for (int r = 2; r <= RM; ++r)
+      if (r == R) LL_ROW(r);
+#pragma unroll
+    for (int r = 2; r < RM; ++r)
+      if (r < R) LL_ROW(r);
+#undef LL_ROW
+  }
+}
+constexpr int LL_UNROLL_ROWS = 7;  // BJ.C2: 1024 rows over 148 CTAs = 6 or 7 rows each
+
 template <int ST>
 __global__ void __launch_bounds__(RS_THREADS, 1) k_resident(const ResidentLaunch p) {
   cg::grid_group grid = cg::this_grid();
@@ -288,7 +403,11 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resident(const ResidentLaunch
   double* A = sm;
   double* B = A + (size_t)(p.rmax + 2) * P;
   double* F = B + (size_t)(p.rmax + 2) * P;
-  double* pub = p.ws + ((G + 1) & ~1);             // [slot][cta][first, last][nx] LL entries (16 B each)
+  // [slot][cta][first, last][nx] LL entries (16 B each); the row's pair q puts
+  // its cells in entries q and nx/2 + q, so every warp-wide store and poll
+  // covers whole 32-B sectors (16-B entries at a 32-B stride -- a pair's two
+  // cells side by side -- double the hop latency: scripts/ll_latency.cu)
+  double* pub = p.ws + ((G + 1) & ~1);
   double* part = pub + (size_t)2 * G * 2 * 2 * nx; // [entry][cta][max, sum]
   const int up = c > 0 ? c - 1 : G - 1, dn = c < G - 1 ? c + 1 : 0;
   const bool top_x = c > 0 || p.ymode[0] == GH_WRAP;      // halo row 0 from CTA `up`
@@ -315,6 +434,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resident(const ResidentLaunch
 
   int entry = 0;
   const bool refl_top = !top_x && p.ymode[0] == GH_REFLECT, refl_bot = !bot_x && p.ymode[1] == GH_REFLECT;
+  const bool unrolled = p.unroll && p.rmax <= LL_UNROLL_ROWS;
   for (int s = 0; s < p.nsweeps; ++s) {
     const bool rec = p.every > 0 && s % p.every == 0;
     const uint32_t tag = (uint32_t)s + 1u;
@@ -331,9 +451,27 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resident(const ResidentLaunch
       if (rec) ll_rows<ST, true>(A, B, F, P, nx, R, lo, hi, p.scale, p.lambda, xm, pf, pl, refl_top, refl_bot, tag, mx, ss);
       else ll_rows<ST, false>(A, B, F, P, nx, R, lo, hi, p.scale, p.lambda, xm, pf, pl, refl_top, refl_bot, tag, mx, ss);
     };
-    sweep(1, 1);
-    if (R > 1) sweep(R, R);
-    if (R > 2) sweep(2, R - 1);
+#if PX_RS_DIAG == 2
+    if (true) {  // diagnostic: publish the rows without computing any
+      for (int q = tid; q < nx / 2; q += nt) {
+        const int x = 2 * q + 2;
+        if (pf) { ll_put(pf + (x - 2), 0.0, tag); ll_put(pf + (x - 2) + nx, 0.0, tag); }
+        if (pl) { ll_put(pl + (x - 2), 0.0, tag); ll_put(pl + (x - 2) + nx, 0.0, tag); }
+      }
+    } else
+#endif
+    if (unrolled) {
+      if (rec)
+        ll_rows_u<ST, true, LL_UNROLL_ROWS>(A, B, F, P, nx, R, p.scale, p.lambda, xm, pf, pl, refl_top, refl_bot,
+                                            tag, mx, ss);
+      else
+        ll_rows_u<ST, false, LL_UNROLL_ROWS>(A, B, F, P, nx, R, p.scale, p.lambda, xm, pf, pl, refl_top, refl_bot,
+                                             tag, mx, ss);
+    } else {
+      sweep(1, 1);
+      if (R > 1) sweep(R, R);
+      if (R > 2) sweep(2, R - 1);
+    }
     if (rec) {
       rs_block_reduce(mx, ss, part + ((size_t)entry * G + c) * 2);
       ++entry;
@@ -347,11 +485,11 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resident(const ResidentLaunch
       const int x = 2 * q + 2;
       double v[4];
       if (top_x && bot_x) {
-        const double* const e[4] = {fu + 4 * q, fu + 4 * q + 2, fd + 4 * q, fd + 4 * q + 2};
+        const double* const e[4] = {fu + 2 * q, fu + 2 * q + nx, fd + 2 * q, fd + 2 * q + nx};
         ll_get<4>(e, tag, v);
       } else if (top_x || bot_x) {
         const double* f = top_x ? fu : fd;
-        const double* const e[4] = {f + 4 * q, f + 4 * q + 2, f, f};
+        const double* const e[4] = {f + 2 * q, f + 2 * q + nx, f, f};
         ll_get<2>(e, tag, v);
         if (!top_x) {
           v[2] = v[0];
@@ -406,6 +544,310 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resident(const ResidentLaunch
     for (int x = tid - 1; x <= nx; x += nt) p.phi_out[-p.ld_out + x] = A[x + 2];
   if (c == G - 1)
     for (int x = tid - 1; x <= nx; x += nt) p.phi_out[(int64_t)p.ny * p.ld_out + x] = A[(size_t)(R + 1) * P + x + 2];
+}
+
+// ---------------------------------------------------------------------------
+// k_resident_reg<ST>: the resident solve with the iterate in REGISTERS.
+// Thread q owns column pair q (columns 2q, 2q+1) of every row of its CTA
+// plus the two halo rows, as double2 registers that persist across sweeps;
+// only ρ stays in shared memory.  W/E neighbours come from the adjacent
+// lanes (__shfl_up/down) and, across warp boundaries, from per-warp edge
+// arrays in shared memory (lane 0's first and the last active lane's second
+// column of every row, double-buffered by sweep parity, written before the
+// one block barrier per sweep); at the domain's x faces from the edge of the
+// last / first warp (periodic), the cell itself (odd reflection) or the fixed
+// ghost columns of φ^0.  Every thread reads its W/E candidates the same way
+// (one shuffle and one shared load, a dummy broadcast address where it has
+// no edge) and selects: no divergent branch per row.  The row count is a
+// template parameter (the CTA's R dispatched once), so the column walk has
+// no per-row predicates.  A sweep: row R, then row 1 (both published to the
+// L2 mailbox at once, as k_resident), then rows 2..R-1 in place with one
+// rolling register of the old row above; then the neighbours' rows of the
+// new iterate are fetched into the halo registers, the edges written, one
+// barrier.  Per cell the same expression tree, per thread the same norm order
+// (row 1, row R, rows 2..R-1; final pass rows 1..R) and the same thread ->
+// pair map as k_resident: bit-identical to it.
+constexpr int RR_RM = 7;  // BJ.C2: 1024 rows over 148 CTAs = 6 or 7 rows each
+struct RrCtx {
+  const double* F;                 // ρ rows [R][nx]
+  double *eL, *eR;                 // [2][NWP][RE]
+  const double* wp;                // west candidate (buffer 0, row 0); dummy broadcast if none
+  const double* ep;                // east candidate
+  int wbs, ebs;                    // buffer stride of wp / ep (0: not double-buffered)
+  bool wld, wneg, eld, eneg;       // take the shared candidate / the negated own cell
+  bool st_l, st_r;                 // this lane stores the warp's left / right edge
+  int warp, x, xs, nx, G, c, up, dn;
+  bool act, top_x, bot_x, refl_top, refl_bot;
+  double *pub, *part;
+};
+template <int ST, int RR>
+__device__ __forceinline__ void rr_body(const ResidentLaunch& p, const RrCtx& k, cg::grid_group& grid) {
+  constexpr int NWP = RS_THREADS / 32, RE = RR_RM + 2, BS = NWP * RE;
+  const int tid = threadIdx.x, nx = k.nx, x = k.x, G = k.G, c = k.c;
+  const int y0 = (int)((int64_t)c * p.ny / G);
+  double2 cur[RR + 2];
+#pragma unroll
+  for (int r = 0; r < RR + 2; ++r) {
+    cur[r] = make_double2(0.0, 0.0);
+    if (k.act) {
+      const double* src = p.phi_in + (int64_t)(y0 - 1 + r) * p.ld_in + x;
+      cur[r] = make_double2(src[0], src[1]);
+    }
+  }
+  auto put_edges = [&](int b) {
+#pragma unroll
+    for (int r = 0; r < RR + 2; ++r) {
+      if (k.st_l) k.eL[b * BS + k.warp * RE + r] = cur[r].x;
+      if (k.st_r) k.eR[b * BS + k.warp * RE + r] = cur[r].y;
+    }
+  };
+  put_edges(0);
+  __threadfence();
+  grid.sync();
+
+  auto west = [&](double2 v, int r, int b) -> double {
+    const double sh = __shfl_up_sync(FULL_MASK, v.y, 1);
+    const double t = k.wp[b * k.wbs + r];
+    return k.wld ? t : (k.wneg ? -v.x : sh);
+  };
+  auto east = [&](double2 v, int r, int b) -> double {
+    const double sh = __shfl_down_sync(FULL_MASK, v.x, 1);
+    const double t = k.ep[b * k.ebs + r];
+    return k.eld ? t : (k.eneg ? -v.y : sh);
+  };
+  // one pair of row r from rows S (r-1), C (r), N (r+1) of buffer b's iterate;
+  // res = the residuals (0 on lanes past the last pair)
+  auto pair = [&](double2 S, double2 C, double2 N, int r, int b, double2& res) -> double2 {
+    const double cw = west(C, r, b), ce = east(C, r, b);
+    double sw = 0.0, se = 0.0, nw = 0.0, ne = 0.0;
+    if (ST) {
+      sw = west(S, r - 1, b);
+      se = east(S, r - 1, b);
+      nw = west(N, r + 1, b);
+      ne = east(N, r + 1, b);
+    }
+    const double L0 = rs_taps<ST>(cw, C.y, S.x, N.x, C.x, sw, S.y, nw, N.y);
+    const double L1 = rs_taps<ST>(C.x, ce, S.y, N.y, C.y, S.x, se, N.x, ne);
+    const double2 f = *reinterpret_cast<const double2*>(k.F + (size_t)(r - 1) * nx + k.xs);
+    res.x = __dsub_rn(__dmul_rn(p.scale, L0), f.x);
+    res.y = __dsub_rn(__dmul_rn(p.scale, L1), f.y);
+    const double2 o = make_double2(__dadd_rn(C.x, __dmul_rn(p.lambda, res.x)),
+                                   __dadd_rn(C.y, __dmul_rn(p.lambda, res.y)));
+    if (!k.act) res = make_double2(0.0, 0.0);
+    return o;
+  };
+  auto acc = [&](double2 res, unsigned long long& mx, double& ss) {
+    mx = umax64(mx, (unsigned long long)__double_as_longlong(fabs(res.x)));
+    ss = fma(res.x, res.x, ss);
+    mx = umax64(mx, (unsigned long long)__double_as_longlong(fabs(res.y)));
+    ss = fma(res.y, res.y, ss);
+  };
+
+  int entry = 0;
+  for (int s = 0; s < p.nsweeps; ++s) {
+    const int b = s & 1;
+    const bool rec = p.every > 0 && s % p.every == 0;
+    const uint32_t tag = (uint32_t)s + 1u;
+    const int slot = (s + 1) & 1;
+    double* mine = k.pub + (size_t)(slot * G + c) * 2 * 2 * nx;
+    unsigned long long mx = 0ull;
+    double ss = 0.0;
+    // row R, then row 1: both published at once
+    double2 rR = make_double2(0.0, 0.0), r1;
+    const double2 nR = RR > 1 ? pair(cur[RR - 1], cur[RR], cur[RR + 1], RR, b, rR) : make_double2(0.0, 0.0);
+    const double2 n1 = pair(cur[0], cur[1], cur[2], 1, b, r1);
+    if (rec) {
+      acc(r1, mx, ss);
+      if (RR > 1) acc(rR, mx, ss);
+    }
+    if (k.act) {
+      if (k.top_x) {
+        ll_put(mine + x, n1.x, tag);
+        ll_put(mine + x + nx, n1.y, tag);
+      }
+      if (k.bot_x) {
+        const double2 o = RR > 1 ? nR : n1;
+        ll_put(mine + 2 * nx + x, o.x, tag);
+        ll_put(mine + 2 * nx + x + nx, o.y, tag);
+      }
+    }
+    // rows 2..R-1 in place; `prev` = the old row above
+    double2 prev = cur[1];
+#pragma unroll
+    for (int r = 2; r < RR; ++r) {
+      double2 res;
+      const double2 o = pair(prev, cur[r], cur[r + 1], r, b, res);
+      if (rec) acc(res, mx, ss);
+      prev = cur[r];
+      cur[r] = o;
+    }
+    cur[1] = n1;
+    if (RR > 1) cur[RR] = nR;
+    if (rec) {
+      rs_block_reduce(mx, ss, k.part + ((size_t)entry * G + c) * 2);
+      ++entry;
+    }
+    // halo rows of φ^{s+1}
+    if (k.act && (k.top_x || k.bot_x)) {
+      const double* fu = k.pub + ((size_t)(slot * G + k.up) * 2 + 1) * 2 * nx;  // up's last row
+      const double* fd = k.pub + ((size_t)(slot * G + k.dn) * 2) * 2 * nx;      // dn's first row
+      double v[4];
+      if (k.top_x && k.bot_x) {
+        const double* const e[4] = {fu + x, fu + x + nx, fd + x, fd + x + nx};
+        ll_get<4>(e, tag, v);
+      } else {
+        const double* f = k.top_x ? fu : fd;
+        const double* const e[4] = {f + x, f + x + nx, f, f};
+        ll_get<2>(e, tag, v);
+        v[2] = v[0];
+        v[3] = v[1];
+      }
+      if (k.top_x) cur[0] = make_double2(v[0], v[1]);
+      if (k.bot_x) cur[RR + 1] = make_double2(v[2], v[3]);
+    }
+    if (k.refl_top) cur[0] = make_double2(-cur[1].x, -cur[1].y);
+    if (k.refl_bot) cur[RR + 1] = make_double2(-cur[RR].x, -cur[RR].y);
+    put_edges(b ^ 1);
+    __syncthreads();
+  }
+  const int bN = p.nsweeps & 1;  // the edge buffer of φ^N
+  if (p.final_norm) {            // rows 1..R in order (k_resident's final pass)
+    unsigned long long mx = 0ull;
+    double ss = 0.0;
+#pragma unroll
+    for (int r = 1; r <= RR; ++r) {
+      double2 res;
+      pair(cur[r - 1], cur[r], cur[r + 1], r, bN, res);
+      acc(res, mx, ss);
+    }
+    rs_block_reduce(mx, ss, k.part + ((size_t)entry * G + c) * 2);
+    ++entry;
+  }
+  __threadfence();
+  grid.sync();
+  for (int e = c; e < entry; e += G) {
+    unsigned long long m = 0ull;
+    double t = 0.0;
+    for (int i = tid; i < G; i += RS_THREADS) {
+      m = umax64(m, (unsigned long long)__double_as_longlong(__ldcg(k.part + ((size_t)e * G + i) * 2)));
+      t = t + __ldcg(k.part + ((size_t)e * G + i) * 2 + 1);
+    }
+    double out[2];
+    rs_block_reduce(m, t, out);
+    if (tid == 0) {
+      p.d_max[e] = out[0];
+      p.d_sum[e] = out[1];
+    }
+  }
+  // φ^N with its ghost columns; the face CTAs also write their halo row (the
+  // domain's ghost row)
+  const bool first = x == 0, last = x == nx - 2;
+#pragma unroll
+  for (int r = 0; r < RR + 2; ++r) {
+    if ((r == 0 && c != 0) || (r == RR + 1 && c != G - 1)) continue;
+    const double w = west(cur[r], r, bN), e = east(cur[r], r, bN);
+    if (k.act) {
+      double* dst = p.phi_out + (int64_t)(y0 - 1 + r) * p.ld_out + x;
+      dst[0] = cur[r].x;
+      dst[1] = cur[r].y;
+      if (first) dst[-1] = w;
+      if (last) dst[2] = e;
+    }
+  }
+}
+
+template <int ST>
+__global__ void __launch_bounds__(RS_THREADS, 1) k_resident_reg(const ResidentLaunch p) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double sm[];
+  constexpr int NWP = RS_THREADS / 32, RE = RR_RM + 2, BS = NWP * RE;
+  const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nx = p.nx, np = nx / 2;
+  const int y0 = (int)((int64_t)c * p.ny / G), y1 = (int)((int64_t)(c + 1) * p.ny / G), R = y1 - y0;
+  RrCtx k;
+  double* F = sm;
+  k.F = F;
+  k.eL = F + (size_t)p.rmax * nx;
+  k.eR = k.eL + 2 * BS;
+  double* gW = k.eR + 2 * BS;  // [RE] fixed ghost column -1 (also the dummy broadcast address)
+  double* gE = gW + RE;        // [RE] fixed ghost column nx
+  k.pub = p.ws + ((G + 1) & ~1);                      // as k_resident (entries q and nx/2 + q)
+  k.part = k.pub + (size_t)2 * G * 2 * 2 * nx;        // [entry][cta][max, sum]
+  k.G = G;
+  k.c = c;
+  k.nx = nx;
+  k.warp = warp;
+  k.up = c > 0 ? c - 1 : G - 1;
+  k.dn = c < G - 1 ? c + 1 : 0;
+  k.top_x = c > 0 || p.ymode[0] == GH_WRAP;
+  k.bot_x = c < G - 1 || p.ymode[1] == GH_WRAP;
+  k.refl_top = !k.top_x && p.ymode[0] == GH_REFLECT;
+  k.refl_bot = !k.bot_x && p.ymode[1] == GH_REFLECT;
+  const int q = tid;
+  k.act = q < np;
+  k.x = 2 * q;
+  k.xs = k.act ? k.x : 0;
+  const bool first = q == 0, last = q == np - 1;
+  const int wlast = (np - 1) >> 5;  // the warp holding column nx-1
+  k.st_l = lane == 0;
+  k.st_r = (lane == 31 && k.act) || last;
+  // west candidate of column 2q
+  k.wp = gW;
+  k.wbs = 0;
+  k.wld = k.wneg = false;
+  if (first) {
+    if (p.xmode[0] == GH_WRAP) {
+      k.wp = k.eR + wlast * RE;
+      k.wbs = BS;
+      k.wld = true;
+    } else if (p.xmode[0] == GH_REFLECT) {
+      k.wneg = true;
+    } else {
+      k.wld = true;  // gW
+    }
+  } else if (lane == 0) {
+    k.wp = k.eR + (warp - 1) * RE;
+    k.wbs = BS;
+    k.wld = true;
+  }
+  // east candidate of column 2q+1
+  k.ep = gW;
+  k.ebs = 0;
+  k.eld = k.eneg = false;
+  if (last) {
+    if (p.xmode[1] == GH_WRAP) {
+      k.ep = k.eL;
+      k.ebs = BS;
+      k.eld = true;
+    } else if (p.xmode[1] == GH_REFLECT) {
+      k.eneg = true;
+    } else {
+      k.ep = gE;
+      k.eld = true;
+    }
+  } else if (lane == 31 && k.act) {
+    k.ep = k.eL + (warp + 1) * RE;
+    k.ebs = BS;
+    k.eld = true;
+  }
+  for (int r = 0; r < R; ++r)
+    for (int i = tid; i < nx; i += RS_THREADS) F[(size_t)r * nx + i] = p.rhs[(int64_t)(y0 + r) * p.ld_rhs + i];
+  if (tid < RE) {
+    gW[tid] = tid < R + 2 ? p.phi_in[(int64_t)(y0 - 1 + tid) * p.ld_in - 1] : 0.0;
+    gE[tid] = tid < R + 2 ? p.phi_in[(int64_t)(y0 - 1 + tid) * p.ld_in + nx] : 0.0;
+  }
+  for (int sl = 0; sl < 2; ++sl)
+    for (int i = tid; i < 2 * 2 * nx; i += RS_THREADS) k.pub[(size_t)(sl * G + c) * 2 * 2 * nx + i] = 0.0;
+  __syncthreads();
+  switch (R) {
+    case 1: rr_body<ST, 1>(p, k, grid); break;
+    case 2: rr_body<ST, 2>(p, k, grid); break;
+    case 3: rr_body<ST, 3>(p, k, grid); break;
+    case 4: rr_body<ST, 4>(p, k, grid); break;
+    case 5: rr_body<ST, 5>(p, k, grid); break;
+    case 6: rr_body<ST, 6>(p, k, grid); break;
+    default: rr_body<ST, 7>(p, k, grid); break;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -691,7 +1133,30 @@ static cudaError_t rs_attr(F* fn, size_t smem, size_t& set) {
   return e;
 }
 
-px_status launch_resident(int stencil, const ResidentLaunch& r, int grid, size_t smem, cudaStream_t s) {
+// PROTOX_RESIDENT_UNROLL=0 selects the rolled column walk (A/B)
+static int rs_unroll_env() {
+  static int u = -1;
+  if (u < 0) {
+    const char* e = getenv("PROTOX_RESIDENT_UNROLL");
+    u = (e && e[0] == '0') ? 0 : 1;
+  }
+  return u;
+}
+
+// PROTOX_RESIDENT_REG=0 selects the shared-memory row walk (k_resident) where
+// the register-resident kernel would run (A/B)
+static int rs_reg_env() {
+  static int u = -1;
+  if (u < 0) {
+    const char* e = getenv("PROTOX_RESIDENT_REG");
+    u = (e && e[0] == '0') ? 0 : 1;
+  }
+  return u;
+}
+
+px_status launch_resident(int stencil, const ResidentLaunch& r_in, int grid, size_t smem, cudaStream_t s) {
+  ResidentLaunch r = r_in;
+  r.unroll = rs_unroll_env();
   int g2 = 0, rm = 0;
   size_t sm2 = 0;
   const int K = resident_k(r.nx, r.ny, &g2, &rm, &sm2);
@@ -700,7 +1165,20 @@ px_status launch_resident(int stencil, const ResidentLaunch& r, int grid, size_t
   const int k = stencil ? 1 : 0;
   void* fn = nullptr;
   cudaError_t e = cudaSuccess;
-  switch (k * 4 + K) {
+  const bool reg = K == 1 && rs_reg_env() && r.rmax <= RR_RM && r.nx / 2 <= RS_THREADS;
+  if (reg) {
+    // ρ rows + edge arrays + fixed ghost columns (k_resident_reg's shared layout)
+    constexpr int RE = RR_RM + 2;
+    smem = ((size_t)r.rmax * r.nx + 2 * 2 * (RS_THREADS / 32) * RE + 2 * RE) * sizeof(double);
+    static size_t reg_set[2] = {};
+    if (k) {
+      e = rs_attr(k_resident_reg<1>, smem, reg_set[1]);
+      fn = (void*)k_resident_reg<1>;
+    } else {
+      e = rs_attr(k_resident_reg<0>, smem, reg_set[0]);
+      fn = (void*)k_resident_reg<0>;
+    }
+  } else switch (k * 4 + K) {
     case 1: e = rs_attr(k_resident<0>, smem, attr_set[0][0]); fn = (void*)k_resident<0>; break;
     case 2: e = rs_attr(k_resident_tb<0, 2>, smem, attr_set[0][1]); fn = (void*)k_resident_tb<0, 2>; break;
     case 3: e = rs_attr(k_resident_tb<0, 3>, smem, attr_set[0][2]); fn = (void*)k_resident_tb<0, 3>; break;
@@ -720,10 +1198,10 @@ px_status launch_resident(int stencil, const ResidentLaunch& r, int grid, size_t
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  void* args[] = {const_cast<ResidentLaunch*>(&r)};
+  void* args[] = {&r};
   e = cudaLaunchKernelExC(&cfg, fn, args);
   if (e == cudaSuccess) e = cudaGetLastError();
-  note_kernel(K == 1 ? "k_resident" : "k_resident_tb");
+  note_kernel(reg ? "k_resident_reg" : (K == 1 ? "k_resident" : "k_resident_tb"));
   count_launches(1);
   return cuda_check(e, "resident solve kernel launch");
 }

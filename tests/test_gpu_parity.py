@@ -204,13 +204,16 @@ def test_solve_whole_box_shapes(shape, bc, st):
         _check_norms(norms, rn)
 
 
-@pytest.mark.parametrize("shape", [(130, 400), (1022, 149), (4, 5000), (1024, 101), (2048, 9)])
+@pytest.mark.parametrize("shape", [(130, 400), (1022, 149), (4, 5000), (1024, 101), (2048, 9), (1100, 900),
+                                   (66, 1036)])
 @pytest.mark.parametrize("bc", [P.PX_BC_PERIODIC, P.PX_BC_DIRICHLET_CC, P.PX_BC_FIXED_GHOSTS])
 @pytest.mark.parametrize("st", [P.PX_LAPLACE_5PT, P.PX_MEHRSTELLEN_9PT])
 def test_solve_resident_shapes(shape, bc, st):
     """Shared-memory-resident solve (k_resident, LL row mailbox): uneven rows
-    per CTA, one row per CTA, 34 rows x 2 column pairs per CTA, an odd CTA
-    count (101, 9: the mailbox alignment), 9 CTAs of one row; even and odd sweep
+    per CTA, one row per CTA, 34 rows x 2 column pairs per CTA (the rolled
+    column walk), an odd CTA count (101, 9: the mailbox alignment), 9 CTAs of
+    one row, 6-7 rows with more column pairs than threads (1100 x 900) and
+    exactly 7 rows per CTA (the unrolled walk's limit); even and odd sweep
     counts; norms every 4."""
     n0, n1 = shape
     h = 1.0 / 1024
