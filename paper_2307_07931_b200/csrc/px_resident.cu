@@ -197,9 +197,9 @@ __device__ __forceinline__ double ll_val(const LL& v) {
 }
 // the n (<= 4) entries e[i], all loads in flight together; re-poll until
 // every tag matches
-template <int n>
-__device__ __forceinline__ void ll_get(const double* const (&e)[4], uint32_t tag, double (&out)[4]) {
-  LL v[4];
+template <int n, int M>
+__device__ __forceinline__ void ll_get(const double* const (&e)[M], uint32_t tag, double (&out)[M]) {
+  LL v[M];
 #pragma unroll
   for (int i = 0; i < n; ++i) v[i] = ll_load(e[i]);
 #if PX_RS_DIAG == 1
@@ -574,8 +574,10 @@ struct RrCtx {
   const double* wp;                // west candidate (buffer 0, row 0); dummy broadcast if none
   const double* ep;                // east candidate
   int wbs, ebs;                    // buffer stride of wp / ep (0: not double-buffered)
-  bool wld, wneg, eld, eneg;       // take the shared candidate / the negated own cell
+  bool wld, eld;                   // take the shared candidate instead of the shuffle
   bool st_l, st_r;                 // this lane stores the warp's left / right edge
+  double *gW, *gE;                 // [2][RE] ghost columns -1 / nx: fixed (both buffers), or the
+  bool st_gw, st_ge;               // odd reflections the first / last pair stores with its edges
   int warp, x, xs, nx, G, c, up, dn;
   bool act, top_x, bot_x, refl_top, refl_bot;
   double *pub, *part;
@@ -599,21 +601,25 @@ __device__ __forceinline__ void rr_body(const ResidentLaunch& p, const RrCtx& k,
     for (int r = 0; r < RR + 2; ++r) {
       if (k.st_l) k.eL[b * BS + k.warp * RE + r] = cur[r].x;
       if (k.st_r) k.eR[b * BS + k.warp * RE + r] = cur[r].y;
+      if (k.st_gw) k.gW[b * RE + r] = -cur[r].x;
+      if (k.st_ge) k.gE[b * RE + r] = -cur[r].y;
     }
   };
   put_edges(0);
   __threadfence();
   grid.sync();
 
+  // every lane loads (a broadcast dummy where it has no edge) and selects:
+  // no divergence around the shuffles
   auto west = [&](double2 v, int r, int b) -> double {
     const double sh = __shfl_up_sync(FULL_MASK, v.y, 1);
     const double t = k.wp[b * k.wbs + r];
-    return k.wld ? t : (k.wneg ? -v.x : sh);
+    return k.wld ? t : sh;
   };
   auto east = [&](double2 v, int r, int b) -> double {
     const double sh = __shfl_down_sync(FULL_MASK, v.x, 1);
     const double t = k.ep[b * k.ebs + r];
-    return k.eld ? t : (k.eneg ? -v.y : sh);
+    return k.eld ? t : sh;
   };
   // one pair of row r from rows S (r-1), C (r), N (r+1) of buffer b's iterate;
   // res = the residuals (0 on lanes past the last pair)
@@ -643,10 +649,11 @@ __device__ __forceinline__ void rr_body(const ResidentLaunch& p, const RrCtx& k,
     ss = fma(res.y, res.y, ss);
   };
 
-  int entry = 0;
+  int entry = 0, phase = 0;  // phase = s mod every (no division per sweep)
   for (int s = 0; s < p.nsweeps; ++s) {
     const int b = s & 1;
-    const bool rec = p.every > 0 && s % p.every == 0;
+    const bool rec = p.every > 0 && phase == 0;
+    if (++phase == p.every) phase = 0;
     const uint32_t tag = (uint32_t)s + 1u;
     const int slot = (s + 1) & 1;
     double* mine = k.pub + (size_t)(slot * G + c) * 2 * 2 * nx;
@@ -756,23 +763,24 @@ __device__ __forceinline__ void rr_body(const ResidentLaunch& p, const RrCtx& k,
   }
 }
 
-template <int ST>
-__global__ void __launch_bounds__(RS_THREADS, 1) k_resident_reg(const ResidentLaunch p) {
-  cg::grid_group grid = cg::this_grid();
-  extern __shared__ __align__(16) double sm[];
-  constexpr int NWP = RS_THREADS / 32, RE = RR_RM + 2, BS = NWP * RE;
+// Shared layout and per-thread context of the register-resident kernels
+// (H halo rows per side, RE row slots): ρ rows | eL[2][NWP][RE] |
+// eR[2][NWP][RE] | gW[2][RE] | gE[2][RE]; the LL mailbox (H rows per side)
+// and the norm partials in the workspace.
+template <int RE, int H>
+__device__ __forceinline__ void rr_setup(const ResidentLaunch& p, RrCtx& k, double* sm) {
+  constexpr int NWP = RS_THREADS / 32, BS = NWP * RE;
   const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nx = p.nx, np = nx / 2;
   const int y0 = (int)((int64_t)c * p.ny / G), y1 = (int)((int64_t)(c + 1) * p.ny / G), R = y1 - y0;
-  RrCtx k;
   double* F = sm;
   k.F = F;
   k.eL = F + (size_t)p.rmax * nx;
   k.eR = k.eL + 2 * BS;
-  double* gW = k.eR + 2 * BS;  // [RE] fixed ghost column -1 (also the dummy broadcast address)
-  double* gE = gW + RE;        // [RE] fixed ghost column nx
-  k.pub = p.ws + ((G + 1) & ~1);                      // as k_resident (entries q and nx/2 + q)
-  k.part = k.pub + (size_t)2 * G * 2 * 2 * nx;        // [entry][cta][max, sum]
+  k.gW = k.eR + 2 * BS;
+  k.gE = k.gW + 2 * RE;
+  k.pub = p.ws + ((G + 1) & ~1);                    // [slot][cta][side][H rows][nx entries of 2 doubles]
+  k.part = k.pub + (size_t)2 * G * 2 * H * 2 * nx;  // [entry][cta][max, sum]
   k.G = G;
   k.c = c;
   k.nx = nx;
@@ -791,40 +799,29 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resident_reg(const ResidentLa
   const int wlast = (np - 1) >> 5;  // the warp holding column nx-1
   k.st_l = lane == 0;
   k.st_r = (lane == 31 && k.act) || last;
-  // west candidate of column 2q
-  k.wp = gW;
+  k.st_gw = first && p.xmode[0] == GH_REFLECT;
+  k.st_ge = last && p.xmode[1] == GH_REFLECT;
+  // west candidate of column 2q: the previous warp's right edge, or at the
+  // domain face the last warp's right edge (periodic) / the ghost column
+  k.wp = k.gW;
   k.wbs = 0;
-  k.wld = k.wneg = false;
+  k.wld = false;
   if (first) {
-    if (p.xmode[0] == GH_WRAP) {
-      k.wp = k.eR + wlast * RE;
-      k.wbs = BS;
-      k.wld = true;
-    } else if (p.xmode[0] == GH_REFLECT) {
-      k.wneg = true;
-    } else {
-      k.wld = true;  // gW
-    }
+    k.wld = true;
+    k.wbs = p.xmode[0] == GH_WRAP ? BS : RE;
+    if (p.xmode[0] == GH_WRAP) k.wp = k.eR + wlast * RE;
   } else if (lane == 0) {
     k.wp = k.eR + (warp - 1) * RE;
     k.wbs = BS;
     k.wld = true;
   }
-  // east candidate of column 2q+1
-  k.ep = gW;
+  k.ep = k.gE;
   k.ebs = 0;
-  k.eld = k.eneg = false;
+  k.eld = false;
   if (last) {
-    if (p.xmode[1] == GH_WRAP) {
-      k.ep = k.eL;
-      k.ebs = BS;
-      k.eld = true;
-    } else if (p.xmode[1] == GH_REFLECT) {
-      k.eneg = true;
-    } else {
-      k.ep = gE;
-      k.eld = true;
-    }
+    k.eld = true;
+    k.ebs = p.xmode[1] == GH_WRAP ? BS : RE;
+    if (p.xmode[1] == GH_WRAP) k.ep = k.eL;
   } else if (lane == 31 && k.act) {
     k.ep = k.eL + (warp + 1) * RE;
     k.ebs = BS;
@@ -832,13 +829,26 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resident_reg(const ResidentLa
   }
   for (int r = 0; r < R; ++r)
     for (int i = tid; i < nx; i += RS_THREADS) F[(size_t)r * nx + i] = p.rhs[(int64_t)(y0 + r) * p.ld_rhs + i];
-  if (tid < RE) {
-    gW[tid] = tid < R + 2 ? p.phi_in[(int64_t)(y0 - 1 + tid) * p.ld_in - 1] : 0.0;
-    gE[tid] = tid < R + 2 ? p.phi_in[(int64_t)(y0 - 1 + tid) * p.ld_in + nx] : 0.0;
+  if (tid < RE) {  // fixed ghost columns of slots 0 .. R+2H-1 (both buffers)
+    const int y = y0 - H + tid;
+    const bool ok = tid < R + 2 * H && y >= -1 && y <= p.ny;
+    const double w = ok ? p.phi_in[(int64_t)y * p.ld_in - 1] : 0.0;
+    const double e = ok ? p.phi_in[(int64_t)y * p.ld_in + nx] : 0.0;
+    k.gW[tid] = k.gW[RE + tid] = w;
+    k.gE[tid] = k.gE[RE + tid] = e;
   }
   for (int sl = 0; sl < 2; ++sl)
-    for (int i = tid; i < 2 * 2 * nx; i += RS_THREADS) k.pub[(size_t)(sl * G + c) * 2 * 2 * nx + i] = 0.0;
+    for (int i = tid; i < 2 * H * 2 * nx; i += RS_THREADS) k.pub[(size_t)(sl * G + c) * 2 * H * 2 * nx + i] = 0.0;
   __syncthreads();
+}
+
+template <int ST>
+__global__ void __launch_bounds__(RS_THREADS, 1) k_resident_reg(const ResidentLaunch p) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double sm[];
+  RrCtx k;
+  rr_setup<RR_RM + 2, 1>(p, k, sm);
+  const int R = (int)((int64_t)(blockIdx.x + 1) * p.ny / gridDim.x) - (int)((int64_t)blockIdx.x * p.ny / gridDim.x);
   switch (R) {
     case 1: rr_body<ST, 1>(p, k, grid); break;
     case 2: rr_body<ST, 2>(p, k, grid); break;
@@ -847,6 +857,289 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resident_reg(const ResidentLa
     case 5: rr_body<ST, 5>(p, k, grid); break;
     case 6: rr_body<ST, 6>(p, k, grid); break;
     default: rr_body<ST, 7>(p, k, grid); break;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_resident_reg2<ST>: k_resident_reg with TEMPORAL BLOCKING of the mailbox
+// handshake -- two sweeps per hop.  A thread keeps its pair of the CTA's rows
+// and of TWO halo rows on each side (rows -1 .. R+2) in registers.  A pass of
+// two levels: level 1 updates rows 0 .. R+1 (the inner halo rows redundantly,
+// exactly as their owners update them; at a non-periodic domain face the
+// ghost row is re-derived instead: odd reflection of row 1 / R, or the fixed
+// φ^0 row), edges, barrier; level 2 updates rows 1 .. R -- rows 1, 2, R-1, R
+// first, published to the L2 mailbox at once (2 rows per side), then the
+// inner rows -- then the neighbours' rows are fetched into the four halo
+// rows, edges, barrier.  The L2 hop (≈ 1.6 µs with its barrier on the B200,
+// scripts/ll_latency.cu) is paid once per two sweeps for two redundant row
+// updates per pass.  An odd sweep count ends with a one-level pass.  φ and
+// the max-norm bit-identical to k_resident; the per-thread Σr² order is row
+// order (within the oracle tolerance, not bitwise equal to k_resident's).
+template <int ST, int RR>
+__device__ __forceinline__ void rr2_body(const ResidentLaunch& p, const RrCtx& k, cg::grid_group& grid) {
+  constexpr int NWP = RS_THREADS / 32, RE = RR_RM + 4, BS = NWP * RE, NI = RR + 4;  // i = row + 1
+  const int tid = threadIdx.x, nx = k.nx, x = k.x, G = k.G, c = k.c;
+  const int y0 = (int)((int64_t)c * p.ny / G);
+  const bool wrap_y = p.ymode[0] == GH_WRAP;
+  double2 cur[NI];
+#pragma unroll
+  for (int i = 0; i < NI; ++i) {
+    cur[i] = make_double2(0.0, 0.0);
+    int y = y0 - 2 + i;
+    if (wrap_y) y = y < -1 ? y + p.ny : (y > p.ny ? y - p.ny : y);
+    if (k.act && y >= -1 && y <= p.ny) {
+      const double* src = p.phi_in + (int64_t)y * p.ld_in + x;
+      cur[i] = make_double2(src[0], src[1]);
+    }
+  }
+  auto put_edges = [&](int b) {
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+      if (k.st_l) k.eL[b * BS + k.warp * RE + i] = cur[i].x;
+      if (k.st_r) k.eR[b * BS + k.warp * RE + i] = cur[i].y;
+      if (k.st_gw) k.gW[b * RE + i] = -cur[i].x;
+      if (k.st_ge) k.gE[b * RE + i] = -cur[i].y;
+    }
+  };
+  put_edges(0);
+  __threadfence();
+  grid.sync();
+
+  auto west = [&](double2 v, int i, int b) -> double {
+    const double sh = __shfl_up_sync(FULL_MASK, v.y, 1);
+    const double t = k.wp[b * k.wbs + i];
+    return k.wld ? t : sh;
+  };
+  auto east = [&](double2 v, int i, int b) -> double {
+    const double sh = __shfl_down_sync(FULL_MASK, v.x, 1);
+    const double t = k.ep[b * k.ebs + i];
+    return k.eld ? t : sh;
+  };
+  // one pair of slot i (row i-1) from slots i-1, i, i+1 of buffer b's level
+  auto pair = [&](double2 S, double2 C, double2 N, int i, int b, double2& res) -> double2 {
+    const double cw = west(C, i, b), ce = east(C, i, b);
+    double sw = 0.0, se = 0.0, nw = 0.0, ne = 0.0;
+    if (ST) {
+      sw = west(S, i - 1, b);
+      se = east(S, i - 1, b);
+      nw = west(N, i + 1, b);
+      ne = east(N, i + 1, b);
+    }
+    const double L0 = rs_taps<ST>(cw, C.y, S.x, N.x, C.x, sw, S.y, nw, N.y);
+    const double L1 = rs_taps<ST>(C.x, ce, S.y, N.y, C.y, S.x, se, N.x, ne);
+    // ρ of row i-1: owned rows from shared memory, halo rows from L2 (wrapped)
+    double2 f;
+    if (i >= 2 && i <= RR + 1) {
+      f = *reinterpret_cast<const double2*>(k.F + (size_t)(i - 2) * nx + k.xs);
+    } else {
+      int y = y0 + i - 2;
+      y = y < 0 ? y + p.ny : (y >= p.ny ? y - p.ny : y);  // only reached for neighbour rows
+      f = __ldg(reinterpret_cast<const double2*>(p.rhs + (int64_t)y * p.ld_rhs + k.xs));
+    }
+    res.x = __dsub_rn(__dmul_rn(p.scale, L0), f.x);
+    res.y = __dsub_rn(__dmul_rn(p.scale, L1), f.y);
+    const double2 o = make_double2(__dadd_rn(C.x, __dmul_rn(p.lambda, res.x)),
+                                   __dadd_rn(C.y, __dmul_rn(p.lambda, res.y)));
+    if (!k.act) res = make_double2(0.0, 0.0);
+    return o;
+  };
+  auto acc = [&](double2 res, unsigned long long& mx, double& ss) {
+    mx = umax64(mx, (unsigned long long)__double_as_longlong(fabs(res.x)));
+    ss = fma(res.x, res.x, ss);
+    mx = umax64(mx, (unsigned long long)__double_as_longlong(fabs(res.y)));
+    ss = fma(res.y, res.y, ss);
+  };
+  const bool top_face = !k.top_x, bot_face = !k.bot_x;  // non-periodic domain faces
+  // ghost row of a domain face after a level: reflection of the first / last
+  // owned row, or (fixed ghosts) untouched
+  auto face_rows = [&]() {
+    if (k.refl_top) cur[1] = make_double2(-cur[2].x, -cur[2].y);
+    if (k.refl_bot) cur[RR + 2] = make_double2(-cur[RR + 1].x, -cur[RR + 1].y);
+  };
+  int entry = 0, cb = 0;
+  int pass = 0;
+  for (int s = 0; s < p.nsweeps; s += 2, ++pass) {
+    const int L = p.nsweeps - s >= 2 ? 2 : 1;
+    const uint32_t tag = (uint32_t)pass + 1u;
+    const int slot = (pass + 1) & 1;
+    double* mine = k.pub + (size_t)(slot * G + c) * 2 * 2 * 2 * nx;  // [side][row][2 nx]
+    // rows 1, 2 (f0, f1) to the first side, rows R-1, R (l0, l1) to the last
+    auto publish = [&](double2 f0, double2 f1, double2 l0, double2 l1) {
+      if (k.act) {
+        if (k.top_x) {
+          ll_put(mine + x, f0.x, tag);
+          ll_put(mine + x + nx, f0.y, tag);
+          ll_put(mine + 2 * nx + x, f1.x, tag);
+          ll_put(mine + 3 * nx + x, f1.y, tag);
+        }
+        if (k.bot_x) {
+          ll_put(mine + 4 * nx + x, l0.x, tag);
+          ll_put(mine + 5 * nx + x, l0.y, tag);
+          ll_put(mine + 6 * nx + x, l1.x, tag);
+          ll_put(mine + 7 * nx + x, l1.y, tag);
+        }
+      }
+    };
+    // ---- level 1: rows 0 .. R+1 (slots 1 .. R+2), in place with a rolling old row
+    {
+      const bool rec = p.every > 0 && s % p.every == 0;
+      unsigned long long mx = 0ull;
+      double ss = 0.0;
+      double2 prev = cur[0];  // the old row above (level 1 updates in place, in row order)
+#pragma unroll
+      for (int i = 1; i <= RR + 2; ++i) {
+        const bool skip = (i == 1 && top_face) || (i == RR + 2 && bot_face);
+        if (!skip) {
+          double2 res;
+          const double2 o = pair(prev, cur[i], cur[i + 1], i, cb, res);
+          if (rec && i >= 2 && i <= RR + 1) acc(res, mx, ss);
+          prev = cur[i];
+          cur[i] = o;
+        } else {
+          prev = cur[i];
+        }
+      }
+      face_rows();
+      if (rec) {
+        rs_block_reduce(mx, ss, k.part + ((size_t)entry * G + c) * 2);
+        ++entry;
+      }
+    }
+    if (L == 2) {
+      put_edges(cb ^ 1);
+      __syncthreads();
+      cb ^= 1;
+      // ---- level 2: rows 1 .. R; rows 1, 2, R-1, R first (published), then 3 .. R-2
+      const bool rec = p.every > 0 && (s + 1) % p.every == 0;
+      unsigned long long mx = 0ull;
+      double ss = 0.0;
+      double2 t[4], rt[4];
+      // boundary slots 2, 3, RR, RR+1 (the distinct ones)
+      constexpr int b0 = 2, b1 = 3, b2 = RR, b3 = RR + 1;
+      constexpr bool u2 = b2 > b1, u3 = b3 > b1 && b3 > b2;
+      t[0] = pair(cur[b0 - 1], cur[b0], cur[b0 + 1], b0, cb, rt[0]);
+      t[1] = pair(cur[b1 - 1], cur[b1], cur[b1 + 1], b1, cb, rt[1]);
+      if (u2) t[2] = pair(cur[b2 - 1], cur[b2], cur[b2 + 1], b2, cb, rt[2]);
+      if (u3) t[3] = pair(cur[b3 - 1], cur[b3], cur[b3 + 1], b3, cb, rt[3]);
+      // the last two rows: slots RR, RR+1
+      const double2 l0 = RR == 2 ? t[0] : (RR == 3 ? t[1] : t[2]);
+      const double2 l1 = RR == 2 ? t[1] : t[3];
+      publish(t[0], t[1], l0, l1);
+      // inner rows 3 .. R-2 (slots 4 .. RR-1) from the old level
+      double2 inner[RR > 4 ? RR - 4 : 1];
+#pragma unroll
+      for (int i = 4; i <= RR - 1; ++i) {
+        double2 res;
+        inner[i - 4] = pair(cur[i - 1], cur[i], cur[i + 1], i, cb, res);
+        if (rec) acc(res, mx, ss);
+      }
+      cur[b0] = t[0];
+      cur[b1] = t[1];
+      if (u2) cur[b2] = t[2];
+      if (u3) cur[b3] = t[3];
+#pragma unroll
+      for (int i = 4; i <= RR - 1; ++i) cur[i] = inner[i - 4];
+      if (rec) {
+        acc(rt[0], mx, ss);
+        acc(rt[1], mx, ss);
+        if (u2) acc(rt[2], mx, ss);
+        if (u3) acc(rt[3], mx, ss);
+        rs_block_reduce(mx, ss, k.part + ((size_t)entry * G + c) * 2);
+        ++entry;
+      }
+    } else {
+      publish(cur[2], cur[3], cur[RR], cur[RR + 1]);
+    }
+    face_rows();
+    // the neighbours' rows of this pass's iterate into the halo slots 0, 1 / R+2, R+3
+    if (k.act && (k.top_x || k.bot_x)) {
+      const double* fu = k.pub + ((size_t)(slot * G + k.up) * 2 + 1) * 2 * 2 * nx;  // up's last rows
+      const double* fd = k.pub + ((size_t)(slot * G + k.dn) * 2) * 2 * 2 * nx;      // dn's first rows
+      if (k.top_x && k.bot_x) {
+        const double* const e[8] = {fu, fu + nx, fu + 2 * nx, fu + 3 * nx, fd, fd + nx, fd + 2 * nx, fd + 3 * nx};
+        const double* const ex[8] = {e[0] + x, e[1] + x, e[2] + x, e[3] + x, e[4] + x, e[5] + x, e[6] + x, e[7] + x};
+        double v[8];
+        ll_get<8>(ex, tag, v);
+        cur[0] = make_double2(v[0], v[1]);
+        cur[1] = make_double2(v[2], v[3]);
+        cur[RR + 2] = make_double2(v[4], v[5]);
+        cur[RR + 3] = make_double2(v[6], v[7]);
+      } else {
+        const double* f = k.top_x ? fu : fd;
+        const double* const ex[4] = {f + x, f + nx + x, f + 2 * nx + x, f + 3 * nx + x};
+        double v[4];
+        ll_get<4>(ex, tag, v);
+        if (k.top_x) {
+          cur[0] = make_double2(v[0], v[1]);
+          cur[1] = make_double2(v[2], v[3]);
+        } else {
+          cur[RR + 2] = make_double2(v[0], v[1]);
+          cur[RR + 3] = make_double2(v[2], v[3]);
+        }
+      }
+    }
+    put_edges(cb ^ 1);
+    __syncthreads();
+    cb ^= 1;
+  }
+  const int bN = cb;  // the edge buffer of φ^N
+  if (p.final_norm) {  // rows 1..R in order (k_resident's final pass)
+    unsigned long long mx = 0ull;
+    double ss = 0.0;
+#pragma unroll
+    for (int i = 2; i <= RR + 1; ++i) {
+      double2 res;
+      pair(cur[i - 1], cur[i], cur[i + 1], i, bN, res);
+      acc(res, mx, ss);
+    }
+    rs_block_reduce(mx, ss, k.part + ((size_t)entry * G + c) * 2);
+    ++entry;
+  }
+  __threadfence();
+  grid.sync();
+  for (int e = c; e < entry; e += G) {
+    unsigned long long m = 0ull;
+    double t = 0.0;
+    for (int i = tid; i < G; i += RS_THREADS) {
+      m = umax64(m, (unsigned long long)__double_as_longlong(__ldcg(k.part + ((size_t)e * G + i) * 2)));
+      t = t + __ldcg(k.part + ((size_t)e * G + i) * 2 + 1);
+    }
+    double out[2];
+    rs_block_reduce(m, t, out);
+    if (tid == 0) {
+      p.d_max[e] = out[0];
+      p.d_sum[e] = out[1];
+    }
+  }
+  const bool first = x == 0, last = x == nx - 2;
+#pragma unroll
+  for (int i = 1; i <= RR + 2; ++i) {
+    if ((i == 1 && c != 0) || (i == RR + 2 && c != G - 1)) continue;
+    const double w = west(cur[i], i, bN), e = east(cur[i], i, bN);
+    if (k.act) {
+      double* dst = p.phi_out + (int64_t)(y0 - 2 + i) * p.ld_out + x;
+      dst[0] = cur[i].x;
+      dst[1] = cur[i].y;
+      if (first) dst[-1] = w;
+      if (last) dst[2] = e;
+    }
+  }
+}
+
+template <int ST>
+__global__ void __launch_bounds__(RS_THREADS, 1) k_resident_reg2(const ResidentLaunch p) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double sm[];
+  RrCtx k;
+  rr_setup<RR_RM + 4, 2>(p, k, sm);
+  const int R = (int)((int64_t)(blockIdx.x + 1) * p.ny / gridDim.x) - (int)((int64_t)blockIdx.x * p.ny / gridDim.x);
+  switch (R) {
+    case 2: rr2_body<ST, 2>(p, k, grid); break;
+    case 3: rr2_body<ST, 3>(p, k, grid); break;
+    case 4: rr2_body<ST, 4>(p, k, grid); break;
+    case 5: rr2_body<ST, 5>(p, k, grid); break;
+    case 6: rr2_body<ST, 6>(p, k, grid); break;
+    default: rr2_body<ST, 7>(p, k, grid); break;
   }
 }
 
@@ -1078,7 +1371,8 @@ static int rs_k_env() {
 size_t resident_ws_doubles(int nx, int grid, int n_entries) {
   // flags (k_resident_tb) or padding, the row mailboxes (k_resident: 2 slots x 2 rows x nx LL entries
   // of 2 doubles; k_resident_tb: 2 slots x 2K rows x nx), the norm partials
-  return (size_t)grid + 1 + (size_t)2 * grid * 2 * (RS_KMAX > 2 ? RS_KMAX : 2) * nx +
+  // k_resident_reg2: 2 slots x 2 sides x 2 rows x nx LL entries of 2 doubles
+  return (size_t)grid + 1 + (size_t)2 * grid * 2 * (RS_KMAX > 4 ? RS_KMAX : 4) * nx +
          (size_t)(n_entries > 0 ? n_entries : 1) * grid * 2;
 }
 
@@ -1143,13 +1437,14 @@ static int rs_unroll_env() {
   return u;
 }
 
-// PROTOX_RESIDENT_REG=0 selects the shared-memory row walk (k_resident) where
-// the register-resident kernel would run (A/B)
+// PROTOX_RESIDENT_REG: 0 = the shared-memory row walk (k_resident), 1 = the
+// register-resident kernel, 2 = its two-sweeps-per-hop variant (A/B)
 static int rs_reg_env() {
   static int u = -1;
   if (u < 0) {
     const char* e = getenv("PROTOX_RESIDENT_REG");
-    u = (e && e[0] == '0') ? 0 : 1;
+    u = e ? atoi(e) : 1;
+    if (u < 0 || u > 2) u = 1;
   }
   return u;
 }
@@ -1165,11 +1460,24 @@ px_status launch_resident(int stencil, const ResidentLaunch& r_in, int grid, siz
   const int k = stencil ? 1 : 0;
   void* fn = nullptr;
   cudaError_t e = cudaSuccess;
-  const bool reg = K == 1 && rs_reg_env() && r.rmax <= RR_RM && r.nx / 2 <= RS_THREADS;
-  if (reg) {
+  const bool reg = K == 1 && rs_reg_env() > 0 && r.rmax <= RR_RM && r.nx / 2 <= RS_THREADS;
+  // two sweeps per mailbox hop: every CTA needs two own rows to publish
+  const bool reg2 = reg && rs_reg_env() == 2 && r.ny / grid >= 2;
+  if (reg2) {
+    constexpr int RE = RR_RM + 4;
+    smem = ((size_t)r.rmax * r.nx + 2 * 2 * (RS_THREADS / 32) * RE + 4 * RE) * sizeof(double);
+    static size_t reg2_set[2] = {};
+    if (k) {
+      e = rs_attr(k_resident_reg2<1>, smem, reg2_set[1]);
+      fn = (void*)k_resident_reg2<1>;
+    } else {
+      e = rs_attr(k_resident_reg2<0>, smem, reg2_set[0]);
+      fn = (void*)k_resident_reg2<0>;
+    }
+  } else if (reg) {
     // ρ rows + edge arrays + fixed ghost columns (k_resident_reg's shared layout)
     constexpr int RE = RR_RM + 2;
-    smem = ((size_t)r.rmax * r.nx + 2 * 2 * (RS_THREADS / 32) * RE + 2 * RE) * sizeof(double);
+    smem = ((size_t)r.rmax * r.nx + 2 * 2 * (RS_THREADS / 32) * RE + 4 * RE) * sizeof(double);
     static size_t reg_set[2] = {};
     if (k) {
       e = rs_attr(k_resident_reg<1>, smem, reg_set[1]);
@@ -1201,7 +1509,7 @@ px_status launch_resident(int stencil, const ResidentLaunch& r_in, int grid, siz
   void* args[] = {&r};
   e = cudaLaunchKernelExC(&cfg, fn, args);
   if (e == cudaSuccess) e = cudaGetLastError();
-  note_kernel(reg ? "k_resident_reg" : (K == 1 ? "k_resident" : "k_resident_tb"));
+  note_kernel(reg2 ? "k_resident_reg2" : (reg ? "k_resident_reg" : (K == 1 ? "k_resident" : "k_resident_tb")));
   count_launches(1);
   return cuda_check(e, "resident solve kernel launch");
 }

@@ -205,7 +205,7 @@ def test_solve_whole_box_shapes(shape, bc, st):
 
 
 @pytest.mark.parametrize("shape", [(130, 400), (1022, 149), (4, 5000), (1024, 101), (2048, 9), (1100, 900),
-                                   (66, 1036)])
+                                   (66, 1036), (1000, 700), (2, 600)])
 @pytest.mark.parametrize("bc", [P.PX_BC_PERIODIC, P.PX_BC_DIRICHLET_CC, P.PX_BC_FIXED_GHOSTS])
 @pytest.mark.parametrize("st", [P.PX_LAPLACE_5PT, P.PX_MEHRSTELLEN_9PT])
 def test_solve_resident_shapes(shape, bc, st):
@@ -213,8 +213,10 @@ def test_solve_resident_shapes(shape, bc, st):
     per CTA, one row per CTA, 34 rows x 2 column pairs per CTA (the rolled
     column walk), an odd CTA count (101, 9: the mailbox alignment), 9 CTAs of
     one row, 6-7 rows with more column pairs than threads (1100 x 900) and
-    exactly 7 rows per CTA (the unrolled walk's limit); even and odd sweep
-    counts; norms every 4."""
+    exactly 7 rows per CTA (the unrolled walk's limit); the register-resident
+    kernel (k_resident_reg: nx/2 <= 512 pairs, <= 7 rows) with a partial last
+    warp (1000 x 700) and a single pair (2 x 600); even and odd sweep counts
+    (k_resident_reg2 ends an odd count with a one-level pass); norms every 4."""
     n0, n1 = shape
     h = 1.0 / 1024
     lam = h * h / 8 if st == 0 else 3 * h * h / 16
@@ -801,16 +803,20 @@ def test_separate_ghost_fill_subprocess():
 
 
 @pytest.mark.gpu
-def test_resident_temporal_blocking_variant_subprocess():
-    """The temporally blocked resident solve (A/B option PROTOX_RESIDENT_K=2,3,
-    read once per process) stays bit-identical: the resident-path tests re-run
-    in child processes."""
+@pytest.mark.parametrize("var", [("PROTOX_RESIDENT_K", "2"), ("PROTOX_RESIDENT_K", "3"),
+                                 ("PROTOX_RESIDENT_REG", "0"), ("PROTOX_RESIDENT_REG", "2")])
+def test_resident_temporal_blocking_variant_subprocess(var):
+    """The resident-solve variants (read once per process) stay bit-identical:
+    the shared-memory temporally blocked kernel (PROTOX_RESIDENT_K=2,3), the
+    shared-memory row walk (PROTOX_RESIDENT_REG=0) and the register kernel with
+    two sweeps per mailbox hop (PROTOX_RESIDENT_REG=2); the resident-path
+    tests re-run in child processes."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    for k in ("2", "3"):
-        env = dict(os.environ, PROTOX_RESIDENT_K=k)
+    for k in (var[1],):
+        env = dict(os.environ, **{var[0]: k})
         r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-m", "gpu",
                             "tests/test_gpu_parity.py", "-k", "resident_shapes or config2_full"],
                            cwd=root, env=env, capture_output=True, text=True, timeout=900)
