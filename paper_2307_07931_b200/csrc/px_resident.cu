@@ -32,6 +32,7 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdint>
 #include <cstdlib>
 
@@ -171,6 +172,9 @@ __device__ __forceinline__ void ll_put(double* e, double v, uint32_t tag) {
                : "memory");
 #endif
 }
+#ifndef PX_RR_PROF
+#define PX_RR_PROF 0  // per-phase clock64 totals of k_resident_reg (printf; scripts/build_variant.py)
+#endif
 #ifndef PX_RS_DIAG
 #define PX_RS_DIAG 0  // A/B diagnostics only (scripts/build_variant.py): 1 no tag wait, 2 no row compute
 #endif
@@ -195,6 +199,57 @@ __device__ __forceinline__ bool ll_ok(const LL& v, uint32_t tag) {
 __device__ __forceinline__ double ll_val(const LL& v) {
   return __longlong_as_double((long long)((v.hi << 32) | (v.lo & 0xffffffffull)));
 }
+// A column pair as ONE 32-B LL entry (sm_100 v4.u64 access; each u64 element
+// = tag << 32 | one half of a double, single-copy atomic as above): one store
+// and one poll per pair and row instead of two.
+__device__ __forceinline__ void ll_put2(double* e, double2 v, uint32_t tag) {
+  const unsigned long long a = (unsigned long long)__double_as_longlong(v.x);
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v.y);
+  const unsigned long long t = (unsigned long long)tag << 32;
+  asm volatile("st.relaxed.gpu.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(e), "l"(t | (a & 0xffffffffull)),
+               "l"(t | (a >> 32)), "l"(t | (b & 0xffffffffull)), "l"(t | (b >> 32))
+               : "memory");
+}
+struct LL2 {
+  unsigned long long w[4];
+};
+__device__ __forceinline__ LL2 ll_load2(const double* e) {
+  LL2 v;
+  asm volatile("ld.relaxed.gpu.global.v4.u64 {%0, %1, %2, %3}, [%4];"
+               : "=l"(v.w[0]), "=l"(v.w[1]), "=l"(v.w[2]), "=l"(v.w[3])
+               : "l"(e)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ bool ll2_ok(const LL2& v, uint32_t tag) {
+  return (uint32_t)(v.w[0] >> 32) == tag && (uint32_t)(v.w[1] >> 32) == tag && (uint32_t)(v.w[2] >> 32) == tag &&
+         (uint32_t)(v.w[3] >> 32) == tag;
+}
+__device__ __forceinline__ double2 ll2_val(const LL2& v) {
+  return make_double2(__longlong_as_double((long long)((v.w[1] << 32) | (v.w[0] & 0xffffffffull))),
+                      __longlong_as_double((long long)((v.w[3] << 32) | (v.w[2] & 0xffffffffull))));
+}
+// the n (<= 2) pair entries e[i], loads in flight together, re-polled until
+// every tag matches
+template <int n>
+__device__ __forceinline__ void ll_get2(const double* const (&e)[2], uint32_t tag, double2 (&out)[2]) {
+  LL2 v[2];
+#pragma unroll
+  for (int i = 0; i < n; ++i) v[i] = ll_load2(e[i]);
+  for (;;) {
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < n; ++i) ok = ok && ll2_ok(v[i], tag);
+    if (ok) break;
+    if (LL_BACKOFF_NS) __nanosleep(LL_BACKOFF_NS);
+#pragma unroll
+    for (int i = 0; i < n; ++i)
+      if (!ll2_ok(v[i], tag)) v[i] = ll_load2(e[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < n; ++i) out[i] = ll2_val(v[i]);
+}
+
 // the n (<= 4) entries e[i], all loads in flight together; re-poll until
 // every tag matches
 template <int n, int M>
@@ -582,7 +637,7 @@ struct RrCtx {
   bool act, top_x, bot_x, refl_top, refl_bot;
   double *pub, *part;
 };
-template <int ST, int RR>
+template <int ST, int RR, bool P2>
 __device__ __forceinline__ void rr_body(const ResidentLaunch& p, const RrCtx& k, cg::grid_group& grid) {
   constexpr int NWP = RS_THREADS / 32, RE = RR_RM + 2, BS = NWP * RE;
   const int tid = threadIdx.x, nx = k.nx, x = k.x, G = k.G, c = k.c;
@@ -632,13 +687,23 @@ __device__ __forceinline__ void rr_body(const ResidentLaunch& p, const RrCtx& k,
       nw = west(N, r + 1, b);
       ne = east(N, r + 1, b);
     }
-    const double L0 = rs_taps<ST>(cw, C.y, S.x, N.x, C.x, sw, S.y, nw, N.y);
-    const double L1 = rs_taps<ST>(C.x, ce, S.y, N.y, C.y, S.x, se, N.x, ne);
     const double2 f = *reinterpret_cast<const double2*>(k.F + (size_t)(r - 1) * nx + k.xs);
-    res.x = __dsub_rn(__dmul_rn(p.scale, L0), f.x);
-    res.y = __dsub_rn(__dmul_rn(p.scale, L1), f.y);
-    const double2 o = make_double2(__dadd_rn(C.x, __dmul_rn(p.lambda, res.x)),
-                                   __dadd_rn(C.y, __dmul_rn(p.lambda, res.y)));
+    double2 o;
+    if (P2) {
+      // power-of-two h and λ, 5-point: -4c, scale·L and λr are exact, so
+      // each fused multiply-add rounds exactly like the separate ops
+      const double L0 = fma(-4.0, C.x, __dadd_rn(__dadd_rn(__dadd_rn(cw, C.y), S.x), N.x));
+      const double L1 = fma(-4.0, C.y, __dadd_rn(__dadd_rn(__dadd_rn(C.x, ce), S.y), N.y));
+      res.x = fma(p.scale, L0, -f.x);
+      res.y = fma(p.scale, L1, -f.y);
+      o = make_double2(fma(p.lambda, res.x, C.x), fma(p.lambda, res.y, C.y));
+    } else {
+      const double L0 = rs_taps<ST>(cw, C.y, S.x, N.x, C.x, sw, S.y, nw, N.y);
+      const double L1 = rs_taps<ST>(C.x, ce, S.y, N.y, C.y, S.x, se, N.x, ne);
+      res.x = __dsub_rn(__dmul_rn(p.scale, L0), f.x);
+      res.y = __dsub_rn(__dmul_rn(p.scale, L1), f.y);
+      o = make_double2(__dadd_rn(C.x, __dmul_rn(p.lambda, res.x)), __dadd_rn(C.y, __dmul_rn(p.lambda, res.y)));
+    }
     if (!k.act) res = make_double2(0.0, 0.0);
     return o;
   };
@@ -650,6 +715,18 @@ __device__ __forceinline__ void rr_body(const ResidentLaunch& p, const RrCtx& k,
   };
 
   int entry = 0, phase = 0;  // phase = s mod every (no division per sweep)
+#if PX_RR_PROF
+  long long tp[7] = {0, 0, 0, 0, 0, 0, 0};
+  long long tq = clock64();
+#define RR_T(i)                  \
+  {                              \
+    const long long t_ = clock64(); \
+    tp[i] += t_ - tq;            \
+    tq = t_;                     \
+  }
+#else
+#define RR_T(i)
+#endif
   for (int s = 0; s < p.nsweeps; ++s) {
     const int b = s & 1;
     const bool rec = p.every > 0 && phase == 0;
@@ -667,17 +744,18 @@ __device__ __forceinline__ void rr_body(const ResidentLaunch& p, const RrCtx& k,
       acc(r1, mx, ss);
       if (RR > 1) acc(rR, mx, ss);
     }
-    if (k.act) {
-      if (k.top_x) {
-        ll_put(mine + x, n1.x, tag);
-        ll_put(mine + x + nx, n1.y, tag);
-      }
-      if (k.bot_x) {
-        const double2 o = RR > 1 ? nR : n1;
-        ll_put(mine + 2 * nx + x, o.x, tag);
-        ll_put(mine + 2 * nx + x + nx, o.y, tag);
-      }
+#if PX_RR_PROF
+    {  // the compute of rows R and 1 complete (consume the results)
+      if (__double_as_longlong(n1.x) == 1 && __double_as_longlong(nR.y) == 3) tp[0] += 1;
     }
+    RR_T(6)
+#endif
+    // pair q of a published row = the 32-B entry at 4q (a warp writes 1 KB contiguously)
+    if (k.act) {
+      if (k.top_x) ll_put2(mine + 2 * x, n1, tag);
+      if (k.bot_x) ll_put2(mine + 2 * nx + 2 * x, RR > 1 ? nR : n1, tag);
+    }
+    RR_T(0)
     // rows 2..R-1 in place; `prev` = the old row above
     double2 prev = cur[1];
 #pragma unroll
@@ -690,33 +768,43 @@ __device__ __forceinline__ void rr_body(const ResidentLaunch& p, const RrCtx& k,
     }
     cur[1] = n1;
     if (RR > 1) cur[RR] = nR;
+    RR_T(1)
     if (rec) {
       rs_block_reduce(mx, ss, k.part + ((size_t)entry * G + c) * 2);
       ++entry;
     }
+    RR_T(2)
     // halo rows of φ^{s+1}
     if (k.act && (k.top_x || k.bot_x)) {
       const double* fu = k.pub + ((size_t)(slot * G + k.up) * 2 + 1) * 2 * nx;  // up's last row
       const double* fd = k.pub + ((size_t)(slot * G + k.dn) * 2) * 2 * nx;      // dn's first row
-      double v[4];
+      double2 v[2];
       if (k.top_x && k.bot_x) {
-        const double* const e[4] = {fu + x, fu + x + nx, fd + x, fd + x + nx};
-        ll_get<4>(e, tag, v);
+        const double* const e[2] = {fu + 2 * x, fd + 2 * x};
+        ll_get2<2>(e, tag, v);
       } else {
-        const double* f = k.top_x ? fu : fd;
-        const double* const e[4] = {f + x, f + x + nx, f, f};
-        ll_get<2>(e, tag, v);
-        v[2] = v[0];
-        v[3] = v[1];
+        const double* const e[2] = {(k.top_x ? fu : fd) + 2 * x, fu};
+        ll_get2<1>(e, tag, v);
+        v[1] = v[0];
       }
-      if (k.top_x) cur[0] = make_double2(v[0], v[1]);
-      if (k.bot_x) cur[RR + 1] = make_double2(v[2], v[3]);
+      if (k.top_x) cur[0] = v[0];
+      if (k.bot_x) cur[RR + 1] = v[1];
     }
+    RR_T(3)
     if (k.refl_top) cur[0] = make_double2(-cur[1].x, -cur[1].y);
     if (k.refl_bot) cur[RR + 1] = make_double2(-cur[RR].x, -cur[RR].y);
     put_edges(b ^ 1);
+    RR_T(4)
     __syncthreads();
+    RR_T(5)
   }
+#if PX_RR_PROF
+  if ((threadIdx.x == 0 || threadIdx.x == 480) && (c == 0 || c == 74))
+    printf("RRPROF cta %d thr %d R %d: rows1R %.0f publish %.0f inner %.0f reduce %.0f poll %.0f edges %.0f bar %.0f cycles/sweep\n", c,
+           threadIdx.x, RR, (double)tp[6] / p.nsweeps, (double)tp[0] / p.nsweeps, (double)tp[1] / p.nsweeps, (double)tp[2] / p.nsweeps,
+           (double)tp[3] / p.nsweeps, (double)tp[4] / p.nsweeps, (double)tp[5] / p.nsweeps);
+#endif
+#undef RR_T
   const int bN = p.nsweeps & 1;  // the edge buffer of φ^N
   if (p.final_norm) {            // rows 1..R in order (k_resident's final pass)
     unsigned long long mx = 0ull;
@@ -779,7 +867,8 @@ __device__ __forceinline__ void rr_setup(const ResidentLaunch& p, RrCtx& k, doub
   k.eR = k.eL + 2 * BS;
   k.gW = k.eR + 2 * BS;
   k.gE = k.gW + 2 * RE;
-  k.pub = p.ws + ((G + 1) & ~1);                    // [slot][cta][side][H rows][nx entries of 2 doubles]
+  // [slot][cta][side][H rows][2 nx doubles], 32-B aligned (the workspace is cudaMalloc'ed)
+  k.pub = p.ws + ((G + 3) & ~3);
   k.part = k.pub + (size_t)2 * G * 2 * H * 2 * nx;  // [entry][cta][max, sum]
   k.G = G;
   k.c = c;
@@ -842,7 +931,7 @@ __device__ __forceinline__ void rr_setup(const ResidentLaunch& p, RrCtx& k, doub
   __syncthreads();
 }
 
-template <int ST>
+template <int ST, bool P2>
 __global__ void __launch_bounds__(RS_THREADS, 1) k_resident_reg(const ResidentLaunch p) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double sm[];
@@ -850,13 +939,13 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resident_reg(const ResidentLa
   rr_setup<RR_RM + 2, 1>(p, k, sm);
   const int R = (int)((int64_t)(blockIdx.x + 1) * p.ny / gridDim.x) - (int)((int64_t)blockIdx.x * p.ny / gridDim.x);
   switch (R) {
-    case 1: rr_body<ST, 1>(p, k, grid); break;
-    case 2: rr_body<ST, 2>(p, k, grid); break;
-    case 3: rr_body<ST, 3>(p, k, grid); break;
-    case 4: rr_body<ST, 4>(p, k, grid); break;
-    case 5: rr_body<ST, 5>(p, k, grid); break;
-    case 6: rr_body<ST, 6>(p, k, grid); break;
-    default: rr_body<ST, 7>(p, k, grid); break;
+    case 1: rr_body<ST, 1, P2>(p, k, grid); break;
+    case 2: rr_body<ST, 2, P2>(p, k, grid); break;
+    case 3: rr_body<ST, 3, P2>(p, k, grid); break;
+    case 4: rr_body<ST, 4, P2>(p, k, grid); break;
+    case 5: rr_body<ST, 5, P2>(p, k, grid); break;
+    case 6: rr_body<ST, 6, P2>(p, k, grid); break;
+    default: rr_body<ST, 7, P2>(p, k, grid); break;
   }
 }
 
@@ -1372,7 +1461,7 @@ size_t resident_ws_doubles(int nx, int grid, int n_entries) {
   // flags (k_resident_tb) or padding, the row mailboxes (k_resident: 2 slots x 2 rows x nx LL entries
   // of 2 doubles; k_resident_tb: 2 slots x 2K rows x nx), the norm partials
   // k_resident_reg2: 2 slots x 2 sides x 2 rows x nx LL entries of 2 doubles
-  return (size_t)grid + 1 + (size_t)2 * grid * 2 * (RS_KMAX > 4 ? RS_KMAX : 4) * nx +
+  return (size_t)grid + 4 + (size_t)2 * grid * 2 * (RS_KMAX > 4 ? RS_KMAX : 4) * nx +
          (size_t)(n_entries > 0 ? n_entries : 1) * grid * 2;
 }
 
@@ -1437,6 +1526,12 @@ static int rs_unroll_env() {
   return u;
 }
 
+static bool rs_pow2(double v) {
+  if (!(v > 0.0) || !std::isfinite(v)) return false;
+  int e;
+  return std::frexp(v, &e) == 0.5;
+}
+
 // PROTOX_RESIDENT_REG: 0 = the shared-memory row walk (k_resident), 1 = the
 // register-resident kernel, 2 = its two-sweeps-per-hop variant (A/B)
 static int rs_reg_env() {
@@ -1478,13 +1573,16 @@ px_status launch_resident(int stencil, const ResidentLaunch& r_in, int grid, siz
     // ρ rows + edge arrays + fixed ghost columns (k_resident_reg's shared layout)
     constexpr int RE = RR_RM + 2;
     smem = ((size_t)r.rmax * r.nx + 2 * 2 * (RS_THREADS / 32) * RE + 4 * RE) * sizeof(double);
-    static size_t reg_set[2] = {};
+    static size_t reg_set[3] = {};
     if (k) {
-      e = rs_attr(k_resident_reg<1>, smem, reg_set[1]);
-      fn = (void*)k_resident_reg<1>;
+      e = rs_attr(k_resident_reg<1, false>, smem, reg_set[1]);
+      fn = (void*)k_resident_reg<1, false>;
+    } else if (rs_pow2(r.scale) && rs_pow2(r.lambda)) {
+      e = rs_attr(k_resident_reg<0, true>, smem, reg_set[2]);
+      fn = (void*)k_resident_reg<0, true>;
     } else {
-      e = rs_attr(k_resident_reg<0>, smem, reg_set[0]);
-      fn = (void*)k_resident_reg<0>;
+      e = rs_attr(k_resident_reg<0, false>, smem, reg_set[0]);
+      fn = (void*)k_resident_reg<0, false>;
     }
   } else switch (k * 4 + K) {
     case 1: e = rs_attr(k_resident<0>, smem, attr_set[0][0]); fn = (void*)k_resident<0>; break;

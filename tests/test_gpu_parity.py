@@ -803,6 +803,24 @@ def test_separate_ghost_fill_subprocess():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("shape", [(1000, 700), (66, 1036), (1024, 1024)])
+@pytest.mark.parametrize("bc", [P.PX_BC_PERIODIC, P.PX_BC_DIRICHLET_CC, P.PX_BC_FIXED_GHOSTS])
+def test_solve_resident_reg_general_h_lambda(shape, bc):
+    """k_resident_reg with h and λ that are not powers of two (its rounded
+    multiply-then-add path; power-of-two h, λ take the exact fused
+    multiply-adds): bit-identical to the oracle."""
+    n0, n1 = shape
+    h = 1.0 / (n1 - 1)
+    lam = 0.9 * h * h / 8
+    phi0, rho = _fields(n0, n1, 1, 23, bc)
+    for N, E in ((11, 3), (6, 0)):
+        out, norms, _ = run_gpu_solve(n0, n1, h, lam, bc, 0, N, E, phi0, rho)
+        ref, rn = oracle.solve(_orc_problem(n0, n1, h, lam, bc, 0, N, E), phi0, rho)
+        assert bits_equal(out, ref[1:-1, 1:-1]), ulp_diff(out, ref[1:-1, 1:-1])
+        _check_norms(norms, rn)
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("var", [("PROTOX_RESIDENT_K", "2"), ("PROTOX_RESIDENT_K", "3"),
                                  ("PROTOX_RESIDENT_REG", "0"), ("PROTOX_RESIDENT_REG", "2")])
 def test_resident_temporal_blocking_variant_subprocess(var):
