@@ -54,21 +54,6 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
   return v;
 }
 
-// Canonical tap sums (oracle order, each op rounded).
-template <int ST>
-__device__ __forceinline__ double rs_taps(double w, double e, double s, double n, double c, double sw,
-                                          double se, double nw, double ne) {
-  if (ST == 0) return __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(w, e), s), n), __dmul_rn(-4.0, c));
-  double q = __dmul_rn(4.0, w);
-  q = __dadd_rn(q, __dmul_rn(4.0, e));
-  q = __dadd_rn(q, __dmul_rn(4.0, s));
-  q = __dadd_rn(q, __dmul_rn(4.0, n));
-  q = __dadd_rn(q, sw);
-  q = __dadd_rn(q, se);
-  q = __dadd_rn(q, nw);
-  q = __dadd_rn(q, ne);
-  return __dadd_rn(q, __dmul_rn(-20.0, c));
-}
 
 // Rows rlo..rhi of the CTA's shared block: B = A + λ(scale·L(A) − F)
 // (WRITE), or residual norms of A only.  A thread walks a column pair down

@@ -12,6 +12,7 @@
 // order) and written to the solve's norm ring.
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdint>
 
 #include "px_device.cuh"
@@ -346,20 +347,295 @@ static size_t box1_smem(const SmallBox& b) {
   return ((size_t)2 * (b.nx + 2) * (b.ny + 2) + (size_t)b.nx * b.ny + (size_t)box1_entries(b) * 32 * 2) *
          sizeof(double);
 }
-// PROTOX_SMALLBOX (read once, A/B): unset = the 8-CTA cluster kernel when
-// the box has 16+ rows, else k_box1, else k_smallbox; "box1" / "old" force
-// k_box1 / k_smallbox
+// PROTOX_SMALLBOX (read once, A/B): unset = k_boxw (nx <= 64, ny <= 128),
+// else the 8-CTA cluster kernel when the box has 16+ rows, else k_box1, else
+// k_smallbox; "cluster" skips k_boxw; "box1" / "old" force k_box1 / k_smallbox
 static int box1_mode() {
   static int m = -1;
   if (m < 0) {
     const char* e = getenv("PROTOX_SMALLBOX");
-    m = !e ? 0 : (e[0] == 'b' ? 1 : (e[0] == 'o' ? 2 : 0));
+    m = !e ? 0 : (e[0] == 'b' ? 1 : (e[0] == 'o' ? 2 : (e[0] == 'c' ? 3 : 0)));
   }
   return m;
 }
 static bool box1_eligible(const SmallBox& b) {
   return box1_mode() != 2 && b.g == 1 && (int64_t)b.nx * b.ny <= (int64_t)BX_THREADS * BX_MAXC &&
          box1_smem(b) <= 200 * 1024;
+}
+
+// ---------------------------------------------------------------------------
+// k_boxw: the whole-box solve with the box IN REGISTERS, one warp per row
+// group (round 2, BASELINE config 1).  Lane l of warp w owns column pair l
+// (columns 2l, 2l+1; nx <= 64) of rows w·RW .. w·RW + RW - 1 (16 warps,
+// ny <= 16·RW, RW <= 4),
+// φ and ρ in registers for the whole solve.  W/E neighbours are indexed
+// shuffles inside the warp (the periodic wrap falls out of the lane index;
+// odd reflection / fixed ghosts are a select at lanes 0 and np-1); N/S
+// neighbours inside the row group are registers, across groups one 16-B
+// shared load per row group edge from a double-buffered row board that every
+// warp writes its first and last rows into (with the y images at the domain
+// faces) before the ONE block barrier per sweep.  A recorded sweep adds a
+// warp butterfly of (max bits, Σr²) whose per-warp partials go to shared
+// memory, reduced over the warps in fixed order after the last sweep.  Per
+// cell the oracle's expression tree (power-of-two h and λ: the exact fused
+// multiply-adds of k_resident_reg): bit-identical φ and max-norm.  The max
+// per warp by two redux.sync steps on the bit pattern, not a 64-bit
+// butterfly (the norm is recorded every sweep at BJ.C1).
+constexpr int BW_THREADS = 512;  // 16 warps: 128 registers a thread, up to 4 rows of φ, ρ in registers
+constexpr int BW_WARPS = BW_THREADS / 32;
+// rows per warp (1, 2 or 4) of an nx x ny box; 0: not eligible
+static int bw_rows_per_warp(int nx, int ny) {
+  if (nx < 2 || nx > 64 || (nx & 1) || ny < 1) return 0;
+  for (int rw = 1; rw <= 4; rw *= 2)
+    if (ny <= BW_WARPS * rw && ny % rw == 0) return rw;
+  return 0;
+}
+template <int ST, bool P2, int RW>
+__global__ void __launch_bounds__(BW_THREADS, 1) k_boxw(const SmallBox b, int n_entries) {
+  extern __shared__ __align__(16) double sm[];
+  const int nx = b.nx, ny = b.ny, np = nx / 2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* board = sm;                                   // [2][ny + 2][nx]: rows -1 .. ny
+  double* part = board + (size_t)2 * (ny + 2) * nx;     // [entry][BW_WARPS][max bits, sum]
+  double* gcor = part + (size_t)n_entries * BW_WARPS * 2;  // [4] fixed corners (-1,-1) (nx,-1) (-1,ny) (nx,ny)
+  const int bsz = (ny + 2) * nx;
+  const int y0 = warp * RW;
+  const bool wact = y0 < ny;                            // warp-uniform
+  const bool act = wact && lane < np;
+  const int xs = lane < np ? 2 * lane : 0;              // clamped column (inactive lanes read valid memory)
+  const bool per = b.bc == PX_BC_PERIODIC, refl = b.bc == PX_BC_DIRICHLET_CC, fixed = b.bc == PX_BC_FIXED_GHOSTS;
+  const int srcW = lane == 0 ? np - 1 : lane - 1, srcE = lane >= np - 1 ? 0 : lane + 1;
+  const bool edgeW = lane == 0, edgeE = lane == np - 1;
+  double2 cur[RW], rho[RW];
+  double gW[RW], gE[RW];
+#pragma unroll
+  for (int j = 0; j < RW; ++j) {
+    const int y = y0 + j;
+    cur[j] = rho[j] = make_double2(0.0, 0.0);
+    gW[j] = gE[j] = 0.0;
+    if (act) {
+      const double* src = b.phi_in + (int64_t)y * b.ld_in + xs;
+      cur[j] = make_double2(src[0], src[1]);
+      const double* f = b.rhs + (int64_t)y * b.ld_rhs + xs;
+      rho[j] = make_double2(f[0], f[1]);
+      if (fixed) {
+        gW[j] = b.phi_in[(int64_t)y * b.ld_in - 1];
+        gE[j] = b.phi_in[(int64_t)y * b.ld_in + nx];
+      }
+    }
+  }
+  // fixed ghost rows (both buffers) and corners
+  if (fixed) {
+    for (int i = tid; i < nx; i += BW_THREADS) {
+      const double lo = b.phi_in[-b.ld_in + i], hi = b.phi_in[(int64_t)ny * b.ld_in + i];
+      board[i] = board[bsz + i] = lo;
+      board[(size_t)(ny + 1) * nx + i] = board[bsz + (size_t)(ny + 1) * nx + i] = hi;
+    }
+    if (tid == 0) {
+      gcor[0] = b.phi_in[-b.ld_in - 1];
+      gcor[1] = b.phi_in[-b.ld_in + nx];
+      gcor[2] = b.phi_in[(int64_t)ny * b.ld_in - 1];
+      gcor[3] = b.phi_in[(int64_t)ny * b.ld_in + nx];
+    }
+  }
+  // the warp's first and last rows (and the y images at the faces) into board buffer bb
+  auto post = [&](int bb) {
+    if (!act) return;
+    double* B = board + (size_t)bb * bsz;
+#pragma unroll
+    for (int j = 0; j < RW; ++j) {
+      if (j != 0 && j != RW - 1) continue;
+      const int y = y0 + j;
+      *reinterpret_cast<double2*>(B + (size_t)(y + 1) * nx + xs) = cur[j];
+      if (y == 0 && !fixed) {
+        if (per) *reinterpret_cast<double2*>(B + (size_t)(ny + 1) * nx + xs) = cur[j];
+        else *reinterpret_cast<double2*>(B + xs) = make_double2(-cur[j].x, -cur[j].y);
+      }
+      if (y == ny - 1 && !fixed) {
+        if (per) *reinterpret_cast<double2*>(B + xs) = cur[j];
+        else *reinterpret_cast<double2*>(B + (size_t)(ny + 1) * nx + xs) = make_double2(-cur[j].x, -cur[j].y);
+      }
+    }
+  };
+  post(0);
+  __syncthreads();
+  // W of column 2l / E of column 2l+1 of a row v (gw / ge: its fixed ghosts)
+  auto west = [&](double2 v, double gw) -> double {
+    const double sh = __shfl_sync(FULL_MASK, v.y, srcW);
+    return edgeW && !per ? (refl ? -v.x : gw) : sh;
+  };
+  auto east = [&](double2 v, double ge) -> double {
+    const double sh = __shfl_sync(FULL_MASK, v.x, srcE);
+    return edgeE && !per ? (refl ? -v.y : ge) : sh;
+  };
+  // fixed ghost columns of the board rows next to the group (rows y0-1 and
+  // y0+RW lie in the domain or its ghost ring)
+  double gWs = 0.0, gEs = 0.0, gWn = 0.0, gEn = 0.0;
+  if (fixed && wact) {
+    gWs = b.phi_in[(int64_t)(y0 - 1) * b.ld_in - 1];
+    gEs = b.phi_in[(int64_t)(y0 - 1) * b.ld_in + nx];
+    gWn = b.phi_in[(int64_t)(y0 + RW) * b.ld_in - 1];
+    gEn = b.phi_in[(int64_t)(y0 + RW) * b.ld_in + nx];
+  }
+  auto update = [&](double2 S, double2 C, double2 N, double2 f, double sw_g, double se_g, double cw_g, double ce_g,
+                    double nw_g, double ne_g, double2& res) -> double2 {
+    const double cw = west(C, cw_g), ce = east(C, ce_g);
+    double sw = 0.0, se = 0.0, nw = 0.0, ne = 0.0;
+    if (ST) {
+      sw = west(S, sw_g);
+      se = east(S, se_g);
+      nw = west(N, nw_g);
+      ne = east(N, ne_g);
+    }
+    double2 o;
+    if (P2) {
+      const double L0 = fma(-4.0, C.x, __dadd_rn(__dadd_rn(__dadd_rn(cw, C.y), S.x), N.x));
+      const double L1 = fma(-4.0, C.y, __dadd_rn(__dadd_rn(__dadd_rn(C.x, ce), S.y), N.y));
+      res.x = fma(b.scale, L0, -f.x);
+      res.y = fma(b.scale, L1, -f.y);
+      o = make_double2(fma(b.lambda, res.x, C.x), fma(b.lambda, res.y, C.y));
+    } else {
+      const double L0 = rs_taps<ST>(cw, C.y, S.x, N.x, C.x, sw, S.y, nw, N.y);
+      const double L1 = rs_taps<ST>(C.x, ce, S.y, N.y, C.y, S.x, se, N.x, ne);
+      res.x = __dsub_rn(__dmul_rn(b.scale, L0), f.x);
+      res.y = __dsub_rn(__dmul_rn(b.scale, L1), f.y);
+      o = make_double2(__dadd_rn(C.x, __dmul_rn(b.lambda, res.x)), __dadd_rn(C.y, __dmul_rn(b.lambda, res.y)));
+    }
+    if (!act) res = make_double2(0.0, 0.0);
+    return o;
+  };
+  // max|r| by fmax (exact: one of its operands; a NaN r is restored from
+  // Σr², which it makes NaN), Σr² by fused multiply-add
+  auto acc = [&](double2 res, double& mx, double& ss) {
+    mx = fmax(mx, fabs(res.x));
+    ss = fma(res.x, res.x, ss);
+    mx = fmax(mx, fabs(res.y));
+    ss = fma(res.y, res.y, ss);
+  };
+  // warp partial: the max as two 32-bit redux.sync steps over the bit pattern
+  // (high word, then the low word among the lanes holding the high maximum),
+  // Σ by a fixed butterfly
+  auto warp_partial = [&](double mxd, double ss, int e) {
+    const unsigned long long mb =
+        isnan(ss) ? 0x7ff8000000000000ull : (unsigned long long)__double_as_longlong(mxd);
+    const unsigned hi = (unsigned)(mb >> 32);
+    const unsigned mhi = __reduce_max_sync(FULL_MASK, hi);
+    const unsigned mlo = __reduce_max_sync(FULL_MASK, hi == mhi ? (unsigned)mb : 0u);
+    for (int o = 16; o > 0; o >>= 1) ss = ss + __shfl_xor_sync(FULL_MASK, ss, o);
+    if (lane == 0) {
+      part[((size_t)e * BW_WARPS + warp) * 2] = __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
+      part[((size_t)e * BW_WARPS + warp) * 2 + 1] = ss;
+    }
+  };
+  // one pass over the group's rows of buffer bb's iterate: WRITE = update
+  // (the new rows replace cur), else residuals only
+  auto pass = [&](int bb, bool write, bool rec, double& mx, double& ss) {
+    const double* B = board + (size_t)bb * bsz;
+    const double2 s_row = *reinterpret_cast<const double2*>(B + (size_t)y0 * nx + xs);        // row y0 - 1
+    const double2 n_row = *reinterpret_cast<const double2*>(B + (size_t)(y0 + RW + 1) * nx + xs);  // row y0 + RW
+    double2 o[RW];
+#pragma unroll
+    for (int j = 0; j < RW; ++j) {
+      const double2 S = j == 0 ? s_row : cur[j - 1];
+      const double2 N = j == RW - 1 ? n_row : cur[j + 1];
+      const double sg_w = j == 0 ? gWs : gW[j - 1], sg_e = j == 0 ? gEs : gE[j - 1];
+      const double ng_w = j == RW - 1 ? gWn : gW[j + 1], ng_e = j == RW - 1 ? gEn : gE[j + 1];
+      double2 res;
+      o[j] = update(S, cur[j], N, rho[j], sg_w, sg_e, gW[j], gE[j], ng_w, ng_e, res);
+      if (rec) acc(res, mx, ss);
+    }
+    if (write)
+#pragma unroll
+      for (int j = 0; j < RW; ++j) cur[j] = o[j];
+  };
+  int entry = 0, phase = 0;
+  for (int s = 0; s < b.nsweeps; ++s) {
+    const bool rec = b.every > 0 && phase == 0;
+    if (++phase == b.every) phase = 0;
+    if (wact) {
+      double mx = 0.0, ss = 0.0;
+      pass(s & 1, true, rec, mx, ss);
+      post((s + 1) & 1);
+      if (rec) warp_partial(mx, ss, entry);
+    } else if (rec && lane == 0) {
+      part[((size_t)entry * BW_WARPS + warp) * 2] = 0.0;
+      part[((size_t)entry * BW_WARPS + warp) * 2 + 1] = 0.0;
+    }
+    if (rec) ++entry;
+    __syncthreads();
+  }
+  const int bN = b.nsweeps & 1;
+  if (b.final_norm) {
+    if (wact) {
+      double mx = 0.0, ss = 0.0;
+      pass(bN, false, true, mx, ss);
+      warp_partial(mx, ss, entry);
+    } else if (lane == 0) {
+      part[((size_t)entry * BW_WARPS + warp) * 2] = 0.0;
+      part[((size_t)entry * BW_WARPS + warp) * 2 + 1] = 0.0;
+    }
+    ++entry;
+  }
+  __syncthreads();
+  for (int e = tid; e < entry; e += BW_THREADS) {  // entries over the warps in fixed order
+    unsigned long long m = 0ull;
+    double t = 0.0;
+    for (int w = 0; w < BW_WARPS; ++w) {
+      m = umax64(m, (unsigned long long)__double_as_longlong(part[((size_t)e * BW_WARPS + w) * 2]));
+      t = w ? __dadd_rn(t, part[((size_t)e * BW_WARPS + w) * 2 + 1]) : part[((size_t)e * BW_WARPS + w) * 2 + 1];
+    }
+    b.d_max[e] = __longlong_as_double((long long)m);
+    b.d_sum[e] = t;
+  }
+  // φ^N with its ghost ring: own rows (+ ghost columns = the W/E images), and
+  // warp 0 the ghost rows -1 / ny from the board (+ the corners)
+  if (wact) {
+#pragma unroll
+    for (int j = 0; j < RW; ++j) {
+      const double w = west(cur[j], gW[j]), e = east(cur[j], gE[j]);
+      if (act) {
+        double* dst = b.phi_out + (int64_t)(y0 + j) * b.ld_out + xs;
+        dst[0] = cur[j].x;
+        dst[1] = cur[j].y;
+        if (edgeW) dst[-1] = w;
+        if (edgeE) dst[2] = e;
+      }
+    }
+  }
+  if (warp == 0) {
+    const double* B = board + (size_t)bN * bsz;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int y = k ? ny : -1;
+      const double2 v = *reinterpret_cast<const double2*>(B + (size_t)(y + 1) * nx + xs);
+      const double w = west(v, gcor[2 * k]), e = east(v, gcor[2 * k + 1]);
+      if (lane < np) {
+        double* dst = b.phi_out + (int64_t)y * b.ld_out + xs;
+        dst[0] = v.x;
+        dst[1] = v.y;
+        if (edgeW) dst[-1] = w;
+        if (edgeE) dst[2] = e;
+      }
+    }
+  }
+}
+
+static size_t bw_smem(const SmallBox& b, int n_entries) {
+  return ((size_t)2 * (b.ny + 2) * b.nx + (size_t)n_entries * BW_WARPS * 2 + 4) * sizeof(double);
+}
+static bool bw_pow2(double v) {
+  if (!(v > 0.0) || !std::isfinite(v)) return false;
+  int e;
+  return std::frexp(v, &e) == 0.5;
+}
+template <int RW>
+static cudaError_t bw_launch(const SmallBox& b, int ne, size_t smem, cudaStream_t s) {
+  const bool p2 = b.stencil == 0 && bw_pow2(b.scale) && bw_pow2(b.lambda);
+  void (*fn)(const SmallBox, int) = b.stencil ? k_boxw<1, false, RW> : (p2 ? k_boxw<0, true, RW> : k_boxw<0, false, RW>);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  if (e != cudaSuccess) return e;
+  fn<<<1, BW_THREADS, smem, s>>>(b, ne);
+  return cudaGetLastError();
 }
 
 size_t smallbox_smem(int nx, int ny) {
@@ -371,7 +647,19 @@ bool smallbox_fits(int nx, int ny) { return nx >= 1 && ny >= 1 && smallbox_smem(
 px_status launch_smallbox(const SmallBox& b, cudaStream_t s) {
   // 16+ rows: spread the box over a cluster of 8 SMs (px_cluster.cu): one SM
   // running k_box1 is issue-bound (73 % issue-active at 1.76 µs per 64² sweep)
-  if (box1_mode() == 0 && cluster_box_eligible(b)) return launch_cluster_box(b, s);
+  if (box1_mode() == 0 && b.g == 1) {
+    const int rw = bw_rows_per_warp(b.nx, b.ny);
+    const int ne = box1_entries(b) > 0 ? box1_entries(b) : 1;
+    const size_t smem = bw_smem(b, ne);
+    if (rw > 0 && smem <= 200 * 1024) {
+      const cudaError_t e = rw == 1 ? bw_launch<1>(b, ne, smem, s)
+                                    : (rw == 2 ? bw_launch<2>(b, ne, smem, s) : bw_launch<4>(b, ne, smem, s));
+      note_kernel("k_boxw");
+      count_launches(1);
+      return cuda_check(e, "small-box kernel launch");
+    }
+  }
+  if ((box1_mode() == 0 || box1_mode() == 3) && cluster_box_eligible(b)) return launch_cluster_box(b, s);
   if (box1_eligible(b)) {
     const size_t smem = box1_smem(b);
     const bool small = (int64_t)b.nx * b.ny <= 4 * BX_THREADS;  // up to 4 cells per thread: all in registers

@@ -83,34 +83,40 @@ def _solve_case(n0, n1, bc, N, E, kind, seed, nranks=1, tk=1, box=None, graph=Tr
     return kern
 
 
-def _box_kernel(rows):
+def _box_kernel(cols, rows):
     """The whole-box kernel px_solve picks (PROTOX_SMALLBOX, read once per
-    process: default the 8-CTA cluster kernel from 16 rows, else k_box1;
-    'box1' / 'old' force k_box1 / the round-1 one-CTA k_smallbox)."""
+    process: default k_boxw for even widths <= 64 and <= 16 rows (any), <= 32
+    (even) or <= 64 (multiple of 4), else the 8-CTA cluster kernel from 16 rows, else k_box1;
+    'cluster' skips k_boxw; 'box1' / 'old' force k_box1 / the round-1 one-CTA
+    k_smallbox)."""
     mode = os.environ.get("PROTOX_SMALLBOX", "")
     if mode.startswith("b"):
         return "k_box1"
     if mode.startswith("o"):
         return "k_smallbox"
+    boxw = cols % 2 == 0 and cols <= 64 and any(rows <= 16 * rw and rows % rw == 0 for rw in (1, 2, 4))
+    if boxw and not mode.startswith("c"):
+        return "k_boxw"
     return "k_cluster_box" if rows >= 16 else "k_box1"
 
 
 @pytest.mark.parametrize("kind", KINDS)
 def test_nan_box_c1(kind):
     """BJ.C1 shape (64², Dirichlet-CC): the whole solve in one launch."""
-    assert _box_kernel(64) in _solve_case(64, 64, P.PX_BC_DIRICHLET_CC, 30, 1, kind, 11)
+    assert _box_kernel(64, 64) in _solve_case(64, 64, P.PX_BC_DIRICHLET_CC, 30, 1, kind, 11)
 
 
 @pytest.mark.parametrize("kind", KINDS)
 def test_nan_box_short(kind):
     """A box of < 16 rows, periodic."""
-    assert _box_kernel(12) in _solve_case(64, 12, P.PX_BC_PERIODIC, 20, 1, kind, 12)
+    assert _box_kernel(64, 12) in _solve_case(64, 12, P.PX_BC_PERIODIC, 20, 1, kind, 12)
 
 
-@pytest.mark.parametrize("mode", ["box1", "old"])
+@pytest.mark.parametrize("mode", ["box1", "old", "cluster"])
 def test_box_kernel_variants_subprocess(mode):
     """The other whole-box kernels (k_box1 for every box it fits; the round-1
-    one-CTA k_smallbox) stay bit-identical: the small-box parity and NaN tests
+    one-CTA k_smallbox; the 8-CTA cluster kernel where k_boxw would run) stay
+    bit-identical: the small-box parity and NaN tests
     re-run in a child process with PROTOX_SMALLBOX=<mode>."""
     import subprocess
     import sys

@@ -185,13 +185,16 @@ def test_solve_ragged_multibox(bc, st, graph):
     _check_norms(norms, rn)
 
 
-@pytest.mark.parametrize("shape", [(64, 64), (3, 5), (1, 40), (40, 1), (127, 129), (100, 40)])
+@pytest.mark.parametrize("shape", [(64, 64), (3, 5), (1, 40), (40, 1), (127, 129), (100, 40), (62, 52), (18, 7),
+                                   (2, 64), (6, 30)])
 @pytest.mark.parametrize("bc", [P.PX_BC_PERIODIC, P.PX_BC_DIRICHLET_CC, P.PX_BC_FIXED_GHOSTS])
 @pytest.mark.parametrize("st", [P.PX_LAPLACE_5PT, P.PX_MEHRSTELLEN_9PT])
 def test_solve_whole_box_shapes(shape, bc, st):
-    """Whole-box solves in one launch (k_box1 by default): up to 4 and up to
-    16 cells per thread (127 x 129 = 16383 cells), one-cell-wide boxes (a cell
-    is then its own image on both sides), every BC and stencil; odd and even
+    """Whole-box solves in one launch: k_boxw (one warp per row group, the box
+    in registers) with four rows per warp (64 x 64, 62 x 52: a partial warp,
+    2 x 64: one column pair), two (6 x 30) and one (40 x 1, 18 x 7), k_box1 with up to 4
+    and up to 16 cells per thread (127 x 129 = 16383 cells), one-cell-wide
+    boxes (a cell is then its own image on both sides), every BC and stencil; odd and even
     sweep counts and norm periods 1, 3 and 0 (final entry only)."""
     n0, n1 = shape
     h = 1.0 / 128
