@@ -515,14 +515,14 @@ __global__ void __launch_bounds__(BW_THREADS, 1) k_boxw(const SmallBox b, int n_
   // warp partial: the max as two 32-bit redux.sync steps over the bit pattern
   // (high word, then the low word among the lanes holding the high maximum),
   // Σ by a fixed butterfly
-  auto warp_partial = [&](double mxd, double ss, int e) {
+  auto warp_partial = [&](double mxd, double ss, int e, bool store) {
     const unsigned long long mb =
         isnan(ss) ? 0x7ff8000000000000ull : (unsigned long long)__double_as_longlong(mxd);
     const unsigned hi = (unsigned)(mb >> 32);
     const unsigned mhi = __reduce_max_sync(FULL_MASK, hi);
     const unsigned mlo = __reduce_max_sync(FULL_MASK, hi == mhi ? (unsigned)mb : 0u);
     for (int o = 16; o > 0; o >>= 1) ss = ss + __shfl_xor_sync(FULL_MASK, ss, o);
-    if (lane == 0) {
+    if (store && lane == 0) {
       part[((size_t)e * BW_WARPS + warp) * 2] = __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
       part[((size_t)e * BW_WARPS + warp) * 2 + 1] = ss;
     }
@@ -548,15 +548,24 @@ __global__ void __launch_bounds__(BW_THREADS, 1) k_boxw(const SmallBox b, int n_
 #pragma unroll
       for (int j = 0; j < RW; ++j) cur[j] = o[j];
   };
+  // a recorded sweep's warp reduction runs after the barrier, overlapping the
+  // next sweep's loads and shuffles (it is off the sweep-to-sweep chain)
   int entry = 0, phase = 0;
+  bool pend = false;
+  double pmx = 0.0, pss = 0.0;
   for (int s = 0; s < b.nsweeps; ++s) {
     const bool rec = b.every > 0 && phase == 0;
     if (++phase == b.every) phase = 0;
     if (wact) {
+      // the previous recorded sweep's reduction in the same block as this
+      // sweep's update (the compiler interleaves the two chains)
+      warp_partial(pmx, pss, entry - 1, pend);
       double mx = 0.0, ss = 0.0;
       pass(s & 1, true, rec, mx, ss);
       post((s + 1) & 1);
-      if (rec) warp_partial(mx, ss, entry);
+      pend = rec;
+      pmx = mx;
+      pss = ss;
     } else if (rec && lane == 0) {
       part[((size_t)entry * BW_WARPS + warp) * 2] = 0.0;
       part[((size_t)entry * BW_WARPS + warp) * 2 + 1] = 0.0;
@@ -564,12 +573,13 @@ __global__ void __launch_bounds__(BW_THREADS, 1) k_boxw(const SmallBox b, int n_
     if (rec) ++entry;
     __syncthreads();
   }
+  if (wact) warp_partial(pmx, pss, entry - 1, pend);
   const int bN = b.nsweeps & 1;
   if (b.final_norm) {
     if (wact) {
       double mx = 0.0, ss = 0.0;
       pass(bN, false, true, mx, ss);
-      warp_partial(mx, ss, entry);
+      warp_partial(mx, ss, entry, true);
     } else if (lane == 0) {
       part[((size_t)entry * BW_WARPS + warp) * 2] = 0.0;
       part[((size_t)entry * BW_WARPS + warp) * 2 + 1] = 0.0;
