@@ -35,6 +35,18 @@ METRIC = "fp64 Gcell-updates/s of fused relax sweep at 1/2/4/8 B200; % HBM roofl
 UNIT = "Gcell-updates/s"
 BYTES_PER_CELL_UPDATE = 24  # read φ 8 + read ρ 8 + write φ' 8
 
+# the whole-solve kernels of the small configs (named by px_last_solve_kernels)
+SOLVE_KERNELS = {
+    "k_resident_reg": "iterate in registers, rows resident on chip across all sweeps, LL row mailbox in L2 "
+                      "between neighbouring CTAs, one launch",
+    "k_resident_reg2": "k_resident_reg with two sweeps per mailbox hop",
+    "k_resident": "iterate resident in shared memory, LL row mailbox, one launch",
+    "k_boxw": "whole box in registers on one CTA, one warp per row group, one launch",
+    "k_cluster_box": "whole solve on an 8-CTA cluster, DSMEM halos, one launch",
+    "k_box1": "whole box on one CTA of 1024 threads, one launch",
+    "k_smallbox": "whole box in shared memory on one CTA, one launch",
+}
+
 CONFIGS = {
     "C3": dict(n=16384, box=256, bc=0, stencil=0, sweeps=100, norm_every=1, rho="hash",
                desc="BASELINE config 3: 2D Poisson 16384x16384 fp64, periodic, 5-point, "
@@ -43,11 +55,11 @@ CONFIGS = {
                desc="BASELINE config 4: 2D Poisson 32768x32768 fp64, periodic, 5-point, 256x256-box "
                     "DisjointBoxLayout, temporal blocking k=4 sweeps per halo exchange (norm per exchange)"),
     "C2": dict(n=1024, box=1024, bc=0, stencil=0, sweeps=1000, norm_every=10, rho="hash",
-               solve_kernel="k_resident (iterate resident in shared memory, all sweeps in one launch)",
+               solve_kernel=True,
                desc="BASELINE config 2: 2D Poisson 1024x1024 single box, 1000 sweeps, "
                     "max-norm every 10 (L2-resident)"),
     "C1": dict(n=64, box=64, bc=1, stencil=0, sweeps=100, norm_every=1, rho="sine",
-               solve_kernel="k_cluster_box (whole solve on an 8-CTA cluster, DSMEM halos, one launch)",
+               solve_kernel=True,
                desc="BASELINE config 1: 64x64 box + 1 ghost layer, Dirichlet, 100 sweeps"),
     "C5": dict(n=8192, box=256, bc=1, stencil=1, sweeps=100, norm_every=1, rho="sine",
                desc="BASELINE config 5: 8192x8192 Mehrstellen 9-point, Dirichlet-CC"),
@@ -590,6 +602,7 @@ def run_native(args):
     ev1.record(stream)
     barrier()
     launches = P.kernel_launch_count() - launches0
+    solve_kernels = P.last_solve_kernels()
     clk = clocks.stop()
     t_ms = max_over_ranks(ev0.elapsed_time(ev1))
     cells = n * n * S * args.steps
@@ -639,8 +652,10 @@ def run_native(args):
         # leaves the chip, so the timed step is that kernel; the fields above describe
         # a single k = 1 sweep launch for comparison with the large configs
         per_step = launches / args.steps
+        kname = next((k for k in SOLVE_KERNELS if k in solve_kernels.split()), solve_kernels)
         roofline["solve_kernel"] = {
-            "name": cfg["solve_kernel"], "launches_per_step": per_step, "ms_per_step": t_ms / args.steps,
+            "name": f"{kname} ({SOLVE_KERNELS.get(kname, 'whole solve in one launch')})",
+            "launches_per_step": per_step, "ms_per_step": t_ms / args.steps,
             "us_per_sweep": 1e3 * t_ms / args.steps / S,
             "bound": "latency (on-chip iterate: block barriers and neighbour handshakes per sweep)",
             "equivalent_GBps_at_24B": BYTES_PER_CELL_UPDATE * value}
