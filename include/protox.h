@@ -361,6 +361,19 @@ px_status px_solve(const px_layout* l, px_comm* c, int32_t rank, const px_relax_
                    const px_patch* rhs, double* h_norms, int32_t cap, int32_t* n_written,
                    int32_t* in_scratch, void* stream);
 
+/* px_solve without the host round trip (the same hot path):
+ * everything is enqueued on `stream` and the call returns at once.  The
+ * recorded norms go to DEVICE memory: d_norms[2j], d_norms[2j+1] = (max|r|,
+ * Σr²) of entry j (global over all ranks), written stream-ordered after the
+ * solve; *n_written and *in_scratch are known on return (they depend on the
+ * options only).  For back-to-back solves of a pipeline (and the device-timed
+ * bench); NCCL asynchronous errors surface at the next px_solve or
+ * synchronising call.  Arguments, caching and errors otherwise as px_solve. */
+px_status px_solve_async(const px_layout* l, px_comm* c, int32_t rank, const px_relax_params* p,
+                         const px_solve_opts* o, px_patch* phi, px_patch* phi_scratch,
+                         const px_patch* rhs, double* d_norms, int32_t cap, int32_t* n_written,
+                         int32_t* in_scratch, void* stream);
+
 /* End-to-end solve on HOST arrays (single rank): copies φ^0 and ρ
  * (n1 x n0 interior, dim-0 fastest, pinned or pageable host memory) to the
  * device, solves, copies φ^N back to h_phi_out.  Device buffers are

@@ -1261,6 +1261,37 @@ px_status px_solve(const px_layout* l, px_comm* c, int32_t rank, const px_relax_
   return PX_OK;
 }
 
+px_status px_solve_async(const px_layout* l, px_comm* c, int32_t rank, const px_relax_params* p,
+                         const px_solve_opts* o, px_patch* phi, px_patch* phi_scratch, const px_patch* rhs,
+                         double* d_norms, int32_t cap, int32_t* n_written, int32_t* in_scratch, void* stream) {
+  if (cap < 0 || (cap > 0 && !d_norms)) return fail(PX_ERR_ARG, "bad norm output");
+  NvtxRange r_solve("protox/px_solve_async");
+  Plan* plan = nullptr;
+  bool odd = false;
+  int32_t nparts = 1;
+  PX_TRY(solve_enqueue(l, c, rank, p, o, phi, phi_scratch, rhs, stream, &plan, &odd, &nparts));
+  cudaStream_t s = (cudaStream_t)stream;
+  const int32_t nw = std::min(plan->n_entries, cap);
+  if (nw > 0) {  // the norm ring interleaved into d_norms (max, Σ) per entry, stream-ordered
+    PX_TRY(cuda_check(cudaMemcpy2DAsync(d_norms, 2 * sizeof(double), plan->d_max, sizeof(double), sizeof(double), nw,
+                                        cudaMemcpyDeviceToDevice, s), "norms"));
+    PX_TRY(cuda_check(cudaMemcpy2DAsync(d_norms + 1, 2 * sizeof(double), plan->d_sum, sizeof(double), sizeof(double),
+                                        nw, cudaMemcpyDeviceToDevice, s), "norms"));
+  }
+  if (odd && !in_scratch) {
+    for (int32_t i = 0; i < nparts; ++i) {
+      const px_patch& a = phi_scratch[i];
+      const px_patch& b = phi[i];
+      PX_TRY(cuda_check(cudaMemcpy2DAsync(b.data, b.ld * sizeof(double), a.data, a.ld * sizeof(double),
+                                          ext(a.box, 0) * sizeof(double), ext(a.box, 1),
+                                          cudaMemcpyDeviceToDevice, s), "copy result"));
+    }
+  }
+  if (n_written) *n_written = nw;
+  if (in_scratch) *in_scratch = odd ? 1 : 0;
+  return PX_OK;
+}
+
 // ----------------------------------------------------------- host e2e path
 struct HostBufs {
   uint64_t gen = 0;

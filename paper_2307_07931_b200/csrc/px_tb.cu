@@ -348,6 +348,9 @@ __global__ void __launch_bounds__(NW * 32 + 32, (NW == 7 ? 2 : 1))
 // ghost column / row is re-derived from the level's own interior by odd
 // reflection (corners by the product rule), so a pass of K levels is exactly
 // K plain sweeps with the ghost fill in between (oracle R5).
+#ifndef PX_TBW_IDLE_SKIP
+#define PX_TBW_IDLE_SKIP 1  // A/B: 0 = idle warps of a narrow strip compute like the others
+#endif
 #ifndef PX_TBW_SWZ
 #define PX_TBW_SWZ 0
 #endif
@@ -697,11 +700,16 @@ __global__ void __launch_bounds__(tbw::NW * 32 + 32, 1)
       const double* pp2 = smem;
       const int nst = (c.nrows + K - 1 + R - 1) / R;
       const int s_steady0 = (3 * K - 1 + R - 1) / R;  // first stage with every level valid
+      // a warp with no column to write in this strip (the last, narrow strip
+      // of a row of strips) only keeps the stage protocol: its levels would be
+      // discarded, and under the board's power cap the saved energy is time
+      const bool widle = PX_TBW_IDLE_SKIP && cload + warp * G::WO + K >= a.nx;
       for (int s = 0; s < nst; ++s) {
         mbar_wait(&full[slot], phase);
         const double* sp = smem + (size_t)slot * G::STAGE;
         const bool steady = s >= s_steady0 && (s * R + R - 1 < c.nrows - K);
-        if (steady)
+        if (widle) {
+        } else if (steady)
           tbw_stage<ST, K, P2, FIX, DIR, NM, false>(a, x, c, s, sp, pp1, pp2, cl, st, mx, ss, ia, act);
         else
           tbw_stage<ST, K, P2, FIX, DIR, NM, true>(a, x, c, s, sp, pp1, pp2, cl, st, mx, ss, ia, act);

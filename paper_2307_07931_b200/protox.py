@@ -100,7 +100,7 @@ EXPORTS = [
     "px_comm_unique_id", "px_comm_create", "px_comm_destroy", "px_comm_allreduce_norms",
     "px_comm_enable_p2p", "px_comm_create_peer", "px_comm_p2p_export", "px_comm_p2p_import",
     "px_exchange_ghosts", "px_exchange_ghosts_local",
-    "px_solve", "px_solve_host", "px_solve_host_batch", "px_release_cached", "px_mg_solve", "px_mg_release", "px_kernel_launch_count",
+    "px_solve", "px_solve_async", "px_solve_host", "px_solve_host_batch", "px_release_cached", "px_mg_solve", "px_mg_release", "px_kernel_launch_count",
     "px_last_solve_kernels",
     "px_relax_variant", "px_stream_ceiling", "px_pointwise_update",
     "px3_layout", "px3_norm_buffer_len", "px3_init_field", "px3_fill_ghosts", "px3_relax_step",
@@ -200,6 +200,9 @@ def lib():
     L.px_exchange_ghosts_local.argtypes = [vp, P(px_patch), vp]
     L.px_solve.restype = st
     L.px_solve.argtypes = [vp, vp, i32, P(px_relax_params), P(px_solve_opts), P(px_patch),
+                           P(px_patch), P(px_patch), P(ctypes.c_double), i32, P(i32), P(i32), vp]
+    L.px_solve_async.restype = st
+    L.px_solve_async.argtypes = [vp, vp, i32, P(px_relax_params), P(px_solve_opts), P(px_patch),
                            P(px_patch), P(px_patch), P(ctypes.c_double), i32, P(i32), P(i32), vp]
     L.px_solve_host.restype = st
     L.px_solve_host.argtypes = [vp, P(px_relax_params), P(px_solve_opts), vp, vp, vp,
@@ -509,6 +512,27 @@ def solve(layout: Layout, comm: Comm | None, rank: int, p: px_relax_params, nswe
                           ctypes.byref(nw), ctypes.byref(ins) if keep_in_scratch else None,
                           _stream(stream)))
     return SolveResult(norms[: nw.value].copy(), bool(ins.value))
+
+
+def solve_async(layout: Layout, comm: Comm | None, rank: int, p: px_relax_params, nsweeps: int,
+                norm_every: int, phi, phi_scratch, rhs, d_norms, temporal_k: int = 1, use_graph: bool = False,
+                stream=None, keep_in_scratch: bool = True) -> tuple[int, bool]:
+    """px_solve_async: as solve(), enqueued without a host round trip; the
+    norms go to d_norms (a float64 cuda tensor of >= 2 * entries elements).
+    Returns (entries written, in_scratch)."""
+    as_list = lambda v: v if isinstance(v, (list, tuple)) else [v]
+    ph, sc, rh = as_list(phi), as_list(phi_scratch), as_list(rhs)
+    n = len(ph)
+    A = px_patch * n
+    opts = px_solve_opts(nsweeps, norm_every, temporal_k, int(use_graph))
+    cap = d_norms.numel() // 2
+    nw, ins = ctypes.c_int32(0), ctypes.c_int32(0)
+    _check(lib().px_solve_async(layout.h, comm.h if comm else None, rank, ctypes.byref(p),
+                                ctypes.byref(opts), A(*ph), A(*sc), A(*rh),
+                                ctypes.cast(d_norms.data_ptr(), ctypes.POINTER(ctypes.c_double)), cap,
+                                ctypes.byref(nw), ctypes.byref(ins) if keep_in_scratch else None,
+                                _stream(stream)))
+    return nw.value, bool(ins.value)
 
 
 def mg_solve(layout: Layout, p: px_relax_params, levels: int, ncycles: int, phi: px_patch,

@@ -171,6 +171,21 @@ int main() {
   cudaEventCreate(&e1);
   const char* names[] = {"flag, 1 thread", "LL 512 thr", "LL 512 thr + bar", "flag + bar", "LL 2 slots", "k_resident exchange", "k_resident exchange, no back-off",
                          "k_resident exchange, sector-contiguous entries", "k_resident exchange, 32-B pair entries"};
+  // payload sweep of the 32-B pair entries (mode 8): columns per row
+  for (int cols : {1024, 512, 256, 64}) {
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaMemset(mb, 0, (size_t)2 * nsm * 8 * nx * 8 + 4096);
+      int r = rounds, m = 8, n = cols;
+      void* args[] = {&mb, &r, &m, &n, &cyc};
+      cudaEventRecord(e0);
+      cudaLaunchCooperativeKernel((void*)k_ring, nsm, 512, args, 0, 0);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      printf("{\"mode\": \"32-B pair entries\", \"cols\": %d, \"us_per_round\": %.3f}\n", cols, 1000.0 * ms / rounds);
+    }
+  }
   for (int threads : {512, 256}) {
     for (int mode = 0; mode < 9; ++mode) {
       for (int rep = 0; rep < 2; ++rep) {

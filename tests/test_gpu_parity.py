@@ -45,8 +45,9 @@ def _check_norms(gpu, orc):
 
 
 def run_gpu_solve(n0, n1, h, lam, bc, st, N, E, phi0_g, rho_g, g=1, box=None, nranks=1,
-                  graph=True, corr=False, tk=1):
-    """Solve on the GPU; nranks > 1 runs all slabs on this device (local transport)."""
+                  graph=True, corr=False, tk=1, async_=False):
+    """Solve on the GPU; nranks > 1 runs all slabs on this device (local
+    transport); async_: through px_solve_async (norms in device memory)."""
     dom = P.box(0, 0, n0 - 1, n1 - 1)
     lay = P.Layout(dom, box or (n0, n1 // nranks), g, bc, nranks)
     phis, scrs, rhss, fs = [], [], [], []
@@ -68,14 +69,22 @@ def run_gpu_solve(n0, n1, h, lam, bc, st, N, E, phi0_g, rho_g, g=1, box=None, nr
         P.exchange_ghosts_local(lay, [lay.patch(r, t) for r, t in enumerate(rhss)])
     stream = torch.cuda.Stream()
     stream.wait_stream(torch.cuda.current_stream())  # allocations/copies ran on the current stream
-    res = P.solve(lay, None, 0, P.relax_params(h, lam, st), N, E,
-                  [lay.patch(r, t) for r, t in enumerate(phis)],
-                  [lay.patch(r, t) for r, t in enumerate(scrs)],
-                  [lay.patch(r, t) for r, t in enumerate(rhss)], use_graph=graph, stream=stream,
-                  temporal_k=tk)
-    out_t = scrs if res.in_scratch else phis
+    parts = ([lay.patch(r, t) for r, t in enumerate(phis)], [lay.patch(r, t) for r, t in enumerate(scrs)],
+             [lay.patch(r, t) for r, t in enumerate(rhss)])
+    if async_:
+        ne = 0 if E < 0 else ((N + E - 1) // E if E > 0 else 0) + 1
+        d = torch.full((2 * max(ne, 1),), -1.0, dtype=torch.float64, device="cuda")
+        nw, ins = P.solve_async(lay, None, 0, P.relax_params(h, lam, st), N, E, *parts, d, use_graph=graph,
+                                stream=stream, temporal_k=tk)
+        stream.synchronize()
+        norms = d.view(-1, 2)[:nw].cpu().numpy()
+    else:
+        res = P.solve(lay, None, 0, P.relax_params(h, lam, st), N, E, *parts, use_graph=graph, stream=stream,
+                      temporal_k=tk)
+        norms, ins = res.norms, res.in_scratch
+    out_t = scrs if ins else phis
     out = np.concatenate([owned_to_host(lay, r, out_t[r]) for r in range(nranks)], axis=0)
-    return out, res.norms, lay
+    return out, norms, lay
 
 
 # --------------------------------------------------------- single sweep
@@ -803,6 +812,26 @@ def test_separate_ghost_fill_subprocess():
                        cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert " passed" in r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", [(64, 64, P.PX_BC_DIRICHLET_CC, 1, 1), (1024, 1024, P.PX_BC_PERIODIC, 10, 1),
+                                  (2048, 1536, P.PX_BC_PERIODIC, 1, 1), (1024, 768, P.PX_BC_DIRICHLET_CC, 4, 4)])
+def test_solve_async_bitwise(case):
+    """px_solve_async (no host round trip, norms to device memory) runs the
+    same solves: φ^N bit-identical to the oracle and the norms as px_solve's,
+    for the whole-box, resident, streaming and temporally blocked paths."""
+    n0, n1, bc, E, tk = case
+    h = 1.0 / max(n0, n1)
+    lam = h * h / 8
+    phi0, rho = _fields(n0, n1, tk, 31, bc)
+    N = 12
+    out, norms, _ = run_gpu_solve(n0, n1, h, lam, bc, 0, N, E, phi0, rho, g=tk, tk=tk, async_=True)
+    ref, rn = oracle.solve(_orc_problem(n0, n1, h, lam, bc, 0, N, E, g=tk), phi0, rho)
+    assert bits_equal(out, ref[tk:-tk, tk:-tk]), ulp_diff(out, ref[tk:-tk, tk:-tk])
+    _check_norms(norms, rn)
+    out2, norms2, _ = run_gpu_solve(n0, n1, h, lam, bc, 0, N, E, phi0, rho, g=tk, tk=tk)
+    assert bits_equal(out, out2) and bits_equal(norms, norms2)
 
 
 @pytest.mark.gpu
