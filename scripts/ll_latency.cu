@@ -47,6 +47,9 @@ __device__ __forceinline__ void ld2(const unsigned long long* p, unsigned long l
 //         entries polled together, __nanosleep(100) between polls, barrier
 // mode 6: mode 5 without the back-off
 // mode 8: mode 5 with each pair's two entries as ONE 32-B access (v4.u64, sm_100)
+// mode 9: plain 16-B data per pair (no tags) + one flag per warp and row: the lanes store, __syncwarp,
+//         lane 0 st.release.gpu of the round; the reader's lane 0 polls the flag (ld.acquire.gpu),
+//         __syncwarp, then every lane loads its pair (ld.relaxed.gpu)
 // mode 7: mode 5 with the pair's two entries in separate halves of the row (entries q and
 //         np + q): every warp-wide access covers whole 32-B sectors
 __global__ void k_ring(unsigned long long* mb, int rounds, int mode, int nx, long long* cycles) {
@@ -66,6 +69,42 @@ __global__ void k_ring(unsigned long long* mb, int rounds, int mode, int nx, lon
         }
       }
       if (mode == 3) __syncthreads();
+    } else if (mode == 9) {
+      const int slot = s & 1;
+      const int np = nx / 2, lane = tid & 31, warp = tid >> 5;
+      // data [slot][cta][2 rows][np pairs][2]; flags [slot][cta][2 rows][np / 32 warps] (128-B apart)
+      unsigned long long* data = mb + (size_t)slot * G * 2 * 2 * np;
+      unsigned long long* flg = mb + (size_t)2 * G * 2 * 2 * np + (size_t)slot * G * 2 * (np / 32) * 16;
+      for (int q = tid; q < np; q += nt) {
+        st2(data + ((size_t)c * 2 + 0) * 2 * np + 2 * q, tag | 1, tag | 2);
+        st2(data + ((size_t)c * 2 + 1) * 2 * np + 2 * q, tag | 1, tag | 2);
+        __syncwarp();
+        if (lane == 0) {
+          const int wq = q >> 5;
+          asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(flg + (((size_t)c * 2 + 0) * (np / 32) + wq) * 16),
+                       "l"((unsigned long long)s) : "memory");
+          asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(flg + (((size_t)c * 2 + 1) * (np / 32) + wq) * 16),
+                       "l"((unsigned long long)s) : "memory");
+        }
+      }
+      for (int q = tid; q < np; q += nt) {
+        const int wq = q >> 5;
+        if (lane == 0) {
+          const unsigned long long* fu = flg + (((size_t)up * 2 + 1) * (np / 32) + wq) * 16;
+          const unsigned long long* fd = flg + (((size_t)dn * 2 + 0) * (np / 32) + wq) * 16;
+          unsigned long long a, b;
+          do {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(a) : "l"(fu) : "memory");
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(b) : "l"(fd) : "memory");
+          } while (a != (unsigned long long)s || b != (unsigned long long)s);
+        }
+        __syncwarp();
+        unsigned long long a0, b0, a1, b1;
+        ld2(data + ((size_t)up * 2 + 1) * 2 * np + 2 * q, a0, b0);
+        ld2(data + ((size_t)dn * 2 + 0) * 2 * np + 2 * q, a1, b1);
+        if ((a0 >> 32) != (unsigned long long)s || (a1 >> 32) != (unsigned long long)s) asm volatile("trap;");
+      }
+      __syncthreads();
     } else if (mode == 8) {
       const int slot = s & 1;
       const int np = nx / 2;
@@ -164,17 +203,18 @@ int main() {
   const int nx = 1024, rounds = 2000;
   unsigned long long* mb;
   long long* cyc;
-  cudaMalloc(&mb, (size_t)2 * nsm * 8 * nx * 8 + 4096);
+  cudaMalloc(&mb, (size_t)4 * nsm * 8 * nx * 8 + 4096);
   cudaMalloc(&cyc, nsm * sizeof(long long));
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   const char* names[] = {"flag, 1 thread", "LL 512 thr", "LL 512 thr + bar", "flag + bar", "LL 2 slots", "k_resident exchange", "k_resident exchange, no back-off",
-                         "k_resident exchange, sector-contiguous entries", "k_resident exchange, 32-B pair entries"};
+                         "k_resident exchange, sector-contiguous entries", "k_resident exchange, 32-B pair entries",
+                         "plain pairs + per-warp release/acquire flag"};
   // payload sweep of the 32-B pair entries (mode 8): columns per row
   for (int cols : {1024, 512, 256, 64}) {
     for (int rep = 0; rep < 2; ++rep) {
-      cudaMemset(mb, 0, (size_t)2 * nsm * 8 * nx * 8 + 4096);
+      cudaMemset(mb, 0, (size_t)4 * nsm * 8 * nx * 8 + 4096);
       int r = rounds, m = 8, n = cols;
       void* args[] = {&mb, &r, &m, &n, &cyc};
       cudaEventRecord(e0);
@@ -187,9 +227,9 @@ int main() {
     }
   }
   for (int threads : {512, 256}) {
-    for (int mode = 0; mode < 9; ++mode) {
+    for (int mode = 0; mode < 10; ++mode) {
       for (int rep = 0; rep < 2; ++rep) {
-        cudaMemset(mb, 0, (size_t)2 * nsm * 8 * nx * 8 + 4096);
+        cudaMemset(mb, 0, (size_t)4 * nsm * 8 * nx * 8 + 4096);
         int r = rounds, m = mode, n = nx;
         void* args[] = {&mb, &r, &m, &n, &cyc};
         cudaEventRecord(e0);
