@@ -34,6 +34,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <type_traits>
 #include <cstdlib>
 
 #include "px_device.cuh"
@@ -214,11 +215,11 @@ __device__ __forceinline__ double2 ll2_val(const LL2& v) {
   return make_double2(__longlong_as_double((long long)((v.w[1] << 32) | (v.w[0] & 0xffffffffull))),
                       __longlong_as_double((long long)((v.w[3] << 32) | (v.w[2] & 0xffffffffull))));
 }
-// the n (<= 2) pair entries e[i], loads in flight together, re-polled until
+// the n (<= M) pair entries e[i], loads in flight together, re-polled until
 // every tag matches
-template <int n>
-__device__ __forceinline__ void ll_get2(const double* const (&e)[2], uint32_t tag, double2 (&out)[2]) {
-  LL2 v[2];
+template <int n, int M>
+__device__ __forceinline__ void ll_get2(const double* const (&e)[M], uint32_t tag, double2 (&out)[M]) {
+  LL2 v[M];
 #pragma unroll
   for (int i = 0; i < n; ++i) v[i] = ll_load2(e[i]);
   for (;;) {
@@ -719,45 +720,55 @@ __device__ __forceinline__ void rr_body(const ResidentLaunch& p, const RrCtx& k,
     const uint32_t tag = (uint32_t)s + 1u;
     const int slot = (s + 1) & 1;
     double* mine = k.pub + (size_t)(slot * G + c) * 2 * 2 * nx;
-    unsigned long long mx = 0ull;
-    double ss = 0.0;
-    // row R, then row 1: both published at once
-    double2 rR = make_double2(0.0, 0.0), r1;
-    const double2 nR = RR > 1 ? pair(cur[RR - 1], cur[RR], cur[RR + 1], RR, b, rR) : make_double2(0.0, 0.0);
-    const double2 n1 = pair(cur[0], cur[1], cur[2], 1, b, r1);
-    if (rec) {
-      acc(r1, mx, ss);
-      if (RR > 1) acc(rR, mx, ss);
-    }
+    // the update of the CTA's rows, compiled once with and once without the
+    // norm accumulation: no branch between the rows, so the scheduler
+    // interleaves their independent expression trees
+    auto rows = [&](auto rec_c) {
+      constexpr bool REC = decltype(rec_c)::value;
+      unsigned long long mx = 0ull;
+      double ss = 0.0;
+      // row R, then row 1: both published at once
+      double2 rR = make_double2(0.0, 0.0), r1;
+      const double2 nR = RR > 1 ? pair(cur[RR - 1], cur[RR], cur[RR + 1], RR, b, rR) : make_double2(0.0, 0.0);
+      const double2 n1 = pair(cur[0], cur[1], cur[2], 1, b, r1);
+      if (REC) {
+        acc(r1, mx, ss);
+        if (RR > 1) acc(rR, mx, ss);
+      }
 #if PX_RR_PROF
-    {  // the compute of rows R and 1 complete (consume the results)
-      if (__double_as_longlong(n1.x) == 1 && __double_as_longlong(nR.y) == 3) tp[0] += 1;
-    }
-    RR_T(6)
+      {  // the compute of rows R and 1 complete (consume the results)
+        if (__double_as_longlong(n1.x) == 1 && __double_as_longlong(nR.y) == 3) tp[0] += 1;
+      }
+      RR_T(6)
 #endif
-    // pair q of a published row = the 32-B entry at 4q (a warp writes 1 KB contiguously)
-    if (k.act) {
-      if (k.top_x) ll_put2(mine + 2 * x, n1, tag);
-      if (k.bot_x) ll_put2(mine + 2 * nx + 2 * x, RR > 1 ? nR : n1, tag);
-    }
-    RR_T(0)
-    // rows 2..R-1 in place; `prev` = the old row above
-    double2 prev = cur[1];
+      // pair q of a published row = the 32-B entry at 4q (a warp writes 1 KB contiguously)
+      if (k.act) {
+        if (k.top_x) ll_put2(mine + 2 * x, n1, tag);
+        if (k.bot_x) ll_put2(mine + 2 * nx + 2 * x, RR > 1 ? nR : n1, tag);
+      }
+      RR_T(0)
+      // rows 2..R-1 from the old iterate (written back after the last of them)
+      double2 o[RR > 2 ? RR - 2 : 1];
 #pragma unroll
-    for (int r = 2; r < RR; ++r) {
-      double2 res;
-      const double2 o = pair(prev, cur[r], cur[r + 1], r, b, res);
-      if (rec) acc(res, mx, ss);
-      prev = cur[r];
-      cur[r] = o;
-    }
-    cur[1] = n1;
-    if (RR > 1) cur[RR] = nR;
-    RR_T(1)
-    if (rec) {
-      rs_block_reduce(mx, ss, k.part + ((size_t)entry * G + c) * 2);
-      ++entry;
-    }
+      for (int r = 2; r < RR; ++r) {
+        double2 res;
+        o[r - 2] = pair(cur[r - 1], cur[r], cur[r + 1], r, b, res);
+        if (REC) acc(res, mx, ss);
+      }
+#pragma unroll
+      for (int r = 2; r < RR; ++r) cur[r] = o[r - 2];
+      cur[1] = n1;
+      if (RR > 1) cur[RR] = nR;
+      RR_T(1)
+      if (REC) {
+        rs_block_reduce(mx, ss, k.part + ((size_t)entry * G + c) * 2);
+        ++entry;
+      }
+    };
+    if (rec)
+      rows(std::true_type{});
+    else
+      rows(std::false_type{});
     RR_T(2)
     // halo rows of φ^{s+1}
     if (k.act && (k.top_x || k.bot_x)) {
@@ -848,7 +859,7 @@ __device__ __forceinline__ void rr_setup(const ResidentLaunch& p, RrCtx& k, doub
   const int y0 = (int)((int64_t)c * p.ny / G), y1 = (int)((int64_t)(c + 1) * p.ny / G), R = y1 - y0;
   double* F = sm;
   k.F = F;
-  k.eL = F + (size_t)p.rmax * nx;
+  k.eL = F + (size_t)(p.rmax + 2 * (H - 1)) * nx;
   k.eR = k.eL + 2 * BS;
   k.gW = k.eR + 2 * BS;
   k.gE = k.gW + 2 * RE;
@@ -901,8 +912,14 @@ __device__ __forceinline__ void rr_setup(const ResidentLaunch& p, RrCtx& k, doub
     k.ebs = BS;
     k.eld = true;
   }
-  for (int r = 0; r < R; ++r)
-    for (int i = tid; i < nx; i += RS_THREADS) F[(size_t)r * nx + i] = p.rhs[(int64_t)(y0 + r) * p.ld_rhs + i];
+  // ρ of the owned rows, and with H = 2 also of the inner halo rows (level 1
+  // updates them): F row r = global row y0 - (H-1) + r (periodic wrap; rows
+  // outside a non-periodic domain are never used)
+  for (int r = 0; r < R + 2 * (H - 1); ++r) {
+    int y = y0 - (H - 1) + r;
+    y = y < 0 ? y + p.ny : (y >= p.ny ? y - p.ny : y);
+    for (int i = tid; i < nx; i += RS_THREADS) F[(size_t)r * nx + i] = p.rhs[(int64_t)y * p.ld_rhs + i];
+  }
   if (tid < RE) {  // fixed ghost columns of slots 0 .. R+2H-1 (both buffers)
     const int y = y0 - H + tid;
     const bool ok = tid < R + 2 * H && y >= -1 && y <= p.ny;
@@ -949,7 +966,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resident_reg(const ResidentLa
 // updates per pass.  An odd sweep count ends with a one-level pass.  φ and
 // the max-norm bit-identical to k_resident; the per-thread Σr² order is row
 // order (within the oracle tolerance, not bitwise equal to k_resident's).
-template <int ST, int RR>
+template <int ST, int RR, bool P2>
 __device__ __forceinline__ void rr2_body(const ResidentLaunch& p, const RrCtx& k, cg::grid_group& grid) {
   constexpr int NWP = RS_THREADS / 32, RE = RR_RM + 4, BS = NWP * RE, NI = RR + 4;  // i = row + 1
   const int tid = threadIdx.x, nx = k.nx, x = k.x, G = k.G, c = k.c;
@@ -999,21 +1016,21 @@ __device__ __forceinline__ void rr2_body(const ResidentLaunch& p, const RrCtx& k
       nw = west(N, i + 1, b);
       ne = east(N, i + 1, b);
     }
-    const double L0 = rs_taps<ST>(cw, C.y, S.x, N.x, C.x, sw, S.y, nw, N.y);
-    const double L1 = rs_taps<ST>(C.x, ce, S.y, N.y, C.y, S.x, se, N.x, ne);
-    // ρ of row i-1: owned rows from shared memory, halo rows from L2 (wrapped)
-    double2 f;
-    if (i >= 2 && i <= RR + 1) {
-      f = *reinterpret_cast<const double2*>(k.F + (size_t)(i - 2) * nx + k.xs);
+    const double2 f = *reinterpret_cast<const double2*>(k.F + (size_t)(i - 1) * nx + k.xs);  // ρ of row i-1
+    double2 o;
+    if (P2) {  // as k_resident_reg
+      const double L0 = fma(-4.0, C.x, __dadd_rn(__dadd_rn(__dadd_rn(cw, C.y), S.x), N.x));
+      const double L1 = fma(-4.0, C.y, __dadd_rn(__dadd_rn(__dadd_rn(C.x, ce), S.y), N.y));
+      res.x = fma(p.scale, L0, -f.x);
+      res.y = fma(p.scale, L1, -f.y);
+      o = make_double2(fma(p.lambda, res.x, C.x), fma(p.lambda, res.y, C.y));
     } else {
-      int y = y0 + i - 2;
-      y = y < 0 ? y + p.ny : (y >= p.ny ? y - p.ny : y);  // only reached for neighbour rows
-      f = __ldg(reinterpret_cast<const double2*>(p.rhs + (int64_t)y * p.ld_rhs + k.xs));
+      const double L0 = rs_taps<ST>(cw, C.y, S.x, N.x, C.x, sw, S.y, nw, N.y);
+      const double L1 = rs_taps<ST>(C.x, ce, S.y, N.y, C.y, S.x, se, N.x, ne);
+      res.x = __dsub_rn(__dmul_rn(p.scale, L0), f.x);
+      res.y = __dsub_rn(__dmul_rn(p.scale, L1), f.y);
+      o = make_double2(__dadd_rn(C.x, __dmul_rn(p.lambda, res.x)), __dadd_rn(C.y, __dmul_rn(p.lambda, res.y)));
     }
-    res.x = __dsub_rn(__dmul_rn(p.scale, L0), f.x);
-    res.y = __dsub_rn(__dmul_rn(p.scale, L1), f.y);
-    const double2 o = make_double2(__dadd_rn(C.x, __dmul_rn(p.lambda, res.x)),
-                                   __dadd_rn(C.y, __dmul_rn(p.lambda, res.y)));
     if (!k.act) res = make_double2(0.0, 0.0);
     return o;
   };
@@ -1038,19 +1055,16 @@ __device__ __forceinline__ void rr2_body(const ResidentLaunch& p, const RrCtx& k
     const int slot = (pass + 1) & 1;
     double* mine = k.pub + (size_t)(slot * G + c) * 2 * 2 * 2 * nx;  // [side][row][2 nx]
     // rows 1, 2 (f0, f1) to the first side, rows R-1, R (l0, l1) to the last
+    // (a pair as one 32-B LL entry at 4q = 2x doubles of its row)
     auto publish = [&](double2 f0, double2 f1, double2 l0, double2 l1) {
       if (k.act) {
         if (k.top_x) {
-          ll_put(mine + x, f0.x, tag);
-          ll_put(mine + x + nx, f0.y, tag);
-          ll_put(mine + 2 * nx + x, f1.x, tag);
-          ll_put(mine + 3 * nx + x, f1.y, tag);
+          ll_put2(mine + 2 * x, f0, tag);
+          ll_put2(mine + 2 * nx + 2 * x, f1, tag);
         }
         if (k.bot_x) {
-          ll_put(mine + 4 * nx + x, l0.x, tag);
-          ll_put(mine + 5 * nx + x, l0.y, tag);
-          ll_put(mine + 6 * nx + x, l1.x, tag);
-          ll_put(mine + 7 * nx + x, l1.y, tag);
+          ll_put2(mine + 4 * nx + 2 * x, l0, tag);
+          ll_put2(mine + 6 * nx + 2 * x, l1, tag);
         }
       }
     };
@@ -1130,25 +1144,24 @@ __device__ __forceinline__ void rr2_body(const ResidentLaunch& p, const RrCtx& k
       const double* fu = k.pub + ((size_t)(slot * G + k.up) * 2 + 1) * 2 * 2 * nx;  // up's last rows
       const double* fd = k.pub + ((size_t)(slot * G + k.dn) * 2) * 2 * 2 * nx;      // dn's first rows
       if (k.top_x && k.bot_x) {
-        const double* const e[8] = {fu, fu + nx, fu + 2 * nx, fu + 3 * nx, fd, fd + nx, fd + 2 * nx, fd + 3 * nx};
-        const double* const ex[8] = {e[0] + x, e[1] + x, e[2] + x, e[3] + x, e[4] + x, e[5] + x, e[6] + x, e[7] + x};
-        double v[8];
-        ll_get<8>(ex, tag, v);
-        cur[0] = make_double2(v[0], v[1]);
-        cur[1] = make_double2(v[2], v[3]);
-        cur[RR + 2] = make_double2(v[4], v[5]);
-        cur[RR + 3] = make_double2(v[6], v[7]);
+        const double* const e[4] = {fu + 2 * x, fu + 2 * nx + 2 * x, fd + 2 * x, fd + 2 * nx + 2 * x};
+        double2 v[4];
+        ll_get2<4>(e, tag, v);
+        cur[0] = v[0];
+        cur[1] = v[1];
+        cur[RR + 2] = v[2];
+        cur[RR + 3] = v[3];
       } else {
         const double* f = k.top_x ? fu : fd;
-        const double* const ex[4] = {f + x, f + nx + x, f + 2 * nx + x, f + 3 * nx + x};
-        double v[4];
-        ll_get<4>(ex, tag, v);
+        const double* const e[2] = {f + 2 * x, f + 2 * nx + 2 * x};
+        double2 v[2];
+        ll_get2<2>(e, tag, v);
         if (k.top_x) {
-          cur[0] = make_double2(v[0], v[1]);
-          cur[1] = make_double2(v[2], v[3]);
+          cur[0] = v[0];
+          cur[1] = v[1];
         } else {
-          cur[RR + 2] = make_double2(v[0], v[1]);
-          cur[RR + 3] = make_double2(v[2], v[3]);
+          cur[RR + 2] = v[0];
+          cur[RR + 3] = v[1];
         }
       }
     }
@@ -1200,7 +1213,7 @@ __device__ __forceinline__ void rr2_body(const ResidentLaunch& p, const RrCtx& k
   }
 }
 
-template <int ST>
+template <int ST, bool P2>
 __global__ void __launch_bounds__(RS_THREADS, 1) k_resident_reg2(const ResidentLaunch p) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double sm[];
@@ -1208,12 +1221,12 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resident_reg2(const ResidentL
   rr_setup<RR_RM + 4, 2>(p, k, sm);
   const int R = (int)((int64_t)(blockIdx.x + 1) * p.ny / gridDim.x) - (int)((int64_t)blockIdx.x * p.ny / gridDim.x);
   switch (R) {
-    case 2: rr2_body<ST, 2>(p, k, grid); break;
-    case 3: rr2_body<ST, 3>(p, k, grid); break;
-    case 4: rr2_body<ST, 4>(p, k, grid); break;
-    case 5: rr2_body<ST, 5>(p, k, grid); break;
-    case 6: rr2_body<ST, 6>(p, k, grid); break;
-    default: rr2_body<ST, 7>(p, k, grid); break;
+    case 2: rr2_body<ST, 2, P2>(p, k, grid); break;
+    case 3: rr2_body<ST, 3, P2>(p, k, grid); break;
+    case 4: rr2_body<ST, 4, P2>(p, k, grid); break;
+    case 5: rr2_body<ST, 5, P2>(p, k, grid); break;
+    case 6: rr2_body<ST, 6, P2>(p, k, grid); break;
+    default: rr2_body<ST, 7, P2>(p, k, grid); break;
   }
 }
 
@@ -1545,14 +1558,17 @@ px_status launch_resident(int stencil, const ResidentLaunch& r_in, int grid, siz
   const bool reg2 = reg && rs_reg_env() == 2 && r.ny / grid >= 2;
   if (reg2) {
     constexpr int RE = RR_RM + 4;
-    smem = ((size_t)r.rmax * r.nx + 2 * 2 * (RS_THREADS / 32) * RE + 4 * RE) * sizeof(double);
-    static size_t reg2_set[2] = {};
+    smem = ((size_t)(r.rmax + 2) * r.nx + 2 * 2 * (RS_THREADS / 32) * RE + 4 * RE) * sizeof(double);
+    static size_t reg2_set[3] = {};
     if (k) {
-      e = rs_attr(k_resident_reg2<1>, smem, reg2_set[1]);
-      fn = (void*)k_resident_reg2<1>;
+      e = rs_attr(k_resident_reg2<1, false>, smem, reg2_set[1]);
+      fn = (void*)k_resident_reg2<1, false>;
+    } else if (rs_pow2(r.scale) && rs_pow2(r.lambda)) {
+      e = rs_attr(k_resident_reg2<0, true>, smem, reg2_set[2]);
+      fn = (void*)k_resident_reg2<0, true>;
     } else {
-      e = rs_attr(k_resident_reg2<0>, smem, reg2_set[0]);
-      fn = (void*)k_resident_reg2<0>;
+      e = rs_attr(k_resident_reg2<0, false>, smem, reg2_set[0]);
+      fn = (void*)k_resident_reg2<0, false>;
     }
   } else if (reg) {
     // ρ rows + edge arrays + fixed ghost columns (k_resident_reg's shared layout)

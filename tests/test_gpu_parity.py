@@ -868,7 +868,8 @@ def test_resident_temporal_blocking_variant_subprocess(var):
     for k in (var[1],):
         env = dict(os.environ, **{var[0]: k})
         r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-m", "gpu",
-                            "tests/test_gpu_parity.py", "-k", "resident_shapes or config2_full"],
+                            "tests/test_gpu_parity.py", "-k",
+                            "resident_shapes or config2_full or resident_reg_general or solve_async"],
                            cwd=root, env=env, capture_output=True, text=True, timeout=900)
         assert r.returncode == 0, (k, r.stdout[-3000:] + r.stderr[-2000:])
 
