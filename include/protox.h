@@ -89,6 +89,11 @@ px_status px_box_ordinal(px_box b, px_point p, int64_t* out);
  *   FIXED_GHOSTS  ghost cells outside Ω belong to the caller and are never
  *                 written (inter-rank ghosts are still exchanged). */
 typedef enum { PX_BC_PERIODIC = 0, PX_BC_DIRICHLET_CC = 1, PX_BC_FIXED_GHOSTS = 2 } px_bc;
+/* Partitions: slabs only.  SURVEY §8(b) sketches PX_PART_TILES (a 2D grid of
+ * ranks); §8(e) makes tiles optional and it is not built: with ≤ 8 GPUs a
+ * slab's two halo rows are contiguous (one 16-B-vector push per row inside
+ * the sweep kernel), and the halo per rank at P = 8 over 16384² is 2 × 131 KB
+ * per sweep, < 0.1 % of the sweep's HBM bytes. */
 typedef enum { PX_PART_SLABS = 0 } px_partition;
 typedef struct px_layout px_layout; /* opaque, library-owned */
 
