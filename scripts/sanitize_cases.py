@@ -84,6 +84,22 @@ def push_solve(n0, n1, N=5, E=1, st=0):
     comm.close()
 
 
+def reg2_solve():
+    os.environ["PROTOX_RESIDENT_REG"] = "2"  # read once per process: this case runs alone
+    solve(1024, 1024, N=5, E=2)
+
+
+def async_solve(n0, n1, N=6, E=2):
+    lay = P.Layout(P.box(0, 0, n0 - 1, n1 - 1), (n0, n1), 1, P.PX_BC_PERIODIC, 1)
+    a, b, r = fields(lay)
+    d = torch.zeros(2 * (N // E + 2), dtype=torch.float64, device="cuda")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    P.solve_async(lay, None, 0, P.relax_params(1.0 / n0, (1.0 / n0) ** 2 / 8), N, E, lay.patch(0, a),
+                  lay.patch(0, b), lay.patch(0, r), d, use_graph=True, stream=s)
+    s.synchronize()
+
+
 def other():
     lay = P.Layout(P.box(0, 0, 199, 99), (200, 100), 1, P.PX_BC_DIRICHLET_CC, 1)
     a, b, r = fields(lay)
@@ -106,6 +122,11 @@ if __name__ == "__main__":
         "bulk_relax9": lambda: relax(2050, 2048, st=1),
         "tb_relax_block": lambda: relax(1000, 300, g=4, k=4),
         "smallbox_solve": lambda: solve(64, 64, bc=P.PX_BC_DIRICHLET_CC),
+        "boxw_fixed9_solve": lambda: solve(62, 52, st=1, bc=P.PX_BC_FIXED_GHOSTS),
+        "resident_reg_solve": lambda: solve(1024, 1024, N=5, E=2),
+        "resident_reg_dirichlet_solve": lambda: solve(1000, 700, N=5, E=2, bc=P.PX_BC_DIRICHLET_CC),
+        "resident_reg2_solve": reg2_solve,
+        "async_solve": lambda: async_solve(1024, 1024),
         "persist_solve": lambda: solve(600, 90, st=1),
         "local_multipart_solve": lambda: solve(256, 150, nranks=3, bc=P.PX_BC_FIXED_GHOSTS),
         "tb_solve": lambda: solve(1000, 300, nranks=3, g=4, tk=4, N=9, E=3),
