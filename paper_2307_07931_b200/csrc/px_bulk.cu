@@ -208,8 +208,9 @@ __global__ void __launch_bounds__(NC * 32 + 32, CPS) k_bulk(const StreamLaunch a
           mbar_arrive_expect_tx(&full[slot], bytes);
           for (int i = 0; i < R; ++i) {
             const int yf = t.y0 - 1 + st * R + i;
+            const int yw = a.wrap ? (yf < 0 ? yf + a.ny : (yf >= a.ny ? yf - a.ny : yf)) : yf;  // periodic image
             if (yf <= t.y1)
-              bulk_g2s(sp + i * W, a.src + (int64_t)yf * a.ld_src + t.c, rowbytes, &full[slot], pol);
+              bulk_g2s(sp + i * W, a.src + (int64_t)yw * a.ld_src + t.c, rowbytes, &full[slot], pol);
             const int yr = yf - 1;
             if ((MODE == MODE_RELAX || MODE == MODE_RESID) && yr >= t.y0 && yr < t.y1)
               bulk_g2s(sp + (R + i) * W, a.rhs + (int64_t)yr * a.ld_rhs + t.c, rowbytes, &full[slot], pol);
@@ -238,9 +239,16 @@ __global__ void __launch_bounds__(NC * 32 + 32, CPS) k_bulk(const StreamLaunch a
         hw_next[i] = 0.0;
         he_next[i] = 0.0;
         if (yf <= t.y1) {
-          const double* row = a.src + (int64_t)yf * a.ld_src;
-          if (L && t.c - 1 >= a.src_x0) hw_next[i] = row[t.c - 1];
-          if (Rt && t.c + t.w <= a.src_x1) he_next[i] = row[t.c + t.w];
+          if (a.wrap) {  // periodic images of row and column
+            const int yw = yf < 0 ? yf + a.ny : (yf >= a.ny ? yf - a.ny : yf);
+            const double* row = a.src + (int64_t)yw * a.ld_src;
+            if (L) hw_next[i] = row[t.c == 0 ? a.nx - 1 : t.c - 1];
+            if (Rt) he_next[i] = row[t.c + t.w == a.nx ? 0 : t.c + t.w];
+          } else {
+            const double* row = a.src + (int64_t)yf * a.ld_src;
+            if (L && t.c - 1 >= a.src_x0) hw_next[i] = row[t.c - 1];
+            if (Rt && t.c + t.w <= a.src_x1) he_next[i] = row[t.c + t.w];
+          }
         }
       }
     };

@@ -131,6 +131,9 @@ struct StreamLaunch {
   NormSlot norms;     // norms.out_max == null: none
   PushSpec ps;        // fused halo push / wait (k_bulk only)
   int32_t pdl;        // launch as a programmatic dependent of the previous kernel (k_bulk only)
+  int32_t wrap;       // k_bulk only: the region is a whole periodic single-rank domain -- φ rows -1 / ny
+                      // and columns -1 / nx are read from rows ny-1 / 0 and columns nx-1 / 0 (the
+                      // ghost ring is not read, so no images or ghost fill are needed per sweep)
 };
 
 // Extra launch state of a temporal-blocking pass (px_tb.cu).

@@ -483,6 +483,22 @@ static px_status push_init(const SolveCtx& x, const px_local_info& li) {
   return launch_push_init(pi, x.s);
 }
 
+// PROTOX_WRAP=1 (A/B, read once): periodic single-rank sweeps on the TMA
+// kernel read the periodic images of their boundary rows / columns in place
+// (no images, no ghost fill per sweep).  Off by default: measured at BJ.C3
+// (scripts/c3_wrap_ab.sh) 248.6-250.8 vs 251.2-251.4
+// Gcell-updates/s with the fill kernels between the sweeps, with or without
+// programmatic dependent launches -- the back-to-back chain of sweep grids
+// costs more than the two small fill launches it removes.
+static bool wrap_enabled() {
+  static int w = -1;
+  if (w < 0) {
+    const char* e = getenv("PROTOX_WRAP");
+    w = (e && e[0] == '1') ? 1 : 0;
+  }
+  return w == 1;
+}
+
 // Slab size (cells) from which a k = 1 sweep fills its ghost ring with a
 // separate kernel instead of fused images (PROTOX_SEP_FILL_CELLS, read once:
 // tests lower it to reach the path at small sizes).
@@ -691,6 +707,8 @@ static px_status enqueue_solve(const SolveCtx& x) {
   // (the push path too: its pushed rows carry their corner images themselves)
   const bool sep_fill = ((!x.c && x.nparts == 1 && x.l->nranks == 1) || p2p) &&
                         (int64_t)ext(pli.owned, 0) * ext(pli.owned, 1) >= sep_fill_cells();
+  const bool wrap_ok = !x.c && x.nparts == 1 && x.l->nranks == 1 && x.l->bc == PX_BC_PERIODIC && wrap_enabled();
+  bool any_wrap = false;
   for (; it < N; ++it) {
     const int32_t slot = (E > 0 && it % E == 0) ? it / E : -1;
     std::vector<SweepLaunch> v;
@@ -733,9 +751,19 @@ static px_status enqueue_solve(const SolveCtx& x) {
       if (split) PX_TRY(launch_stream(MODE_RELAX, x.p->stencil, v[2].a, x.s));
       PX_TRY(cuda_check(cudaStreamWaitEvent(x.s, plan->ev_comm, 0), "stream wait"));
     } else {
-      if (sep_fill) v[0].a.gs.g = 0;
+      // a whole periodic single-rank domain on the TMA kernel reads the
+      // periodic images of its boundary rows / columns straight from the
+      // interior: no images written, no ghost fill per sweep
+      const bool wr = wrap_ok && v.size() == 1 && bulk_eligible(MODE_RELAX, v[0].a);
+      if (wr) {
+        v[0].a.wrap = 1;
+        v[0].a.gs.g = 0;
+        any_wrap = true;
+      } else if (sep_fill) {
+        v[0].a.gs.g = 0;
+      }
       for (auto& sl : v) PX_TRY(launch_stream(MODE_RELAX, x.p->stencil, sl.a, x.s));
-      if (sep_fill) PX_TRY(launch_fill_ghosts(x.l, 0, nxt[0], x.s));
+      if (sep_fill && !wr) PX_TRY(launch_fill_ghosts(x.l, 0, nxt[0], x.s));
       if (x.nparts > 1) PX_TRY(local_rows(x.l, nxt, x.s));
     }
     std::swap(cur, nxt);
@@ -747,6 +775,9 @@ static px_status enqueue_solve(const SolveCtx& x) {
     w.rel = 1;  // publish the last sweep's pushes
     PX_TRY(launch_wait(w, x.s));
   }
+  // φ^N leaves with its ghost ring filled, as the fused-image sweeps leave it
+  // (and the final residual pass reads it)
+  if (any_wrap) PX_TRY(launch_fill_ghosts(x.l, 0, cur[0], x.s));
   if (E >= 0) {
     std::vector<SweepLaunch> v;
     for (int32_t part = 0; part < x.nparts; ++part)

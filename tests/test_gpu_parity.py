@@ -854,7 +854,8 @@ def test_solve_resident_reg_general_h_lambda(shape, bc):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("var", [("PROTOX_RESIDENT_K", "2"), ("PROTOX_RESIDENT_K", "3"),
-                                 ("PROTOX_RESIDENT_REG", "0"), ("PROTOX_RESIDENT_REG", "2")])
+                                 ("PROTOX_RESIDENT_REG", "0"), ("PROTOX_RESIDENT_REG", "2"),
+                                 ("PROTOX_WRAP", "1")])
 def test_resident_temporal_blocking_variant_subprocess(var):
     """The resident-solve variants (read once per process) stay bit-identical:
     the shared-memory temporally blocked kernel (PROTOX_RESIDENT_K=2,3), the
@@ -869,7 +870,8 @@ def test_resident_temporal_blocking_variant_subprocess(var):
         env = dict(os.environ, **{var[0]: k})
         r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-m", "gpu",
                             "tests/test_gpu_parity.py", "-k",
-                            "resident_shapes or config2_full or resident_reg_general or solve_async"],
+                            "resident_shapes or config2_full or resident_reg_general or solve_async or "
+                            "solve_bulk_kernel"],
                            cwd=root, env=env, capture_output=True, text=True, timeout=900)
         assert r.returncode == 0, (k, r.stdout[-3000:] + r.stderr[-2000:])
 
