@@ -42,13 +42,10 @@ constexpr size_t smem_bytes() {
 using namespace ptx;
 
 // ---- fused halo push over peer memory (PushSpec, px_internal.h) ----
-// spin until own arrival counter `side` reaches base + wcount (acquire, system scope)
+// spin until own arrival counter `side` reaches base + wcount (acquire, system
+// scope; bounded: px_spin_until)
 __device__ __forceinline__ void ps_wait(const PushSpec& ps, int side) {
-  const unsigned long long target = *ps.epoch + ps.wcount;
-  unsigned long long v;
-  do {
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(ps.wflag[side]) : "memory");
-  } while (v < target);
+  px_spin_until(ps.wflag[side], *ps.epoch + ps.wcount, ps.err);
 }
 // The pair (x, x+1) of a row pushed into the neighbour's ghost row rp, with
 // the x images of the pair's cells at the domain's x faces (corners).  Rare

@@ -152,4 +152,36 @@ __device__ __forceinline__ double rs_taps(double w, double e, double s, double n
   return __dadd_rn(q, __dmul_rn(-20.0, c));
 }
 
+// Bounded spin for the cross-process waits of the peer-memory path: wait
+// until *flag >= target (acquire, system scope); give up after
+// PX_SPIN_TIMEOUT_NS of %globaltimer, or at once when an earlier wait of the
+// communicator already gave up, and count it in *err (the synchronous solve
+// reports PX_ERR_STATE; the bench's start-up self-check then falls back to
+// NCCL).  A lost peer therefore ends the solve with an error, not a hang.
+#ifndef PX_SPIN_TIMEOUT_NS
+#define PX_SPIN_TIMEOUT_NS 2000000000ull
+#endif
+__device__ __forceinline__ unsigned long long px_globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void px_spin_until(const unsigned long long* flag, unsigned long long target,
+                                              unsigned long long* err) {
+  unsigned long long v, t0 = 0;
+  for (unsigned it = 0;; ++it) {
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+    if (v >= target) return;
+    if ((it & 1023u) == 0u && err) {
+      const unsigned long long t = px_globaltimer();
+      if (it == 0) {
+        t0 = t;
+      } else if (t - t0 > PX_SPIN_TIMEOUT_NS || *(volatile unsigned long long*)err) {
+        atomicAdd(err, 1ull);
+        return;
+      }
+    }
+  }
+}
+
 }  // namespace px

@@ -116,6 +116,7 @@ struct PushSpec {
   int32_t on;                      // any push / wait: boundary chunks are scheduled first
   int32_t rel;                     // publish the previous sweep's pushes (CTA 0, at kernel start)
   int32_t xg, xn0, xm0, xm1;       // x images of pushed cells (corners): depth, owned width, lo/hi modes
+  unsigned long long* err;         // own timed-out-wait counter (px_spin_until)
 };
 
 struct StreamLaunch {
@@ -241,6 +242,7 @@ struct PeerAllreduce {
   unsigned long long* own_arrive;
   unsigned long long* own_done;
   unsigned long long* round;                 // own round counter
+  unsigned long long* err;                   // own timed-out-wait counter (px_spin_until)
 };
 px_status launch_peer_allreduce(const PeerAllreduce& ar, cudaStream_t s);
 px_status launch_epoch_bump(unsigned long long* epoch, unsigned long long per_solve, cudaStream_t s);

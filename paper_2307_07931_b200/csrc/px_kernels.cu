@@ -398,13 +398,6 @@ px_status launch_stream(int mode, int stencil, const StreamLaunch& a, cudaStream
 int32_t stream_launch_blocks_ldg(const StreamLaunch& a) { return ldg_blocks(a.nx, a.ny, a.phase); }
 
 // ---- fused halo push over peer memory: per-solve helpers (px_solve P2P mode)
-__device__ __forceinline__ void spin_until(const unsigned long long* flag, unsigned long long target) {
-  unsigned long long v;
-  do {
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
-  } while (v < target);
-}
-
 __global__ void k_wait(const PushSpec ps) {
   if (ps.rel)  // the previous kernel (the last sweep) has completed: its pushes are performed
     for (int side = 0; side < 2; ++side)
@@ -412,7 +405,7 @@ __global__ void k_wait(const PushSpec ps) {
         asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(ps.rflag[side]), "l"(1ull) : "memory");
   const unsigned long long target = *ps.epoch + ps.wcount;
   for (int side = 0; side < 2; ++side)
-    if (ps.wflag[side]) spin_until(ps.wflag[side], target);
+    if (ps.wflag[side]) px_spin_until(ps.wflag[side], target, ps.err);
 }
 // e[0] = arrival base of this solve, e[1] = arrivals per side of the previous
 // solve: every solve adds its own count, so solves of different lengths mix.
@@ -463,7 +456,7 @@ __global__ void __launch_bounds__(256) k_peer_allreduce(const PeerAllreduce ar) 
       for (int p = 0; p < P; ++p)
         if (p != ar.rank)
           asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(ar.arrive[p]), "l"(1ull) : "memory");
-      spin_until(ar.own_arrive, q * (unsigned long long)(P - 1));
+      px_spin_until(ar.own_arrive, q * (unsigned long long)(P - 1), ar.err);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < m; i += blockDim.x) {
@@ -486,7 +479,7 @@ __global__ void __launch_bounds__(256) k_peer_allreduce(const PeerAllreduce ar) 
       for (int p = 0; p < P; ++p)
         if (p != ar.rank)
           asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(ar.done[p]), "l"(1ull) : "memory");
-      spin_until(ar.own_done, q * (unsigned long long)(P - 1));
+      px_spin_until(ar.own_done, q * (unsigned long long)(P - 1), ar.err);
     }
     __syncthreads();
   }

@@ -44,6 +44,7 @@ enum : int {
   CTL_AR_ARRIVE = 4,  // peer norm all-reduce: mailboxes published by peers
   CTL_AR_DONE = 5,    //   mailboxes read by peers
   CTL_AR_ROUND = 6,   //   own round counter
+  CTL_TIMEOUT = 7,    // waits of this rank that gave up (px_spin_until): the communicator is broken
   CTL_MBOX = 8,       // mailbox: 2 * PX_MBOX_ENTRIES doubles
 };
 static constexpr size_t CTL_BYTES = (CTL_MBOX + 2 * px::PX_MBOX_ENTRIES) * sizeof(unsigned long long);
@@ -425,6 +426,7 @@ static px_status peer_allreduce(const px_comm* c, double* d_max, double* d_sum, 
   ar.own_arrive = st.ctl + CTL_AR_ARRIVE;
   ar.own_done = st.ctl + CTL_AR_DONE;
   ar.round = st.ctl + CTL_AR_ROUND;
+  ar.err = st.ctl + CTL_TIMEOUT;
   return launch_peer_allreduce(ar, s);
 }
 
@@ -681,6 +683,7 @@ static px_status enqueue_solve(const SolveCtx& x) {
     ps.on = 1;
     ps.g = x.l->ghost;
     ps.epoch = st.ctl + CTL_EPOCH;
+    ps.err = st.ctl + CTL_TIMEOUT;
     const GhostSpec gsp = ghost_spec(x.l, pli, pli.owned, false);  // x images of the pushed rows
     ps.xg = gsp.g;
     ps.xn0 = gsp.n[0];
@@ -1277,6 +1280,11 @@ px_status px_solve(const px_layout* l, px_comm* c, int32_t rank, const px_relax_
     }
   }
   PX_TRY(cuda_check(cudaStreamSynchronize(s), "solve"));
+  if (c && c->p2p.enabled) {  // a peer wait that gave up (lost or stalled peer): report, do not hang
+    unsigned long long to = 0;
+    PX_TRY(cuda_check(cudaMemcpy(&to, c->p2p.ctl + CTL_TIMEOUT, sizeof to, cudaMemcpyDeviceToHost), "timeout flag"));
+    if (to) return fail(PX_ERR_STATE, "peer-memory halo wait timed out (%llu waits): a peer is lost or stalled", to);
+  }
   if (c && c->nccl) {
     ncclResult_t ar;
     ncclCommGetAsyncError(c->nccl, &ar);

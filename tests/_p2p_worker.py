@@ -62,6 +62,20 @@ def main():
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
     torch.cuda.synchronize()
+    if os.environ.get("PROTOX_TEST_LOST_PEER") == "1":
+        # rank 1 never solves: rank 0's waits for its pushes must give up
+        # (px_spin_until) and px_solve report PX_ERR_STATE instead of hanging
+        import time
+        msg, t0 = "", time.time()
+        if rank == 0:
+            try:
+                P.solve(lay, comm, rank, prm, na, E, pa, pb, pr, use_graph=bool(graph), stream=s)
+            except P.PxError as e:
+                msg = str(e)
+        np.savez(os.path.join(out, f"rank{rank}.npz"), msg=np.array(msg), secs=time.time() - t0)
+        dist.barrier()
+        dist.destroy_process_group()
+        return
     r1 = P.solve(lay, comm, rank, prm, na, E, pa, pb, pr, use_graph=bool(graph), stream=s)
     k1 = P.last_solve_kernels()
     # continue from φ^na wherever it is (the registered pair in swapped order)

@@ -128,3 +128,15 @@ def test_p2p_inf_nan_through_peer_allreduce(tmp_path):
     assert np.array_equal(np.isnan(gn[:, 0]), np.isnan(rn[:, 0])), (gn[:, 0], rn[:, 0])
     assert np.isnan(gn[1:, 0]).all()
     assert np.array_equal(np.isnan(gn[:, 1]), np.isnan(rn[:, 1]))
+
+
+def test_p2p_lost_peer_reports_instead_of_hanging(tmp_path):
+    """A rank whose neighbour never runs its solve: the bounded peer waits
+    (px_spin_until, %globaltimer) give up after PX_SPIN_TIMEOUT_NS and
+    px_solve returns PX_ERR_STATE ('timed out') within seconds -- a lost or
+    stalled peer ends the solve with an error, not a GPU hang."""
+    res = _run(tmp_path, 2, P.PX_BC_PERIODIC, 384, 192, 4, 1, 1, 5, 0, 0,
+               extra_env={"PROTOX_TEST_LOST_PEER": "1"})
+    assert "timed out" in str(res[0]["msg"]), str(res[0]["msg"])
+    assert float(res[0]["secs"]) < 60.0
+
