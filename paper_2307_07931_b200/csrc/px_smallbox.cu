@@ -383,6 +383,7 @@ static bool box1_eligible(const SmallBox& b) {
 // butterfly (the norm is recorded every sweep at BJ.C1).
 constexpr int BW_THREADS = 512;  // 16 warps: 128 registers a thread, up to 4 rows of φ, ρ in registers
 constexpr int BW_WARPS = BW_THREADS / 32;
+constexpr int BW_CL_DEFAULT = 8;  // 64² (BJ.C1): 1 / 2 / 4 / 8 CTAs 1.14 / 1.26 / 0.955 / 0.89 µs per sweep
 // rows per warp (1, 2 or 4) of an nx x ny box; 0: not eligible
 static int bw_rows_per_warp(int nx, int ny) {
   if (nx < 2 || nx > 64 || (nx & 1) || ny < 1) return 0;
@@ -390,17 +391,48 @@ static int bw_rows_per_warp(int nx, int ny) {
     if (ny <= BW_WARPS * rw && ny % rw == 0) return rw;
   return 0;
 }
-template <int ST, bool P2, int RW>
+// CL > 1: the box over a cluster of CL CTAs (CTA rank cr owns rows cr·ny/CL ..),
+// each keeping a full-height row board; a row another CTA reads (the CTA's
+// first / last row, the periodic y images) is also stored into that CTA's
+// board through DSMEM, and the per-sweep barrier is the cluster barrier.
+__device__ __forceinline__ unsigned bw_cta_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void bw_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// 16-B store of v at local shared address p into CTA t's copy of the same slot
+__device__ __forceinline__ void bw_st_remote(const double* p, unsigned t, double2 v) {
+  const unsigned la = (unsigned)__cvta_generic_to_shared(p);
+  unsigned ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(t));
+  asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(ra), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ double2 bw_ld_remote(const double* p, unsigned t) {
+  const unsigned la = (unsigned)__cvta_generic_to_shared(p);
+  unsigned ra;
+  double2 v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(t));
+  asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(ra) : "memory");
+  return v;
+}
+
+template <int ST, bool P2, int RW, int CL>
 __global__ void __launch_bounds__(BW_THREADS, 1) k_boxw(const SmallBox b, int n_entries) {
   extern __shared__ __align__(16) double sm[];
   const int nx = b.nx, ny = b.ny, np = nx / 2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cr = CL > 1 ? (int)bw_cta_rank() : 0;
+  const int nyl = ny / CL, yb = cr * nyl;  // this CTA's rows yb .. yb + nyl - 1
+  if (CL > 1) bw_cluster_sync();           // every CTA of the cluster runs before any DSMEM store
   double* board = sm;                                   // [2][ny + 2][nx]: rows -1 .. ny
   double* part = board + (size_t)2 * (ny + 2) * nx;     // [entry][BW_WARPS][max bits, sum]
   double* gcor = part + (size_t)n_entries * BW_WARPS * 2;  // [4] fixed corners (-1,-1) (nx,-1) (-1,ny) (nx,ny)
   const int bsz = (ny + 2) * nx;
-  const int y0 = warp * RW;
-  const bool wact = y0 < ny;                            // warp-uniform
+  const int y0 = yb + warp * RW;
+  const bool wact = warp * RW < nyl;                    // warp-uniform
   const bool act = wact && lane < np;
   const int xs = lane < np ? 2 * lane : 0;              // clamped column (inactive lanes read valid memory)
   const bool per = b.bc == PX_BC_PERIODIC, refl = b.bc == PX_BC_DIRICHLET_CC, fixed = b.bc == PX_BC_FIXED_GHOSTS;
@@ -438,6 +470,18 @@ __global__ void __launch_bounds__(BW_THREADS, 1) k_boxw(const SmallBox b, int n_
       gcor[3] = b.phi_in[(int64_t)ny * b.ld_in + nx];
     }
   }
+  // board row Y (-1 .. ny) of buffer bb := v, locally and, when Y is a halo
+  // row of a neighbouring CTA of the cluster, in that CTA's board too
+  auto put = [&](double* B, int Y, double2 v) {
+    double* q = B + (size_t)(Y + 1) * nx + xs;
+    *reinterpret_cast<double2*>(q) = v;
+    if (CL > 1) {
+      const int up = cr > 0 ? cr - 1 : CL - 1, dn = cr < CL - 1 ? cr + 1 : 0;
+      // Y read as a halo row by CTA t: Y == t·nyl - 1 or Y == (t+1)·nyl
+      if (up != cr && (Y == up * nyl - 1 || Y == (up + 1) * nyl)) bw_st_remote(q, (unsigned)up, v);
+      if (dn != cr && dn != up && (Y == dn * nyl - 1 || Y == (dn + 1) * nyl)) bw_st_remote(q, (unsigned)dn, v);
+    }
+  };
   // the warp's first and last rows (and the y images at the faces) into board buffer bb
   auto post = [&](int bb) {
     if (!act) return;
@@ -446,19 +490,20 @@ __global__ void __launch_bounds__(BW_THREADS, 1) k_boxw(const SmallBox b, int n_
     for (int j = 0; j < RW; ++j) {
       if (j != 0 && j != RW - 1) continue;
       const int y = y0 + j;
-      *reinterpret_cast<double2*>(B + (size_t)(y + 1) * nx + xs) = cur[j];
+      put(B, y, cur[j]);
       if (y == 0 && !fixed) {
-        if (per) *reinterpret_cast<double2*>(B + (size_t)(ny + 1) * nx + xs) = cur[j];
-        else *reinterpret_cast<double2*>(B + xs) = make_double2(-cur[j].x, -cur[j].y);
+        if (per) put(B, ny, cur[j]);
+        else put(B, -1, make_double2(-cur[j].x, -cur[j].y));
       }
       if (y == ny - 1 && !fixed) {
-        if (per) *reinterpret_cast<double2*>(B + xs) = cur[j];
-        else *reinterpret_cast<double2*>(B + (size_t)(ny + 1) * nx + xs) = make_double2(-cur[j].x, -cur[j].y);
+        if (per) put(B, -1, cur[j]);
+        else put(B, ny, make_double2(-cur[j].x, -cur[j].y));
       }
     }
   };
   post(0);
-  __syncthreads();
+  if (CL > 1) bw_cluster_sync();
+  else __syncthreads();
   // W of column 2l / E of column 2l+1 of a row v (gw / ge: its fixed ghosts)
   auto west = [&](double2 v, double gw) -> double {
     const double sh = __shfl_sync(FULL_MASK, v.y, srcW);
@@ -571,7 +616,8 @@ __global__ void __launch_bounds__(BW_THREADS, 1) k_boxw(const SmallBox b, int n_
       part[((size_t)entry * BW_WARPS + warp) * 2 + 1] = 0.0;
     }
     if (rec) ++entry;
-    __syncthreads();
+    if (CL > 1) bw_cluster_sync();
+    else __syncthreads();
   }
   if (wact) warp_partial(pmx, pss, entry - 1, pend);
   const int bN = b.nsweeps & 1;
@@ -586,17 +632,22 @@ __global__ void __launch_bounds__(BW_THREADS, 1) k_boxw(const SmallBox b, int n_
     }
     ++entry;
   }
-  __syncthreads();
-  for (int e = tid; e < entry; e += BW_THREADS) {  // entries over the warps in fixed order
-    unsigned long long m = 0ull;
-    double t = 0.0;
-    for (int w = 0; w < BW_WARPS; ++w) {
-      m = umax64(m, (unsigned long long)__double_as_longlong(part[((size_t)e * BW_WARPS + w) * 2]));
-      t = w ? __dadd_rn(t, part[((size_t)e * BW_WARPS + w) * 2 + 1]) : part[((size_t)e * BW_WARPS + w) * 2 + 1];
+  if (CL > 1) bw_cluster_sync();
+  else __syncthreads();
+  // entries over the warps (of CTA 0, 1, .. of the cluster) in fixed order, by CTA 0
+  if (cr == 0)
+    for (int e = tid; e < entry; e += BW_THREADS) {
+      unsigned long long m = 0ull;
+      double t = 0.0;
+      for (int k = 0; k < CL * BW_WARPS; ++k) {
+        const double* pp = part + ((size_t)e * BW_WARPS + (k % BW_WARPS)) * 2;
+        const double2 v = CL > 1 ? bw_ld_remote(pp, (unsigned)(k / BW_WARPS)) : *reinterpret_cast<const double2*>(pp);
+        m = umax64(m, (unsigned long long)__double_as_longlong(v.x));
+        t = k ? __dadd_rn(t, v.y) : v.y;
+      }
+      b.d_max[e] = __longlong_as_double((long long)m);
+      b.d_sum[e] = t;
     }
-    b.d_max[e] = __longlong_as_double((long long)m);
-    b.d_sum[e] = t;
-  }
   // φ^N with its ghost ring: own rows (+ ghost columns = the W/E images), and
   // warp 0 the ghost rows -1 / ny from the board (+ the corners)
   if (wact) {
@@ -616,6 +667,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1) k_boxw(const SmallBox b, int n_
     const double* B = board + (size_t)bN * bsz;
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
+      if ((k == 0 && cr != 0) || (k == 1 && cr != CL - 1)) continue;  // the face CTAs hold the ghost rows
       const int y = k ? ny : -1;
       const double2 v = *reinterpret_cast<const double2*>(B + (size_t)(y + 1) * nx + xs);
       const double w = west(v, gcor[2 * k]), e = east(v, gcor[2 * k + 1]);
@@ -628,6 +680,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1) k_boxw(const SmallBox b, int n_
       }
     }
   }
+  if (CL > 1) bw_cluster_sync();  // no CTA leaves while CTA 0 may still read its partials
 }
 
 static size_t bw_smem(const SmallBox& b, int n_entries) {
@@ -638,14 +691,46 @@ static bool bw_pow2(double v) {
   int e;
   return std::frexp(v, &e) == 0.5;
 }
-template <int RW>
+template <int RW, int CL>
 static cudaError_t bw_launch(const SmallBox& b, int ne, size_t smem, cudaStream_t s) {
   const bool p2 = b.stencil == 0 && bw_pow2(b.scale) && bw_pow2(b.lambda);
-  void (*fn)(const SmallBox, int) = b.stencil ? k_boxw<1, false, RW> : (p2 ? k_boxw<0, true, RW> : k_boxw<0, false, RW>);
+  void (*fn)(const SmallBox, int) =
+      b.stencil ? k_boxw<1, false, RW, CL> : (p2 ? k_boxw<0, true, RW, CL> : k_boxw<0, false, RW, CL>);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   if (e != cudaSuccess) return e;
-  fn<<<1, BW_THREADS, smem, s>>>(b, ne);
-  return cudaGetLastError();
+  if (CL == 1) {
+    fn<<<1, BW_THREADS, smem, s>>>(b, ne);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CL);
+  cfg.blockDim = dim3(BW_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, fn, b, ne);
+}
+template <int CL>
+static cudaError_t bw_launch_rw(const SmallBox& b, int rw, int ne, size_t smem, cudaStream_t s) {
+  return rw == 1 ? bw_launch<1, CL>(b, ne, smem, s)
+                 : (rw == 2 ? bw_launch<2, CL>(b, ne, smem, s) : bw_launch<4, CL>(b, ne, smem, s));
+}
+// CTAs of the k_boxw cluster (PROTOX_BOXW_CL = 1, 2, 4 or 8, read once; the box
+// rows must split evenly)
+static int bw_cl_env() {
+  static int c = -1;
+  if (c < 0) {
+    const char* e = getenv("PROTOX_BOXW_CL");
+    c = e ? atoi(e) : BW_CL_DEFAULT;
+    if (c != 1 && c != 2 && c != 4 && c != 8) c = BW_CL_DEFAULT;
+  }
+  return c;
 }
 
 size_t smallbox_smem(int nx, int ny) {
@@ -658,12 +743,16 @@ px_status launch_smallbox(const SmallBox& b, cudaStream_t s) {
   // 16+ rows: spread the box over a cluster of 8 SMs (px_cluster.cu): one SM
   // running k_box1 is issue-bound (73 % issue-active at 1.76 µs per 64² sweep)
   if (box1_mode() == 0 && b.g == 1) {
-    const int rw = bw_rows_per_warp(b.nx, b.ny);
+    int cl = bw_cl_env();
+    while (cl > 1 && (b.ny % cl || bw_rows_per_warp(b.nx, b.ny / cl) == 0)) cl /= 2;
+    const int rw = bw_rows_per_warp(b.nx, b.ny / cl);
     const int ne = box1_entries(b) > 0 ? box1_entries(b) : 1;
     const size_t smem = bw_smem(b, ne);
     if (rw > 0 && smem <= 200 * 1024) {
-      const cudaError_t e = rw == 1 ? bw_launch<1>(b, ne, smem, s)
-                                    : (rw == 2 ? bw_launch<2>(b, ne, smem, s) : bw_launch<4>(b, ne, smem, s));
+      const cudaError_t e = cl == 1   ? bw_launch_rw<1>(b, rw, ne, smem, s)
+                            : cl == 2 ? bw_launch_rw<2>(b, rw, ne, smem, s)
+                            : cl == 4 ? bw_launch_rw<4>(b, rw, ne, smem, s)
+                                      : bw_launch_rw<8>(b, rw, ne, smem, s);
       note_kernel("k_boxw");
       count_launches(1);
       return cuda_check(e, "small-box kernel launch");

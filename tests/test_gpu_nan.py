@@ -94,7 +94,12 @@ def _box_kernel(cols, rows):
         return "k_box1"
     if mode.startswith("o"):
         return "k_smallbox"
-    boxw = cols % 2 == 0 and cols <= 64 and any(rows <= 16 * rw and rows % rw == 0 for rw in (1, 2, 4))
+    cl = int(os.environ.get("PROTOX_BOXW_CL", "8"))
+    cl = cl if cl in (1, 2, 4, 8) else 8
+    fits = lambda r: any(r <= 16 * rw and r % rw == 0 for rw in (1, 2, 4))  # noqa: E731
+    while cl > 1 and (rows % cl or not fits(rows // cl)):
+        cl //= 2
+    boxw = cols % 2 == 0 and cols <= 64 and fits(rows // cl)
     if boxw and not mode.startswith("c"):
         return "k_boxw"
     return "k_cluster_box" if rows >= 16 else "k_box1"
@@ -112,16 +117,17 @@ def test_nan_box_short(kind):
     assert _box_kernel(64, 12) in _solve_case(64, 12, P.PX_BC_PERIODIC, 20, 1, kind, 12)
 
 
-@pytest.mark.parametrize("mode", ["box1", "old", "cluster"])
+@pytest.mark.parametrize("mode", ["box1", "old", "cluster", "boxw_cl1", "boxw_cl2", "boxw_cl4"])
 def test_box_kernel_variants_subprocess(mode):
     """The other whole-box kernels (k_box1 for every box it fits; the round-1
-    one-CTA k_smallbox; the 8-CTA cluster kernel where k_boxw would run) stay
+    one-CTA k_smallbox; the 8-CTA cluster kernel where k_boxw would run;
+    k_boxw on one CTA or over a cluster of 2 or 4 CTAs instead of 8) stay
     bit-identical: the small-box parity and NaN tests
     re-run in a child process with PROTOX_SMALLBOX=<mode>."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, PROTOX_SMALLBOX=mode)
+    env = dict(os.environ, **({"PROTOX_BOXW_CL": mode[-1]} if mode.startswith("boxw") else {"PROTOX_SMALLBOX": mode}))
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-m", "gpu",
                         "tests/test_gpu_nan.py", "tests/test_gpu_parity.py", "-k",
                         "nan_box_c1 or nan_box_short or config1 or test_solve_ragged_multibox or "
