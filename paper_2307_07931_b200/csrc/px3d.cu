@@ -852,6 +852,7 @@ static px_status solve3_impl(px_comm* comm, px_bc bc, const px_relax_params* p, 
     PX_TRY(cuda_check(cudaMalloc(&P.d_ring, sizeof(double) * 2 * (n_entries > 0 ? n_entries : 1)), "norm ring"));
     PX_TRY(cuda_check(cudaMalloc(&P.d_ws, sizeof(double) * (2 + 2 * k3::MAX_GRID)), "norm workspace"));
     PX_TRY(cuda_check(cudaMemset(P.d_ws, 0, sizeof(double) * (2 + 2 * k3::MAX_GRID)), "norm workspace"));
+    PX_TRY(cuda_check(cudaDeviceSynchronize(), "init zero-fill"));  // the legacy-stream fills before any user-stream work
     if (o->use_graph) {
       cudaGraph_t graph;
       const int64_t before = px_kernel_launch_count();
@@ -1040,6 +1041,7 @@ px_status px3_solve_host_batch(px_bc bc, const px_relax_params* p, const px_solv
         PX_TRY(cuda_check(cudaMalloc(&q, alloc * sizeof(double)), "cudaMalloc"));
         PX_TRY(cuda_check(cudaMemset(q, 0, alloc * sizeof(double)), "memset"));
       }
+    PX_TRY(cuda_check(cudaDeviceSynchronize(), "init zero-fill"));  // the legacy-stream fills before any user-stream work
     B.ne = ne > 0 ? ne : 1;
     for (auto& h : B.h_ring) PX_TRY(cuda_check(cudaMallocHost(&h, 2 * (size_t)B.ne * sizeof(double)), "cudaMallocHost"));
     std::memcpy(B.n, n, sizeof B.n);
@@ -1066,6 +1068,7 @@ px_status px3_solve_host_batch(px_bc bc, const px_relax_params* p, const px_solv
     PX_TRY(cuda_check(cudaMalloc(&P.d_ring, sizeof(double) * 2 * (ne > 0 ? ne : 1)), "norm ring"));
     PX_TRY(cuda_check(cudaMalloc(&P.d_ws, sizeof(double) * (2 + 2 * k3::MAX_GRID)), "norm workspace"));
     PX_TRY(cuda_check(cudaMemset(P.d_ws, 0, sizeof(double) * (2 + 2 * k3::MAX_GRID)), "norm workspace"));
+    PX_TRY(cuda_check(cudaDeviceSynchronize(), "init zero-fill"));  // the legacy-stream fills before any user-stream work
     if (o->use_graph) {
       cudaGraph_t graph;
       const int64_t before = px_kernel_launch_count();

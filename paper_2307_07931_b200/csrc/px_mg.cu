@@ -362,6 +362,7 @@ px_status px_mg_solve(const px_layout* l, const px_relax_params* p, const px_mg_
     const int64_t wsl = std::max<int64_t>(4 + 2 * (int64_t)stream_blocks(n0, n1, 1), 8192);
     PX_TRY(cuda_check(cudaMalloc(&np->d_ws, wsl * sizeof(double)), "cudaMalloc ws"));
     PX_TRY(cuda_check(cudaMemset(np->d_ws, 0, wsl * sizeof(double)), "memset ws"));
+    PX_TRY(cuda_check(cudaDeviceSynchronize(), "init zero-fill"));  // the legacy-stream fills before any user-stream work
     P = np.get();
     mg_plans().push_back(std::move(np));
   }

@@ -698,6 +698,10 @@ static cudaError_t bw_launch(const SmallBox& b, int ne, size_t smem, cudaStream_
       b.stencil ? k_boxw<1, false, RW, CL> : (p2 ? k_boxw<0, true, RW, CL> : k_boxw<0, false, RW, CL>);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   if (e != cudaSuccess) return e;
+  if (CL > 8) {  // 16 CTAs: a non-portable cluster size
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
   if (CL == 1) {
     fn<<<1, BW_THREADS, smem, s>>>(b, ne);
     return cudaGetLastError();
@@ -721,14 +725,14 @@ static cudaError_t bw_launch_rw(const SmallBox& b, int rw, int ne, size_t smem, 
   return rw == 1 ? bw_launch<1, CL>(b, ne, smem, s)
                  : (rw == 2 ? bw_launch<2, CL>(b, ne, smem, s) : bw_launch<4, CL>(b, ne, smem, s));
 }
-// CTAs of the k_boxw cluster (PROTOX_BOXW_CL = 1, 2, 4 or 8, read once; the box
+// CTAs of the k_boxw cluster (PROTOX_BOXW_CL = 1, 2, 4, 8 or 16, read once; the box
 // rows must split evenly)
 static int bw_cl_env() {
   static int c = -1;
   if (c < 0) {
     const char* e = getenv("PROTOX_BOXW_CL");
     c = e ? atoi(e) : BW_CL_DEFAULT;
-    if (c != 1 && c != 2 && c != 4 && c != 8) c = BW_CL_DEFAULT;
+    if (c != 1 && c != 2 && c != 4 && c != 8 && c != 16) c = BW_CL_DEFAULT;
   }
   return c;
 }
@@ -752,7 +756,8 @@ px_status launch_smallbox(const SmallBox& b, cudaStream_t s) {
       const cudaError_t e = cl == 1   ? bw_launch_rw<1>(b, rw, ne, smem, s)
                             : cl == 2 ? bw_launch_rw<2>(b, rw, ne, smem, s)
                             : cl == 4 ? bw_launch_rw<4>(b, rw, ne, smem, s)
-                                      : bw_launch_rw<8>(b, rw, ne, smem, s);
+                            : cl == 8 ? bw_launch_rw<8>(b, rw, ne, smem, s)
+                                      : bw_launch_rw<16>(b, rw, ne, smem, s);
       note_kernel("k_boxw");
       count_launches(1);
       return cuda_check(e, "small-box kernel launch");

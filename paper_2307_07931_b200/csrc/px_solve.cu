@@ -1190,6 +1190,7 @@ static px_status solve_enqueue(const px_layout* l, px_comm* c, int32_t rank, con
     PX_TRY(cuda_check(cudaMalloc(&np->d_sum, ne * sizeof(double)), "cudaMalloc ring"));
     PX_TRY(cuda_check(cudaMalloc(&np->d_ws, np->ws_len * sizeof(double)), "cudaMalloc ws"));
     PX_TRY(cuda_check(cudaMemset(np->d_ws, 0, np->ws_len * sizeof(double)), "memset ws"));
+    PX_TRY(cuda_check(cudaDeviceSynchronize(), "init zero-fill"));  // the legacy-stream fill before any user-stream work
     {  // workspace of the shared-memory-resident solve (allocated here: not during graph capture)
       px_local_info l0;
       PX_TRY(local_info(l, c ? rank : 0, &l0));
@@ -1364,6 +1365,7 @@ px_status px_solve_host(const px_layout* l, const px_relax_params* p, const px_s
     PX_TRY(cuda_check(cudaMemset(g_host.phi, 0, b), "memset"));
     PX_TRY(cuda_check(cudaMemset(g_host.scr, 0, b), "memset"));
     PX_TRY(cuda_check(cudaMemset(g_host.rhs, 0, b), "memset"));
+    PX_TRY(cuda_check(cudaDeviceSynchronize(), "init zero-fill"));  // the legacy-stream fill before any user-stream work
     g_host.elems = li.alloc_elems;
     g_host.gen = layout_generation(l);
   }
@@ -1469,6 +1471,7 @@ px_status px_solve_host_batch(const px_layout* l, const px_relax_params* p, cons
         PX_TRY(cuda_check(cudaMalloc(&q, b), "cudaMalloc"));
         PX_TRY(cuda_check(cudaMemset(q, 0, b), "memset"));
       }
+    PX_TRY(cuda_check(cudaDeviceSynchronize(), "init zero-fill"));  // the legacy-stream fill before any user-stream work
     for (auto& h : B.h_ring)
       PX_TRY(cuda_check(cudaMallocHost(&h, 2 * (size_t)std::max(ne, 1) * sizeof(double)), "cudaMallocHost"));
     B.elems = li.alloc_elems;
