@@ -410,6 +410,23 @@ __device__ __forceinline__ void bw_st_remote(const double* p, unsigned t, double
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(t));
   asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(ra), "d"(v.x), "d"(v.y) : "memory");
 }
+// the same store as st.async, counted (16 bytes) on CTA t's mbarrier `bar`
+__device__ __forceinline__ void bw_st_async(const double* p, unsigned t, double2 v, const uint64_t* bar) {
+  const unsigned la = (unsigned)__cvta_generic_to_shared(p), lb = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned ra, rb;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(t));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(lb), "r"(t));
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(ra),
+               "d"(v.x), "d"(v.y), "r"(rb)
+               : "memory");
+}
+__device__ __forceinline__ void bw_mbar_wait(const uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nWAIT_%=:\nmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n}\n" ::"r"((unsigned)__cvta_generic_to_shared(b)),
+      "r"(parity)
+      : "memory");
+}
 __device__ __forceinline__ double2 bw_ld_remote(const double* p, unsigned t) {
   const unsigned la = (unsigned)__cvta_generic_to_shared(p);
   unsigned ra;
@@ -420,8 +437,9 @@ __device__ __forceinline__ double2 bw_ld_remote(const double* p, unsigned t) {
 }
 
 template <int ST, bool P2, int RW, int CL>
-__global__ void __launch_bounds__(BW_THREADS, 1) k_boxw(const SmallBox b, int n_entries) {
+__global__ void __launch_bounds__(BW_THREADS, 1) k_boxw(const SmallBox b, int n_entries, int mb) {
   extern __shared__ __align__(16) double sm[];
+  __shared__ __align__(8) uint64_t hb[2];  // mb: the remote halo rows of board buffer 0 / 1 (bytes counted)
   const int nx = b.nx, ny = b.ny, np = nx / 2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int cr = CL > 1 ? (int)bw_cta_rank() : 0;
@@ -478,8 +496,15 @@ __global__ void __launch_bounds__(BW_THREADS, 1) k_boxw(const SmallBox b, int n_
     if (CL > 1) {
       const int up = cr > 0 ? cr - 1 : CL - 1, dn = cr < CL - 1 ? cr + 1 : 0;
       // Y read as a halo row by CTA t: Y == t·nyl - 1 or Y == (t+1)·nyl
-      if (up != cr && (Y == up * nyl - 1 || Y == (up + 1) * nyl)) bw_st_remote(q, (unsigned)up, v);
-      if (dn != cr && dn != up && (Y == dn * nyl - 1 || Y == (dn + 1) * nyl)) bw_st_remote(q, (unsigned)dn, v);
+      const uint64_t* bar = &hb[B == board ? 0 : 1];
+      if (up != cr && (Y == up * nyl - 1 || Y == (up + 1) * nyl)) {
+        if (mb) bw_st_async(q, (unsigned)up, v, bar);
+        else bw_st_remote(q, (unsigned)up, v);
+      }
+      if (dn != cr && dn != up && (Y == dn * nyl - 1 || Y == (dn + 1) * nyl)) {
+        if (mb) bw_st_async(q, (unsigned)dn, v, bar);
+        else bw_st_remote(q, (unsigned)dn, v);
+      }
     }
   };
   // the warp's first and last rows (and the y images at the faces) into board buffer bb
@@ -501,8 +526,38 @@ __global__ void __launch_bounds__(BW_THREADS, 1) k_boxw(const SmallBox b, int n_
       }
     }
   };
+  // mb: the halo rows another CTA writes arrive by st.async, counted on the
+  // board buffer's mbarrier; the warps that read them wait for its phase, the
+  // others only need the CTA barrier (no cluster barrier per sweep)
+  const bool up_remote = CL > 1 && (cr > 0 || per), dn_remote = CL > 1 && (cr < CL - 1 || per);
+  const uint32_t E = (uint32_t)((up_remote ? 1 : 0) + (dn_remote ? 1 : 0)) * (uint32_t)np * 16u;
+  const bool waiter = mb && CL > 1 && wact && (warp == 0 || (warp + 1) * RW >= nyl);
+  uint32_t ph[2] = {0u, 0u};
+  if (CL > 1 && mb) {
+    if (tid == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&hb[0])) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&hb[1])) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      for (int k = 0; k < 2; ++k)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                         (unsigned)__cvta_generic_to_shared(&hb[k])),
+                     "r"(E)
+                     : "memory");
+    }
+    bw_cluster_sync();  // every CTA's barriers armed before any st.async
+  }
+  auto halo_wait = [&](int bb, bool rearm) {
+    if (!waiter) return;
+    bw_mbar_wait(&hb[bb], ph[bb]);
+    ph[bb] ^= 1u;
+    if (rearm && tid == 0)  // the next use of this buffer (two sweeps on)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                       (unsigned)__cvta_generic_to_shared(&hb[bb])),
+                   "r"(E)
+                   : "memory");
+  };
   post(0);
-  if (CL > 1) bw_cluster_sync();
+  if (CL > 1 && !mb) bw_cluster_sync();
   else __syncthreads();
   // W of column 2l / E of column 2l+1 of a row v (gw / ge: its fixed ghosts)
   auto west = [&](double2 v, double gw) -> double {
@@ -606,6 +661,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1) k_boxw(const SmallBox b, int n_
       // sweep's update (the compiler interleaves the two chains)
       warp_partial(pmx, pss, entry - 1, pend);
       double mx = 0.0, ss = 0.0;
+      halo_wait(s & 1, true);
       pass(s & 1, true, rec, mx, ss);
       post((s + 1) & 1);
       pend = rec;
@@ -616,11 +672,13 @@ __global__ void __launch_bounds__(BW_THREADS, 1) k_boxw(const SmallBox b, int n_
       part[((size_t)entry * BW_WARPS + warp) * 2 + 1] = 0.0;
     }
     if (rec) ++entry;
-    if (CL > 1) bw_cluster_sync();
+    if (CL > 1 && !mb) bw_cluster_sync();
     else __syncthreads();
   }
   if (wact) warp_partial(pmx, pss, entry - 1, pend);
   const int bN = b.nsweeps & 1;
+  halo_wait(bN, false);  // φ^N's remote halo rows (final residual, ghost rows)
+  __syncthreads();
   if (b.final_norm) {
     if (wact) {
       double mx = 0.0, ss = 0.0;
@@ -691,10 +749,21 @@ static bool bw_pow2(double v) {
   int e;
   return std::frexp(v, &e) == 0.5;
 }
+// PROTOX_BOXW_MB=0 (read once, A/B): the cluster k_boxw exchanges its halo
+// rows with plain DSMEM stores and a cluster barrier per sweep instead of
+// st.async counted on per-buffer mbarriers
+static int bw_mb_env() {
+  static int m = -1;
+  if (m < 0) {
+    const char* e = getenv("PROTOX_BOXW_MB");
+    m = (e && e[0] == '0') ? 0 : 1;
+  }
+  return m;
+}
 template <int RW, int CL>
 static cudaError_t bw_launch(const SmallBox& b, int ne, size_t smem, cudaStream_t s) {
   const bool p2 = b.stencil == 0 && bw_pow2(b.scale) && bw_pow2(b.lambda);
-  void (*fn)(const SmallBox, int) =
+  void (*fn)(const SmallBox, int, int) =
       b.stencil ? k_boxw<1, false, RW, CL> : (p2 ? k_boxw<0, true, RW, CL> : k_boxw<0, false, RW, CL>);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   if (e != cudaSuccess) return e;
@@ -703,7 +772,7 @@ static cudaError_t bw_launch(const SmallBox& b, int ne, size_t smem, cudaStream_
     if (e != cudaSuccess) return e;
   }
   if (CL == 1) {
-    fn<<<1, BW_THREADS, smem, s>>>(b, ne);
+    fn<<<1, BW_THREADS, smem, s>>>(b, ne, 0);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};
@@ -718,7 +787,7 @@ static cudaError_t bw_launch(const SmallBox& b, int ne, size_t smem, cudaStream_
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, fn, b, ne);
+  return cudaLaunchKernelEx(&cfg, fn, b, ne, bw_mb_env());
 }
 template <int CL>
 static cudaError_t bw_launch_rw(const SmallBox& b, int rw, int ne, size_t smem, cudaStream_t s) {

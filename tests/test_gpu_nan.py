@@ -117,17 +117,24 @@ def test_nan_box_short(kind):
     assert _box_kernel(64, 12) in _solve_case(64, 12, P.PX_BC_PERIODIC, 20, 1, kind, 12)
 
 
-@pytest.mark.parametrize("mode", ["box1", "old", "cluster", "boxw_cl1", "boxw_cl2", "boxw_cl4"])
+@pytest.mark.parametrize("mode", ["box1", "old", "cluster", "boxw_cl1", "boxw_cl2", "boxw_cl4", "boxw_nomb"])
 def test_box_kernel_variants_subprocess(mode):
     """The other whole-box kernels (k_box1 for every box it fits; the round-1
     one-CTA k_smallbox; the 8-CTA cluster kernel where k_boxw would run;
-    k_boxw on one CTA or over a cluster of 2 or 4 CTAs instead of 8) stay
+    k_boxw on one CTA or over a cluster of 2 or 4 CTAs instead of 8, and with
+    plain DSMEM stores + a cluster barrier per sweep instead of st.async
+    counted on mbarriers) stay
     bit-identical: the small-box parity and NaN tests
     re-run in a child process with PROTOX_SMALLBOX=<mode>."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, **({"PROTOX_BOXW_CL": mode[-1]} if mode.startswith("boxw") else {"PROTOX_SMALLBOX": mode}))
+    extra = {"PROTOX_SMALLBOX": mode}
+    if mode.startswith("boxw_cl"):
+        extra = {"PROTOX_BOXW_CL": mode[-1]}
+    elif mode == "boxw_nomb":
+        extra = {"PROTOX_BOXW_MB": "0"}
+    env = dict(os.environ, **extra)
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-m", "gpu",
                         "tests/test_gpu_nan.py", "tests/test_gpu_parity.py", "-k",
                         "nan_box_c1 or nan_box_short or config1 or test_solve_ragged_multibox or "
