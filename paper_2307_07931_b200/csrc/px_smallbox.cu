@@ -366,9 +366,9 @@ static bool box1_eligible(const SmallBox& b) {
 // ---------------------------------------------------------------------------
 // k_boxw: the whole-box solve with the box IN REGISTERS, one warp per row
 // group (round 2, BASELINE config 1).  Lane l of warp w owns column pair l
-// (columns 2l, 2l+1; nx <= 64) of rows w·RW .. w·RW + RW - 1 (16 warps,
-// ny <= 16·RW, RW <= 4),
-// φ and ρ in registers for the whole solve.  W/E neighbours are indexed
+// (columns 2l, 2l+1; nx <= 64) of rows w·RW .. w·RW + RW - 1 of its CTA's
+// ny/CL rows (16 warps, ny/CL <= 16·RW, RW <= 4; CL CTAs form a cluster,
+// below), φ and ρ in registers for the whole solve.  W/E neighbours are indexed
 // shuffles inside the warp (the periodic wrap falls out of the lane index;
 // odd reflection / fixed ghosts are a select at lanes 0 and np-1); N/S
 // neighbours inside the row group are registers, across groups one 16-B
@@ -380,7 +380,11 @@ static bool box1_eligible(const SmallBox& b) {
 // cell the oracle's expression tree (power-of-two h and λ: the exact fused
 // multiply-adds of k_resident_reg): bit-identical φ and max-norm.  The max
 // per warp by two redux.sync steps on the bit pattern, not a 64-bit
-// butterfly (the norm is recorded every sweep at BJ.C1).
+// butterfly (the norm is recorded every sweep at BJ.C1).  Over a cluster of
+// CL CTAs (default 8 at 64²: 0.79 µs per sweep, one CTA 1.14) the halo rows a
+// CTA reads from its neighbours arrive by st.async counted on a per-buffer
+// mbarrier that only the reading warps wait on, and the per-sweep barrier is
+// the CTA's own.
 constexpr int BW_THREADS = 512;  // 16 warps: 128 registers a thread, up to 4 rows of φ, ρ in registers
 constexpr int BW_WARPS = BW_THREADS / 32;
 constexpr int BW_CL_DEFAULT = 8;  // 64² (BJ.C1): 1 / 2 / 4 / 8 CTAs 1.14 / 1.26 / 0.955 / 0.89 µs per sweep
